@@ -1,0 +1,142 @@
+"""Freeze the calibration constants of the synthetic models (run once, committed output).
+
+TEST INFRASTRUCTURE: this script calls only oracle/ (and the seeded generator
+``workloads``); it writes workloads/calib/cfg{2,3}.json, which both the CUDA
+path and the oracle then read as model parameters.  No value here comes from
+the CUDA path.
+
+Why: random-init weights make every predicate degenerate (0 %
+of samples exit, gates all ~0.5), so the dynamic path would never branch.
+Recipe (SURVEY.md §8(d) "Calibration"), on 512 calibration
+samples drawn with seed CALIB_SEED=2 (disjoint from the measured inputs):
+
+* config 2 exit heads k=0..3: logits = w (g - mu_k), w = bf16(s_k H_k), with
+  mu_k the calibration mean of the pooled features g at that IC and s_k found
+  by bisection so that 25 % of the samples ARRIVING at head k exit
+  (conf >= tau = 0.9); final head: s = 4, centred the same way.
+* config 3 gates i=2..18, calibrated in order along the dynamic path:
+  raw r = H_i . g, a_i = median(r), s_i = 2 / std(r); gate logit
+  z = bf16(s_i H_i) . g - s_i a_i  (~50 % execute); final head s = 4, centred.
+
+Usage:  python -m oracle.calibrate [--n 512]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+import workloads as wl
+
+from . import programs as prg
+from .core import dense, gap, max_softmax, sigmoid
+
+
+def _pool():
+    return ThreadPoolExecutor(max_workers=len(os.sched_getaffinity(0)))
+
+
+def calibrate_cfg2(n: int, mode: str = "mirror") -> dict:
+    X = wl.image_inputs(wl.CALIB_SEED, 0, n)
+    P = prg.prepare(wl.sdn_r56_weights(calib={
+        k: {"scale": 1.0, "mu": [0.0] * c} for k, c in
+        [("ic0", 16), ("ic1", 32), ("ic2", 32), ("ic3", 64), ("final", 64)]}))
+
+    def feats(i):
+        f = []
+        prg.sdn_resnet56(X[i], P, mode, tau=2.0, features=f)   # tau > 1: never exits
+        return f
+
+    with _pool() as ex:
+        F = list(ex.map(feats, range(n)))
+    names = ["ic0", "ic1", "ic2", "ic3", "final"]
+    G = {nm: np.stack([f[j] for f in F]) for j, nm in enumerate(names)}
+    raw = wl.sdn_r56_raw_heads()
+    out = {}
+    arriving = np.ones(n, dtype=bool)
+    for k in range(4):
+        nm = f"ic{k}"
+        g = G[nm]
+        mu = g.mean(axis=0)
+
+        def exits(s):
+            w, b = wl._centered_head(raw[nm], s, mu)
+            wf = prg._bf16_to_f64(w)
+            conf = np.array([max_softmax(dense(wf, b, gi)) for gi in g])
+            return conf >= wl.EXIT_TAU
+
+        lo, hi = np.log(0.01), np.log(1000.0)
+        for _ in range(60):
+            mid = 0.5 * (lo + hi)
+            frac = exits(np.exp(mid))[arriving].mean()
+            if frac < 0.25:
+                lo = mid
+            else:
+                hi = mid
+        s = float(np.exp(hi))
+        ex_k = exits(s)
+        out[nm] = {"scale": s, "mu": [float(v) for v in mu],
+                   "exit_frac_of_arriving": float(ex_k[arriving].mean()),
+                   "arriving": int(arriving.sum())}
+        arriving &= ~ex_k
+    out["final"] = {"scale": 4.0, "mu": [float(v) for v in G["final"].mean(axis=0)],
+                    "arriving": int(arriving.sum())}
+    out["_recipe"] = ("oracle/calibrate.py calibrate_cfg2: n=%d calibration samples "
+                      "(seed %d), mode=%s, target 25%% exits of arriving, tau=%.2f"
+                      % (n, wl.CALIB_SEED, mode, wl.EXIT_TAU))
+    return out
+
+
+def calibrate_cfg3(n: int, mode: str = "mirror") -> dict:
+    X = wl.image_inputs(wl.CALIB_SEED, 0, n)
+    W = wl.skipnet_r38_weights(calib=None)
+    P = prg.prepare(W)
+    raw = wl.skipnet_r38_raw_gates()
+    with _pool() as ex:
+        H = list(ex.map(lambda i: prg.basic_block(prg.stem(X[i], P, mode), P, 1, 6, mode), range(n)))
+        out = {}
+        executed = []
+        for i in wl.SKIP_GATED:
+            g = np.stack([gap(h) for h in H])
+            r = g @ raw[f"gate{i}"][0]
+            a = float(np.median(r))
+            s = float(2.0 / r.std())
+            w = prg._bf16_to_f64(wl.f32_to_bf16_bits(s * raw[f"gate{i}"]))[0]
+            z = g @ w - s * a
+            run = sigmoid(z) > 0.5
+            executed.append(float(run.mean()))
+            out[f"gate{i}"] = {"scale": s, "median": a, "exec_frac": float(run.mean())}
+            ci, co, stride = prg._block_io(i, 6)
+
+            def step(j, i=i, run=run, co=co, stride=stride):
+                if run[j]:
+                    return prg.basic_block(H[j], P, i, 6, mode)
+                return prg.option_a(H[j], co) if stride == 2 else H[j]
+
+            H = list(ex.map(step, range(n)))
+    out["final"] = {"scale": 4.0, "mu": [float(v) for v in np.stack([gap(h) for h in H]).mean(axis=0)]}
+    out["_recipe"] = ("oracle/calibrate.py calibrate_cfg3: n=%d calibration samples (seed %d), "
+                      "mode=%s, gates in path order, a=median, s=2/std; mean executed %.2f/17"
+                      % (n, wl.CALIB_SEED, mode, sum(executed)))
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--cfg", type=int, nargs="*", default=[2, 3])
+    a = ap.parse_args()
+    os.makedirs(os.path.join(wl.HERE, "calib"), exist_ok=True)
+    for c in a.cfg:
+        res = calibrate_cfg2(a.n) if c == 2 else calibrate_cfg3(a.n)
+        path = os.path.join(wl.HERE, "calib", f"cfg{c}.json")
+        with open(path, "w") as f:
+            json.dump(res, f, indent=1)
+        print("wrote", path, res.get("_recipe"))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,180 @@
+"""The original (unrewritten) dynamic programs, interpreted one sample at a time.
+
+TEST INFRASTRUCTURE -- see oracle/__init__.py.
+
+Each program is the DyNN as written before DyCL's rewriting (Sec. 5.2,
+L588-591): a loop over blocks with real ``if`` / ``return``, so the oracle is
+the left-hand side of Eq. 2 (P_DyNN(x)).  Per sample it returns
+the output logits, the path taken, and every predicate value it evaluated
+(kind, value, threshold) so the harness can apply the 1e-3 band (reading R12).
+
+Rounding (mode='mirror'): bf16 RNE at the production path's storage points --
+after the input cast (a0), after every conv/dense epilogue (bias [+shortcut]
+-> ReLU -> round).  Pooled features, head/gate logits and predicates stay fp64.
+Mode 'exact': no rounding after the bf16 input.  (reading R13.)
+"""
+from __future__ import annotations
+
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+from .core import (conv2d, dense, gap, max_softmax, option_a, relu, round_bf16,
+                   sigmoid)
+
+
+def _bf16_to_f64(bits):
+    """Decode bf16 bit patterns: the value is the fp32 whose top half is the bits."""
+    b = np.ascontiguousarray(np.asarray(bits, dtype=np.uint16))
+    return (b.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+def prepare(W: dict) -> dict:
+    """bf16 (uint16) tensors -> fp64; fp32 tensors -> fp64."""
+    P = {}
+    for k, v in W.items():
+        v = np.asarray(v)
+        P[k] = _bf16_to_f64(v) if v.dtype == np.uint16 else v.astype(np.float64)
+    return P
+
+
+def _rnd(v, mode):
+    return round_bf16(v) if mode == "mirror" else v
+
+
+# ---------------------------------------------------------------------------
+# Config 1: tiny early-exit MLP (BASELINE configs[0]).
+#   h = x; for k in 0..2: h = relu(W_k h + b_k); z = H_k h + c_k
+#          if k < 2 and maxsoftmax(z) >= tau: return (z, k)
+#   return (z, 2)
+# Early termination per Shallow-Deep; comparator '>=' is
+# reading R1; the final head is the default exit (reading R3).
+# ---------------------------------------------------------------------------
+def mlp_ee(x, P, mode="mirror", tau=0.9):
+    preds = []
+    h = _rnd(np.asarray(x, np.float64), "mirror")            # a0: input cast to bf16
+    for k in range(3):
+        h = _rnd(relu(dense(P[f"fc{k}.w"], P[f"fc{k}.b"], h)), mode)
+        z = dense(P[f"head{k}.w"], P[f"head{k}.b"], h)
+        if k < 2:
+            conf = max_softmax(z)
+            preds.append(("exit", conf, tau))
+            if conf >= tau:
+                return z, k, preds
+    return z, 2, preds
+
+
+# ---------------------------------------------------------------------------
+# CIFAR ResNet pieces shared by configs 2 and 3 (He et al. basic block,
+# 'option A' parameter-free shortcut at stage transitions).
+# ---------------------------------------------------------------------------
+def _block_io(i, per_stage, widths=(16, 32, 64)):
+    s = (i - 1) // per_stage
+    first = (i - 1) % per_stage == 0
+    if s > 0 and first:
+        return widths[s - 1], widths[s], 2
+    return widths[s], widths[s], 1
+
+
+def basic_block(h, P, i, per_stage, mode):
+    """relu(conv2(relu(conv1(h) + b1)) + b2 + shortcut(h))."""
+    ci, co, stride = _block_io(i, per_stage)
+    t = _rnd(relu(conv2d(h, P[f"b{i}.c1.w"], P[f"b{i}.c1.b"], stride, 1)), mode)
+    sc = h if stride == 1 else option_a(h, co)
+    return _rnd(relu(conv2d(t, P[f"b{i}.c2.w"], P[f"b{i}.c2.b"], 1, 1) + sc), mode)
+
+
+def stem(x, P, mode):
+    h = _rnd(np.asarray(x, np.float64), "mirror")            # a0: input cast to bf16
+    return _rnd(relu(conv2d(h, P["stem.w"], P["stem.b"], 1, 1)), mode)
+
+
+# ---------------------------------------------------------------------------
+# Config 2: ShallowDeep-style early-exit ResNet-56 (BASELINE configs[1]).
+#   h = stem(x); for blk in 1..27: h = block(h)
+#       if blk in {5,11,16,22}: z = IC_k(GAP(h)); if maxsoftmax(z) >= tau: return (z, k)
+#   return (FC_final(GAP(h)), 4)
+# IC placement: reading R4.  Head = GAP -> FC (reading R5).
+# ---------------------------------------------------------------------------
+SDN_IC_AFTER = (5, 11, 16, 22)
+
+
+def sdn_resnet56(x, P, mode="mirror", tau=0.9, features=None):
+    preds = []
+    h = stem(x, P, mode)
+    k = 0
+    for blk in range(1, 28):
+        h = basic_block(h, P, blk, 9, mode)
+        if blk in SDN_IC_AFTER:
+            g = gap(h)
+            if features is not None:
+                features.append(g)
+            z = dense(P[f"ic{k}.w"], P[f"ic{k}.b"], g)
+            conf = max_softmax(z)
+            preds.append(("exit", conf, tau))
+            if conf >= tau:
+                return z, k, preds
+            k += 1
+    g = gap(h)
+    if features is not None:
+        features.append(g)
+    return dense(P["final.w"], P["final.b"], g), 4, preds
+
+
+# ---------------------------------------------------------------------------
+# Config 3: SkipNet-style gated ResNet-38 (BASELINE configs[2]).
+# Listing 3: the first block always runs; for the others
+#   'if mask == 0: x = (1 - mask) * prev  else: x = layer(x)'.
+#   h = stem(x); h = block_1(h); mask = 0
+#   for i in 2..18: p = sigmoid(gate_i(GAP(h)))           # gate on the block INPUT
+#        if p > 0.5: h = block_i(h); mask |= 1 << (i-2)
+#        else:       h = optionA(h) if i in {7,13} else h   # skip = identity path
+#   return (FC(GAP(h)), mask)
+# Comparator '>' : reading R2; transition skips: reading R7.
+# ---------------------------------------------------------------------------
+def skipnet_resnet38(x, P, mode="mirror", thr=0.5, gate_hook=None):
+    preds = []
+    h = stem(x, P, mode)
+    h = basic_block(h, P, 1, 6, mode)
+    mask = 0
+    for i in range(2, 19):
+        g = gap(h)
+        z = dense(P[f"gate{i}.w"], P[f"gate{i}.b"], g)[0]
+        if gate_hook is not None:
+            gate_hook(i, g, z)
+        p = sigmoid(z)
+        preds.append(("gate", p, thr))
+        if p > thr:
+            h = basic_block(h, P, i, 6, mode)
+            mask |= 1 << (i - 2)
+        else:
+            ci, co, stride = _block_io(i, 6)
+            h = option_a(h, co) if stride == 2 else h
+    return dense(P["final.w"], P["final.b"], gap(h)), mask, preds
+
+
+PROGRAMS = {1: mlp_ee, 2: sdn_resnet56, 3: skipnet_resnet38}
+
+
+def run_batch(program, X, P, mode="mirror", threads=None, **kw):
+    """Run ``program`` independently on every sample of X (no batching).
+
+    Returns (logits [B, K] fp64, path [B] int64, preds list-of-lists).
+    Samples are spread over a thread pool; the C conv releases the GIL.
+    """
+    threads = threads or len(os.sched_getaffinity(0))
+    n = len(X)
+
+    def one(i):
+        return program(X[i], P, mode, **kw)
+
+    if threads <= 1 or n <= 1:
+        res = [one(i) for i in range(n)]
+    else:
+        with ThreadPoolExecutor(max_workers=threads) as ex:
+            res = list(ex.map(one, range(n)))
+    logits = np.stack([np.asarray(r[0], np.float64) for r in res]) if n else np.zeros((0, 10))
+    path = np.array([r[1] for r in res], dtype=np.int64)
+    preds = [r[2] for r in res]
+    return logits, path, preds

@@ -1,0 +1,250 @@
+"""Pins of the CPU oracle against things other than itself (runs without a GPU).
+
+Each test names what fixes the expected value: a closed form, a value printed
+in the paper/spec (tests/golden/*.json, cited), a library routine the case
+reduces to (torch fp64), or an independent brute-force re-implementation.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import workloads as wl
+from oracle import programs as prg
+from oracle.metrics import delta, eta, in_band
+from tests import torch_ref as TR
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+# --------------------------------------------------------------------- layers
+@pytest.mark.parametrize("H,C,Co,k,stride,pad", [
+    (8, 3, 5, 3, 1, 1), (9, 4, 6, 3, 2, 1), (7, 8, 4, 1, 2, 0), (12, 3, 8, 7, 2, 3), (5, 16, 16, 3, 1, 1)])
+def test_conv2d_is_torch_conv2d(H, C, Co, k, stride, pad):
+    """Library special case: the oracle conv equals torch.nn.functional.conv2d in fp64."""
+    rng = np.random.default_rng(H * 100 + k)
+    x = rng.standard_normal((H, H + 1, C))
+    w = rng.standard_normal((Co, k, k, C))
+    b = rng.standard_normal(Co)
+    y = O.conv2d(x, w, b, stride, pad)
+    t = torch.nn.functional.conv2d(torch.tensor(x).permute(2, 0, 1)[None], torch.tensor(w).permute(0, 3, 1, 2),
+                                   torch.tensor(b), stride=stride, padding=pad)[0].permute(1, 2, 0).numpy()
+    assert y.shape == t.shape
+    np.testing.assert_allclose(y, t, rtol=0, atol=1e-12)
+
+
+def test_round_bf16_matches_torch_cast_and_ties():
+    rng = np.random.default_rng(7)
+    v32 = (rng.standard_normal(20000) * np.exp(rng.uniform(-20, 20, 20000))).astype(np.float32)
+    ref = torch.tensor(v32).to(torch.bfloat16).to(torch.float64).numpy()
+    np.testing.assert_array_equal(O.round_bf16(v32.astype(np.float64)), ref)
+    # hand ties (bf16: 8 significant bits, ulp(1) = 2^-7): ties go to the even significand
+    assert O.round_bf16(1 + 2 ** -8) == 1.0
+    assert O.round_bf16(1 + 3 * 2 ** -8) == 1 + 2 ** -6
+    assert O.round_bf16(-(1 + 2 ** -8 + 2 ** -30)) == -(1 + 2 ** -7)
+    assert O.round_bf16(0.0) == 0.0
+
+
+def test_option_a_is_subsample_and_symmetric_channel_pad():
+    rng = np.random.default_rng(1)
+    h = rng.standard_normal((8, 8, 16))
+    a = O.option_a(h, 32)
+    t = TR.shortcut_a(torch.tensor(h).permute(2, 0, 1)[None], 32)[0].permute(1, 2, 0).numpy()
+    np.testing.assert_array_equal(a, t)
+    assert a.shape == (4, 4, 32) and np.all(a[:, :, :8] == 0) and np.all(a[:, :, 24:] == 0)
+
+
+# ------------------------------------------------------------------ predicates
+def test_exit_confidence_closed_form():
+    g = _gold("exit_closed_form.json")
+    for c in g["cases"]:
+        z = np.zeros(g["K"])
+        z[0] = c["b"]
+        conf = O.max_softmax(z)
+        assert conf == pytest.approx(c["conf"], rel=1e-14)
+        assert (conf >= g["tau"]) == c["exits"]
+    z = np.zeros(g["K"])
+    z[0] = g["b_star"]
+    assert O.max_softmax(z) == pytest.approx(0.9, abs=1e-15)
+    # shift invariance of softmax: adding a constant changes nothing
+    assert O.max_softmax(z + 123.0) == pytest.approx(O.max_softmax(z), rel=1e-14)
+
+
+def test_softmax_symmetry_and_argmax_ties():
+    g = _gold("softmax_symmetry.json")
+    assert O.max_softmax([0.0, 0.0, 0.0]) == pytest.approx(g["softmax_zeros3_max"], rel=1e-15)
+    assert O.argmax_lowest(g["argmax_case"]["z"]) == g["argmax_case"]["argmax"]
+    assert O.argmax_lowest(g["argmax_tie"]["z"]) == g["argmax_tie"]["argmax"]
+
+
+def test_gate_at_half_skips():
+    """Reading R2: execute iff p > 0.5, so sigma(0) = 0.5 skips."""
+    assert O.sigmoid(0.0) == 0.5
+    assert not (O.sigmoid(0.0) > 0.5)
+    assert O.sigmoid(1e-9) > 0.5
+
+
+def test_metrics_golden():
+    g = _gold("metrics.json")
+    a = [np.arange(10.0), np.ones(3)]
+    assert delta(a, a) == pytest.approx(g["delta_identical"], abs=1e-12)
+    b = [np.arange(10.0), np.ones(3)]
+    b[1] = b[1].copy()
+    b[1][2] += 1e-5
+    assert delta(b, a) == pytest.approx(g["delta_one_1e-5"], abs=1e-6)
+    v = [0] * 1000
+    c = [1] * 830 + [0] * 170
+    assert eta(c, v) == pytest.approx(g["eta_830_of_1000"])
+    # unequal-length generations are inconsistent (reading R15)
+    assert eta([np.array([1, 2])], [np.array([1, 2, 3])]) == 1.0
+
+
+# ------------------------------------------------------------------- config 1
+def _mlp_bruteforce(x, W, mode, tau=0.9):
+    """Independent fp64 NumPy implementation of the 3-block early-exit MLP."""
+    def f(name):
+        a = np.asarray(W[name])
+        if a.dtype == np.uint16:
+            a = (a.astype(np.uint32) << 16).view(np.float32)
+        return a.astype(np.float64)
+
+    def r(v):  # bf16 RNE via float32 bit tricks would double-round; use torch on exact fp64 -> ok only
+        return O.round_bf16(v) if mode == "mirror" else v
+
+    h = torch.tensor(np.float32(x)).to(torch.bfloat16).double().numpy()
+    outs = []
+    for k in range(3):
+        h = r(np.maximum(f(f"fc{k}.w").dot(h) + f(f"fc{k}.b"), 0))
+        z = f(f"head{k}.w").dot(h) + f(f"head{k}.b")
+        e = np.exp(z - z.max())
+        outs.append((z, (e / e.sum()).max()))
+    for k in range(2):
+        if outs[k][1] >= tau:
+            return outs[k][0], k
+    return outs[2][0], 2
+
+
+@pytest.mark.parametrize("mode", ["mirror", "exact"])
+def test_mlp_matches_bruteforce(mode):
+    W = wl.mlp_weights()
+    X = wl.mlp_inputs(wl.INPUT_SEED, 0, 32)
+    P = prg.prepare(W)
+    L, path, preds = O.run_batch(O.mlp_ee, X, P, mode, threads=1)
+    for i in range(32):
+        z, p = _mlp_bruteforce(X[i], W, mode)
+        assert path[i] == p
+        np.testing.assert_allclose(L[i], z, rtol=0, atol=1e-12)
+    assert np.bincount(path, minlength=3).sum() == 32
+
+
+def test_mlp_degenerate_thresholds():
+    """tau > 1: never exits (static net, final head); tau <= 1/K: everyone exits at head 0."""
+    W = wl.mlp_weights()
+    X = wl.mlp_inputs(wl.INPUT_SEED, 0, 16)
+    P = prg.prepare(W)
+    _, p_hi, _ = O.run_batch(O.mlp_ee, X, P, "exact", threads=1, tau=1.01)
+    _, p_lo, _ = O.run_batch(O.mlp_ee, X, P, "exact", threads=1, tau=0.1)
+    assert np.all(p_hi == 2) and np.all(p_lo == 0)
+
+
+# ------------------------------------------------------------------- config 2
+@pytest.fixture(scope="module")
+def r56():
+    return wl.sdn_r56_weights()
+
+
+def test_sdn_never_exit_is_static_resnet56(r56):
+    """tau > 1 => the dynamic program is the static ResNet-56 + final head (torch fp64)."""
+    X = wl.image_inputs(wl.INPUT_SEED, 0, 2)
+    P = prg.prepare(r56)
+    for i in range(2):
+        z, path, preds = O.sdn_resnet56(X[i], P, "exact", tau=1.5)
+        assert path == 4 and len(preds) == 4
+        ref = TR.head(TR.static_resnet(X[i], r56, 9), r56, "final").numpy()
+        np.testing.assert_allclose(z, ref, rtol=1e-12, atol=1e-12)
+
+
+def test_sdn_all_exit_at_ic1_is_prefix_net(r56):
+    """tau <= 1/K => every sample exits at IC after block 5 with that head's logits."""
+    X = wl.image_inputs(wl.INPUT_SEED, 5, 2)
+    P = prg.prepare(r56)
+    for i in range(2):
+        z, path, preds = O.sdn_resnet56(X[i], P, "exact", tau=0.1)
+        assert path == 0 and len(preds) == 1
+        ref = TR.head(TR.static_resnet(X[i], r56, 9, upto=5), r56, "ic0").numpy()
+        np.testing.assert_allclose(z, ref, rtol=1e-12, atol=1e-12)
+
+
+def test_sdn_mirror_stores_bf16_values(r56):
+    """Mirror mode: every stored activation is bf16-representable (rounding points R13)."""
+    X = wl.image_inputs(wl.INPUT_SEED, 0, 1)
+    P = prg.prepare(r56)
+    h = prg.stem(X[0], P, "mirror")
+    assert np.array_equal(O.round_bf16(h), h)
+    h2 = prg.basic_block(h, P, 1, 9, "mirror")
+    assert np.array_equal(O.round_bf16(h2), h2)
+    # and mirror differs from exact only by rounding-size perturbations
+    he = prg.basic_block(prg.stem(X[0], P, "exact"), P, 1, 9, "exact")
+    assert np.max(np.abs(he - h2)) < 0.05 * np.max(np.abs(he))
+
+
+def test_sdn_calibrated_exit_histogram(r56):
+    """The calibration makes the dynamic path branch (each exit taken) on held-out inputs."""
+    X = wl.image_inputs(wl.INPUT_SEED, 0, 48)
+    P = prg.prepare(r56)
+    _, path, preds = O.run_batch(O.sdn_resnet56, X, P, "mirror")
+    h = np.bincount(path, minlength=5)
+    assert h.sum() == 48 and np.count_nonzero(h) >= 4
+    for p, pr in zip(path, preds):          # path word = number of predicates evaluated - 1 on exit
+        assert len(pr) == min(p + 1, 4)
+
+
+# ------------------------------------------------------------------- config 3
+@pytest.fixture(scope="module")
+def r38():
+    return wl.skipnet_r38_weights()
+
+
+def _forced_gates(W, pattern):
+    W = dict(W)
+    for i in wl.SKIP_GATED:
+        W[f"gate{i}.b"] = np.array([1e9 if pattern(i) else -1e9], np.float32)
+    return W
+
+
+@pytest.mark.parametrize("name,pattern", [
+    ("all_execute", lambda i: True), ("all_skip", lambda i: False), ("even_blocks", lambda i: i % 2 == 0)])
+def test_skipnet_forced_gates_equal_static_composition(r38, name, pattern):
+    """Gate bias +-inf reduces SkipNet to a fixed static network (Listing 3 semantics)."""
+    W = _forced_gates(r38, pattern)
+    P = prg.prepare(W)
+    X = wl.image_inputs(wl.INPUT_SEED, 11, 1)
+    z, mask, preds = O.skipnet_resnet38(X[0], P, "exact")
+    execd = {1} | {i for i in wl.SKIP_GATED if pattern(i)}
+    assert mask == sum(1 << (i - 2) for i in wl.SKIP_GATED if pattern(i))
+    ref = TR.head(TR.static_resnet(X[0], W, 6, exec_blocks=execd), W, "final").numpy()
+    np.testing.assert_allclose(z, ref, rtol=1e-12, atol=1e-12)
+    assert len(preds) == 17
+
+
+def test_skipnet_calibrated_gates_branch(r38):
+    X = wl.image_inputs(wl.INPUT_SEED, 0, 24)
+    P = prg.prepare(r38)
+    _, mask, preds = O.run_batch(O.skipnet_resnet38, X, P, "mirror")
+    bits = np.array([bin(int(m)).count("1") for m in mask])
+    assert len(set(mask.tolist())) > 10          # many distinct paths (2^17 possible)
+    assert 3 <= bits.mean() <= 14
+
+
+def test_band_exclusion():
+    assert in_band([("exit", 0.9004, 0.9)])
+    assert not in_band([("exit", 0.902, 0.9), ("gate", 0.3, 0.5)])

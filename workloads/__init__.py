@@ -1,0 +1,288 @@
+"""Seeded synthetic workloads shared by the CUDA path and the oracle.
+
+This module is the ONLY code both sides use.  It holds no arithmetic of the
+method (no layer, predicate, compaction or scatter); it only draws numbers:
+
+* network inputs (images, MLP vectors) as a pure function of
+  (seed, global sample index, element index), so any subset can be
+  regenerated independently (SURVEY.md §8(d) "Seeds");
+* random-init weights of the five architectures (He-normal trunks, N(0,1/C)
+  heads/gates), rounded once to bf16 (RNE) -- the weight file both sides read;
+* application of frozen calibration constants (workloads/calib/*.json, written
+  by the committed script ``oracle/calibrate.py``, which calls only oracle/).
+
+Recipes are stated in DESIGN.md §3 ("Input recipe").
+"""
+from __future__ import annotations
+
+import json
+import math
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+# Listing 2: the host program's Normalize constants.
+IMAGENET_MEAN = np.array([0.485, 0.456, 0.406], dtype=np.float32)
+IMAGENET_STD = np.array([0.229, 0.224, 0.225], dtype=np.float32)
+
+WEIGHT_SEED = 0
+INPUT_SEED = 1
+CALIB_SEED = 2
+ORACLE_SUBSET_SEED = 3
+
+
+# ----------------------------------------------------------------------------
+# bf16 storage helpers (round-to-nearest-even of fp32 bit patterns).
+# ----------------------------------------------------------------------------
+def f32_to_bf16_bits(a) -> np.ndarray:
+    """fp32 -> bf16 bit pattern (uint16), round to nearest, ties to even."""
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float32))
+    u = a.view(np.uint32).astype(np.uint64)
+    lsb = (u >> 16) & 1
+    r = ((u + 0x7FFF + lsb) >> 16).astype(np.uint16)
+    # NaN stays NaN (not produced by the generators, guarded anyway)
+    nan = np.isnan(a)
+    if nan.any():
+        r[nan] = 0x7FC0
+    return r
+
+
+def bf16_bits_to_f32(b) -> np.ndarray:
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.uint16))
+    return (b.astype(np.uint32) << 16).view(np.float32)
+
+
+# ----------------------------------------------------------------------------
+# Counter-based uniform generator: splitmix64 finaliser of (seed, sample, elem).
+# ----------------------------------------------------------------------------
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def _splitmix64(x: np.ndarray) -> np.ndarray:
+    with np.errstate(over="ignore"):
+        z = x + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return z
+
+
+def counter_uniform(seed: int, sample: np.ndarray, elem: np.ndarray, stream: int = 0) -> np.ndarray:
+    """u in [0,1) with 24 random bits: top 24 bits of splitmix64(key)/2^24."""
+    with np.errstate(over="ignore"):
+        key = (np.uint64(seed) * np.uint64(0xD1B54A32D192ED03)) ^ (
+            np.asarray(sample, dtype=np.uint64) * np.uint64(0x100000001B3)
+            + np.asarray(elem, dtype=np.uint64) * np.uint64(0x9E3779B1)
+            + np.uint64(stream) * np.uint64(0xA24BAED4963EE407))
+    z = _splitmix64(key)
+    return ((z >> np.uint64(40)).astype(np.float64) / float(1 << 24))
+
+
+def _per_sample_normals(seed: int, idx: np.ndarray, n: int, stream: int) -> np.ndarray:
+    """Box-Muller normals, shape [len(idx), n], from counter uniforms."""
+    e = np.arange(n, dtype=np.uint64)[None, :]
+    s = idx.astype(np.uint64)[:, None]
+    u1 = counter_uniform(seed, s, 2 * e, stream)
+    u2 = counter_uniform(seed, s, 2 * e + np.uint64(1), stream)
+    u1 = np.maximum(u1, 1.0 / (1 << 25))
+    return np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * math.pi * u2)
+
+
+def image_inputs(seed: int, start: int, count: int, hw: int = 32, idx=None) -> np.ndarray:
+    """Normalized fp32 NHWC images [count, hw, hw, 3] (SURVEY §8(d) inputs).
+
+    u ~ U[0,1) per pixel, per-sample contrast g = exp(0.5 N(0,1)), per-sample
+    per-channel brightness b_c ~ N(0, 0.5^2);  p = 0.5 + g (u - 0.5) + 0.25 b_c;
+    x = (p - mean_c) / std_c with Listing 2's constants.
+    All per-pixel arithmetic in fp32, in this exact op order.
+    """
+    if idx is None:
+        idx = np.arange(start, start + count, dtype=np.int64)
+    idx = np.asarray(idx, dtype=np.int64)
+    n = len(idx)
+    nrm = _per_sample_normals(seed, idx, 4, stream=7)
+    gamma = np.exp(0.5 * nrm[:, 0]).astype(np.float32)
+    beta = (0.5 * nrm[:, 1:4]).astype(np.float32)
+    elem = np.arange(hw * hw * 3, dtype=np.uint64)[None, :]
+    u = counter_uniform(seed, idx.astype(np.uint64)[:, None], elem).astype(np.float32)
+    u = u.reshape(n, hw, hw, 3)
+    p = np.float32(0.5) + gamma[:, None, None, None] * (u - np.float32(0.5))
+    p = p + np.float32(0.25) * beta[:, None, None, :]
+    x = (p - IMAGENET_MEAN) / IMAGENET_STD
+    return np.ascontiguousarray(x.astype(np.float32))
+
+
+def mlp_inputs(seed: int, start: int, count: int, dim: int = 64, idx=None) -> np.ndarray:
+    """fp32 [count, dim], x ~ N(0,1) (config 1: 'random fp32 inputs')."""
+    if idx is None:
+        idx = np.arange(start, start + count, dtype=np.int64)
+    idx = np.asarray(idx, dtype=np.int64)
+    return _per_sample_normals(seed, idx, dim, stream=3).astype(np.float32)
+
+
+# ----------------------------------------------------------------------------
+# Architectures (parameter shapes only) and seeded random-init weights.
+# ----------------------------------------------------------------------------
+@dataclass(frozen=True)
+class ResNetCifarSpec:
+    blocks_per_stage: int          # 9 -> ResNet-56, 6 -> ResNet-38
+    widths: tuple = (16, 32, 64)
+
+    @property
+    def n_blocks(self):
+        return 3 * self.blocks_per_stage
+
+    def block_io(self, i: int):
+        """1-based block i -> (c_in, c_out, stride, hw_in)."""
+        s = (i - 1) // self.blocks_per_stage
+        first = (i - 1) % self.blocks_per_stage == 0
+        c_out = self.widths[s]
+        if s > 0 and first:
+            return self.widths[s - 1], c_out, 2, 32 >> (s - 1)
+        return c_out, c_out, 1, 32 >> s
+
+
+R56 = ResNetCifarSpec(9)
+R38 = ResNetCifarSpec(6)
+SDN_IC_AFTER = (5, 11, 16, 22)          # SURVEY §8(c) reading 4
+SKIP_GATED = tuple(range(2, 19))        # reading 7: blocks 2..18 gated
+NUM_CLASSES = 10
+EXIT_TAU = 0.9                          # config 1 value, reused
+
+
+class _Rng:
+    """One independent PCG64 stream per tensor, in a fixed registration order."""
+
+    def __init__(self, seed):
+        self.seed = seed
+        self.k = 0
+
+    def next(self):
+        self.k += 1
+        return np.random.default_rng([self.seed, self.k])
+
+
+def _he_conv(rng, co, k, ci, scale=1.0):
+    std = math.sqrt(2.0 / (k * k * ci)) * scale
+    return (rng.standard_normal((co, k, k, ci)) * std).astype(np.float32)
+
+
+def _bias(rng, n, amp=0.05):
+    return rng.uniform(-amp, amp, size=(n,)).astype(np.float32)
+
+
+def _bf16(a):
+    return f32_to_bf16_bits(a)
+
+
+def load_calib(name: str):
+    path = os.path.join(HERE, "calib", f"{name}.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        return json.load(f)
+
+
+def mlp_weights(seed: int = WEIGHT_SEED, head_scale: float = 4.0) -> dict:
+    """Config 1: 3 dense blocks 64->64 ReLU, heads 64->10 after blocks 1,2 and final."""
+    rng = _Rng(seed)
+    W = {}
+    for k in range(3):
+        W[f"fc{k}.w"] = _bf16(rng.next().standard_normal((64, 64)) * math.sqrt(2.0 / 64))
+        W[f"fc{k}.b"] = _bias(rng.next(), 64, 0.1)
+    for k in range(3):
+        W[f"head{k}.w"] = _bf16(rng.next().standard_normal((10, 64)) * (head_scale / 8.0))
+        W[f"head{k}.b"] = _bias(rng.next(), 10, 0.1)
+    return W
+
+
+def resnet_cifar_trunk(spec: ResNetCifarSpec, seed: int) -> dict:
+    """Stem 3->16 + basic blocks; conv2 of each block scaled by 1/sqrt(n_blocks)."""
+    rng = _Rng(seed)
+    W = {}
+    W["stem.w"] = _bf16(_he_conv(rng.next(), 16, 3, 3))
+    W["stem.b"] = _bias(rng.next(), 16)
+    for i in range(1, spec.n_blocks + 1):
+        ci, co, _, _ = spec.block_io(i)
+        W[f"b{i}.c1.w"] = _bf16(_he_conv(rng.next(), co, 3, ci))
+        W[f"b{i}.c1.b"] = _bias(rng.next(), co)
+        W[f"b{i}.c2.w"] = _bf16(_he_conv(rng.next(), co, 3, co, 1.0 / math.sqrt(spec.n_blocks)))
+        W[f"b{i}.c2.b"] = _bias(rng.next(), co)
+    return W, rng
+
+
+def _centered_head(H_raw: np.ndarray, scale: float, mu: np.ndarray):
+    """w = bf16(scale * H_raw); b = -(w . mu) so logits = w (g - mu)."""
+    w = _bf16(scale * H_raw)
+    wf = bf16_bits_to_f32(w).astype(np.float64)
+    b = (-(wf @ np.asarray(mu, dtype=np.float64))).astype(np.float32)
+    return w, b
+
+
+def sdn_r56_raw_heads(seed: int = WEIGHT_SEED) -> dict:
+    """Raw (uncalibrated) IC and final head directions H ~ N(0, 1/C)."""
+    rng = np.random.default_rng([seed, 1000])
+    out = {}
+    for k, blk in enumerate(SDN_IC_AFTER):
+        c = R56.block_io(blk)[1]
+        out[f"ic{k}"] = rng.standard_normal((NUM_CLASSES, c)) / math.sqrt(c)
+    out["final"] = rng.standard_normal((NUM_CLASSES, 64)) / math.sqrt(64)
+    return out
+
+
+def sdn_r56_weights(seed: int = WEIGHT_SEED, calib=None) -> dict:
+    """Config 2: ShallowDeep-style ResNet-56, ICs after blocks 5, 11, 16, 22."""
+    W, _ = resnet_cifar_trunk(R56, seed)
+    if calib is None:
+        calib = load_calib("cfg2")
+    raw = sdn_r56_raw_heads(seed)
+    for name, H in raw.items():
+        c = H.shape[1]
+        if calib is not None:
+            scale, mu = calib[name]["scale"], np.array(calib[name]["mu"])
+        else:  # uncalibrated default (used only by the calibration script itself)
+            scale, mu = 1.0, np.zeros(c)
+        W[f"{name}.w"], W[f"{name}.b"] = _centered_head(H, scale, mu)
+    W["tau"] = np.float32(EXIT_TAU)
+    return W
+
+
+def skipnet_r38_raw_gates(seed: int = WEIGHT_SEED) -> dict:
+    rng = np.random.default_rng([seed, 2000])
+    out = {}
+    for i in SKIP_GATED:
+        c = R38.block_io(i)[0]          # the gate sees the block INPUT (Listing 3)
+        out[f"gate{i}"] = rng.standard_normal((1, c)) / math.sqrt(c)
+    out["final"] = rng.standard_normal((NUM_CLASSES, 64)) / math.sqrt(64)
+    return out
+
+
+def skipnet_r38_weights(seed: int = WEIGHT_SEED, calib=None) -> dict:
+    """Config 3: SkipNet-style ResNet-38 with 17 feed-forward gates (blocks 2..18)."""
+    W, _ = resnet_cifar_trunk(R38, seed)
+    if calib is None:
+        calib = load_calib("cfg3")
+    raw = skipnet_r38_raw_gates(seed)
+    for i in SKIP_GATED:
+        g = raw[f"gate{i}"]
+        if calib is not None:
+            s, a = calib[f"gate{i}"]["scale"], calib[f"gate{i}"]["median"]
+        else:
+            s, a = 1.0, 0.0
+        W[f"gate{i}.w"] = _bf16(s * g)
+        W[f"gate{i}.b"] = np.array([-s * a], dtype=np.float32)
+    fin = raw["final"]
+    mu = np.array(calib["final"]["mu"]) if calib is not None else np.zeros(64)
+    W["final.w"], W["final.b"] = _centered_head(fin, 4.0, mu)
+    W["thr"] = np.float32(0.5)
+    return W
+
+
+CONFIGS = {
+    1: dict(name="mlp_ee", batch=32, desc="tiny early-exit MLP: 3 blocks width 64, 2 exit heads, tau 0.9, batch 32"),
+    2: dict(name="sdn_resnet56", batch=4096, desc="ShallowDeep-style early-exit ResNet-56, 32x32x3, batch 4096, 4 ICs"),
+    3: dict(name="skipnet_resnet38", batch=8192, desc="SkipNet-style gated ResNet-38, 32x32x3, batch 8192, 17 gates"),
+}
