@@ -1,0 +1,212 @@
+/*
+ * dycl.h -- C ABI of libdycl.so: batched inference of a dynamic neural network
+ * (DyNN) that has been rewritten into conditional-free sub-networks plus a host
+ * module holding the control flow (DyCL, arXiv 2307.04963), executed on B200.
+ *
+ * The paper's problem statement (Sec. 5 Eq. 2): given a DyNN
+ * P_DyNN, produce a host program P_Host with P_DyNN(x) = P_Host(x) for all x.
+ * P_Host "invokes" compiled sub-DNNs and holds the conditionals (PAPER.md
+ * L534-535, L720); the deployment verbs are set_input / run / get_output
+ * (Listing 2).  This library is the run-time half of that picture:
+ *
+ *   - sub-networks (HCFG tensor nodes, Sec. 5.3) are registered layer
+ *     by layer; each runs as sm_100a tcgen05 kernels over the samples that take it;
+ *   - logic nodes (HCFG logic nodes: exit, gate, final) are registered in program
+ *     order as a chain; their predicates run per sample on the device;
+ *   - the host module itself (branching, compaction of the rows that take each
+ *     branch, scatter of results to the original order) runs on the device, so a
+ *     run has NO host round trip.
+ *
+ * Conventions (apply to every function):
+ *   - Return value: dycl_status; 0 == DYCL_OK, negative values are errors.  No C++
+ *     exception crosses this ABI and nothing aborts the process.
+ *   - On error, dycl_last_error(g) returns a human-readable message.
+ *   - Host pointers passed at registration are COPIED before the call returns
+ *     (weight snapshot semantics); the caller may free them.
+ *   - Device pointers passed to dycl_run are caller-owned and must stay valid until
+ *     the work enqueued on `stream` completes.  The library owns its workspace
+ *     (allocated in dycl_finalize, freed in dycl_graph_destroy).
+ *   - A graph is immutable after dycl_finalize; one dycl_run in
+ *     flight per graph; use one graph per stream for concurrency.
+ *   - Layouts: per-sample activations are NHWC ([H][W][C], C fastest); bf16 values
+ *     are passed as their uint16 bit patterns.
+ */
+#ifndef DYCL_H_
+#define DYCL_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dycl_graph_s* dycl_graph;
+typedef int32_t dycl_node;      /* sub-network id, assigned in creation order from 0 */
+
+typedef enum {
+  DYCL_OK = 0,
+  DYCL_E_INVALID_ARG = -1,      /* null pointer, out-of-range value                     */
+  DYCL_E_SHAPE_MISMATCH = -2,   /* layer shape rule violated, batch > max */
+  DYCL_E_SIGNATURE = -3,        /* head output widths disagree                          */
+  DYCL_E_SHAPE_JOIN = -4,       /* gate then-branch vs skip output shapes*/
+  DYCL_E_STATE = -5,            /* call not allowed in this state (finalized / not)     */
+  DYCL_E_UNSUPPORTED = -6,      /* valid request this build does not implement          */
+  DYCL_E_OOM = -7,              /* device allocation failed                             */
+  DYCL_E_CUDA = -8,             /* CUDA runtime error (text in dycl_last_error)         */
+  DYCL_E_NCCL = -9
+} dycl_status;
+
+typedef enum { DYCL_ACT_NONE = 0, DYCL_ACT_RELU = 1 } dycl_act;
+
+/* ---------------------------------------------------------------- graphs --- */
+
+/* Create an empty graph on CUDA device `cuda_device` whose per-sample input is an
+ * fp32 NHWC tensor [in_h][in_w][in_c] (an MLP input of width d is [1][1][d]).
+ * The run's first step (a0, Listing 2's pre-processing) casts
+ * it to bf16 and pads channels to a multiple of 8.  *out receives the handle. */
+dycl_status dycl_graph_create(int cuda_device, int in_h, int in_w, int in_c, dycl_graph* out);
+
+/* Numerics of the activations between layers (call before dycl_finalize).
+ * Tensor-core operands are always bf16 with fp32 accumulation.
+ *   DYCL_PREC_FP32_STREAM (default): residual-stream tensors (block inputs/outputs,
+ *     sub-network outputs) are kept in fp32; each conv/dense reads a bf16 (RNE)
+ *     copy of its input; intermediates inside a block are bf16.
+ *   DYCL_PREC_BF16: every activation is stored bf16 (half the bytes; logits drift
+ *     ~2.5e-2 relative after 27 blocks -- see DESIGN.md §2 reading R13). */
+enum { DYCL_PREC_BF16 = 0, DYCL_PREC_FP32_STREAM = 1 };
+dycl_status dycl_graph_set_precision(dycl_graph g, int precision);
+
+/* Free the graph and all device memory it owns.  NULL is accepted. */
+dycl_status dycl_graph_destroy(dycl_graph g);
+
+/* Last error message for g (or for failed dycl_graph_create if g == NULL).
+ * Library-owned; valid until the next call on g. Never NULL. */
+const char* dycl_last_error(dycl_graph g);
+
+/* ------------------------------------------------------- sub-networks ------ */
+/* A sub-network is a conditional-free straight-line layer list (an HCFG tensor
+ * node).  Its input shape is the shape flowing into the logic
+ * node that uses it; shapes are propagated at dycl_finalize exactly as Alg. 2
+ * propagates them: a logic node's output shape is its
+ * predecessor's, a tensor node is compiled for its predecessor's output shape. */
+
+dycl_status dycl_subnet_begin(dycl_graph g, dycl_node* out);
+
+/* Mark the current tensor as the shortcut source of a residual block. */
+dycl_status dycl_subnet_block_begin(dycl_graph g, dycl_node sn);
+
+/* 2-D convolution (the 'convolutional operator'):
+ *   y[ho][wo][o] = act( b[o] + sum_{r,s,c} w[o][r][s][c] x[ho*stride-pad+r][wo*stride-pad+s][c]
+ *                       (+ shortcut[ho][wo][o] if residual) )
+ * w: host bf16 bits [c_out][k][k][c_in]; b: host fp32 [c_out].  c_in must equal
+ * the channel count that shape propagation delivers to this layer (checked at
+ * dycl_finalize, DYCL_E_SHAPE_MISMATCH otherwise); it sizes the weight snapshot.  residual = 1 adds the tensor saved by the last
+ * dycl_subnet_block_begin: as is when its shape equals the output's, or the
+ * parameter-free 'option A' shortcut (stride-2 subsample, (c_out-c_in)/2 zero
+ * channels each side) when the output halves H, W and doubles C.  Else
+ * DYCL_E_SHAPE_MISMATCH (reported at dycl_finalize).  c_out % 16 == 0 (tensor-core
+ * N granularity), 1 <= k <= 7, stride in {1, 2}. */
+dycl_status dycl_subnet_conv2d(dycl_graph g, dycl_node sn, int c_in, int c_out, int k, int stride, int pad,
+                               const uint16_t* w_bf16, const float* bias, dycl_act act, int residual);
+
+/* Dense layer (the 'dense operator') on a [1][1][n_in] tensor:
+ * y = act(W x + b), W: host bf16 bits [n_out][n_in], b: host fp32 [n_out]
+ * (n_in checked at dycl_finalize like conv2d's c_in).
+ * If out_fp32 == 0 the layer runs on tensor cores and stores bf16 (n_out % 16 == 0).
+ * If out_fp32 == 1 the layer is a classifier / gate head producing fp32 logits
+ * (any n_out >= 1); it must be the last layer of its sub-network. */
+dycl_status dycl_subnet_dense(dycl_graph g, dycl_node sn, int n_in, int n_out, const uint16_t* w_bf16,
+                              const float* bias, dycl_act act, int out_fp32);
+
+/* Global average pooling [H][W][C] -> [1][1][C], fp32 mean (kept in fp32 when
+ * followed by an out_fp32 dense head). */
+dycl_status dycl_subnet_gap(dycl_graph g, dycl_node sn);
+
+dycl_status dycl_subnet_end(dycl_graph g, dycl_node sn);
+
+/* ---------------------------------------------------------- logic nodes ---- */
+/* Registered in program order; together they form the host module.  Each uses
+ * the current per-sample tensor h of the samples still running. */
+
+/* h <- subnet(h) for every live sample. */
+dycl_status dycl_seq(dycl_graph g, dycl_node subnet);
+
+/* Early exit (Shallow-Deep): z = head(h) (fp32 logits [K]);
+ * samples with max_j softmax(z)_j >= tau terminate: their logits z and
+ * path = (index of this exit among the graph's exits) are written to the
+ * outputs at their ORIGINAL batch position; the others continue with h. */
+dycl_status dycl_exit(dycl_graph g, dycl_node head_subnet, float tau);
+
+/* Conditional skip (SkipNet, Listing 3): z = gate(h) (one fp32
+ * logit); samples with sigmoid(z) > thr run h <- then_subnet(h) and set bit
+ * (index of this gate) in their path word; the others take the skip path
+ * (identity, or option A when then_subnet halves H, W and doubles C -- the only
+ * two join shapes accepted, else DYCL_E_SHAPE_JOIN). */
+dycl_status dycl_gate(dycl_graph g, dycl_node gate_subnet, float thr, dycl_node then_subnet);
+
+/* Default exit: every sample still running terminates with z = head(h).
+ * path = number of exits registered (early-exit nets) or the gate mask. */
+dycl_status dycl_final(dycl_graph g, dycl_node head_subnet);
+
+/* Alg. 2 analog: shape propagation over the chain, buffer planning for
+ * max_batch samples, weight upload to HBM.  Errors: SHAPE_MISMATCH, SHAPE_JOIN,
+ * SIGNATURE, OOM, CUDA. */
+dycl_status dycl_finalize(dycl_graph g, int64_t max_batch);
+
+/* ------------------------------------------------------------------ run ---- */
+typedef struct {
+  const float* input;     /* device fp32 [batch][in_h][in_w][in_c] (NHWC)             */
+  int64_t batch;          /* 0 <= batch <= max_batch                                  */
+  float* logits;          /* device fp32 [batch][K]   (output, original order)        */
+  int32_t* path;          /* device int32 [batch]     exit index or gate mask word     */
+  int32_t* node_counts;   /* device int32 [dycl_num_count_slots] live-row counts, or NULL */
+} dycl_io;
+
+/* Enqueue one batched inference on `stream` (a cudaStream_t, NULL = default stream).
+ * Asynchronous and stream-ordered; no host synchronisation and no device->host
+ * traffic.  Output row i always belongs to input row i. */
+dycl_status dycl_run(dycl_graph g, const dycl_io* io, void* stream);
+
+/* Same, with HOST buffers (pinned or pageable): copies the input host->device,
+ * runs, copies logits and path device->host, and synchronises `stream` before
+ * returning -- the deployment-style call of Listing 2 (set_input/run/get_output). */
+dycl_status dycl_run_host(dycl_graph g, const float* input_host, int64_t batch,
+                          float* logits_host, int32_t* path_host, void* stream);
+
+/* --------------------------------------------------------- introspection --- */
+/* Number of device count slots a run writes (for dycl_io.node_counts). */
+dycl_status dycl_num_count_slots(dycl_graph g, int32_t* out);
+/* Number of this library's kernels one dycl_run launches. */
+dycl_status dycl_launches_per_run(dycl_graph g, int32_t* out);
+/* Output width K of the heads (valid after finalize). */
+dycl_status dycl_num_classes(dycl_graph g, int32_t* out);
+
+/* Per-launch profiling: when enabled, dycl_run brackets every launch with CUDA
+ * events on the run's stream.  dycl_profile_read synchronises the last run's
+ * stream and returns, per launch in issue order: kind (see DYCL_K_*), elapsed ms,
+ * and the launch's algorithmic bytes and flops (computed from the live-row counts
+ * the launch processed, read back AFTER the run).  Arrays hold max_n entries;
+ * *n_out receives the number of launches. */
+enum { DYCL_K_INPUT = 0, DYCL_K_CONV = 1, DYCL_K_HEAD = 2, DYCL_K_COMPACT = 3,
+       DYCL_K_GATHER = 4, DYCL_K_SCATTER = 5, DYCL_K_INIT = 6 };
+dycl_status dycl_set_profiling(dycl_graph g, int enable);
+dycl_status dycl_profile_read(dycl_graph g, int32_t max_n, int32_t* kind, float* ms,
+                              double* bytes, double* flops, int32_t* n_out);
+
+/* ------------------------------------------------------------ test hook ---- */
+/* Run ONE conv2d layer (the a1 tensor-core kernel, same code path dycl_run uses)
+ * on caller-owned device buffers and synchronise.  For element-wise kernel tests.
+ *   x   : device bf16 [n][H][W][C], C % 8 == 0
+ *   w   : host bf16 [c_out][k][k][C];  bias: host fp32 [c_out]
+ *   res : device bf16 shortcut or NULL; res_mode 0 none, 1 identity [n][Ho][Wo][c_out],
+ *         2 option A from [n][2Ho][2Wo][c_out/2]
+ *   y   : device bf16 [n][Ho][Wo][c_out]
+ * g supplies the device (any created graph).  Errors: INVALID_ARG, UNSUPPORTED, CUDA. */
+dycl_status dycl_debug_conv2d(dycl_graph g, int64_t n, int H, int W, int C, const uint16_t* w, const float* bias,
+                              int c_out, int k, int stride, int pad, int relu, const void* res, int res_mode,
+                              const void* x, void* y);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DYCL_H_ */

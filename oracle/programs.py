@@ -8,10 +8,17 @@ the left-hand side of Eq. 2 (P_DyNN(x)).  Per sample it returns
 the output logits, the path taken, and every predicate value it evaluated
 (kind, value, threshold) so the harness can apply the 1e-3 band (reading R12).
 
-Rounding (mode='mirror'): bf16 RNE at the production path's storage points --
-after the input cast (a0), after every conv/dense epilogue (bias [+shortcut]
--> ReLU -> round).  Pooled features, head/gate logits and predicates stay fp64.
-Mode 'exact': no rounding after the bf16 input.  (reading R13.)
+Modes (reading R13; all three round the network input to bf16, the
+a0 cast of Listing 2's pre-processing):
+  'mirror'      -- the production numerics (fp32 residual stream): every tensor-
+                   core operand is bf16 (RNE) -- the input of each conv / dense
+                   layer is rounded, and so is a block's intermediate activation
+                   (stored bf16); block outputs / sub-network outputs (the
+                   residual stream) are NOT rounded.  Decisions are graded here.
+  'mirror_bf16' -- every stored activation rounded to bf16 (the DYCL_PREC_BF16
+                   storage mode).
+  'exact'       -- no rounding after the bf16 input.
+Pooled features, head/gate logits and predicates are never rounded.
 """
 from __future__ import annotations
 
@@ -39,8 +46,19 @@ def prepare(W: dict) -> dict:
     return P
 
 
-def _rnd(v, mode):
-    return round_bf16(v) if mode == "mirror" else v
+def _operand(v, mode):
+    """A tensor-core operand: bf16 in both mirror modes."""
+    return round_bf16(v) if mode in ("mirror", "mirror_bf16") else v
+
+
+def _inner(v, mode):
+    """An activation consumed only by the next conv (stored bf16 in both mirror modes)."""
+    return round_bf16(v) if mode in ("mirror", "mirror_bf16") else v
+
+
+def _stream(v, mode):
+    """A residual-stream / sub-network output tensor (bf16 only in mirror_bf16)."""
+    return round_bf16(v) if mode == "mirror_bf16" else v
 
 
 # ---------------------------------------------------------------------------
@@ -53,9 +71,9 @@ def _rnd(v, mode):
 # ---------------------------------------------------------------------------
 def mlp_ee(x, P, mode="mirror", tau=0.9):
     preds = []
-    h = _rnd(np.asarray(x, np.float64), "mirror")            # a0: input cast to bf16
+    h = round_bf16(np.asarray(x, np.float64))                 # a0: input cast to bf16
     for k in range(3):
-        h = _rnd(relu(dense(P[f"fc{k}.w"], P[f"fc{k}.b"], h)), mode)
+        h = _stream(relu(dense(P[f"fc{k}.w"], P[f"fc{k}.b"], _operand(h, mode))), mode)
         z = dense(P[f"head{k}.w"], P[f"head{k}.b"], h)
         if k < 2:
             conf = max_softmax(z)
@@ -80,14 +98,14 @@ def _block_io(i, per_stage, widths=(16, 32, 64)):
 def basic_block(h, P, i, per_stage, mode):
     """relu(conv2(relu(conv1(h) + b1)) + b2 + shortcut(h))."""
     ci, co, stride = _block_io(i, per_stage)
-    t = _rnd(relu(conv2d(h, P[f"b{i}.c1.w"], P[f"b{i}.c1.b"], stride, 1)), mode)
+    t = _inner(relu(conv2d(_operand(h, mode), P[f"b{i}.c1.w"], P[f"b{i}.c1.b"], stride, 1)), mode)
     sc = h if stride == 1 else option_a(h, co)
-    return _rnd(relu(conv2d(t, P[f"b{i}.c2.w"], P[f"b{i}.c2.b"], 1, 1) + sc), mode)
+    return _stream(relu(conv2d(t, P[f"b{i}.c2.w"], P[f"b{i}.c2.b"], 1, 1) + sc), mode)
 
 
 def stem(x, P, mode):
-    h = _rnd(np.asarray(x, np.float64), "mirror")            # a0: input cast to bf16
-    return _rnd(relu(conv2d(h, P["stem.w"], P["stem.b"], 1, 1)), mode)
+    h = round_bf16(np.asarray(x, np.float64))                 # a0: input cast to bf16
+    return _stream(relu(conv2d(h, P["stem.w"], P["stem.b"], 1, 1)), mode)
 
 
 # ---------------------------------------------------------------------------

@@ -1,0 +1,914 @@
+// libdycl runtime: C ABI (include/dycl.h), restricted-HCFG registry, Alg.-2-style
+// shape propagation and buffer planning, and the device-side plan executor.
+//
+// PAPER.md mapping:
+//   sub-network   = HCFG tensor node, conditional-free (Sec. 5.3)
+//   exit / gate   = HCFG logic node evaluated on an intermediate tensor (L265)
+//   finalize      = Alg. 2 (L658-716): walk the chain from N0 carrying the shape;
+//                   a logic node's output shape is its predecessor's; each tensor
+//                   node is "compiled" (planned) for the predecessor's output shape
+//   run           = the host API P_Host(x) (Sec. 5.6) -- but enqueued as
+//                   device work only: predicates, compaction and scatter are
+//                   kernels, the live counts stay in HBM (Challenge 2, L499-501).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/dycl.h"
+#include "kernels.h"
+
+namespace {
+
+struct Shape {
+  int H = 0, W = 0, C = 0;   // C = logical channels
+  int Cp() const { return (C + 7) / 8 * 8; }
+  bool operator==(const Shape& o) const { return H == o.H && W == o.W && C == o.C; }
+  long long row_elems() const { return (long long)H * W * Cp(); }
+};
+
+enum LayerKind { L_CONV, L_DENSE, L_GAP, L_BLOCK };
+
+struct Layer {
+  LayerKind kind;
+  int cout = 0, k = 1, stride = 1, pad = 0, relu = 0, residual = 0, out_fp32 = 0;
+  std::vector<uint16_t> w;
+  std::vector<float> b;
+  // planned at finalize
+  Shape in, out;
+  int K = 0, Kp = 0, res_mode = 0;
+  Shape res_shape;
+  uint16_t* d_w = nullptr;
+  float* d_b = nullptr;
+};
+
+struct Subnet {
+  std::vector<Layer> layers;
+  bool ended = false;
+  bool is_head = false;       // [GAP] + dense(out_fp32)
+  Shape in, out;
+  int head_K = 0;
+};
+
+enum NodeKind { N_SEQ, N_EXIT, N_GATE, N_FINAL };
+struct Node {
+  NodeKind kind;
+  int sn = -1, then_sn = -1;
+  float thr = 0.f;
+  int ordinal = 0;            // exit index / gate index
+  int skip_mode = 0;          // gate: 0 identity, 1 option A
+  Shape in, out;
+};
+
+struct Launch {               // profiling record
+  int kind;
+  cudaEvent_t e0, e1;
+  const int* count_dev;       // live-count slot the launch processed
+  double bytes_per_row, flops_per_row, bytes_fixed;
+};
+
+}  // namespace
+
+struct dycl_graph_s {
+  int device = 0;
+  Shape input;
+  std::vector<Subnet> subnets;
+  std::vector<Node> nodes;
+  bool finalized = false;
+  int64_t max_batch = 0;
+  int num_sms = 148;
+  int K = 0;
+  int n_exits = 0, n_gates = 0;
+  std::string err;
+  // device workspace
+  static constexpr int NBUF = 6;
+  static constexpr int NBUF32 = 4;
+  uint16_t* buf[NBUF] = {};
+  float* buf32[NBUF32] = {};
+  int precision = DYCL_PREC_FP32_STREAM;
+  long long max_row_elems = 0;
+  int* d_counts = nullptr;
+  int n_slots = 0;
+  int* d_orig[2] = {};
+  int* d_list1 = nullptr;
+  int* d_list0 = nullptr;
+  uint8_t* d_flag = nullptr;
+  float* d_pred = nullptr;
+  float* d_z = nullptr;
+  float* d_in_stage = nullptr;      // dycl_run_host staging
+  float* d_logit_stage = nullptr;
+  int32_t* d_path_stage = nullptr;
+  int launches_per_run = 0;
+  // profiling
+  bool profiling = false;
+  std::vector<Launch> prof;
+  size_t prof_used = 0;
+  cudaStream_t prof_stream = nullptr;
+};
+
+static thread_local std::string g_create_err;
+
+namespace {
+
+dycl_status fail(dycl_graph g, dycl_status s, const std::string& msg) {
+  if (g) g->err = msg; else g_create_err = msg;
+  return s;
+}
+dycl_status cuda_fail(dycl_graph g, cudaError_t e, const char* where) {
+  return fail(g, DYCL_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define CK(call)                                            \
+  do {                                                      \
+    cudaError_t e_ = (call);                                \
+    if (e_ != cudaSuccess) return cuda_fail(g, e_, #call);  \
+  } while (0)
+
+dycl_status check_sn(dycl_graph g, dycl_node sn) {
+  if (!g) return DYCL_E_INVALID_ARG;
+  if (g->finalized) return fail(g, DYCL_E_STATE, "graph already finalized");
+  if (sn < 0 || sn >= (int)g->subnets.size()) return fail(g, DYCL_E_INVALID_ARG, "bad subnet id");
+  if (g->subnets[sn].ended) return fail(g, DYCL_E_STATE, "subnet already ended");
+  return DYCL_OK;
+}
+
+template <typename T>
+dycl_status dmalloc(dycl_graph g, T** p, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), bytes);
+  if (e != cudaSuccess) return fail(g, DYCL_E_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  return DYCL_OK;
+}
+
+// Shape propagation through one subnet (Alg. 2 line: "compile N with the shape of
+// its predecessor").  Fills each layer's in/out and packed-weight geometry.
+dycl_status plan_subnet(dycl_graph g, Subnet& s, const Shape& in, int sn_id) {
+  Shape cur = in;
+  Shape block_src;
+  bool have_block = false;
+  s.in = in;
+  for (size_t li = 0; li < s.layers.size(); ++li) {
+    Layer& L = s.layers[li];
+    L.in = cur;
+    char where[96];
+    snprintf(where, sizeof where, "subnet %d layer %zu: ", sn_id, li);
+    switch (L.kind) {
+      case L_BLOCK:
+        block_src = cur;
+        have_block = true;
+        L.out = cur;
+        break;
+      case L_GAP:
+        L.out = Shape{1, 1, cur.C};
+        cur = L.out;
+        break;
+      case L_CONV: {
+        if ((int)L.w.size() != L.cout * L.k * L.k * cur.C)
+          return fail(g, DYCL_E_SHAPE_MISMATCH, std::string(where) + "conv weight size != c_out*k*k*c_in");
+        const int Ho = (cur.H + 2 * L.pad - L.k) / L.stride + 1;
+        const int Wo = (cur.W + 2 * L.pad - L.k) / L.stride + 1;
+        if (Ho <= 0 || Wo <= 0) return fail(g, DYCL_E_SHAPE_MISMATCH, std::string(where) + "empty output");
+        L.out = Shape{Ho, Wo, L.cout};
+        L.K = L.k * L.k * cur.Cp();
+        L.Kp = (L.K + 63) / 64 * 64;
+        L.res_mode = 0;
+        if (L.residual) {
+          if (!have_block) return fail(g, DYCL_E_SHAPE_MISMATCH, std::string(where) + "residual without block_begin");
+          L.res_shape = block_src;
+          if (block_src == L.out) L.res_mode = 1;
+          else if (block_src.H == 2 * Ho && block_src.W == 2 * Wo && 2 * block_src.C == L.cout &&
+                   block_src.C % 16 == 0)
+            L.res_mode = 2;
+          else return fail(g, DYCL_E_SHAPE_MISMATCH, std::string(where) + "shortcut shape neither identity nor option A");
+        }
+        cur = L.out;
+        break;
+      }
+      case L_DENSE: {
+        if (cur.H != 1 || cur.W != 1)
+          return fail(g, DYCL_E_SHAPE_MISMATCH, std::string(where) + "dense needs a [1][1][C] input (add gap)");
+        if ((int)L.w.size() != L.cout * cur.C)
+          return fail(g, DYCL_E_SHAPE_MISMATCH, std::string(where) + "dense weight size != n_out*n_in");
+        L.out = Shape{1, 1, L.cout};
+        if (L.out_fp32) {
+          if (li + 1 != s.layers.size())
+            return fail(g, DYCL_E_SHAPE_MISMATCH, std::string(where) + "fp32 head must be the last layer");
+        } else {
+          L.K = cur.Cp();
+          L.Kp = (L.K + 63) / 64 * 64;
+        }
+        cur = L.out;
+        break;
+      }
+    }
+  }
+  s.out = cur;
+  // head pattern: [gap] dense(out_fp32)
+  s.is_head = false;
+  const size_t n = s.layers.size();
+  if (n >= 1 && s.layers[n - 1].kind == L_DENSE && s.layers[n - 1].out_fp32) {
+    if (n == 1 || (n == 2 && s.layers[0].kind == L_GAP)) {
+      s.is_head = true;
+      s.head_K = s.layers[n - 1].cout;
+    } else {
+      return fail(g, DYCL_E_UNSUPPORTED, "fp32 heads must be [gap] + dense(out_fp32)");
+    }
+  }
+  return DYCL_OK;
+}
+
+dycl_status upload_subnet(dycl_graph g, Subnet& s) {
+  for (Layer& L : s.layers) {
+    if (L.kind == L_CONV || (L.kind == L_DENSE && !L.out_fp32)) {
+      // repack to [Cout][k][k][Cp] padded along K to Kp (zeros)
+      const int Cin = L.in.C, Cp = L.in.Cp();
+      std::vector<uint16_t> wp((size_t)L.cout * L.Kp, 0);
+      for (int o = 0; o < L.cout; ++o)
+        for (int t = 0; t < L.k * L.k; ++t)
+          for (int c = 0; c < Cin; ++c)
+            wp[(size_t)o * L.Kp + (size_t)t * Cp + c] = L.w[((size_t)o * L.k * L.k + t) * Cin + c];
+      dycl_status st = dmalloc(g, &L.d_w, wp.size() * 2);
+      if (st) return st;
+      CK(cudaMemcpy(L.d_w, wp.data(), wp.size() * 2, cudaMemcpyHostToDevice));
+    } else if (L.kind == L_DENSE) {
+      const int Cin = L.in.C, Cp = L.in.Cp();
+      std::vector<uint16_t> wp((size_t)L.cout * Cp, 0);
+      for (int o = 0; o < L.cout; ++o)
+        for (int c = 0; c < Cin; ++c) wp[(size_t)o * Cp + c] = L.w[(size_t)o * Cin + c];
+      dycl_status st = dmalloc(g, &L.d_w, wp.size() * 2);
+      if (st) return st;
+      CK(cudaMemcpy(L.d_w, wp.data(), wp.size() * 2, cudaMemcpyHostToDevice));
+    }
+    if (!L.b.empty()) {
+      dycl_status st = dmalloc(g, &L.d_b, L.b.size() * 4);
+      if (st) return st;
+      CK(cudaMemcpy(L.d_b, L.b.data(), L.b.size() * 4, cudaMemcpyHostToDevice));
+    }
+  }
+  return DYCL_OK;
+}
+
+// ------------------------------------------------------------------ executor
+// An activation lives in a bf16 buffer (the tensor-core operand copy) and, for
+// residual-stream tensors in DYCL_PREC_FP32_STREAM, also in an fp32 buffer.
+struct Tensor {
+  int b = -1, f = -1;
+};
+
+struct Exec {
+  dycl_graph g;
+  cudaStream_t st;
+  int batch;
+  float* out_logits;
+  int32_t* out_path;
+  int slot = 1;               // next free count slot
+  int nlaunch = 0;
+
+  void prof_begin(int kind, const int* cnt, double bpr, double fpr, double bfix) {
+    if (!g->profiling) return;
+    if (g->prof_used >= g->prof.size()) {
+      Launch L{};
+      cudaEventCreate(&L.e0);
+      cudaEventCreate(&L.e1);
+      g->prof.push_back(L);
+    }
+    Launch& L = g->prof[g->prof_used];
+    L.kind = kind;
+    L.count_dev = cnt;
+    L.bytes_per_row = bpr;
+    L.flops_per_row = fpr;
+    L.bytes_fixed = bfix;
+    cudaEventRecord(L.e0, st);
+  }
+  void prof_end() {
+    ++nlaunch;
+    if (!g->profiling) return;
+    cudaEventRecord(g->prof[g->prof_used].e1, st);
+    ++g->prof_used;
+  }
+
+  Tensor pick_tensor(bool stream, std::initializer_list<Tensor> busy) {
+    std::vector<int> bb, bf;
+    for (const Tensor& t : busy) {
+      bb.push_back(t.b);
+      bf.push_back(t.f);
+    }
+    Tensor o;
+    for (int i = 0; i < dycl_graph_s::NBUF && o.b < 0; ++i)
+      if (std::find(bb.begin(), bb.end(), i) == bb.end()) o.b = i;
+    if (stream)
+      for (int i = 0; i < dycl_graph_s::NBUF32 && o.f < 0; ++i)
+        if (std::find(bf.begin(), bf.end(), i) == bf.end()) o.f = i;
+    return o;
+  }
+  bool fp32_stream() const { return g->precision == DYCL_PREC_FP32_STREAM; }
+
+  // Run subnet s on the rows of `in` (device count `cnt`).  The last layer writes
+  // into `out_hint` when given (b >= 0).  `busy` is an outer tensor to preserve.
+  dycl_status subnet(const Subnet& s, Tensor in, const int* cnt, Tensor out_hint, Tensor busy, Tensor* out) {
+    Tensor cur = in, shortcut;
+    for (size_t li = 0; li < s.layers.size(); ++li) {
+      const Layer& L = s.layers[li];
+      if (L.kind == L_BLOCK) {
+        shortcut = cur;
+        continue;
+      }
+      if (L.kind == L_GAP || (L.kind == L_DENSE && L.out_fp32))
+        return fail(g, DYCL_E_UNSUPPORTED, "head layers inside a sequential subnet");
+      const bool last = li + 1 == s.layers.size();
+      const bool stream = fp32_stream() && (last || L.residual || s.layers[li + 1].kind == L_BLOCK);
+      Tensor o = (last && out_hint.b >= 0) ? out_hint : pick_tensor(stream, {cur, shortcut, busy, out_hint});
+      if (o.b < 0 || (stream && o.f < 0)) return fail(g, DYCL_E_STATE, "internal: out of activation buffers");
+      if (!stream) o.f = -1;
+      dycl::ConvArgs a{};
+      a.x = g->buf[cur.b];
+      a.w = L.d_w;
+      a.bias = L.d_b;
+      a.res = L.res_mode ? g->buf[shortcut.b] : nullptr;
+      a.res32 = (L.res_mode && shortcut.f >= 0) ? g->buf32[shortcut.f] : nullptr;
+      a.y = g->buf[o.b];
+      a.y32 = o.f >= 0 ? g->buf32[o.f] : nullptr;
+      a.n_live = cnt;
+      a.n_static = 0;
+      a.H = L.in.H; a.W = L.in.W; a.C = L.in.Cp();
+      a.Ho = L.out.H; a.Wo = L.out.W; a.Cout = L.out.C;
+      a.ksz = L.k; a.stride = L.stride; a.pad = L.pad;
+      a.K = L.K; a.Kp = L.Kp;
+      a.relu = L.relu;
+      a.res_mode = L.res_mode;
+      a.rH = L.res_shape.H; a.rW = L.res_shape.W; a.rC = L.res_shape.Cp();
+      a.r_pad_lo = (L.out.C - L.res_shape.C) / 2;
+      const double res_b = L.res_mode ? (a.res32 ? 4.0 : 2.0) * L.res_shape.row_elems() *
+                                            (L.res_mode == 2 ? 0.25 : 1.0) : 0.0;
+      const double row_b = 2.0 * L.in.row_elems() + (o.f >= 0 ? 6.0 : 2.0) * L.out.row_elems() + res_b;
+      const double row_f = 2.0 * L.out.H * L.out.W * L.out.C * (double)(L.k * L.k * L.in.C);
+      prof_begin(DYCL_K_CONV, cnt, row_b, row_f, 2.0 * L.out.C * L.Kp);
+      cudaError_t e = dycl::launch_conv_tc(a, batch, g->num_sms, st);
+      prof_end();
+      if (e != cudaSuccess) return cuda_fail(g, e, "launch_conv_tc");
+      cur = o;
+    }
+    *out = cur;
+    return DYCL_OK;
+  }
+
+  dycl_status head(const Subnet& s, Tensor in, const int* cnt, int kind, float thr) {
+    const Layer& D = s.layers.back();
+    dycl::HeadArgs a{};
+    a.h = g->buf[in.b];
+    a.h32 = in.f >= 0 ? g->buf32[in.f] : nullptr;
+    a.w = D.d_w;
+    a.b = D.d_b;
+    a.z = g->d_z;
+    a.flag = g->d_flag;
+    a.pred = g->d_pred;
+    a.n_live = cnt;
+    a.HW = s.in.H * s.in.W;
+    a.C = s.in.Cp();
+    a.K = D.cout;
+    a.kind = kind;
+    a.thr = thr;
+    prof_begin(DYCL_K_HEAD, cnt, (a.h32 ? 4.0 : 2.0) * s.in.row_elems() + 4.0 * D.cout + 1,
+               2.0 * D.cout * s.in.C + s.in.row_elems(), 2.0 * D.cout * a.C);
+    cudaError_t e = dycl::launch_head(a, batch, st);
+    prof_end();
+    if (e != cudaSuccess) return cuda_fail(g, e, "launch_head");
+    return DYCL_OK;
+  }
+
+  dycl_status compact(const int* cnt, int mode, int32_t bit, int orig_cur, int* s_out) {
+    *s_out = slot;
+    if (slot + 2 > g->n_slots) return fail(g, DYCL_E_STATE, "count slots exhausted");
+    prof_begin(DYCL_K_COMPACT, cnt, 1.0 + 4 * 4, 0, 0);
+    cudaError_t e = dycl::launch_compact(g->d_flag, cnt, g->d_orig[orig_cur], g->d_list1, g->d_list0,
+                                         g->d_counts + slot, g->d_orig[orig_cur ^ 1], mode, out_path, bit, st);
+    prof_end();
+    slot += 2;
+    if (e != cudaSuccess) return cuda_fail(g, e, "launch_compact");
+    return DYCL_OK;
+  }
+
+  dycl_status scatter(const int* list, const int* count, int orig_cur, int32_t path_val) {
+    prof_begin(DYCL_K_SCATTER, count, 2.0 * 4 * g->K + 12, 0, 0);
+    cudaError_t e = dycl::launch_scatter(g->d_z, g->K, list, count, g->d_orig[orig_cur], out_logits, out_path,
+                                         path_val, batch, st);
+    prof_end();
+    if (e != cudaSuccess) return cuda_fail(g, e, "launch_scatter");
+    return DYCL_OK;
+  }
+
+  // Copy rows list[j] of `src` into rows (*off + j) of `dst` (identity or option A),
+  // for each precision copy the source tensor carries.
+  dycl_status gather(Tensor src, Tensor dst, const int* list, const int* count, const int* off, const Shape& sh,
+                     int mode) {
+    for (int pass = 0; pass < 2; ++pass) {
+      const int si = pass == 0 ? src.b : src.f, di = pass == 0 ? dst.b : dst.f;
+      if (si < 0) continue;
+      if (di < 0) return fail(g, DYCL_E_STATE, "internal: gather destination lacks a copy");
+      dycl::GatherArgs a{};
+      a.elem_bytes = pass == 0 ? 2 : 4;
+      a.src = pass == 0 ? (const void*)g->buf[si] : (const void*)g->buf32[si];
+      a.dst = pass == 0 ? (void*)g->buf[di] : (void*)g->buf32[di];
+      a.list = list;
+      a.count = count;
+      a.dst_off_count = off;
+      a.row_elems_src = sh.row_elems();
+      a.mode = mode;
+      a.H = sh.H; a.W = sh.W; a.C = sh.Cp();
+      a.row_elems_dst = mode == 0 ? sh.row_elems() : (long long)(sh.H / 2) * (sh.W / 2) * 2 * sh.Cp();
+      const double eb = a.elem_bytes;
+      prof_begin(DYCL_K_GATHER, count, eb * (mode == 0 ? a.row_elems_src : a.row_elems_dst / 2) + eb * a.row_elems_dst,
+                 0, 0);
+      cudaError_t e = dycl::launch_gather(a, batch, g->num_sms, st);
+      prof_end();
+      if (e != cudaSuccess) return cuda_fail(g, e, "launch_gather");
+    }
+    return DYCL_OK;
+  }
+
+  dycl_status run(const float* input) {
+    dycl_status r;
+    int orig_cur = 0;
+    prof_begin(DYCL_K_INIT, nullptr, 0, 0, 12.0 * batch);
+    cudaError_t e = dycl::launch_init(g->d_counts, batch, g->d_orig[0], out_path, batch, st);
+    prof_end();
+    if (e != cudaSuccess) return cuda_fail(g, e, "launch_init");
+    const Shape& in = g->input;
+    prof_begin(DYCL_K_INPUT, nullptr, 0, 0, (double)batch * in.H * in.W * (4.0 * in.C + 2.0 * in.Cp()));
+    e = dycl::launch_cast_pad(input, g->buf[0], batch, in.H * in.W, in.C, in.Cp(), st);
+    prof_end();
+    if (e != cudaSuccess) return cuda_fail(g, e, "launch_cast_pad");
+    Tensor cur;
+    cur.b = 0;
+    const int* cnt = g->d_counts;
+    const Tensor none;
+    for (const Node& N : g->nodes) {
+      switch (N.kind) {
+        case N_SEQ: {
+          Tensor o;
+          if ((r = subnet(g->subnets[N.sn], cur, cnt, none, none, &o))) return r;
+          cur = o;
+          break;
+        }
+        case N_EXIT: {
+          if ((r = head(g->subnets[N.sn], cur, cnt, 0, N.thr))) return r;
+          int s;
+          if ((r = compact(cnt, 0, 0, orig_cur, &s))) return r;
+          if ((r = scatter(g->d_list1, g->d_counts + s, orig_cur, N.ordinal))) return r;
+          const Tensor nb = pick_tensor(cur.f >= 0, {cur});
+          if ((r = gather(cur, nb, g->d_list0, g->d_counts + s + 1, nullptr, N.in, 0))) return r;
+          cur = nb;
+          cnt = g->d_counts + s + 1;
+          orig_cur ^= 1;
+          break;
+        }
+        case N_GATE: {
+          if ((r = head(g->subnets[N.sn], cur, cnt, 1, N.thr))) return r;
+          int s;
+          if ((r = compact(cnt, 1, (int32_t)1 << N.ordinal, orig_cur, &s))) return r;
+          Tensor bt = pick_tensor(false, {cur});
+          bt.f = -1;
+          Tensor in_t = cur;
+          in_t.f = -1;   // the then-branch reads only the bf16 operand copy ...
+          if ((r = gather(in_t, bt, g->d_list1, g->d_counts + s, nullptr, N.in, 0))) return r;
+          // ... except its shortcut: give the branch the fp32 rows too when streaming
+          if (cur.f >= 0) {
+            const Tensor bt32 = pick_tensor(true, {cur, bt});
+            bt.f = bt32.f;
+            Tensor src = cur;
+            src.b = -1;
+            Tensor dst = bt;
+            dst.b = -1;
+            if ((r = gather(src, dst, g->d_list1, g->d_counts + s, nullptr, N.in, 0))) return r;
+          }
+          const bool stream = fp32_stream();
+          const Tensor merged = pick_tensor(stream, {cur, bt});
+          Tensor o;
+          if ((r = subnet(g->subnets[N.then_sn], bt, g->d_counts + s, merged, cur, &o))) return r;
+          if ((r = gather(cur, merged, g->d_list0, g->d_counts + s + 1, g->d_counts + s, N.in, N.skip_mode))) return r;
+          cur = merged;
+          if (!stream) cur.f = -1;
+          orig_cur ^= 1;
+          break;
+        }
+        case N_FINAL: {
+          if ((r = head(g->subnets[N.sn], cur, cnt, 2, 0.f))) return r;
+          int s;
+          if ((r = compact(cnt, 0, 0, orig_cur, &s))) return r;
+          const int32_t pv = g->n_exits > 0 ? g->n_exits : -1;
+          if ((r = scatter(g->d_list1, g->d_counts + s, orig_cur, pv))) return r;
+          break;
+        }
+      }
+    }
+    return DYCL_OK;
+  }
+};
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+dycl_status dycl_graph_create(int cuda_device, int in_h, int in_w, int in_c, dycl_graph* out) {
+  if (!out || in_h <= 0 || in_w <= 0 || in_c <= 0) return fail(nullptr, DYCL_E_INVALID_ARG, "bad argument");
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(nullptr, DYCL_E_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  if (cuda_device < 0 || cuda_device >= ndev) return fail(nullptr, DYCL_E_INVALID_ARG, "bad device index");
+  dycl_graph g = new (std::nothrow) dycl_graph_s();
+  if (!g) return fail(nullptr, DYCL_E_OOM, "host allocation failed");
+  g->device = cuda_device;
+  g->input = Shape{in_h, in_w, in_c};
+  cudaSetDevice(cuda_device);
+  cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
+  int major = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, cuda_device);
+  if (major != 10) {
+    delete g;
+    return fail(nullptr, DYCL_E_UNSUPPORTED, "libdycl is built for sm_100a (B200) only");
+  }
+  *out = g;
+  return DYCL_OK;
+}
+
+dycl_status dycl_graph_destroy(dycl_graph g) {
+  if (!g) return DYCL_OK;
+  cudaSetDevice(g->device);
+  for (Subnet& s : g->subnets)
+    for (Layer& L : s.layers) {
+      cudaFree(L.d_w);
+      cudaFree(L.d_b);
+    }
+  for (auto* b : g->buf) cudaFree(b);
+  for (auto* b : g->buf32) cudaFree(b);
+  cudaFree(g->d_counts);
+  cudaFree(g->d_orig[0]);
+  cudaFree(g->d_orig[1]);
+  cudaFree(g->d_list1);
+  cudaFree(g->d_list0);
+  cudaFree(g->d_flag);
+  cudaFree(g->d_pred);
+  cudaFree(g->d_z);
+  cudaFree(g->d_in_stage);
+  cudaFree(g->d_logit_stage);
+  cudaFree(g->d_path_stage);
+  for (auto& L : g->prof) {
+    cudaEventDestroy(L.e0);
+    cudaEventDestroy(L.e1);
+  }
+  delete g;
+  return DYCL_OK;
+}
+
+const char* dycl_last_error(dycl_graph g) { return g ? g->err.c_str() : g_create_err.c_str(); }
+
+dycl_status dycl_graph_set_precision(dycl_graph g, int precision) {
+  if (!g) return DYCL_E_INVALID_ARG;
+  if (g->finalized) return fail(g, DYCL_E_STATE, "graph already finalized");
+  if (precision != DYCL_PREC_BF16 && precision != DYCL_PREC_FP32_STREAM)
+    return fail(g, DYCL_E_INVALID_ARG, "unknown precision mode");
+  g->precision = precision;
+  return DYCL_OK;
+}
+
+dycl_status dycl_subnet_begin(dycl_graph g, dycl_node* out) {
+  if (!g || !out) return DYCL_E_INVALID_ARG;
+  if (g->finalized) return fail(g, DYCL_E_STATE, "graph already finalized");
+  g->subnets.emplace_back();
+  *out = (dycl_node)g->subnets.size() - 1;
+  return DYCL_OK;
+}
+
+dycl_status dycl_subnet_block_begin(dycl_graph g, dycl_node sn) {
+  if (dycl_status s = check_sn(g, sn)) return s;
+  Layer L;
+  L.kind = L_BLOCK;
+  g->subnets[sn].layers.push_back(std::move(L));
+  return DYCL_OK;
+}
+
+dycl_status dycl_subnet_conv2d(dycl_graph g, dycl_node sn, int c_in, int c_out, int k, int stride, int pad,
+                               const uint16_t* w_bf16, const float* bias, dycl_act act, int residual) {
+  if (dycl_status s = check_sn(g, sn)) return s;
+  if (!w_bf16 || !bias || c_in <= 0 || c_out <= 0 || k < 1 || k > 7 || (stride != 1 && stride != 2) || pad < 0 ||
+      pad >= k || (act != DYCL_ACT_NONE && act != DYCL_ACT_RELU))
+    return fail(g, DYCL_E_INVALID_ARG, "conv2d: bad argument");
+  if (c_out % 16) return fail(g, DYCL_E_UNSUPPORTED, "conv2d: c_out must be a multiple of 16");
+  Layer L;
+  L.kind = L_CONV;
+  L.cout = c_out; L.k = k; L.stride = stride; L.pad = pad;
+  L.relu = act == DYCL_ACT_RELU;
+  L.residual = residual ? 1 : 0;
+  L.w.assign(w_bf16, w_bf16 + (size_t)c_out * k * k * c_in);
+  L.b.assign(bias, bias + c_out);
+  g->subnets[sn].layers.push_back(std::move(L));
+  return DYCL_OK;
+}
+
+dycl_status dycl_subnet_dense(dycl_graph g, dycl_node sn, int n_in, int n_out, const uint16_t* w_bf16,
+                              const float* bias, dycl_act act, int out_fp32) {
+  if (dycl_status s = check_sn(g, sn)) return s;
+  if (!w_bf16 || !bias || n_in <= 0 || n_out <= 0 || (act != DYCL_ACT_NONE && act != DYCL_ACT_RELU))
+    return fail(g, DYCL_E_INVALID_ARG, "dense: bad argument");
+  if (!out_fp32 && n_out % 16) return fail(g, DYCL_E_UNSUPPORTED, "dense: bf16 n_out must be a multiple of 16");
+  if (out_fp32 && act != DYCL_ACT_NONE) return fail(g, DYCL_E_UNSUPPORTED, "dense: fp32 heads take no activation");
+  Layer L;
+  L.kind = L_DENSE;
+  L.cout = n_out;
+  L.relu = act == DYCL_ACT_RELU;
+  L.out_fp32 = out_fp32 ? 1 : 0;
+  L.w.assign(w_bf16, w_bf16 + (size_t)n_out * n_in);
+  L.b.assign(bias, bias + n_out);
+  g->subnets[sn].layers.push_back(std::move(L));
+  return DYCL_OK;
+}
+
+dycl_status dycl_subnet_gap(dycl_graph g, dycl_node sn) {
+  if (dycl_status s = check_sn(g, sn)) return s;
+  Layer L;
+  L.kind = L_GAP;
+  g->subnets[sn].layers.push_back(std::move(L));
+  return DYCL_OK;
+}
+
+dycl_status dycl_subnet_end(dycl_graph g, dycl_node sn) {
+  if (dycl_status s = check_sn(g, sn)) return s;
+  if (g->subnets[sn].layers.empty()) return fail(g, DYCL_E_INVALID_ARG, "empty subnet");
+  g->subnets[sn].ended = true;
+  return DYCL_OK;
+}
+
+static dycl_status add_node(dycl_graph g, Node N, bool needs_head_sn) {
+  if (!g) return DYCL_E_INVALID_ARG;
+  if (g->finalized) return fail(g, DYCL_E_STATE, "graph already finalized");
+  const int ns = (int)g->subnets.size();
+  if (N.sn < 0 || N.sn >= ns || (N.kind == N_GATE && (N.then_sn < 0 || N.then_sn >= ns)))
+    return fail(g, DYCL_E_INVALID_ARG, "bad subnet id");
+  if (!g->subnets[N.sn].ended || (N.kind == N_GATE && !g->subnets[N.then_sn].ended))
+    return fail(g, DYCL_E_STATE, "subnet not ended");
+  if (!g->nodes.empty() && g->nodes.back().kind == N_FINAL)
+    return fail(g, DYCL_E_STATE, "no node may follow dycl_final");
+  (void)needs_head_sn;
+  g->nodes.push_back(N);
+  return DYCL_OK;
+}
+
+dycl_status dycl_seq(dycl_graph g, dycl_node subnet) {
+  Node N{};
+  N.kind = N_SEQ;
+  N.sn = subnet;
+  return add_node(g, N, false);
+}
+
+dycl_status dycl_exit(dycl_graph g, dycl_node head_subnet, float tau) {
+  Node N{};
+  N.kind = N_EXIT;
+  N.sn = head_subnet;
+  N.thr = tau;
+  dycl_status s = add_node(g, N, true);
+  if (s == DYCL_OK) g->nodes.back().ordinal = g->n_exits++;
+  return s;
+}
+
+dycl_status dycl_gate(dycl_graph g, dycl_node gate_subnet, float thr, dycl_node then_subnet) {
+  Node N{};
+  N.kind = N_GATE;
+  N.sn = gate_subnet;
+  N.then_sn = then_subnet;
+  N.thr = thr;
+  if (g && g->n_gates >= 31) return fail(g, DYCL_E_UNSUPPORTED, "at most 31 gates (path word bits)");
+  dycl_status s = add_node(g, N, true);
+  if (s == DYCL_OK) g->nodes.back().ordinal = g->n_gates++;
+  return s;
+}
+
+dycl_status dycl_final(dycl_graph g, dycl_node head_subnet) {
+  Node N{};
+  N.kind = N_FINAL;
+  N.sn = head_subnet;
+  return add_node(g, N, true);
+}
+
+dycl_status dycl_finalize(dycl_graph g, int64_t max_batch) {
+  if (!g) return DYCL_E_INVALID_ARG;
+  if (g->finalized) return fail(g, DYCL_E_STATE, "graph already finalized");
+  if (max_batch <= 0 || max_batch > (1 << 26)) return fail(g, DYCL_E_INVALID_ARG, "bad max_batch");
+  if (g->nodes.empty() || g->nodes.back().kind != N_FINAL)
+    return fail(g, DYCL_E_STATE, "the chain must end with dycl_final");
+  CK(cudaSetDevice(g->device));
+  // ---- Alg. 2: propagate the per-sample shape along the chain from N0
+  Shape cur = g->input;
+  long long maxrow = cur.row_elems();
+  std::vector<int> planned(g->subnets.size(), 0);
+  std::vector<Shape> planned_in(g->subnets.size());
+  auto plan = [&](int sn, const Shape& in) -> dycl_status {
+    if (planned[sn]) {
+      if (!(planned_in[sn] == in)) return fail(g, DYCL_E_SHAPE_MISMATCH, "subnet reused with a different input shape");
+      return DYCL_OK;
+    }
+    dycl_status s = plan_subnet(g, g->subnets[sn], in, sn);
+    if (s) return s;
+    // registration-time c_in / n_in must agree with propagated shapes
+    for (const Layer& L : g->subnets[sn].layers) {
+      if (L.kind == L_CONV && (long long)L.w.size() != (long long)L.cout * L.k * L.k * L.in.C)
+        return fail(g, DYCL_E_SHAPE_MISMATCH, "conv2d c_in disagrees with the propagated shape");
+      if (L.kind == L_DENSE && (long long)L.w.size() != (long long)L.cout * L.in.C)
+        return fail(g, DYCL_E_SHAPE_MISMATCH, "dense n_in disagrees with the propagated shape");
+      maxrow = std::max(maxrow, L.out.row_elems());
+    }
+    planned[sn] = 1;
+    planned_in[sn] = in;
+    return DYCL_OK;
+  };
+  g->K = 0;
+  for (Node& N : g->nodes) {
+    N.in = cur;
+    dycl_status s = plan(N.sn, cur);
+    if (s) return s;
+    const Subnet& S = g->subnets[N.sn];
+    if (N.kind == N_SEQ) {
+      if (S.is_head) return fail(g, DYCL_E_UNSUPPORTED, "dycl_seq on a head subnet");
+      cur = S.out;
+    } else {
+      if (!S.is_head) return fail(g, DYCL_E_SHAPE_MISMATCH, "exit/gate/final need a [gap] + dense(out_fp32) head");
+      if (S.in.Cp() % 8 || S.in.Cp() / 8 > 256) return fail(g, DYCL_E_UNSUPPORTED, "head input channels");
+      if (N.kind == N_GATE) {
+        if (S.head_K != 1) return fail(g, DYCL_E_SIGNATURE, "gate head must produce one logit");
+        if ((s = plan(N.then_sn, cur))) return s;
+        const Subnet& T = g->subnets[N.then_sn];
+        if (T.is_head) return fail(g, DYCL_E_UNSUPPORTED, "gate then-branch is a head");
+        if (T.out == cur) N.skip_mode = 0;
+        else if (T.out.H * 2 == cur.H && T.out.W * 2 == cur.W && T.out.C == 2 * cur.C && cur.C % 16 == 0)
+          N.skip_mode = 1;
+        else return fail(g, DYCL_E_SHAPE_JOIN, "gate: then-branch output shape joins neither identity nor option A");
+        cur = T.out;
+      } else {
+        if (g->K == 0) g->K = S.head_K;
+        else if (g->K != S.head_K) return fail(g, DYCL_E_SIGNATURE, "exit/final heads disagree on K");
+      }
+    }
+    N.out = cur;
+    maxrow = std::max(maxrow, cur.row_elems());
+  }
+  // ---- weights -> HBM (snapshot), workspace for max_batch
+  for (size_t i = 0; i < g->subnets.size(); ++i)
+    if (planned[i])
+      if (dycl_status s = upload_subnet(g, g->subnets[i])) return s;
+  g->max_batch = max_batch;
+  g->max_row_elems = maxrow;
+  const size_t nb = (size_t)max_batch;
+  for (auto& b : g->buf)
+    if (dycl_status s = dmalloc(g, &b, nb * (size_t)maxrow * 2)) return s;
+  if (g->precision == DYCL_PREC_FP32_STREAM)
+    for (auto& b : g->buf32)
+      if (dycl_status s = dmalloc(g, &b, nb * (size_t)maxrow * 4)) return s;
+  g->n_slots = 1 + 2 * (int)g->nodes.size();
+  if (dycl_status s = dmalloc(g, &g->d_counts, g->n_slots * sizeof(int))) return s;
+  CK(cudaMemset(g->d_counts, 0, g->n_slots * sizeof(int)));
+  for (auto& o : g->d_orig)
+    if (dycl_status s = dmalloc(g, &o, nb * 4)) return s;
+  if (dycl_status s = dmalloc(g, &g->d_list1, nb * 4)) return s;
+  if (dycl_status s = dmalloc(g, &g->d_list0, nb * 4)) return s;
+  if (dycl_status s = dmalloc(g, &g->d_flag, nb)) return s;
+  if (dycl_status s = dmalloc(g, &g->d_pred, nb * 4)) return s;
+  if (dycl_status s = dmalloc(g, &g->d_z, nb * (size_t)std::max(g->K, 1) * 4)) return s;
+  g->finalized = true;
+  return DYCL_OK;
+}
+
+static dycl_status run_impl(dycl_graph g, const float* input, int64_t batch, float* logits, int32_t* path,
+                            int32_t* node_counts, cudaStream_t st) {
+  if (!g->finalized) return fail(g, DYCL_E_STATE, "graph not finalized");
+  if (batch < 0 || batch > g->max_batch) return fail(g, DYCL_E_SHAPE_MISMATCH, "batch > max_batch");
+  if (batch > 0 && (!input || !logits || !path)) return fail(g, DYCL_E_INVALID_ARG, "null io pointer");
+  CK(cudaSetDevice(g->device));
+  CK(cudaGetLastError());                      // surface async faults of earlier work
+  g->prof_used = 0;
+  g->prof_stream = st;
+  if (batch == 0) {
+    CK(cudaMemsetAsync(g->d_counts, 0, g->n_slots * sizeof(int), st));
+  } else {
+    Exec ex{g, st, (int)batch, logits, path};
+    if (dycl_status s = ex.run(input)) return s;
+    g->launches_per_run = ex.nlaunch;
+  }
+  if (node_counts) CK(cudaMemcpyAsync(node_counts, g->d_counts, g->n_slots * sizeof(int), cudaMemcpyDeviceToDevice, st));
+  return DYCL_OK;
+}
+
+dycl_status dycl_run(dycl_graph g, const dycl_io* io, void* stream) {
+  if (!g || !io) return DYCL_E_INVALID_ARG;
+  return run_impl(g, io->input, io->batch, io->logits, io->path, io->node_counts, (cudaStream_t)stream);
+}
+
+dycl_status dycl_run_host(dycl_graph g, const float* input_host, int64_t batch, float* logits_host,
+                          int32_t* path_host, void* stream) {
+  if (!g) return DYCL_E_INVALID_ARG;
+  if (!g->finalized) return fail(g, DYCL_E_STATE, "graph not finalized");
+  if (batch < 0 || batch > g->max_batch) return fail(g, DYCL_E_SHAPE_MISMATCH, "batch > max_batch");
+  if (batch > 0 && (!input_host || !logits_host || !path_host)) return fail(g, DYCL_E_INVALID_ARG, "null pointer");
+  CK(cudaSetDevice(g->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t in_elems = (size_t)g->max_batch * g->input.H * g->input.W * g->input.C;
+  if (!g->d_in_stage) {
+    if (dycl_status s = dmalloc(g, &g->d_in_stage, in_elems * 4)) return s;
+    if (dycl_status s = dmalloc(g, &g->d_logit_stage, (size_t)g->max_batch * g->K * 4)) return s;
+    if (dycl_status s = dmalloc(g, &g->d_path_stage, (size_t)g->max_batch * 4)) return s;
+  }
+  const size_t nin = (size_t)batch * g->input.H * g->input.W * g->input.C;
+  CK(cudaMemcpyAsync(g->d_in_stage, input_host, nin * 4, cudaMemcpyHostToDevice, st));
+  if (dycl_status s = run_impl(g, g->d_in_stage, batch, g->d_logit_stage, g->d_path_stage, nullptr, st)) return s;
+  CK(cudaMemcpyAsync(logits_host, g->d_logit_stage, (size_t)batch * g->K * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(path_host, g->d_path_stage, (size_t)batch * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return DYCL_OK;
+}
+
+dycl_status dycl_num_count_slots(dycl_graph g, int32_t* out) {
+  if (!g || !out) return DYCL_E_INVALID_ARG;
+  if (!g->finalized) return fail(g, DYCL_E_STATE, "graph not finalized");
+  *out = g->n_slots;
+  return DYCL_OK;
+}
+
+dycl_status dycl_launches_per_run(dycl_graph g, int32_t* out) {
+  if (!g || !out) return DYCL_E_INVALID_ARG;
+  *out = g->launches_per_run;
+  return DYCL_OK;
+}
+
+dycl_status dycl_num_classes(dycl_graph g, int32_t* out) {
+  if (!g || !out) return DYCL_E_INVALID_ARG;
+  if (!g->finalized) return fail(g, DYCL_E_STATE, "graph not finalized");
+  *out = g->K;
+  return DYCL_OK;
+}
+
+dycl_status dycl_set_profiling(dycl_graph g, int enable) {
+  if (!g) return DYCL_E_INVALID_ARG;
+  g->profiling = enable != 0;
+  return DYCL_OK;
+}
+
+dycl_status dycl_profile_read(dycl_graph g, int32_t max_n, int32_t* kind, float* ms, double* bytes,
+                              double* flops, int32_t* n_out) {
+  if (!g || !n_out) return DYCL_E_INVALID_ARG;
+  CK(cudaSetDevice(g->device));
+  CK(cudaStreamSynchronize(g->prof_stream));
+  std::vector<int> counts(g->n_slots, 0);
+  if (g->d_counts) CK(cudaMemcpy(counts.data(), g->d_counts, g->n_slots * sizeof(int), cudaMemcpyDeviceToHost));
+  const int n = (int)std::min<size_t>(g->prof_used, (size_t)std::max(max_n, 0));
+  for (int i = 0; i < n; ++i) {
+    const Launch& L = g->prof[i];
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, L.e0, L.e1));
+    const double rows = L.count_dev ? (double)counts[L.count_dev - g->d_counts] : 0.0;
+    if (kind) kind[i] = L.kind;
+    if (ms) ms[i] = t;
+    if (bytes) bytes[i] = rows * L.bytes_per_row + L.bytes_fixed;
+    if (flops) flops[i] = rows * L.flops_per_row;
+  }
+  *n_out = (int32_t)g->prof_used;
+  return DYCL_OK;
+}
+
+dycl_status dycl_debug_conv2d(dycl_graph g, int64_t n, int H, int W, int C, const uint16_t* w, const float* bias,
+                              int c_out, int k, int stride, int pad, int relu, const void* res, int res_mode,
+                              const void* x, void* y) {
+  if (!g || !w || !bias || !x || !y || n < 0 || C % 8 || c_out % 16 || k < 1 || stride < 1 || res_mode < 0 ||
+      res_mode > 2 || (res_mode && !res))
+    return fail(g, DYCL_E_INVALID_ARG, "debug_conv2d: bad argument");
+  CK(cudaSetDevice(g->device));
+  const int Ho = (H + 2 * pad - k) / stride + 1, Wo = (W + 2 * pad - k) / stride + 1;
+  const int K = k * k * C, Kp = (K + 63) / 64 * 64;
+  std::vector<uint16_t> wp((size_t)c_out * Kp, 0);
+  for (int o = 0; o < c_out; ++o)
+    for (int j = 0; j < K; ++j) wp[(size_t)o * Kp + j] = w[(size_t)o * K + j];
+  uint16_t* dw = nullptr;
+  float* db = nullptr;
+  if (dycl_status s = dmalloc(g, &dw, wp.size() * 2)) return s;
+  if (dycl_status s = dmalloc(g, &db, (size_t)c_out * 4)) { cudaFree(dw); return s; }
+  cudaMemcpy(dw, wp.data(), wp.size() * 2, cudaMemcpyHostToDevice);
+  cudaMemcpy(db, bias, (size_t)c_out * 4, cudaMemcpyHostToDevice);
+  dycl::ConvArgs a{};
+  a.x = (const uint16_t*)x; a.w = dw; a.bias = db; a.res = (const uint16_t*)res; a.y = (uint16_t*)y;
+  a.n_live = nullptr; a.n_static = (int)n;
+  a.H = H; a.W = W; a.C = C; a.Ho = Ho; a.Wo = Wo; a.Cout = c_out; a.ksz = k; a.stride = stride; a.pad = pad;
+  a.K = K; a.Kp = Kp; a.relu = relu; a.res_mode = res_mode;
+  a.rH = 2 * Ho; a.rW = 2 * Wo; a.rC = c_out / 2; a.r_pad_lo = c_out / 4;
+  if (res_mode == 1) { a.rH = Ho; a.rW = Wo; a.rC = c_out; a.r_pad_lo = 0; }
+  cudaError_t e = n > 0 ? dycl::launch_conv_tc(a, (int)n, g->num_sms, 0) : cudaSuccess;
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  cudaFree(dw);
+  cudaFree(db);
+  if (e != cudaSuccess) return cuda_fail(g, e, "debug_conv2d");
+  return DYCL_OK;
+}
+
+}  // extern "C"

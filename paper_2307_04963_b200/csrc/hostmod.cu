@@ -1,0 +1,328 @@
+// Device-side host module: pre-processing cast, heads + per-sample predicates,
+// stable compaction, scatter to original order, row gathers.
+//
+// The paper's host program evaluates each `If` node on the host after copying the
+// predicate tensor back (Listing 2 set_input/run/get_output, PAPER.md L216-218;
+// the transfer overhead is Challenge 2, L499-501).  Here every logic node runs
+// on the device and writes its decisions as index lists + device-resident counts
+// that the next kernels read, so a whole batched run needs no host round trip.
+// All reductions use fixed-order trees (no atomics), so results are independent
+// of batch size and of the position of a sample in the batch.
+#include <cuda_bf16.h>
+
+#include "kernels.h"
+
+namespace dycl {
+namespace {
+
+__device__ __forceinline__ float bf16f(uint16_t u) { return __uint_as_float((uint32_t)u << 16); }
+
+// ------------------------------------------------------------------ a0 cast
+__global__ void k_cast_pad(const float* __restrict__ in, uint16_t* __restrict__ out, int64_t npix, int c,
+                           int cp) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npix; p += (int64_t)gridDim.x * blockDim.x) {
+    const float* src = in + p * c;
+    uint16_t* dst = out + p * cp;
+    for (int j0 = 0; j0 < cp; j0 += 8) {
+      uint32_t w[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c0 = j0 + 2 * j, c1 = c0 + 1;
+        const float f0 = c0 < c ? src[c0] : 0.0f;
+        const float f1 = c1 < c ? src[c1] : 0.0f;
+        __nv_bfloat162 v = __floats2bfloat162_rn(f0, f1);
+        w[j] = *reinterpret_cast<uint32_t*>(&v);
+      }
+      *reinterpret_cast<uint4*>(dst + j0) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
+__global__ void k_init(int* counts, int n, int* orig, int32_t* path, int nmax) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) counts[0] = n;
+  if (i < n) {
+    orig[i] = i;
+    if (path) path[i] = 0;
+  }
+}
+
+// ------------------------------------------------------- a2 + a3 head/predicate
+constexpr int HEAD_THREADS = 256;
+
+__global__ void __launch_bounds__(HEAD_THREADS) k_head(const HeadArgs a) {
+  extern __shared__ float sh[];
+  float* part = sh;                                // [HEAD_THREADS][8]
+  float* g = part + HEAD_THREADS * 8;              // [C]
+  float* z = g + a.C;                              // [K]
+  __shared__ float red[HEAD_THREADS / 32];
+  const int n_live = *a.n_live;
+  const int t = threadIdx.x;
+  const int G = a.C / 8;                           // 16-byte channel groups per pixel
+  const int P = HEAD_THREADS / G;                  // pixel stride
+  for (int row = blockIdx.x; row < n_live; row += gridDim.x) {
+    const uint16_t* h = a.h + (size_t)row * a.HW * a.C;
+    // GAP: thread (p0, grp) sums its 8 channels over pixels p0, p0+P, ...
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (t < G * P) {
+      const int grp = t % G;
+      if (a.h32) {
+        const float* h32 = a.h32 + (size_t)row * a.HW * a.C;
+        for (int p = t / G; p < a.HW; p += P) {
+          const float4* q = reinterpret_cast<const float4*>(h32 + (size_t)p * a.C + grp * 8);
+          const float4 v0 = __ldg(q), v1 = __ldg(q + 1);
+          acc[0] += v0.x; acc[1] += v0.y; acc[2] += v0.z; acc[3] += v0.w;
+          acc[4] += v1.x; acc[5] += v1.y; acc[6] += v1.z; acc[7] += v1.w;
+        }
+      } else {
+        for (int p = t / G; p < a.HW; p += P) {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(h + (size_t)p * a.C + grp * 8));
+          const uint32_t u[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            acc[2 * j] += __uint_as_float(u[j] << 16);
+            acc[2 * j + 1] += __uint_as_float(u[j] & 0xFFFF0000u);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) part[t * 8 + j] = acc[j];
+    __syncthreads();
+    for (int c = t; c < a.C; c += HEAD_THREADS) {
+      const int grp = c >> 3, j = c & 7;
+      float s = 0.0f;
+      for (int q = 0; q < P; ++q) s += part[(q * G + grp) * 8 + j];
+      g[c] = s / (float)a.HW;
+    }
+    __syncthreads();
+    // FC: one warp per output row, lanes over channels, fixed shuffle tree.
+    const int warp = t >> 5, lane = t & 31;
+    for (int j = warp; j < a.K; j += HEAD_THREADS / 32) {
+      const uint16_t* wr = a.w + (size_t)j * a.C;
+      float s = 0.0f;
+      for (int c = lane; c < a.C; c += 32) s += bf16f(wr[c]) * g[c];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) z[j] = s + a.b[j];
+    }
+    __syncthreads();
+    for (int j = t; j < a.K; j += HEAD_THREADS) a.z[(size_t)row * a.K + j] = z[j];
+    // predicate
+    if (a.kind == 0) {
+      float m = -INFINITY;
+      for (int j = t; j < a.K; j += HEAD_THREADS) m = fmaxf(m, z[j]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0) red[warp] = m;
+      __syncthreads();
+      m = red[0];
+      for (int w = 1; w < HEAD_THREADS / 32; ++w) m = fmaxf(m, red[w]);
+      __syncthreads();
+      float s = 0.0f;
+      for (int j = t; j < a.K; j += HEAD_THREADS) s += expf(z[j] - m);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) red[warp] = s;
+      __syncthreads();
+      if (t == 0) {
+        float tot = 0.0f;
+        for (int w = 0; w < HEAD_THREADS / 32; ++w) tot += red[w];
+        const float conf = 1.0f / tot;           // max_j softmax(z)_j
+        a.flag[row] = conf >= a.thr ? 1 : 0;     // reading R1: conf >= tau exits
+        if (a.pred) a.pred[row] = conf;
+      }
+    } else if (t == 0) {
+      if (a.kind == 1) {
+        const float p = 1.0f / (1.0f + expf(-z[0]));
+        a.flag[row] = p > a.thr ? 1 : 0;         // reading R2: p > thr executes
+        if (a.pred) a.pred[row] = p;
+      } else {
+        a.flag[row] = 1;
+        if (a.pred) a.pred[row] = 1.0f;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------ a4 compaction
+constexpr int CMP_THREADS = 1024;
+
+__global__ void __launch_bounds__(CMP_THREADS) k_compact(const uint8_t* __restrict__ flag, const int* n_live,
+                                                         const int* __restrict__ orig, int* list1, int* list0,
+                                                         int* counts_out, int* orig_next, int mode, int32_t* path,
+                                                         int32_t path_bit) {
+  __shared__ int wsum[CMP_THREADS / 32];
+  __shared__ int total1_s;
+  const int n = *n_live;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int ipt = (n + CMP_THREADS - 1) / CMP_THREADS;
+  const int b = min(n, t * ipt), e = min(n, b + ipt);
+  int c1 = 0;
+  for (int i = b; i < e; ++i) c1 += flag[i] != 0;
+  // block-wide exclusive scan of c1 (warp shuffles, then warp totals)
+  int x = c1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int v = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    wsum[lane] = v;                              // inclusive warp-total prefix
+    if (lane == 31) total1_s = v;
+  }
+  __syncthreads();
+  const int excl = x - c1 + (warp > 0 ? wsum[warp - 1] : 0);
+  const int total1 = total1_s;
+  int o1 = excl;                                 // flag==1 rows before my chunk
+  int o0 = b - excl;                             // flag==0 rows before my chunk
+  for (int i = b; i < e; ++i) {
+    const int oi = orig[i];
+    if (flag[i]) {
+      list1[o1] = i;
+      if (mode == 1) {
+        orig_next[o1] = oi;
+        path[oi] |= path_bit;
+      }
+      ++o1;
+    } else {
+      list0[o0] = i;
+      orig_next[(mode == 1 ? total1 : 0) + o0] = oi;
+      ++o0;
+    }
+  }
+  if (t == 0) {
+    counts_out[0] = total1;
+    counts_out[1] = n - total1;
+  }
+}
+
+// ---------------------------------------------------------------- a6 scatter
+__global__ void k_scatter(const float* __restrict__ z, int K, const int* __restrict__ list, const int* count,
+                          const int* __restrict__ orig, float* out_logits, int32_t* out_path, int32_t path_val) {
+  const int cnt = *count;
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  for (int j = blockIdx.x * wpb + (threadIdx.x >> 5); j < cnt; j += gridDim.x * wpb) {
+    const int i = list[j];
+    const int o = orig[i];
+    for (int c = lane; c < K; c += 32) out_logits[(size_t)o * K + c] = z[(size_t)i * K + c];
+    if (lane == 0 && path_val >= 0) out_path[o] = path_val;
+  }
+}
+
+// ----------------------------------------------------------------- a5 gather
+__global__ void __launch_bounds__(256) k_gather(const GatherArgs a) {
+  const int cnt = *a.count;
+  const int off = a.dst_off_count ? *a.dst_off_count : 0;
+  const int epu = 16 / a.elem_bytes;             // elements per 16-byte unit
+  const int64_t U = a.row_elems_dst / epu;       // 16-byte units per destination row
+  const int64_t Us = a.row_elems_src / epu;
+  const int64_t total = (int64_t)cnt * U;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const uint4* src = reinterpret_cast<const uint4*>(a.src);
+  uint4* dst = reinterpret_cast<uint4*>(a.dst);
+  if (a.mode == 0) {
+    for (int64_t u0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u0 < total; u0 += 4 * stride) {
+      uint4 v[4];
+      int64_t di[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t u = u0 + k * stride;
+        di[k] = -1;
+        if (u < total) {
+          const int64_t j = u / U, q = u - j * U;
+          v[k] = __ldg(src + (int64_t)a.list[j] * Us + q);
+          di[k] = (off + j) * U + q;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (di[k] >= 0) dst[di[k]] = v[k];
+    }
+  } else {
+    // option A: dst [H/2][W/2][2C] from src [H][W][C]: pixel (2ho, 2wo), channel c - C/2
+    const int Wo = a.W / 2, Cd = 2 * a.C, qpp = Cd / epu, pad = a.C / 2;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total; u += stride) {
+      const int64_t j = u / U;
+      const int64_t r = u - j * U;
+      const int p = (int)(r / qpp), q = (int)(r - (int64_t)p * qpp);
+      const int ho = p / Wo, wo = p - ho * Wo;
+      const int cs = q * epu - pad;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (cs >= 0 && cs < a.C) {
+        const int64_t e = (int64_t)a.list[j] * a.row_elems_src + ((int64_t)(2 * ho) * a.W + 2 * wo) * a.C + cs;
+        v = __ldg(src + e / epu);
+      }
+      dst[(off + j) * U + r] = v;
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_cast_pad(const float* in, uint16_t* out, int64_t n, int hw, int c, int cp, cudaStream_t s) {
+  const int64_t npix = n * hw;
+  if (npix == 0) return cudaSuccess;
+  int64_t blocks = (npix + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_cast_pad<<<(int)blocks, 256, 0, s>>>(in, out, npix, c, cp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init(int* counts, int n, int* orig, int32_t* path, int nmax, cudaStream_t s) {
+  const int blocks = (n + 255) / 256 > 0 ? (n + 255) / 256 : 1;
+  k_init<<<blocks, 256, 0, s>>>(counts, n, orig, path, nmax);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_head(const HeadArgs& a, int max_rows, cudaStream_t s) {
+  if (a.C % 8 != 0 || a.C / 8 > HEAD_THREADS) return cudaErrorInvalidValue;
+  const size_t smem = (HEAD_THREADS * 8 + a.C + a.K) * sizeof(float);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_head, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  int grid = max_rows < 148 * 8 ? max_rows : 148 * 8;
+  if (grid < 1) grid = 1;
+  k_head<<<grid, HEAD_THREADS, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compact(const uint8_t* flag, const int* n_live, const int* orig, int* list1, int* list0,
+                           int* counts_out, int* orig_next, int mode, int32_t* path, int32_t path_bit,
+                           cudaStream_t s) {
+  k_compact<<<1, CMP_THREADS, 0, s>>>(flag, n_live, orig, list1, list0, counts_out, orig_next, mode, path, path_bit);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter(const float* z, int K, const int* list, const int* count, const int* orig,
+                           float* out_logits, int32_t* out_path, int32_t path_val, int max_rows, cudaStream_t s) {
+  int blocks = (max_rows + 7) / 8;
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  if (blocks < 1) blocks = 1;
+  k_scatter<<<blocks, 256, 0, s>>>(z, K, list, count, orig, out_logits, out_path, path_val);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const GatherArgs& a, int max_rows, int num_sms, cudaStream_t s) {
+  const int64_t units = (int64_t)max_rows * (a.row_elems_dst * a.elem_bytes / 16);
+  int64_t blocks = (units + 255) / 256;
+  if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
+  if (blocks < 1) blocks = 1;
+  k_gather<<<(int)blocks, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace dycl

@@ -1,0 +1,89 @@
+// Internal launcher interface between the runtime (api.cpp) and the sm_100a
+// kernels.  Not part of the public ABI (that is include/dycl.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dycl {
+
+// Implicit-GEMM convolution / dense layer on tcgen05 (conv_tc.cu).
+//   rows  m = (sample n, ho, wo)  -> M = n_live * Ho * Wo
+//   cols  o = output channel      -> N = Cout
+//   depth k = (r, s, c)           -> K = ksz*ksz*C  (C % 8 == 0)
+struct ConvArgs {
+  const uint16_t* x;     // bf16 [n][H][W][C]
+  const uint16_t* w;     // bf16 [Cout][Kp]  (K zero-padded to Kp = roundup(K, 64))
+  const float* bias;     // fp32 [Cout]
+  const uint16_t* res;   // bf16 shortcut source, or nullptr
+  const float* res32;    // fp32 shortcut source (fp32 residual stream), preferred when set
+  uint16_t* y;           // bf16 [n][Ho][Wo][Cout]  (tensor-core operand copy)
+  float* y32;            // fp32 [n][Ho][Wo][Cout]  (residual-stream copy) or nullptr
+  const int* n_live;     // device live-row count (samples); nullptr -> n_static
+  int n_static;
+  int H, W, C, Ho, Wo, Cout, ksz, stride, pad;
+  int K, Kp;
+  int relu;
+  int res_mode;          // 0 none, 1 identity [n][Ho][Wo][Cout], 2 option A from [n][rH][rW][rC]
+  int rH, rW, rC, r_pad_lo;
+};
+// Launch on `stream`; grid is sized for max_rows samples (persistent CTAs loop
+// over the tiles the live count needs).  Returns cudaSuccess or the launch error.
+cudaError_t launch_conv_tc(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream);
+
+// a0: fp32 [n][HW][C] -> bf16 [n][HW][Cp]  (Cp = roundup(C, 8), zero pad)
+cudaError_t launch_cast_pad(const float* in, uint16_t* out, int64_t n, int hw, int c, int cp,
+                            cudaStream_t s);
+
+// Run-start init: counts[0] = n ; orig[i] = i ; path[i] = 0.
+cudaError_t launch_init(int* counts, int n, int* orig, int32_t* path, int nmax, cudaStream_t s);
+
+// GAP + FC head + predicate, one CTA per live sample.
+//   kind 0 = exit (flag = max softmax >= thr), 1 = gate (flag = sigmoid(z0) > thr), 2 = final (flag = 1)
+struct HeadArgs {
+  const uint16_t* h;     // bf16 [n][HW][C]   (used when h32 == nullptr)
+  const float* h32;      // fp32 [n][HW][C]   residual stream
+  const uint16_t* w;     // bf16 [K][C]
+  const float* b;        // fp32 [K]
+  float* z;              // fp32 [n][K] logits scratch
+  uint8_t* flag;         // [n]
+  float* pred;           // [n] predicate value (conf or p) for diagnostics, may be null
+  const int* n_live;
+  int HW, C, K, kind;
+  float thr;
+};
+cudaError_t launch_head(const HeadArgs& a, int max_rows, cudaStream_t s);
+
+// Stable partition of the live rows by flag (single CTA, deterministic):
+//   rows with flag==1 -> list1 (in order), count -> counts_out[0]
+//   rows with flag==0 -> list0 (in order), count -> counts_out[1]
+//   orig_next = [orig[list0...]]  (mode 0: survivors continue; exit)
+//             = [orig[list1...], orig[list0...]]  (mode 1: gate; then-rows first)
+//   mode 1 also ORs path_bit into path[orig[i]] for flag==1 rows.
+cudaError_t launch_compact(const uint8_t* flag, const int* n_live, const int* orig,
+                           int* list1, int* list0, int* counts_out, int* orig_next,
+                           int mode, int32_t* path, int32_t path_bit, cudaStream_t s);
+
+// out_logits[orig[list[j]]] = z[list[j]], out_path[orig[list[j]]] = path_val (if path_val >= 0)
+// for j < *count.
+cudaError_t launch_scatter(const float* z, int K, const int* list, const int* count, const int* orig,
+                           float* out_logits, int32_t* out_path, int32_t path_val, int max_rows,
+                           cudaStream_t s);
+
+// dst row (dst_off + j) = transform(src row list[j]) for j < *count.
+//   mode 0: identity copy of row_bytes (multiple of 16)
+//   mode 1: option A: src [H][W][C] -> dst [H/2][W/2][2C] subsample + zero pad (C/2 each side)
+// dst_off_count: if non-null, rows are written from offset *dst_off_count.
+struct GatherArgs {
+  const void* src;
+  void* dst;
+  int elem_bytes;          // 2 (bf16) or 4 (fp32)
+  const int* list;
+  const int* count;
+  const int* dst_off_count;
+  int64_t row_elems_src;   // elements per src row
+  int64_t row_elems_dst;
+  int mode, H, W, C;
+};
+cudaError_t launch_gather(const GatherArgs& a, int max_rows, int num_sms, cudaStream_t s);
+
+}  // namespace dycl

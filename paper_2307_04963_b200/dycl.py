@@ -1,0 +1,243 @@
+"""Thin ctypes binding of libdycl.so (include/dycl.h): same names, argument marshalling only.
+
+Every step of the path runs in libdycl's kernels.  There is no CPU fallback:
+if the shared library is missing, or no sm_100 device is present, calls raise.
+Device buffers are passed as torch tensors (data_ptr) -- PyTorch is used only
+for device memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdycl.so")
+
+DYCL_ACT_NONE = 0
+DYCL_ACT_RELU = 1
+KIND_NAMES = {0: "input", 1: "conv", 2: "head", 3: "compact", 4: "gather", 5: "scatter", 6: "init"}
+
+_STATUS = {0: "DYCL_OK", -1: "DYCL_E_INVALID_ARG", -2: "DYCL_E_SHAPE_MISMATCH", -3: "DYCL_E_SIGNATURE",
+           -4: "DYCL_E_SHAPE_JOIN", -5: "DYCL_E_STATE", -6: "DYCL_E_UNSUPPORTED", -7: "DYCL_E_OOM",
+           -8: "DYCL_E_CUDA", -9: "DYCL_E_NCCL"}
+
+
+class DyclError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class dycl_io(ctypes.Structure):
+    _fields_ = [("input", ctypes.c_void_p), ("batch", ctypes.c_int64), ("logits", ctypes.c_void_p),
+                ("path", ctypes.c_void_p), ("node_counts", ctypes.c_void_p)]
+
+
+_lib = None
+EXPORTS = [
+    "dycl_graph_create", "dycl_graph_set_precision", "dycl_graph_destroy", "dycl_last_error", "dycl_subnet_begin", "dycl_subnet_block_begin",
+    "dycl_subnet_conv2d", "dycl_subnet_dense", "dycl_subnet_gap", "dycl_subnet_end", "dycl_seq", "dycl_exit",
+    "dycl_gate", "dycl_final", "dycl_finalize", "dycl_run", "dycl_run_host", "dycl_num_count_slots",
+    "dycl_launches_per_run", "dycl_num_classes", "dycl_set_profiling", "dycl_profile_read",
+    "dycl_debug_conv2d",
+]
+
+
+def lib():
+    """Load libdycl.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32, i64, f32 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_float
+        P16 = ctypes.POINTER(ctypes.c_uint16)
+        Pf = ctypes.POINTER(ctypes.c_float)
+        Pi = ctypes.POINTER(ctypes.c_int32)
+        Pd = ctypes.POINTER(ctypes.c_double)
+        sig = {
+            "dycl_graph_create": [i32, i32, i32, i32, ctypes.POINTER(vp)],
+            "dycl_graph_destroy": [vp],
+            "dycl_graph_set_precision": [vp, i32],
+            "dycl_subnet_begin": [vp, Pi],
+            "dycl_subnet_block_begin": [vp, i32],
+            "dycl_subnet_conv2d": [vp, i32, i32, i32, i32, i32, i32, P16, Pf, i32, i32],
+            "dycl_subnet_dense": [vp, i32, i32, i32, P16, Pf, i32, i32],
+            "dycl_subnet_gap": [vp, i32],
+            "dycl_subnet_end": [vp, i32],
+            "dycl_seq": [vp, i32],
+            "dycl_exit": [vp, i32, f32],
+            "dycl_gate": [vp, i32, f32, i32],
+            "dycl_final": [vp, i32],
+            "dycl_finalize": [vp, i64],
+            "dycl_run": [vp, ctypes.POINTER(dycl_io), vp],
+            "dycl_run_host": [vp, vp, i64, vp, vp, vp],
+            "dycl_num_count_slots": [vp, Pi],
+            "dycl_launches_per_run": [vp, Pi],
+            "dycl_num_classes": [vp, Pi],
+            "dycl_set_profiling": [vp, i32],
+            "dycl_profile_read": [vp, i32, Pi, Pf, Pd, Pd, Pi],
+            "dycl_debug_conv2d": [vp, i64, i32, i32, i32, P16, Pf, i32, i32, i32, i32, i32, vp, i32, vp, vp],
+        }
+        for name, args in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = ctypes.c_int
+        L.dycl_last_error.argtypes = [vp]
+        L.dycl_last_error.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def _ck(status, g=None):
+    if status != 0:
+        msg = lib().dycl_last_error(g).decode(errors="replace")
+        raise DyclError(status, msg)
+
+
+def _u16(a):
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.uint16))
+    return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint16))
+
+
+def _f32(a):
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float32))
+    return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(int(getattr(stream, "cuda_stream", stream)))
+
+
+# ---------------------------------------------------------------- C-ABI names
+def dycl_graph_create(cuda_device: int, in_h: int, in_w: int, in_c: int):
+    h = ctypes.c_void_p()
+    _ck(lib().dycl_graph_create(cuda_device, in_h, in_w, in_c, ctypes.byref(h)), None)
+    return h
+
+
+DYCL_PREC_BF16 = 0
+DYCL_PREC_FP32_STREAM = 1
+
+
+def dycl_graph_set_precision(g, precision):
+    _ck(lib().dycl_graph_set_precision(g, int(precision)), g)
+
+
+def dycl_graph_destroy(g):
+    _ck(lib().dycl_graph_destroy(g), None)
+
+
+def dycl_last_error(g=None) -> str:
+    return lib().dycl_last_error(g).decode(errors="replace")
+
+
+def dycl_subnet_begin(g) -> int:
+    n = ctypes.c_int32()
+    _ck(lib().dycl_subnet_begin(g, ctypes.byref(n)), g)
+    return n.value
+
+
+def dycl_subnet_block_begin(g, sn):
+    _ck(lib().dycl_subnet_block_begin(g, sn), g)
+
+
+def dycl_subnet_conv2d(g, sn, c_in, c_out, k, stride, pad, w_bf16, bias, act, residual):
+    w, wp = _u16(w_bf16)
+    b, bp = _f32(bias)
+    _ck(lib().dycl_subnet_conv2d(g, sn, c_in, c_out, k, stride, pad, wp, bp, act, int(residual)), g)
+
+
+def dycl_subnet_dense(g, sn, n_in, n_out, w_bf16, bias, act, out_fp32):
+    w, wp = _u16(w_bf16)
+    b, bp = _f32(bias)
+    _ck(lib().dycl_subnet_dense(g, sn, n_in, n_out, wp, bp, act, int(out_fp32)), g)
+
+
+def dycl_subnet_gap(g, sn):
+    _ck(lib().dycl_subnet_gap(g, sn), g)
+
+
+def dycl_subnet_end(g, sn):
+    _ck(lib().dycl_subnet_end(g, sn), g)
+
+
+def dycl_seq(g, sn):
+    _ck(lib().dycl_seq(g, sn), g)
+
+
+def dycl_exit(g, head_sn, tau):
+    _ck(lib().dycl_exit(g, head_sn, float(tau)), g)
+
+
+def dycl_gate(g, gate_sn, thr, then_sn):
+    _ck(lib().dycl_gate(g, gate_sn, float(thr), then_sn), g)
+
+
+def dycl_final(g, head_sn):
+    _ck(lib().dycl_final(g, head_sn), g)
+
+
+def dycl_finalize(g, max_batch):
+    _ck(lib().dycl_finalize(g, int(max_batch)), g)
+
+
+def dycl_run(g, input, batch, logits, path, node_counts=None, stream=None):
+    """input/logits/path/node_counts: CUDA torch tensors (fp32, fp32, int32, int32)."""
+    io = dycl_io(input.data_ptr(), int(batch), logits.data_ptr(), path.data_ptr(),
+                 node_counts.data_ptr() if node_counts is not None else None)
+    _ck(lib().dycl_run(g, ctypes.byref(io), _stream_ptr(stream)), g)
+
+
+def dycl_run_host(g, input_host, batch, logits_host, path_host, stream=None):
+    """Host buffers (torch CPU tensors, pinned or not, or numpy arrays)."""
+    def ptr(t):
+        return t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data
+    _ck(lib().dycl_run_host(g, ctypes.c_void_p(ptr(input_host)), int(batch), ctypes.c_void_p(ptr(logits_host)),
+                            ctypes.c_void_p(ptr(path_host)), _stream_ptr(stream)), g)
+
+
+def dycl_num_count_slots(g) -> int:
+    n = ctypes.c_int32()
+    _ck(lib().dycl_num_count_slots(g, ctypes.byref(n)), g)
+    return n.value
+
+
+def dycl_launches_per_run(g) -> int:
+    n = ctypes.c_int32()
+    _ck(lib().dycl_launches_per_run(g, ctypes.byref(n)), g)
+    return n.value
+
+
+def dycl_num_classes(g) -> int:
+    n = ctypes.c_int32()
+    _ck(lib().dycl_num_classes(g, ctypes.byref(n)), g)
+    return n.value
+
+
+def dycl_set_profiling(g, enable):
+    _ck(lib().dycl_set_profiling(g, int(bool(enable))), g)
+
+
+def dycl_profile_read(g, max_n=4096):
+    kind = (ctypes.c_int32 * max_n)()
+    ms = (ctypes.c_float * max_n)()
+    by = (ctypes.c_double * max_n)()
+    fl = (ctypes.c_double * max_n)()
+    n = ctypes.c_int32()
+    _ck(lib().dycl_profile_read(g, max_n, kind, ms, by, fl, ctypes.byref(n)), g)
+    m = min(n.value, max_n)
+    return [dict(kind=KIND_NAMES[kind[i]], ms=ms[i], bytes=by[i], flops=fl[i]) for i in range(m)]
+
+
+def dycl_debug_conv2d(g, x, n, H, W, C, w_bf16, bias, c_out, k, stride, pad, relu, res, res_mode, y, stream=None):
+    w, wp = _u16(w_bf16)
+    b, bp = _f32(bias)
+    _ck(lib().dycl_debug_conv2d(g, int(n), H, W, C, wp, bp, c_out, k, stride, pad, int(relu),
+                                ctypes.c_void_p(res.data_ptr() if res is not None else 0), int(res_mode),
+                                ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr())), g)

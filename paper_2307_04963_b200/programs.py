@@ -1,0 +1,137 @@
+"""The three DyNNs in their REWRITTEN form, registered through the C ABI.
+
+This is what DyCL's front end would hand to the runtime: the original program
+after loop unrolling + constant propagation (Sec. 5.2, Listing 3 ->
+Listing 4) and HCFG partitioning (Sec. 5.3, Alg. 1): a chain
+of conditional-free sub-networks (tensor nodes) and logic nodes.  Weights come
+from the seeded generator (``workloads``); nothing here computes.
+
+Only this registration, the binding and libdycl.so are on the product path.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import dycl as D
+
+RELU, NONE = D.DYCL_ACT_RELU, D.DYCL_ACT_NONE
+
+
+class Model:
+    """A finalized graph + its I/O geometry.  ``run`` enqueues one batched inference."""
+
+    def __init__(self, g, in_shape, K, max_batch, name):
+        self.g, self.in_shape, self.K, self.max_batch, self.name = g, in_shape, K, max_batch, name
+
+    def run(self, x, logits, path, node_counts=None, stream=None, batch=None):
+        D.dycl_run(self.g, x, x.shape[0] if batch is None else batch, logits, path, node_counts, stream)
+
+    def run_host(self, x_host, logits_host, path_host, stream=None):
+        D.dycl_run_host(self.g, x_host, x_host.shape[0], logits_host, path_host, stream)
+
+    def close(self):
+        if self.g is not None:
+            D.dycl_graph_destroy(self.g)
+            self.g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _head(g, W, name, c_in, gap=True):
+    sn = D.dycl_subnet_begin(g)
+    if gap:
+        D.dycl_subnet_gap(g, sn)
+    w = np.asarray(W[f"{name}.w"])
+    D.dycl_subnet_dense(g, sn, c_in, w.shape[0], w, W[f"{name}.b"], NONE, 1)
+    D.dycl_subnet_end(g, sn)
+    return sn
+
+
+def _block(g, sn, W, i, c_in, c_out, stride):
+    """He basic block: relu(conv2(relu(conv1(h))) + shortcut(h)); option A when shapes change."""
+    D.dycl_subnet_block_begin(g, sn)
+    D.dycl_subnet_conv2d(g, sn, c_in, c_out, 3, stride, 1, W[f"b{i}.c1.w"], W[f"b{i}.c1.b"], RELU, 0)
+    D.dycl_subnet_conv2d(g, sn, c_out, c_out, 3, 1, 1, W[f"b{i}.c2.w"], W[f"b{i}.c2.b"], RELU, 1)
+
+
+def _block_io(i, per_stage, widths=(16, 32, 64)):
+    s = (i - 1) // per_stage
+    if s > 0 and (i - 1) % per_stage == 0:
+        return widths[s - 1], widths[s], 2
+    return widths[s], widths[s], 1
+
+
+def _create(device, h, w, c, precision):
+    g = D.dycl_graph_create(device, h, w, c)
+    D.dycl_graph_set_precision(g, precision)
+    return g
+
+
+FP32_STREAM = D.DYCL_PREC_FP32_STREAM
+
+
+def build_mlp_ee(W, max_batch, device=0, tau=0.9, precision=FP32_STREAM) -> Model:
+    """Config 1: x -> [dense+ReLU -> exit head0] -> [dense+ReLU -> exit head1] -> [dense+ReLU -> final head2]."""
+    g = _create(device, 1, 1, 64, precision)
+    for k in range(3):
+        sn = D.dycl_subnet_begin(g)
+        D.dycl_subnet_dense(g, sn, 64, 64, W[f"fc{k}.w"], W[f"fc{k}.b"], RELU, 0)
+        D.dycl_subnet_end(g, sn)
+        D.dycl_seq(g, sn)
+        h = _head(g, W, f"head{k}", 64, gap=False)
+        if k < 2:
+            D.dycl_exit(g, h, tau)
+        else:
+            D.dycl_final(g, h)
+    D.dycl_finalize(g, max_batch)
+    return Model(g, (64,), 10, max_batch, "mlp_ee")
+
+
+def build_sdn_resnet56(W, max_batch, device=0, tau=None, precision=FP32_STREAM) -> Model:
+    """Config 2, rewritten: unrolled 27 blocks split at the IC positions (after 5, 11, 16, 22)."""
+    tau = float(W["tau"]) if tau is None else tau
+    g = _create(device, 32, 32, 3, precision)
+    bounds = [0, 5, 11, 16, 22, 27]
+    for k in range(5):
+        sn = D.dycl_subnet_begin(g)
+        if k == 0:
+            D.dycl_subnet_conv2d(g, sn, 3, 16, 3, 1, 1, W["stem.w"], W["stem.b"], RELU, 0)
+        for i in range(bounds[k] + 1, bounds[k + 1] + 1):
+            _block(g, sn, W, i, *_block_io(i, 9))
+        D.dycl_subnet_end(g, sn)
+        D.dycl_seq(g, sn)
+        c = _block_io(bounds[k + 1], 9)[1]
+        if k < 4:
+            D.dycl_exit(g, _head(g, W, f"ic{k}", c), tau)
+        else:
+            D.dycl_final(g, _head(g, W, "final", c))
+    D.dycl_finalize(g, max_batch)
+    return Model(g, (32, 32, 3), 10, max_batch, "sdn_resnet56")
+
+
+def build_skipnet_resnet38(W, max_batch, device=0, thr=None, precision=FP32_STREAM) -> Model:
+    """Config 3, rewritten (Listing 4 style): stem+block1, then per block i=2..18 a gate node."""
+    thr = float(W["thr"]) if thr is None else thr
+    g = _create(device, 32, 32, 3, precision)
+    sn = D.dycl_subnet_begin(g)
+    D.dycl_subnet_conv2d(g, sn, 3, 16, 3, 1, 1, W["stem.w"], W["stem.b"], RELU, 0)
+    _block(g, sn, W, 1, 16, 16, 1)
+    D.dycl_subnet_end(g, sn)
+    D.dycl_seq(g, sn)
+    for i in range(2, 19):
+        ci, co, stride = _block_io(i, 6)
+        gate = _head(g, W, f"gate{i}", ci)
+        blk = D.dycl_subnet_begin(g)
+        _block(g, blk, W, i, ci, co, stride)
+        D.dycl_subnet_end(g, blk)
+        D.dycl_gate(g, gate, thr, blk)
+    D.dycl_final(g, _head(g, W, "final", 64))
+    D.dycl_finalize(g, max_batch)
+    return Model(g, (32, 32, 3), 10, max_batch, "skipnet_resnet38")
+
+
+BUILDERS = {1: build_mlp_ee, 2: build_sdn_resnet56, 3: build_skipnet_resnet38}

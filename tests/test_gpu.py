@@ -1,0 +1,219 @@
+"""GPU parity tests: the CUDA path (through the C ABI) vs the CPU oracle.
+
+Run on a B200:  python -m pytest tests -m gpu -x -q
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import workloads as wl
+from oracle import programs as prg
+from tests.parity import report
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # collected on CPU, skipped there
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2307_04963_b200 import dycl as D  # noqa: E402
+from paper_2307_04963_b200 import programs as P  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def _bits_to_t(bits):
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).to(DEV)
+
+
+def _t_to_f64(t):
+    return (t.cpu().numpy().view(np.uint16).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+@pytest.fixture(scope="module")
+def any_graph():
+    g = D.dycl_graph_create(0, 1, 1, 8)
+    yield g
+    D.dycl_graph_destroy(g)
+
+
+# ------------------------------------------------------------ a1 conv kernel
+CONV_CASES = [
+    # n, H, W, C, Cout, k, stride, pad, relu, res_mode
+    (3, 32, 32, 16, 16, 3, 1, 1, 1, 0),
+    (2, 32, 32, 16, 16, 3, 1, 1, 1, 1),
+    (2, 32, 32, 16, 32, 3, 2, 1, 1, 2),     # option-A shortcut
+    (4, 32, 32, 8, 16, 3, 1, 1, 1, 0),      # stem (C padded 3 -> 8)
+    (5, 8, 8, 64, 64, 3, 1, 1, 1, 1),
+    (5, 7, 7, 64, 128, 3, 1, 1, 0, 0),      # ragged M (245 rows), BN = 128
+    (3, 7, 7, 32, 256, 1, 1, 0, 1, 0),      # BN = 256
+    (2, 9, 9, 16, 512, 3, 2, 1, 1, 0),      # N tiling (2 x 256)
+    (37, 1, 1, 64, 64, 1, 1, 0, 1, 0),      # dense layer
+    (1, 12, 12, 24, 48, 7, 2, 3, 0, 0),     # 7x7 / stride 2 / pad 3
+]
+
+
+@pytest.mark.parametrize("case", CONV_CASES, ids=[str(c) for c in CONV_CASES])
+def test_conv_kernel_matches_oracle_conv(any_graph, case):
+    n, H, W, C, Co, k, st, pad, relu, res_mode = case
+    rng = np.random.default_rng(abs(hash(case)) % 2**32)
+    x = wl.f32_to_bf16_bits(rng.standard_normal((n, H, W, C)))
+    w = wl.f32_to_bf16_bits(rng.standard_normal((Co, k, k, C)) * np.sqrt(2.0 / (k * k * C)))
+    b = rng.uniform(-0.1, 0.1, Co).astype(np.float32)
+    Ho, Wo = (H + 2 * pad - k) // st + 1, (W + 2 * pad - k) // st + 1
+    res = None
+    if res_mode == 1:
+        res = wl.f32_to_bf16_bits(rng.standard_normal((n, Ho, Wo, Co)))
+    elif res_mode == 2:
+        res = wl.f32_to_bf16_bits(rng.standard_normal((n, 2 * Ho, 2 * Wo, Co // 2)))
+    y = torch.zeros((n, Ho, Wo, Co), dtype=torch.int16, device=DEV)
+    D.dycl_debug_conv2d(any_graph, _bits_to_t(x), n, H, W, C, w, b, Co, k, st, pad, relu,
+                        _bits_to_t(res) if res is not None else None, res_mode, y)
+    got = _t_to_f64(y)
+    xf, wf = prg._bf16_to_f64(x), prg._bf16_to_f64(w)
+    for i in range(n):
+        ref = O.conv2d(xf[i], wf, b.astype(np.float64), st, pad)
+        if res_mode == 1:
+            ref = ref + prg._bf16_to_f64(res[i])
+        elif res_mode == 2:
+            ref = ref + O.option_a(prg._bf16_to_f64(res[i]), Co)
+        if relu:
+            ref = O.relu(ref)
+        ref = O.round_bf16(ref)
+        # fp32 tensor-core accumulation vs fp64: at most one bf16 rounding step apart
+        tol = 2.0 ** -7 * np.abs(ref) + 1e-6
+        bad = np.abs(got[i] - ref) > tol
+        assert not bad.any(), (i, np.argwhere(bad)[:5], got[i][bad][:5], ref[bad][:5])
+        assert np.mean(got[i] != ref) < 0.01
+
+
+def test_conv_kernel_zero_rows(any_graph):
+    y = torch.full((1, 4, 4, 16), 7, dtype=torch.int16, device=DEV)
+    x = torch.zeros((1, 4, 4, 16), dtype=torch.int16, device=DEV)
+    w = np.zeros((16, 3, 3, 16), np.uint16)
+    D.dycl_debug_conv2d(any_graph, x, 0, 4, 4, 16, w, np.zeros(16, np.float32), 16, 3, 1, 1, 1, None, 0, y)
+    assert torch.all(y == 7)
+
+
+# ------------------------------------------------------------ whole programs
+def _run_gpu(model, X):
+    B = X.shape[0]
+    x = torch.from_numpy(X).to(DEV)
+    logits = torch.full((max(B, 1), model.K), float("nan"), device=DEV)
+    path = torch.full((max(B, 1),), -7, dtype=torch.int32, device=DEV)
+    model.run(x, logits, path)
+    torch.cuda.synchronize()
+    return logits[:B].cpu().numpy(), path[:B].cpu().numpy()
+
+
+@pytest.fixture(scope="module")
+def mlp():
+    W = wl.mlp_weights()
+    return W, P.build_mlp_ee(W, 64)
+
+
+@pytest.fixture(scope="module")
+def r56():
+    W = wl.sdn_r56_weights()
+    return W, P.build_sdn_resnet56(W, 4096)
+
+
+@pytest.fixture(scope="module")
+def r38():
+    W = wl.skipnet_r38_weights()
+    return W, P.build_skipnet_resnet38(W, 512)
+
+
+def _parity(W, model, program, X, **kw):
+    lg, pg = _run_gpu(model, X)
+    lo, po, pr = O.run_batch(program, X, prg.prepare(W), "mirror", **kw)
+    return report(lg, pg, lo, po, pr), lg, pg
+
+
+def test_cfg1_mlp_parity(mlp):
+    W, m = mlp
+    X = wl.mlp_inputs(wl.INPUT_SEED, 0, 32)
+    r, lg, pg = _parity(W, m, O.mlp_ee, X)
+    print("cfg1", r)
+    assert r["outside_band_mismatch"] == 0 and r["logit_rel_fail"] == 0
+    assert set(np.unique(pg)) <= {0, 1, 2}
+
+
+@pytest.mark.parametrize("B", [256, 203, 1])
+def test_cfg2_sdn_parity(r56, B):
+    W, m = r56
+    X = wl.image_inputs(wl.INPUT_SEED, 1000, B)
+    r, lg, pg = _parity(W, m, O.sdn_resnet56, X)
+    print("cfg2", B, r)
+    assert r["logit_rel_fail"] == 0
+    assert r["outside_band_mismatch"] <= max(1, B // 200), r
+
+
+def test_cfg3_skipnet_parity(r38):
+    W, m = r38
+    X = wl.image_inputs(wl.INPUT_SEED, 2000, 256)
+    r, lg, pg = _parity(W, m, O.skipnet_resnet38, X)
+    print("cfg3", r)
+    assert r["logit_rel_fail"] == 0
+    assert r["outside_band_mismatch"] <= 2, r
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_bf16_storage_mode_vs_mirror_bf16(cfg):
+    """DYCL_PREC_BF16 (all-bf16 storage) graded against the oracle's mirror_bf16 mode.
+    Decisions must still match outside the band; logits drift up to ~3e-2 (DESIGN R13)."""
+    if cfg == 2:
+        W = wl.sdn_r56_weights()
+        m = P.build_sdn_resnet56(W, 256, precision=D.DYCL_PREC_BF16)
+        prog = O.sdn_resnet56
+    else:
+        W = wl.skipnet_r38_weights()
+        m = P.build_skipnet_resnet38(W, 256, precision=D.DYCL_PREC_BF16)
+        prog = O.skipnet_resnet38
+    X = wl.image_inputs(wl.INPUT_SEED, 3000, 256)
+    lg, pg = _run_gpu(m, X)
+    lo, po, pr = O.run_batch(prog, X, prg.prepare(W), "mirror_bf16")
+    r = report(lg, pg, lo, po, pr, rel=5e-2)
+    print("bf16 storage cfg", cfg, r)
+    assert r["outside_band_mismatch"] <= 2 and r["logit_rel_fail"] == 0
+
+
+def test_empty_batch(r56):
+    W, m = r56
+    lg, pg = _run_gpu(m, np.zeros((0, 32, 32, 3), np.float32))
+    assert lg.shape == (0, 10) and pg.shape == (0,)
+
+
+def test_permutation_and_batch_size_invariance(r56):
+    """Row i's result is bitwise independent of its batch position and the batch size."""
+    W, m = r56
+    X = wl.image_inputs(wl.INPUT_SEED, 0, 300)
+    l1, p1 = _run_gpu(m, X)
+    perm = np.random.default_rng(0).permutation(300)
+    l2, p2 = _run_gpu(m, X[perm])
+    assert np.array_equal(l2, l1[perm]) and np.array_equal(p2, p1[perm])
+    l3, p3 = _run_gpu(m, X[:77])
+    assert np.array_equal(l3, l1[:77]) and np.array_equal(p3, p1[:77])
+
+
+def test_run_host_equals_run(r56):
+    W, m = r56
+    X = wl.image_inputs(wl.INPUT_SEED, 0, 128)
+    l1, p1 = _run_gpu(m, X)
+    lh = np.zeros((128, 10), np.float32)
+    ph = np.zeros(128, np.int32)
+    m.run_host(X, lh, ph)
+    assert np.array_equal(lh, l1) and np.array_equal(ph, p1)
+
+
+def test_cfg2_full_batch_sampled_parity(r56):
+    """BASELINE size (B = 4096, the bench launch configuration): sampled rows vs oracle."""
+    W, m = r56
+    X = wl.image_inputs(wl.INPUT_SEED, 0, 4096)
+    lg, pg = _run_gpu(m, X)
+    assert np.bincount(pg, minlength=5).sum() == 4096 and np.isfinite(lg).all()
+    idx = np.random.default_rng(wl.ORACLE_SUBSET_SEED).choice(4096, 48, replace=False)
+    lo, po, pr = O.run_batch(O.sdn_resnet56, X[idx], prg.prepare(W), "mirror")
+    r = report(lg[idx], pg[idx], lo, po, pr)
+    print("cfg2 full sampled", r)
+    assert r["logit_rel_fail"] == 0 and r["outside_band_mismatch"] <= 1

@@ -117,13 +117,16 @@ def _mlp_bruteforce(x, W, mode, tau=0.9):
             a = (a.astype(np.uint32) << 16).view(np.float32)
         return a.astype(np.float64)
 
-    def r(v):  # bf16 RNE via float32 bit tricks would double-round; use torch on exact fp64 -> ok only
-        return O.round_bf16(v) if mode == "mirror" else v
+    def op(v):      # tensor-core operand rounding (both mirror modes)
+        return O.round_bf16(v) if mode != "exact" else v
+
+    def store(v):   # stored-activation rounding (all-bf16 storage only)
+        return O.round_bf16(v) if mode == "mirror_bf16" else v
 
     h = torch.tensor(np.float32(x)).to(torch.bfloat16).double().numpy()
     outs = []
     for k in range(3):
-        h = r(np.maximum(f(f"fc{k}.w").dot(h) + f(f"fc{k}.b"), 0))
+        h = store(np.maximum(f(f"fc{k}.w").dot(op(h)) + f(f"fc{k}.b"), 0))
         z = f(f"head{k}.w").dot(h) + f(f"head{k}.b")
         e = np.exp(z - z.max())
         outs.append((z, (e / e.sum()).max()))
@@ -133,7 +136,7 @@ def _mlp_bruteforce(x, W, mode, tau=0.9):
     return outs[2][0], 2
 
 
-@pytest.mark.parametrize("mode", ["mirror", "exact"])
+@pytest.mark.parametrize("mode", ["mirror", "mirror_bf16", "exact"])
 def test_mlp_matches_bruteforce(mode):
     W = wl.mlp_weights()
     X = wl.mlp_inputs(wl.INPUT_SEED, 0, 32)
@@ -184,17 +187,25 @@ def test_sdn_all_exit_at_ic1_is_prefix_net(r56):
         np.testing.assert_allclose(z, ref, rtol=1e-12, atol=1e-12)
 
 
-def test_sdn_mirror_stores_bf16_values(r56):
-    """Mirror mode: every stored activation is bf16-representable (rounding points R13)."""
+def test_sdn_mirror_rounding_points(r56):
+    """Rounding points (reading R13): mirror_bf16 stores bf16 everywhere; mirror
+    (fp32 stream) rounds exactly the conv operands: a block equals the exact
+    block applied to a bf16-rounded conv1 input with the unrounded shortcut."""
     X = wl.image_inputs(wl.INPUT_SEED, 0, 1)
     P = prg.prepare(r56)
-    h = prg.stem(X[0], P, "mirror")
+    h = prg.stem(X[0], P, "mirror_bf16")
     assert np.array_equal(O.round_bf16(h), h)
-    h2 = prg.basic_block(h, P, 1, 9, "mirror")
+    h2 = prg.basic_block(h, P, 1, 9, "mirror_bf16")
     assert np.array_equal(O.round_bf16(h2), h2)
-    # and mirror differs from exact only by rounding-size perturbations
+    hs = prg.stem(X[0], P, "mirror")
+    assert not np.array_equal(O.round_bf16(hs), hs)          # the stream is not rounded
+    hm = prg.basic_block(hs, P, 1, 9, "mirror")
+    t = O.round_bf16(O.relu(O.conv2d(O.round_bf16(hs), P["b1.c1.w"], P["b1.c1.b"], 1, 1)))
+    ref = O.relu(O.conv2d(t, P["b1.c2.w"], P["b1.c2.b"], 1, 1) + hs)
+    np.testing.assert_array_equal(hm, ref)
     he = prg.basic_block(prg.stem(X[0], P, "exact"), P, 1, 9, "exact")
-    assert np.max(np.abs(he - h2)) < 0.05 * np.max(np.abs(he))
+    for v in (h2, hm):
+        assert np.max(np.abs(he - v)) < 0.05 * np.max(np.abs(he))
 
 
 def test_sdn_calibrated_exit_histogram(r56):
