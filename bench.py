@@ -1,0 +1,283 @@
+"""Benchmark: batched dynamic-NN inference (DyCL, arXiv 2307.04963) on B200.
+
+Workload (BASELINE.json configs[1], the configuration its metric is quoted on):
+ShallowDeep-style early-exit ResNet-56 on synthetic 32x32x3 CIFAR-shaped inputs,
+batch 4096 per GPU, 4 internal classifiers + final head, tau = 0.9, calibrated
+heads (workloads/calib/cfg2.json).  One step = one full pass of the hot path
+(input cast, every sub-network, predicates, compaction, gathers, scatters) over
+one batch, through the C ABI (dycl_run).
+
+  python bench.py [--gpus N --steps K --warmup W]            # our arm
+  python bench.py --impl reference ...                        # the CPU oracle arm
+  torchrun --nproc-per-node N bench.py --gpus N ...           # N > 1: one rank per GPU
+
+Multi-GPU: samples are independent (Eq. 2 is per-x), so each rank processes its
+own 4096-sample slice of the global batch (weak scaling) with no collective on
+the data path; timing = max over ranks of the per-rank device time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "dynamic-inference samples/sec"
+UNIT = "samples/s"
+BATCH = 4096
+WORKLOAD = ("cfg2: ShallowDeep-style early-exit ResNet-56, synthetic 32x32x3 CIFAR-shaped inputs, "
+            "4 ICs after blocks 5/11/16/22 + final head, tau=0.9, calibrated heads")
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p["bf16_tflops"], p["bf16_tflops_sustained"], "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = f"/tmp/dycl_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 9:
+                    continue
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+                for n, v in zip(names, f[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        except Exception:
+            return None
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_oracle_rate(n_samples: int, seed_offset: int = 0):
+    """The oracle (as it stands) on this host's cores: per-sample interpreter, mirror mode."""
+    import oracle as O
+    import workloads as wl
+    from oracle import programs as prg
+    P = prg.prepare(wl.sdn_r56_weights())
+    X = wl.image_inputs(wl.INPUT_SEED, seed_offset, n_samples)
+    cores = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    O.run_batch(O.sdn_resnet56, X, P, "mirror", threads=cores)
+    dt = time.perf_counter() - t0
+    return n_samples / dt, cores, dt
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    per_step = args.ref_samples
+    times = []
+    cores = len(os.sched_getaffinity(0))
+    for i in range(args.warmup + args.steps):
+        rate, cores, dt = cpu_oracle_rate(per_step, seed_offset=i * per_step)
+        if i >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    value = per_step * args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": WORKLOAD, "samples_per_step": per_step},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{per_step} samples of cfg2 per step (seeded inputs), per-sample fp64 interpreter"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_dycl(args):
+    import torch
+    import workloads as wl
+    from paper_2307_04963_b200 import dycl as D
+    from paper_2307_04963_b200 import programs as P
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    stream = torch.cuda.current_stream()
+
+    W = wl.sdn_r56_weights()
+    model = P.build_sdn_resnet56(W, BATCH, device=local)
+    X = wl.image_inputs(wl.INPUT_SEED, rank * BATCH, BATCH)            # this rank's global slice
+    x = torch.from_numpy(X).to(dev)
+    logits = torch.empty((BATCH, 10), device=dev)
+    path = torch.empty(BATCH, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > L2 (126 MB)
+
+    for _ in range(args.warmup):
+        model.run(x, logits, path, stream=stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+
+    D.dycl_set_profiling(model.g, 1)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    conv_ms = conv_bytes = conv_flops = 0.0
+    conv_launches = 0
+    kind_ms = {}
+    clocks = ClockSampler(local)
+    clocks.start()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.zero_()                          # evict L2 between timed steps (not timed)
+        ev[i][0].record(stream)
+        model.run(x, logits, path, stream=stream)
+        ev[i][1].record(stream)
+        for p in D.dycl_profile_read(model.g):    # syncs the stream; events already recorded
+            kind_ms[p["kind"]] = kind_ms.get(p["kind"], 0.0) + p["ms"]
+            if p["kind"] == "conv":
+                conv_ms += p["ms"]
+                conv_bytes += p["bytes"]
+                conv_flops += p["flops"]
+                conv_launches += 1
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    D.dycl_set_profiling(model.g, 0)
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    launches = D.dycl_launches_per_run(model.g) * args.steps
+    hist = np.bincount(path.cpu().numpy(), minlength=5).tolist()
+
+    # e2e: the public host-buffer call (pinned input; H2D + run + D2H each step)
+    xh = torch.from_numpy(X).pin_memory()
+    lh = torch.empty((BATCH, 10), dtype=torch.float32).pin_memory()
+    ph = torch.empty(BATCH, dtype=torch.int32).pin_memory()
+    model.run_host(xh, lh, ph, stream=stream)
+    torch.cuda.synchronize()
+    e2e_ms = 0.0
+    for i in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        model.run_host(xh, lh, ph, stream=stream)
+        e2e_ms += (time.perf_counter() - t0) * 1e3
+    assert np.array_equal(ph.numpy(), path.cpu().numpy()), "host-buffer run disagrees with device run"
+
+    t = torch.tensor([total_ms, e2e_ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.barrier()
+    total_ms, e2e_ms = float(t[0]), float(t[1])
+    if rank != 0:
+        if ws > 1:
+            torch.distributed.destroy_process_group()
+        return
+
+    hbm, tf_burst, tf_sus, peak_src = _peaks()
+    value = BATCH * ws * args.steps / (total_ms / 1e3)
+    achieved = conv_bytes / (conv_ms / 1e3) / 1e9 if conv_ms else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "conv_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "batch_per_gpu": BATCH, "global_batch": BATCH * ws,
+                   "precision": "bf16 tensor-core operands, fp32 accumulate, fp32 residual stream",
+                   "l2": "flushed (256 MB write) before every timed step, flush not timed",
+                   "parallelism": f"dp{ws} (independent shards, no collective)",
+                   "exit_histogram_rank0": hist},
+        "clocks": clk,
+        "e2e": {"value": BATCH * ws * args.steps / (e2e_ms / 1e3), "unit": UNIT,
+                "h2d_bytes_per_step": int(X.nbytes), "d2h_bytes_per_step": int(lh.numel() * 4 + ph.numel() * 4)},
+        "gpu_launches": launches,
+        "roofline": {"kernel": "k_conv_tma (a1: implicit-GEMM conv on tcgen05, fused epilogue)",
+                     "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
+                     "share_of_step": conv_ms / total_ms if total_ms else None,
+                     "tensor_tflops": conv_flops / (conv_ms / 1e3) / 1e12 if conv_ms else 0.0,
+                     "tensor_frac_of_sustained": (conv_flops / (conv_ms / 1e3) / 1e12) / tf_sus if conv_ms else 0.0,
+                     "launches_per_step": conv_launches // max(args.steps, 1)},
+        "kernel_ms_per_step": {k: v / args.steps for k, v in sorted(kind_ms.items(), key=lambda kv: -kv[1])},
+    }
+    if ws == 1 and not args.no_cpu_baseline:
+        rate, cores, dt = cpu_oracle_rate(args.cpu_samples)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                "sample": f"{args.cpu_samples} cfg2 samples (seeded inputs 0..{args.cpu_samples - 1}), "
+                                          f"per-sample fp64 interpreter, mirror mode, {dt:.1f} s wall"}
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="dycl", choices=["dycl", "reference"])
+    ap.add_argument("--cpu-samples", type=int, default=4096)
+    ap.add_argument("--ref-samples", type=int, default=32)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_dycl(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -201,10 +201,12 @@ dycl_status dycl_profile_read(dycl_graph g, int32_t max_n, int32_t* kind, float*
  *   res : device bf16 shortcut or NULL; res_mode 0 none, 1 identity [n][Ho][Wo][c_out],
  *         2 option A from [n][2Ho][2Wo][c_out/2]
  *   y   : device bf16 [n][Ho][Wo][c_out]
+ *   path: 0 = the kernel dycl_run would pick, 1 = cp.async-fed kernel, 2 = TMA-fed kernel
+ *         (CUDA error "operation not supported" if the shape does not qualify)
  * g supplies the device (any created graph).  Errors: INVALID_ARG, UNSUPPORTED, CUDA. */
 dycl_status dycl_debug_conv2d(dycl_graph g, int64_t n, int H, int W, int C, const uint16_t* w, const float* bias,
                               int c_out, int k, int stride, int pad, int relu, const void* res, int res_mode,
-                              const void* x, void* y);
+                              const void* x, void* y, int path);
 
 #ifdef __cplusplus
 }

@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -90,6 +91,8 @@ struct dycl_graph_s {
   uint16_t* buf[NBUF] = {};
   float* buf32[NBUF32] = {};
   int precision = DYCL_PREC_FP32_STREAM;
+  int conv_path = 0;                 // 0 auto; DYCL_CONV_PATH=1 forces the cp.async kernel
+  int conv_dbg = 0;                  // DYCL_CONV_DBG: timing experiments only (results invalid)
   long long max_row_elems = 0;
   int* d_counts = nullptr;
   int n_slots = 0;
@@ -341,12 +344,13 @@ struct Exec {
       a.res_mode = L.res_mode;
       a.rH = L.res_shape.H; a.rW = L.res_shape.W; a.rC = L.res_shape.Cp();
       a.r_pad_lo = (L.out.C - L.res_shape.C) / 2;
+      a.dbg = g->conv_dbg;
       const double res_b = L.res_mode ? (a.res32 ? 4.0 : 2.0) * L.res_shape.row_elems() *
                                             (L.res_mode == 2 ? 0.25 : 1.0) : 0.0;
       const double row_b = 2.0 * L.in.row_elems() + (o.f >= 0 ? 6.0 : 2.0) * L.out.row_elems() + res_b;
       const double row_f = 2.0 * L.out.H * L.out.W * L.out.C * (double)(L.k * L.k * L.in.C);
       prof_begin(DYCL_K_CONV, cnt, row_b, row_f, 2.0 * L.out.C * L.Kp);
-      cudaError_t e = dycl::launch_conv_tc(a, batch, g->num_sms, st);
+      cudaError_t e = dycl::launch_conv(a, batch, g->num_sms, st, g->conv_path);
       prof_end();
       if (e != cudaSuccess) return cuda_fail(g, e, "launch_conv_tc");
       cur = o;
@@ -525,6 +529,8 @@ dycl_status dycl_graph_create(int cuda_device, int in_h, int in_w, int in_c, dyc
   if (!g) return fail(nullptr, DYCL_E_OOM, "host allocation failed");
   g->device = cuda_device;
   g->input = Shape{in_h, in_w, in_c};
+  if (const char* cp = getenv("DYCL_CONV_PATH")) g->conv_path = atoi(cp);
+  if (const char* cd = getenv("DYCL_CONV_DBG")) g->conv_dbg = atoi(cd);
   cudaSetDevice(cuda_device);
   cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
   int major = 0;
@@ -880,7 +886,7 @@ dycl_status dycl_profile_read(dycl_graph g, int32_t max_n, int32_t* kind, float*
 
 dycl_status dycl_debug_conv2d(dycl_graph g, int64_t n, int H, int W, int C, const uint16_t* w, const float* bias,
                               int c_out, int k, int stride, int pad, int relu, const void* res, int res_mode,
-                              const void* x, void* y) {
+                              const void* x, void* y, int path) {
   if (!g || !w || !bias || !x || !y || n < 0 || C % 8 || c_out % 16 || k < 1 || stride < 1 || res_mode < 0 ||
       res_mode > 2 || (res_mode && !res))
     return fail(g, DYCL_E_INVALID_ARG, "debug_conv2d: bad argument");
@@ -903,7 +909,7 @@ dycl_status dycl_debug_conv2d(dycl_graph g, int64_t n, int H, int W, int C, cons
   a.K = K; a.Kp = Kp; a.relu = relu; a.res_mode = res_mode;
   a.rH = 2 * Ho; a.rW = 2 * Wo; a.rC = c_out / 2; a.r_pad_lo = c_out / 4;
   if (res_mode == 1) { a.rH = Ho; a.rW = Wo; a.rC = c_out; a.r_pad_lo = 0; }
-  cudaError_t e = n > 0 ? dycl::launch_conv_tc(a, (int)n, g->num_sms, 0) : cudaSuccess;
+  cudaError_t e = n > 0 ? dycl::launch_conv(a, (int)n, g->num_sms, 0, path) : cudaSuccess;
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   cudaFree(dw);
   cudaFree(db);

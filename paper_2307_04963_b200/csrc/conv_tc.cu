@@ -11,10 +11,12 @@
 //   warps 0-3  epilogue: tcgen05.ld TMEM -> regs, +bias, +shortcut (identity or
 //              option A), ReLU, RNE to bf16, 16-byte stores (one output pixel row
 //              of BN channels per thread)
-//   warps 4-7  producers: im2col gather of A and the B tile with 16-byte
+//   warps 4-11 producers: im2col gather of A and the B tile with 16-byte
 //              cp.async (zero-fill implements the padding) into a STAGES-deep ring
-//              laid out in the UMMA 128B-swizzle K-major canonical layout
-//   warp  8    TMEM allocator + MMA issuer: one lane issues tcgen05.mma
+//              laid out in the UMMA 128B-swizzle K-major canonical layout; the
+//              per-chunk tap geometry (r, s, c) is row-independent and read from a
+//              shared-memory table built once per CTA (no divisions in the loop)
+//   warp  12   TMEM allocator + MMA issuer: one lane issues tcgen05.mma
 //              (M=128, N=BN, K=16) and tcgen05.commit to free ring slots and to
 //              hand a finished accumulator to the epilogue
 // Two TMEM accumulators (2*BN columns) let the epilogue of tile i overlap the
@@ -30,7 +32,10 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;          // bf16 elements per K block = one 128-byte swizzle row
-constexpr int NUM_THREADS = 288;
+constexpr int NUM_PRODUCERS = 256;   // 8 warps: two threads per A row, 4 chunks each
+constexpr int NUM_THREADS = 128 + NUM_PRODUCERS + 32;
+constexpr int MMA_WARP = (128 + NUM_PRODUCERS) / 32;
+constexpr int MAX_KCH = 1024;        // K chunks (8 elements) covered by the tap table (K <= 8192)
 
 template <int BN>
 struct Cfg {
@@ -40,7 +45,7 @@ struct Cfg {
   static constexpr int STAGES = (196608 / STAGE_BYTES) > 8 ? 8 : (196608 / STAGE_BYTES);
   static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128
                                    : (2 * BN) <= 256 ? 256 : 512;
-  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256 + MAX_KCH * 8;
   // Producer lag: each producer thread keeps LAG cp.async groups (ring fills) in
   // flight before it arrives on the oldest fill's full barrier.  LAG <= STAGES-1
   // is deadlock-free: before issuing fill f+1 the producer waits for the MMA to
@@ -71,6 +76,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_conv_tc(const ConvArgs a) {
   const uint32_t tfull0 = empty0 + 8 * S;
   const uint32_t tempty0 = tfull0 + 16;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
+  int2* tap_tab = reinterpret_cast<int2*>(reinterpret_cast<uint8_t*>(bars) + 256);   // [Kp/8]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -84,9 +90,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_conv_tc(const ConvArgs a) {
   const int ksteps = (a.K + 15) >> 4;
   const int kblocks = (ksteps + 3) >> 2;
 
+  // tap table: chunk j covers k = 8j..8j+7 = tap (r, s), channels c..c+7.
+  //   .x = element offset (r*W + s)*C + c from the window origin, .y = (r << 16) | s,
+  //   .y = -1 marks chunks beyond K (zero-filled).
+  for (int j = threadIdx.x; j < a.Kp / 8 && j < MAX_KCH; j += blockDim.x) {
+    const int k = j * 8;
+    if (k < a.K) {
+      const int tap = k / a.C, c = k - (k / a.C) * a.C;
+      const int r = tap / a.ksz, s2 = tap - (tap / a.ksz) * a.ksz;
+      tap_tab[j] = make_int2((r * a.W + s2) * a.C + c, (r << 16) | s2);
+    } else {
+      tap_tab[j] = make_int2(0, -1);
+    }
+  }
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
-      ptx::mbar_init(full0 + 8 * i, 128);
+      ptx::mbar_init(full0 + 8 * i, NUM_PRODUCERS);
       ptx::mbar_init(empty0 + 8 * i, 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -95,24 +114,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_conv_tc(const ConvArgs a) {
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 8) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), C::TMEM_COLS);
+  if (warp == MMA_WARP) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), C::TMEM_COLS);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp >= 4 && warp < 8) {
+  if (warp >= 4 && warp < MMA_WARP) {
     // ------------------------------------------------------------ producers
     const int t = threadIdx.x - 128;
-    const uint32_t a_row_off = (uint32_t)((t >> 3) * 1024 + (t & 7) * 128);
-    const int sw = t & 7;
+    const int row = t & 127;                 // A row of the tile this thread fills
+    const int qh = (t >> 7) * 4;             // its chunks: qh .. qh+3 of every K block
+    const uint32_t a_row_off = (uint32_t)((row >> 3) * 1024 + (row & 7) * 128);
+    const int sw = row & 7;
     int stage = 0;
     uint32_t phase = 0;
     int issued = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       const int m_tile = tile / n_tiles;
       const int n_tile = tile - m_tile * n_tiles;
-      const long long m = (long long)m_tile * BM + t;
+      const long long m = (long long)m_tile * BM + row;
       const bool row_ok = m < M;
       int n = 0, ho = 0, wo = 0;
       if (row_ok) {
@@ -121,36 +142,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_conv_tc(const ConvArgs a) {
         ho = p / a.Wo;
         wo = p - ho * a.Wo;
       }
-      const uint16_t* xs = a.x + (size_t)n * a.H * a.W * a.C;
       const int hi0 = ho * a.stride - a.pad;
       const int wi0 = wo * a.stride - a.pad;
+      // window origin (may point before the sample for padded rows; only used when in bounds)
+      const long long base = ((long long)n * a.H * a.W + (long long)hi0 * a.W + wi0) * a.C;
       const uint16_t* wt = a.w + (size_t)n_tile * BN * a.Kp;
       for (int kb = 0; kb < kblocks; ++kb) {
         ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1);
         const int kused = min(BK, ksteps * 16 - kb * BK);   // K elements the MMAs read in this block
         const uint32_t sa = ptx::smem_u32(sA + stage * C::A_BYTES) + a_row_off;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int qq = 0; qq < 4; ++qq) {
+          const int q = qh + qq;
           if (q * 8 < kused) {
-            const int k = kb * BK + q * 8;
+            const int2 tb = tap_tab[kb * 8 + q];
+            const int r = tb.y >> 16, s2 = tb.y & 0xFFFF;
             const void* src = a.x;
             uint32_t bytes = 0;
-            if (row_ok && k < a.K) {
-              const int tap = k / a.C;
-              const int c = k - tap * a.C;
-              const int r = tap / a.ksz;
-              const int s = tap - r * a.ksz;
-              const int hi = hi0 + r, wi = wi0 + s;
-              if ((unsigned)hi < (unsigned)a.H && (unsigned)wi < (unsigned)a.W) {
-                src = xs + ((size_t)hi * a.W + wi) * a.C + c;
-                bytes = 16;
-              }
+            if (row_ok && tb.y >= 0 && (unsigned)(hi0 + r) < (unsigned)a.H && (unsigned)(wi0 + s2) < (unsigned)a.W) {
+              src = a.x + base + tb.x;
+              bytes = 16;
             }
             ptx::cp_async_16_ca(sa + (uint32_t)((q ^ sw) << 4), src, bytes);
           }
         }
         const uint32_t sb = ptx::smem_u32(sB + stage * C::B_BYTES);
-        for (int i = t; i < BN * 8; i += 128) {
+        for (int i = t; i < BN * 8; i += NUM_PRODUCERS) {
           const int nrow = i % BN;
           const int q = i / BN;
           if (q * 8 < kused) {
@@ -176,7 +193,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_conv_tc(const ConvArgs a) {
     ptx::fence_proxy_async_smem();
     const int pend = issued < LAG ? issued : LAG;
     for (int j = pend; j >= 1; --j) ptx::mbar_arrive(full0 + 8 * ((stage - j + S) % S));
-  } else if (warp == 8) {
+  } else if (warp == MMA_WARP) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t IDESC = ptx::make_idesc_bf16(BM, BN);
     int stage = 0;
@@ -298,7 +315,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_conv_tc(const ConvArgs a) {
   }
 
   __syncthreads();
-  if (warp == 8) {
+  if (warp == MMA_WARP) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
@@ -324,6 +341,7 @@ cudaError_t launch_bn(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t
 }  // namespace
 
 cudaError_t launch_conv_tc(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream) {
+  if (a.Kp / 8 > MAX_KCH || a.C % 8 != 0) return cudaErrorInvalidValue;
   // N tile: the whole Cout when it fits one UMMA (<= 256), else 256 / 128 tiles.
   if (a.Cout <= 256) {
     switch (a.Cout) {

@@ -25,10 +25,16 @@ struct ConvArgs {
   int relu;
   int res_mode;          // 0 none, 1 identity [n][Ho][Wo][Cout], 2 option A from [n][rH][rW][rC]
   int rH, rW, rC, r_pad_lo;
+  int dbg = 0;           // experiments only: bit0 skip epilogue math/stores, bit1 skip MMAs, bit2 skip A loads
 };
 // Launch on `stream`; grid is sized for max_rows samples (persistent CTAs loop
 // over the tiles the live count needs).  Returns cudaSuccess or the launch error.
 cudaError_t launch_conv_tc(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream);
+// TMA-fed variant (conv_tma.cu) for layers whose output tiles are rectangular
+// boxes; *handled = false (and nothing launched) when the shape does not qualify.
+cudaError_t launch_conv_tma(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream, bool* handled);
+// Dispatch: path 0 = auto (TMA when possible), 1 = cp.async kernel, 2 = TMA only.
+cudaError_t launch_conv(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream, int path = 0);
 
 // a0: fp32 [n][HW][C] -> bf16 [n][HW][Cp]  (Cp = roundup(C, 8), zero pad)
 cudaError_t launch_cast_pad(const float* in, uint16_t* out, int64_t n, int hw, int c, int cp,

@@ -79,7 +79,7 @@ def lib():
             "dycl_num_classes": [vp, Pi],
             "dycl_set_profiling": [vp, i32],
             "dycl_profile_read": [vp, i32, Pi, Pf, Pd, Pd, Pi],
-            "dycl_debug_conv2d": [vp, i64, i32, i32, i32, P16, Pf, i32, i32, i32, i32, i32, vp, i32, vp, vp],
+            "dycl_debug_conv2d": [vp, i64, i32, i32, i32, P16, Pf, i32, i32, i32, i32, i32, vp, i32, vp, vp, i32],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -235,9 +235,9 @@ def dycl_profile_read(g, max_n=4096):
     return [dict(kind=KIND_NAMES[kind[i]], ms=ms[i], bytes=by[i], flops=fl[i]) for i in range(m)]
 
 
-def dycl_debug_conv2d(g, x, n, H, W, C, w_bf16, bias, c_out, k, stride, pad, relu, res, res_mode, y, stream=None):
+def dycl_debug_conv2d(g, x, n, H, W, C, w_bf16, bias, c_out, k, stride, pad, relu, res, res_mode, y, path=0):
     w, wp = _u16(w_bf16)
     b, bp = _f32(bias)
     _ck(lib().dycl_debug_conv2d(g, int(n), H, W, C, wp, bp, c_out, k, stride, pad, int(relu),
                                 ctypes.c_void_p(res.data_ptr() if res is not None else 0), int(res_mode),
-                                ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr())), g)
+                                ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()), int(path)), g)

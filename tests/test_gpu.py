@@ -53,8 +53,12 @@ CONV_CASES = [
 ]
 
 
-@pytest.mark.parametrize("case", CONV_CASES, ids=[str(c) for c in CONV_CASES])
-def test_conv_kernel_matches_oracle_conv(any_graph, case):
+TMA_CASES = [c for c in CONV_CASES if c[3] in (8, 16, 32, 64) and c[4] in (16, 32, 64, 128, 256)]
+
+
+@pytest.mark.parametrize("path,case", [(1, c) for c in CONV_CASES] + [(2, c) for c in TMA_CASES],
+                         ids=[f"cpasync-{c}" for c in CONV_CASES] + [f"tma-{c}" for c in TMA_CASES])
+def test_conv_kernel_matches_oracle_conv(any_graph, path, case):
     n, H, W, C, Co, k, st, pad, relu, res_mode = case
     rng = np.random.default_rng(abs(hash(case)) % 2**32)
     x = wl.f32_to_bf16_bits(rng.standard_normal((n, H, W, C)))
@@ -68,7 +72,7 @@ def test_conv_kernel_matches_oracle_conv(any_graph, case):
         res = wl.f32_to_bf16_bits(rng.standard_normal((n, 2 * Ho, 2 * Wo, Co // 2)))
     y = torch.zeros((n, Ho, Wo, Co), dtype=torch.int16, device=DEV)
     D.dycl_debug_conv2d(any_graph, _bits_to_t(x), n, H, W, C, w, b, Co, k, st, pad, relu,
-                        _bits_to_t(res) if res is not None else None, res_mode, y)
+                        _bits_to_t(res) if res is not None else None, res_mode, y, path)
     got = _t_to_f64(y)
     xf, wf = prg._bf16_to_f64(x), prg._bf16_to_f64(w)
     for i in range(n):
