@@ -196,11 +196,13 @@ dycl_status dycl_profile_read(dycl_graph g, int32_t max_n, int32_t* kind, float*
 /* ------------------------------------------------------------ test hook ---- */
 /* Run ONE conv2d layer (the a1 tensor-core kernel, same code path dycl_run uses)
  * on caller-owned device buffers and synchronise.  For element-wise kernel tests.
- *   x   : device bf16 [n][H][W][C], C % 8 == 0
+ * bf16 tensors use the library's internal channel-planar layout [n][C/8][H][W][8]
+ * (DESIGN.md §4); the residual-stream fp32 tensors dycl_run keeps are NHWC.
+ *   x   : device bf16 [n][C/8][H][W][8], C % 8 == 0
  *   w   : host bf16 [c_out][k][k][C];  bias: host fp32 [c_out]
- *   res : device bf16 shortcut or NULL; res_mode 0 none, 1 identity [n][Ho][Wo][c_out],
- *         2 option A from [n][2Ho][2Wo][c_out/2]
- *   y   : device bf16 [n][Ho][Wo][c_out]
+ *   res : device bf16 shortcut (channel-planar) or NULL; res_mode 0 none, 1 identity
+ *         [n][c_out/8][Ho][Wo][8], 2 option A from [n][c_out/16][2Ho][2Wo][8]
+ *   y   : device bf16 [n][c_out/8][Ho][Wo][8]
  *   path: 0 = the kernel dycl_run would pick, 1 = cp.async-fed kernel, 2 = TMA-fed kernel
  *         (CUDA error "operation not supported" if the shape does not qualify)
  * g supplies the device (any created graph).  Errors: INVALID_ARG, UNSUPPORTED, CUDA. */

@@ -8,9 +8,8 @@
 //   A[m, k] = x[n][ho*stride - pad + r][wo*stride - pad + s][c]   (0 outside the image)
 //
 // Persistent, warp-specialised CTA (one per SM):
-//   warps 0-3  epilogue: tcgen05.ld TMEM -> regs, +bias, +shortcut (identity or
-//              option A), ReLU, RNE to bf16, 16-byte stores (one output pixel row
-//              of BN channels per thread)
+//   warps 0-3  epilogue: tcgen05.ld TMEM -> regs -> conv_finish16 (bias, shortcut,
+//              ReLU, bf16 channel-planar + fp32 NHWC stores; epilogue.cuh)
 //   warps 4-11 producers: im2col gather of A and the B tile with 16-byte
 //              cp.async (zero-fill implements the padding) into a STAGES-deep ring
 //              laid out in the UMMA 128B-swizzle K-major canonical layout; the
@@ -24,6 +23,7 @@
 // launch serves every batch the host module produces without a host round trip.
 #include <cuda_bf16.h>
 
+#include "epilogue.cuh"
 #include "kernels.h"
 #include "ptx.cuh"
 
@@ -54,12 +54,6 @@ struct Cfg {
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA M=128 needs N%16==0, 16<=N<=256");
 };
 
-__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
-__device__ __forceinline__ float bf16_lo(uint32_t u) { return __uint_as_float(u << 16); }
-__device__ __forceinline__ float bf16_hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
 
 template <int BN>
 __global__ void __launch_bounds__(NUM_THREADS, 1) k_conv_tc(const ConvArgs a) {
@@ -90,15 +84,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_conv_tc(const ConvArgs a) {
   const int ksteps = (a.K + 15) >> 4;
   const int kblocks = (ksteps + 3) >> 2;
 
-  // tap table: chunk j covers k = 8j..8j+7 = tap (r, s), channels c..c+7.
-  //   .x = element offset (r*W + s)*C + c from the window origin, .y = (r << 16) | s,
-  //   .y = -1 marks chunks beyond K (zero-filled).
+  // tap table: chunk j covers k = 8j..8j+7 = tap (r, s), channels c..c+7 = plane c/8
+  // of the channel-planar input [n][C/8][H][W][8].
+  //   .x = element offset (c/8)*H*W*8 + (r*W + s)*8 from the window origin,
+  //   .y = (r << 16) | s;  .y = -1 marks chunks beyond K (zero-filled).
   for (int j = threadIdx.x; j < a.Kp / 8 && j < MAX_KCH; j += blockDim.x) {
     const int k = j * 8;
     if (k < a.K) {
       const int tap = k / a.C, c = k - (k / a.C) * a.C;
       const int r = tap / a.ksz, s2 = tap - (tap / a.ksz) * a.ksz;
-      tap_tab[j] = make_int2((r * a.W + s2) * a.C + c, (r << 16) | s2);
+      tap_tab[j] = make_int2((c >> 3) * a.H * a.W * 8 + (r * a.W + s2) * 8, (r << 16) | s2);
     } else {
       tap_tab[j] = make_int2(0, -1);
     }
@@ -145,7 +140,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_conv_tc(const ConvArgs a) {
       const int hi0 = ho * a.stride - a.pad;
       const int wi0 = wo * a.stride - a.pad;
       // window origin (may point before the sample for padded rows; only used when in bounds)
-      const long long base = ((long long)n * a.H * a.W + (long long)hi0 * a.W + wi0) * a.C;
+      const long long base = (long long)n * a.H * a.W * a.C + ((long long)hi0 * a.W + wi0) * 8;
       const uint16_t* wt = a.w + (size_t)n_tile * BN * a.Kp;
       for (int kb = 0; kb < kblocks; ++kb) {
         ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1);
@@ -241,14 +236,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_conv_tc(const ConvArgs a) {
       ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
       ptx::tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * BN);
-      size_t rbase = 0;               // element offset of this row's shortcut pixel
-      if (ok && a.res_mode == 1) {
-        rbase = (size_t)m * a.Cout;
-      } else if (ok && a.res_mode == 2) {
-        const int n = (int)(m / HoWo);
+      int n = 0, ho = 0, wo = 0;
+      if (ok) {
+        n = (int)(m / HoWo);
         const int p = (int)(m - (long long)n * HoWo);
-        const int ho = p / a.Wo, wo = p - (p / a.Wo) * a.Wo;
-        rbase = (((size_t)n * a.rH + 2 * ho) * a.rW + 2 * wo) * a.rC;
+        ho = p / a.Wo;
+        wo = p - ho * a.Wo;
       }
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 16) {
@@ -256,57 +249,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_conv_tc(const ConvArgs a) {
         ptx::tmem_ld_32x32b_x16(taddr + (uint32_t)c0, v);
         ptx::tmem_ld_wait();
         if (ok) {
-          const int o0 = n_tile * BN + c0;
           float f[16];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v[j]) + __ldg(a.bias + o0 + j);
-          if (a.res_mode == 1) {
-            if (a.res32) {
-              const float4* rp = reinterpret_cast<const float4*>(a.res32 + rbase + o0);
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const float4 r = __ldg(rp + j);
-                f[4 * j] += r.x; f[4 * j + 1] += r.y; f[4 * j + 2] += r.z; f[4 * j + 3] += r.w;
-              }
-            } else {
-              const uint4* rp = reinterpret_cast<const uint4*>(a.res + rbase + o0);
-              const uint4 r0 = __ldg(rp), r1 = __ldg(rp + 1);
-              const uint32_t rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                f[2 * j] += bf16_lo(rr[j]);
-                f[2 * j + 1] += bf16_hi(rr[j]);
-              }
-            }
-          } else if (a.res_mode == 2) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int ci = o0 + j - a.r_pad_lo;
-              if (ci >= 0 && ci < a.rC)
-                f[j] += a.res32 ? __ldg(a.res32 + rbase + ci) : __uint_as_float((uint32_t)a.res[rbase + ci] << 16);
-            }
-          }
-          if (a.relu) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.0f);
-          }
-          uint4 o0v, o1v;
-          o0v.x = pack_bf16x2(f[0], f[1]);
-          o0v.y = pack_bf16x2(f[2], f[3]);
-          o0v.z = pack_bf16x2(f[4], f[5]);
-          o0v.w = pack_bf16x2(f[6], f[7]);
-          o1v.x = pack_bf16x2(f[8], f[9]);
-          o1v.y = pack_bf16x2(f[10], f[11]);
-          o1v.z = pack_bf16x2(f[12], f[13]);
-          o1v.w = pack_bf16x2(f[14], f[15]);
-          uint4* yp = reinterpret_cast<uint4*>(a.y + (size_t)m * a.Cout + o0);
-          yp[0] = o0v;
-          yp[1] = o1v;
-          if (a.y32) {
-            float4* yq = reinterpret_cast<float4*>(a.y32 + (size_t)m * a.Cout + o0);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) yq[j] = make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
-          }
+          for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v[j]);
+          conv_finish16(a, n, ho, wo, n_tile * BN + c0, f);
         }
       }
       ptx::tc_fence_before();

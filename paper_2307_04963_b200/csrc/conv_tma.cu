@@ -1,28 +1,33 @@
-// TMA-fed implicit-GEMM convolution / dense layer on tcgen05 (sm_100a) -- the
-// fast path of SURVEY §8(a) a1 for every layer whose output rows tile as
-// rectangular boxes (all CIFAR ResNet / MLP layers).
+// TMA-fed implicit-GEMM convolution / dense layer on tcgen05 (sm_100a): the fast
+// path of SURVEY §8(a) a1 for layers whose output tiles are rectangular boxes.
 //
 //   D[m, o] = sum_k A[m, k] B[o, k],  m = output pixel, k = (tap r,s ; channel c)
 //
-// Implicit GEMM without an im2col buffer: for a tile of output pixels that forms a
-// box (bn samples x bh output rows x Wo columns, <= 128 rows) the A operand of one
-// filter tap (r, s) is itself a 4-D box of the NHWC input
-//     x[n0 .. n0+bn)[ho0*st-pad+r :: st][-pad+s :: st][c0 .. c0+CW)
-// which ONE TMA instruction fetches (negative / past-the-end coordinates are
-// zero-filled by the TMA unit: that is the convolution's zero padding; the
-// traversal stride implements stride 2).  The box lands as 128 K-major rows of
-// CW channels in the UMMA canonical layout whose swizzle equals the row width
-// (32/64/128 B), so each TMA box feeds CW/16 tcgen05.mma K-steps directly.
+// Operands live in SMEM in the UMMA K-major no-swizzle ("interleaved") layout:
+// 8 rows x 16 bytes core matrices, consecutive rows 16 B apart (SBO = 128 B), K
+// chunks of 8 channels one "plane" apart (LBO = plane bytes).  Activations are
+// stored channel-planar in HBM ([n][C/8][H][W][8]), so one TMA box row is a whole
+// image row of one 8-channel plane (512 B at 32x32) and the box lands in SMEM
+// already in that layout -- no im2col buffer, no re-layout:
 //
-// Warp roles (persistent CTA per SM, 6 warps):
-//   warps 0-3  epilogue: tcgen05.ld -> +bias, +shortcut (identity / option A,
-//              bf16 or fp32 residual stream), ReLU, RNE->bf16 (+ fp32 copy)
-//   warp  4    TMA producer (one elected lane): weights once (resident in smem),
-//              then one A box per (tile, tap, channel chunk) into a deep ring
-//   warp  5    TMEM allocator + MMA issuer (one lane), double-buffered accumulator
+//   halo mode (stride 1, one sample per tile): per super-tile and per filter
+//     column s, ONE box of (MT*bh + k - 1) input rows shifted by s-pad pixels
+//     (out-of-range coordinates are zero-filled by the TMA unit = the conv's
+//     zero padding).  Filter row r is then just a descriptor offset of r image
+//     rows, so the k*k taps cost k boxes instead of k*k (3.4x fewer L2->SMEM
+//     bytes than per-tap im2col for 3x3 at MT*bh = 16).
+//   tap mode (several samples per tile, or stride 2): one box per tap.
+//
+// A super-tile = MT UMMA tiles of 128 rows; the host builds the per-tile TMA box
+// list and tcgen05.mma list once (TmaPlan, kernel parameter), so the producer and
+// MMA threads only loop over tables.  Warp roles (persistent CTA per SM, 10 warps):
+//   warps 0-7  two epilogue warpgroups, alternating super-tiles (4 TMEM accumulators)
+//   warp  8    TMA producer (one lane): resident weights once, then the A ring
+//   warp  9    TMEM allocator + MMA issuer (one lane)
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include "epilogue.cuh"
 #include "kernels.h"
 #include "ptx.cuh"
 
@@ -30,132 +35,166 @@ namespace dycl {
 namespace {
 
 constexpr int BM = 128;
-constexpr int THREADS = 192;
-constexpr int SMEM_BUDGET = 200 * 1024;
+constexpr int THREADS = 320;
+constexpr int PRODUCER_WARP = 8;
+constexpr int MMA_WARP = 9;
+constexpr int NACC = 4;
+constexpr int SMEM_BUDGET = 210 * 1024;
+constexpr int MAX_KS = 16;
+constexpr int MAX_BOX = 80;
+constexpr int MAX_MMA = 288;
 
-// K is cut into "units": one (tap, channel chunk) = one TMA box of CW channels.
-// A ring stage holds U units (amortising the per-stage mbarrier handshakes over
-// several taps); a tile takes nks = ceil(nunits / U) stages.
-struct TmaGeom {
-  int CW;            // channels per unit (box inner dimension)
-  int cchunks;       // C / CW
-  int nunits;        // ksz*ksz*cchunks (even for C == 8: phantom zero unit appended)
-  int U;             // units per ring stage
-  int nks;           // ring stages per tile
-  int layout;        // UMMA layout code (0 none, 2/4/6 = 128/64/32-byte swizzle)
-  int row_bytes;     // bytes of one row of a unit (CW * 2)
-  int unit_bytes;    // A smem per unit: 128 rows
-  int b_unit_bytes;  // B smem per unit: BN rows
-  int bn, bh, rows;  // tile box: samples x output rows; rows = bn*bh*Wo
+struct BoxOp {
+  int map;         // 0: fused-row map (stride 1), 1: unfused map (any stride)
+  int dst;         // byte offset in the stage
+  int dx, dh, dn;  // coordinate deltas (dx in fused elements or pixels, dh rows, dn samples)
+};
+struct MmaOp {
+  int j;           // UMMA tile within the super-tile
+  uint32_t a_off;  // byte offset in the stage
+  uint32_t b_off;  // byte offset in the resident weights (n-tile 0)
+  int acc;         // accumulate (0 for the first K step of tile j)
 };
 
-__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
-
-struct TmaParams {
+struct TmaPlan {
   ConvArgs a;
-  TmaGeom g;
-  int stages;
-  int tiles_per_img_group;   // tiles covering one group of bn samples
+  int mode;                 // 0 halo, 1 tap
+  int MT, bn, bh;           // super-tile = MT UMMA tiles; UMMA tile = bn samples x bh rows x Wo
+  int sub_rows;             // valid rows of one UMMA tile (bn*bh*Wo)
+  int tiles_per_group;      // super-tiles per group of samples
+  int samples_per_group;    // bn*MT (tap mode) or 1 (halo mode)
+  int rows_per_super;       // output rows (ho) covered by one super-tile (bn == 1)
+  int nks, S, stage_bytes;
+  int a_lbo;                // bytes between consecutive 8-channel planes of a stage
+  int shift_bytes;          // halo mode: bytes between the k W-shifted boxes
+  int kchunks;              // UMMA K steps per tap (C/16; 0 when C == 8)
+  int U, ntap;              // tap mode: taps per stage, taps incl. the C == 8 phantom
+  int res_bytes;            // residual prefetch buffer bytes per super-tile (0: no prefetch)
+  int b_bytes;              // resident weight bytes per N tile
+  int b_chunks;             // Kp / 8
+  int box_begin[MAX_KS + 1];
+  int mma_begin[MAX_KS + 1];
+  uint32_t stage_tx[MAX_KS];
+  BoxOp box[MAX_BOX];
+  MmaOp mma[MAX_MMA];
 };
 
-template <int BN>
+template <int BN, int KCH>
 __global__ void __launch_bounds__(THREADS, 1)
-    k_conv_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TmaParams P) {
+    k_conv_tma(const __grid_constant__ CUtensorMap tmF, const __grid_constant__ CUtensorMap tmU,
+               const __grid_constant__ CUtensorMap tmB, const __grid_constant__ TmaPlan P) {
   const ConvArgs& a = P.a;
-  const TmaGeom& G = P.g;
-  const int S = P.stages;
+  const int S = P.S;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int n_tiles = a.Cout / BN;
-  uint8_t* sB = smem;                                         // resident weights [n_tiles][nunits][BN rows]
-  const int b_total = (G.nunits * G.b_unit_bytes * n_tiles + 1023) & ~1023;
-  const int a_stage_bytes = G.U * G.unit_bytes;
-  uint8_t* sA = smem + b_total;                               // ring: S stages x U units
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + S * a_stage_bytes);
+  uint8_t* sB = smem;
+  const int b_total = (P.b_bytes * n_tiles + 1023) & ~1023;
+  uint8_t* sA = smem + b_total;
+  float* sRes = reinterpret_cast<float*>(sA + S * P.stage_bytes);            // [2][res_bytes]
+  float* sBias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(sRes) + 2 * P.res_bytes);   // [Cout]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sBias + ((a.Cout + 3) & ~3));
   const uint32_t full0 = ptx::smem_u32(bars);
   const uint32_t empty0 = full0 + 8 * S;
   const uint32_t tfull0 = empty0 + 8 * S;
-  const uint32_t tempty0 = tfull0 + 16;
-  const uint32_t bfull = tempty0 + 16;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 5);
+  const uint32_t tempty0 = tfull0 + 8 * NACC;
+  const uint32_t bfull = tempty0 + 8 * NACC;
+  const uint32_t rfull0 = bfull + 8;          // residual buffer g filled (g = it & 1)
+  const uint32_t rempty0 = rfull0 + 16;       // residual buffer g consumed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 2 * NACC + 5);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_live = a.n_live ? *a.n_live : a.n_static;
-  const int groups = (n_live + G.bn - 1) / G.bn;             // sample groups of bn
-  const int m_tiles = groups * P.tiles_per_img_group;
+  const int groups = (n_live + P.samples_per_group - 1) / P.samples_per_group;
+  const int m_tiles = groups * P.tiles_per_group;
   const int num_tiles = m_tiles * n_tiles;
-  constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
+  const int acc_cols = P.MT * BN;                // NACC * acc_cols <= 512 (host-checked)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
       ptx::mbar_init(full0 + 8 * i, 1);
       ptx::mbar_init(empty0 + 8 * i, 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NACC; ++i) {
       ptx::mbar_init(tfull0 + 8 * i, 1);
       ptx::mbar_init(tempty0 + 8 * i, 128);
     }
     ptx::mbar_init(bfull, 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(rfull0 + 8 * i, 1);
+      ptx::mbar_init(rempty0 + 8 * i, 128);
+    }
     ptx::fence_mbar_init();
   }
-  if (warp == 5) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), TMEM_COLS);
+  for (int i = threadIdx.x; i < a.Cout; i += blockDim.x) sBias[i] = a.bias[i];
+  if (warp == MMA_WARP) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), 512);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int taps = a.ksz * a.ksz;
-  if (warp == 4) {
+  if (warp == PRODUCER_WARP) {
     // ---------------------------------------------------------------- TMA producer
     if (lane == 0) {
-      ptx::tma_prefetch_desc(&tmA);
+      ptx::tma_prefetch_desc(&tmF);
+      ptx::tma_prefetch_desc(&tmU);
       ptx::tma_prefetch_desc(&tmB);
-      // Weights of every unit of every N tile: resident for the whole persistent loop.
-      ptx::mbar_arrive_expect_tx(bfull, (uint32_t)(G.nunits * G.b_unit_bytes * n_tiles));
+      // weights, resident for the whole persistent loop: [n_tile][K chunk][BN rows][16 B]
+      ptx::mbar_arrive_expect_tx(bfull, (uint32_t)(P.b_bytes * n_tiles));
       for (int nt = 0; nt < n_tiles; ++nt)
-        for (int u = 0; u < G.nunits; ++u) {
-          const uint32_t dst = ptx::smem_u32(sB + (nt * G.nunits + u) * G.b_unit_bytes);
-          const int tap = u / G.cchunks, cc = u - tap * G.cchunks;
-          ptx::tma_load_2d(dst, &tmB, bfull, tap * a.C + cc * G.CW, nt * BN);   // phantom tap: zero weights
+        for (int c0 = 0; c0 < P.b_chunks; c0 += 256) {
+          const uint32_t dst = ptx::smem_u32(sB + nt * P.b_bytes + c0 * BN * 16);
+          asm volatile(
+              "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+              "%5}], [%2];" ::"r"(dst),
+              "l"(&tmB), "r"(bfull), "r"(0), "r"(nt * BN), "r"(c0)
+              : "memory");
         }
-      const uint32_t unit_tx = (uint32_t)(G.rows * G.row_bytes);
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      int itp = 0;
+      const int HoWo = a.Ho * a.Wo;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++itp) {
         const int m_tile = tile / n_tiles;
-        const int grp = m_tile / P.tiles_per_img_group;
-        const int ho0 = (m_tile - grp * P.tiles_per_img_group) * G.bh;
-        const int n0 = grp * G.bn;
-        const int h0 = ho0 * a.stride - a.pad;
-        const int w0 = -a.pad;
-        int r = 0, sc = 0, cc = 0, tap = 0;     // running (tap row, tap col, channel chunk)
-        for (int ks = 0; ks < G.nks; ++ks) {
-          const int nu = min(G.U, G.nunits - ks * G.U);
+        const int grp = m_tile / P.tiles_per_group;
+        const int ho0 = (m_tile - grp * P.tiles_per_group) * P.rows_per_super;
+        const int n0 = grp * P.samples_per_group;
+        const int h_org = ho0 * a.stride - a.pad;
+        if (P.res_bytes) {
+          // identity shortcut rows of this super-tile: one contiguous fp32 NHWC range
+          const int g = itp & 1;
+          ptx::mbar_wait(rempty0 + 8 * g, ((itp >> 1) & 1) ^ 1);
+          const long long pix0 = (long long)n0 * HoWo + (long long)ho0 * a.Wo;
+          long long npix = P.bn == 1 ? (long long)P.rows_per_super * a.Wo
+                                     : (long long)min(P.samples_per_group, n_live - n0) * HoWo;
+          const uint32_t bytes = (uint32_t)(npix * a.Cout * 4);
+          ptx::mbar_arrive_expect_tx(rfull0 + 8 * g, bytes);
+          ptx::bulk_load(ptx::smem_u32(reinterpret_cast<uint8_t*>(sRes) + g * P.res_bytes),
+                         a.res32 + pix0 * a.Cout, bytes, rfull0 + 8 * g);
+        }
+        for (int ks = 0; ks < P.nks; ++ks) {
           ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const uint32_t bar = full0 + 8 * stage;
           if (a.dbg & 4) {
             ptx::mbar_arrive(bar);
-            if (++stage == S) {
-              stage = 0;
-              phase ^= 1;
-            }
-            continue;
-          }
-          ptx::mbar_arrive_expect_tx(bar, unit_tx * (uint32_t)nu);
-          uint32_t dst = ptx::smem_u32(sA + stage * a_stage_bytes);
-          for (int u = 0; u < nu; ++u, dst += G.unit_bytes) {
-            // phantom tap (C == 8 padding to an even unit count): fully out of range -> zeros
-            const int hh = tap < taps ? h0 + r : -(1 << 20);
-            ptx::tma_load_4d(dst, &tmA, bar, cc * G.CW, w0 + sc, hh, n0);
-            if (++cc == G.cchunks) {
-              cc = 0;
-              ++tap;
-              if (++sc == a.ksz) {
-                sc = 0;
-                ++r;
+          } else {
+            ptx::mbar_arrive_expect_tx(bar, P.stage_tx[ks]);
+            const uint32_t base = ptx::smem_u32(sA + stage * P.stage_bytes);
+            for (int b = P.box_begin[ks]; b < P.box_begin[ks + 1]; ++b) {
+              const BoxOp& o = P.box[b];
+              if (o.map == 0) {
+                // fused-row map {W*8, H, N, P}: all planes of the box in one instruction
+                asm volatile(
+                    "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, "
+                    "{%3, %4, %5, %6}], [%2];" ::"r"(base + o.dst),
+                    "l"(&tmF), "r"(bar), "r"(o.dx), "r"(h_org + o.dh), "r"(n0 + o.dn), "r"(0)
+                    : "memory");
+              } else {
+                asm volatile(
+                    "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, "
+                    "{%3, %4, %5, %6, %7}], [%2];" ::"r"(base + o.dst),
+                    "l"(&tmU), "r"(bar), "r"(0), "r"(o.dx), "r"(h_org + o.dh), "r"(n0 + o.dn), "r"(0)
+                    : "memory");
               }
             }
           }
@@ -166,149 +205,146 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == MMA_WARP) {
     // ---------------------------------------------------------------- MMA issuer
     const uint32_t IDESC = ptx::make_idesc_bf16(BM, BN);
-    const bool pair = G.CW == 8;                               // 16-byte rows: a K-step spans two units
-    const int ksteps_unit = pair ? 1 : G.CW / 16;
-    const uint32_t a_sbo = pair ? 128u : (uint32_t)(8 * G.row_bytes);
-    const uint32_t a_lbo = pair ? (uint32_t)G.unit_bytes : 16u;
-    const uint32_t b_lbo = pair ? (uint32_t)G.b_unit_bytes : 16u;
-    const uint64_t adesc0 = ptx::make_smem_desc(ptx::smem_u32(sA), G.layout, a_lbo, a_sbo);
-    const uint64_t bdesc0 = ptx::make_smem_desc(ptx::smem_u32(sB), G.layout, b_lbo, a_sbo);
     ptx::mbar_wait(bfull, 0);
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
+    const uint32_t sA0 = ptx::smem_u32(sA), sB0 = ptx::smem_u32(sB);
+    const uint64_t adesc0 = ptx::make_smem_desc(sA0, 0, (uint32_t)P.a_lbo, 128u);
+    const uint64_t bdesc0 = ptx::make_smem_desc(sB0, 0, (uint32_t)(BN * 16), 128u);
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
+      const int acc = it % NACC;
+      const uint32_t acc_phase = (it / NACC) & 1;
       const int n_tile = tile % n_tiles;
       ptx::mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
       ptx::tc_fence_after();
-      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-      uint32_t b_off = (uint32_t)(n_tile * G.nunits * G.b_unit_bytes);
-      for (int ks = 0; ks < G.nks; ++ks) {
-        const int nu = min(G.U, G.nunits - ks * G.U);
+      const uint32_t d_base = tmem_base + (uint32_t)(acc * acc_cols);
+      const uint32_t b_nt = (uint32_t)(n_tile * P.b_bytes);
+      for (int ks = 0; ks < P.nks; ++ks) {
         ptx::mbar_wait(full0 + 8 * stage, phase);
         ptx::tc_fence_after();
-        if (lane == 0) {
-          uint32_t a_off = (uint32_t)(stage * a_stage_bytes);
-          const int step_units = pair ? 2 : 1;
-          for (int u = 0; u < nu && !(a.dbg & 2); u += step_units) {
-            for (int j = 0; j < ksteps_unit; ++j) {
-              ptx::mma_bf16_ss(d_tmem, adesc0 + ((a_off + 32 * j) >> 4), bdesc0 + ((b_off + 32 * j) >> 4), IDESC,
-                               (ks | u | j) != 0);
+        if (!(a.dbg & 2)) {
+          // Warp-uniform, compile-time-unrolled issue: descriptor offsets stay in
+          // uniform registers, one elected lane issues each tcgen05.mma.
+          const uint64_t ad0 = adesc0 + ((uint32_t)(stage * P.stage_bytes) >> 4);
+          const uint64_t bd0 = bdesc0 + (b_nt >> 4);
+          const uint32_t plane16 = (uint32_t)P.a_lbo >> 4;            // 16-byte units
+          const uint32_t tapb16 = (uint32_t)((a.C / 8) * BN);        // weights per tap, 16-byte units
+          if (P.mode == 0) {
+            // halo (3x3): tap (r, s) of tile j = shift block s, image rows (j*bh + r)
+            const uint32_t shift16 = (uint32_t)P.shift_bytes >> 4;
+            const uint32_t row16 = (uint32_t)a.W;                      // W*16 bytes
+            for (int j = 0; j < P.MT; ++j) {
+              const uint32_t dj = d_base + (uint32_t)(j * BN);
+              const uint64_t aj = ad0 + (uint32_t)(j * P.bh) * row16;
+#pragma unroll
+              for (int t = 0; t < 9; ++t) {
+                const uint32_t ao = (uint32_t)(t % 3) * shift16 + (uint32_t)(t / 3) * row16;
+#pragma unroll
+                for (int q = 0; q < KCH; ++q)
+                  ptx::mma_bf16_ss_elect(dj, aj + ao + 2 * q * plane16, bd0 + t * tapb16 + (uint32_t)(2 * q * BN),
+                                         IDESC, (uint32_t)((t | q) != 0));
+              }
             }
-            a_off += step_units * G.unit_bytes;
-            b_off += step_units * G.b_unit_bytes;
+          } else {
+            // tap: taps [t0, t1) of this stage, one box each
+            const int t0 = ks * P.U;
+            const int t1 = min(t0 + P.U, P.ntap);
+            const uint32_t tap16 = (uint32_t)(a.C / 8) * plane16;
+            const uint32_t sub16 = (uint32_t)P.sub_rows;               // sub_rows*16 bytes
+            for (int j = 0; j < P.MT; ++j) {
+              const uint32_t dj = d_base + (uint32_t)(j * BN);
+              uint64_t at = ad0 + (uint32_t)j * sub16;
+              uint64_t bt = bd0 + (uint32_t)t0 * tapb16;
+              if (KCH == 0) {                       // C == 8: K step = a pair of taps (LBO = one tap)
+                for (int t = t0; t < t1; t += 2, at += 2 * tap16, bt += 2 * tapb16)
+                  ptx::mma_bf16_ss_elect(dj, at, bt, IDESC, (uint32_t)(t != 0));
+              } else {
+                for (int t = t0; t < t1; ++t, at += tap16, bt += tapb16) {
+#pragma unroll
+                  for (int q = 0; q < KCH; ++q)
+                    ptx::mma_bf16_ss_elect(dj, at + 2 * q * plane16, bt + (uint32_t)(2 * q * BN), IDESC,
+                                           (uint32_t)((t | q) != 0));
+                }
+              }
+            }
           }
-          ptx::mma_commit(empty0 + 8 * stage);
         }
-        if (lane != 0) b_off += (uint32_t)(nu * G.b_unit_bytes);
+        ptx::mma_commit_elect(empty0 + 8 * stage);
         __syncwarp();
         if (++stage == S) {
           stage = 0;
           phase ^= 1;
         }
       }
-      if (lane == 0) ptx::mma_commit(tfull0 + 8 * acc);
+      ptx::mma_commit_elect(tfull0 + 8 * acc);
       __syncwarp();
     }
   } else {
     // ---------------------------------------------------------------- epilogue
-    const int row = warp * 32 + lane;
-    const int img_rows = G.bh * a.Wo;                          // rows of one sample inside the tile box
+    const int wg = warp >> 2;                      // epilogue warpgroup 0 / 1
+    const int quad = warp & 3;                     // TMEM lane quadrant of this warp
+    const int r = quad * 32 + lane;                // row inside each UMMA tile
     const int HoWo = a.Ho * a.Wo;
     int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
+      if ((it & 1) != wg) continue;
+      const int acc = it % NACC;
+      const uint32_t acc_phase = (it / NACC) & 1;
       const int m_tile = tile / n_tiles;
       const int n_tile = tile - m_tile * n_tiles;
-      const int grp = m_tile / P.tiles_per_img_group;
-      const int ho0 = (m_tile - grp * P.tiles_per_img_group) * G.bh;
-      const int nn = row / img_rows;
-      const int rr = row - nn * img_rows;
-      const int n = grp * G.bn + nn;
-      const int ho = ho0 + rr / a.Wo;
-      const int wo = rr - (rr / a.Wo) * a.Wo;
-      const bool ok = row < G.rows && n < n_live && ho < a.Ho;
-      const size_t m = (size_t)n * HoWo + (size_t)ho * a.Wo + wo;   // output pixel (row of y)
+      const int grp = m_tile / P.tiles_per_group;
+      const int ho0 = (m_tile - grp * P.tiles_per_group) * P.rows_per_super;
+      const int n0 = grp * P.samples_per_group;
+      const float* res_tile = nullptr;
+      if (P.res_bytes) {
+        ptx::mbar_wait(rfull0 + 8 * wg, (it >> 1) & 1);        // tile it uses residual buffer it & 1 == wg
+        res_tile = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(sRes) + wg * P.res_bytes);
+      }
       ptx::mbar_wait(tfull0 + 8 * acc, acc_phase);
       ptx::tc_fence_after();
-      const uint32_t taddr = tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * BN);
-      size_t rbase = 0;
-      if (a.res_mode == 1) rbase = m * a.Cout;
-      else if (a.res_mode == 2) rbase = (((size_t)n * a.rH + 2 * ho) * a.rW + 2 * wo) * a.rC;
+      const uint32_t t_base = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * acc_cols);
+      for (int j = 0; j < P.MT; ++j) {
+        int n, ho, wo;
+        if (P.bn == 1) {
+          n = n0;
+          ho = ho0 + j * P.bh + r / a.Wo;
+          wo = r % a.Wo;
+        } else {
+          const int nn = r / HoWo, p = r - (r / HoWo) * HoWo;
+          n = n0 + j * P.bn + nn;
+          ho = p / a.Wo;
+          wo = p - ho * a.Wo;
+        }
+        const bool ok = r < P.sub_rows && n < n_live && ho < a.Ho;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t v[16];
-        ptx::tmem_ld_32x32b_x16(taddr + (uint32_t)c0, v);
-        ptx::tmem_ld_wait();
-        if (ok && !(a.dbg & 1)) {
-          const int o0 = n_tile * BN + c0;
-          float f[16];
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          uint32_t v[16];
+          ptx::tmem_ld_32x32b_x16(t_base + (uint32_t)(j * BN + c0), v);
+          ptx::tmem_ld_wait();
+          if (ok && !(a.dbg & 1)) {
+            float f[16];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v[j]) + __ldg(a.bias + o0 + j);
-          if (a.res_mode == 1) {
-            if (a.res32) {
-              const float4* rp = reinterpret_cast<const float4*>(a.res32 + rbase + o0);
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const float4 q = __ldg(rp + j);
-                f[4 * j] += q.x; f[4 * j + 1] += q.y; f[4 * j + 2] += q.z; f[4 * j + 3] += q.w;
-              }
-            } else {
-              const uint4* rp = reinterpret_cast<const uint4*>(a.res + rbase + o0);
-              const uint4 r0 = __ldg(rp), r1 = __ldg(rp + 1);
-              const uint32_t u[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                f[2 * j] += __uint_as_float(u[j] << 16);
-                f[2 * j + 1] += __uint_as_float(u[j] & 0xFFFF0000u);
-              }
-            }
-          } else if (a.res_mode == 2) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int ci = o0 + j - a.r_pad_lo;
-              if (ci >= 0 && ci < a.rC)
-                f[j] += a.res32 ? __ldg(a.res32 + rbase + ci) : __uint_as_float((uint32_t)a.res[rbase + ci] << 16);
-            }
-          }
-          if (a.relu) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.0f);
-          }
-          uint4 o0v, o1v;
-          o0v.x = pack_bf16x2(f[0], f[1]);
-          o0v.y = pack_bf16x2(f[2], f[3]);
-          o0v.z = pack_bf16x2(f[4], f[5]);
-          o0v.w = pack_bf16x2(f[6], f[7]);
-          o1v.x = pack_bf16x2(f[8], f[9]);
-          o1v.y = pack_bf16x2(f[10], f[11]);
-          o1v.z = pack_bf16x2(f[12], f[13]);
-          o1v.w = pack_bf16x2(f[14], f[15]);
-          uint4* yp = reinterpret_cast<uint4*>(a.y + m * a.Cout + o0);
-          yp[0] = o0v;
-          yp[1] = o1v;
-          if (a.y32) {
-            float4* yq = reinterpret_cast<float4*>(a.y32 + m * a.Cout + o0);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) yq[j] = make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
+            for (int q = 0; q < 16; ++q) f[q] = __uint_as_float(v[q]);
+            // pixel index inside the super-tile's residual rows
+            const float* rs = res_tile ? res_tile + (size_t)(j * P.sub_rows + r) * a.Cout + c0 : nullptr;
+            conv_finish16(a, n, ho, wo, n_tile * BN + c0, f, sBias, rs);
           }
         }
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(tempty0 + 8 * acc);
+      if (P.res_bytes) ptx::mbar_arrive(rempty0 + 8 * wg);
     }
   }
 
   __syncthreads();
-  if (warp == 5) {
+  if (warp == MMA_WARP) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+    ptx::tmem_dealloc(tmem_base, 512);
   }
 }
 
@@ -329,104 +365,253 @@ EncodeTiledFn get_encode() {
   return fn;
 }
 
-bool plan_geom(const ConvArgs& a, int BN, TmaGeom* g, int* stages, int* tiles_per_group) {
-  if (a.Wo * a.stride > 256 || a.Wo > BM) return false;
-  if (a.C == 8 || a.C == 16 || a.C == 32 || a.C == 64) g->CW = a.C;
-  else if (a.C % 64 == 0) g->CW = 64;
-  else return false;
-  g->cchunks = a.C / g->CW;
-  g->row_bytes = g->CW * 2;
-  g->layout = g->row_bytes == 16 ? 0 : g->row_bytes == 32 ? 6 : g->row_bytes == 64 ? 4 : 2;
-  g->nunits = a.ksz * a.ksz * g->cchunks;
-  if (g->CW == 8 && (g->nunits & 1)) g->nunits += 1;       // pair units into 16-element K steps
-  if (g->nunits * g->CW > a.Kp) return false;
-  g->unit_bytes = BM * g->row_bytes;
-  g->b_unit_bytes = BN * g->row_bytes;
+// Build the per-super-tile TMA box list and MMA list.  Returns false if the
+// layer does not fit this kernel (caller falls back to the cp.async kernel).
+bool build_plan(const ConvArgs& a, int BN, TmaPlan* P) {
+  const int C = a.C, Pn = C / 8, k = a.ksz, taps = k * k;
+  if (C % 8 || a.Cout % BN || Pn > 256) return false;
+  if (C != 8 && C != 16 && C != 32 && C != 64 && C != 128) return false;   // KCH instantiations
   const int HoWo = a.Ho * a.Wo;
+  int bn, bh;                                       // UMMA tile box
   if (HoWo >= BM) {
-    g->bn = 1;
-    g->bh = BM / a.Wo;
-    if (g->bh > a.Ho) g->bh = a.Ho;
-    *tiles_per_group = (a.Ho + g->bh - 1) / g->bh;
+    bn = 1;
+    bh = BM / a.Wo;
+    if (bh < 1) return false;
+    if (bh > a.Ho) bh = a.Ho;
   } else {
-    g->bh = a.Ho;
-    g->bn = BM / HoWo;
-    if (g->bn > 256) g->bn = 256;
-    *tiles_per_group = 1;
+    bh = a.Ho;
+    bn = BM / HoWo;
   }
-  if (g->bh * a.stride > 256) return false;
-  g->rows = g->bn * g->bh * a.Wo;
+  const int sub_rows = bn * bh * a.Wo;
+  const bool fused_ok = a.stride == 1 && a.W * 8 <= 256 && a.Wo == a.W;
+  const bool halo = fused_ok && bn == 1 && k == 3 && a.pad == 1 && C >= 16;
+  const int kchunks = C / 16;                        // UMMA K steps per tap (C == 8: pairs of taps)
+  const int b_chunks = a.Kp / 8;
+  const int b_bytes = b_chunks * BN * 16;
   const int n_tiles = a.Cout / BN;
-  const int b_total = (g->nunits * g->b_unit_bytes * n_tiles + 1023) & ~1023;
-  const int avail = SMEM_BUDGET - b_total - 512;
-  // units per stage: up to ~48 KB of A per stage, at least 3 stages in the ring
-  int U = (48 * 1024) / g->unit_bytes;
-  if (U > g->nunits) U = g->nunits;
-  if (g->CW == 8 && (U & 1)) U -= 1;
-  if (U < 1) U = 1;
-  while (U > (g->CW == 8 ? 2 : 1) && avail / (U * g->unit_bytes) < 3) U -= (g->CW == 8 ? 2 : 1);
-  g->U = U;
-  g->nks = (g->nunits + U - 1) / U;
-  int s = avail / (U * g->unit_bytes);
-  if (s > 8) s = 8;
-  if (s < 2) return false;
-  *stages = s;
+  const int b_total = (b_bytes * n_tiles + 1023) & ~1023;
+  if (b_total > 120 * 1024) return false;            // resident-weight design (large layers: fallback)
+  // identity-shortcut prefetch (fp32 stream, single N tile): 2 buffers of one super-tile of rows
+  const bool res_pf = a.res_mode == 1 && a.res32 != nullptr && n_tiles == 1 && (a.dbg & 8) == 0;
+  const int budget = SMEM_BUDGET - b_total - 1024 - ((a.Cout + 3) & ~3) * 4;
+  const int ntap = taps + ((C == 8 && (taps & 1)) ? 1 : 0);
+  const int ustep = C == 8 ? 2 : 1;
+  int MT = 0, stage_bytes = 0, U = 0;
+  for (int mt = (512 / (NACC * BN) < 8 ? 512 / (NACC * BN) : 8); mt >= 1; --mt) {
+    if (bn == 1 && (mt * bh > a.Ho || a.Ho % (mt * bh) != 0)) continue;
+    if (bn > 1 && mt * bn > 256) continue;
+    int sb, u = 0;
+    if (halo) {
+      sb = k * Pn * (mt * bh + k - 1) * a.W * 16;
+      if (mt * bh + k - 1 > 256) continue;
+    } else {
+      const int tap_b = Pn * mt * sub_rows * 16;
+      u = ntap;
+      while (u > ustep && (u * tap_b + 2048) * 3 > budget) u -= ustep;
+      sb = u * tap_b;
+    }
+    const int rb = res_pf ? mt * sub_rows * a.Cout * 4 : 0;
+    if ((sb + 2048) * 2 + 2 * rb <= budget) {
+      MT = mt;
+      stage_bytes = sb;
+      U = u;
+      break;
+    }
+  }
+  if (MT == 0) return false;
+  P->mode = halo ? 0 : 1;
+  P->kchunks = kchunks;
+  P->U = U;
+  P->ntap = ntap;
+  P->shift_bytes = 0;
+  P->MT = MT;
+  P->bn = bn;
+  P->bh = bh;
+  P->sub_rows = sub_rows;
+  P->b_bytes = b_bytes;
+  P->b_chunks = b_chunks;
+  if (bn == 1) {
+    P->samples_per_group = 1;
+    P->rows_per_super = MT * bh;
+    P->tiles_per_group = a.Ho / (MT * bh);
+  } else {
+    P->samples_per_group = bn * MT;
+    P->rows_per_super = 0;
+    P->tiles_per_group = 1;
+  }
+  int nbox = 0, nmma = 0, nks = 0;
+  auto b_off_of = [&](int kk) { return (uint32_t)((kk / 8) * BN * 16); };   // K element -> chunk offset
+  P->box_begin[0] = 0;
+  P->mma_begin[0] = 0;
+  if (halo) {
+    const int rows_h = MT * bh + k - 1;
+    const int plane = rows_h * a.W * 16;
+    for (int s = 0; s < k; ++s) {
+      BoxOp& o = P->box[nbox++];
+      o.map = 0;
+      o.dst = s * Pn * plane;
+      o.dx = (s - a.pad) * 8;
+      o.dh = 0;
+      o.dn = 0;
+    }
+    for (int j = 0; j < MT; ++j)
+      for (int t = 0; t < taps; ++t)
+        for (int q = 0; q < kchunks; ++q) {
+          if (nmma >= MAX_MMA) return false;
+          const int r = t / k, s = t % k;
+          MmaOp& m = P->mma[nmma++];
+          m.j = j;
+          m.a_off = (uint32_t)(s * Pn * plane + 2 * q * plane + (j * bh + r) * a.W * 16);
+          m.b_off = b_off_of(t * C + 16 * q);
+          m.acc = (t | q) != 0;
+        }
+    P->stage_tx[0] = (uint32_t)(k * Pn * plane);
+    P->shift_bytes = Pn * plane;
+    nks = 1;
+    P->box_begin[1] = nbox;
+    P->mma_begin[1] = nmma;
+    P->a_lbo = plane;
+  } else {
+    const int plane = MT * sub_rows * 16;
+    const int tap_b = Pn * plane;
+    for (int t0 = 0; t0 < ntap; t0 += U) {
+      const int t1 = t0 + U < ntap ? t0 + U : ntap;
+      if (nks >= MAX_KS) return false;
+      uint32_t tx = 0;
+      for (int t = t0; t < t1; ++t) {
+        if (nbox >= MAX_BOX) return false;
+        const int r = t / k, s = t % k;
+        BoxOp& o = P->box[nbox++];
+        o.map = fused_ok ? 0 : 1;
+        o.dst = (t - t0) * tap_b;
+        o.dx = fused_ok ? (s - a.pad) * 8 : (s - a.pad);
+        o.dh = t < taps ? r : -(1 << 20);          // phantom tap (C == 8 pairs): fully out of range
+        o.dn = 0;
+        tx += (uint32_t)tap_b;
+      }
+      for (int j = 0; j < MT; ++j) {
+        if (C == 8) {
+          for (int t = t0; t < t1; t += 2) {
+            if (nmma >= MAX_MMA) return false;
+            MmaOp& m = P->mma[nmma++];
+            m.j = j;
+            m.a_off = (uint32_t)((t - t0) * tap_b + j * sub_rows * 16);
+            m.b_off = b_off_of(t * 8);
+            m.acc = t != 0;
+          }
+        } else {
+          for (int t = t0; t < t1; ++t)
+            for (int q = 0; q < kchunks; ++q) {
+              if (nmma >= MAX_MMA) return false;
+              MmaOp& m = P->mma[nmma++];
+              m.j = j;
+              m.a_off = (uint32_t)((t - t0) * tap_b + 2 * q * plane + j * sub_rows * 16);
+              m.b_off = b_off_of(t * C + 16 * q);
+              m.acc = (t | q) != 0;
+            }
+        }
+      }
+      P->stage_tx[nks] = tx;
+      ++nks;
+      P->box_begin[nks] = nbox;
+      P->mma_begin[nks] = nmma;
+    }
+    P->a_lbo = plane;
+  }
+  P->nks = nks;
+  P->res_bytes = res_pf ? ((MT * sub_rows * a.Cout * 4 + 1023) & ~1023) : 0;
+  P->stage_bytes = (stage_bytes + 2048 + 1023) & ~1023;     // +128 rows of slack: the last tile's MMA reads 128 rows
+  int S = (budget - 2 * P->res_bytes) / P->stage_bytes;
+  if (S > 6) S = 6;
+  if (S < 2) return false;
+  P->S = S;
   return true;
 }
 
 template <int BN>
 cudaError_t launch_tma_bn(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream, bool* handled) {
-  TmaParams P;
+  *handled = false;
+  static TmaPlan P;                 // host-side scratch (the kernel parameter is copied at launch)
   P.a = a;
-  if (!plan_geom(a, BN, &P.g, &P.stages, &P.tiles_per_img_group)) {
-    *handled = false;
-    return cudaSuccess;
-  }
+  if (!build_plan(a, BN, &P)) return cudaSuccess;
   EncodeTiledFn enc = get_encode();
-  if (!enc) {
-    *handled = false;
-    return cudaSuccess;
-  }
-  const TmaGeom& G = P.g;
-  CUtensorMap tmA, tmB;
+  if (!enc) return cudaSuccess;
+  CUtensorMap tmF, tmU, tmB;
+  const int Pn = a.C / 8;
+  const cuuint64_t plane_b = (cuuint64_t)a.H * a.W * 16;
+  const int nb = P.bn == 1 ? 1 : P.bn * P.MT;
+  // fused-row map {W*8, H, N, P} (stride 1, W*8 <= 256)
   {
-    const int n_alloc = max_rows + G.bn;     // rows a tile may touch (the buffer holds >= max_rows)
-    (void)n_alloc;
-    cuuint64_t dims[4] = {(cuuint64_t)a.C, (cuuint64_t)a.W, (cuuint64_t)a.H, (cuuint64_t)max_rows};
-    cuuint64_t strides[3] = {(cuuint64_t)a.C * 2, (cuuint64_t)a.W * a.C * 2, (cuuint64_t)a.H * a.W * a.C * 2};
-    cuuint32_t box[4] = {(cuuint32_t)G.CW, (cuuint32_t)(a.Wo * a.stride), (cuuint32_t)(G.bh * a.stride),
-                         (cuuint32_t)G.bn};
-    cuuint32_t es[4] = {1, (cuuint32_t)a.stride, (cuuint32_t)a.stride, 1};
-    const CUtensorMapSwizzle sw = G.layout == 0 ? CU_TENSOR_MAP_SWIZZLE_NONE
-                                  : G.layout == 6 ? CU_TENSOR_MAP_SWIZZLE_32B
-                                  : G.layout == 4 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
-    CUresult r = enc(&tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)a.x, dims, strides, box, es,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+    cuuint64_t dims[4] = {(cuuint64_t)a.W * 8, (cuuint64_t)a.H, (cuuint64_t)max_rows, (cuuint64_t)Pn};
+    cuuint64_t strides[3] = {(cuuint64_t)a.W * 16, plane_b * Pn, plane_b};
+    int rows = P.mode == 0 ? P.MT * P.bh + a.ksz - 1 : (P.bn == 1 ? P.MT * P.bh : a.Ho);
+    if (rows > 256) rows = 256;
+    cuuint32_t box[4] = {(cuuint32_t)(a.W * 8 <= 256 ? a.W * 8 : 8), (cuuint32_t)rows, (cuuint32_t)nb,
+                         (cuuint32_t)Pn};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = enc(&tmF, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)a.x, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    cuuint64_t wd[2] = {(cuuint64_t)a.Kp, (cuuint64_t)a.Cout};
-    cuuint64_t ws[1] = {(cuuint64_t)a.Kp * 2};
-    cuuint32_t wb[2] = {(cuuint32_t)G.CW, (cuuint32_t)BN};
-    cuuint32_t we[2] = {1, 1};
-    r = enc(&tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)a.w, wd, ws, wb, we, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  // unfused map {8, W, H, N, P} with traversal strides (any stride)
+  {
+    cuuint64_t dims[5] = {8, (cuuint64_t)a.W, (cuuint64_t)a.H, (cuuint64_t)max_rows, (cuuint64_t)Pn};
+    cuuint64_t strides[4] = {16, (cuuint64_t)a.W * 16, plane_b * Pn, plane_b};
+    const int rows = P.bn == 1 ? P.MT * P.bh : a.Ho;
+    cuuint32_t box[5] = {8, (cuuint32_t)(a.Wo * a.stride), (cuuint32_t)(rows * a.stride), (cuuint32_t)nb,
+                         (cuuint32_t)Pn};
+    cuuint32_t es[5] = {1, (cuuint32_t)a.stride, (cuuint32_t)a.stride, 1, 1};
+    bool fits = true;
+    for (int i = 1; i < 4; ++i) fits = fits && box[i] <= 256;
+    if (!fits) {
+      for (int i = 1; i < 4; ++i)
+        if (box[i] > 256) box[i] = 256;
+      bool needs_unfused = false;
+      for (int b = 0; b < P.box_begin[P.nks]; ++b) needs_unfused |= P.box[b].map == 1;
+      if (needs_unfused) return cudaSuccess;
+    }
+    CUresult r = enc(&tmU, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, (void*)a.x, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
+  // weights {8, Cout, Kp/8} -> smem [K chunk][BN rows][16 B]
+  {
+    cuuint64_t dims[3] = {8, (cuuint64_t)a.Cout, (cuuint64_t)(a.Kp / 8)};
+    cuuint64_t strides[2] = {(cuuint64_t)a.Kp * 2, 16};
+    cuuint32_t box[3] = {8, (cuuint32_t)BN, (cuuint32_t)(a.Kp / 8 < 256 ? a.Kp / 8 : 256)};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(&tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, (void*)a.w, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   }
   const int n_tiles = a.Cout / BN;
-  const int b_total = (G.nunits * G.b_unit_bytes * n_tiles + 1023) & ~1023;
-  const int smem = 1024 + b_total + P.stages * G.U * G.unit_bytes + 256;
-  static int attr = 0;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_conv_tma<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BUDGET + 2048);
-    if (e != cudaSuccess) return e;
-    attr = SMEM_BUDGET + 2048;
+  const int b_total = (P.b_bytes * n_tiles + 1023) & ~1023;
+  const int smem = 1024 + b_total + P.S * P.stage_bytes + 2 * P.res_bytes + ((a.Cout + 3) & ~3) * 4 + 256;
+  if (smem > 227 * 1024) return cudaSuccess;
+  void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TmaPlan);
+  switch (a.C / 16) {
+    case 0: kern = k_conv_tma<BN, 0>; break;
+    case 1: kern = k_conv_tma<BN, 1>; break;
+    case 2: kern = k_conv_tma<BN, 2>; break;
+    case 4: kern = k_conv_tma<BN, 4>; break;
+    case 8: kern = k_conv_tma<BN, 8>; break;
+    default: return cudaSuccess;
   }
-  const long long groups = (max_rows + G.bn - 1) / G.bn;
-  const long long tiles = groups * P.tiles_per_img_group * n_tiles;
+  static bool attr[9] = {false};
+  if (!attr[a.C / 16]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr[a.C / 16] = true;
+  }
+  const long long groups = (max_rows + P.samples_per_group - 1) / P.samples_per_group;
+  const long long tiles = groups * P.tiles_per_group * n_tiles;
   int grid = (int)(tiles < num_sms ? tiles : num_sms);
   if (grid < 1) grid = 1;
   *handled = true;
-  k_conv_tma<BN><<<grid, THREADS, smem, stream>>>(tmA, tmB, P);
+  kern<<<grid, THREADS, smem, stream>>>(tmF, tmU, tmB, P);
   return cudaGetLastError();
 }
 
@@ -439,7 +624,6 @@ cudaError_t launch_conv_tma(const ConvArgs& a, int max_rows, int num_sms, cudaSt
     case 32: return launch_tma_bn<32>(a, max_rows, num_sms, stream, handled);
     case 64: return launch_tma_bn<64>(a, max_rows, num_sms, stream, handled);
     case 128: return launch_tma_bn<128>(a, max_rows, num_sms, stream, handled);
-    case 256: return launch_tma_bn<256>(a, max_rows, num_sms, stream, handled);
     default: return cudaSuccess;
   }
 }

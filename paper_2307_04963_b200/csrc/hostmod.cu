@@ -18,23 +18,26 @@ namespace {
 __device__ __forceinline__ float bf16f(uint16_t u) { return __uint_as_float((uint32_t)u << 16); }
 
 // ------------------------------------------------------------------ a0 cast
-__global__ void k_cast_pad(const float* __restrict__ in, uint16_t* __restrict__ out, int64_t npix, int c,
+// fp32 NHWC [n][hw][c] -> bf16 channel-planar [n][cp/8][hw][8] (channels >= c zero).
+__global__ void k_cast_pad(const float* __restrict__ in, uint16_t* __restrict__ out, int64_t npix, int hw, int c,
                            int cp) {
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npix; p += (int64_t)gridDim.x * blockDim.x) {
-    const float* src = in + p * c;
-    uint16_t* dst = out + p * cp;
-    for (int j0 = 0; j0 < cp; j0 += 8) {
-      uint32_t w[4];
+  const int planes = cp / 8;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < npix * planes;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t gp = u % npix;                     // global pixel (n*hw + p): consecutive threads, one plane
+    const int q = (int)(u / npix);
+    const int64_t n = gp / hw, p = gp - n * hw;
+    const float* src = in + gp * c;
+    uint32_t w[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int c0 = j0 + 2 * j, c1 = c0 + 1;
-        const float f0 = c0 < c ? src[c0] : 0.0f;
-        const float f1 = c1 < c ? src[c1] : 0.0f;
-        __nv_bfloat162 v = __floats2bfloat162_rn(f0, f1);
-        w[j] = *reinterpret_cast<uint32_t*>(&v);
-      }
-      *reinterpret_cast<uint4*>(dst + j0) = make_uint4(w[0], w[1], w[2], w[3]);
+    for (int j = 0; j < 4; ++j) {
+      const int c0 = q * 8 + 2 * j, c1 = c0 + 1;
+      const float f0 = c0 < c ? src[c0] : 0.0f;
+      const float f1 = c1 < c ? src[c1] : 0.0f;
+      __nv_bfloat162 v = __floats2bfloat162_rn(f0, f1);
+      w[j] = *reinterpret_cast<uint32_t*>(&v);
     }
+    *reinterpret_cast<uint4*>(out + ((n * planes + q) * hw + p) * 8) = make_uint4(w[0], w[1], w[2], w[3]);
   }
 }
 
@@ -75,8 +78,9 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head(const HeadArgs a) {
           acc[4] += v1.x; acc[5] += v1.y; acc[6] += v1.z; acc[7] += v1.w;
         }
       } else {
+        // bf16 channel-planar [C/8][HW][8]
         for (int p = t / G; p < a.HW; p += P) {
-          const uint4 v = __ldg(reinterpret_cast<const uint4*>(h + (size_t)p * a.C + grp * 8));
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(h + ((size_t)grp * a.HW + p) * 8));
           const uint32_t u[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -249,8 +253,24 @@ __global__ void __launch_bounds__(256) k_gather(const GatherArgs a) {
       for (int k = 0; k < 4; ++k)
         if (di[k] >= 0) dst[di[k]] = v[k];
     }
+  } else if (a.elem_bytes == 2) {
+    // option A, bf16 channel-planar: dst [2C/8][H/2][W/2][8] from src [C/8][H][W][8]
+    const int Ho = a.H / 2, Wo = a.W / 2, HWo = Ho * Wo, padp = a.C / 16;   // C/2 channels = C/16 planes
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total; u += stride) {
+      const int64_t j = u / U;
+      const int64_t r = u - j * U;
+      const int pd = (int)(r / HWo), p = (int)(r - (int64_t)pd * HWo);
+      const int ho = p / Wo, wo = p - ho * Wo;
+      const int ps = pd - padp;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (ps >= 0 && ps < a.C / 8) {
+        const int64_t e = (int64_t)a.list[j] * a.row_elems_src + ((int64_t)ps * a.H * a.W + (2 * ho) * a.W + 2 * wo) * 8;
+        v = __ldg(src + e / 8);
+      }
+      dst[(off + j) * U + r] = v;
+    }
   } else {
-    // option A: dst [H/2][W/2][2C] from src [H][W][C]: pixel (2ho, 2wo), channel c - C/2
+    // option A, fp32 NHWC: dst [H/2][W/2][2C] from src [H][W][C]: pixel (2ho, 2wo), channel c - C/2
     const int Wo = a.W / 2, Cd = 2 * a.C, qpp = Cd / epu, pad = a.C / 2;
     for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total; u += stride) {
       const int64_t j = u / U;
@@ -273,9 +293,9 @@ __global__ void __launch_bounds__(256) k_gather(const GatherArgs a) {
 cudaError_t launch_cast_pad(const float* in, uint16_t* out, int64_t n, int hw, int c, int cp, cudaStream_t s) {
   const int64_t npix = n * hw;
   if (npix == 0) return cudaSuccess;
-  int64_t blocks = (npix + 255) / 256;
+  int64_t blocks = (npix * (cp / 8) + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_cast_pad<<<(int)blocks, 256, 0, s>>>(in, out, npix, c, cp);
+  k_cast_pad<<<(int)blocks, 256, 0, s>>>(in, out, npix, hw, c, cp);
   return cudaGetLastError();
 }
 
