@@ -44,6 +44,8 @@ struct Layer {
   int K = 0, Kp = 0, res_mode = 0;
   Shape res_shape;
   uint16_t* d_w = nullptr;
+  uint16_t* d_wrt = nullptr;    // row-tap layout (3x3 / stride 1 / pad 1 convs)
+  int Kp_rt = 0;
   float* d_b = nullptr;
 };
 
@@ -236,6 +238,13 @@ dycl_status upload_subnet(dycl_graph g, Subnet& s) {
       dycl_status st = dmalloc(g, &L.d_w, wp.size() * 2);
       if (st) return st;
       CK(cudaMemcpy(L.d_w, wp.data(), wp.size() * 2, cudaMemcpyHostToDevice));
+      if (L.kind == L_CONV && L.k == 3 && L.stride == 1 && L.pad == 1) {
+        L.Kp_rt = (3 * Cp + 63) / 64 * 64;
+        std::vector<uint16_t> wr((size_t)3 * L.cout * L.Kp_rt);
+        dycl::pack_rowtap(wp.data(), L.cout, L.Kp, Cp, wr.data(), L.Kp_rt);
+        if ((st = dmalloc(g, &L.d_wrt, wr.size() * 2))) return st;
+        CK(cudaMemcpy(L.d_wrt, wr.data(), wr.size() * 2, cudaMemcpyHostToDevice));
+      }
     } else if (L.kind == L_DENSE) {
       const int Cin = L.in.C, Cp = L.in.Cp();
       std::vector<uint16_t> wp((size_t)L.cout * Cp, 0);
@@ -329,6 +338,8 @@ struct Exec {
       dycl::ConvArgs a{};
       a.x = g->buf[cur.b];
       a.w = L.d_w;
+      a.w_rt = L.d_wrt;
+      a.Kp_rt = L.Kp_rt;
       a.bias = L.d_b;
       a.res = L.res_mode ? g->buf[shortcut.b] : nullptr;
       a.res32 = (L.res_mode && shortcut.f >= 0) ? g->buf32[shortcut.f] : nullptr;
@@ -549,6 +560,7 @@ dycl_status dycl_graph_destroy(dycl_graph g) {
   for (Subnet& s : g->subnets)
     for (Layer& L : s.layers) {
       cudaFree(L.d_w);
+      cudaFree(L.d_wrt);
       cudaFree(L.d_b);
     }
   for (auto* b : g->buf) cudaFree(b);
@@ -902,15 +914,26 @@ dycl_status dycl_debug_conv2d(dycl_graph g, int64_t n, int H, int W, int C, cons
   if (dycl_status s = dmalloc(g, &db, (size_t)c_out * 4)) { cudaFree(dw); return s; }
   cudaMemcpy(dw, wp.data(), wp.size() * 2, cudaMemcpyHostToDevice);
   cudaMemcpy(db, bias, (size_t)c_out * 4, cudaMemcpyHostToDevice);
+  uint16_t* dwr = nullptr;
+  int kp_rt = 0;
+  if (k == 3 && stride == 1 && pad == 1 && path != 3) {
+    kp_rt = (3 * C + 63) / 64 * 64;
+    std::vector<uint16_t> wr((size_t)3 * c_out * kp_rt);
+    dycl::pack_rowtap(wp.data(), c_out, Kp, C, wr.data(), kp_rt);
+    if (cudaMalloc(&dwr, wr.size() * 2) == cudaSuccess) cudaMemcpy(dwr, wr.data(), wr.size() * 2, cudaMemcpyHostToDevice);
+  }
   dycl::ConvArgs a{};
-  a.x = (const uint16_t*)x; a.w = dw; a.bias = db; a.res = (const uint16_t*)res; a.y = (uint16_t*)y;
+  a.x = (const uint16_t*)x; a.w = dw; a.w_rt = dwr; a.Kp_rt = kp_rt; a.bias = db;
+  a.res = (const uint16_t*)res; a.y = (uint16_t*)y;
   a.n_live = nullptr; a.n_static = (int)n;
   a.H = H; a.W = W; a.C = C; a.Ho = Ho; a.Wo = Wo; a.Cout = c_out; a.ksz = k; a.stride = stride; a.pad = pad;
   a.K = K; a.Kp = Kp; a.relu = relu; a.res_mode = res_mode;
   a.rH = 2 * Ho; a.rW = 2 * Wo; a.rC = c_out / 2; a.r_pad_lo = c_out / 4;
   if (res_mode == 1) { a.rH = Ho; a.rW = Wo; a.rC = c_out; a.r_pad_lo = 0; }
-  cudaError_t e = n > 0 ? dycl::launch_conv(a, (int)n, g->num_sms, 0, path) : cudaSuccess;
+  if (path == 2 && dwr) a.dbg |= 32;          // path 2 exercises the row-tap mode where eligible
+  cudaError_t e = n > 0 ? dycl::launch_conv(a, (int)n, g->num_sms, 0, path == 3 ? 2 : path) : cudaSuccess;
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  cudaFree(dwr);
   cudaFree(dw);
   cudaFree(db);
   if (e != cudaSuccess) return cuda_fail(g, e, "debug_conv2d");

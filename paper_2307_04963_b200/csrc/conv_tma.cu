@@ -58,7 +58,10 @@ struct MmaOp {
 
 struct TmaPlan {
   ConvArgs a;
-  int mode;                 // 0 halo, 1 tap
+  int mode;                 // 0 halo, 1 tap, 2 row-tap (halo rows, W taps in the MMA's N)
+  int ncol;                 // TMEM columns per UMMA tile: BN, or 3*BN in row-tap mode
+  int nacc;                 // TMEM accumulator buffers (2 or 4)
+  uint32_t idesc;           // tcgen05 instruction descriptor (M = 128, N = ncol)
   int MT, bn, bh;           // super-tile = MT UMMA tiles; UMMA tile = bn samples x bh rows x Wo
   int sub_rows;             // valid rows of one UMMA tile (bn*bh*Wo)
   int tiles_per_group;      // super-tiles per group of samples
@@ -108,7 +111,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int groups = (n_live + P.samples_per_group - 1) / P.samples_per_group;
   const int m_tiles = groups * P.tiles_per_group;
   const int num_tiles = m_tiles * n_tiles;
-  const int acc_cols = P.MT * BN;                // NACC * acc_cols <= 512 (host-checked)
+  const int acc_cols = P.MT * P.ncol;            // nacc * acc_cols <= 512 (host-checked)
+  const int nacc = P.nacc;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
@@ -143,11 +147,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       ptx::mbar_arrive_expect_tx(bfull, (uint32_t)(P.b_bytes * n_tiles));
       for (int nt = 0; nt < n_tiles; ++nt)
         for (int c0 = 0; c0 < P.b_chunks; c0 += 256) {
-          const uint32_t dst = ptx::smem_u32(sB + nt * P.b_bytes + c0 * BN * 16);
+          const uint32_t dst = ptx::smem_u32(sB + nt * P.b_bytes + c0 * P.ncol * 16);
           asm volatile(
               "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
               "%5}], [%2];" ::"r"(dst),
-              "l"(&tmB), "r"(bfull), "r"(0), "r"(nt * BN), "r"(c0)
+              "l"(&tmB), "r"(bfull), "r"(0), "r"(nt * P.ncol), "r"(c0)
               : "memory");
         }
       int stage = 0;
@@ -207,17 +211,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else if (warp == MMA_WARP) {
     // ---------------------------------------------------------------- MMA issuer
-    const uint32_t IDESC = ptx::make_idesc_bf16(BM, BN);
+    const uint32_t IDESC = P.idesc;
     ptx::mbar_wait(bfull, 0);
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
     const uint32_t sA0 = ptx::smem_u32(sA), sB0 = ptx::smem_u32(sB);
     const uint64_t adesc0 = ptx::make_smem_desc(sA0, 0, (uint32_t)P.a_lbo, 128u);
-    const uint64_t bdesc0 = ptx::make_smem_desc(sB0, 0, (uint32_t)(BN * 16), 128u);
+    const uint64_t bdesc0 = ptx::make_smem_desc(sB0, 0, (uint32_t)(P.ncol * 16), 128u);
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-      const int acc = it % NACC;
-      const uint32_t acc_phase = (it / NACC) & 1;
+      const int acc = it % nacc;
+      const uint32_t acc_phase = (it / nacc) & 1;
       const int n_tile = tile % n_tiles;
       ptx::mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
       ptx::tc_fence_after();
@@ -233,7 +237,24 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint64_t bd0 = bdesc0 + (b_nt >> 4);
           const uint32_t plane16 = (uint32_t)P.a_lbo >> 4;            // 16-byte units
           const uint32_t tapb16 = (uint32_t)((a.C / 8) * BN);        // weights per tap, 16-byte units
-          if (P.mode == 0) {
+          if (P.mode == 2) {
+            // row-tap (3x3): per filter row r ONE MMA with N = 3*BN (the three W taps s
+            // side by side); A = the centre halo box shifted by r image rows.
+            const uint32_t row16 = (uint32_t)a.W;
+            const uint32_t chunk16 = (uint32_t)P.ncol;                 // one 8-channel K chunk of B
+            for (int j = 0; j < P.MT; ++j) {
+              const uint32_t dj = d_base + (uint32_t)(j * P.ncol);
+              const uint64_t aj = ad0 + (uint32_t)(j * P.bh) * row16;
+#pragma unroll
+              for (int r = 0; r < 3; ++r) {
+#pragma unroll
+                for (int q = 0; q < KCH; ++q)
+                  ptx::mma_bf16_ss_elect(dj, aj + (uint32_t)r * row16 + 2 * q * plane16,
+                                         bd0 + (uint32_t)(r * (a.C / 8) + 2 * q) * chunk16, IDESC,
+                                         (uint32_t)((r | q) != 0));
+              }
+            }
+          } else if (P.mode == 0) {
             // halo (3x3): tap (r, s) of tile j = shift block s, image rows (j*bh + r)
             const uint32_t shift16 = (uint32_t)P.shift_bytes >> 4;
             const uint32_t row16 = (uint32_t)a.W;                      // W*16 bytes
@@ -292,8 +313,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       if ((it & 1) != wg) continue;
-      const int acc = it % NACC;
-      const uint32_t acc_phase = (it / NACC) & 1;
+      const int acc = it % nacc;
+      const uint32_t acc_phase = (it / nacc) & 1;
       const int m_tile = tile / n_tiles;
       const int n_tile = tile - m_tile * n_tiles;
       const int grp = m_tile / P.tiles_per_group;
@@ -323,12 +344,29 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 16) {
           uint32_t v[16];
-          ptx::tmem_ld_32x32b_x16(t_base + (uint32_t)(j * BN + c0), v);
-          ptx::tmem_ld_wait();
-          if (ok && !(a.dbg & 1)) {
-            float f[16];
+          float f[16];
+          if (P.mode == 2) {
+            // out(w) = D_0(w-1) + D_1(w) + D_2(w+1): neighbouring pixels of an image row are
+            // neighbouring lanes of this warp (zero padding at the row ends).
+            uint32_t v0[16], v2[16];
+            ptx::tmem_ld_32x32b_x16(t_base + (uint32_t)(j * P.ncol + c0), v0);
+            ptx::tmem_ld_32x32b_x16(t_base + (uint32_t)(j * P.ncol + BN + c0), v);
+            ptx::tmem_ld_32x32b_x16(t_base + (uint32_t)(j * P.ncol + 2 * BN + c0), v2);
+            ptx::tmem_ld_wait();
+            const bool has_l = wo > 0, has_r = wo < a.Wo - 1;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              const float lft = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[q]), 1);
+              const float rgt = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[q]), 1);
+              f[q] = __uint_as_float(v[q]) + (has_l ? lft : 0.0f) + (has_r ? rgt : 0.0f);
+            }
+          } else {
+            ptx::tmem_ld_32x32b_x16(t_base + (uint32_t)(j * P.ncol + c0), v);
+            ptx::tmem_ld_wait();
 #pragma unroll
             for (int q = 0; q < 16; ++q) f[q] = __uint_as_float(v[q]);
+          }
+          if (ok && !(a.dbg & 1)) {
             // pixel index inside the super-tile's residual rows
             const float* rs = res_tile ? res_tile + (size_t)(j * P.sub_rows + r) * a.Cout + c0 : nullptr;
             conv_finish16(a, n, ho, wo, n_tile * BN + c0, f, sBias, rs);
@@ -385,9 +423,14 @@ bool build_plan(const ConvArgs& a, int BN, TmaPlan* P) {
   const int sub_rows = bn * bh * a.Wo;
   const bool fused_ok = a.stride == 1 && a.W * 8 <= 256 && a.Wo == a.W;
   const bool halo = fused_ok && bn == 1 && k == 3 && a.pad == 1 && C >= 16;
+  // row-tap mode: measured slower than halo mode end-to-end on config 2 (epilogue-bound,
+  // profiles/r01_profile.json), so it is opt-in (ConvArgs.dbg bit 5, DYCL_CONV_DBG=32).
+  const bool rowtap = halo && a.w_rt != nullptr && 3 * BN <= 256 && a.Cout == BN && (a.dbg & 32) != 0;
+  const int ncol = rowtap ? 3 * BN : BN;
+  const int nacc = rowtap ? 2 : NACC;
   const int kchunks = C / 16;                        // UMMA K steps per tap (C == 8: pairs of taps)
-  const int b_chunks = a.Kp / 8;
-  const int b_bytes = b_chunks * BN * 16;
+  const int b_chunks = (rowtap ? a.Kp_rt : a.Kp) / 8;
+  const int b_bytes = b_chunks * ncol * 16;
   const int n_tiles = a.Cout / BN;
   const int b_total = (b_bytes * n_tiles + 1023) & ~1023;
   if (b_total > 120 * 1024) return false;            // resident-weight design (large layers: fallback)
@@ -397,12 +440,12 @@ bool build_plan(const ConvArgs& a, int BN, TmaPlan* P) {
   const int ntap = taps + ((C == 8 && (taps & 1)) ? 1 : 0);
   const int ustep = C == 8 ? 2 : 1;
   int MT = 0, stage_bytes = 0, U = 0;
-  for (int mt = (512 / (NACC * BN) < 8 ? 512 / (NACC * BN) : 8); mt >= 1; --mt) {
+  for (int mt = (512 / (nacc * ncol) < 8 ? 512 / (nacc * ncol) : 8); mt >= 1; --mt) {
     if (bn == 1 && (mt * bh > a.Ho || a.Ho % (mt * bh) != 0)) continue;
     if (bn > 1 && mt * bn > 256) continue;
     int sb, u = 0;
     if (halo) {
-      sb = k * Pn * (mt * bh + k - 1) * a.W * 16;
+      sb = (rowtap ? 1 : k) * Pn * (mt * bh + k - 1) * a.W * 16;
       if (mt * bh + k - 1 > 256) continue;
     } else {
       const int tap_b = Pn * mt * sub_rows * 16;
@@ -419,7 +462,10 @@ bool build_plan(const ConvArgs& a, int BN, TmaPlan* P) {
     }
   }
   if (MT == 0) return false;
-  P->mode = halo ? 0 : 1;
+  P->mode = rowtap ? 2 : halo ? 0 : 1;
+  P->ncol = ncol;
+  P->nacc = nacc;
+  P->idesc = ptx::make_idesc_bf16(BM, ncol);
   P->kchunks = kchunks;
   P->U = U;
   P->ntap = ntap;
@@ -443,7 +489,22 @@ bool build_plan(const ConvArgs& a, int BN, TmaPlan* P) {
   auto b_off_of = [&](int kk) { return (uint32_t)((kk / 8) * BN * 16); };   // K element -> chunk offset
   P->box_begin[0] = 0;
   P->mma_begin[0] = 0;
-  if (halo) {
+  if (rowtap) {
+    const int rows_h = MT * bh + 2;
+    const int plane = rows_h * a.W * 16;
+    BoxOp& o = P->box[nbox++];
+    o.map = 0;
+    o.dst = 0;
+    o.dx = 0;            // centre column only: the W taps are combined in the epilogue
+    o.dh = 0;
+    o.dn = 0;
+    P->stage_tx[0] = (uint32_t)(Pn * plane);
+    P->shift_bytes = 0;
+    nks = 1;
+    P->box_begin[1] = nbox;
+    P->mma_begin[1] = nmma;
+    P->a_lbo = plane;
+  } else if (halo) {
     const int rows_h = MT * bh + k - 1;
     const int plane = rows_h * a.W * 16;
     for (int s = 0; s < k; ++s) {
@@ -544,7 +605,7 @@ cudaError_t launch_tma_bn(const ConvArgs& a, int max_rows, int num_sms, cudaStre
   {
     cuuint64_t dims[4] = {(cuuint64_t)a.W * 8, (cuuint64_t)a.H, (cuuint64_t)max_rows, (cuuint64_t)Pn};
     cuuint64_t strides[3] = {(cuuint64_t)a.W * 16, plane_b * Pn, plane_b};
-    int rows = P.mode == 0 ? P.MT * P.bh + a.ksz - 1 : (P.bn == 1 ? P.MT * P.bh : a.Ho);
+    int rows = P.mode != 1 ? P.MT * P.bh + a.ksz - 1 : (P.bn == 1 ? P.MT * P.bh : a.Ho);   // halo rows in modes 0 / 2
     if (rows > 256) rows = 256;
     cuuint32_t box[4] = {(cuuint32_t)(a.W * 8 <= 256 ? a.W * 8 : 8), (cuuint32_t)rows, (cuuint32_t)nb,
                          (cuuint32_t)Pn};
@@ -576,13 +637,16 @@ cudaError_t launch_tma_bn(const ConvArgs& a, int max_rows, int num_sms, cudaStre
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   }
-  // weights {8, Cout, Kp/8} -> smem [K chunk][BN rows][16 B]
+  // weights {8, rows, Kp/8} -> smem [K chunk][ncol rows][16 B]
   {
-    cuuint64_t dims[3] = {8, (cuuint64_t)a.Cout, (cuuint64_t)(a.Kp / 8)};
-    cuuint64_t strides[2] = {(cuuint64_t)a.Kp * 2, 16};
-    cuuint32_t box[3] = {8, (cuuint32_t)BN, (cuuint32_t)(a.Kp / 8 < 256 ? a.Kp / 8 : 256)};
+    const bool rt = P.mode == 2;
+    const int kp = rt ? a.Kp_rt : a.Kp;
+    const int nrows = rt ? 3 * a.Cout : a.Cout;
+    cuuint64_t dims[3] = {8, (cuuint64_t)nrows, (cuuint64_t)(kp / 8)};
+    cuuint64_t strides[2] = {(cuuint64_t)kp * 2, 16};
+    cuuint32_t box[3] = {8, (cuuint32_t)P.ncol, (cuuint32_t)(kp / 8 < 256 ? kp / 8 : 256)};
     cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = enc(&tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, (void*)a.w, dims, strides, box, es,
+    CUresult r = enc(&tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, (void*)(rt ? a.w_rt : a.w), dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;

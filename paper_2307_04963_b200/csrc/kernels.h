@@ -13,6 +13,8 @@ namespace dycl {
 struct ConvArgs {
   const uint16_t* x;     // bf16 [n][H][W][C]
   const uint16_t* w;     // bf16 [Cout][Kp]  (K zero-padded to Kp = roundup(K, 64))
+  const uint16_t* w_rt;  // 3x3 stride-1 only: "row-tap" weights [3*Cout][Kp_rt], row (s, o), col (r, c), or nullptr
+  int Kp_rt;
   const float* bias;     // fp32 [Cout]
   const uint16_t* res;   // bf16 shortcut source, or nullptr
   const float* res32;    // fp32 shortcut source (fp32 residual stream), preferred when set
@@ -25,11 +27,24 @@ struct ConvArgs {
   int relu;
   int res_mode;          // 0 none, 1 identity [n][Ho][Wo][Cout], 2 option A from [n][rH][rW][rC]
   int rH, rW, rC, r_pad_lo;
-  int dbg = 0;           // experiments only: bit0 skip epilogue math/stores, bit1 skip MMAs, bit2 skip A loads
+  int dbg = 0;           // bit5 (32): row-tap mode opt-in; experiments only (results invalid): bit0 skip
+                         // epilogue math/stores, bit1 skip MMAs, bit2 skip A loads, bit3 no residual prefetch
 };
 // Launch on `stream`; grid is sized for max_rows samples (persistent CTAs loop
 // over the tiles the live count needs).  Returns cudaSuccess or the launch error.
 cudaError_t launch_conv_tc(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream);
+// Row-tap weight layout for 3x3 / stride 1 / pad 1 convs: from the standard packed
+// weights wp [cout][kp] (k = (r*3 + s)*cp + c) build [3*cout][kp_rt] with row s*cout + o,
+// column r*cp + c (kp_rt = roundup(3*cp, 64)); the W taps then share one MMA (N = 3*cout).
+inline void pack_rowtap(const uint16_t* wp, int cout, int kp, int cp, uint16_t* out, int kp_rt) {
+  for (int s = 0; s < 3; ++s)
+    for (int o = 0; o < cout; ++o) {
+      uint16_t* row = out + ((size_t)s * cout + o) * kp_rt;
+      for (int j = 0; j < kp_rt; ++j) row[j] = 0;
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < cp; ++c) row[r * cp + c] = wp[(size_t)o * kp + (size_t)(r * 3 + s) * cp + c];
+    }
+}
 // TMA-fed variant (conv_tma.cu) for layers whose output tiles are rectangular
 // boxes; *handled = false (and nothing launched) when the shape does not qualify.
 cudaError_t launch_conv_tma(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream, bool* handled);

@@ -71,8 +71,14 @@ CONV_CASES = [
 TMA_CASES = [c for c in CONV_CASES if c[4] in (16, 32, 64)]
 
 
-@pytest.mark.parametrize("path,case", [(1, c) for c in CONV_CASES] + [(2, c) for c in TMA_CASES],
-                         ids=[f"cpasync-{c}" for c in CONV_CASES] + [f"tma-{c}" for c in TMA_CASES])
+ROWTAP_CASES = [c for c in TMA_CASES if c[5] == 3 and c[6] == 1 and c[7] == 1 and c[3] >= 16 and c[1] * c[2] >= 128]
+
+
+# path 1: cp.async-fed kernel; 2: TMA kernel (row-tap mode where eligible); 3: TMA kernel, no row-tap
+@pytest.mark.parametrize("path,case", [(1, c) for c in CONV_CASES] + [(2, c) for c in TMA_CASES] +
+                         [(3, c) for c in ROWTAP_CASES],
+                         ids=[f"cpasync-{c}" for c in CONV_CASES] + [f"tma-{c}" for c in TMA_CASES] +
+                             [f"tma-norowtap-{c}" for c in ROWTAP_CASES])
 def test_conv_kernel_matches_oracle_conv(any_graph, path, case):
     n, H, W, C, Co, k, st, pad, relu, res_mode = case
     rng = np.random.default_rng(abs(hash(case)) % 2**32)
