@@ -118,6 +118,18 @@ dycl_status dycl_subnet_conv2d(dycl_graph g, dycl_node sn, int c_in, int c_out, 
 dycl_status dycl_subnet_dense(dycl_graph g, dycl_node sn, int n_in, int n_out, const uint16_t* w_bf16,
                               const float* bias, dycl_act act, int out_fp32);
 
+/* Projection shortcut (ResNet "option B"): a 1x1 convolution with the given stride
+ * applied to the tensor saved by dycl_subnet_block_begin; its output (c_out channels,
+ * no activation) replaces the saved tensor as the shortcut the next residual conv adds.
+ * w: host bf16 [c_out][1][1][c_in], b: host fp32 [c_out]; c_in = the saved tensor's
+ * channel count (checked at dycl_finalize). */
+dycl_status dycl_subnet_projection(dycl_graph g, dycl_node sn, int c_in, int c_out, int stride,
+                                   const uint16_t* w_bf16, const float* bias);
+
+/* Max pooling with a k x k window, stride, zero-size padding of `pad` pixels on each side
+ * (padded positions never win): y[ho][wo][c] = max over the window (torchvision MaxPool2d). */
+dycl_status dycl_subnet_maxpool(dycl_graph g, dycl_node sn, int k, int stride, int pad);
+
 /* Global average pooling [H][W][C] -> [1][1][C], fp32 mean (kept in fp32 when
  * followed by an out_fp32 dense head). */
 dycl_status dycl_subnet_gap(dycl_graph g, dycl_node sn);
@@ -188,7 +200,7 @@ dycl_status dycl_num_classes(dycl_graph g, int32_t* out);
  * the launch processed, read back AFTER the run).  Arrays hold max_n entries;
  * *n_out receives the number of launches. */
 enum { DYCL_K_INPUT = 0, DYCL_K_CONV = 1, DYCL_K_HEAD = 2, DYCL_K_COMPACT = 3,
-       DYCL_K_GATHER = 4, DYCL_K_SCATTER = 5, DYCL_K_INIT = 6 };
+       DYCL_K_GATHER = 4, DYCL_K_SCATTER = 5, DYCL_K_INIT = 6, DYCL_K_POOL = 7 };
 dycl_status dycl_set_profiling(dycl_graph g, int enable);
 dycl_status dycl_profile_read(dycl_graph g, int32_t max_n, int32_t* kind, float* ms,
                               double* bytes, double* flops, int32_t* n_out);

@@ -124,14 +124,62 @@ def calibrate_cfg3(n: int, mode: str = "mirror") -> dict:
     return out
 
 
+def calibrate_cfg5(n: int, mode: str = "mirror") -> dict:
+    """Config 5 heads (exits after stages 1-3, 1000 classes): same recipe as config 2."""
+    X = wl.image_inputs(wl.CALIB_SEED, 0, n, hw=224)
+    P = prg.prepare(wl.resnet50_ee_weights(calib={
+        k: {"scale": 1.0, "mu": [0.0] * c} for k, c in [("ic0", 256), ("ic1", 512), ("ic2", 1024), ("final", 2048)]}))
+
+    def feats(i):
+        f = []
+        prg.resnet50_ee(X[i], P, mode, tau=2.0, features=f)
+        return f
+
+    with _pool() as ex:
+        F = list(ex.map(feats, range(n)))
+    names = ["ic0", "ic1", "ic2", "final"]
+    G = {nm: np.stack([f[j] for f in F]) for j, nm in enumerate(names)}
+    raw = wl.r50_raw_heads()
+    out = {}
+    arriving = np.ones(n, dtype=bool)
+    for k in range(3):
+        nm = f"ic{k}"
+        g = G[nm]
+        mu = g.mean(axis=0)
+
+        def exits(s):
+            w, b = wl._centered_head(raw[nm], s, mu)
+            wf = prg._bf16_to_f64(w)
+            conf = np.array([max_softmax(dense(wf, b, gi)) for gi in g])
+            return conf >= wl.EXIT_TAU
+
+        lo, hi = np.log(0.01), np.log(1000.0)
+        for _ in range(50):
+            mid = 0.5 * (lo + hi)
+            if exits(np.exp(mid))[arriving].mean() < 0.25:
+                lo = mid
+            else:
+                hi = mid
+        s = float(np.exp(hi))
+        ex_k = exits(s)
+        out[nm] = {"scale": s, "mu": [float(v) for v in mu],
+                   "exit_frac_of_arriving": float(ex_k[arriving].mean()), "arriving": int(arriving.sum())}
+        arriving &= ~ex_k
+    out["final"] = {"scale": 4.0, "mu": [float(v) for v in G["final"].mean(axis=0)], "arriving": int(arriving.sum())}
+    out["_recipe"] = ("oracle/calibrate.py calibrate_cfg5: n=%d calibration samples (seed %d), 224x224, mode=%s, "
+                      "target 25%% exits of arriving, tau=%.2f" % (n, wl.CALIB_SEED, mode, wl.EXIT_TAU))
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=512)
     ap.add_argument("--cfg", type=int, nargs="*", default=[2, 3])
+    ap.add_argument("--n5", type=int, default=128)
     a = ap.parse_args()
     os.makedirs(os.path.join(wl.HERE, "calib"), exist_ok=True)
     for c in a.cfg:
-        res = calibrate_cfg2(a.n) if c == 2 else calibrate_cfg3(a.n)
+        res = calibrate_cfg2(a.n) if c == 2 else calibrate_cfg3(a.n) if c == 3 else calibrate_cfg5(a.n5)
         path = os.path.join(wl.HERE, "calib", f"cfg{c}.json")
         with open(path, "w") as f:
             json.dump(res, f, indent=1)

@@ -126,3 +126,19 @@ def option_a(h, c_out: int):
     sub = h[::2, ::2, :]
     p = (c_out - h.shape[2]) // 2
     return np.pad(sub, ((0, 0), (0, 0), (p, c_out - h.shape[2] - p)))
+
+
+def maxpool2d(h, k: int = 3, stride: int = 2, pad: int = 1):
+    """Max pooling of one NHWC sample: y[ho][wo][c] = max over the k x k window at
+    (ho*stride - pad, wo*stride - pad); out-of-range positions never win (-inf padding)."""
+    h = np.asarray(h, np.float64)
+    H, W, C = h.shape
+    Ho = (H + 2 * pad - k) // stride + 1
+    Wo = (W + 2 * pad - k) // stride + 1
+    hp = np.full((H + 2 * pad, W + 2 * pad, C), -np.inf)
+    hp[pad:pad + H, pad:pad + W] = h
+    y = np.full((Ho, Wo, C), -np.inf)
+    for r in range(k):
+        for s in range(k):
+            y = np.maximum(y, hp[r:r + stride * Ho:stride, s:s + stride * Wo:stride])
+    return y

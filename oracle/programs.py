@@ -27,8 +27,8 @@ from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
-from .core import (conv2d, dense, gap, max_softmax, option_a, relu, round_bf16,
-                   sigmoid)
+from .core import (conv2d, dense, gap, max_softmax, maxpool2d, option_a, relu,
+                   round_bf16, sigmoid)
 
 
 def _bf16_to_f64(bits):
@@ -172,7 +172,58 @@ def skipnet_resnet38(x, P, mode="mirror", thr=0.5, gate_hook=None):
     return dense(P["final.w"], P["final.b"], gap(h)), mask, preds
 
 
-PROGRAMS = {1: mlp_ee, 2: sdn_resnet56, 3: skipnet_resnet38}
+# ---------------------------------------------------------------------------
+# Config 5: early-exit ResNet-50 v1.5 (BASELINE configs[4]).
+#   h = maxpool(relu(conv7x7/2(x)))
+#   for stage s in 1..4: for each bottleneck b: h = bottleneck(h)
+#       if s in {1,2,3}: z = IC_s(GAP(h)); if maxsoftmax(z) >= tau: return (z, s-1)
+#   return (FC(GAP(h)), 3)
+# bottleneck(h) = relu(conv1x1(relu(conv3x3/stride(relu(conv1x1(h))))) + shortcut(h)),
+# shortcut = conv1x1/stride(h) (projection) for the first block of a stage, else h.
+# Exit placement: reading R6.  1000 classes.
+# ---------------------------------------------------------------------------
+R50_LAYERS = (3, 4, 6, 3)
+R50_WIDTHS = (64, 128, 256, 512)
+
+
+def bottleneck(h, P, s, b, mode):
+    stride = 2 if (b == 0 and s > 1) else 1
+    p = f"s{s}b{b}"
+    t = _inner(relu(conv2d(_operand(h, mode), P[f"{p}.c1.w"], P[f"{p}.c1.b"], 1, 0)), mode)
+    t = _inner(relu(conv2d(t, P[f"{p}.c2.w"], P[f"{p}.c2.b"], stride, 1)), mode)
+    if b == 0:
+        sc = _stream(conv2d(_operand(h, mode), P[f"{p}.proj.w"], P[f"{p}.proj.b"], stride, 0), mode)
+    else:
+        sc = h
+    return _stream(relu(conv2d(t, P[f"{p}.c3.w"], P[f"{p}.c3.b"], 1, 0) + sc), mode)
+
+
+def resnet50_ee(x, P, mode="mirror", tau=0.9, features=None):
+    preds = []
+    h = round_bf16(np.asarray(x, np.float64))                 # a0: input cast to bf16
+    h = _stream(relu(conv2d(h, P["stem.w"], P["stem.b"], 2, 3)), mode)
+    h = maxpool2d(h, 3, 2, 1)
+    k = 0
+    for s in range(1, 5):
+        for b in range(R50_LAYERS[s - 1]):
+            h = bottleneck(h, P, s, b, mode)
+        if s < 4:
+            g = gap(h)
+            if features is not None:
+                features.append(g)
+            z = dense(P[f"ic{k}.w"], P[f"ic{k}.b"], g)
+            conf = max_softmax(z)
+            preds.append(("exit", conf, tau))
+            if conf >= tau:
+                return z, k, preds
+            k += 1
+    g = gap(h)
+    if features is not None:
+        features.append(g)
+    return dense(P["final.w"], P["final.b"], g), 3, preds
+
+
+PROGRAMS = {1: mlp_ee, 2: sdn_resnet56, 3: skipnet_resnet38, 5: resnet50_ee}
 
 
 def run_batch(program, X, P, mode="mirror", threads=None, **kw):

@@ -32,7 +32,7 @@ struct Shape {
   long long row_elems() const { return (long long)H * W * Cp(); }
 };
 
-enum LayerKind { L_CONV, L_DENSE, L_GAP, L_BLOCK };
+enum LayerKind { L_CONV, L_DENSE, L_GAP, L_BLOCK, L_MAXPOOL, L_PROJ };
 
 struct Layer {
   LayerKind kind;
@@ -170,6 +170,25 @@ dycl_status plan_subnet(dycl_graph g, Subnet& s, const Shape& in, int sn_id) {
         L.out = Shape{1, 1, cur.C};
         cur = L.out;
         break;
+      case L_MAXPOOL: {
+        const int Ho = (cur.H + 2 * L.pad - L.k) / L.stride + 1;
+        const int Wo = (cur.W + 2 * L.pad - L.k) / L.stride + 1;
+        if (Ho <= 0 || Wo <= 0 || cur.C % 8) return fail(g, DYCL_E_SHAPE_MISMATCH, std::string(where) + "maxpool shape");
+        L.out = Shape{Ho, Wo, cur.C};
+        cur = L.out;
+        break;
+      }
+      case L_PROJ: {
+        if (!have_block) return fail(g, DYCL_E_SHAPE_MISMATCH, std::string(where) + "projection without block_begin");
+        L.in = block_src;
+        if ((int)L.w.size() != L.cout * block_src.C)
+          return fail(g, DYCL_E_SHAPE_MISMATCH, std::string(where) + "projection c_in disagrees with the saved tensor");
+        L.out = Shape{(block_src.H - 1) / L.stride + 1, (block_src.W - 1) / L.stride + 1, L.cout};
+        L.K = block_src.Cp();
+        L.Kp = (L.K + 63) / 64 * 64;
+        block_src = L.out;            // the projection is now the shortcut
+        break;
+      }
       case L_CONV: {
         if ((int)L.w.size() != L.cout * L.k * L.k * cur.C)
           return fail(g, DYCL_E_SHAPE_MISMATCH, std::string(where) + "conv weight size != c_out*k*k*c_in");
@@ -227,7 +246,7 @@ dycl_status plan_subnet(dycl_graph g, Subnet& s, const Shape& in, int sn_id) {
 
 dycl_status upload_subnet(dycl_graph g, Subnet& s) {
   for (Layer& L : s.layers) {
-    if (L.kind == L_CONV || (L.kind == L_DENSE && !L.out_fp32)) {
+    if (L.kind == L_CONV || L.kind == L_PROJ || (L.kind == L_DENSE && !L.out_fp32)) {
       // repack to [Cout][k][k][Cp] padded along K to Kp (zeros)
       const int Cin = L.in.C, Cp = L.in.Cp();
       std::vector<uint16_t> wp((size_t)L.cout * L.Kp, 0);
@@ -331,6 +350,52 @@ struct Exec {
       if (L.kind == L_GAP || (L.kind == L_DENSE && L.out_fp32))
         return fail(g, DYCL_E_UNSUPPORTED, "head layers inside a sequential subnet");
       const bool last = li + 1 == s.layers.size();
+      if (L.kind == L_MAXPOOL) {
+        const bool stream_mp = fp32_stream() && (last || s.layers[li + 1].kind == L_BLOCK);
+        Tensor o = (last && out_hint.b >= 0) ? out_hint : pick_tensor(stream_mp, {cur, shortcut, busy, out_hint});
+        if (o.b < 0 || (stream_mp && o.f < 0)) return fail(g, DYCL_E_STATE, "internal: out of activation buffers");
+        if (!stream_mp) o.f = -1;
+        dycl::PoolArgs pa{};
+        pa.x = g->buf[cur.b];
+        pa.x32 = cur.f >= 0 ? g->buf32[cur.f] : nullptr;
+        pa.y = g->buf[o.b];
+        pa.y32 = o.f >= 0 ? g->buf32[o.f] : nullptr;
+        pa.n_live = cnt;
+        pa.H = L.in.H; pa.W = L.in.W; pa.C = L.in.Cp(); pa.Ho = L.out.H; pa.Wo = L.out.W;
+        pa.k = L.k; pa.stride = L.stride; pa.pad = L.pad;
+        prof_begin(DYCL_K_POOL, cnt, (pa.x32 ? 4.0 : 2.0) * L.in.row_elems() + (o.f >= 0 ? 6.0 : 2.0) * L.out.row_elems(), 0, 0);
+        cudaError_t e = dycl::launch_maxpool(pa, batch, g->num_sms, st);
+        prof_end();
+        if (e != cudaSuccess) return cuda_fail(g, e, "launch_maxpool");
+        cur = o;
+        continue;
+      }
+      if (L.kind == L_PROJ) {
+        // shortcut <- conv1x1/stride(shortcut): a residual-stream tensor
+        Tensor o = pick_tensor(fp32_stream(), {cur, shortcut, busy, out_hint});
+        if (o.b < 0 || (fp32_stream() && o.f < 0)) return fail(g, DYCL_E_STATE, "internal: out of activation buffers");
+        if (!fp32_stream()) o.f = -1;
+        dycl::ConvArgs a{};
+        a.x = g->buf[shortcut.b];
+        a.w = L.d_w;
+        a.bias = L.d_b;
+        a.y = g->buf[o.b];
+        a.y32 = o.f >= 0 ? g->buf32[o.f] : nullptr;
+        a.n_live = cnt;
+        a.H = L.in.H; a.W = L.in.W; a.C = L.in.Cp();
+        a.Ho = L.out.H; a.Wo = L.out.W; a.Cout = L.out.C;
+        a.ksz = 1; a.stride = L.stride; a.pad = 0;
+        a.K = L.K; a.Kp = L.Kp;
+        a.relu = 0;
+        a.dbg = g->conv_dbg;
+        prof_begin(DYCL_K_CONV, cnt, 2.0 * L.in.row_elems() + (o.f >= 0 ? 6.0 : 2.0) * L.out.row_elems(),
+                   2.0 * L.out.H * L.out.W * L.out.C * (double)L.in.C, 2.0 * L.out.C * L.Kp);
+        cudaError_t e = dycl::launch_conv(a, batch, g->num_sms, st, g->conv_path);
+        prof_end();
+        if (e != cudaSuccess) return cuda_fail(g, e, "launch_conv(projection)");
+        shortcut = o;
+        continue;
+      }
       const bool stream = fp32_stream() && (last || L.residual || s.layers[li + 1].kind == L_BLOCK);
       Tensor o = (last && out_hint.b >= 0) ? out_hint : pick_tensor(stream, {cur, shortcut, busy, out_hint});
       if (o.b < 0 || (stream && o.f < 0)) return fail(g, DYCL_E_STATE, "internal: out of activation buffers");
@@ -647,6 +712,32 @@ dycl_status dycl_subnet_dense(dycl_graph g, dycl_node sn, int n_in, int n_out, c
   return DYCL_OK;
 }
 
+dycl_status dycl_subnet_projection(dycl_graph g, dycl_node sn, int c_in, int c_out, int stride,
+                                   const uint16_t* w_bf16, const float* bias) {
+  if (dycl_status s = check_sn(g, sn)) return s;
+  if (!w_bf16 || !bias || c_in <= 0 || c_out <= 0 || stride < 1 || stride > 2)
+    return fail(g, DYCL_E_INVALID_ARG, "projection: bad argument");
+  if (c_out % 16) return fail(g, DYCL_E_UNSUPPORTED, "projection: c_out must be a multiple of 16");
+  Layer L;
+  L.kind = L_PROJ;
+  L.cout = c_out; L.k = 1; L.stride = stride; L.pad = 0;
+  L.w.assign(w_bf16, w_bf16 + (size_t)c_out * c_in);
+  L.b.assign(bias, bias + c_out);
+  g->subnets[sn].layers.push_back(std::move(L));
+  return DYCL_OK;
+}
+
+dycl_status dycl_subnet_maxpool(dycl_graph g, dycl_node sn, int k, int stride, int pad) {
+  if (dycl_status s = check_sn(g, sn)) return s;
+  if (k < 1 || k > 7 || stride < 1 || stride > 4 || pad < 0 || pad >= k)
+    return fail(g, DYCL_E_INVALID_ARG, "maxpool: bad argument");
+  Layer L;
+  L.kind = L_MAXPOOL;
+  L.k = k; L.stride = stride; L.pad = pad;
+  g->subnets[sn].layers.push_back(std::move(L));
+  return DYCL_OK;
+}
+
 dycl_status dycl_subnet_gap(dycl_graph g, dycl_node sn) {
   if (dycl_status s = check_sn(g, sn)) return s;
   Layer L;
@@ -734,7 +825,7 @@ dycl_status dycl_finalize(dycl_graph g, int64_t max_batch) {
     if (s) return s;
     // registration-time c_in / n_in must agree with propagated shapes
     for (const Layer& L : g->subnets[sn].layers) {
-      if (L.kind == L_CONV && (long long)L.w.size() != (long long)L.cout * L.k * L.k * L.in.C)
+      if ((L.kind == L_CONV || L.kind == L_PROJ) && (long long)L.w.size() != (long long)L.cout * L.k * L.k * L.in.C)
         return fail(g, DYCL_E_SHAPE_MISMATCH, "conv2d c_in disagrees with the propagated shape");
       if (L.kind == L_DENSE && (long long)L.w.size() != (long long)L.cout * L.in.C)
         return fail(g, DYCL_E_SHAPE_MISMATCH, "dense n_in disagrees with the propagated shape");

@@ -288,7 +288,71 @@ __global__ void __launch_bounds__(256) k_gather(const GatherArgs a) {
   }
 }
 
+// ------------------------------------------------------------------ max pool
+// one thread per (sample, output pixel, 8-channel group); consecutive threads =
+// consecutive output pixels of one group (planar stores coalesce).
+__global__ void k_maxpool(const PoolArgs a) {
+  const int n_live = *a.n_live;
+  const int G = a.C / 8;
+  const int HWo = a.Ho * a.Wo;
+  const int64_t total = (int64_t)n_live * G * HWo;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total; u += (int64_t)gridDim.x * blockDim.x) {
+    const int p = (int)(u % HWo);
+    const int64_t t = u / HWo;
+    const int g = (int)(t % G);
+    const int64_t n = t / G;
+    const int ho = p / a.Wo, wo = p - (p / a.Wo) * a.Wo;
+    float m[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) m[j] = -INFINITY;
+    for (int r = 0; r < a.k; ++r) {
+      const int hi = ho * a.stride - a.pad + r;
+      if (hi < 0 || hi >= a.H) continue;
+      for (int s2 = 0; s2 < a.k; ++s2) {
+        const int wi = wo * a.stride - a.pad + s2;
+        if (wi < 0 || wi >= a.W) continue;
+        const int64_t pix = (int64_t)hi * a.W + wi;
+        if (a.x32) {
+          const float4* q = reinterpret_cast<const float4*>(a.x32 + (n * a.H * a.W + pix) * a.C + g * 8);
+          const float4 v0 = __ldg(q), v1 = __ldg(q + 1);
+          m[0] = fmaxf(m[0], v0.x); m[1] = fmaxf(m[1], v0.y); m[2] = fmaxf(m[2], v0.z); m[3] = fmaxf(m[3], v0.w);
+          m[4] = fmaxf(m[4], v1.x); m[5] = fmaxf(m[5], v1.y); m[6] = fmaxf(m[6], v1.z); m[7] = fmaxf(m[7], v1.w);
+        } else {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.x + ((n * G + g) * (int64_t)a.H * a.W + pix) * 8));
+          const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            m[2 * j] = fmaxf(m[2 * j], __uint_as_float(w4[j] << 16));
+            m[2 * j + 1] = fmaxf(m[2 * j + 1], __uint_as_float(w4[j] & 0xFFFF0000u));
+          }
+        }
+      }
+    }
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      __nv_bfloat162 v = __floats2bfloat162_rn(m[2 * j], m[2 * j + 1]);
+      o[j] = *reinterpret_cast<uint32_t*>(&v);
+    }
+    *reinterpret_cast<uint4*>(a.y + ((n * G + g) * (int64_t)HWo + p) * 8) = make_uint4(o[0], o[1], o[2], o[3]);
+    if (a.y32) {
+      float4* q = reinterpret_cast<float4*>(a.y32 + (n * HWo + p) * a.C + g * 8);
+      q[0] = make_float4(m[0], m[1], m[2], m[3]);
+      q[1] = make_float4(m[4], m[5], m[6], m[7]);
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_maxpool(const PoolArgs& a, int max_rows, int num_sms, cudaStream_t s) {
+  const int64_t total = (int64_t)max_rows * (a.C / 8) * a.Ho * a.Wo;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > (int64_t)num_sms * 16) blocks = (int64_t)num_sms * 16;
+  if (blocks < 1) blocks = 1;
+  k_maxpool<<<(int)blocks, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_cast_pad(const float* in, uint16_t* out, int64_t n, int hw, int c, int cp, cudaStream_t s) {
   const int64_t npix = n * hw;

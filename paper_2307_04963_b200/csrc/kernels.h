@@ -107,4 +107,16 @@ struct GatherArgs {
 };
 cudaError_t launch_gather(const GatherArgs& a, int max_rows, int num_sms, cudaStream_t s);
 
+// Max pooling (k x k, stride, pad) of a tensor pair: input fp32 NHWC (x32) if given,
+// else bf16 channel-planar (x); output bf16 channel-planar (y) and fp32 NHWC (y32, optional).
+struct PoolArgs {
+  const uint16_t* x;
+  const float* x32;
+  uint16_t* y;
+  float* y32;
+  const int* n_live;
+  int H, W, C, Ho, Wo, k, stride, pad;
+};
+cudaError_t launch_maxpool(const PoolArgs& a, int max_rows, int num_sms, cudaStream_t s);
+
 }  // namespace dycl

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "libdycl.so")
 
 DYCL_ACT_NONE = 0
 DYCL_ACT_RELU = 1
-KIND_NAMES = {0: "input", 1: "conv", 2: "head", 3: "compact", 4: "gather", 5: "scatter", 6: "init"}
+KIND_NAMES = {0: "input", 1: "conv", 2: "head", 3: "compact", 4: "gather", 5: "scatter", 6: "init", 7: "pool"}
 
 _STATUS = {0: "DYCL_OK", -1: "DYCL_E_INVALID_ARG", -2: "DYCL_E_SHAPE_MISMATCH", -3: "DYCL_E_SIGNATURE",
            -4: "DYCL_E_SHAPE_JOIN", -5: "DYCL_E_STATE", -6: "DYCL_E_UNSUPPORTED", -7: "DYCL_E_OOM",
@@ -38,7 +38,7 @@ class dycl_io(ctypes.Structure):
 _lib = None
 EXPORTS = [
     "dycl_graph_create", "dycl_graph_set_precision", "dycl_graph_destroy", "dycl_last_error", "dycl_subnet_begin", "dycl_subnet_block_begin",
-    "dycl_subnet_conv2d", "dycl_subnet_dense", "dycl_subnet_gap", "dycl_subnet_end", "dycl_seq", "dycl_exit",
+    "dycl_subnet_conv2d", "dycl_subnet_dense", "dycl_subnet_gap", "dycl_subnet_projection", "dycl_subnet_maxpool", "dycl_subnet_end", "dycl_seq", "dycl_exit",
     "dycl_gate", "dycl_final", "dycl_finalize", "dycl_run", "dycl_run_host", "dycl_num_count_slots",
     "dycl_launches_per_run", "dycl_num_classes", "dycl_set_profiling", "dycl_profile_read",
     "dycl_debug_conv2d",
@@ -66,6 +66,8 @@ def lib():
             "dycl_subnet_conv2d": [vp, i32, i32, i32, i32, i32, i32, P16, Pf, i32, i32],
             "dycl_subnet_dense": [vp, i32, i32, i32, P16, Pf, i32, i32],
             "dycl_subnet_gap": [vp, i32],
+            "dycl_subnet_projection": [vp, i32, i32, i32, i32, P16, Pf],
+            "dycl_subnet_maxpool": [vp, i32, i32, i32, i32],
             "dycl_subnet_end": [vp, i32],
             "dycl_seq": [vp, i32],
             "dycl_exit": [vp, i32, f32],
@@ -157,6 +159,16 @@ def dycl_subnet_dense(g, sn, n_in, n_out, w_bf16, bias, act, out_fp32):
     w, wp = _u16(w_bf16)
     b, bp = _f32(bias)
     _ck(lib().dycl_subnet_dense(g, sn, n_in, n_out, wp, bp, act, int(out_fp32)), g)
+
+
+def dycl_subnet_projection(g, sn, c_in, c_out, stride, w_bf16, bias):
+    w, wp = _u16(w_bf16)
+    b, bp = _f32(bias)
+    _ck(lib().dycl_subnet_projection(g, sn, c_in, c_out, stride, wp, bp), g)
+
+
+def dycl_subnet_maxpool(g, sn, k, stride, pad):
+    _ck(lib().dycl_subnet_maxpool(g, sn, k, stride, pad), g)
 
 
 def dycl_subnet_gap(g, sn):

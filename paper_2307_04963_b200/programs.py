@@ -134,4 +134,40 @@ def build_skipnet_resnet38(W, max_batch, device=0, thr=None, precision=FP32_STRE
     return Model(g, (32, 32, 3), 10, max_batch, "skipnet_resnet38")
 
 
-BUILDERS = {1: build_mlp_ee, 2: build_sdn_resnet56, 3: build_skipnet_resnet38}
+R50_LAYERS = (3, 4, 6, 3)
+R50_WIDTHS = (64, 128, 256, 512)
+
+
+def build_resnet50_ee(W, max_batch, device=0, tau=None, precision=FP32_STREAM, hw=224) -> Model:
+    """Config 5, rewritten: one sub-network per stage (stem + maxpool fused into the first),
+    exits after stages 1-3, final head after stage 4 (1000 classes)."""
+    tau = float(W["tau"]) if tau is None else tau
+    g = _create(device, hw, hw, 3, precision)
+    c_in = 64
+    for s in range(1, 5):
+        sn = D.dycl_subnet_begin(g)
+        if s == 1:
+            D.dycl_subnet_conv2d(g, sn, 3, 64, 7, 2, 3, W["stem.w"], W["stem.b"], RELU, 0)
+            D.dycl_subnet_maxpool(g, sn, 3, 2, 1)
+        w = R50_WIDTHS[s - 1]
+        for b in range(R50_LAYERS[s - 1]):
+            p = f"s{s}b{b}"
+            stride = 2 if (b == 0 and s > 1) else 1
+            D.dycl_subnet_block_begin(g, sn)
+            D.dycl_subnet_conv2d(g, sn, c_in, w, 1, 1, 0, W[f"{p}.c1.w"], W[f"{p}.c1.b"], RELU, 0)
+            D.dycl_subnet_conv2d(g, sn, w, w, 3, stride, 1, W[f"{p}.c2.w"], W[f"{p}.c2.b"], RELU, 0)
+            if b == 0:
+                D.dycl_subnet_projection(g, sn, c_in, 4 * w, stride, W[f"{p}.proj.w"], W[f"{p}.proj.b"])
+            D.dycl_subnet_conv2d(g, sn, w, 4 * w, 1, 1, 0, W[f"{p}.c3.w"], W[f"{p}.c3.b"], RELU, 1)
+            c_in = 4 * w
+        D.dycl_subnet_end(g, sn)
+        D.dycl_seq(g, sn)
+        if s < 4:
+            D.dycl_exit(g, _head(g, W, f"ic{s - 1}", c_in), tau)
+        else:
+            D.dycl_final(g, _head(g, W, "final", c_in))
+    D.dycl_finalize(g, max_batch)
+    return Model(g, (hw, hw, 3), 1000, max_batch, "resnet50_ee")
+
+
+BUILDERS = {1: build_mlp_ee, 2: build_sdn_resnet56, 3: build_skipnet_resnet38, 5: build_resnet50_ee}

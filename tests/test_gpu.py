@@ -242,3 +242,25 @@ def test_cfg2_full_batch_sampled_parity(r56):
     r = report(lg[idx], pg[idx], lo, po, pr)
     print("cfg2 full sampled", r)
     assert r["logit_rel_fail"] == 0 and r["outside_band_mismatch"] <= 1
+
+
+# ------------------------------------------------------------------- config 5
+@pytest.fixture(scope="module")
+def r50():
+    W = wl.resnet50_ee_weights()
+    return W, P.build_resnet50_ee(W, 64)
+
+
+def test_gpu_input_generator_matches_numpy():
+    a = wl.image_inputs(wl.INPUT_SEED, 123, 3, hw=224)
+    b = wl.image_inputs_torch(wl.INPUT_SEED, 123, 3, hw=224, device="cuda").cpu().numpy()
+    assert np.array_equal(a, b)
+
+
+def test_cfg5_resnet50_parity(r50):
+    W, m = r50
+    X = wl.image_inputs(wl.INPUT_SEED, 4000, 24, hw=224)
+    r, lg, pg = _parity(W, m, O.resnet50_ee, X)
+    print("cfg5", r)
+    assert r["logit_rel_fail"] == 0
+    assert r["outside_band_mismatch"] <= 1, r

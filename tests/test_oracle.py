@@ -259,3 +259,74 @@ def test_skipnet_calibrated_gates_branch(r38):
 def test_band_exclusion():
     assert in_band([("exit", 0.9004, 0.9)])
     assert not in_band([("exit", 0.902, 0.9), ("gate", 0.3, 0.5)])
+
+
+# ------------------------------------------------------------------- config 5
+def test_maxpool_is_torch_maxpool():
+    rng = np.random.default_rng(3)
+    h = rng.standard_normal((13, 12, 8))
+    y = O.maxpool2d(h, 3, 2, 1)
+    t = torch.nn.functional.max_pool2d(torch.tensor(h).permute(2, 0, 1)[None], 3, 2, 1)[0].permute(1, 2, 0).numpy()
+    np.testing.assert_array_equal(y, t)
+
+
+def _torchvision_r50(W):
+    """torchvision's ResNet-50 (v1.5) with our weights; BatchNorm reduced to a pure bias
+    (weight 1, running mean 0, var 1 - eps -> y = x + b up to one fp64 rounding)."""
+    import torchvision
+    m = torchvision.models.resnet50(weights=None).double().eval()
+
+    def setc(conv, bn, name):
+        w = np.asarray(W[name + ".w"])
+        w = (w.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+        conv.weight.data = torch.tensor(w).permute(0, 3, 1, 2).contiguous()
+        bn.weight.data.fill_(1.0)
+        bn.bias.data = torch.tensor(np.asarray(W[name + ".b"], np.float64))
+        bn.running_mean.zero_()
+        bn.running_var.fill_(1.0 - bn.eps)
+
+    setc(m.conv1, m.bn1, "stem")
+    for s, layer in enumerate([m.layer1, m.layer2, m.layer3, m.layer4], start=1):
+        for b, blk in enumerate(layer):
+            p = f"s{s}b{b}"
+            setc(blk.conv1, blk.bn1, p + ".c1")
+            setc(blk.conv2, blk.bn2, p + ".c2")
+            setc(blk.conv3, blk.bn3, p + ".c3")
+            if blk.downsample is not None:
+                setc(blk.downsample[0], blk.downsample[1], p + ".proj")
+    fw = np.asarray(W["final.w"])
+    m.fc.weight.data = torch.tensor((fw.astype(np.uint32) << 16).view(np.float32).astype(np.float64))
+    m.fc.bias.data = torch.tensor(np.asarray(W["final.b"], np.float64))
+    return m
+
+
+def test_resnet50_never_exit_is_torchvision_resnet50():
+    """tau > 1: the early-exit ResNet-50 program is torchvision's resnet50 (the v1.5 topology:
+    stride in the 3x3, 1x1 projection shortcuts, 3x3/2 max-pool) with BN folded -- library
+    special case, fp64, on a 64x64 input (the topology is resolution independent)."""
+    W = wl.resnet50_ee_weights()
+    m = _torchvision_r50(W)
+    P = prg.prepare(W)
+    X = wl.image_inputs(wl.INPUT_SEED, 0, 1, hw=64)
+    z, path, preds = O.resnet50_ee(X[0], P, "exact", tau=1.5)
+    assert path == 3 and len(preds) == 3
+    xt = torch.tensor(X[0]).to(torch.bfloat16).double().permute(2, 0, 1)[None]
+    with torch.no_grad():
+        ref = m(xt)[0].numpy()
+    np.testing.assert_allclose(z, ref, rtol=1e-10, atol=1e-10)
+
+
+def test_resnet50_exit_after_stage1_is_prefix():
+    """tau <= 1/K: every sample exits after stage 1 with IC0's logits on GAP(layer1(stem))."""
+    W = wl.resnet50_ee_weights()
+    m = _torchvision_r50(W)
+    P = prg.prepare(W)
+    X = wl.image_inputs(wl.INPUT_SEED, 1, 1, hw=64)
+    z, path, _ = O.resnet50_ee(X[0], P, "exact", tau=1e-4)
+    assert path == 0
+    xt = torch.tensor(X[0]).to(torch.bfloat16).double().permute(2, 0, 1)[None]
+    with torch.no_grad():
+        h = m.layer1(m.maxpool(m.relu(m.bn1(m.conv1(xt)))))
+        g = h.mean(dim=(2, 3))[0].numpy()
+    wf = prg._bf16_to_f64(W["ic0.w"])
+    np.testing.assert_allclose(z, wf @ g + W["ic0.b"], rtol=1e-10, atol=1e-10)

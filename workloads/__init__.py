@@ -281,8 +281,117 @@ def skipnet_r38_weights(seed: int = WEIGHT_SEED, calib=None) -> dict:
     return W
 
 
+# ----------------------------------------------------------------------------
+# Config 5: early-exit ResNet-50 v1.5 (torchvision topology, BN folded into biases).
+# ----------------------------------------------------------------------------
+R50_LAYERS = (3, 4, 6, 3)
+R50_WIDTHS = (64, 128, 256, 512)
+R50_EXIT_AFTER_STAGE = (1, 2, 3)          # SURVEY §8(c) reading R6: exits after stages 1, 2, 3 + final
+R50_CLASSES = 1000
+
+
+def r50_blocks():
+    """[(stage, block, c_in, width, c_out, stride)] in program order."""
+    out = []
+    c_in = 64
+    for s, (n, w) in enumerate(zip(R50_LAYERS, R50_WIDTHS)):
+        for b in range(n):
+            stride = 2 if (b == 0 and s > 0) else 1
+            out.append((s + 1, b, c_in, w, 4 * w, stride))
+            c_in = 4 * w
+    return out
+
+
+def r50_raw_heads(seed: int = WEIGHT_SEED) -> dict:
+    rng = np.random.default_rng([seed, 5000])
+    out = {}
+    for k, st in enumerate(R50_EXIT_AFTER_STAGE):
+        c = 4 * R50_WIDTHS[st - 1]
+        out[f"ic{k}"] = rng.standard_normal((R50_CLASSES, c)) / math.sqrt(c)
+    out["final"] = rng.standard_normal((R50_CLASSES, 2048)) / math.sqrt(2048)
+    return out
+
+
+def resnet50_ee_weights(seed: int = WEIGHT_SEED, calib=None) -> dict:
+    """Config 5: early-exit ResNet-50.  Conv weights [Co][k][k][Ci] bf16; conv3 of every
+    bottleneck scaled by 1/sqrt(16) (16 residual blocks) to keep the stream bounded."""
+    rng = _Rng(seed + 50)
+    W = {}
+    W["stem.w"] = _bf16(_he_conv(rng.next(), 64, 7, 3))
+    W["stem.b"] = _bias(rng.next(), 64)
+    for (s, b, ci, w, co, stride) in r50_blocks():
+        p = f"s{s}b{b}"
+        W[f"{p}.c1.w"] = _bf16(_he_conv(rng.next(), w, 1, ci))
+        W[f"{p}.c1.b"] = _bias(rng.next(), w)
+        W[f"{p}.c2.w"] = _bf16(_he_conv(rng.next(), w, 3, w))
+        W[f"{p}.c2.b"] = _bias(rng.next(), w)
+        W[f"{p}.c3.w"] = _bf16(_he_conv(rng.next(), co, 1, w, 1.0 / math.sqrt(16)))
+        W[f"{p}.c3.b"] = _bias(rng.next(), co)
+        if b == 0:
+            W[f"{p}.proj.w"] = _bf16(_he_conv(rng.next(), co, 1, ci))
+            W[f"{p}.proj.b"] = _bias(rng.next(), co)
+    if calib is None:
+        calib = load_calib("cfg5")
+    raw = r50_raw_heads(seed)
+    for name, H in raw.items():
+        c = H.shape[1]
+        if calib is not None:
+            scale, mu = calib[name]["scale"], np.array(calib[name]["mu"])
+        else:
+            scale, mu = 1.0, np.zeros(c)
+        W[f"{name}.w"], W[f"{name}.b"] = _centered_head(H, scale, mu)
+    W["tau"] = np.float32(EXIT_TAU)
+    return W
+
+
+def image_inputs_torch(seed: int, start: int, count: int, hw: int, device="cuda"):
+    """The SAME counter-based generator as image_inputs(), evaluated with torch on a
+    device (for config 5's 39.5 GB of inputs).  Integer hash: int64 with wrap-around
+    and masked logical shifts; per-pixel float math: the identical sequence of fp32
+    IEEE operations (separate kernels, no fused multiply-add), so values are
+    bit-identical to the numpy path (tests/test_workloads.py checks this).
+    Per-sample gamma/beta come from the numpy path (4 transcendental draws per sample)."""
+    import torch
+    idx = np.arange(start, start + count, dtype=np.int64)
+    nrm = _per_sample_normals(seed, idx, 4, stream=7)
+    gamma = torch.from_numpy(np.exp(0.5 * nrm[:, 0]).astype(np.float32)).to(device)
+    beta = torch.from_numpy((0.5 * nrm[:, 1:4]).astype(np.float32)).to(device)
+    mean = torch.from_numpy(IMAGENET_MEAN).to(device)
+    std = torch.from_numpy(IMAGENET_STD).to(device)
+
+    def u64(v):
+        v = int(v) & 0xFFFFFFFFFFFFFFFF
+        return v - (1 << 64) if v >= (1 << 63) else v
+
+    def lsr(x, k):                         # logical shift right of int64 bit patterns
+        return (x >> k) & ((1 << (64 - k)) - 1)
+
+    n_el = hw * hw * 3
+    out = torch.empty((count, hw, hw, 3), dtype=torch.float32, device=device)
+    elem = torch.arange(n_el, dtype=torch.int64, device=device)[None, :]
+    C2, C3 = u64(0x100000001B3), u64(0x9E3779B1)
+    seed_term = u64(seed * 0xD1B54A32D192ED03)
+    blk = max(1, (1 << 25) // n_el)                     # samples per vectorised block
+    half = torch.tensor(0.5, dtype=torch.float32, device=device)
+    quarter = torch.tensor(0.25, dtype=torch.float32, device=device)
+    for i0 in range(0, count, blk):
+        i1 = min(count, i0 + blk)
+        smp = torch.arange(start + i0, start + i1, dtype=torch.int64, device=device)[:, None]
+        key = (smp * C2 + elem * C3) ^ seed_term          # stream 0
+        z = key + u64(0x9E3779B97F4A7C15)
+        z = (z ^ lsr(z, 30)) * u64(0xBF58476D1CE4E5B9)
+        z = (z ^ lsr(z, 27)) * u64(0x94D049BB133111EB)
+        z = z ^ lsr(z, 31)
+        u = (lsr(z, 40).to(torch.float32) / float(1 << 24)).view(i1 - i0, hw, hw, 3)
+        p = half + gamma[i0:i1, None, None, None] * (u - half)
+        p = p + quarter * beta[i0:i1, None, None, :]
+        out[i0:i1] = (p - mean) / std
+    return out
+
+
 CONFIGS = {
     1: dict(name="mlp_ee", batch=32, desc="tiny early-exit MLP: 3 blocks width 64, 2 exit heads, tau 0.9, batch 32"),
     2: dict(name="sdn_resnet56", batch=4096, desc="ShallowDeep-style early-exit ResNet-56, 32x32x3, batch 4096, 4 ICs"),
     3: dict(name="skipnet_resnet38", batch=8192, desc="SkipNet-style gated ResNet-38, 32x32x3, batch 8192, 17 gates"),
+    5: dict(name="resnet50_ee", batch=65536, desc="early-exit ResNet-50, 224x224x3, batch 65536, exits after stages 1-3"),
 }
