@@ -81,7 +81,7 @@ __device__ __forceinline__ void conv_finish16(const ConvArgs& a, int n, int ho, 
     for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.0f);
   }
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < 2 && a.y; ++h) {
     uint4 o;
     o.x = pack_bf16x2_rn(f[8 * h + 0], f[8 * h + 1]);
     o.y = pack_bf16x2_rn(f[8 * h + 2], f[8 * h + 3]);

@@ -330,3 +330,104 @@ def test_resnet50_exit_after_stage1_is_prefix():
         g = h.mean(dim=(2, 3))[0].numpy()
     wf = prg._bf16_to_f64(W["ic0.w"])
     np.testing.assert_allclose(z, wf @ g + W["ic0.b"], rtol=1e-10, atol=1e-10)
+
+
+# ------------------------------------------------------------------- config 4
+@pytest.fixture(scope="module")
+def s2s():
+    from oracle import seq2seq as S
+    W = wl.seq2seq_weights()
+    return W, S.prepare_s2s(W)
+
+
+def _torch_s2s(P, cfg):
+    """torch.nn Transformer layers (post-LN, ReLU, dropout 0) in fp64 with our weights."""
+    import torch.nn as nn
+    d, H, f = cfg["d"], cfg["heads"], cfg["d_ff"]
+    enc = [nn.TransformerEncoderLayer(d, H, f, dropout=0.0, batch_first=True).double().eval()
+           for _ in range(cfg["enc_layers"])]
+    dec = [nn.TransformerDecoderLayer(d, H, f, dropout=0.0, batch_first=True).double().eval()
+           for _ in range(cfg["dec_layers"])]
+    T = lambda a: torch.tensor(np.asarray(a, np.float64))  # noqa: E731
+    with torch.no_grad():
+        for l, L in enumerate(enc):
+            p = f"enc{l}"
+            L.self_attn.in_proj_weight.copy_(T(P[p + ".wqkv"]))
+            L.self_attn.in_proj_bias.copy_(T(P[p + ".bqkv"]))
+            L.self_attn.out_proj.weight.copy_(T(P[p + ".wo"]))
+            L.self_attn.out_proj.bias.copy_(T(P[p + ".bo"]))
+            L.norm1.weight.copy_(T(P[p + ".ln1.g"])); L.norm1.bias.copy_(T(P[p + ".ln1.b"]))
+            L.linear1.weight.copy_(T(P[p + ".w1"])); L.linear1.bias.copy_(T(P[p + ".b1"]))
+            L.linear2.weight.copy_(T(P[p + ".w2"])); L.linear2.bias.copy_(T(P[p + ".b2"]))
+            L.norm2.weight.copy_(T(P[p + ".ln2.g"])); L.norm2.bias.copy_(T(P[p + ".ln2.b"]))
+        for l, L in enumerate(dec):
+            p = f"dec{l}"
+            L.self_attn.in_proj_weight.copy_(T(P[p + ".wqkv"]))
+            L.self_attn.in_proj_bias.copy_(T(P[p + ".bqkv"]))
+            L.self_attn.out_proj.weight.copy_(T(P[p + ".wo"]))
+            L.self_attn.out_proj.bias.copy_(T(P[p + ".bo"]))
+            L.norm1.weight.copy_(T(P[p + ".ln1.g"])); L.norm1.bias.copy_(T(P[p + ".ln1.b"]))
+            L.multihead_attn.in_proj_weight.copy_(torch.cat([T(P[p + ".wq2"]), T(P[p + ".wkv2"])]))
+            L.multihead_attn.in_proj_bias.copy_(torch.cat([T(P[p + ".bq2"]), T(P[p + ".bkv2"])]))
+            L.multihead_attn.out_proj.weight.copy_(T(P[p + ".wo2"]))
+            L.multihead_attn.out_proj.bias.copy_(T(P[p + ".bo2"]))
+            L.norm2.weight.copy_(T(P[p + ".ln2.g"])); L.norm2.bias.copy_(T(P[p + ".ln2.b"]))
+            L.linear1.weight.copy_(T(P[p + ".w1"])); L.linear1.bias.copy_(T(P[p + ".b1"]))
+            L.linear2.weight.copy_(T(P[p + ".w2"])); L.linear2.bias.copy_(T(P[p + ".b2"]))
+            L.norm3.weight.copy_(T(P[p + ".ln3.g"])); L.norm3.bias.copy_(T(P[p + ".ln3.b"]))
+    return enc, dec
+
+
+def test_seq2seq_fixed_length_is_torch_transformer_greedy(s2s):
+    """EOS bias -inf => fixed-length greedy decoding == torch.nn Transformer layers (full-prefix
+    recompute with a causal mask each step), exact mode: tokens equal, logits to 1e-9."""
+    from oracle import seq2seq as S
+    W, P = s2s
+    cfg = dict(wl.S2S)
+    src = wl.token_inputs(wl.INPUT_SEED, 7, 1)[0]
+    steps = 6
+    out, L, top1, z0, _ = S.greedy_decode(src, P, cfg, "exact", eos_bias=lambda t, s: -np.inf, max_steps=steps)
+    enc, dec = _torch_s2s(P, cfg)
+    d = cfg["d"]
+    pe = torch.tensor(S.positional_encoding(64, d))
+    with torch.no_grad():
+        x = torch.tensor(P["src_emb"][src]) * math.sqrt(d) + pe[:len(src)]
+        m = x[None]
+        for L_ in enc:
+            m = L_(m)
+        y = [cfg["bos"]]
+        for t in range(steps):
+            yt = torch.tensor(P["tgt_emb"][np.array(y)]) * math.sqrt(d) + pe[:len(y)]
+            h = yt[None]
+            mask = torch.triu(torch.full((len(y), len(y)), float("-inf"), dtype=torch.float64), 1)
+            for L_ in dec:
+                h = L_(h, m, tgt_mask=mask)
+            z = torch.tensor(P["lm.w"]) @ h[0, -1] + torch.tensor(P["lm.b"])
+            z[cfg["eos"]] = -np.inf
+            tok = int(torch.argmax(z))
+            assert tok == out[t], (t, tok, out[t])
+            assert abs(float(z[tok]) - top1[t]) < 1e-9
+            if t == 0:
+                zz = z.numpy().copy()
+                zz[cfg["eos"]] = 0
+                z0c = z0.copy()
+                z0c[cfg["eos"]] = 0
+                np.testing.assert_allclose(z0c, zz, rtol=1e-9, atol=1e-9)
+            y.append(tok)
+
+
+def test_seq2seq_length_guard(s2s):
+    """Loop guard: EOS bias +inf ends every sequence after 1 token; with the length table the
+    sequence ends at floor(LEN[src0]) + 1 when margins are large (beta = 16); PAD after done."""
+    from oracle import seq2seq as S
+    W, P = s2s
+    cfg = dict(wl.S2S)
+    src = wl.token_inputs(wl.INPUT_SEED, 0, 3)
+    for i in range(3):
+        out, L, top1, _, _ = S.greedy_decode(src[i], P, cfg, "exact", eos_bias=lambda t, s: np.inf)
+        assert L == 1 and out[0] == cfg["eos"] and np.all(out[1:] == cfg["pad"]) and np.isnan(top1[1:]).all()
+    for i in range(2):
+        out, L, top1, _, preds = S.greedy_decode(src[i], P, cfg, "exact")
+        assert L == int(np.floor(P["len_table"][src[i][0]])) + 1
+        assert out[L - 1] == cfg["eos"] and np.all(out[L:] == cfg["pad"]) and cfg["eos"] not in out[:L - 1]
+        assert len(preds) == L

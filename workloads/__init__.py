@@ -389,9 +389,68 @@ def image_inputs_torch(seed: int, start: int, count: int, hw: int, device="cuda"
     return out
 
 
+# ----------------------------------------------------------------------------
+# Config 4: 6+6 post-LN Transformer seq2seq, greedy decode with an EOS/length guard.
+# ----------------------------------------------------------------------------
+S2S = dict(vocab=32000, d=512, heads=8, d_ff=2048, enc_layers=6, dec_layers=6, src_len=64, max_len=64,
+           pad=0, bos=1, eos=2, beta=16.0)
+
+
+def token_inputs(seed: int, start: int, count: int, src_len: int = 64, vocab: int = 32000) -> np.ndarray:
+    """int32 [count, src_len], tokens uniform on [3, vocab) (PAD/BOS/EOS never appear)."""
+    idx = np.arange(start, start + count, dtype=np.uint64)[:, None]
+    e = np.arange(src_len, dtype=np.uint64)[None, :]
+    u = counter_uniform(seed, idx, e, stream=11)
+    return (3 + np.floor(u * (vocab - 3))).astype(np.int32)
+
+
+def seq2seq_weights(seed: int = WEIGHT_SEED) -> dict:
+    """Embeddings N(0,1); linears N(0, 1/fan_in) (bf16); biases U(-0.05, 0.05);
+    LayerNorm gamma = 1 + U(-0.1, 0.1), beta = U(-0.05, 0.05) (fp32).
+    Length table LEN[v] = U{0..63} + 0.5 (fp32): with beta = 16 the EOS bias
+    beta*(t+1-LEN[src[0]]) makes a sequence end after ~LEN+1 tokens."""
+    c = S2S
+    rng = _Rng(seed + 40)
+    d, f, V = c["d"], c["d_ff"], c["vocab"]
+
+    def lin(n_out, n_in):
+        return _bf16(rng.next().standard_normal((n_out, n_in)) / math.sqrt(n_in))
+
+    def ln():
+        r = rng.next()
+        return (1.0 + r.uniform(-0.1, 0.1, d)).astype(np.float32), r.uniform(-0.05, 0.05, d).astype(np.float32)
+
+    W = {"src_emb": _bf16(rng.next().standard_normal((V, d))), "tgt_emb": _bf16(rng.next().standard_normal((V, d)))}
+    for l in range(c["enc_layers"]):
+        p = f"enc{l}"
+        W[p + ".wqkv"], W[p + ".bqkv"] = lin(3 * d, d), _bias(rng.next(), 3 * d)
+        W[p + ".wo"], W[p + ".bo"] = lin(d, d), _bias(rng.next(), d)
+        W[p + ".ln1.g"], W[p + ".ln1.b"] = ln()
+        W[p + ".w1"], W[p + ".b1"] = lin(f, d), _bias(rng.next(), f)
+        W[p + ".w2"], W[p + ".b2"] = lin(d, f), _bias(rng.next(), d)
+        W[p + ".ln2.g"], W[p + ".ln2.b"] = ln()
+    for l in range(c["dec_layers"]):
+        p = f"dec{l}"
+        W[p + ".wqkv"], W[p + ".bqkv"] = lin(3 * d, d), _bias(rng.next(), 3 * d)
+        W[p + ".wo"], W[p + ".bo"] = lin(d, d), _bias(rng.next(), d)
+        W[p + ".ln1.g"], W[p + ".ln1.b"] = ln()
+        W[p + ".wq2"], W[p + ".bq2"] = lin(d, d), _bias(rng.next(), d)
+        W[p + ".wkv2"], W[p + ".bkv2"] = lin(2 * d, d), _bias(rng.next(), 2 * d)
+        W[p + ".wo2"], W[p + ".bo2"] = lin(d, d), _bias(rng.next(), d)
+        W[p + ".ln2.g"], W[p + ".ln2.b"] = ln()
+        W[p + ".w1"], W[p + ".b1"] = lin(f, d), _bias(rng.next(), f)
+        W[p + ".w2"], W[p + ".b2"] = lin(d, f), _bias(rng.next(), d)
+        W[p + ".ln3.g"], W[p + ".ln3.b"] = ln()
+    W["lm.w"], W["lm.b"] = lin(V, d), _bias(rng.next(), V)
+    W["len_table"] = (rng.next().integers(0, c["max_len"], V) + 0.5).astype(np.float32)
+    W["beta"] = np.float32(c["beta"])
+    return W
+
+
 CONFIGS = {
     1: dict(name="mlp_ee", batch=32, desc="tiny early-exit MLP: 3 blocks width 64, 2 exit heads, tau 0.9, batch 32"),
     2: dict(name="sdn_resnet56", batch=4096, desc="ShallowDeep-style early-exit ResNet-56, 32x32x3, batch 4096, 4 ICs"),
     3: dict(name="skipnet_resnet38", batch=8192, desc="SkipNet-style gated ResNet-38, 32x32x3, batch 8192, 17 gates"),
+    4: dict(name="seq2seq", batch=1024, desc="6+6 Transformer d=512 greedy decode, EOS/max-len 64 guard, batch 1024"),
     5: dict(name="resnet50_ee", batch=65536, desc="early-exit ResNet-50, 224x224x3, batch 65536, exits after stages 1-3"),
 }
