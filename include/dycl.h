@@ -205,6 +205,67 @@ dycl_status dycl_set_profiling(dycl_graph g, int enable);
 dycl_status dycl_profile_read(dycl_graph g, int32_t max_n, int32_t* kind, float* ms,
                               double* bytes, double* flops, int32_t* n_out);
 
+/* ---------------------------------------------- generative DyNN (config 4) --- */
+/* A sequence-to-sequence Transformer decoded greedily under a per-sequence loop guard:
+ * the paper's generative DyNNs (AttentionNet), whose `If` node tests the
+ * output token to decide whether generation is complete (L265), with the constant
+ * maximum-iteration flag the paper prescribes (L267-268).  Rewritten form: an encoder
+ * sub-network run once, a decoder-step sub-network + LM head run inside the guarded
+ * loop; per step the guard is evaluated on the device and the still-active sequences
+ * are compacted (KV caches stay in slot order), so the loop has no host round trip.
+ * Post-LN layers (x = LN(x + SA(x)); [x = LN(x + CA(x, mem))]; x = LN(x + FFN(x))),
+ * ReLU FFN, sinusoidal PE, embeddings x sqrt(d_model), head dim 64, no final norm. */
+typedef struct dycl_s2s_s* dycl_s2s;
+typedef struct {
+  int vocab, d_model, heads, d_ff, enc_layers, dec_layers;
+  int src_len;           /* <= 64, every source sequence has exactly this length   */
+  int max_len;           /* <= 64, the loop's constant iteration bound (L267)      */
+  int pad, bos, eos;
+} dycl_s2s_config;
+/* Weights of one layer (host pointers, copied).  bf16 matrices are [n_out][n_in];
+ * q|k|v stacked in wqkv [3d][d]; cross-attention: wq2 [d][d], k|v stacked in wkv2 [2d][d].
+ * ln_sa / ln_ca / ln_ff: LayerNorm after self-attention / cross-attention (decoder only,
+ * NULL for encoder layers) / feed-forward; gamma, beta fp32 [d]; eps 1e-5. */
+typedef struct {
+  const uint16_t* wqkv; const float* bqkv;
+  const uint16_t* wo;   const float* bo;
+  const float* ln_sa_g; const float* ln_sa_b;
+  const uint16_t* wq2;  const float* bq2;
+  const uint16_t* wkv2; const float* bkv2;
+  const uint16_t* wo2;  const float* bo2;
+  const float* ln_ca_g; const float* ln_ca_b;
+  const uint16_t* w1;   const float* b1;
+  const uint16_t* w2;   const float* b2;
+  const float* ln_ff_g; const float* ln_ff_b;
+} dycl_s2s_layer;
+
+dycl_status dycl_s2s_create(int cuda_device, const dycl_s2s_config* cfg, dycl_s2s* out);
+dycl_status dycl_s2s_destroy(dycl_s2s s);
+const char* dycl_s2s_last_error(dycl_s2s s);
+/* src_emb, tgt_emb: bf16 [vocab][d_model]. */
+dycl_status dycl_s2s_set_embeddings(dycl_s2s s, const uint16_t* src_emb, const uint16_t* tgt_emb);
+dycl_status dycl_s2s_add_encoder_layer(dycl_s2s s, const dycl_s2s_layer* w);
+dycl_status dycl_s2s_add_decoder_layer(dycl_s2s s, const dycl_s2s_layer* w);
+/* Untied LM head: w bf16 [vocab][d_model], b fp32 [vocab]. */
+dycl_status dycl_s2s_set_lm_head(dycl_s2s s, const uint16_t* w, const float* b);
+/* The loop guard (the logic node on the output token): at step t the EOS logit gets
+ * beta * (t + 1 - len_table[src[0]]) added (len_table fp32 [vocab]; pass beta = 0 for the
+ * plain argmax guard); tok = argmax (lowest index on ties); a sequence is done after it
+ * emits EOS (EOS counted in its length) or after max_len steps; PAD fills the rest. */
+dycl_status dycl_s2s_set_loop_guard(dycl_s2s s, const float* len_table, float beta);
+dycl_status dycl_s2s_finalize(dycl_s2s s, int64_t max_batch);
+/* Device buffers: src int32 [batch][src_len]; tokens int32 [batch][max_len] (out);
+ * lengths int32 [batch] (out); top1 fp32 [batch][max_len] (out, the chosen token's logit,
+ * NaN after done) or NULL; logits0 fp32 [batch][vocab] (out, step-0 logits incl. the
+ * guard bias) or NULL.  Stream-ordered, no host synchronisation. */
+dycl_status dycl_s2s_run(dycl_s2s s, const int32_t* src, int64_t batch, int32_t* tokens, int32_t* lengths,
+                         float* top1, float* logits0, void* stream);
+/* Host buffers (src, tokens, lengths): H2D copy, run, D2H copy, synchronise. */
+dycl_status dycl_s2s_run_host(dycl_s2s s, const int32_t* src_host, int64_t batch, int32_t* tokens_host,
+                              int32_t* lengths_host, void* stream);
+/* Number of this library's kernels the last run launched. */
+dycl_status dycl_s2s_launches(dycl_s2s s, int32_t* out);
+
 /* ------------------------------------------------------------ test hook ---- */
 /* Run ONE conv2d layer (the a1 tensor-core kernel, same code path dycl_run uses)
  * on caller-owned device buffers and synchronise.  For element-wise kernel tests.

@@ -1,0 +1,366 @@
+// libdycl: the generative-DyNN graph (config 4) -- registration, loop-guard executor.
+//
+// P_Host for a generative DyNN: run the encoder sub-network
+// once, then the decoder-step sub-network inside a loop bounded by the constant max_len;
+// the logic node on the output token (EOS / length guard) runs on the device every step
+// and the still-active sequences are compacted (k_compact), so the next step's kernels
+// process exactly the active rows.  KV caches stay in slot order (rows carry their slot).
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/dycl.h"
+#include "kernels.h"
+#include "s2s_kernels.h"
+
+namespace {
+
+struct DevLayer {
+  uint16_t *wqkv = nullptr, *wo = nullptr, *wq2 = nullptr, *wkv2 = nullptr, *wo2 = nullptr, *w1 = nullptr,
+           *w2 = nullptr;
+  float *bqkv = nullptr, *bo = nullptr, *bq2 = nullptr, *bkv2 = nullptr, *bo2 = nullptr, *b1 = nullptr, *b2 = nullptr;
+  float *lsg = nullptr, *lsb = nullptr, *lcg = nullptr, *lcb = nullptr, *lfg = nullptr, *lfb = nullptr;
+};
+
+}  // namespace
+
+struct dycl_s2s_s {
+  dycl_s2s_config c{};
+  int device = 0, num_sms = 148;
+  std::string err;
+  std::vector<void*> allocs;
+  std::vector<DevLayer> enc, dec;
+  uint16_t *src_emb = nullptr, *tgt_emb = nullptr, *lm_w = nullptr;
+  float *lm_b = nullptr, *len_table = nullptr;
+  float beta = 0.f;
+  bool finalized = false;
+  int64_t max_batch = 0;
+  // workspace
+  float *x32 = nullptr, *pre = nullptr, *logits = nullptr;
+  uint16_t *xb = nullptr, *qkv = nullptr, *att = nullptr, *h = nullptr;
+  std::vector<uint16_t*> cross, cache;
+  int32_t *cur_tok = nullptr, *active[2] = {}, *list1 = nullptr, *list0 = nullptr;
+  int* counts = nullptr;
+  uint8_t* flag = nullptr;
+  int32_t *src_stage = nullptr, *tok_stage = nullptr, *len_stage = nullptr;
+  int launches = 0;
+};
+
+static thread_local std::string g_s2s_err;
+
+namespace {
+
+dycl_status sfail(dycl_s2s s, dycl_status st, const std::string& m) {
+  if (s) s->err = m; else g_s2s_err = m;
+  return st;
+}
+#define SCK(call)                                                                   \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess) return sfail(s, DYCL_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <typename T>
+dycl_status upload(dycl_s2s s, T** dst, const T* src, size_t n) {
+  if (!src) return sfail(s, DYCL_E_INVALID_ARG, "null weight pointer");
+  void* p = nullptr;
+  if (cudaMalloc(&p, n * sizeof(T)) != cudaSuccess) return sfail(s, DYCL_E_OOM, "cudaMalloc (weights)");
+  s->allocs.push_back(p);
+  SCK(cudaMemcpy(p, src, n * sizeof(T), cudaMemcpyHostToDevice));
+  *dst = static_cast<T*>(p);
+  return DYCL_OK;
+}
+template <typename T>
+dycl_status alloc(dycl_s2s s, T** dst, size_t n) {
+  void* p = nullptr;
+  if (cudaMalloc(&p, (n ? n : 1) * sizeof(T)) != cudaSuccess) return sfail(s, DYCL_E_OOM, "cudaMalloc (workspace)");
+  s->allocs.push_back(p);
+  *dst = static_cast<T*>(p);
+  return DYCL_OK;
+}
+
+dycl_status add_layer(dycl_s2s s, const dycl_s2s_layer* w, bool decoder) {
+  if (!s || !w) return DYCL_E_INVALID_ARG;
+  if (s->finalized) return sfail(s, DYCL_E_STATE, "already finalized");
+  const size_t d = s->c.d_model, f = s->c.d_ff;
+  DevLayer L;
+  dycl_status r;
+  if ((r = upload(s, &L.wqkv, w->wqkv, 3 * d * d)) || (r = upload(s, &L.bqkv, w->bqkv, 3 * d)) ||
+      (r = upload(s, &L.wo, w->wo, d * d)) || (r = upload(s, &L.bo, w->bo, d)) ||
+      (r = upload(s, &L.lsg, w->ln_sa_g, d)) || (r = upload(s, &L.lsb, w->ln_sa_b, d)) ||
+      (r = upload(s, &L.w1, w->w1, f * d)) || (r = upload(s, &L.b1, w->b1, f)) ||
+      (r = upload(s, &L.w2, w->w2, d * f)) || (r = upload(s, &L.b2, w->b2, d)) ||
+      (r = upload(s, &L.lfg, w->ln_ff_g, d)) || (r = upload(s, &L.lfb, w->ln_ff_b, d)))
+    return r;
+  if (decoder) {
+    if ((r = upload(s, &L.wq2, w->wq2, d * d)) || (r = upload(s, &L.bq2, w->bq2, d)) ||
+        (r = upload(s, &L.wkv2, w->wkv2, 2 * d * d)) || (r = upload(s, &L.bkv2, w->bkv2, 2 * d)) ||
+        (r = upload(s, &L.wo2, w->wo2, d * d)) || (r = upload(s, &L.bo2, w->bo2, d)) ||
+        (r = upload(s, &L.lcg, w->ln_ca_g, d)) || (r = upload(s, &L.lcb, w->ln_ca_b, d)))
+      return r;
+    s->dec.push_back(L);
+  } else {
+    s->enc.push_back(L);
+  }
+  return DYCL_OK;
+}
+
+struct S2SExec {
+  dycl_s2s s;
+  cudaStream_t st;
+  int B;
+  int n = 0;
+
+  // y = act(x W^T + b [+ res]) on rows [0, *cnt) through the tcgen05 GEMM path (a dense
+  // layer = 1x1 conv on [rows][1][1][K]).
+  cudaError_t gemm(const uint16_t* x, int K, const uint16_t* w, const float* b, int N, const float* res32,
+                   uint16_t* yb, float* y32, int relu, const int* cnt, int n_static, int max_rows) {
+    dycl::ConvArgs a{};
+    a.x = x; a.w = w; a.bias = b; a.res32 = res32; a.res_mode = res32 ? 1 : 0;
+    a.y = yb; a.y32 = y32; a.n_live = cnt; a.n_static = n_static;
+    a.H = a.W = a.Ho = a.Wo = 1; a.C = K; a.Cout = N; a.ksz = 1; a.stride = 1; a.pad = 0;
+    a.K = K; a.Kp = K; a.relu = relu;
+    a.rH = a.rW = 1; a.rC = N;
+    ++n;
+    return dycl::launch_conv(a, max_rows, s->num_sms, st, 0);
+  }
+  cudaError_t ln(const float* in, const float* g, const float* b, const int* cnt, int n_static, int max_rows) {
+    dycl::S2SLnArgs a{in, g, b, s->x32, s->xb, cnt, n_static, s->c.d_model, 1e-5f};
+    ++n;
+    return dycl::launch_layernorm(a, max_rows, st);
+  }
+
+  dycl_status run(const int32_t* src, int32_t* tokens, int32_t* lengths, float* top1, float* logits0) {
+    const dycl_s2s_config& c = s->c;
+    const int d = c.d_model, S = c.src_len, R = B * S;
+    cudaError_t e;
+#define E(x)                                                                        \
+  do {                                                                              \
+    e = (x);                                                                        \
+    if (e != cudaSuccess) return sfail(s, DYCL_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e)); \
+  } while (0)
+    dycl::S2SInitArgs ia{tokens, top1, s->cur_tok, lengths, s->active[0], s->counts, B, c.max_len, c.pad, c.bos};
+    E(dycl::launch_s2s_init(ia, st));
+    ++n;
+    // ---------------- encoder sub-network (once), rows = B*S tokens
+    dycl::S2SEmbedArgs ea{s->src_emb, src, nullptr, nullptr, s->x32, s->xb, nullptr, R, d, S, 0};
+    E(dycl::launch_embed(ea, R, st));
+    ++n;
+    for (const DevLayer& L : s->enc) {
+      E(gemm(s->xb, d, L.wqkv, L.bqkv, 3 * d, nullptr, s->qkv, nullptr, 0, nullptr, R, R));
+      dycl::S2SAttnArgs aa{};
+      aa.qkv = s->qkv; aa.out = s->att; aa.n_static = B; aa.d = d; aa.heads = c.heads; aa.S = S;
+      E(dycl::launch_attn_encoder(aa, B, st));
+      ++n;
+      E(gemm(s->att, d, L.wo, L.bo, d, s->x32, nullptr, s->pre, 0, nullptr, R, R));
+      E(ln(s->pre, L.lsg, L.lsb, nullptr, R, R));
+      E(gemm(s->xb, d, L.w1, L.b1, c.d_ff, nullptr, s->h, nullptr, 1, nullptr, R, R));
+      E(gemm(s->h, c.d_ff, L.w2, L.b2, d, s->x32, nullptr, s->pre, 0, nullptr, R, R));
+      E(ln(s->pre, L.lfg, L.lfb, nullptr, R, R));
+    }
+    // cross-attention K/V of every decoder layer from the encoder output (bf16 operand copy)
+    for (size_t l = 0; l < s->dec.size(); ++l)
+      E(gemm(s->xb, d, s->dec[l].wkv2, s->dec[l].bkv2, 2 * d, nullptr, s->cross[l], nullptr, 0, nullptr, R, R));
+    // ---------------- guarded greedy loop: t < max_len (the constant bound), active rows only
+    int cur = 0;
+    const int* cnt = s->counts;
+    for (int t = 0; t < c.max_len; ++t) {
+      const int32_t* slot = s->active[cur];
+      dycl::S2SEmbedArgs de{s->tgt_emb, nullptr, slot, s->cur_tok, s->x32, s->xb, cnt, 0, d, S, t};
+      E(dycl::launch_embed(de, B, st));
+      ++n;
+      for (size_t l = 0; l < s->dec.size(); ++l) {
+        const DevLayer& L = s->dec[l];
+        E(gemm(s->xb, d, L.wqkv, L.bqkv, 3 * d, nullptr, s->qkv, nullptr, 0, cnt, 0, B));
+        dycl::S2SAttnArgs sa{};
+        sa.qkv = s->qkv; sa.q = s->qkv; sa.q_stride = 3 * d; sa.kv = nullptr; sa.cache = s->cache[l];
+        sa.out = s->att; sa.slot = slot; sa.n_live = cnt; sa.d = d; sa.heads = c.heads; sa.S = S;
+        sa.max_len = c.max_len; sa.t = t;
+        E(dycl::launch_attn_decoder(sa, B, st));
+        ++n;
+        E(gemm(s->att, d, L.wo, L.bo, d, s->x32, nullptr, s->pre, 0, cnt, 0, B));
+        E(ln(s->pre, L.lsg, L.lsb, cnt, 0, B));
+        E(gemm(s->xb, d, L.wq2, L.bq2, d, nullptr, s->att, nullptr, 0, cnt, 0, B));
+        dycl::S2SAttnArgs ca{};
+        ca.q = s->att; ca.q_stride = d; ca.kv = s->cross[l]; ca.out = s->qkv;  // reuse qkv as scratch
+        ca.slot = slot; ca.n_live = cnt; ca.d = d; ca.heads = c.heads; ca.S = S; ca.max_len = c.max_len; ca.t = t;
+        E(dycl::launch_attn_decoder(ca, B, st));
+        ++n;
+        E(gemm(s->qkv, d, L.wo2, L.bo2, d, s->x32, nullptr, s->pre, 0, cnt, 0, B));
+        E(ln(s->pre, L.lcg, L.lcb, cnt, 0, B));
+        E(gemm(s->xb, d, L.w1, L.b1, c.d_ff, nullptr, s->h, nullptr, 1, cnt, 0, B));
+        E(gemm(s->h, c.d_ff, L.w2, L.b2, d, s->x32, nullptr, s->pre, 0, cnt, 0, B));
+        E(ln(s->pre, L.lfg, L.lfb, cnt, 0, B));
+      }
+      E(gemm(s->xb, d, s->lm_w, s->lm_b, c.vocab, nullptr, nullptr, s->logits, 0, cnt, 0, B));
+      dycl::S2SArgmaxArgs ga{s->logits, slot, src, s->len_table, s->beta, tokens, top1, logits0,
+                             s->cur_tok, lengths, s->flag, cnt, c.vocab, S, c.max_len, t, c.eos};
+      E(dycl::launch_argmax_guard(ga, B, st));
+      ++n;
+      // the logic node's decision -> stable compaction of the still-active sequences
+      int* out_counts = s->counts + 1 + 2 * t;
+      E(dycl::launch_compact(s->flag, cnt, slot, s->list1, s->list0, out_counts, s->active[cur ^ 1], 0,
+                             nullptr, 0, st));
+      ++n;
+      cnt = out_counts + 1;
+      cur ^= 1;
+    }
+#undef E
+    return DYCL_OK;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+dycl_status dycl_s2s_create(int cuda_device, const dycl_s2s_config* cfg, dycl_s2s* out) {
+  if (!cfg || !out) return sfail(nullptr, DYCL_E_INVALID_ARG, "null argument");
+  *out = nullptr;
+  if (cfg->d_model % 64 || cfg->heads * 64 != cfg->d_model || cfg->d_model > 1024 || cfg->src_len < 1 ||
+      cfg->src_len > 64 || cfg->max_len < 1 || cfg->max_len > 64 || cfg->vocab % 256 || cfg->d_ff % 256 ||
+      cfg->enc_layers < 1 || cfg->dec_layers < 1 || cfg->eos < 0 || cfg->eos >= cfg->vocab)
+    return sfail(nullptr, DYCL_E_UNSUPPORTED,
+                 "s2s config: head dim 64, d_model <= 1024, src_len/max_len <= 64, vocab and d_ff multiples of 256");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return sfail(nullptr, DYCL_E_CUDA, "no CUDA device");
+  if (cuda_device < 0 || cuda_device >= ndev) return sfail(nullptr, DYCL_E_INVALID_ARG, "bad device index");
+  int major = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, cuda_device);
+  if (major != 10) return sfail(nullptr, DYCL_E_UNSUPPORTED, "libdycl is built for sm_100a (B200) only");
+  dycl_s2s s = new (std::nothrow) dycl_s2s_s();
+  if (!s) return sfail(nullptr, DYCL_E_OOM, "host allocation");
+  s->c = *cfg;
+  s->device = cuda_device;
+  cudaSetDevice(cuda_device);
+  cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
+  *out = s;
+  return DYCL_OK;
+}
+
+dycl_status dycl_s2s_destroy(dycl_s2s s) {
+  if (!s) return DYCL_OK;
+  cudaSetDevice(s->device);
+  for (void* p : s->allocs) cudaFree(p);
+  delete s;
+  return DYCL_OK;
+}
+
+const char* dycl_s2s_last_error(dycl_s2s s) { return s ? s->err.c_str() : g_s2s_err.c_str(); }
+
+dycl_status dycl_s2s_set_embeddings(dycl_s2s s, const uint16_t* src_emb, const uint16_t* tgt_emb) {
+  if (!s) return DYCL_E_INVALID_ARG;
+  if (s->finalized) return sfail(s, DYCL_E_STATE, "already finalized");
+  cudaSetDevice(s->device);
+  const size_t n = (size_t)s->c.vocab * s->c.d_model;
+  if (dycl_status r = upload(s, &s->src_emb, src_emb, n)) return r;
+  return upload(s, &s->tgt_emb, tgt_emb, n);
+}
+
+dycl_status dycl_s2s_add_encoder_layer(dycl_s2s s, const dycl_s2s_layer* w) {
+  if (s) cudaSetDevice(s->device);
+  return add_layer(s, w, false);
+}
+dycl_status dycl_s2s_add_decoder_layer(dycl_s2s s, const dycl_s2s_layer* w) {
+  if (s) cudaSetDevice(s->device);
+  return add_layer(s, w, true);
+}
+
+dycl_status dycl_s2s_set_lm_head(dycl_s2s s, const uint16_t* w, const float* b) {
+  if (!s) return DYCL_E_INVALID_ARG;
+  if (s->finalized) return sfail(s, DYCL_E_STATE, "already finalized");
+  cudaSetDevice(s->device);
+  if (dycl_status r = upload(s, &s->lm_w, w, (size_t)s->c.vocab * s->c.d_model)) return r;
+  return upload(s, &s->lm_b, b, (size_t)s->c.vocab);
+}
+
+dycl_status dycl_s2s_set_loop_guard(dycl_s2s s, const float* len_table, float beta) {
+  if (!s) return DYCL_E_INVALID_ARG;
+  if (s->finalized) return sfail(s, DYCL_E_STATE, "already finalized");
+  cudaSetDevice(s->device);
+  s->beta = beta;
+  std::vector<float> zeros;
+  if (!len_table) {
+    zeros.assign(s->c.vocab, 0.f);
+    len_table = zeros.data();
+  }
+  return upload(s, &s->len_table, len_table, (size_t)s->c.vocab);
+}
+
+dycl_status dycl_s2s_finalize(dycl_s2s s, int64_t max_batch) {
+  if (!s) return DYCL_E_INVALID_ARG;
+  if (s->finalized) return sfail(s, DYCL_E_STATE, "already finalized");
+  if (max_batch <= 0 || max_batch > 65536) return sfail(s, DYCL_E_INVALID_ARG, "bad max_batch");
+  if (s->enc.size() != (size_t)s->c.enc_layers || s->dec.size() != (size_t)s->c.dec_layers || !s->src_emb ||
+      !s->lm_w)
+    return sfail(s, DYCL_E_STATE, "missing layers / embeddings / LM head");
+  if (!s->len_table)
+    if (dycl_status r = dycl_s2s_set_loop_guard(s, nullptr, 0.f)) return r;
+  SCK(cudaSetDevice(s->device));
+  const size_t B = max_batch, d = s->c.d_model, S = s->c.src_len, R = B * S, L = s->c.max_len;
+  dycl_status r;
+  if ((r = alloc(s, &s->x32, R * d)) || (r = alloc(s, &s->pre, R * d)) || (r = alloc(s, &s->xb, R * d)) ||
+      (r = alloc(s, &s->qkv, R * 3 * d)) || (r = alloc(s, &s->att, R * d)) ||
+      (r = alloc(s, &s->h, R * (size_t)s->c.d_ff)) || (r = alloc(s, &s->logits, B * (size_t)s->c.vocab)) ||
+      (r = alloc(s, &s->cur_tok, B)) || (r = alloc(s, &s->active[0], B)) || (r = alloc(s, &s->active[1], B)) ||
+      (r = alloc(s, &s->list1, B)) || (r = alloc(s, &s->list0, B)) || (r = alloc(s, &s->counts, 2 * L + 2)) ||
+      (r = alloc(s, &s->flag, B)))
+    return r;
+  s->cross.resize(s->dec.size());
+  s->cache.resize(s->dec.size());
+  for (size_t l = 0; l < s->dec.size(); ++l)
+    if ((r = alloc(s, &s->cross[l], R * 2 * d)) || (r = alloc(s, &s->cache[l], B * L * 2 * d))) return r;
+  s->max_batch = max_batch;
+  s->finalized = true;
+  return DYCL_OK;
+}
+
+dycl_status dycl_s2s_run(dycl_s2s s, const int32_t* src, int64_t batch, int32_t* tokens, int32_t* lengths,
+                         float* top1, float* logits0, void* stream) {
+  if (!s) return DYCL_E_INVALID_ARG;
+  if (!s->finalized) return sfail(s, DYCL_E_STATE, "not finalized");
+  if (batch < 0 || batch > s->max_batch) return sfail(s, DYCL_E_SHAPE_MISMATCH, "batch > max_batch");
+  if (batch == 0) return DYCL_OK;
+  if (!src || !tokens || !lengths) return sfail(s, DYCL_E_INVALID_ARG, "null io pointer");
+  SCK(cudaSetDevice(s->device));
+  SCK(cudaGetLastError());
+  S2SExec ex{s, (cudaStream_t)stream, (int)batch};
+  dycl_status r = ex.run(src, tokens, lengths, top1, logits0);
+  s->launches = ex.n;
+  return r;
+}
+
+dycl_status dycl_s2s_run_host(dycl_s2s s, const int32_t* src_host, int64_t batch, int32_t* tokens_host,
+                              int32_t* lengths_host, void* stream) {
+  if (!s) return DYCL_E_INVALID_ARG;
+  if (!s->finalized) return sfail(s, DYCL_E_STATE, "not finalized");
+  if (batch < 0 || batch > s->max_batch) return sfail(s, DYCL_E_SHAPE_MISMATCH, "batch > max_batch");
+  if (batch == 0) return DYCL_OK;
+  SCK(cudaSetDevice(s->device));
+  const size_t B = s->max_batch;
+  if (!s->src_stage) {
+    dycl_status r;
+    if ((r = alloc(s, &s->src_stage, B * s->c.src_len)) || (r = alloc(s, &s->tok_stage, B * s->c.max_len)) ||
+        (r = alloc(s, &s->len_stage, B)))
+      return r;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  SCK(cudaMemcpyAsync(s->src_stage, src_host, (size_t)batch * s->c.src_len * 4, cudaMemcpyHostToDevice, st));
+  if (dycl_status r = dycl_s2s_run(s, s->src_stage, batch, s->tok_stage, s->len_stage, nullptr, nullptr, stream))
+    return r;
+  SCK(cudaMemcpyAsync(tokens_host, s->tok_stage, (size_t)batch * s->c.max_len * 4, cudaMemcpyDeviceToHost, st));
+  SCK(cudaMemcpyAsync(lengths_host, s->len_stage, (size_t)batch * 4, cudaMemcpyDeviceToHost, st));
+  SCK(cudaStreamSynchronize(st));
+  return DYCL_OK;
+}
+
+dycl_status dycl_s2s_launches(dycl_s2s s, int32_t* out) {
+  if (!s || !out) return DYCL_E_INVALID_ARG;
+  *out = s->launches;
+  return DYCL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,293 @@
+// Config 4 (generative DyNN) kernels: token embedding + sinusoidal PE, LayerNorm,
+// multi-head attention (encoder self, decoder causal self with KV-cache append,
+// cross), and the LM-head argmax with the EOS / length loop guard.
+//
+// Numerics (R13): residual stream fp32; every tensor-core operand and the
+// q/k/v, K/V caches, attention outputs bf16 (RNE); softmax / LayerNorm / logits fp32.
+// All reductions are fixed-order warp trees (batch-position independent).
+#include <cuda_bf16.h>
+
+#include "s2s_kernels.h"
+
+namespace dycl {
+namespace {
+
+__device__ __forceinline__ float bf(uint16_t u) { return __uint_as_float((uint32_t)u << 16); }
+__device__ __forceinline__ uint16_t to_bf(float f) {
+  __nv_bfloat16 h = __float2bfloat16_rn(f);
+  return *reinterpret_cast<uint16_t*>(&h);
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// x = emb[tok] * sqrt(d) + PE(pos); one warp per row, d / 32 elements per lane.
+__global__ void k_embed(const S2SEmbedArgs a) {
+  const int n = a.n_live ? *a.n_live : a.n_static;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  int tok, pos;
+  if (a.src) {                       // encoder: row = b*S + i
+    tok = a.src[warp];
+    pos = warp % a.S;
+  } else {                           // decoder step: row -> slot
+    const int slot = a.slot[warp];
+    tok = a.cur_tok[slot];
+    pos = a.t;
+  }
+  const uint16_t* e = a.table + (size_t)tok * a.d;
+  const float sd = sqrtf((float)a.d);
+  for (int c = lane; c < a.d; c += 32) {
+    const int i2 = c & ~1;
+    const float ang = (float)pos / powf(10000.0f, (float)i2 / (float)a.d);
+    const float pe = (c & 1) ? cosf(ang) : sinf(ang);
+    const float v = bf(e[c]) * sd + pe;
+    a.x32[(size_t)warp * a.d + c] = v;
+    a.xb[(size_t)warp * a.d + c] = to_bf(v);
+  }
+}
+
+// LayerNorm of [rows][d] fp32 (d <= 1024): warp per row, biased variance, eps.
+__global__ void k_layernorm(const S2SLnArgs a) {
+  const int n = a.n_live ? *a.n_live : a.n_static;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  const float* x = a.in + (size_t)warp * a.d;
+  float v[32];
+  const int per = a.d / 32;
+  float s = 0.f;
+  for (int j = 0; j < per; ++j) {
+    v[j] = x[lane + 32 * j];
+    s += v[j];
+  }
+  const float mu = warp_sum(s) / (float)a.d;
+  float q = 0.f;
+  for (int j = 0; j < per; ++j) {
+    const float dd = v[j] - mu;
+    q += dd * dd;
+  }
+  const float rstd = rsqrtf(warp_sum(q) / (float)a.d + a.eps);
+  for (int j = 0; j < per; ++j) {
+    const int c = lane + 32 * j;
+    const float y = (v[j] - mu) * rstd * a.gamma[c] + a.beta[c];
+    a.out32[(size_t)warp * a.d + c] = y;
+    a.outb[(size_t)warp * a.d + c] = to_bf(y);
+  }
+}
+
+// Encoder self-attention: one CTA per (sequence, head), S <= 64 tokens, head dim 64.
+// qkv: bf16 [B*S][3d] (q | k | v), out: bf16 [B*S][d].
+__global__ void __launch_bounds__(128) k_attn_encoder(const S2SAttnArgs a) {
+  __shared__ float sk[64][65];
+  __shared__ float sv[64][65];
+  __shared__ float sq[4][64];
+  __shared__ float sp[4][64];
+  const int b = blockIdx.x / a.heads, h = blockIdx.x % a.heads;
+  const int n_seq = a.n_live ? *a.n_live : a.n_static;
+  if (b >= n_seq) return;
+  const int S = a.S, d = a.d, dh = 64;
+  const uint16_t* base = a.qkv + (size_t)b * S * 3 * d;
+  for (int i = threadIdx.x; i < S * dh; i += blockDim.x) {
+    const int j = i / dh, c = i % dh;
+    sk[j][c] = bf(base[(size_t)j * 3 * d + d + h * dh + c]);
+    sv[j][c] = bf(base[(size_t)j * 3 * d + 2 * d + h * dh + c]);
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float scale = 0.125f;          // 1/sqrt(64)
+  for (int i = warp; i < S; i += 4) {
+    sq[warp][lane] = bf(base[(size_t)i * 3 * d + h * dh + lane]);
+    sq[warp][lane + 32] = bf(base[(size_t)i * 3 * d + h * dh + lane + 32]);
+    __syncwarp();
+    float s0 = -INFINITY, s1 = -INFINITY;
+    if (lane < S) {
+      float acc = 0.f;
+      for (int c = 0; c < dh; ++c) acc += sq[warp][c] * sk[lane][c];
+      s0 = acc * scale;
+    }
+    if (lane + 32 < S) {
+      float acc = 0.f;
+      for (int c = 0; c < dh; ++c) acc += sq[warp][c] * sk[lane + 32][c];
+      s1 = acc * scale;
+    }
+    const float m = warp_max(fmaxf(s0, s1));
+    const float e0 = lane < S ? expf(s0 - m) : 0.f, e1 = lane + 32 < S ? expf(s1 - m) : 0.f;
+    const float inv = 1.f / warp_sum(e0 + e1);
+    sp[warp][lane] = e0 * inv;
+    sp[warp][lane + 32] = e1 * inv;
+    __syncwarp();
+    float o0 = 0.f, o1 = 0.f;
+    for (int j = 0; j < S; ++j) {
+      o0 += sp[warp][j] * sv[j][lane];
+      o1 += sp[warp][j] * sv[j][lane + 32];
+    }
+    uint16_t* out = a.out + ((size_t)b * S + i) * d + h * dh;
+    out[lane] = to_bf(o0);
+    out[lane + 32] = to_bf(o1);
+    __syncwarp();
+  }
+}
+
+// Decoder attention for one query per active row, one warp per (row, head).
+//   self  (kv == nullptr): append this row's k, v (from qkv) at position t of the slot's
+//         cache, then attend over positions 0..t of the cache;
+//   cross (kv != nullptr): attend over the S encoder positions of the slot's cross K/V.
+__global__ void __launch_bounds__(256) k_attn_decoder(const S2SAttnArgs a) {
+  const int n = a.n_live ? *a.n_live : a.n_static;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int row = gw / a.heads, h = gw % a.heads;
+  if (row >= n) return;
+  const int slot = a.slot[row];
+  const int d = a.d, dh = 64;
+  const uint16_t* qrow = a.q + (size_t)row * a.q_stride + h * dh;
+  const float q0 = bf(qrow[lane]), q1 = bf(qrow[lane + 32]);
+  const uint16_t* kv;           // [positions][2d]: K at [0, d), V at [d, 2d)
+  int nk;
+  if (a.kv == nullptr) {
+    uint16_t* cache = a.cache + (size_t)slot * a.max_len * 2 * d;
+    const uint16_t* src = a.qkv + (size_t)row * 3 * d;
+    uint16_t* dst = cache + (size_t)a.t * 2 * d;
+    dst[h * dh + lane] = src[d + h * dh + lane];
+    dst[h * dh + lane + 32] = src[d + h * dh + lane + 32];
+    dst[d + h * dh + lane] = src[2 * d + h * dh + lane];
+    dst[d + h * dh + lane + 32] = src[2 * d + h * dh + lane + 32];
+    __syncwarp();
+    kv = cache;
+    nk = a.t + 1;
+  } else {
+    kv = a.kv + (size_t)slot * a.S * 2 * d;
+    nk = a.S;
+  }
+  // scores for keys lane and lane+32 (nk <= 64)
+  float s0 = -INFINITY, s1 = -INFINITY;
+  for (int j = 0; j < nk; ++j) {
+    const uint16_t* kj = kv + (size_t)j * 2 * d + h * dh;
+    const float p = warp_sum(q0 * bf(kj[lane]) + q1 * bf(kj[lane + 32])) * 0.125f;
+    if (j == lane) s0 = p;
+    if (j == lane + 32) s1 = p;
+  }
+  const float m = warp_max(fmaxf(s0, s1));
+  const float e0 = lane < nk ? expf(s0 - m) : 0.f, e1 = lane + 32 < nk ? expf(s1 - m) : 0.f;
+  const float inv = 1.f / warp_sum(e0 + e1);
+  float o0 = 0.f, o1 = 0.f;
+  for (int j = 0; j < nk; ++j) {
+    const float pj = __shfl_sync(0xffffffffu, j < 32 ? e0 : e1, j & 31) * inv;
+    const uint16_t* vj = kv + (size_t)j * 2 * d + d + h * dh;
+    o0 += pj * bf(vj[lane]);
+    o1 += pj * bf(vj[lane + 32]);
+  }
+  uint16_t* out = a.out + (size_t)row * d + h * dh;
+  out[lane] = to_bf(o0);
+  out[lane + 32] = to_bf(o1);
+}
+
+// LM-head argmax + EOS / length loop guard, one CTA per active row:
+//   z[EOS] += beta * (t + 1 - LEN[src[slot][0]]);  tok = argmax z (lowest index on ties)
+//   tokens[slot][t] = tok; top1[slot][t] = z[tok]; done -> length = t + 1, flag = 1
+__global__ void __launch_bounds__(256) k_argmax_guard(const S2SArgmaxArgs a) {
+  __shared__ float sv[8];
+  __shared__ int si[8];
+  const int n = *a.n_live;
+  const int row = blockIdx.x;
+  if (row >= n) return;
+  const int slot = a.slot[row];
+  const float* z = a.logits + (size_t)row * a.V;
+  const float bias = a.beta * ((float)(a.t + 1) - a.len_table[a.src[(size_t)slot * a.S]]);
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int j = threadIdx.x; j < a.V; j += blockDim.x) {
+    float v = z[j];
+    if (j == a.eos) v += bias;
+    if (a.logits0 && a.t == 0) a.logits0[(size_t)slot * a.V + j] = v;
+    if (v > best || (v == best && j < bi)) {
+      best = v;
+      bi = j;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    sv[warp] = best;
+    si[warp] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (sv[w] > best || (sv[w] == best && si[w] < bi)) {
+        best = sv[w];
+        bi = si[w];
+      }
+    a.tokens[(size_t)slot * a.max_len + a.t] = bi;
+    if (a.top1) a.top1[(size_t)slot * a.max_len + a.t] = best;
+    a.cur_tok[slot] = bi;
+    const bool done = bi == a.eos;
+    if (done) a.lengths[slot] = a.t + 1;
+    a.flag[row] = done ? 1 : 0;
+  }
+}
+
+// run start: tokens = PAD, lengths = max_len, top1 = NaN, cur_tok = BOS, active = iota, count.
+__global__ void k_s2s_init(S2SInitArgs a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) a.count[0] = a.B;
+  if (i < a.B) {
+    a.cur_tok[i] = a.bos;
+    a.lengths[i] = a.max_len;
+    a.active[i] = i;
+    for (int t = 0; t < a.max_len; ++t) {
+      a.tokens[(size_t)i * a.max_len + t] = a.pad;
+      if (a.top1) a.top1[(size_t)i * a.max_len + t] = __int_as_float(0x7fc00000);
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_embed(const S2SEmbedArgs& a, int max_rows, cudaStream_t s) {
+  const int blocks = (max_rows * 32 + 255) / 256;
+  k_embed<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_layernorm(const S2SLnArgs& a, int max_rows, cudaStream_t s) {
+  if (a.d % 32 || a.d > 1024) return cudaErrorInvalidValue;
+  const int blocks = (max_rows * 32 + 255) / 256;
+  k_layernorm<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_attn_encoder(const S2SAttnArgs& a, int max_seqs, cudaStream_t s) {
+  if (a.S > 64 || a.d / a.heads != 64) return cudaErrorInvalidValue;
+  k_attn_encoder<<<max_seqs * a.heads > 0 ? max_seqs * a.heads : 1, 128, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_attn_decoder(const S2SAttnArgs& a, int max_rows, cudaStream_t s) {
+  if (a.S > 64 || a.max_len > 64 || a.d / a.heads != 64) return cudaErrorInvalidValue;
+  const int warps = max_rows * a.heads;
+  const int blocks = (warps * 32 + 255) / 256;
+  k_attn_decoder<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_argmax_guard(const S2SArgmaxArgs& a, int max_rows, cudaStream_t s) {
+  k_argmax_guard<<<max_rows > 0 ? max_rows : 1, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_s2s_init(const S2SInitArgs& a, cudaStream_t s) {
+  k_s2s_init<<<(a.B + 255) / 256 > 0 ? (a.B + 255) / 256 : 1, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace dycl

@@ -35,8 +35,22 @@ class dycl_io(ctypes.Structure):
                 ("path", ctypes.c_void_p), ("node_counts", ctypes.c_void_p)]
 
 
+class dycl_s2s_config(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in ("vocab", "d_model", "heads", "d_ff", "enc_layers", "dec_layers",
+                                            "src_len", "max_len", "pad", "bos", "eos")]
+
+
+class dycl_s2s_layer(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in (
+        "wqkv", "bqkv", "wo", "bo", "ln_sa_g", "ln_sa_b", "wq2", "bq2", "wkv2", "bkv2", "wo2", "bo2",
+        "ln_ca_g", "ln_ca_b", "w1", "b1", "w2", "b2", "ln_ff_g", "ln_ff_b")]
+
+
 _lib = None
 EXPORTS = [
+    "dycl_s2s_create", "dycl_s2s_destroy", "dycl_s2s_last_error", "dycl_s2s_set_embeddings",
+    "dycl_s2s_add_encoder_layer", "dycl_s2s_add_decoder_layer", "dycl_s2s_set_lm_head", "dycl_s2s_set_loop_guard",
+    "dycl_s2s_finalize", "dycl_s2s_run", "dycl_s2s_run_host", "dycl_s2s_launches",
     "dycl_graph_create", "dycl_graph_set_precision", "dycl_graph_destroy", "dycl_last_error", "dycl_subnet_begin", "dycl_subnet_block_begin",
     "dycl_subnet_conv2d", "dycl_subnet_dense", "dycl_subnet_gap", "dycl_subnet_projection", "dycl_subnet_maxpool", "dycl_subnet_end", "dycl_seq", "dycl_exit",
     "dycl_gate", "dycl_final", "dycl_finalize", "dycl_run", "dycl_run_host", "dycl_num_count_slots",
@@ -83,12 +97,27 @@ def lib():
             "dycl_profile_read": [vp, i32, Pi, Pf, Pd, Pd, Pi],
             "dycl_debug_conv2d": [vp, i64, i32, i32, i32, P16, Pf, i32, i32, i32, i32, i32, vp, i32, vp, vp, i32],
         }
+        sig.update({
+            "dycl_s2s_create": [i32, ctypes.POINTER(dycl_s2s_config), ctypes.POINTER(vp)],
+            "dycl_s2s_destroy": [vp],
+            "dycl_s2s_set_embeddings": [vp, vp, vp],
+            "dycl_s2s_add_encoder_layer": [vp, ctypes.POINTER(dycl_s2s_layer)],
+            "dycl_s2s_add_decoder_layer": [vp, ctypes.POINTER(dycl_s2s_layer)],
+            "dycl_s2s_set_lm_head": [vp, vp, vp],
+            "dycl_s2s_set_loop_guard": [vp, vp, f32],
+            "dycl_s2s_finalize": [vp, i64],
+            "dycl_s2s_run": [vp, vp, i64, vp, vp, vp, vp, vp],
+            "dycl_s2s_run_host": [vp, vp, i64, vp, vp, vp],
+            "dycl_s2s_launches": [vp, Pi],
+        })
         for name, args in sig.items():
             fn = getattr(L, name)
             fn.argtypes = args
             fn.restype = ctypes.c_int
         L.dycl_last_error.argtypes = [vp]
         L.dycl_last_error.restype = ctypes.c_char_p
+        L.dycl_s2s_last_error.argtypes = [vp]
+        L.dycl_s2s_last_error.restype = ctypes.c_char_p
         _lib = L
     return _lib
 
@@ -253,3 +282,98 @@ def dycl_debug_conv2d(g, x, n, H, W, C, w_bf16, bias, c_out, k, stride, pad, rel
     _ck(lib().dycl_debug_conv2d(g, int(n), H, W, C, wp, bp, c_out, k, stride, pad, int(relu),
                                 ctypes.c_void_p(res.data_ptr() if res is not None else 0), int(res_mode),
                                 ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()), int(path)), g)
+
+
+# ------------------------------------------------------------ generative graph (config 4)
+def _s2s_ck(status, s=None):
+    if status != 0:
+        raise DyclError(status, lib().dycl_s2s_last_error(s).decode(errors="replace"))
+
+
+def _hp(a, dtype):
+    """Host pointer of a contiguous numpy copy (the caller keeps the returned array alive)."""
+    a = np.ascontiguousarray(np.asarray(a, dtype=dtype))
+    return a, ctypes.c_void_p(a.ctypes.data)
+
+
+def dycl_s2s_create(cuda_device, cfg: dict):
+    c = dycl_s2s_config(**{f: int(cfg[f]) for f, _ in dycl_s2s_config._fields_})
+    h = ctypes.c_void_p()
+    _s2s_ck(lib().dycl_s2s_create(cuda_device, ctypes.byref(c), ctypes.byref(h)))
+    return h
+
+
+def dycl_s2s_destroy(s):
+    _s2s_ck(lib().dycl_s2s_destroy(s))
+
+
+def dycl_s2s_last_error(s=None) -> str:
+    return lib().dycl_s2s_last_error(s).decode(errors="replace")
+
+
+def dycl_s2s_set_embeddings(s, src_emb, tgt_emb):
+    a, pa = _hp(src_emb, np.uint16)
+    b, pb = _hp(tgt_emb, np.uint16)
+    _s2s_ck(lib().dycl_s2s_set_embeddings(s, pa, pb), s)
+
+
+def _layer_struct(w: dict):
+    keep = []
+    kw = {}
+    for f, _ in dycl_s2s_layer._fields_:
+        v = w.get(f)
+        if v is None:
+            kw[f] = None
+            continue
+        a, p = _hp(v, np.uint16 if np.asarray(v).dtype == np.uint16 else np.float32)
+        keep.append(a)
+        kw[f] = p.value
+    return dycl_s2s_layer(**kw), keep
+
+
+def dycl_s2s_add_encoder_layer(s, w: dict):
+    st, keep = _layer_struct(w)
+    _s2s_ck(lib().dycl_s2s_add_encoder_layer(s, ctypes.byref(st)), s)
+
+
+def dycl_s2s_add_decoder_layer(s, w: dict):
+    st, keep = _layer_struct(w)
+    _s2s_ck(lib().dycl_s2s_add_decoder_layer(s, ctypes.byref(st)), s)
+
+
+def dycl_s2s_set_lm_head(s, w, b):
+    a, pa = _hp(w, np.uint16)
+    c, pc = _hp(b, np.float32)
+    _s2s_ck(lib().dycl_s2s_set_lm_head(s, pa, pc), s)
+
+
+def dycl_s2s_set_loop_guard(s, len_table, beta):
+    if len_table is None:
+        _s2s_ck(lib().dycl_s2s_set_loop_guard(s, None, float(beta)), s)
+        return
+    a, pa = _hp(len_table, np.float32)
+    _s2s_ck(lib().dycl_s2s_set_loop_guard(s, pa, float(beta)), s)
+
+
+def dycl_s2s_finalize(s, max_batch):
+    _s2s_ck(lib().dycl_s2s_finalize(s, int(max_batch)), s)
+
+
+def dycl_s2s_run(s, src, batch, tokens, lengths, top1=None, logits0=None, stream=None):
+    """Device tensors: src int32 [B][S], tokens int32 [B][L], lengths int32 [B], top1 fp32 [B][L], logits0 [B][V]."""
+    ptr = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
+    _s2s_ck(lib().dycl_s2s_run(s, ptr(src), int(batch), ptr(tokens), ptr(lengths), ptr(top1), ptr(logits0),
+                               _stream_ptr(stream)), s)
+
+
+def dycl_s2s_run_host(s, src_host, batch, tokens_host, lengths_host, stream=None):
+    def p(t):
+        return ctypes.c_void_p(t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data)
+    _s2s_ck(lib().dycl_s2s_run_host(s, p(src_host), int(batch), p(tokens_host), p(lengths_host),
+                                    _stream_ptr(stream)), s)
+
+
+def dycl_s2s_launches(s) -> int:
+    n = ctypes.c_int32()
+    _s2s_ck(lib().dycl_s2s_launches(s, ctypes.byref(n)), s)
+    return n.value

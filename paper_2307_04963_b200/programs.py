@@ -170,4 +170,55 @@ def build_resnet50_ee(W, max_batch, device=0, tau=None, precision=FP32_STREAM, h
     return Model(g, (hw, hw, 3), 1000, max_batch, "resnet50_ee")
 
 
+class Seq2Seq:
+    """Config 4: the generative graph (encoder once, decoder step + LM head under the loop guard)."""
+
+    def __init__(self, h, cfg, max_batch):
+        self.h, self.cfg, self.max_batch = h, cfg, max_batch
+
+    def run(self, src, tokens, lengths, top1=None, logits0=None, stream=None, batch=None):
+        D.dycl_s2s_run(self.h, src, src.shape[0] if batch is None else batch, tokens, lengths, top1, logits0, stream)
+
+    def run_host(self, src_host, tokens_host, lengths_host, stream=None):
+        D.dycl_s2s_run_host(self.h, src_host, src_host.shape[0], tokens_host, lengths_host, stream)
+
+    def close(self):
+        if self.h is not None:
+            D.dycl_s2s_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def build_seq2seq(W, cfg, max_batch, device=0) -> Seq2Seq:
+    """Config 4, rewritten: encoder sub-network + decoder-step sub-network + LM head, with the
+    EOS / length guard registered as the loop's logic node."""
+    cfg = dict(cfg)
+    cfg.setdefault("d_model", cfg.get("d"))
+    h = D.dycl_s2s_create(device, cfg)
+    D.dycl_s2s_set_embeddings(h, W["src_emb"], W["tgt_emb"])
+    for l in range(cfg["enc_layers"]):
+        p = f"enc{l}."
+        D.dycl_s2s_add_encoder_layer(h, dict(
+            wqkv=W[p + "wqkv"], bqkv=W[p + "bqkv"], wo=W[p + "wo"], bo=W[p + "bo"],
+            ln_sa_g=W[p + "ln1.g"], ln_sa_b=W[p + "ln1.b"], w1=W[p + "w1"], b1=W[p + "b1"],
+            w2=W[p + "w2"], b2=W[p + "b2"], ln_ff_g=W[p + "ln2.g"], ln_ff_b=W[p + "ln2.b"]))
+    for l in range(cfg["dec_layers"]):
+        p = f"dec{l}."
+        D.dycl_s2s_add_decoder_layer(h, dict(
+            wqkv=W[p + "wqkv"], bqkv=W[p + "bqkv"], wo=W[p + "wo"], bo=W[p + "bo"],
+            ln_sa_g=W[p + "ln1.g"], ln_sa_b=W[p + "ln1.b"], wq2=W[p + "wq2"], bq2=W[p + "bq2"],
+            wkv2=W[p + "wkv2"], bkv2=W[p + "bkv2"], wo2=W[p + "wo2"], bo2=W[p + "bo2"],
+            ln_ca_g=W[p + "ln2.g"], ln_ca_b=W[p + "ln2.b"], w1=W[p + "w1"], b1=W[p + "b1"],
+            w2=W[p + "w2"], b2=W[p + "b2"], ln_ff_g=W[p + "ln3.g"], ln_ff_b=W[p + "ln3.b"]))
+    D.dycl_s2s_set_lm_head(h, W["lm.w"], W["lm.b"])
+    D.dycl_s2s_set_loop_guard(h, W["len_table"], float(W["beta"]))
+    D.dycl_s2s_finalize(h, max_batch)
+    return Seq2Seq(h, cfg, max_batch)
+
+
 BUILDERS = {1: build_mlp_ee, 2: build_sdn_resnet56, 3: build_skipnet_resnet38, 5: build_resnet50_ee}

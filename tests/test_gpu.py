@@ -264,3 +264,79 @@ def test_cfg5_resnet50_parity(r50):
     print("cfg5", r)
     assert r["logit_rel_fail"] == 0
     assert r["outside_band_mismatch"] <= 1, r
+
+
+# ------------------------------------------------------------------- config 4
+@pytest.fixture(scope="module")
+def s2s_model():
+    from oracle import seq2seq as S
+    W = wl.seq2seq_weights()
+    return W, S.prepare_s2s(W), P.build_seq2seq(W, wl.S2S, 1024)
+
+
+def _run_s2s(m, src):
+    B = src.shape[0]
+    L, V = wl.S2S["max_len"], wl.S2S["vocab"]
+    s = torch.from_numpy(src).to(DEV)
+    tok = torch.full((B, L), -5, dtype=torch.int32, device=DEV)
+    ln = torch.full((B,), -5, dtype=torch.int32, device=DEV)
+    top1 = torch.empty((B, L), device=DEV)
+    z0 = torch.empty((B, V), device=DEV)
+    m.run(s, tok, ln, top1, z0)
+    torch.cuda.synchronize()
+    return tok.cpu().numpy(), ln.cpu().numpy(), top1.cpu().numpy(), z0.cpu().numpy()
+
+
+def _s2s_parity(P_, src, tok, ln, top1, z0):
+    from oracle import seq2seq as S
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle.metrics import in_band
+    with ThreadPoolExecutor(8) as ex:
+        res = list(ex.map(lambda i: S.greedy_decode(src[i], P_, wl.S2S, "mirror"), range(len(src))))
+    rep = dict(n=len(src), band_excluded=0, mismatch=0, max_top1_rel=0.0, max_z0_rel=0.0)
+    for i, (o_tok, o_len, o_top1, o_z0, preds) in enumerate(res):
+        rel0 = np.max(np.abs(z0[i] - o_z0)) / np.max(np.abs(o_z0))
+        rep["max_z0_rel"] = max(rep["max_z0_rel"], float(rel0))
+        if in_band(preds):
+            rep["band_excluded"] += 1
+            continue
+        if not (np.array_equal(tok[i], o_tok) and ln[i] == o_len):
+            rep["mismatch"] += 1
+            continue
+        k = o_len
+        r = np.max(np.abs(top1[i, :k] - o_top1[:k]) / np.maximum(1.0, np.abs(o_top1[:k])))
+        rep["max_top1_rel"] = max(rep["max_top1_rel"], float(r))
+    return rep
+
+
+@pytest.mark.parametrize("B", [8, 5, 1])
+def test_cfg4_seq2seq_parity(s2s_model, B):
+    W, P_, m = s2s_model
+    src = wl.token_inputs(wl.INPUT_SEED, 100, B)
+    tok, ln, top1, z0 = _run_s2s(m, src)
+    assert ((ln >= 1) & (ln <= 64)).all()
+    for i in range(B):                              # PAD after the end, EOS at the end (unless 64)
+        assert np.all(tok[i, ln[i]:] == wl.S2S["pad"])
+        if ln[i] < 64:
+            assert tok[i, ln[i] - 1] == wl.S2S["eos"]
+    rep = _s2s_parity(P_, src, tok, ln, top1, z0)
+    print("cfg4", B, rep)
+    assert rep["mismatch"] == 0 and rep["max_top1_rel"] <= 2e-2 and rep["max_z0_rel"] <= 2e-2, rep
+
+
+def test_cfg4_full_batch_sampled_parity(s2s_model):
+    W, P_, m = s2s_model
+    src = wl.token_inputs(wl.INPUT_SEED, 0, 1024)
+    tok, ln, top1, z0 = _run_s2s(m, src)
+    idx = np.random.default_rng(wl.ORACLE_SUBSET_SEED).choice(1024, 12, replace=False)
+    rep = _s2s_parity(P_, src[idx], tok[idx], ln[idx], top1[idx], z0[idx])
+    print("cfg4 full sampled", rep, "mean length", ln.mean())
+    assert rep["mismatch"] == 0 and rep["max_top1_rel"] <= 2e-2
+    # batch-position independence: a permuted sub-batch decodes identically
+    perm = np.random.default_rng(1).permutation(64)
+    tok2, ln2, _, _ = _run_s2s(m, src[:64][perm])
+    assert np.array_equal(tok2, tok[:64][perm]) and np.array_equal(ln2, ln[:64][perm])
+    th = np.zeros((64, 64), np.int32)
+    lh = np.zeros(64, np.int32)
+    m.run_host(src[:64], th, lh)
+    assert np.array_equal(th, tok[:64]) and np.array_equal(lh, ln[:64])
