@@ -139,11 +139,110 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+WORKLOADS = {
+    1: "cfg1: tiny early-exit MLP, 3 blocks width 64, 2 exit heads + final, tau=0.9, batch 32 random fp32 inputs",
+    2: WORKLOAD,
+    3: "cfg3: SkipNet-style gated ResNet-38, 17 feed-forward gates, synthetic 32x32x3, batch 8192",
+    4: "cfg4: 6+6 post-LN Transformer d=512, greedy decode with per-sequence EOS / max-len 64 loop guard, "
+       "batch 1024 random-token sequences (src len 64)",
+    5: "cfg5: early-exit ResNet-50 v1.5, synthetic 224x224x3, exits after stages 1/2/3 + final, batch 65536 per GPU "
+       "(processed in chunks of 2048, all inputs resident in HBM)",
+}
+BATCHES = {1: 32, 2: 4096, 3: 8192, 4: 1024, 5: 65536}
+
+
+class ImageJob:
+    """configs 1/2/3/5: one step = dycl_run over every chunk of the per-rank batch."""
+
+    def __init__(self, cfg, rank, dev, torch):
+        import workloads as wl
+        from paper_2307_04963_b200 import programs as P
+        self.cfg, self.torch = cfg, torch
+        self.B = BATCHES[cfg]
+        self.chunk = 2048 if cfg == 5 else self.B
+        W = {1: wl.mlp_weights, 2: wl.sdn_r56_weights, 3: wl.skipnet_r38_weights, 5: wl.resnet50_ee_weights}[cfg]()
+        self.model = P.BUILDERS[cfg](W, self.chunk, device=dev.index or 0)
+        g0 = rank * self.B
+        if cfg == 1:
+            X = torch.from_numpy(wl.mlp_inputs(wl.INPUT_SEED, g0, self.B)).to(dev)
+        elif cfg == 5:
+            X = wl.image_inputs_torch(wl.INPUT_SEED, g0, self.B, hw=224, device=dev)
+        else:
+            X = torch.from_numpy(wl.image_inputs(wl.INPUT_SEED, g0, self.B)).to(dev)
+        self.x = X
+        K = self.model.K
+        self.logits = torch.empty((self.B, K), device=dev)
+        self.path = torch.empty(self.B, dtype=torch.int32, device=dev)
+        self.g = self.model.g
+        self.h2d = int(X.numel() * 4)
+        self.d2h = int(self.B * (K * 4 + 4))
+
+    def step(self, stream):
+        for c0 in range(0, self.B, self.chunk):
+            c1 = min(self.B, c0 + self.chunk)
+            self.model.run(self.x[c0:c1], self.logits[c0:c1], self.path[c0:c1], stream=stream)
+
+    def host_setup(self):
+        torch = self.torch
+        self.xh = self.x.cpu().pin_memory()
+        self.lh = torch.empty(tuple(self.logits.shape), dtype=torch.float32).pin_memory()
+        self.ph = torch.empty(self.B, dtype=torch.int32).pin_memory()
+
+    def step_host(self, stream):
+        for c0 in range(0, self.B, self.chunk):
+            c1 = min(self.B, c0 + self.chunk)
+            self.model.run_host(self.xh[c0:c1], self.lh[c0:c1], self.ph[c0:c1], stream=stream)
+
+    def check_host(self):
+        return bool(np.array_equal(self.ph.numpy(), self.path.cpu().numpy()))
+
+    def hist(self):
+        p = self.path.cpu().numpy()
+        return np.bincount(p, minlength=5).tolist() if self.cfg != 3 else \
+            {"mean_blocks_executed": float(np.mean([bin(int(v)).count("1") for v in p]) + 1)}
+
+
+class S2SJob:
+    """config 4: one step = encoder + guarded greedy decode of the per-rank batch."""
+
+    def __init__(self, cfg, rank, dev, torch):
+        import workloads as wl
+        from paper_2307_04963_b200 import programs as P
+        self.cfg, self.torch = cfg, torch
+        self.B = BATCHES[4]
+        c = wl.S2S
+        self.model = P.build_seq2seq(wl.seq2seq_weights(), c, self.B, device=dev.index or 0)
+        self.g = None
+        src = wl.token_inputs(wl.INPUT_SEED, rank * self.B, self.B)
+        self.src = torch.from_numpy(src).to(dev)
+        self.tok = torch.empty((self.B, c["max_len"]), dtype=torch.int32, device=dev)
+        self.len = torch.empty(self.B, dtype=torch.int32, device=dev)
+        self.h2d = int(src.nbytes)
+        self.d2h = int(self.B * (c["max_len"] + 1) * 4)
+
+    def step(self, stream):
+        self.model.run(self.src, self.tok, self.len, stream=stream)
+
+    def host_setup(self):
+        torch = self.torch
+        self.sh = self.src.cpu().pin_memory()
+        self.th = torch.empty(tuple(self.tok.shape), dtype=torch.int32).pin_memory()
+        self.lh = torch.empty(self.B, dtype=torch.int32).pin_memory()
+
+    def step_host(self, stream):
+        self.model.run_host(self.sh, self.th, self.lh, stream=stream)
+
+    def check_host(self):
+        return bool(np.array_equal(self.lh.numpy(), self.len.cpu().numpy()))
+
+    def hist(self):
+        ln = self.len.cpu().numpy()
+        return {"mean_length": float(ln.mean()), "tokens": int(ln.sum())}
+
+
 def run_dycl(args):
     import torch
-    import workloads as wl
     from paper_2307_04963_b200 import dycl as D
-    from paper_2307_04963_b200 import programs as P
 
     ws, rank, local = _dist()
     if ws > 1:
@@ -152,17 +251,12 @@ def run_dycl(args):
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     stream = torch.cuda.current_stream()
-
-    W = wl.sdn_r56_weights()
-    model = P.build_sdn_resnet56(W, BATCH, device=local)
-    X = wl.image_inputs(wl.INPUT_SEED, rank * BATCH, BATCH)            # this rank's global slice
-    x = torch.from_numpy(X).to(dev)
-    logits = torch.empty((BATCH, 10), device=dev)
-    path = torch.empty(BATCH, dtype=torch.int32, device=dev)
+    job = (S2SJob if args.config == 4 else ImageJob)(args.config, rank, dev, torch)
+    B = job.B
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > L2 (126 MB)
 
     for _ in range(args.warmup):
-        model.run(x, logits, path, stream=stream)
+        job.step(stream)
     torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
@@ -175,47 +269,49 @@ def run_dycl(args):
     for i in range(args.steps):
         flush.zero_()                          # evict L2 between timed steps (not timed)
         ev[i][0].record(stream)
-        model.run(x, logits, path, stream=stream)
+        job.step(stream)
         ev[i][1].record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
     # Pass 2 (the roofline): the same K steps again with per-launch CUDA events recorded by
     # libdycl on the launch stream around every kernel (kept out of pass 1: ~80 event pairs
     # per step perturb the step time).
-    D.dycl_set_profiling(model.g, 1)
     conv_ms = conv_bytes = conv_flops = 0.0
     conv_launches = 0
     kind_ms = {}
-    for i in range(args.steps):
-        flush.zero_()
-        model.run(x, logits, path, stream=stream)
-        for p in D.dycl_profile_read(model.g):    # syncs the stream
-            kind_ms[p["kind"]] = kind_ms.get(p["kind"], 0.0) + p["ms"]
-            if p["kind"] == "conv":
-                conv_ms += p["ms"]
-                conv_bytes += p["bytes"]
-                conv_flops += p["flops"]
-                conv_launches += 1
-    torch.cuda.synchronize()
-    D.dycl_set_profiling(model.g, 0)
-    total_ms = sum(a.elapsed_time(b) for a, b in ev)
-    launches = D.dycl_launches_per_run(model.g) * args.steps
-    hist = np.bincount(path.cpu().numpy(), minlength=5).tolist()
+    launches = 0
+    if job.g is not None:
+        D.dycl_set_profiling(job.g, 1)
+        for i in range(args.steps):
+            flush.zero_()
+            job.step(stream)     # profiling records the last chunk's launches; chunks are identical in shape
+            for p in D.dycl_profile_read(job.g):    # syncs the stream
+                kind_ms[p["kind"]] = kind_ms.get(p["kind"], 0.0) + p["ms"]
+                if p["kind"] == "conv":
+                    conv_ms += p["ms"]
+                    conv_bytes += p["bytes"]
+                    conv_flops += p["flops"]
+                    conv_launches += 1
+        torch.cuda.synchronize()
+        D.dycl_set_profiling(job.g, 0)
+        launches = D.dycl_launches_per_run(job.g) * args.steps * ((B + job.chunk - 1) // job.chunk)
+    else:
+        launches = D.dycl_s2s_launches(job.model.h) * args.steps
+    hist = job.hist()
 
-    # e2e: the public host-buffer call (pinned input; H2D + run + D2H each step)
-    xh = torch.from_numpy(X).pin_memory()
-    lh = torch.empty((BATCH, 10), dtype=torch.float32).pin_memory()
-    ph = torch.empty(BATCH, dtype=torch.int32).pin_memory()
-    model.run_host(xh, lh, ph, stream=stream)
+    # e2e: the public host-buffer call (pinned buffers; H2D + run + D2H each step)
+    job.host_setup()
+    job.step_host(stream)
     torch.cuda.synchronize()
     e2e_ms = 0.0
     for i in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        model.run_host(xh, lh, ph, stream=stream)
+        job.step_host(stream)
         e2e_ms += (time.perf_counter() - t0) * 1e3
-    assert np.array_equal(ph.numpy(), path.cpu().numpy()), "host-buffer run disagrees with device run"
+    assert job.check_host(), "host-buffer run disagrees with device run"
 
     t = torch.tensor([total_ms, e2e_ms], dtype=torch.float64, device=dev)
     if ws > 1:
@@ -228,47 +324,86 @@ def run_dycl(args):
         return
 
     hbm, tf_burst, tf_sus, peak_src = _peaks()
-    value = BATCH * ws * args.steps / (total_ms / 1e3)
-    achieved = conv_bytes / (conv_ms / 1e3) / 1e9 if conv_ms else 0.0
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "conv_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    value = B * ws * args.steps / (total_ms / 1e3)
+    roof = None
+    if conv_ms:
+        achieved = conv_bytes / (conv_ms / 1e3) / 1e9
+        tflops = conv_flops / (conv_ms / 1e3) / 1e12
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "conv_traffic.json")
+        if args.config == 2 and os.path.exists(tpath):
+            try:
+                traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        if args.config == 5:       # ResNet-50 convs: tensor-bound
+            roof = {"kernel": "conv (a1: implicit-GEMM conv on tcgen05)", "bound": "tensor", "achieved": tflops,
+                    "peak": tf_sus, "unit": "TFLOP/s", "frac": tflops / tf_sus, "traffic": None,
+                    "peak_source": peak_src + " bf16 sustained", "hbm_GBps": achieved}
+        else:
+            roof = {"kernel": "k_conv_tma (a1: implicit-GEMM conv on tcgen05, fused epilogue)",
+                    "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                    "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
+                    "tensor_tflops": tflops, "tensor_frac_of_sustained": tflops / tf_sus}
+        roof.update({"share_of_step": conv_ms / sum(kind_ms.values()) if kind_ms else None,
+                     "measured": "per-launch CUDA events (libdycl profiling) over a second pass of the same "
+                                 "K steps; achieved = algorithmic bytes (or FLOPs) / kernel time",
+                     "launches_per_step": conv_launches // max(args.steps, 1)})
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "batch_per_gpu": BATCH, "global_batch": BATCH * ws,
+        "config": {"workload": WORKLOADS[args.config], "batch_per_gpu": B, "global_batch": B * ws,
                    "precision": "bf16 tensor-core operands, fp32 accumulate, fp32 residual stream",
                    "l2": "flushed (256 MB write) before every timed step, flush not timed",
                    "parallelism": f"dp{ws} (independent shards, no collective)",
-                   "exit_histogram_rank0": hist},
+                   "decisions_rank0": hist},
         "clocks": clk,
-        "e2e": {"value": BATCH * ws * args.steps / (e2e_ms / 1e3), "unit": UNIT,
-                "h2d_bytes_per_step": int(X.nbytes), "d2h_bytes_per_step": int(lh.numel() * 4 + ph.numel() * 4)},
+        "e2e": {"value": B * ws * args.steps / (e2e_ms / 1e3), "unit": UNIT,
+                "h2d_bytes_per_step": job.h2d, "d2h_bytes_per_step": job.d2h},
         "gpu_launches": launches,
-        "roofline": {"kernel": "k_conv_tma (a1: implicit-GEMM conv on tcgen05, fused epilogue)",
-                     "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
-                     "share_of_step": conv_ms / sum(kind_ms.values()) if kind_ms else None,
-                     "measured": "per-launch CUDA events (libdycl profiling) over a second pass of the same "
-                                 "K steps; achieved = algorithmic bytes / kernel time",
-                     "tensor_tflops": conv_flops / (conv_ms / 1e3) / 1e12 if conv_ms else 0.0,
-                     "tensor_frac_of_sustained": (conv_flops / (conv_ms / 1e3) / 1e12) / tf_sus if conv_ms else 0.0,
-                     "launches_per_step": conv_launches // max(args.steps, 1)},
+        "roofline": roof,
         "kernel_ms_per_step": {k: v / args.steps for k, v in sorted(kind_ms.items(), key=lambda kv: -kv[1])},
     }
+    if args.config == 4:
+        line["tokens_per_s"] = hist["tokens"] * ws * args.steps / (total_ms / 1e3)
     if ws == 1 and not args.no_cpu_baseline:
-        rate, cores, dt = cpu_oracle_rate(args.cpu_samples)
+        n_cpu = {1: 4096, 2: args.cpu_samples, 3: 2048, 4: 48, 5: 32}[args.config]
+        rate, cores, dt, what = cpu_oracle_rate_cfg(args.config, n_cpu)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
-                                "sample": f"{args.cpu_samples} cfg2 samples (seeded inputs 0..{args.cpu_samples - 1}), "
-                                          f"per-sample fp64 interpreter, mirror mode, {dt:.1f} s wall"}
+                                "sample": f"{what}, {dt:.1f} s wall"}
     print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def cpu_oracle_rate_cfg(cfg, n):
+    """The oracle on this host's cores for a bounded sample of config `cfg`."""
+    import oracle as O
+    import workloads as wl
+    from oracle import programs as prg
+    cores = len(os.sched_getaffinity(0))
+    if cfg == 2:
+        rate, cores, dt = cpu_oracle_rate(n)
+        return rate, cores, dt, f"{n} cfg2 samples (seeded inputs 0..{n - 1}), per-sample fp64 interpreter, mirror mode"
+    if cfg == 4:
+        from concurrent.futures import ThreadPoolExecutor
+        from oracle import seq2seq as S
+        P = S.prepare_s2s(wl.seq2seq_weights())
+        src = wl.token_inputs(wl.INPUT_SEED, 0, n)
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(cores) as ex:
+            list(ex.map(lambda i: S.greedy_decode(src[i], P, wl.S2S, "mirror"), range(n)))
+        dt = time.perf_counter() - t0
+        return n / dt, cores, dt, f"{n} cfg4 sequences (seeded tokens), per-sequence fp64 greedy decode, mirror mode"
+    W = {1: wl.mlp_weights, 3: wl.skipnet_r38_weights, 5: wl.resnet50_ee_weights}[cfg]()
+    P = prg.prepare(W)
+    X = (wl.mlp_inputs(wl.INPUT_SEED, 0, n) if cfg == 1 else
+         wl.image_inputs(wl.INPUT_SEED, 0, n, hw=224 if cfg == 5 else 32))
+    t0 = time.perf_counter()
+    O.run_batch(O.PROGRAMS[cfg], X, P, "mirror", threads=cores)
+    dt = time.perf_counter() - t0
+    return n / dt, cores, dt, f"{n} cfg{cfg} samples (seeded inputs), per-sample fp64 interpreter, mirror mode"
 
 
 def main():
@@ -277,6 +412,8 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="dycl", choices=["dycl", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5],
+                    help="BASELINE.json config (default 2: the configuration the metric is quoted on)")
     ap.add_argument("--cpu-samples", type=int, default=4096)
     ap.add_argument("--ref-samples", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
