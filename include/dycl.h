@@ -205,6 +205,18 @@ dycl_status dycl_set_profiling(dycl_graph g, int enable);
 dycl_status dycl_profile_read(dycl_graph g, int32_t max_n, int32_t* kind, float* ms,
                               double* bytes, double* flops, int32_t* n_out);
 
+/* ------------------------------------------------- multi-GPU rebalancing ---- */
+/* Survivor rebalancing plan after an exit point: given every rank's
+ * survivor count counts[0..world-1], the target is T = ceil(S / world), S = sum(counts).
+ * Ranks with more than T survivors send their LAST (count - T) rows, in order, to the
+ * ranks with fewer than T, matched in rank order (surplus rank ascending x deficit rank
+ * ascending).  Received rows are appended after a rank's own survivors in source-rank
+ * order.  For `rank`: send[j] = rows sent to rank j (taken from the tail, destination
+ * rank ascending), recv[j] = rows received from rank j, *new_count = rows held after.
+ * Pure host function (no device, no communicator); deterministic.  Errors: INVALID_ARG. */
+dycl_status dycl_rebalance_plan(const int32_t* counts, int world, int rank, int32_t* send, int32_t* recv,
+                                int32_t* new_count);
+
 /* ---------------------------------------------- generative DyNN (config 4) --- */
 /* A sequence-to-sequence Transformer decoded greedily under a per-sequence loop guard:
  * the paper's generative DyNNs (AttentionNet), whose `If` node tests the

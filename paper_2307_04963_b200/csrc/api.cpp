@@ -1031,4 +1031,39 @@ dycl_status dycl_debug_conv2d(dycl_graph g, int64_t n, int H, int W, int C, cons
   return DYCL_OK;
 }
 
+dycl_status dycl_rebalance_plan(const int32_t* counts, int world, int rank, int32_t* send, int32_t* recv,
+                                int32_t* new_count) {
+  if (!counts || world < 1 || rank < 0 || rank >= world || !send || !recv || !new_count)
+    return fail(nullptr, DYCL_E_INVALID_ARG, "rebalance_plan: bad argument");
+  long long S = 0;
+  for (int r = 0; r < world; ++r) {
+    if (counts[r] < 0) return fail(nullptr, DYCL_E_INVALID_ARG, "rebalance_plan: negative count");
+    S += counts[r];
+  }
+  const long long T = (S + world - 1) / world;
+  for (int j = 0; j < world; ++j) send[j] = recv[j] = 0;
+  // two-pointer matching: surplus ranks (ascending) give to deficit ranks (ascending)
+  std::vector<long long> give(world), take(world);
+  for (int r = 0; r < world; ++r) {
+    give[r] = counts[r] > T ? counts[r] - T : 0;
+    take[r] = counts[r] < T ? T - counts[r] : 0;
+  }
+  int d = 0;
+  for (int sr = 0; sr < world; ++sr) {
+    while (give[sr] > 0) {
+      while (d < world && take[d] == 0) ++d;
+      if (d >= world) break;                 // cannot happen: total deficit >= total surplus
+      const long long m = give[sr] < take[d] ? give[sr] : take[d];
+      if (sr == rank) send[d] += (int32_t)m;
+      if (d == rank) recv[sr] += (int32_t)m;
+      give[sr] -= m;
+      take[d] -= m;
+    }
+  }
+  long long held = counts[rank];
+  for (int j = 0; j < world; ++j) held += recv[j] - send[j];
+  *new_count = (int32_t)held;
+  return DYCL_OK;
+}
+
 }  // extern "C"
