@@ -693,6 +693,7 @@ cudaError_t launch_conv_tma(const ConvArgs& a, int max_rows, int num_sms, cudaSt
 }
 
 cudaError_t launch_conv(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream, int path) {
+  if (path != 1 && gemm_tma_eligible(a) && (a.dbg & 64) == 0) return launch_gemm_tma(a, max_rows, num_sms, stream);
   if (path != 1) {
     bool handled = false;
     cudaError_t e = launch_conv_tma(a, max_rows, num_sms, stream, &handled);

@@ -1,0 +1,226 @@
+// Dense layers on tcgen05 with TMA-fed 128-byte-swizzled tiles (SURVEY §8(a) a1 for
+// [rows][K] activations: the MLP trunk of config 1 and every projection / FFN / LM-head
+// GEMM of config 4).
+//
+//   D[m, n] = sum_k A[m, k] W[n, k] (+ bias, + fp32 residual, ReLU) -> bf16 and/or fp32
+//
+// A = activations [M][K] bf16 (K contiguous; the channel-planar layout of a [1][1][C]
+// tensor is exactly this), W = [N][Kp] bf16.  Classic persistent warp-specialised
+// Blackwell GEMM: 128 x 64 A boxes and BN x 64 W boxes (TMA, SWIZZLE_128B) into a
+// 4-stage ring, one elected lane issues 128 x BN x 16 tcgen05.mma (BN = 256 or 128)
+// into one of two TMEM accumulators, two epilogue warpgroups alternate tiles and run
+// the shared fused epilogue (conv_finish16).  Warps: 0-7 epilogue, 8 TMA, 9 MMA.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "epilogue.cuh"
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace dycl {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BKE = 64;                  // K elements per stage (one 128-byte swizzle row)
+constexpr int THREADS = 320;
+constexpr int STAGES = 4;
+
+template <int BN>
+struct GCfg {
+  static constexpr int A_BYTES = BM * BKE * 2;
+  static constexpr int B_BYTES = BN * BKE * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_gemm_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const ConvArgs a) {
+  using C = GCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES);
+  const uint32_t full0 = ptx::smem_u32(bars);
+  const uint32_t empty0 = full0 + 8 * STAGES;
+  const uint32_t tfull0 = empty0 + 8 * STAGES;
+  const uint32_t tempty0 = tfull0 + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int M = a.n_live ? *a.n_live : a.n_static;
+  const int m_tiles = (M + BM - 1) / BM;
+  const int n_tiles = a.Cout / BN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int kblocks = a.K / BKE;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      ptx::mbar_init(full0 + 8 * i, 1);
+      ptx::mbar_init(empty0 + 8 * i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(tfull0 + 8 * i, 1);
+      ptx::mbar_init(tempty0 + 8 * i, 128);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 9) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      ptx::tma_prefetch_desc(&tmA);
+      ptx::tma_prefetch_desc(&tmB);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m_tile = tile / n_tiles, n_tile = tile - m_tile * n_tiles;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1);
+          const uint32_t bar = full0 + 8 * stage;
+          ptx::mbar_arrive_expect_tx(bar, (uint32_t)C::STAGE);
+          ptx::tma_load_2d(ptx::smem_u32(sA + stage * C::A_BYTES), &tmA, bar, kb * BKE, m_tile * BM);
+          ptx::tma_load_2d(ptx::smem_u32(sB + stage * C::B_BYTES), &tmB, bar, kb * BKE, n_tile * BN);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 9) {
+    constexpr uint32_t IDESC = ptx::make_idesc_bf16(BM, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      ptx::mbar_wait(tempty0 + 8 * acc, ((it >> 1) & 1) ^ 1);
+      ptx::tc_fence_after();
+      const uint32_t d = tmem_base + (uint32_t)(acc * BN);
+      for (int kb = 0; kb < kblocks; ++kb) {
+        ptx::mbar_wait(full0 + 8 * stage, phase);
+        ptx::tc_fence_after();
+        const uint64_t ad = ptx::make_smem_desc_sw128(ptx::smem_u32(sA + stage * C::A_BYTES));
+        const uint64_t bd = ptx::make_smem_desc_sw128(ptx::smem_u32(sB + stage * C::B_BYTES));
+#pragma unroll
+        for (int j = 0; j < BKE / 16; ++j)
+          ptx::mma_bf16_ss_elect(d, ad + (uint64_t)(2 * j), bd + (uint64_t)(2 * j), IDESC, (uint32_t)((kb | j) != 0));
+        ptx::mma_commit_elect(empty0 + 8 * stage);
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      ptx::mma_commit_elect(tfull0 + 8 * acc);
+      __syncwarp();
+    }
+  } else {
+    const int wg = warp >> 2, quad = warp & 3;
+    const int r = quad * 32 + lane;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      if ((it & 1) != wg) continue;
+      const int acc = it & 1;
+      const int m_tile = tile / n_tiles, n_tile = tile - m_tile * n_tiles;
+      const int m = m_tile * BM + r;
+      ptx::mbar_wait(tfull0 + 8 * acc, (it >> 1) & 1);
+      ptx::tc_fence_after();
+      const uint32_t t_base = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t v[16];
+        ptx::tmem_ld_32x32b_x16(t_base + (uint32_t)c0, v);
+        ptx::tmem_ld_wait();
+        if (m < M) {
+          float f[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) f[q] = __uint_as_float(v[q]);
+          conv_finish16(a, m, 0, 0, n_tile * BN + c0, f);
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(tempty0 + 8 * acc);
+    }
+  }
+  __syncthreads();
+  if (warp == 9) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, 512);
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+template <int BN>
+cudaError_t launch_bn(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  CUtensorMap tmA, tmB;
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)a.K, (cuuint64_t)(max_rows > 0 ? max_rows : 1)};
+    cuuint64_t strides[1] = {(cuuint64_t)a.K * 2};
+    cuuint32_t box[2] = {BKE, BM};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)a.x, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)a.Kp, (cuuint64_t)a.Cout};
+    cuuint64_t strides[1] = {(cuuint64_t)a.Kp * 2};
+    cuuint32_t box[2] = {BKE, BN};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)a.w, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_tma<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, GCfg<BN>::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const long long tiles = (long long)((max_rows + BM - 1) / BM) * (a.Cout / BN);
+  int grid = (int)(tiles < num_sms ? tiles : num_sms);
+  if (grid < 1) grid = 1;
+  k_gemm_tma<BN><<<grid, THREADS, GCfg<BN>::SMEM, stream>>>(tmA, tmB, a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool gemm_tma_eligible(const ConvArgs& a) {
+  return a.H == 1 && a.W == 1 && a.ksz == 1 && a.stride == 1 && a.pad == 0 && a.C % 64 == 0 && a.K == a.C &&
+         a.Kp == a.K && (a.Cout % 128 == 0) && a.res_mode != 2;
+}
+
+cudaError_t launch_gemm_tma(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream) {
+  // 256-wide N tiles unless they leave more than half of the SMs idle (small-M decode GEMMs)
+  const long long m_tiles = (max_rows + BM - 1) / BM;
+  if (a.Cout % 256 == 0 && m_tiles * (a.Cout / 256) >= num_sms / 2) return launch_bn<256>(a, max_rows, num_sms, stream);
+  return launch_bn<128>(a, max_rows, num_sms, stream);
+}
+
+}  // namespace dycl

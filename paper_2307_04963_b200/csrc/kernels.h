@@ -48,6 +48,9 @@ inline void pack_rowtap(const uint16_t* wp, int cout, int kp, int cp, uint16_t* 
 // TMA-fed variant (conv_tma.cu) for layers whose output tiles are rectangular
 // boxes; *handled = false (and nothing launched) when the shape does not qualify.
 cudaError_t launch_conv_tma(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream, bool* handled);
+// Dense-layer GEMM on tcgen05 with TMA SWIZZLE_128B tiles (gemm_tma.cu): [rows][K] x [N][K].
+bool gemm_tma_eligible(const ConvArgs& a);
+cudaError_t launch_gemm_tma(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream);
 // Dispatch: path 0 = auto (TMA when possible), 1 = cp.async kernel, 2 = TMA only.
 cudaError_t launch_conv(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream, int path = 0);
 

@@ -54,31 +54,37 @@ __global__ void k_embed(const S2SEmbedArgs a) {
   }
 }
 
-// LayerNorm of [rows][d] fp32 (d <= 1024): warp per row, biased variance, eps.
+// LayerNorm of [rows][d] fp32 (d <= 1024, d % 32 == 0): warp per row, the row in registers
+// (compile-time unrolled, guarded), biased variance, eps.
 __global__ void k_layernorm(const S2SLnArgs a) {
   const int n = a.n_live ? *a.n_live : a.n_static;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= n) return;
   const float* x = a.in + (size_t)warp * a.d;
-  float v[32];
   const int per = a.d / 32;
+  float v[32];
   float s = 0.f;
-  for (int j = 0; j < per; ++j) {
-    v[j] = x[lane + 32 * j];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    v[j] = j < per ? x[lane + 32 * j] : 0.f;
     s += v[j];
   }
   const float mu = warp_sum(s) / (float)a.d;
   float q = 0.f;
-  for (int j = 0; j < per; ++j) {
-    const float dd = v[j] - mu;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float dd = j < per ? v[j] - mu : 0.f;
     q += dd * dd;
   }
   const float rstd = rsqrtf(warp_sum(q) / (float)a.d + a.eps);
-  for (int j = 0; j < per; ++j) {
-    const int c = lane + 32 * j;
-    const float y = (v[j] - mu) * rstd * a.gamma[c] + a.beta[c];
-    a.out32[(size_t)warp * a.d + c] = y;
-    a.outb[(size_t)warp * a.d + c] = to_bf(y);
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    if (j < per) {
+      const int c = lane + 32 * j;
+      const float y = (v[j] - mu) * rstd * __ldg(a.gamma + c) + __ldg(a.beta + c);
+      a.out32[(size_t)warp * a.d + c] = y;
+      a.outb[(size_t)warp * a.d + c] = to_bf(y);
+    }
   }
 }
 
@@ -165,27 +171,48 @@ __global__ void __launch_bounds__(256) k_attn_decoder(const S2SAttnArgs a) {
     kv = a.kv + (size_t)slot * a.S * 2 * d;
     nk = a.S;
   }
-  // scores for keys lane and lane+32 (nk <= 64)
+  // scores: lane j owns keys j and j+32 (nk <= 64); q is broadcast through shuffles and
+  // each lane reads its key's 64-dim head slice as 8 x 16-byte vectors.
   float s0 = -INFINITY, s1 = -INFINITY;
-  for (int j = 0; j < nk; ++j) {
-    const uint16_t* kj = kv + (size_t)j * 2 * d + h * dh;
-    const float p = warp_sum(q0 * bf(kj[lane]) + q1 * bf(kj[lane + 32])) * 0.125f;
-    if (j == lane) s0 = p;
-    if (j == lane + 32) s1 = p;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const int j = lane + 32 * half;
+    float acc = 0.f;
+    const bool valid = j < nk;
+    const uint4* kp = reinterpret_cast<const uint4*>(kv + (size_t)(valid ? j : 0) * 2 * d + h * dh);
+#pragma unroll
+    for (int c8 = 0; c8 < 8; ++c8) {
+      // plain (coherent) load: the self cache row t was written by this warp in this kernel
+      const uint4 w4 = valid ? kp[c8] : make_uint4(0, 0, 0, 0);
+      const uint32_t u[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int c = c8 * 8 + 2 * e;                    // dims c, c+1 of q live on lanes c%32 (q0 / q1)
+        const float qa = __shfl_sync(0xffffffffu, c < 32 ? q0 : q1, c & 31);
+        const float qb = __shfl_sync(0xffffffffu, c + 1 < 32 ? q0 : q1, (c + 1) & 31);
+        acc += qa * __uint_as_float(u[e] << 16) + qb * __uint_as_float(u[e] & 0xFFFF0000u);
+      }
+    }
+    if (valid) {
+      if (half == 0) s0 = acc * 0.125f;
+      else s1 = acc * 0.125f;
+    }
   }
   const float m = warp_max(fmaxf(s0, s1));
   const float e0 = lane < nk ? expf(s0 - m) : 0.f, e1 = lane + 32 < nk ? expf(s1 - m) : 0.f;
   const float inv = 1.f / warp_sum(e0 + e1);
+  // out[2*lane .. 2*lane+1] = sum_j p_j v_j: one coalesced 4-byte load per lane per key
   float o0 = 0.f, o1 = 0.f;
+  const uint32_t* vbase = reinterpret_cast<const uint32_t*>(kv + d + h * dh) + lane;
+#pragma unroll 8
   for (int j = 0; j < nk; ++j) {
     const float pj = __shfl_sync(0xffffffffu, j < 32 ? e0 : e1, j & 31) * inv;
-    const uint16_t* vj = kv + (size_t)j * 2 * d + d + h * dh;
-    o0 += pj * bf(vj[lane]);
-    o1 += pj * bf(vj[lane + 32]);
+    const uint32_t vv = vbase[(size_t)j * d];           // row stride 2d bf16 = d uint32
+    o0 += pj * __uint_as_float(vv << 16);
+    o1 += pj * __uint_as_float(vv & 0xFFFF0000u);
   }
-  uint16_t* out = a.out + (size_t)row * d + h * dh;
-  out[lane] = to_bf(o0);
-  out[lane + 32] = to_bf(o1);
+  uint32_t* out = reinterpret_cast<uint32_t*>(a.out + (size_t)row * d + h * dh) + lane;
+  *out = (uint32_t)to_bf(o0) | ((uint32_t)to_bf(o1) << 16);
 }
 
 // LM-head argmax + EOS / length loop guard, one CTA per active row:

@@ -65,10 +65,12 @@ CONV_CASES = [
     (3, 16, 16, 32, 64, 3, 2, 1, 1, 2),     # stage-2 -> 3 transition, option A
     (7, 8, 8, 64, 64, 3, 1, 1, 1, 0),       # odd sample count across 2-sample tiles
     (5, 32, 32, 16, 16, 3, 1, 1, 1, 1),
+    (300, 1, 1, 512, 1536, 1, 1, 0, 0, 0),  # dense GEMM, TMA SW128 path (BN 256), ragged M
+    (77, 1, 1, 128, 384, 1, 1, 0, 1, 1),    # dense GEMM BN 128 + residual + ReLU
 ]
 
 
-TMA_CASES = [c for c in CONV_CASES if c[4] in (16, 32, 64)]
+TMA_CASES = [c for c in CONV_CASES if c[4] in (16, 32, 64) or (c[1] == c[2] == 1 and c[3] % 64 == 0 and c[4] % 128 == 0)]
 
 
 ROWTAP_CASES = [c for c in TMA_CASES if c[5] == 3 and c[6] == 1 and c[7] == 1 and c[3] >= 16 and c[1] * c[2] >= 128]
