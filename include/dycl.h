@@ -295,6 +295,11 @@ dycl_status dycl_debug_conv2d(dycl_graph g, int64_t n, int H, int W, int C, cons
                               int c_out, int k, int stride, int pad, int relu, const void* res, int res_mode,
                               const void* x, void* y, int path);
 
+/* Development hook: with DYCL_TS set in the environment at graph creation, copies the
+ * clock64 phase stamps of the last fused-block launch (CTA 0, first 8 samples, 16 slots
+ * each) into out128.  Errors: STATE if DYCL_TS was not set. */
+dycl_status dycl_debug_timestamps(dycl_graph g, long long* out128);
+
 #ifdef __cplusplus
 }
 #endif

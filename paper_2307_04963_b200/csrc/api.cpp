@@ -95,6 +95,8 @@ struct dycl_graph_s {
   int precision = DYCL_PREC_FP32_STREAM;
   int conv_path = 0;                 // 0 auto; DYCL_CONV_PATH=1 forces the cp.async kernel
   int conv_dbg = 0;                  // DYCL_CONV_DBG: timing experiments only (results invalid)
+  int no_fuse = 0;                   // DYCL_NO_FUSE=1: run basic blocks as two conv launches
+  long long* dbg_ts = nullptr;       // DYCL_TS=1: fused-block phase timestamps (development)
   long long max_row_elems = 0;
   int* d_counts = nullptr;
   int n_slots = 0;
@@ -337,12 +339,54 @@ struct Exec {
   }
   bool fp32_stream() const { return g->precision == DYCL_PREC_FP32_STREAM; }
 
+  // A basic block the fused kernel can run: BLOCK, conv3x3/s1/p1 ReLU (C->C),
+  // conv3x3/s1/p1 ReLU + identity residual, on an eligible sample shape.
+  static bool fusable(const Subnet& s, size_t li) {
+    if (li + 2 >= s.layers.size()) return false;
+    const Layer &B = s.layers[li], &c1 = s.layers[li + 1], &c2 = s.layers[li + 2];
+    if (B.kind != L_BLOCK || c1.kind != L_CONV || c2.kind != L_CONV) return false;
+    for (const Layer* c : {&c1, &c2})
+      if (c->k != 3 || c->stride != 1 || c->pad != 1 || !c->relu || !c->d_wrt || c->in.C != c->out.C ||
+          !(c->in == c->out))
+        return false;
+    if (c1.residual || !c2.residual || c2.res_mode != 1) return false;
+    return dycl::block_fused_eligible(c1.in.C, c1.in.H, c1.in.W);
+  }
+
   // Run subnet s on the rows of `in` (device count `cnt`).  The last layer writes
   // into `out_hint` when given (b >= 0).  `busy` is an outer tensor to preserve.
   dycl_status subnet(const Subnet& s, Tensor in, const int* cnt, Tensor out_hint, Tensor busy, Tensor* out) {
     Tensor cur = in, shortcut;
     for (size_t li = 0; li < s.layers.size(); ++li) {
       const Layer& L = s.layers[li];
+      if (L.kind == L_BLOCK && fp32_stream() && !g->no_fuse && cur.f >= 0 && fusable(s, li)) {
+        const Layer &c1 = s.layers[li + 1], &c2 = s.layers[li + 2];
+        const bool last = li + 3 == s.layers.size();
+        const bool need_b = last || !fusable(s, li + 3);   // the next layer reads the bf16 copy
+        Tensor o = (last && out_hint.b >= 0) ? out_hint : pick_tensor(true, {cur, busy, out_hint});
+        if (o.b < 0 || o.f < 0) return fail(g, DYCL_E_STATE, "internal: out of activation buffers");
+        dycl::BlockArgs ba{};
+        ba.x32 = g->buf32[cur.f];
+        ba.y32 = g->buf32[o.f];
+        ba.yb = need_b ? g->buf[o.b] : nullptr;
+        ba.w1_rt = c1.d_wrt;
+        ba.w2_rt = c2.d_wrt;
+        ba.b1 = c1.d_b;
+        ba.b2 = c2.d_b;
+        ba.n_live = cnt;
+        ba.C = c1.in.C; ba.H = c1.in.H; ba.W = c1.in.W;
+        ba.ts = g->dbg_ts;
+        const double row_b = (4.0 + 4.0 + (need_b ? 2.0 : 0.0)) * c1.in.row_elems();
+        const double row_f = 2.0 * 2.0 * c1.out.H * c1.out.W * c1.out.C * (double)(9 * c1.in.C);
+        prof_begin(DYCL_K_CONV, cnt, row_b, row_f, 2.0 * 2 * 3 * c1.out.C * c1.Kp_rt);
+        cudaError_t e = dycl::launch_block_fused(ba, batch, g->num_sms, st);
+        prof_end();
+        if (e != cudaSuccess) return cuda_fail(g, e, "launch_block_fused");
+        if (!need_b) o.b = -1;                        // no valid bf16 copy
+        cur = o;
+        li += 2;
+        continue;
+      }
       if (L.kind == L_BLOCK) {
         shortcut = cur;
         continue;
@@ -438,7 +482,7 @@ struct Exec {
   dycl_status head(const Subnet& s, Tensor in, const int* cnt, int kind, float thr) {
     const Layer& D = s.layers.back();
     dycl::HeadArgs a{};
-    a.h = g->buf[in.b];
+    a.h = in.b >= 0 ? g->buf[in.b] : nullptr;
     a.h32 = in.f >= 0 ? g->buf32[in.f] : nullptr;
     a.w = D.d_w;
     a.b = D.d_b;
@@ -607,6 +651,11 @@ dycl_status dycl_graph_create(int cuda_device, int in_h, int in_w, int in_c, dyc
   g->input = Shape{in_h, in_w, in_c};
   if (const char* cp = getenv("DYCL_CONV_PATH")) g->conv_path = atoi(cp);
   if (const char* cd = getenv("DYCL_CONV_DBG")) g->conv_dbg = atoi(cd);
+  if (const char* nf = getenv("DYCL_NO_FUSE")) g->no_fuse = atoi(nf);
+  if (getenv("DYCL_TS")) {
+    cudaMalloc(&g->dbg_ts, 8 * 16 * sizeof(long long));
+    cudaMemset(g->dbg_ts, 0, 8 * 16 * sizeof(long long));
+  }
   cudaSetDevice(cuda_device);
   cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
   int major = 0;
@@ -641,6 +690,7 @@ dycl_status dycl_graph_destroy(dycl_graph g) {
   cudaFree(g->d_in_stage);
   cudaFree(g->d_logit_stage);
   cudaFree(g->d_path_stage);
+  cudaFree(g->dbg_ts);
   for (auto& L : g->prof) {
     cudaEventDestroy(L.e0);
     cudaEventDestroy(L.e1);
@@ -1063,6 +1113,14 @@ dycl_status dycl_rebalance_plan(const int32_t* counts, int world, int rank, int3
   long long held = counts[rank];
   for (int j = 0; j < world; ++j) held += recv[j] - send[j];
   *new_count = (int32_t)held;
+  return DYCL_OK;
+}
+
+dycl_status dycl_debug_timestamps(dycl_graph g, long long* out128) {
+  if (!g || !out128) return DYCL_E_INVALID_ARG;
+  if (!g->dbg_ts) return fail(g, DYCL_E_STATE, "DYCL_TS not set");
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(out128, g->dbg_ts, 128 * sizeof(long long), cudaMemcpyDeviceToHost));
   return DYCL_OK;
 }
 

@@ -1,0 +1,445 @@
+// Fused residual basic block on tcgen05: y = relu(conv2(relu(conv1(x))) + x) for one
+// whole sample at a time per CTA, stride 1, 3x3, C in {16, 32} (CIFAR stages 1-2).
+//
+// Why: per block the unfused kernels move x (bf16 operand copy), T (written + read),
+// x (fp32 shortcut) and y (fp32 + bf16) through HBM: 256 KB per 32x32x16 sample.  Here
+// the sample's fp32 residual stream is bulk-copied into SMEM once; the bf16 conv1
+// operand is built from it in SMEM, T never leaves SMEM, the shortcut is read from SMEM,
+// and only y (fp32, + a bf16 copy when the next layer needs one) is written: 128 KB.
+//
+// Operands use the row-tap form: per filter row r one tcgen05.mma with N = 3*C (the three
+// W taps side by side), A = the sample's bf16 image in the UMMA K-major no-swizzle layout
+// ([plane][H+2 rows][W][8 ch], two zero halo rows) shifted by r rows; the epilogue adds
+// the three W-shifted partial sums with warp shuffles (pixel w-1 / w+1 = lane -1 / +1).
+//
+// SMEM banks: the epilogue owns one pixel per thread (TMEM lane = pixel), so plain NHWC
+// fp32 rows (64 / 128 B apart) put 8 lanes of every LDS.128 phase in the same banks.  The
+// fp32 sample is therefore moved by TMA with the 64B / 128B swizzle (16-byte chunk index
+// XOR the 128-byte row index bits), read and written through swz(), and y32 leaves through
+// the same tensor map, which un-swizzles it: conflict-free shortcut reads / output writes.
+//
+// Warps: 0-7 two epilogue/converter warpgroups (sub-tiles split even / odd), 8 bulk-copy
+// producer (double-buffered fp32 sample), 9 TMEM allocator + MMA issuer.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace dycl {
+namespace {
+
+constexpr int THREADS = 320;
+
+template <int C, int H>
+struct BCfg {
+  static constexpr int W = H, HW = H * W, P = C / 8;
+  static constexpr int NSUB = HW / 128;                 // UMMA tiles per sample
+  static constexpr int BH = 128 / W;                    // image rows per UMMA tile
+  static constexpr int N = 3 * C;                       // row-tap MMA width
+  static constexpr int X32_BYTES = HW * C * 4;
+  static constexpr int YB_BYTES = HW * C * 2;
+  static constexpr int PLANE = (H + 2) * W * 16;        // one 8-channel plane with halo rows
+  static constexpr int OPER = P * PLANE;                // bf16 operand image (x or T)
+  static constexpr int KP_RT = (3 * C + 63) / 64 * 64;
+  static constexpr int WCH = KP_RT / 8;                 // K chunks of the row-tap weights
+  static constexpr int W_BYTES = WCH * N * 16;
+  static constexpr int BOX_ROWS = HW < 256 ? HW : 256;  // pixels per TMA box (box dims <= 256)
+  static constexpr int NBOX = HW / BOX_ROWS;
+  static constexpr int FIXED = 1024 + X32_BYTES /*y staging*/ + 2 * OPER + 2 * W_BYTES + 2 * C * 4 + 256;
+  // fp32 input buffers (2 if they fit) and a separate bf16 output staging buffer if it fits
+  static constexpr int NXB = FIXED + 2 * X32_BYTES + YB_BYTES <= 227 * 1024 ? 2 : 1;
+  static constexpr bool YB_SEP = FIXED + NXB * X32_BYTES + YB_BYTES <= 227 * 1024;
+  static constexpr int SMEM = FIXED + NXB * X32_BYTES + (YB_SEP ? YB_BYTES : 0);
+  // separate TMEM accumulators for conv1 and conv2 if two fit: conv1(s+1) overlaps epilogue 2(s)
+  static constexpr int NSETS = 2 * 256 >= 2 * NSUB * N && NSUB * N <= 256 ? 2 : 1;
+  static_assert(HW % 128 == 0 && 128 % W == 0, "sample must tile into 128-row UMMA tiles");
+  static_assert(NSUB * N <= 512, "TMEM");
+  static_assert(SMEM <= 227 * 1024, "SMEM");
+};
+
+// byte offset inside a swizzled fp32 sample buffer (1024-aligned): C=32 -> 128B swizzle,
+// C=16 -> 64B swizzle (CU_TENSOR_MAP_SWIZZLE_128B / _64B patterns)
+template <int C>
+__device__ __forceinline__ uint32_t swz(uint32_t o) {
+  return C == 32 ? o ^ (((o >> 7) & 7u) << 4) : o ^ (((o >> 7) & 3u) << 4);
+}
+
+__device__ __forceinline__ uint32_t pk(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int C, int H>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_block_fused(const __grid_constant__ CUtensorMap tmW1, const __grid_constant__ CUtensorMap tmW2,
+                  const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY, const BlockArgs a) {
+  using G = BCfg<C, H>;
+  constexpr int W = G::W, HW = G::HW, P = G::P;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* x32s = smem;                                                   // [NXB][HW][C] fp32, swizzled
+  uint8_t* ys = x32s + G::NXB * G::X32_BYTES;                             // [HW][C] fp32 y staging, swizzled
+  uint8_t* xb = ys + G::X32_BYTES;                                        // [P][H+2][W][8] bf16
+  uint8_t* tb = xb + G::OPER;
+  uint8_t* w1s = tb + G::OPER;
+  uint8_t* w2s = w1s + G::W_BYTES;
+  uint8_t* ybs = w2s + G::W_BYTES;                                        // [P][HW][8] bf16 y staging
+  float* b1s = reinterpret_cast<float*>(ybs + (G::YB_SEP ? G::YB_BYTES : 0));
+  float* b2s = b1s + C;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(b2s + C + ((2 * C) & 1));
+  const uint32_t xfull0 = ptx::smem_u32(bars), xempty0 = xfull0 + 16;
+  const uint32_t xb_full = xempty0 + 16, xb_empty = xb_full + 8, acc1 = xb_empty + 8, tb_full = acc1 + 8;
+  const uint32_t acc2 = tb_full + 8, acc1_empty = acc2 + 8, wfull = acc1_empty + 8, acc2_empty = wfull + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  constexpr uint32_t SET2 = G::NSETS == 2 ? 256u : 0u;    // TMEM column of the conv2 accumulator
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_live = a.n_live ? *a.n_live : a.n_static;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(xfull0 + 8 * i, 1);
+      ptx::mbar_init(xempty0 + 8 * i, 256);
+    }
+    ptx::mbar_init(xb_full, 256);
+    ptx::mbar_init(xb_empty, 1);
+    ptx::mbar_init(acc1, 1);
+    ptx::mbar_init(tb_full, 256);
+    ptx::mbar_init(acc2, 1);
+    ptx::mbar_init(acc1_empty, 256);
+    ptx::mbar_init(acc2_empty, 256);
+    ptx::mbar_init(wfull, 1);
+    ptx::fence_mbar_init();
+  }
+  // zero the halo rows (row 0 and row H+1 of every plane) of both operand images, once
+  for (int i = threadIdx.x; i < 2 * P * 2 * W; i += blockDim.x) {
+    const int img = i / (P * 2 * W), rem = i % (P * 2 * W);
+    const int p = rem / (2 * W), k = rem % (2 * W);
+    const int row = k < W ? 0 : H + 1, w = k % W;
+    uint8_t* base = img ? tb : xb;
+    *reinterpret_cast<uint4*>(base + p * G::PLANE + (row * W + w) * 16) = make_uint4(0, 0, 0, 0);
+  }
+  for (int i = threadIdx.x; i < C; i += blockDim.x) {
+    b1s[i] = a.b1[i];
+    b2s[i] = a.b2[i];
+  }
+  ptx::fence_proxy_async_smem();
+  if (warp == 9) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      ptx::tma_prefetch_desc(&tmW1);
+      ptx::tma_prefetch_desc(&tmW2);
+      ptx::tma_prefetch_desc(&tmX);
+      ptx::mbar_arrive_expect_tx(wfull, 2 * G::W_BYTES);
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+          "%5}], [%2];" ::"r"(ptx::smem_u32(w1s)),
+          "l"(&tmW1), "r"(wfull), "r"(0), "r"(0), "r"(0)
+          : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+          "%5}], [%2];" ::"r"(ptx::smem_u32(w2s)),
+          "l"(&tmW2), "r"(wfull), "r"(0), "r"(0), "r"(0)
+          : "memory");
+      int it = 0;
+      for (int smp = blockIdx.x; smp < n_live; smp += gridDim.x, ++it) {
+        const int b = it % G::NXB;
+        ptx::mbar_wait(xempty0 + 8 * b, ((it / G::NXB) & 1) ^ 1);
+        if (a.ts && blockIdx.x == 0 && it < 8) a.ts[it * 16 + 10] = clock64();
+        const int src = a.list ? a.list[smp] : smp;
+        ptx::mbar_arrive_expect_tx(xfull0 + 8 * b, G::X32_BYTES);
+#pragma unroll
+        for (int k = 0; k < G::NBOX; ++k)
+          ptx::tma_load_2d(ptx::smem_u32(x32s + (size_t)b * G::X32_BYTES + k * G::BOX_ROWS * C * 4), &tmX,
+                           xfull0 + 8 * b, 0, src * HW + k * G::BOX_ROWS);
+      }
+    }
+  } else if (warp == 9) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t IDESC = ptx::make_idesc_bf16(128, G::N);
+    const uint64_t xdesc = ptx::make_smem_desc(ptx::smem_u32(xb), 0, G::PLANE, 128);
+    const uint64_t tdesc = ptx::make_smem_desc(ptx::smem_u32(tb), 0, G::PLANE, 128);
+    const uint64_t w1d = ptx::make_smem_desc(ptx::smem_u32(w1s), 0, G::N * 16, 128);
+    const uint64_t w2d = ptx::make_smem_desc(ptx::smem_u32(w2s), 0, G::N * 16, 128);
+    ptx::mbar_wait(wfull, 0);
+    int it = 0;
+    for (int smp = blockIdx.x; smp < n_live; smp += gridDim.x, ++it) {
+      const uint32_t ph = it & 1;
+      // conv1 accumulator free: drained by epilogue 1 (two sets) / epilogue 2 (shared set)
+      ptx::mbar_wait(G::NSETS == 2 ? acc1_empty : acc2_empty, ph ^ 1);
+      ptx::mbar_wait(xb_full, ph);                    // x operand converted
+      ptx::tc_fence_after();
+      const bool mstamp = a.ts && blockIdx.x == 0 && lane == 0 && it < 8;
+      if (mstamp) a.ts[it * 16 + 6] = clock64();
+#pragma unroll
+      for (int j = 0; j < G::NSUB; ++j)
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int q = 0; q < C / 16; ++q)
+            ptx::mma_bf16_ss_elect(tmem + j * G::N, xdesc + (uint64_t)(((j * G::BH + r) * W * 16 + 2 * q * G::PLANE) >> 4),
+                                   w1d + (uint64_t)(((r * P + 2 * q) * G::N * 16) >> 4), IDESC,
+                                   (uint32_t)((r | q) != 0));
+      ptx::mma_commit_elect(xb_empty);
+      ptx::mma_commit_elect(acc1);
+      __syncwarp();
+      if (mstamp) a.ts[it * 16 + 7] = clock64();
+      ptx::mbar_wait(tb_full, ph);                    // T written (and conv1 TMEM read) by epilogue 1
+      if (G::NSETS == 2) ptx::mbar_wait(acc2_empty, ph ^ 1);
+      ptx::tc_fence_after();
+      if (mstamp) a.ts[it * 16 + 8] = clock64();
+#pragma unroll
+      for (int j = 0; j < G::NSUB; ++j)
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int q = 0; q < C / 16; ++q)
+            ptx::mma_bf16_ss_elect(tmem + SET2 + j * G::N,
+                                   tdesc + (uint64_t)(((j * G::BH + r) * W * 16 + 2 * q * G::PLANE) >> 4),
+                                   w2d + (uint64_t)(((r * P + 2 * q) * G::N * 16) >> 4), IDESC,
+                                   (uint32_t)((r | q) != 0));
+      ptx::mma_commit_elect(acc2);
+      __syncwarp();
+      if (mstamp) a.ts[it * 16 + 9] = clock64();
+    }
+  } else {
+    // ------------------------------------------------------------ converters / epilogues
+    const int wg = warp >> 2, quad = warp & 3;
+    const int r = quad * 32 + lane;                    // TMEM lane = row of a UMMA tile
+    const int et = threadIdx.x;                        // 0..255
+    const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
+    constexpr int CPS = C / 16;                        // 16-channel chunks per sub-tile
+    constexpr int UPT = (G::NSUB / 2) * CPS;           // (sub-tile, chunk) units per thread
+    static_assert(UPT % 2 == 0, "units are processed in pairs");
+
+    // fp32 stream -> bf16 operand image (RNE); frees the fp32 input buffer
+    auto convert = [&](int itc) {
+      const int b = itc % G::NXB;
+      const uint8_t* xs = x32s + (size_t)b * G::X32_BYTES;
+      ptx::mbar_wait(xfull0 + 8 * b, (itc / G::NXB) & 1);
+      ptx::mbar_wait(xb_empty, (itc & 1) ^ 1);         // conv1 of the previous sample read xb
+      for (int u = et; u < HW * P; u += 256) {
+        const int pix = u % HW, p = u / HW;            // lanes = consecutive pixels (swizzled rows)
+        const float4 v0 = *reinterpret_cast<const float4*>(xs + swz<C>((uint32_t)(pix * C + p * 8) * 4));
+        const float4 v1 = *reinterpret_cast<const float4*>(xs + swz<C>((uint32_t)(pix * C + p * 8 + 4) * 4));
+        *reinterpret_cast<uint4*>(xb + p * G::PLANE + (W + pix) * 16) =
+            make_uint4(pk(v0.x, v0.y), pk(v0.z, v0.w), pk(v1.x, v1.y), pk(v1.z, v1.w));
+      }
+      ptx::fence_proxy_async_smem();
+      ptx::mbar_arrive(xb_full);
+      ptx::mbar_arrive(xempty0 + 8 * b);
+    };
+
+    int it = 0;
+    if ((int)blockIdx.x < n_live) convert(0);
+    for (int smp = blockIdx.x; smp < n_live; smp += gridDim.x, ++it) {
+      const uint32_t ph = it & 1;
+      const int dst = smp;                             // outputs are dense in row order
+      const bool stamp = a.ts && blockIdx.x == 0 && et == 0 && it < 8;
+      // ---- epilogue 1: T = relu(conv1 + b1) -> bf16 operand image (SMEM)
+      ptx::mbar_wait(acc1, ph);
+      ptx::tc_fence_after();
+      if (!G::YB_SEP) {                                // T doubles as the bf16 y staging buffer
+        if (et == 0) ptx::bulk_wait_read1();          // the bf16 group (older of the two) has read T
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+      }
+      if (stamp) a.ts[it * 16 + 2] = clock64();
+#pragma unroll
+      for (int g = 0; g < UPT; g += 2) {
+        uint32_t v[2][3][16];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int j = wg + 2 * ((g + u) / CPS), c0 = ((g + u) % CPS) * 16;
+          const uint32_t t = lane_base + (uint32_t)(j * G::N + c0);
+          ptx::tmem_ld_32x32b_x16(t, v[u][0]);
+          ptx::tmem_ld_32x32b_x16(t + C, v[u][1]);
+          ptx::tmem_ld_32x32b_x16(t + 2 * C, v[u][2]);
+        }
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int j = wg + 2 * ((g + u) / CPS), c0 = ((g + u) % CPS) * 16;
+          const int pix = j * 128 + r, w = pix % W;
+          float f[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float lft = __shfl_up_sync(0xffffffffu, __uint_as_float(v[u][0][q]), 1);
+            const float rgt = __shfl_down_sync(0xffffffffu, __uint_as_float(v[u][2][q]), 1);
+            f[q] = fmaxf(__uint_as_float(v[u][1][q]) + (w > 0 ? lft : 0.f) + (w < W - 1 ? rgt : 0.f) + b1s[c0 + q],
+                         0.f);
+          }
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2)
+            *reinterpret_cast<uint4*>(tb + ((c0 >> 3) + h2) * G::PLANE + (W + pix) * 16) =
+                make_uint4(pk(f[8 * h2], f[8 * h2 + 1]), pk(f[8 * h2 + 2], f[8 * h2 + 3]),
+                           pk(f[8 * h2 + 4], f[8 * h2 + 5]), pk(f[8 * h2 + 6], f[8 * h2 + 7]));
+        }
+      }
+      ptx::fence_proxy_async_smem();
+      ptx::tc_fence_before();
+      if (stamp) a.ts[it * 16 + 3] = clock64();
+      ptx::mbar_arrive(tb_full);
+      if (G::NSETS == 2) ptx::mbar_arrive(acc1_empty);
+      // ---- next sample's operand conversion overlaps conv2 of this one
+      if (smp + (int)gridDim.x < n_live) {
+        if (stamp) a.ts[(it + 1) * 16 + 0] = clock64();
+        convert(it + 1);
+        if (stamp) a.ts[(it + 1) * 16 + 1] = clock64();
+      }
+      // ---- epilogue 2: y = relu(conv2 + b2 + x) -> fp32 stream (+ bf16 operand copy)
+      const float* xg = a.x32 + (size_t)(a.list ? a.list[smp] : smp) * HW * C;   // shortcut (L2-resident)
+      ptx::mbar_wait(acc2, ph);
+      ptx::tc_fence_after();
+      if (et == 0) ptx::bulk_wait_read0();             // previous sample's y staging drained
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (stamp) a.ts[it * 16 + 4] = clock64();
+#pragma unroll
+      for (int g = 0; g < UPT; g += 2) {
+        uint32_t v[2][3][16];
+        float4 rs[2][4];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int j = wg + 2 * ((g + u) / CPS), c0 = ((g + u) % CPS) * 16;
+          const int pix = j * 128 + r;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) rs[u][q] = __ldg(reinterpret_cast<const float4*>(xg + pix * C + c0) + q);
+          const uint32_t t = lane_base + SET2 + (uint32_t)(j * G::N + c0);
+          ptx::tmem_ld_32x32b_x16(t, v[u][0]);
+          ptx::tmem_ld_32x32b_x16(t + C, v[u][1]);
+          ptx::tmem_ld_32x32b_x16(t + 2 * C, v[u][2]);
+        }
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int j = wg + 2 * ((g + u) / CPS), c0 = ((g + u) % CPS) * 16;
+          const int pix = j * 128 + r, w = pix % W;
+          const float* res = reinterpret_cast<const float*>(rs[u]);
+          float f[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float lft = __shfl_up_sync(0xffffffffu, __uint_as_float(v[u][0][q]), 1);
+            const float rgt = __shfl_down_sync(0xffffffffu, __uint_as_float(v[u][2][q]), 1);
+            f[q] = fmaxf(__uint_as_float(v[u][1][q]) + (w > 0 ? lft : 0.f) + (w < W - 1 ? rgt : 0.f) + b2s[c0 + q] +
+                             res[q],
+                         0.f);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            *reinterpret_cast<float4*>(ys + swz<C>((uint32_t)(pix * C + c0 + 4 * q) * 4)) =
+                make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+          if (a.yb) {
+            uint8_t* yb_pl = G::YB_SEP ? ybs : tb + W * 16;     // plane stride: HW*16 / PLANE
+            constexpr int PSTR = G::YB_SEP ? HW * 16 : G::PLANE;
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2)
+              *reinterpret_cast<uint4*>(yb_pl + ((c0 >> 3) + h2) * PSTR + pix * 16) =
+                  make_uint4(pk(f[8 * h2], f[8 * h2 + 1]), pk(f[8 * h2 + 2], f[8 * h2 + 3]),
+                             pk(f[8 * h2 + 4], f[8 * h2 + 5]), pk(f[8 * h2 + 6], f[8 * h2 + 7]));
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(acc2_empty);                    // conv2 accumulator drained
+      // staging writes visible to the async proxy, then one thread stores the sample
+      ptx::fence_proxy_async_smem();
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (et == 0) {
+        if (a.yb) {
+          if (G::YB_SEP)
+            ptx::bulk_store(a.yb + (size_t)dst * C * HW, ptx::smem_u32(ybs), G::YB_BYTES);
+          else
+            for (int p = 0; p < P; ++p)
+              ptx::bulk_store(a.yb + (size_t)dst * C * HW + (size_t)p * HW * 8,
+                              ptx::smem_u32(tb + p * G::PLANE + W * 16), HW * 16);
+        }
+        ptx::bulk_commit();                            // group 1: bf16 copy (T is reused first)
+#pragma unroll
+        for (int k = 0; k < G::NBOX; ++k)
+          ptx::tma_store_2d(&tmY, ptx::smem_u32(ys + k * G::BOX_ROWS * C * 4), 0, dst * HW + k * G::BOX_ROWS);
+        ptx::bulk_commit();                            // group 2: fp32 stream
+      }
+      if (stamp) a.ts[it * 16 + 5] = clock64();
+    }
+    if (et == 0) ptx::bulk_wait0();                    // y writes complete before the CTA retires
+  }
+  __syncthreads();
+  if (warp == 9) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn enc_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+template <int C, int H>
+cudaError_t launch_ch(const BlockArgs& a, int max_rows, int num_sms, cudaStream_t stream) {
+  using G = BCfg<C, H>;
+  EncodeTiledFn enc = enc_fn();
+  if (!enc) return cudaErrorNotSupported;
+  CUtensorMap tm[4];
+  const uint16_t* ws[2] = {a.w1_rt, a.w2_rt};
+  for (int i = 0; i < 2; ++i) {
+    cuuint64_t dims[3] = {8, (cuuint64_t)G::N, (cuuint64_t)G::WCH};
+    cuuint64_t strides[2] = {(cuuint64_t)G::KP_RT * 2, 16};
+    cuuint32_t box[3] = {8, (cuuint32_t)G::N, (cuuint32_t)G::WCH};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (enc(&tm[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, (void*)ws[i], dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  // fp32 stream in / out: [rows][C] fp32, box [BOX_ROWS][C], swizzled to the C*4-byte row
+  const float* xy[2] = {a.x32, a.y32};
+  for (int i = 0; i < 2; ++i) {
+    cuuint64_t dims[2] = {(cuuint64_t)C, (cuuint64_t)max_rows * G::HW};
+    cuuint64_t strides[1] = {(cuuint64_t)C * 4};
+    cuuint32_t box[2] = {(cuuint32_t)C, (cuuint32_t)G::BOX_ROWS};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&tm[2 + i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)xy[i], dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, C == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_block_fused<C, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int grid = max_rows < num_sms ? max_rows : num_sms;
+  if (grid < 1) grid = 1;
+  k_block_fused<C, H><<<grid, THREADS, G::SMEM, stream>>>(tm[0], tm[1], tm[2], tm[3], a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool block_fused_eligible(int C, int H, int W) { return H == W && ((C == 16 && H == 32) || (C == 32 && H == 16)); }
+
+cudaError_t launch_block_fused(const BlockArgs& a, int max_rows, int num_sms, cudaStream_t stream) {
+  if (a.C == 16 && a.H == 32 && a.W == 32) return launch_ch<16, 32>(a, max_rows, num_sms, stream);
+  if (a.C == 32 && a.H == 16 && a.W == 16) return launch_ch<32, 16>(a, max_rows, num_sms, stream);
+  return cudaErrorNotSupported;
+}
+
+}  // namespace dycl

@@ -122,4 +122,22 @@ struct PoolArgs {
 };
 cudaError_t launch_maxpool(const PoolArgs& a, int max_rows, int num_sms, cudaStream_t s);
 
+// Fused residual basic block (block_fused.cu): y = relu(conv2(relu(conv1(x))) + x), 3x3 / stride 1,
+// whole sample per CTA iteration, fp32 stream in/out (+ optional bf16 channel-planar copy).
+struct BlockArgs {
+  const float* x32;        // fp32 NHWC [n][H][W][C] (the block input, also the shortcut)
+  const int32_t* list;     // optional row index list (input row = list[i]), nullptr = identity
+  float* y32;              // fp32 NHWC [n][H][W][C]
+  uint16_t* yb;            // bf16 channel-planar copy or nullptr
+  const uint16_t* w1_rt;   // row-tap weights [3C][Kp_rt] (pack_rowtap)
+  const uint16_t* w2_rt;
+  const float* b1;
+  const float* b2;
+  const int* n_live;
+  int n_static, C, H, W;
+  long long* ts;           // debug only: per-phase clock64 stamps of CTA 0 (nullptr = off)
+};
+bool block_fused_eligible(int C, int H, int W);
+cudaError_t launch_block_fused(const BlockArgs& a, int max_rows, int num_sms, cudaStream_t stream);
+
 }  // namespace dycl

@@ -55,7 +55,7 @@ EXPORTS = [
     "dycl_subnet_conv2d", "dycl_subnet_dense", "dycl_subnet_gap", "dycl_subnet_projection", "dycl_subnet_maxpool", "dycl_subnet_end", "dycl_seq", "dycl_exit",
     "dycl_gate", "dycl_final", "dycl_finalize", "dycl_run", "dycl_run_host", "dycl_num_count_slots",
     "dycl_launches_per_run", "dycl_num_classes", "dycl_set_profiling", "dycl_profile_read",
-    "dycl_debug_conv2d", "dycl_rebalance_plan",
+    "dycl_debug_conv2d", "dycl_rebalance_plan", "dycl_debug_timestamps",
 ]
 
 
@@ -96,6 +96,7 @@ def lib():
             "dycl_set_profiling": [vp, i32],
             "dycl_profile_read": [vp, i32, Pi, Pf, Pd, Pd, Pi],
             "dycl_rebalance_plan": [Pi, i32, i32, Pi, Pi, Pi],
+            "dycl_debug_timestamps": [vp, ctypes.POINTER(ctypes.c_longlong)],
             "dycl_debug_conv2d": [vp, i64, i32, i32, i32, P16, Pf, i32, i32, i32, i32, i32, vp, i32, vp, vp, i32],
         }
         sig.update({
@@ -390,3 +391,9 @@ def dycl_rebalance_plan(counts, rank):
     P = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))  # noqa: E731
     _ck(lib().dycl_rebalance_plan(P(c), w, int(rank), P(snd), P(rcv), ctypes.byref(nc)), None)
     return snd, rcv, nc.value
+
+
+def dycl_debug_timestamps(g):
+    buf = (ctypes.c_longlong * 128)()
+    _ck(lib().dycl_debug_timestamps(g, buf), g)
+    return np.array(buf[:], dtype=np.int64).reshape(8, 16)
