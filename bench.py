@@ -341,7 +341,8 @@ def run_dycl(args):
                     "peak": tf_sus, "unit": "TFLOP/s", "frac": tflops / tf_sus, "traffic": None,
                     "peak_source": peak_src + " bf16 sustained", "hbm_GBps": achieved}
         else:
-            roof = {"kernel": "k_conv_tma (a1: implicit-GEMM conv on tcgen05, fused epilogue)",
+            roof = {"kernel": "a1 conv class: k_block_fused (whole residual block per sample, SMEM-resident) + "
+                              "k_conv_tma / k_gemm_tma (implicit-GEMM conv / dense on tcgen05, fused epilogue)",
                     "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                     "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
                     "tensor_tflops": tflops, "tensor_frac_of_sustained": tflops / tf_sus}
