@@ -289,7 +289,10 @@ dycl_status dycl_s2s_launches(dycl_s2s s, int32_t* out);
  *         [n][c_out/8][Ho][Wo][8], 2 option A from [n][c_out/16][2Ho][2Wo][8]
  *   y   : device bf16 [n][c_out/8][Ho][Wo][8]
  *   path: 0 = the kernel dycl_run would pick, 1 = cp.async-fed kernel, 2 = TMA-fed kernel
- *         (CUDA error "operation not supported" if the shape does not qualify)
+ *         (CUDA error "operation not supported" if the shape does not qualify),
+ *         4 = NHWC layout: x [n][H][W][C], res [n][Ho][Wo][c_out], y [n][Ho][Wo][c_out], run by
+ *         the im2col-TMA GEMM (C % 64 == 0, c_out % 64 == 0; the 8-channel stem by the planar
+ *         kernels, which coincide with NHWC at C = 8)
  * g supplies the device (any created graph).  Errors: INVALID_ARG, UNSUPPORTED, CUDA. */
 dycl_status dycl_debug_conv2d(dycl_graph g, int64_t n, int H, int W, int C, const uint16_t* w, const float* bias,
                               int c_out, int k, int stride, int pad, int relu, const void* res, int res_mode,

@@ -96,6 +96,7 @@ struct dycl_graph_s {
   int conv_path = 0;                 // 0 auto; DYCL_CONV_PATH=1 forces the cp.async kernel
   int conv_dbg = 0;                  // DYCL_CONV_DBG: timing experiments only (results invalid)
   int no_fuse = 0;                   // DYCL_NO_FUSE=1: run basic blocks as two conv launches
+  int nhwc = 0;                      // bf16 activations NHWC (decided at finalize; DYCL_NHWC=0 disables)
   long long* dbg_ts = nullptr;       // DYCL_TS=1: fused-block phase timestamps (development)
   long long max_row_elems = 0;
   int* d_counts = nullptr;
@@ -407,6 +408,7 @@ struct Exec {
         pa.n_live = cnt;
         pa.H = L.in.H; pa.W = L.in.W; pa.C = L.in.Cp(); pa.Ho = L.out.H; pa.Wo = L.out.W;
         pa.k = L.k; pa.stride = L.stride; pa.pad = L.pad;
+        pa.nhwc = g->nhwc;
         prof_begin(DYCL_K_POOL, cnt, (pa.x32 ? 4.0 : 2.0) * L.in.row_elems() + (o.f >= 0 ? 6.0 : 2.0) * L.out.row_elems(), 0, 0);
         cudaError_t e = dycl::launch_maxpool(pa, batch, g->num_sms, st);
         prof_end();
@@ -431,6 +433,7 @@ struct Exec {
         a.ksz = 1; a.stride = L.stride; a.pad = 0;
         a.K = L.K; a.Kp = L.Kp;
         a.relu = 0;
+        a.nhwc = g->nhwc;
         a.dbg = g->conv_dbg;
         prof_begin(DYCL_K_CONV, cnt, 2.0 * L.in.row_elems() + (o.f >= 0 ? 6.0 : 2.0) * L.out.row_elems(),
                    2.0 * L.out.H * L.out.W * L.out.C * (double)L.in.C, 2.0 * L.out.C * L.Kp);
@@ -464,6 +467,7 @@ struct Exec {
       a.res_mode = L.res_mode;
       a.rH = L.res_shape.H; a.rW = L.res_shape.W; a.rC = L.res_shape.Cp();
       a.r_pad_lo = (L.out.C - L.res_shape.C) / 2;
+      a.nhwc = g->nhwc;
       a.dbg = g->conv_dbg;
       const double res_b = L.res_mode ? (a.res32 ? 4.0 : 2.0) * L.res_shape.row_elems() *
                                             (L.res_mode == 2 ? 0.25 : 1.0) : 0.0;
@@ -495,6 +499,7 @@ struct Exec {
     a.K = D.cout;
     a.kind = kind;
     a.thr = thr;
+    a.nhwc = g->nhwc;
     prof_begin(DYCL_K_HEAD, cnt, (a.h32 ? 4.0 : 2.0) * s.in.row_elems() + 4.0 * D.cout + 1,
                2.0 * D.cout * s.in.C + s.in.row_elems(), 2.0 * D.cout * a.C);
     cudaError_t e = dycl::launch_head(a, batch, st);
@@ -915,6 +920,22 @@ dycl_status dycl_finalize(dycl_graph g, int64_t max_batch) {
     N.out = cur;
     maxrow = std::max(maxrow, cur.row_elems());
   }
+  // ---- activation layout: NHWC when every conv past an (at most 8-channel) input has 64-multiple
+  // channel counts (the im2col GEMM's operand boxes are 64 channels wide) and no gate needs an
+  // option-A skip copy; channel-planar otherwise (the CIFAR-width kernels).
+  {
+    bool any = false, ok = g->input.Cp() == 8;
+    for (size_t i = 0; i < g->subnets.size() && ok; ++i)
+      if (planned[i])
+        for (const Layer& L : g->subnets[i].layers)
+          if ((L.kind == L_CONV || L.kind == L_PROJ) && L.in.Cp() > 8) {
+            any = true;
+            ok = ok && L.in.C % 64 == 0 && L.out.C % 64 == 0 && L.res_mode != 2;
+          }
+    for (const Node& N : g->nodes) ok = ok && !(N.kind == N_GATE && N.skip_mode == 1);
+    const char* env = getenv("DYCL_NHWC");
+    g->nhwc = any && ok && !(env && atoi(env) == 0);
+  }
   // ---- weights -> HBM (snapshot), workspace for max_batch
   for (size_t i = 0; i < g->subnets.size(); ++i)
     if (planned[i])
@@ -1057,7 +1078,7 @@ dycl_status dycl_debug_conv2d(dycl_graph g, int64_t n, int H, int W, int C, cons
   cudaMemcpy(db, bias, (size_t)c_out * 4, cudaMemcpyHostToDevice);
   uint16_t* dwr = nullptr;
   int kp_rt = 0;
-  if (k == 3 && stride == 1 && pad == 1 && path != 3) {
+  if (k == 3 && stride == 1 && pad == 1 && path != 3 && path != 4) {
     kp_rt = (3 * C + 63) / 64 * 64;
     std::vector<uint16_t> wr((size_t)3 * c_out * kp_rt);
     dycl::pack_rowtap(wp.data(), c_out, Kp, C, wr.data(), kp_rt);
@@ -1072,7 +1093,9 @@ dycl_status dycl_debug_conv2d(dycl_graph g, int64_t n, int H, int W, int C, cons
   a.rH = 2 * Ho; a.rW = 2 * Wo; a.rC = c_out / 2; a.r_pad_lo = c_out / 4;
   if (res_mode == 1) { a.rH = Ho; a.rW = Wo; a.rC = c_out; a.r_pad_lo = 0; }
   if (path == 2 && dwr) a.dbg |= 32;          // path 2 exercises the row-tap mode where eligible
-  cudaError_t e = n > 0 ? dycl::launch_conv(a, (int)n, g->num_sms, 0, path == 3 ? 2 : path) : cudaSuccess;
+  a.nhwc = path == 4;                         // path 4: NHWC tensors, im2col GEMM (8-channel stem: planar kernels)
+  cudaError_t e = n > 0 ? dycl::launch_conv(a, (int)n, g->num_sms, 0, path == 3 ? 2 : path == 4 ? 0 : path)
+                        : cudaSuccess;
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   cudaFree(dwr);
   cudaFree(dw);

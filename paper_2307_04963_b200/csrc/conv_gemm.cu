@@ -1,0 +1,339 @@
+// NHWC implicit-GEMM convolution on tcgen05 with TMA im2col operand loads (SURVEY §8(a) a1,
+// the ImageNet-scale layers of config 5: 1x1 / 3x3 / strided convs with C_in, C_out >= 64).
+//
+//   D[m, o] = sum_{r,s,c} X[n, ho*st - pad + r, wo*st - pad + s, c] * W[o, (r*k + s)*C + c]
+//   m = flat output pixel (n, ho, wo) -- M runs across samples, so a 128-row tile never
+//   wastes rows on a sample boundary (7x7 maps at stage 4 would waste 62% with per-sample
+//   tiles).
+//
+// A operand (activations, bf16 NHWC [n][H][W][C]): one TMA im2col box per (tap, 64-channel
+// block): 128 consecutive output pixels x 64 channels, the tap given as the im2col offset,
+// the conv's zero padding and stride done by the TMA unit (bounding box = the output grid,
+// traversal stride = conv stride; verified in tools/im2col_probe.cu).  1x1 / stride-1 layers
+// use a plain 2-D tiled box of the [M][C] matrix.  B operand (weights [Cout][k*k*C], K
+// ordered (r, s, c)): a 2-D tiled box.  Both land in SMEM in the 128-byte-swizzled K-major
+// layout; tcgen05.mma 128 x BN x 16 reads them by descriptor.
+//
+// Persistent warp-specialised CTA (one per SM): warp 8 = TMA producer (one lane), warp 9 =
+// TMEM allocator + MMA issuer (one lane), warps 0-7 = two epilogue warpgroups alternating
+// tiles over two TMEM accumulators.  The fused epilogue adds bias (+ identity shortcut from
+// the fp32 residual stream or the bf16 tensor), applies ReLU and writes bf16 NHWC (+ the fp32
+// stream copy).  Tiles are numbered with the N tile fastest, so the CTAs running at the same
+// time share A tiles through L2.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace dycl {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BKE = 64;                 // K elements per stage: one 128-byte swizzle row
+constexpr int THREADS = 320;
+
+template <int BN>
+struct CG {
+  static constexpr int A_BYTES = BM * BKE * 2;
+  static constexpr int B_BYTES = BN * BKE * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+};
+
+__device__ __forceinline__ void tma_im2col_4d(uint32_t dst, const void* tmap, uint32_t bar, int c, int w, int h, int n,
+                                              uint16_t ow, uint16_t oh) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, "
+      "%6}], [%2], {%7, %8};" ::"r"(dst),
+      "l"(tmap), "r"(bar), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow), "h"(oh)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t pk2(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int BN, bool IM2COL>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_conv_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const ConvArgs a) {
+  using G = CG<BN>;
+  constexpr int S = G::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * G::A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + S * G::B_BYTES);
+  const uint32_t full0 = ptx::smem_u32(bars);
+  const uint32_t empty0 = full0 + 8 * S;
+  const uint32_t tfull0 = empty0 + 8 * S;
+  const uint32_t tempty0 = tfull0 + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_live = a.n_live ? *a.n_live : a.n_static;
+  const int HWo = a.Ho * a.Wo;
+  const long long M = (long long)n_live * HWo;
+  const int m_tiles = (int)((M + BM - 1) / BM);
+  const int n_tiles = a.Cout / BN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int cblocks = a.C / BKE;
+  const int kblocks = a.ksz * a.ksz * cblocks;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      ptx::mbar_init(full0 + 8 * i, 1);
+      ptx::mbar_init(empty0 + 8 * i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(tfull0 + 8 * i, 1);
+      ptx::mbar_init(tempty0 + 8 * i, 128);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 9) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), G::TMEM_COLS);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 8) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      ptx::tma_prefetch_desc(&tmA);
+      ptx::tma_prefetch_desc(&tmB);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m_tile = tile / n_tiles, n_tile = tile - m_tile * n_tiles;
+        const long long p0 = (long long)m_tile * BM;
+        const int n0 = (int)(p0 / HWo);
+        const int rem = (int)(p0 - (long long)n0 * HWo);
+        const int ho0 = rem / a.Wo, wo0 = rem - (rem / a.Wo) * a.Wo;
+        const int wb = wo0 * a.stride - a.pad, hb = ho0 * a.stride - a.pad;
+        int kb = 0;
+        for (int r = 0; r < a.ksz; ++r)
+          for (int s = 0; s < a.ksz; ++s)
+            for (int cb = 0; cb < cblocks; ++cb, ++kb) {
+              ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1);
+              const uint32_t bar = full0 + 8 * stage;
+              ptx::mbar_arrive_expect_tx(bar, (uint32_t)G::STAGE);
+              const uint32_t da = ptx::smem_u32(sA + stage * G::A_BYTES);
+              if (IM2COL)
+                tma_im2col_4d(da, &tmA, bar, cb * BKE, wb, hb, n0, (uint16_t)s, (uint16_t)r);
+              else
+                ptx::tma_load_2d(da, &tmA, bar, cb * BKE, (int)p0);
+              ptx::tma_load_2d(ptx::smem_u32(sB + stage * G::B_BYTES), &tmB, bar, kb * BKE, n_tile * BN);
+              if (++stage == S) {
+                stage = 0;
+                phase ^= 1;
+              }
+            }
+      }
+    }
+  } else if (warp == 9) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t IDESC = ptx::make_idesc_bf16(BM, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      ptx::mbar_wait(tempty0 + 8 * acc, ((it >> 1) & 1) ^ 1);
+      ptx::tc_fence_after();
+      const uint32_t d = tmem_base + (uint32_t)(acc * BN);
+      for (int kb = 0; kb < kblocks; ++kb) {
+        ptx::mbar_wait(full0 + 8 * stage, phase);
+        ptx::tc_fence_after();
+        const uint64_t ad = ptx::make_smem_desc_sw128(ptx::smem_u32(sA + stage * G::A_BYTES));
+        const uint64_t bd = ptx::make_smem_desc_sw128(ptx::smem_u32(sB + stage * G::B_BYTES));
+#pragma unroll
+        for (int j = 0; j < BKE / 16; ++j)
+          ptx::mma_bf16_ss_elect(d, ad + (uint64_t)(2 * j), bd + (uint64_t)(2 * j), IDESC, (uint32_t)((kb | j) != 0));
+        ptx::mma_commit_elect(empty0 + 8 * stage);
+        __syncwarp();
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      ptx::mma_commit_elect(tfull0 + 8 * acc);
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (2 warpgroups)
+    const int wg = warp >> 2, quad = warp & 3;
+    const int r = quad * 32 + lane;                         // TMEM lane = row of the tile
+    const bool res = a.res_mode == 1;
+    const bool res_f = res && a.res32 != nullptr;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      if ((it & 1) != wg) continue;
+      const int acc = it & 1;
+      const int m_tile = tile / n_tiles, n_tile = tile - m_tile * n_tiles;
+      const long long m = (long long)m_tile * BM + r;
+      const bool ok = m < M;
+      const int col0 = n_tile * BN;
+      const size_t rowo = (size_t)(ok ? m : 0) * a.Cout + col0;
+      // shortcut chunk (32 channels) prefetch: issued before the accumulator wait
+      float4 rs[8];
+      auto load_res = [&](int c0) {
+        if (res_f) {
+          const float4* q = reinterpret_cast<const float4*>(a.res32 + rowo + c0);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) rs[j] = ok ? __ldg(q + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        } else if (res) {
+          const uint4* q = reinterpret_cast<const uint4*>(a.res + rowo + c0);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint4 u = ok ? __ldg(q + j) : make_uint4(0, 0, 0, 0);
+            rs[2 * j] = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u),
+                                    __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xFFFF0000u));
+            rs[2 * j + 1] = make_float4(__uint_as_float(u.z << 16), __uint_as_float(u.z & 0xFFFF0000u),
+                                        __uint_as_float(u.w << 16), __uint_as_float(u.w & 0xFFFF0000u));
+          }
+        }
+      };
+      if (res) load_res(0);
+      ptx::mbar_wait(tfull0 + 8 * acc, (it >> 1) & 1);
+      ptx::tc_fence_after();
+      const uint32_t t_base = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t v[32];
+        ptx::tmem_ld_32x32b_x16(t_base + (uint32_t)c0, *reinterpret_cast<uint32_t(*)[16]>(v));
+        ptx::tmem_ld_32x32b_x16(t_base + (uint32_t)c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
+        ptx::tmem_ld_wait();
+        float f[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]) + __ldg(a.bias + col0 + c0 + j);
+        if (res) {
+          const float* rf = reinterpret_cast<const float*>(rs);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) f[j] += rf[j];
+          if (c0 + 32 < BN) load_res(c0 + 32);              // next chunk's shortcut in flight
+        }
+        if (a.relu) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) f[j] = fmaxf(f[j], 0.0f);
+        }
+        if (ok) {
+          if (a.y) {
+            uint4* yq = reinterpret_cast<uint4*>(a.y + rowo + c0);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              yq[j] = make_uint4(pk2(f[8 * j], f[8 * j + 1]), pk2(f[8 * j + 2], f[8 * j + 3]),
+                                 pk2(f[8 * j + 4], f[8 * j + 5]), pk2(f[8 * j + 6], f[8 * j + 7]));
+          }
+          if (a.y32) {
+            float4* zq = reinterpret_cast<float4*>(a.y32 + rowo + c0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) zq[j] = make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(tempty0 + 8 * acc);
+    }
+  }
+  __syncthreads();
+  if (warp == 9) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, G::TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+typedef CUresult (*EncodeIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t, const cuuint32_t*,
+                                   CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                   CUtensorMapFloatOOBfill);
+
+template <typename F>
+F driver_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
+    return reinterpret_cast<F>(p);
+  return nullptr;
+}
+
+template <int BN, bool IM2COL>
+cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream) {
+  static EncodeTiledFn enc = driver_fn<EncodeTiledFn>("cuTensorMapEncodeTiled");
+  static EncodeIm2colFn enc_i2c = driver_fn<EncodeIm2colFn>("cuTensorMapEncodeIm2col");
+  if (!enc || !enc_i2c) return cudaErrorNotSupported;
+  CUtensorMap tmA, tmB;
+  const int rows = max_rows > 0 ? max_rows : 1;
+  if (IM2COL) {
+    cuuint64_t dims[4] = {(cuuint64_t)a.C, (cuuint64_t)a.W, (cuuint64_t)a.H, (cuuint64_t)rows};
+    cuuint64_t strides[3] = {(cuuint64_t)a.C * 2, (cuuint64_t)a.W * a.C * 2, (cuuint64_t)a.H * a.W * a.C * 2};
+    // bounding box of the filter origins = the output grid: {W, H} order (tools/im2col_probe.cu)
+    int lower[2] = {-a.pad, -a.pad};
+    int upper[2] = {(a.Wo - 1) * a.stride - a.pad - (a.W - 1), (a.Ho - 1) * a.stride - a.pad - (a.H - 1)};
+    cuuint32_t es[4] = {1, (cuuint32_t)a.stride, (cuuint32_t)a.stride, 1};
+    if (enc_i2c(&tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)a.x, dims, strides, lower, upper, BKE, BM, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  } else {
+    cuuint64_t dims[2] = {(cuuint64_t)a.C, (cuuint64_t)rows * a.H * a.W};
+    cuuint64_t strides[1] = {(cuuint64_t)a.C * 2};
+    cuuint32_t box[2] = {BKE, BM};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)a.x, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)a.Kp, (cuuint64_t)a.Cout};
+    cuuint64_t strides[1] = {(cuuint64_t)a.Kp * 2};
+    cuuint32_t box[2] = {BKE, BN};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)a.w, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e =
+        cudaFuncSetAttribute(k_conv_gemm<BN, IM2COL>, cudaFuncAttributeMaxDynamicSharedMemorySize, CG<BN>::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const long long tiles = ((long long)rows * a.Ho * a.Wo + BM - 1) / BM * (a.Cout / BN);
+  int grid = (int)(tiles < num_sms ? tiles : num_sms);
+  if (grid < 1) grid = 1;
+  k_conv_gemm<BN, IM2COL><<<grid, THREADS, CG<BN>::SMEM, stream>>>(tmA, tmB, a);
+  return cudaGetLastError();
+}
+
+template <int BN>
+cudaError_t launch_bn(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream) {
+  const bool tiled = a.ksz == 1 && a.stride == 1 && a.pad == 0;
+  return tiled ? launch_t<BN, false>(a, max_rows, num_sms, stream) : launch_t<BN, true>(a, max_rows, num_sms, stream);
+}
+
+}  // namespace
+
+bool conv_gemm_eligible(const ConvArgs& a) {
+  return a.nhwc && a.C % BKE == 0 && a.Cout % 64 == 0 && a.K == a.ksz * a.ksz * a.C && a.Kp == a.K &&
+         a.res_mode != 2 && a.pad <= 32 && a.stride <= 8 && (a.ksz > 1 || a.stride > 1 || a.H == a.Ho);
+}
+
+cudaError_t launch_conv_gemm(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream) {
+  if (!conv_gemm_eligible(a)) return cudaErrorNotSupported;
+  if (a.Cout % 256 == 0) return launch_bn<256>(a, max_rows, num_sms, stream);
+  if (a.Cout % 128 == 0) return launch_bn<128>(a, max_rows, num_sms, stream);
+  return launch_bn<64>(a, max_rows, num_sms, stream);
+}
+
+}  // namespace dycl

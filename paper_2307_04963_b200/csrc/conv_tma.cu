@@ -693,6 +693,12 @@ cudaError_t launch_conv_tma(const ConvArgs& a, int max_rows, int num_sms, cudaSt
 }
 
 cudaError_t launch_conv(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream, int path) {
+  if (a.nhwc) {
+    // NHWC graphs: the im2col GEMM for every C % 64 layer; the 8-channel stem (planar == NHWC
+    // at C = 8) keeps the planar kernels, whose epilogue writes NHWC.
+    if (conv_gemm_eligible(a)) return launch_conv_gemm(a, max_rows, num_sms, stream);
+    if (a.C != 8) return cudaErrorNotSupported;
+  }
   if (path != 1 && gemm_tma_eligible(a) && (a.dbg & 64) == 0) return launch_gemm_tma(a, max_rows, num_sms, stream);
   if (path != 1) {
     bool handled = false;

@@ -5,6 +5,7 @@
 //   bf16 activations: channel-planar "NC8HW8"  [n][C/8][H][W][8]  (16-byte pixel chunks;
 //                     a TMA box row is then a whole image row of one 8-channel plane)
 //   fp32 stream:      NHWC                     [n][H][W][C]
+//   (ConvArgs.nhwc: bf16 activations NHWC as well -- the config-5 layout)
 #pragma once
 #include <cuda_bf16.h>
 
@@ -53,7 +54,8 @@ __device__ __forceinline__ void conv_finish16(const ConvArgs& a, int n, int ho, 
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const uint4 r = __ldg(reinterpret_cast<const uint4*>(
-            a.res + (size_t)n * a.Cout * HWo + (size_t)((o0 >> 3) + h) * HWo * 8 + pix * 8));
+            a.nhwc ? a.res + ((size_t)n * HWo + pix) * a.Cout + o0 + 8 * h
+                   : a.res + (size_t)n * a.Cout * HWo + (size_t)((o0 >> 3) + h) * HWo * 8 + pix * 8));
         const uint32_t u[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -87,7 +89,8 @@ __device__ __forceinline__ void conv_finish16(const ConvArgs& a, int n, int ho, 
     o.y = pack_bf16x2_rn(f[8 * h + 2], f[8 * h + 3]);
     o.z = pack_bf16x2_rn(f[8 * h + 4], f[8 * h + 5]);
     o.w = pack_bf16x2_rn(f[8 * h + 6], f[8 * h + 7]);
-    *reinterpret_cast<uint4*>(a.y + (size_t)n * a.Cout * HWo + (size_t)((o0 >> 3) + h) * HWo * 8 + pix * 8) = o;
+    *reinterpret_cast<uint4*>(a.nhwc ? a.y + ((size_t)n * HWo + pix) * a.Cout + o0 + 8 * h
+                                     : a.y + (size_t)n * a.Cout * HWo + (size_t)((o0 >> 3) + h) * HWo * 8 + pix * 8) = o;
   }
   if (a.y32) {
     float4* yq = reinterpret_cast<float4*>(a.y32 + ((size_t)n * HWo + pix) * a.Cout + o0);

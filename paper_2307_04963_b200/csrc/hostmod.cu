@@ -78,9 +78,10 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head(const HeadArgs a) {
           acc[4] += v1.x; acc[5] += v1.y; acc[6] += v1.z; acc[7] += v1.w;
         }
       } else {
-        // bf16 channel-planar [C/8][HW][8]
+        // bf16 channel-planar [C/8][HW][8] (or NHWC [HW][C])
         for (int p = t / G; p < a.HW; p += P) {
-          const uint4 v = __ldg(reinterpret_cast<const uint4*>(h + ((size_t)grp * a.HW + p) * 8));
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.nhwc ? h + (size_t)p * a.C + grp * 8
+                                                                      : h + ((size_t)grp * a.HW + p) * 8));
           const uint32_t u[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -297,10 +298,19 @@ __global__ void k_maxpool(const PoolArgs a) {
   const int HWo = a.Ho * a.Wo;
   const int64_t total = (int64_t)n_live * G * HWo;
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total; u += (int64_t)gridDim.x * blockDim.x) {
-    const int p = (int)(u % HWo);
-    const int64_t t = u / HWo;
-    const int g = (int)(t % G);
-    const int64_t n = t / G;
+    int p, g;
+    int64_t n;
+    if (a.nhwc) {                                    // consecutive threads = consecutive channel groups
+      g = (int)(u % G);
+      const int64_t t = u / G;
+      p = (int)(t % HWo);
+      n = t / HWo;
+    } else {
+      p = (int)(u % HWo);
+      const int64_t t = u / HWo;
+      g = (int)(t % G);
+      n = t / G;
+    }
     const int ho = p / a.Wo, wo = p - (p / a.Wo) * a.Wo;
     float m[8];
 #pragma unroll
@@ -318,7 +328,8 @@ __global__ void k_maxpool(const PoolArgs a) {
           m[0] = fmaxf(m[0], v0.x); m[1] = fmaxf(m[1], v0.y); m[2] = fmaxf(m[2], v0.z); m[3] = fmaxf(m[3], v0.w);
           m[4] = fmaxf(m[4], v1.x); m[5] = fmaxf(m[5], v1.y); m[6] = fmaxf(m[6], v1.z); m[7] = fmaxf(m[7], v1.w);
         } else {
-          const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.x + ((n * G + g) * (int64_t)a.H * a.W + pix) * 8));
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(
+              a.nhwc ? a.x + (n * a.H * a.W + pix) * a.C + g * 8 : a.x + ((n * G + g) * (int64_t)a.H * a.W + pix) * 8));
           const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -334,7 +345,8 @@ __global__ void k_maxpool(const PoolArgs a) {
       __nv_bfloat162 v = __floats2bfloat162_rn(m[2 * j], m[2 * j + 1]);
       o[j] = *reinterpret_cast<uint32_t*>(&v);
     }
-    *reinterpret_cast<uint4*>(a.y + ((n * G + g) * (int64_t)HWo + p) * 8) = make_uint4(o[0], o[1], o[2], o[3]);
+    *reinterpret_cast<uint4*>(a.nhwc ? a.y + (n * HWo + p) * a.C + g * 8 : a.y + ((n * G + g) * (int64_t)HWo + p) * 8) =
+        make_uint4(o[0], o[1], o[2], o[3]);
     if (a.y32) {
       float4* q = reinterpret_cast<float4*>(a.y32 + (n * HWo + p) * a.C + g * 8);
       q[0] = make_float4(m[0], m[1], m[2], m[3]);

@@ -27,6 +27,7 @@ struct ConvArgs {
   int relu;
   int res_mode;          // 0 none, 1 identity [n][Ho][Wo][Cout], 2 option A from [n][rH][rW][rC]
   int rH, rW, rC, r_pad_lo;
+  int nhwc = 0;          // 1: bf16 tensors (x, y, res) are NHWC [n][H][W][C] instead of channel-planar
   int dbg = 0;           // bit5 (32): row-tap mode opt-in; experiments only (results invalid): bit0 skip
                          // epilogue math/stores, bit1 skip MMAs, bit2 skip A loads, bit3 no residual prefetch
 };
@@ -51,6 +52,9 @@ cudaError_t launch_conv_tma(const ConvArgs& a, int max_rows, int num_sms, cudaSt
 // Dense-layer GEMM on tcgen05 with TMA SWIZZLE_128B tiles (gemm_tma.cu): [rows][K] x [N][K].
 bool gemm_tma_eligible(const ConvArgs& a);
 cudaError_t launch_gemm_tma(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream);
+// NHWC implicit-GEMM conv with TMA im2col operand loads (conv_gemm.cu): C % 64 == 0, Cout % 64 == 0.
+bool conv_gemm_eligible(const ConvArgs& a);
+cudaError_t launch_conv_gemm(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream);
 // Dispatch: path 0 = auto (TMA when possible), 1 = cp.async kernel, 2 = TMA only.
 cudaError_t launch_conv(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream, int path = 0);
 
@@ -74,6 +78,7 @@ struct HeadArgs {
   const int* n_live;
   int HW, C, K, kind;
   float thr;
+  int nhwc = 0;          // bf16 h is NHWC [n][HW][C] (else channel-planar)
 };
 cudaError_t launch_head(const HeadArgs& a, int max_rows, cudaStream_t s);
 
@@ -119,6 +124,7 @@ struct PoolArgs {
   float* y32;
   const int* n_live;
   int H, W, C, Ho, Wo, k, stride, pad;
+  int nhwc = 0;          // bf16 x / y are NHWC (else channel-planar)
 };
 cudaError_t launch_maxpool(const PoolArgs& a, int max_rows, int num_sms, cudaStream_t s);
 

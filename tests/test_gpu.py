@@ -114,6 +114,48 @@ def test_conv_kernel_matches_oracle_conv(any_graph, path, case):
         assert np.mean(got[i] != ref) < 0.01
 
 
+# NHWC im2col-TMA GEMM (config-5 layers): flat M across samples with ragged tails
+NHWC_CASES = [
+    # n, H, W, C, Cout, k, stride, pad, relu, res_mode
+    (3, 14, 14, 64, 64, 1, 1, 0, 1, 0),      # 1x1, tiled A box, BN 64, M = 588 (ragged)
+    (2, 14, 14, 128, 256, 1, 1, 0, 0, 1),    # 1x1 + identity shortcut, BN 256
+    (3, 7, 7, 64, 128, 3, 1, 1, 1, 0),       # 3x3 im2col, 7x7 maps: tiles span 3 samples
+    (2, 12, 10, 128, 128, 3, 1, 1, 1, 1),    # non-square, shortcut, two channel blocks
+    (3, 14, 14, 64, 128, 3, 2, 1, 1, 0),     # 3x3 stride 2 (stage transition)
+    (3, 14, 14, 128, 512, 1, 2, 0, 0, 0),    # 1x1 stride 2 projection, N tiling 2 x 256
+    (2, 9, 9, 64, 64, 7, 2, 3, 1, 0),        # 7x7 stride 2 pad 3
+    (4, 16, 16, 8, 64, 7, 2, 3, 1, 0),       # stem (C = 8): planar kernels, NHWC output
+    (1, 1, 1, 64, 64, 1, 1, 0, 1, 0),        # single row
+]
+
+
+@pytest.mark.parametrize("case", NHWC_CASES, ids=[f"nhwc-{c}" for c in NHWC_CASES])
+def test_conv_gemm_nhwc_matches_oracle_conv(any_graph, case):
+    n, H, W, C, Co, k, st, pad, relu, res_mode = case
+    rng = np.random.default_rng(abs(hash(case)) % 2**32)
+    x = wl.f32_to_bf16_bits(rng.standard_normal((n, H, W, C)))
+    w = wl.f32_to_bf16_bits(rng.standard_normal((Co, k, k, C)) * np.sqrt(2.0 / (k * k * C)))
+    b = rng.uniform(-0.1, 0.1, Co).astype(np.float32)
+    Ho, Wo = (H + 2 * pad - k) // st + 1, (W + 2 * pad - k) // st + 1
+    res = wl.f32_to_bf16_bits(rng.standard_normal((n, Ho, Wo, Co))) if res_mode == 1 else None
+    y = torch.zeros((n, Ho, Wo, Co), dtype=torch.int16, device=DEV)
+    D.dycl_debug_conv2d(any_graph, _bits_to_t(x), n, H, W, C, w, b, Co, k, st, pad, relu,
+                        _bits_to_t(res) if res is not None else None, res_mode, y, 4)
+    got = _t_to_f64(y)
+    xf, wf = prg._bf16_to_f64(x), prg._bf16_to_f64(w)
+    for i in range(n):
+        ref = O.conv2d(xf[i], wf, b.astype(np.float64), st, pad)
+        if res_mode == 1:
+            ref = ref + prg._bf16_to_f64(res[i])
+        if relu:
+            ref = O.relu(ref)
+        ref = O.round_bf16(ref)
+        tol = 2.0 ** -7 * np.abs(ref) + 1e-6
+        bad = np.abs(got[i] - ref) > tol
+        assert not bad.any(), (i, np.argwhere(bad)[:5], got[i][bad][:5], ref[bad][:5])
+        assert np.mean(got[i] != ref) < 0.01
+
+
 def test_conv_kernel_zero_rows(any_graph):
     y = torch.full((1, 4, 4, 16), 7, dtype=torch.int16, device=DEV)
     x = torch.zeros((1, 4, 4, 16), dtype=torch.int16, device=DEV)
