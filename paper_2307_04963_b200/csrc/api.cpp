@@ -47,6 +47,12 @@ struct Layer {
   uint16_t* d_wrt = nullptr;    // row-tap layout (3x3 / stride 1 / pad 1 convs)
   int Kp_rt = 0;
   float* d_b = nullptr;
+  // space-to-depth stem (NHWC graphs): a 7x7 / stride-2 conv on <= 4 channels runs as a 3x3 /
+  // stride-1 conv over 4x4 pixel blocks (64 channels) producing the 2x2 output phases as
+  // 4*cout channels; d_w / d_b then hold that packed form ([4*cout][9*64], [4*cout])
+  int s4d = 0;
+  int pool_s2d = 0;           // maxpool reading that phase layout (3x3 / stride 2 / pad 1)
+  uint16_t* d_wt = nullptr;   // wide fp32 heads (K >= 128): weights transposed [C][K] for the batched FC
 };
 
 struct Subnet {
@@ -97,6 +103,7 @@ struct dycl_graph_s {
   int conv_dbg = 0;                  // DYCL_CONV_DBG: timing experiments only (results invalid)
   int no_fuse = 0;                   // DYCL_NO_FUSE=1: run basic blocks as two conv launches
   int nhwc = 0;                      // bf16 activations NHWC (decided at finalize; DYCL_NHWC=0 disables)
+  int stem_s4d = 0;                  // input cast to 4x4 space-to-depth for the stem (DYCL_STEM_S4D=0 disables)
   long long* dbg_ts = nullptr;       // DYCL_TS=1: fused-block phase timestamps (development)
   long long max_row_elems = 0;
   int* d_counts = nullptr;
@@ -107,6 +114,7 @@ struct dycl_graph_s {
   uint8_t* d_flag = nullptr;
   float* d_pred = nullptr;
   float* d_z = nullptr;
+  float* d_gpool = nullptr;         // pooled features of wide heads [max_batch][max head C]
   float* d_in_stage = nullptr;      // dycl_run_host staging
   float* d_logit_stage = nullptr;
   int32_t* d_path_stage = nullptr;
@@ -249,6 +257,35 @@ dycl_status plan_subnet(dycl_graph g, Subnet& s, const Shape& in, int sn_id) {
 
 dycl_status upload_subnet(dycl_graph g, Subnet& s) {
   for (Layer& L : s.layers) {
+    if (L.kind == L_CONV && L.s4d) {
+      // W'[(b*2+b')*cout + o][(R*3+S)*64 + (pr*4+ps)*Cin + c] = w[o][r][s][c] with
+      // r = 4(R-1) + pr - 2b + pad, s = 4(S-1) + ps - 2b' + pad (zero outside the 7x7 window):
+      // output pixel (2P+b, 2Q+b') reads input rows 4(P+R-1)+pr of blocks P-1..P+1.
+      const int Cin = L.in.C, co = L.cout, K4 = 9 * 64;
+      std::vector<uint16_t> w4((size_t)4 * co * K4, 0);
+      for (int b = 0; b < 2; ++b)
+        for (int b2 = 0; b2 < 2; ++b2)
+          for (int o = 0; o < co; ++o)
+            for (int R = 0; R < 3; ++R)
+              for (int S = 0; S < 3; ++S)
+                for (int pr = 0; pr < 4; ++pr)
+                  for (int ps = 0; ps < 4; ++ps) {
+                    const int r = 4 * (R - 1) + pr - 2 * b + L.pad, s2 = 4 * (S - 1) + ps - 2 * b2 + L.pad;
+                    if (r < 0 || r >= L.k || s2 < 0 || s2 >= L.k) continue;
+                    for (int c = 0; c < Cin; ++c)
+                      w4[(size_t)((b * 2 + b2) * co + o) * K4 + (R * 3 + S) * 64 + (pr * 4 + ps) * Cin + c] =
+                          L.w[(((size_t)o * L.k + r) * L.k + s2) * Cin + c];
+                  }
+      dycl_status st = dmalloc(g, &L.d_w, w4.size() * 2);
+      if (st) return st;
+      CK(cudaMemcpy(L.d_w, w4.data(), w4.size() * 2, cudaMemcpyHostToDevice));
+      std::vector<float> b4((size_t)4 * co);
+      for (int q = 0; q < 4; ++q)
+        for (int o = 0; o < co; ++o) b4[(size_t)q * co + o] = L.b[o];
+      if ((st = dmalloc(g, &L.d_b, b4.size() * 4))) return st;
+      CK(cudaMemcpy(L.d_b, b4.data(), b4.size() * 4, cudaMemcpyHostToDevice));
+      continue;
+    }
     if (L.kind == L_CONV || L.kind == L_PROJ || (L.kind == L_DENSE && !L.out_fp32)) {
       // repack to [Cout][k][k][Cp] padded along K to Kp (zeros)
       const int Cin = L.in.C, Cp = L.in.Cp();
@@ -275,6 +312,13 @@ dycl_status upload_subnet(dycl_graph g, Subnet& s) {
       dycl_status st = dmalloc(g, &L.d_w, wp.size() * 2);
       if (st) return st;
       CK(cudaMemcpy(L.d_w, wp.data(), wp.size() * 2, cudaMemcpyHostToDevice));
+      if (L.cout >= 128 && L.cout <= 1024) {
+        std::vector<uint16_t> wt((size_t)Cp * L.cout, 0);
+        for (int o = 0; o < L.cout; ++o)
+          for (int c = 0; c < Cin; ++c) wt[(size_t)c * L.cout + o] = L.w[(size_t)o * Cin + c];
+        if ((st = dmalloc(g, &L.d_wt, wt.size() * 2))) return st;
+        CK(cudaMemcpy(L.d_wt, wt.data(), wt.size() * 2, cudaMemcpyHostToDevice));
+      }
     }
     if (!L.b.empty()) {
       dycl_status st = dmalloc(g, &L.d_b, L.b.size() * 4);
@@ -409,6 +453,7 @@ struct Exec {
         pa.H = L.in.H; pa.W = L.in.W; pa.C = L.in.Cp(); pa.Ho = L.out.H; pa.Wo = L.out.W;
         pa.k = L.k; pa.stride = L.stride; pa.pad = L.pad;
         pa.nhwc = g->nhwc;
+        pa.s2d = L.pool_s2d;
         prof_begin(DYCL_K_POOL, cnt, (pa.x32 ? 4.0 : 2.0) * L.in.row_elems() + (o.f >= 0 ? 6.0 : 2.0) * L.out.row_elems(), 0, 0);
         cudaError_t e = dycl::launch_maxpool(pa, batch, g->num_sms, st);
         prof_end();
@@ -468,6 +513,13 @@ struct Exec {
       a.rH = L.res_shape.H; a.rW = L.res_shape.W; a.rC = L.res_shape.Cp();
       a.r_pad_lo = (L.out.C - L.res_shape.C) / 2;
       a.nhwc = g->nhwc;
+      if (L.s4d) {                     // 3x3 / stride 1 over 4x4 blocks, 2x2 output phases in N
+        a.H = L.in.H / 4; a.W = L.in.W / 4; a.C = 64;
+        a.Ho = L.out.H / 2; a.Wo = L.out.W / 2; a.Cout = 4 * L.out.C;
+        a.ksz = 3; a.stride = 1; a.pad = 1;
+        a.K = a.Kp = 9 * 64;
+        a.w_rt = nullptr;
+      }
       a.dbg = g->conv_dbg;
       const double res_b = L.res_mode ? (a.res32 ? 4.0 : 2.0) * L.res_shape.row_elems() *
                                             (L.res_mode == 2 ? 0.25 : 1.0) : 0.0;
@@ -500,6 +552,10 @@ struct Exec {
     a.kind = kind;
     a.thr = thr;
     a.nhwc = g->nhwc;
+    if (D.d_wt && kind != 1 && g->d_gpool) {
+      a.wt = D.d_wt;
+      a.gpool = g->d_gpool;
+    }
     prof_begin(DYCL_K_HEAD, cnt, (a.h32 ? 4.0 : 2.0) * s.in.row_elems() + 4.0 * D.cout + 1,
                2.0 * D.cout * s.in.C + s.in.row_elems(), 2.0 * D.cout * a.C);
     cudaError_t e = dycl::launch_head(a, batch, st);
@@ -567,7 +623,8 @@ struct Exec {
     if (e != cudaSuccess) return cuda_fail(g, e, "launch_init");
     const Shape& in = g->input;
     prof_begin(DYCL_K_INPUT, nullptr, 0, 0, (double)batch * in.H * in.W * (4.0 * in.C + 2.0 * in.Cp()));
-    e = dycl::launch_cast_pad(input, g->buf[0], batch, in.H * in.W, in.C, in.Cp(), st);
+    e = g->stem_s4d ? dycl::launch_cast_s4d(input, g->buf[0], batch, in.H, in.W, in.C, st)
+                    : dycl::launch_cast_pad(input, g->buf[0], batch, in.H * in.W, in.C, in.Cp(), st);
     prof_end();
     if (e != cudaSuccess) return cuda_fail(g, e, "launch_cast_pad");
     Tensor cur;
@@ -680,6 +737,7 @@ dycl_status dycl_graph_destroy(dycl_graph g) {
     for (Layer& L : s.layers) {
       cudaFree(L.d_w);
       cudaFree(L.d_wrt);
+      cudaFree(L.d_wt);
       cudaFree(L.d_b);
     }
   for (auto* b : g->buf) cudaFree(b);
@@ -692,6 +750,7 @@ dycl_status dycl_graph_destroy(dycl_graph g) {
   cudaFree(g->d_flag);
   cudaFree(g->d_pred);
   cudaFree(g->d_z);
+  cudaFree(g->d_gpool);
   cudaFree(g->d_in_stage);
   cudaFree(g->d_logit_stage);
   cudaFree(g->d_path_stage);
@@ -935,6 +994,23 @@ dycl_status dycl_finalize(dycl_graph g, int64_t max_batch) {
     for (const Node& N : g->nodes) ok = ok && !(N.kind == N_GATE && N.skip_mode == 1);
     const char* env = getenv("DYCL_NHWC");
     g->nhwc = any && ok && !(env && atoi(env) == 0);
+    // space-to-depth stem: the first layer run is a 7x7 / stride-2 / pad-3 conv on <= 4 input
+    // channels followed by a 3x3 / stride-2 / pad-1 max pool (the ImageNet ResNet stem)
+    g->stem_s4d = 0;
+    const char* env4 = getenv("DYCL_STEM_S4D");
+    if (g->nhwc && !(env4 && atoi(env4) == 0)) {
+      Subnet& S0 = g->subnets[g->nodes[0].sn];
+      if (S0.layers.size() >= 2) {
+        Layer &L0 = S0.layers[0], &L1 = S0.layers[1];
+        if (L0.kind == L_CONV && L0.k == 7 && L0.stride == 2 && L0.pad == 3 && L0.in.C <= 4 && !L0.residual &&
+            L0.relu && L0.in.H % 4 == 0 && L0.in.W % 4 == 0 && L0.out.H * 2 == L0.in.H && L0.out.W * 2 == L0.in.W &&
+            L1.kind == L_MAXPOOL && L1.k == 3 && L1.stride == 2 && L1.pad == 1 && L0.cout % 16 == 0) {
+          L0.s4d = 1;
+          L1.pool_s2d = 1;
+          g->stem_s4d = 1;
+        }
+      }
+    }
   }
   // ---- weights -> HBM (snapshot), workspace for max_batch
   for (size_t i = 0; i < g->subnets.size(); ++i)
@@ -958,6 +1034,13 @@ dycl_status dycl_finalize(dycl_graph g, int64_t max_batch) {
   if (dycl_status s = dmalloc(g, &g->d_flag, nb)) return s;
   if (dycl_status s = dmalloc(g, &g->d_pred, nb * 4)) return s;
   if (dycl_status s = dmalloc(g, &g->d_z, nb * (size_t)std::max(g->K, 1) * 4)) return s;
+  {
+    int cmax = 0;
+    for (const Node& N : g->nodes)
+      if (N.kind != N_SEQ && g->subnets[N.sn].layers.back().d_wt) cmax = std::max(cmax, g->subnets[N.sn].in.Cp());
+    if (cmax > 0)
+      if (dycl_status s = dmalloc(g, &g->d_gpool, nb * (size_t)cmax * 4)) return s;
+  }
   g->finalized = true;
   return DYCL_OK;
 }

@@ -38,9 +38,19 @@ struct CG {
   static constexpr int A_BYTES = BM * BKE * 2;
   static constexpr int B_BYTES = BN * BKE * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;
-  static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+};
+constexpr int MAX_STAGES = 8;
+constexpr int SMEM_LIMIT = 227 * 1024;
+constexpr int SMEM_MISC = 1024 + 512;        // alignment slack + barriers
+// TMA-staged epilogue, per warpgroup: residual chunk (128 rows x 32 fp32, SW128), fp32 output
+// chunk (SW128) and bf16 output chunk (128 rows x 32 bf16 = 64 B, SW64).
+constexpr int EPI_RES = BM * 32 * 4, EPI_O32 = BM * 32 * 4, EPI_O16 = BM * 32 * 2;
+constexpr int EPI_WG = EPI_RES + EPI_O32 + EPI_O16;
+
+struct GemmPlan {
+  int stages;      // mainloop ring depth
+  int staged;      // 1: epilogue through SMEM + TMA stores (and TMA residual loads)
 };
 
 __device__ __forceinline__ void tma_im2col_4d(uint32_t dst, const void* tmap, uint32_t bar, int c, int w, int h, int n,
@@ -56,22 +66,31 @@ __device__ __forceinline__ uint32_t pk2(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
 }
+__device__ __forceinline__ void wg_sync(int wg) { asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory"); }
+// 16-byte chunk j of row r in a 1024-B-aligned buffer with 128-byte rows, 128B swizzle
+__device__ __forceinline__ uint32_t sw128(int r, int j) { return (uint32_t)(r * 128 + ((j ^ (r & 7)) << 4)); }
+// 16-byte chunk j of row r with 64-byte rows, 64B swizzle (chunk bits XOR address bits [7,9))
+__device__ __forceinline__ uint32_t sw64(int r, int j) { return (uint32_t)(r * 64 + ((j ^ ((r >> 1) & 3)) << 4)); }
 
 template <int BN, bool IM2COL>
 __global__ void __launch_bounds__(THREADS, 1)
-    k_conv_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const ConvArgs a) {
+    k_conv_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmY32,
+                const __grid_constant__ CUtensorMap tmY16, const ConvArgs a, const GemmPlan pl) {
   using G = CG<BN>;
-  constexpr int S = G::STAGES;
+  const int S = pl.stages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * G::A_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + S * G::B_BYTES);
+  uint8_t* sE = sB + S * G::B_BYTES;                       // [2 WG][res | o32 | o16] when staged
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sE + (pl.staged ? 2 * EPI_WG : 0));
   const uint32_t full0 = ptx::smem_u32(bars);
   const uint32_t empty0 = full0 + 8 * S;
   const uint32_t tfull0 = empty0 + 8 * S;
   const uint32_t tempty0 = tfull0 + 16;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
+  const uint32_t rbar0 = tempty0 + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 6);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_live = a.n_live ? *a.n_live : a.n_static;
@@ -91,6 +110,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(tfull0 + 8 * i, 1);
       ptx::mbar_init(tempty0 + 8 * i, 128);
+      ptx::mbar_init(rbar0 + 8 * i, 1);
     }
     ptx::fence_mbar_init();
   }
@@ -167,20 +187,39 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ------------------------------------------------------------ epilogue (2 warpgroups)
     const int wg = warp >> 2, quad = warp & 3;
     const int r = quad * 32 + lane;                         // TMEM lane = row of the tile
+    const bool leader = (threadIdx.x & 127) == 0;
     const bool res = a.res_mode == 1;
     const bool res_f = res && a.res32 != nullptr;
+    const bool staged = pl.staged != 0;
+    uint8_t* eR = sE + wg * EPI_WG;
+    uint8_t* eO32 = eR + EPI_RES;
+    uint8_t* eO16 = eO32 + EPI_O32;
+    const uint32_t rbar = rbar0 + 8 * wg;
+    uint32_t rphase = 0;
+    if (staged && leader) {
+      if (res) ptx::tma_prefetch_desc(&tmR);
+      if (a.y32) ptx::tma_prefetch_desc(&tmY32);
+      if (a.y) ptx::tma_prefetch_desc(&tmY16);
+    }
     int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       if ((it & 1) != wg) continue;
       const int acc = it & 1;
       const int m_tile = tile / n_tiles, n_tile = tile - m_tile * n_tiles;
-      const long long m = (long long)m_tile * BM + r;
+      const long long m0 = (long long)m_tile * BM;
+      const long long m = m0 + r;
       const bool ok = m < M;
+      const bool full = m0 + BM <= M;
       const int col0 = n_tile * BN;
       const size_t rowo = (size_t)(ok ? m : 0) * a.Cout + col0;
-      // shortcut chunk (32 channels) prefetch: issued before the accumulator wait
+      auto res_load = [&](int c0) {
+        ptx::mbar_arrive_expect_tx(rbar, res_f ? EPI_RES : EPI_RES / 2);
+        ptx::tma_load_2d(ptx::smem_u32(eR), &tmR, rbar, col0 + c0, (int)m0);
+      };
+      if (staged && res && leader) res_load(0);
+      // unstaged shortcut chunk (32 channels) prefetch, issued before the accumulator wait
       float4 rs[8];
-      auto load_res = [&](int c0) {
+      auto load_res_g = [&](int c0) {
         if (res_f) {
           const float4* q = reinterpret_cast<const float4*>(a.res32 + rowo + c0);
 #pragma unroll
@@ -197,7 +236,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
       };
-      if (res) load_res(0);
+      if (!staged && res) load_res_g(0);
       ptx::mbar_wait(tfull0 + 8 * acc, (it >> 1) & 1);
       ptx::tc_fence_after();
       const uint32_t t_base = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN);
@@ -210,17 +249,65 @@ __global__ void __launch_bounds__(THREADS, 1)
         float f[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]) + __ldg(a.bias + col0 + c0 + j);
-        if (res) {
+        if (staged && res) {
+          ptx::mbar_wait(rbar, rphase);
+          rphase ^= 1;
+          if (res_f) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 q = *reinterpret_cast<const float4*>(eR + sw128(r, j));
+              f[4 * j] += q.x; f[4 * j + 1] += q.y; f[4 * j + 2] += q.z; f[4 * j + 3] += q.w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint4 u = *reinterpret_cast<const uint4*>(eR + sw64(r, j));
+              const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                f[8 * j + 2 * q] += __uint_as_float(w4[q] << 16);
+                f[8 * j + 2 * q + 1] += __uint_as_float(w4[q] & 0xFFFF0000u);
+              }
+            }
+          }
+        } else if (res) {
           const float* rf = reinterpret_cast<const float*>(rs);
 #pragma unroll
           for (int j = 0; j < 32; ++j) f[j] += rf[j];
-          if (c0 + 32 < BN) load_res(c0 + 32);              // next chunk's shortcut in flight
+          if (c0 + 32 < BN) load_res_g(c0 + 32);            // next chunk's shortcut in flight
         }
         if (a.relu) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) f[j] = fmaxf(f[j], 0.0f);
         }
-        if (ok) {
+        if (staged) {
+          // all rows consumed the residual buffer; the previous chunk's stores have read the
+          // output staging: refill the one, rewrite the other
+          if (leader) ptx::bulk_wait_read0();
+          wg_sync(wg);
+          if (res && leader && c0 + 32 < BN) res_load(c0 + 32);
+        }
+        if (staged && full) {
+          if (a.y32) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<float4*>(eO32 + sw128(r, j)) = make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
+          }
+          if (a.y) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              *reinterpret_cast<uint4*>(eO16 + sw64(r, j)) =
+                  make_uint4(pk2(f[8 * j], f[8 * j + 1]), pk2(f[8 * j + 2], f[8 * j + 3]),
+                             pk2(f[8 * j + 4], f[8 * j + 5]), pk2(f[8 * j + 6], f[8 * j + 7]));
+          }
+          ptx::fence_proxy_async_smem();
+          wg_sync(wg);
+          if (leader) {
+            if (a.y32) ptx::tma_store_2d(&tmY32, ptx::smem_u32(eO32), col0 + c0, (int)m0);
+            if (a.y) ptx::tma_store_2d(&tmY16, ptx::smem_u32(eO16), col0 + c0, (int)m0);
+            ptx::bulk_commit();
+          }
+        } else if (ok) {
           if (a.y) {
             uint4* yq = reinterpret_cast<uint4*>(a.y + rowo + c0);
 #pragma unroll
@@ -238,6 +325,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       ptx::tc_fence_before();
       ptx::mbar_arrive(tempty0 + 8 * acc);
     }
+    if (staged && leader) ptx::bulk_wait0();                 // stores done reading SMEM before exit
   }
   __syncthreads();
   if (warp == 9) {
@@ -269,8 +357,9 @@ cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t 
   static EncodeTiledFn enc = driver_fn<EncodeTiledFn>("cuTensorMapEncodeTiled");
   static EncodeIm2colFn enc_i2c = driver_fn<EncodeIm2colFn>("cuTensorMapEncodeIm2col");
   if (!enc || !enc_i2c) return cudaErrorNotSupported;
-  CUtensorMap tmA, tmB;
+  CUtensorMap tmA, tmB, tmR, tmY32, tmY16;
   const int rows = max_rows > 0 ? max_rows : 1;
+  const cuuint64_t Mmax = (cuuint64_t)rows * a.Ho * a.Wo;
   if (IM2COL) {
     cuuint64_t dims[4] = {(cuuint64_t)a.C, (cuuint64_t)a.W, (cuuint64_t)a.H, (cuuint64_t)rows};
     cuuint64_t strides[3] = {(cuuint64_t)a.C * 2, (cuuint64_t)a.W * a.C * 2, (cuuint64_t)a.H * a.W * a.C * 2};
@@ -292,27 +381,56 @@ cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t 
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  {
-    cuuint64_t dims[2] = {(cuuint64_t)a.Kp, (cuuint64_t)a.Cout};
-    cuuint64_t strides[1] = {(cuuint64_t)a.Kp * 2};
-    cuuint32_t box[2] = {BKE, BN};
+  auto mat2d = [&](CUtensorMap* t, const void* p, CUtensorMapDataType dt, int esz, cuuint64_t inner, cuuint64_t outer,
+                   cuuint32_t bi, cuuint32_t bo, CUtensorMapSwizzle sw) {
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {inner * (cuuint64_t)esz};
+    cuuint32_t box[2] = {bi, bo};
     cuuint32_t es[2] = {1, 1};
-    if (enc(&tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)a.w, dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return enc(t, dt, 2, (void*)p, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  if (!mat2d(&tmB, a.w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.Kp, a.Cout, BKE, BN, CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  // epilogue plan: SMEM-staged TMA stores when the epilogue moves more than a bf16 tile
+  // (fp32 stream copy and / or a shortcut) and the ring keeps >= 2 stages beside the staging
+  GemmPlan pl{};
+  const int kblocks = a.ksz * a.ksz * (a.C / BKE);
+  const bool heavy = a.y32 != nullptr || a.res_mode == 1;
+  const int avail_staged = SMEM_LIMIT - SMEM_MISC - 2 * EPI_WG;
+  pl.staged = heavy && avail_staged / CG<BN>::STAGE >= 2 && !(a.dbg & 128);
+  const int avail = pl.staged ? avail_staged : SMEM_LIMIT - SMEM_MISC;
+  pl.stages = avail / CG<BN>::STAGE;
+  if (pl.stages > MAX_STAGES) pl.stages = MAX_STAGES;
+  if (pl.stages > kblocks + 1 && kblocks >= 1) pl.stages = kblocks + 1 > 2 ? kblocks + 1 : 2;
+  tmR = tmY32 = tmY16 = tmB;
+  if (pl.staged) {
+    if (a.res_mode == 1) {
+      const bool f32 = a.res32 != nullptr;
+      if (!mat2d(&tmR, f32 ? (const void*)a.res32 : (const void*)a.res,
+                 f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, f32 ? 4 : 2, a.Cout, Mmax,
+                 32, BM, f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B))
+        return cudaErrorInvalidValue;
+    }
+    if (a.y32 && !mat2d(&tmY32, a.y32, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.Cout, Mmax, 32, BM,
+                        CU_TENSOR_MAP_SWIZZLE_128B))
+      return cudaErrorInvalidValue;
+    if (a.y && !mat2d(&tmY16, a.y, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.Cout, Mmax, 32, BM,
+                      CU_TENSOR_MAP_SWIZZLE_64B))
       return cudaErrorInvalidValue;
   }
+  const int smem = SMEM_MISC + pl.stages * CG<BN>::STAGE + (pl.staged ? 2 * EPI_WG : 0);
   static bool attr = false;
   if (!attr) {
-    cudaError_t e =
-        cudaFuncSetAttribute(k_conv_gemm<BN, IM2COL>, cudaFuncAttributeMaxDynamicSharedMemorySize, CG<BN>::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(k_conv_gemm<BN, IM2COL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         SMEM_LIMIT);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const long long tiles = ((long long)rows * a.Ho * a.Wo + BM - 1) / BM * (a.Cout / BN);
+  const long long tiles = ((long long)Mmax + BM - 1) / BM * (a.Cout / BN);
   int grid = (int)(tiles < num_sms ? tiles : num_sms);
   if (grid < 1) grid = 1;
-  k_conv_gemm<BN, IM2COL><<<grid, THREADS, CG<BN>::SMEM, stream>>>(tmA, tmB, a);
+  k_conv_gemm<BN, IM2COL><<<grid, THREADS, smem, stream>>>(tmA, tmB, tmR, tmY32, tmY16, a, pl);
   return cudaGetLastError();
 }
 

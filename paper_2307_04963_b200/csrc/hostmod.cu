@@ -99,8 +99,10 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head(const HeadArgs a) {
       float s = 0.0f;
       for (int q = 0; q < P; ++q) s += part[(q * G + grp) * 8 + j];
       g[c] = s / (float)a.HW;
+      if (a.wt) a.gpool[(size_t)row * a.C + c] = g[c];
     }
     __syncthreads();
+    if (a.wt) continue;                            // wide head: FC + predicate in k_head_fc
     // FC: one warp per output row, lanes over channels, fixed shuffle tree.
     const int warp = t >> 5, lane = t & 31;
     for (int j = warp; j < a.K; j += HEAD_THREADS / 32) {
@@ -148,6 +150,78 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head(const HeadArgs a) {
       }
     }
     __syncthreads();
+  }
+}
+
+// Wide heads (K = 1000): logits for FC_ROWS samples x 256 classes per CTA from the pooled
+// features, so the [C][K] weights stream once per FC_ROWS samples (the per-sample form re-read
+// 4 MB of weights per ResNet-50 sample).  Thread = one class; the pooled rows sit in SMEM as
+// [C][FC_ROWS] (two LDS.128 per c, broadcast); the sum over c runs in order, fp32.
+constexpr int FC_ROWS = 8;
+constexpr int FC_UNROLL = 8;
+
+__global__ void __launch_bounds__(HEAD_THREADS) k_head_fc(const HeadArgs a) {
+  extern __shared__ float gs[];                    // [C][FC_ROWS]
+  const int n_live = *a.n_live;
+  const int t = threadIdx.x;
+  const int j = blockIdx.y * HEAD_THREADS + t;     // class
+  for (int r0 = blockIdx.x * FC_ROWS; r0 < n_live; r0 += gridDim.x * FC_ROWS) {
+    const int nr = min(FC_ROWS, n_live - r0);
+    for (int i = t; i < FC_ROWS * a.C; i += HEAD_THREADS) {
+      const int r = i / a.C, c = i - r * a.C;
+      gs[c * FC_ROWS + r] = r < nr ? a.gpool[(size_t)(r0 + r) * a.C + c] : 0.0f;
+    }
+    __syncthreads();
+    float acc[FC_ROWS];
+#pragma unroll
+    for (int r = 0; r < FC_ROWS; ++r) acc[r] = 0.0f;
+    if (j < a.K) {
+      const uint16_t* wj = a.wt + j;
+      for (int c0 = 0; c0 < a.C; c0 += FC_UNROLL) {
+        float w[FC_UNROLL];
+#pragma unroll
+        for (int u = 0; u < FC_UNROLL; ++u) w[u] = bf16f(__ldg(wj + (size_t)(c0 + u) * a.K));
+#pragma unroll
+        for (int u = 0; u < FC_UNROLL; ++u) {
+          const float4 g0 = *reinterpret_cast<const float4*>(gs + (c0 + u) * FC_ROWS);
+          const float4 g1 = *reinterpret_cast<const float4*>(gs + (c0 + u) * FC_ROWS + 4);
+          acc[0] = fmaf(w[u], g0.x, acc[0]); acc[1] = fmaf(w[u], g0.y, acc[1]);
+          acc[2] = fmaf(w[u], g0.z, acc[2]); acc[3] = fmaf(w[u], g0.w, acc[3]);
+          acc[4] = fmaf(w[u], g1.x, acc[4]); acc[5] = fmaf(w[u], g1.y, acc[5]);
+          acc[6] = fmaf(w[u], g1.z, acc[6]); acc[7] = fmaf(w[u], g1.w, acc[7]);
+        }
+      }
+      const float bj = a.b[j];
+      for (int r = 0; r < nr; ++r) a.z[(size_t)(r0 + r) * a.K + j] = acc[r] + bj;
+    }
+    __syncthreads();
+  }
+}
+
+// Predicate of a wide head: one warp per live row over the logits in a.z (fixed-order reductions).
+__global__ void k_head_pred(const HeadArgs a) {
+  const int n_live = *a.n_live;
+  const int lane = threadIdx.x & 31;
+  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < n_live; row += (gridDim.x * blockDim.x) >> 5) {
+    const float* z = a.z + (size_t)row * a.K;
+    float m = -INFINITY;
+    for (int j = lane; j < a.K; j += 32) m = fmaxf(m, z[j]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float sum = 0.0f;
+    for (int j = lane; j < a.K; j += 32) sum += expf(z[j] - m);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) {
+      if (a.kind == 0) {
+        const float conf = 1.0f / sum;             // max_j softmax(z)_j
+        a.flag[row] = conf >= a.thr ? 1 : 0;       // reading R1: conf >= tau exits
+        if (a.pred) a.pred[row] = conf;
+      } else {
+        a.flag[row] = 1;                           // final head
+        if (a.pred) a.pred[row] = 1.0f;
+      }
+    }
   }
 }
 
@@ -355,9 +429,121 @@ __global__ void k_maxpool(const PoolArgs a) {
   }
 }
 
+// 3x3 / stride-2 / pad-1 max pool over the space-to-depth stem output: input [n][Ho][Wo][4C],
+// channel (b*2+b')*C + c holds pixel (2P+b, 2Q+b'); output pixel (P, Q) takes the max over
+// rows 2P-1..2P+1 x cols 2Q-1..2Q+1 = its own 4 phases, phases b = 1 of block P-1, b' = 1 of
+// block Q-1 and phase (1,1) of block (P-1, Q-1).  One thread per (sample, pixel, 8-channel group).
+__global__ void k_maxpool_s2d(const PoolArgs a) {
+  const int n_live = *a.n_live;
+  const int G = a.C / 8, C4 = 4 * a.C;
+  const int HWo = a.Ho * a.Wo;
+  const int64_t total = (int64_t)n_live * HWo * G;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total; u += (int64_t)gridDim.x * blockDim.x) {
+    const int g = (int)(u % G);
+    const int64_t t = u / G;
+    const int p = (int)(t % HWo);
+    const int64_t n = t / HWo;
+    const int P = p / a.Wo, Q = p - (p / a.Wo) * a.Wo;
+    float m[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) m[j] = -INFINITY;
+    auto take = [&](int pp, int qq, int ph) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.x + ((n * a.Ho + pp) * a.Wo + qq) * C4 + ph * a.C + g * 8));
+      const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        m[2 * j] = fmaxf(m[2 * j], __uint_as_float(w4[j] << 16));
+        m[2 * j + 1] = fmaxf(m[2 * j + 1], __uint_as_float(w4[j] & 0xFFFF0000u));
+      }
+    };
+#pragma unroll
+    for (int ph = 0; ph < 4; ++ph) take(P, Q, ph);
+    if (P > 0) { take(P - 1, Q, 2); take(P - 1, Q, 3); }
+    if (Q > 0) { take(P, Q - 1, 1); take(P, Q - 1, 3); }
+    if (P > 0 && Q > 0) take(P - 1, Q - 1, 3);
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      __nv_bfloat162 v = __floats2bfloat162_rn(m[2 * j], m[2 * j + 1]);
+      o[j] = *reinterpret_cast<uint32_t*>(&v);
+    }
+    *reinterpret_cast<uint4*>(a.y + (n * HWo + p) * a.C + g * 8) = make_uint4(o[0], o[1], o[2], o[3]);
+    if (a.y32) {
+      float4* q = reinterpret_cast<float4*>(a.y32 + (n * HWo + p) * a.C + g * 8);
+      q[0] = make_float4(m[0], m[1], m[2], m[3]);
+      q[1] = make_float4(m[4], m[5], m[6], m[7]);
+    }
+  }
+}
+
+// fp32 NHWC [n][H][W][c] -> bf16 4x4 space-to-depth [n][H/4][W/4][64]; one thread per output
+// pixel: the 4 input rows of its block are 4 contiguous runs of 4*c floats (c == 3: 3 float4
+// each; lanes = consecutive blocks, so a warp reads contiguous 1.5 KB rows), 128 B out.
+__global__ void k_cast_s4d(const float* __restrict__ in, uint16_t* __restrict__ out, int64_t total, int H, int W,
+                           int c, int vec) {
+  const int Wb = W / 4, Hb = H / 4;
+  for (int64_t pix = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pix < total;
+       pix += (int64_t)gridDim.x * blockDim.x) {
+    const int Q = (int)(pix % Wb);
+    const int64_t t = pix / Wb;
+    const int P = (int)(t % Hb);
+    const int64_t n = t / Hb;
+    float v[64];
+#pragma unroll
+    for (int k = 0; k < 64; ++k) v[k] = 0.0f;
+    if (vec) {
+#pragma unroll
+      for (int pr = 0; pr < 4; ++pr) {
+        const float4* src = reinterpret_cast<const float4*>(in + ((n * H + 4 * P + pr) * (int64_t)W + 4 * Q) * 3);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const float4 f = __ldg(src + q);
+          v[pr * 12 + 4 * q] = f.x; v[pr * 12 + 4 * q + 1] = f.y; v[pr * 12 + 4 * q + 2] = f.z; v[pr * 12 + 4 * q + 3] = f.w;
+        }
+      }
+    } else {
+      for (int ch = 0; ch < 16 * c; ++ch) {
+        const int ph = ch / c, ci = ch - ph * c;
+        v[ch] = __ldg(in + ((n * H + 4 * P + (ph >> 2)) * (int64_t)W + 4 * Q + (ph & 3)) * c + ci);
+      }
+    }
+    uint4* dst = reinterpret_cast<uint4*>(out + pix * 64);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t o[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        __nv_bfloat162 b = __floats2bfloat162_rn(v[8 * j + 2 * k], v[8 * j + 2 * k + 1]);
+        o[k] = *reinterpret_cast<uint32_t*>(&b);
+      }
+      dst[j] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
 }  // namespace
 
+cudaError_t launch_cast_s4d(const float* in, uint16_t* out, int64_t n, int H, int W, int c, cudaStream_t s) {
+  if (H % 4 || W % 4 || c > 4) return cudaErrorInvalidValue;
+  const int64_t total = n * (H / 4) * (W / 4);
+  if (total == 0) return cudaSuccess;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  const int vec = c == 3 && ((uintptr_t)in & 15) == 0;
+  k_cast_s4d<<<(int)blocks, 256, 0, s>>>(in, out, total, H, W, c, vec);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_maxpool(const PoolArgs& a, int max_rows, int num_sms, cudaStream_t s) {
+  if (a.s2d) {
+    if (!a.nhwc || a.k != 3 || a.stride != 2 || a.pad != 1) return cudaErrorInvalidValue;
+    const int64_t total = (int64_t)max_rows * (a.C / 8) * a.Ho * a.Wo;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > (int64_t)num_sms * 16) blocks = (int64_t)num_sms * 16;
+    if (blocks < 1) blocks = 1;
+    k_maxpool_s2d<<<(int)blocks, 256, 0, s>>>(a);
+    return cudaGetLastError();
+  }
   const int64_t total = (int64_t)max_rows * (a.C / 8) * a.Ho * a.Wo;
   int64_t blocks = (total + 255) / 256;
   if (blocks > (int64_t)num_sms * 16) blocks = (int64_t)num_sms * 16;
@@ -393,6 +579,24 @@ cudaError_t launch_head(const HeadArgs& a, int max_rows, cudaStream_t s) {
   int grid = max_rows < 148 * 8 ? max_rows : 148 * 8;
   if (grid < 1) grid = 1;
   k_head<<<grid, HEAD_THREADS, smem, s>>>(a);
+  if (!a.wt) return cudaGetLastError();
+  if (a.kind == 1 || !a.gpool) return cudaErrorInvalidValue;
+  const size_t smem_fc = (size_t)FC_ROWS * a.C * sizeof(float);
+  static size_t attr_fc = 0;
+  if (smem_fc > 48 * 1024 && smem_fc > attr_fc) {
+    cudaError_t e = cudaFuncSetAttribute(k_head_fc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fc);
+    if (e != cudaSuccess) return e;
+    attr_fc = smem_fc;
+  }
+  if (a.C % FC_UNROLL) return cudaErrorInvalidValue;
+  int gx = (max_rows + FC_ROWS - 1) / FC_ROWS;
+  if (gx > 148 * 2) gx = 148 * 2;
+  if (gx < 1) gx = 1;
+  k_head_fc<<<dim3(gx, (a.K + HEAD_THREADS - 1) / HEAD_THREADS), HEAD_THREADS, smem_fc, s>>>(a);
+  int gp = (max_rows + 7) / 8;
+  if (gp > 148 * 8) gp = 148 * 8;
+  if (gp < 1) gp = 1;
+  k_head_pred<<<gp, 256, 0, s>>>(a);
   return cudaGetLastError();
 }
 

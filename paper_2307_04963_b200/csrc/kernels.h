@@ -62,6 +62,10 @@ cudaError_t launch_conv(const ConvArgs& a, int max_rows, int num_sms, cudaStream
 cudaError_t launch_cast_pad(const float* in, uint16_t* out, int64_t n, int hw, int c, int cp,
                             cudaStream_t s);
 
+// a0 for a space-to-depth stem: fp32 NHWC [n][H][W][c] -> bf16 [n][H/4][W/4][64], channel
+// (pr*4 + ps)*c + ci = input pixel (4P+pr, 4Q+ps) channel ci; channels >= 16c zero (c <= 4).
+cudaError_t launch_cast_s4d(const float* in, uint16_t* out, int64_t n, int H, int W, int c, cudaStream_t s);
+
 // Run-start init: counts[0] = n ; orig[i] = i ; path[i] = 0.
 cudaError_t launch_init(int* counts, int n, int* orig, int32_t* path, int nmax, cudaStream_t s);
 
@@ -79,6 +83,9 @@ struct HeadArgs {
   int HW, C, K, kind;
   float thr;
   int nhwc = 0;          // bf16 h is NHWC [n][HW][C] (else channel-planar)
+  // wide heads (K >= 128): FC batched over FC_ROWS samples per CTA from the transposed weights
+  const uint16_t* wt = nullptr;   // bf16 [C][K] (nullptr: per-sample FC inside the GAP kernel)
+  float* gpool = nullptr;         // fp32 [rows][C] pooled-feature scratch for the batched FC
 };
 cudaError_t launch_head(const HeadArgs& a, int max_rows, cudaStream_t s);
 
@@ -125,6 +132,8 @@ struct PoolArgs {
   const int* n_live;
   int H, W, C, Ho, Wo, k, stride, pad;
   int nhwc = 0;          // bf16 x / y are NHWC (else channel-planar)
+  int s2d = 0;           // 3x3/2/1 pool over a 2x2-phase input [n][Ho][Wo][4C] (channel (b*2+b')*C + c
+                         // = pixel (2ho+b, 2wo+b')); output NHWC [n][Ho][Wo][C]
 };
 cudaError_t launch_maxpool(const PoolArgs& a, int max_rows, int num_sms, cudaStream_t s);
 
