@@ -53,6 +53,11 @@ struct Layer {
   int s4d = 0;
   int pool_s2d = 0;           // maxpool reading that phase layout (3x3 / stride 2 / pad 1)
   uint16_t* d_wt = nullptr;   // wide fp32 heads (K >= 128): weights transposed [C][K] for the batched FC
+  // NHWC bottleneck: this 1x1 conv and the projection shortcut before it run as ONE GEMM over
+  // K-concatenated operands [t | x] with weights [W | W_proj] and bias b + b_proj
+  int fuse_proj = 0;
+  uint16_t* d_wcat = nullptr;
+  float* d_bcat = nullptr;
 };
 
 struct Subnet {
@@ -61,6 +66,7 @@ struct Subnet {
   bool is_head = false;       // [GAP] + dense(out_fp32)
   Shape in, out;
   int head_K = 0;
+  bool needs_in32 = true;     // reads its input's fp32 residual-stream copy (set at finalize)
 };
 
 enum NodeKind { N_SEQ, N_EXIT, N_GATE, N_FINAL };
@@ -256,7 +262,26 @@ dycl_status plan_subnet(dycl_graph g, Subnet& s, const Shape& in, int sn_id) {
 }
 
 dycl_status upload_subnet(dycl_graph g, Subnet& s) {
-  for (Layer& L : s.layers) {
+  for (size_t li = 0; li < s.layers.size(); ++li) {
+    Layer& L = s.layers[li];
+    if (g->nhwc && L.kind == L_CONV && li > 0 && s.layers[li - 1].kind == L_PROJ && L.k == 1 && L.stride == 1 &&
+        L.res_mode == 1 && L.in.C % 64 == 0 && s.layers[li - 1].in.C % 64 == 0 && !getenv("DYCL_NO_FUSE_PROJ")) {
+      const Layer& Pj = s.layers[li - 1];
+      const int K1 = L.in.C, K2 = Pj.in.C, co = L.cout;
+      std::vector<uint16_t> wc((size_t)co * (K1 + K2));
+      std::vector<float> bc(co);
+      for (int o = 0; o < co; ++o) {
+        for (int c = 0; c < K1; ++c) wc[(size_t)o * (K1 + K2) + c] = L.w[(size_t)o * K1 + c];
+        for (int c = 0; c < K2; ++c) wc[(size_t)o * (K1 + K2) + K1 + c] = Pj.w[(size_t)o * K2 + c];
+        bc[o] = L.b[o] + Pj.b[o];
+      }
+      dycl_status st = dmalloc(g, &L.d_wcat, wc.size() * 2);
+      if (st) return st;
+      CK(cudaMemcpy(L.d_wcat, wc.data(), wc.size() * 2, cudaMemcpyHostToDevice));
+      if ((st = dmalloc(g, &L.d_bcat, bc.size() * 4))) return st;
+      CK(cudaMemcpy(L.d_bcat, bc.data(), bc.size() * 4, cudaMemcpyHostToDevice));
+      L.fuse_proj = 1;
+    }
     if (L.kind == L_CONV && L.s4d) {
       // W'[(b*2+b')*cout + o][(R*3+S)*64 + (pr*4+ps)*Cin + c] = w[o][r][s][c] with
       // r = 4(R-1) + pr - 2b + pad, s = 4(S-1) + ps - 2b' + pad (zero outside the 7x7 window):
@@ -401,7 +426,7 @@ struct Exec {
   // Run subnet s on the rows of `in` (device count `cnt`).  The last layer writes
   // into `out_hint` when given (b >= 0).  `busy` is an outer tensor to preserve.
   dycl_status subnet(const Subnet& s, Tensor in, const int* cnt, Tensor out_hint, Tensor busy, Tensor* out) {
-    Tensor cur = in, shortcut;
+    Tensor cur = in, shortcut, proj_src;
     for (size_t li = 0; li < s.layers.size(); ++li) {
       const Layer& L = s.layers[li];
       if (L.kind == L_BLOCK && fp32_stream() && !g->no_fuse && cur.f >= 0 && fusable(s, li)) {
@@ -461,6 +486,10 @@ struct Exec {
         cur = o;
         continue;
       }
+      if (L.kind == L_PROJ && li + 1 < s.layers.size() && s.layers[li + 1].fuse_proj) {
+        proj_src = shortcut;           // consumed by the next conv's fused GEMM
+        continue;
+      }
       if (L.kind == L_PROJ) {
         // shortcut <- conv1x1/stride(shortcut): a residual-stream tensor
         Tensor o = pick_tensor(fp32_stream(), {cur, shortcut, busy, out_hint});
@@ -513,6 +542,20 @@ struct Exec {
       a.rH = L.res_shape.H; a.rW = L.res_shape.W; a.rC = L.res_shape.Cp();
       a.r_pad_lo = (L.out.C - L.res_shape.C) / 2;
       a.nhwc = g->nhwc;
+      double fused_b = 0.0, fused_f = 0.0;
+      if (L.fuse_proj) {               // [t | x] x [W | W_proj]: no projection tensor, no shortcut read
+        const Layer& Pj = s.layers[li - 1];
+        a.x2 = g->buf[proj_src.b];
+        a.C2 = Pj.in.C; a.H2 = Pj.in.H; a.W2 = Pj.in.W; a.stride2 = Pj.stride;
+        a.K = a.Kp = L.in.C + Pj.in.C;
+        a.w = L.d_wcat;
+        a.bias = L.d_bcat;
+        a.res_mode = 0;
+        a.res = nullptr;
+        a.res32 = nullptr;
+        fused_b = 2.0 * L.out.H * L.out.W * Pj.in.C;   // the strided pixels of x the GEMM reads
+        fused_f = 2.0 * L.out.H * L.out.W * L.out.C * (double)Pj.in.C;
+      }
       if (L.s4d) {                     // 3x3 / stride 1 over 4x4 blocks, 2x2 output phases in N
         a.H = L.in.H / 4; a.W = L.in.W / 4; a.C = 64;
         a.Ho = L.out.H / 2; a.Wo = L.out.W / 2; a.Cout = 4 * L.out.C;
@@ -521,10 +564,10 @@ struct Exec {
         a.w_rt = nullptr;
       }
       a.dbg = g->conv_dbg;
-      const double res_b = L.res_mode ? (a.res32 ? 4.0 : 2.0) * L.res_shape.row_elems() *
-                                            (L.res_mode == 2 ? 0.25 : 1.0) : 0.0;
-      const double row_b = 2.0 * L.in.row_elems() + (o.f >= 0 ? 6.0 : 2.0) * L.out.row_elems() + res_b;
-      const double row_f = 2.0 * L.out.H * L.out.W * L.out.C * (double)(L.k * L.k * L.in.C);
+      const double res_b = a.res_mode ? (a.res32 ? 4.0 : 2.0) * L.res_shape.row_elems() *
+                                            (a.res_mode == 2 ? 0.25 : 1.0) : 0.0;
+      const double row_b = 2.0 * L.in.row_elems() + (o.f >= 0 ? 6.0 : 2.0) * L.out.row_elems() + res_b + fused_b;
+      const double row_f = 2.0 * L.out.H * L.out.W * L.out.C * (double)(L.k * L.k * L.in.C) + fused_f;
       prof_begin(DYCL_K_CONV, cnt, row_b, row_f, 2.0 * L.out.C * L.Kp);
       cudaError_t e = dycl::launch_conv(a, batch, g->num_sms, st, g->conv_path);
       prof_end();
@@ -631,7 +674,8 @@ struct Exec {
     cur.b = 0;
     const int* cnt = g->d_counts;
     const Tensor none;
-    for (const Node& N : g->nodes) {
+    for (size_t ni = 0; ni < g->nodes.size(); ++ni) {
+      const Node& N = g->nodes[ni];
       switch (N.kind) {
         case N_SEQ: {
           Tensor o;
@@ -644,8 +688,15 @@ struct Exec {
           int s;
           if ((r = compact(cnt, 0, 0, orig_cur, &s))) return r;
           if ((r = scatter(g->d_list1, g->d_counts + s, orig_cur, N.ordinal))) return r;
-          const Tensor nb = pick_tensor(cur.f >= 0, {cur});
-          if ((r = gather(cur, nb, g->d_list0, g->d_counts + s + 1, nullptr, N.in, 0))) return r;
+          // survivors move on; their fp32 stream copy only if the next reader uses it (a
+          // ResNet-50 stage starts with a projection block: its input is read as bf16 only)
+          const bool next_seq = ni + 1 < g->nodes.size() && g->nodes[ni + 1].kind == N_SEQ;
+          const bool keep32 = cur.f >= 0 && !(next_seq && !g->subnets[g->nodes[ni + 1].sn].needs_in32);
+          Tensor src = cur;
+          if (!keep32) src.f = -1;
+          Tensor nb = pick_tensor(keep32, {cur});
+          if (!keep32) nb.f = -1;
+          if ((r = gather(src, nb, g->d_list0, g->d_counts + s + 1, nullptr, N.in, 0))) return r;
           cur = nb;
           cnt = g->d_counts + s + 1;
           orig_cur ^= 1;
@@ -738,6 +789,8 @@ dycl_status dycl_graph_destroy(dycl_graph g) {
       cudaFree(L.d_w);
       cudaFree(L.d_wrt);
       cudaFree(L.d_wt);
+      cudaFree(L.d_wcat);
+      cudaFree(L.d_bcat);
       cudaFree(L.d_b);
     }
   for (auto* b : g->buf) cudaFree(b);
@@ -1010,6 +1063,24 @@ dycl_status dycl_finalize(dycl_graph g, int64_t max_batch) {
           g->stem_s4d = 1;
         }
       }
+    }
+  }
+  // ---- which subnets read their input's fp32 stream copy: a leading block with an identity
+  // shortcut (conv residual, no projection) or a max pool; conservative otherwise
+  for (Subnet& S : g->subnets) {
+    S.needs_in32 = true;
+    if (S.layers.empty() || S.is_head) continue;
+    const Layer& L0 = S.layers[0];
+    if (L0.kind == L_CONV || L0.kind == L_DENSE) {
+      S.needs_in32 = false;                      // a plain first layer reads the bf16 operand copy
+    } else if (L0.kind == L_BLOCK) {
+      bool proj = false, res = false;
+      for (size_t li = 1; li < S.layers.size() && S.layers[li].kind != L_BLOCK; ++li) {
+        proj = proj || S.layers[li].kind == L_PROJ;
+        res = res || S.layers[li].residual;
+        if (S.layers[li].kind != L_CONV && S.layers[li].kind != L_PROJ) res = true;   // anything else: keep
+      }
+      S.needs_in32 = res && !proj;
     }
   }
   // ---- weights -> HBM (snapshot), workspace for max_batch

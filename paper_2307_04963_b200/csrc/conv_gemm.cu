@@ -76,7 +76,8 @@ template <int BN, bool IM2COL>
 __global__ void __launch_bounds__(THREADS, 1)
     k_conv_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmY32,
-                const __grid_constant__ CUtensorMap tmY16, const ConvArgs a, const GemmPlan pl) {
+                const __grid_constant__ CUtensorMap tmY16, const __grid_constant__ CUtensorMap tmA2, const ConvArgs a,
+                const GemmPlan pl) {
   using G = CG<BN>;
   const int S = pl.stages;
   extern __shared__ uint8_t smem_raw[];
@@ -100,7 +101,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int n_tiles = a.Cout / BN;
   const int num_tiles = m_tiles * n_tiles;
   const int cblocks = a.C / BKE;
-  const int kblocks = a.ksz * a.ksz * cblocks;
+  const int kblocks1 = a.ksz * a.ksz * cblocks;
+  const int kblocks = kblocks1 + (a.x2 ? a.C2 / BKE : 0);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
@@ -125,6 +127,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       ptx::tma_prefetch_desc(&tmA);
       ptx::tma_prefetch_desc(&tmB);
+      if (a.x2) ptx::tma_prefetch_desc(&tmA2);
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -152,6 +155,22 @@ __global__ void __launch_bounds__(THREADS, 1)
                 phase ^= 1;
               }
             }
+        // fused projection shortcut: K blocks of the second operand (1x1, stride2)
+        for (int cb = 0; kb < kblocks; ++cb, ++kb) {
+          ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1);
+          const uint32_t bar = full0 + 8 * stage;
+          ptx::mbar_arrive_expect_tx(bar, (uint32_t)G::STAGE);
+          const uint32_t da = ptx::smem_u32(sA + stage * G::A_BYTES);
+          if (a.stride2 > 1)
+            tma_im2col_4d(da, &tmA2, bar, cb * BKE, wo0 * a.stride2, ho0 * a.stride2, n0, 0, 0);
+          else
+            ptx::tma_load_2d(da, &tmA2, bar, cb * BKE, (int)p0);
+          ptx::tma_load_2d(ptx::smem_u32(sB + stage * G::B_BYTES), &tmB, bar, kb * BKE, n_tile * BN);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
       }
     }
   } else if (warp == 9) {
@@ -392,10 +411,27 @@ cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t 
   };
   if (!mat2d(&tmB, a.w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.Kp, a.Cout, BKE, BN, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
+  CUtensorMap tmA2 = tmB;
+  if (a.x2) {
+    if (a.stride2 > 1) {
+      cuuint64_t dims[4] = {(cuuint64_t)a.C2, (cuuint64_t)a.W2, (cuuint64_t)a.H2, (cuuint64_t)rows};
+      cuuint64_t strides[3] = {(cuuint64_t)a.C2 * 2, (cuuint64_t)a.W2 * a.C2 * 2, (cuuint64_t)a.H2 * a.W2 * a.C2 * 2};
+      int lower[2] = {0, 0};
+      int upper[2] = {(a.Wo - 1) * a.stride2 - (a.W2 - 1), (a.Ho - 1) * a.stride2 - (a.H2 - 1)};
+      cuuint32_t es[4] = {1, (cuuint32_t)a.stride2, (cuuint32_t)a.stride2, 1};
+      if (enc_i2c(&tmA2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)a.x2, dims, strides, lower, upper, BKE, BM, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    } else if (!mat2d(&tmA2, a.x2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.C2, Mmax, BKE, BM,
+                      CU_TENSOR_MAP_SWIZZLE_128B)) {
+      return cudaErrorInvalidValue;
+    }
+  }
   // epilogue plan: SMEM-staged TMA stores when the epilogue moves more than a bf16 tile
   // (fp32 stream copy and / or a shortcut) and the ring keeps >= 2 stages beside the staging
   GemmPlan pl{};
-  const int kblocks = a.ksz * a.ksz * (a.C / BKE);
+  const int kblocks = a.ksz * a.ksz * (a.C / BKE) + (a.x2 ? a.C2 / BKE : 0);
   const bool heavy = a.y32 != nullptr || a.res_mode == 1;
   const int avail_staged = SMEM_LIMIT - SMEM_MISC - 2 * EPI_WG;
   pl.staged = heavy && avail_staged / CG<BN>::STAGE >= 2 && !(a.dbg & 128);
@@ -430,7 +466,7 @@ cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t 
   const long long tiles = ((long long)Mmax + BM - 1) / BM * (a.Cout / BN);
   int grid = (int)(tiles < num_sms ? tiles : num_sms);
   if (grid < 1) grid = 1;
-  k_conv_gemm<BN, IM2COL><<<grid, THREADS, smem, stream>>>(tmA, tmB, tmR, tmY32, tmY16, a, pl);
+  k_conv_gemm<BN, IM2COL><<<grid, THREADS, smem, stream>>>(tmA, tmB, tmR, tmY32, tmY16, tmA2, a, pl);
   return cudaGetLastError();
 }
 
@@ -443,7 +479,11 @@ cudaError_t launch_bn(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t
 }  // namespace
 
 bool conv_gemm_eligible(const ConvArgs& a) {
-  return a.nhwc && a.C % BKE == 0 && a.Cout % 64 == 0 && a.K == a.ksz * a.ksz * a.C && a.Kp == a.K &&
+  const int k2 = a.x2 ? a.C2 : 0;
+  if (a.x2 && (a.C2 % BKE || a.stride2 < 1 || a.stride2 > 8 || (a.H2 - 1) / a.stride2 + 1 != a.Ho ||
+               (a.W2 - 1) / a.stride2 + 1 != a.Wo))
+    return false;
+  return a.nhwc && a.C % BKE == 0 && a.Cout % 64 == 0 && a.K == a.ksz * a.ksz * a.C + k2 && a.Kp == a.K &&
          a.res_mode != 2 && a.pad <= 32 && a.stride <= 8 && (a.ksz > 1 || a.stride > 1 || a.H == a.Ho);
 }
 

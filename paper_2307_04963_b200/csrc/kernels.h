@@ -28,6 +28,10 @@ struct ConvArgs {
   int res_mode;          // 0 none, 1 identity [n][Ho][Wo][Cout], 2 option A from [n][rH][rW][rC]
   int rH, rW, rC, r_pad_lo;
   int nhwc = 0;          // 1: bf16 tensors (x, y, res) are NHWC [n][H][W][C] instead of channel-planar
+  // conv_gemm only: a second A operand concatenated along K (the fused projection shortcut of a
+  // bottleneck block: D = conv1x1(x) + proj1x1/stride2(x2)); w is then [Cout][K + C2]
+  const uint16_t* x2 = nullptr;   // bf16 NHWC [n][H2][W2][C2]
+  int C2 = 0, H2 = 0, W2 = 0, stride2 = 1;
   int dbg = 0;           // bit5 (32): row-tap mode opt-in; experiments only (results invalid): bit0 skip
                          // epilogue math/stores, bit1 skip MMAs, bit2 skip A loads, bit3 no residual prefetch
 };
