@@ -111,6 +111,7 @@ struct dycl_graph_s {
   int nhwc = 0;                      // bf16 activations NHWC (decided at finalize; DYCL_NHWC=0 disables)
   int stem_s4d = 0;                  // input cast to 4x4 space-to-depth for the stem (DYCL_STEM_S4D=0 disables)
   long long* dbg_ts = nullptr;       // DYCL_TS=1: fused-block phase timestamps (development)
+  int dbg_ts_pick = 0;               // DYCL_TS=k > 1: record the k-th fused launch of a run (else the last)
   long long max_row_elems = 0;
   int* d_counts = nullptr;
   int n_slots = 0;
@@ -368,6 +369,7 @@ struct Exec {
   float* out_logits;
   int32_t* out_path;
   int slot = 1;               // next free count slot
+  int fused_launch = 0;       // fused-block launches so far in this run (DYCL_TS selection)
   int nlaunch = 0;
 
   void prof_begin(int kind, const int* cnt, double bpr, double fpr, double bfix) {
@@ -445,7 +447,8 @@ struct Exec {
         ba.b2 = c2.d_b;
         ba.n_live = cnt;
         ba.C = c1.in.C; ba.H = c1.in.H; ba.W = c1.in.W;
-        ba.ts = g->dbg_ts;
+        ++fused_launch;
+        ba.ts = (g->dbg_ts_pick == 0 || g->dbg_ts_pick == fused_launch) ? g->dbg_ts : nullptr;
         const double row_b = (4.0 + 4.0 + (need_b ? 2.0 : 0.0)) * c1.in.row_elems();
         const double row_f = 2.0 * 2.0 * c1.out.H * c1.out.W * c1.out.C * (double)(9 * c1.in.C);
         prof_begin(DYCL_K_CONV, cnt, row_b, row_f, 2.0 * 2 * 3 * c1.out.C * c1.Kp_rt);
@@ -767,6 +770,7 @@ dycl_status dycl_graph_create(int cuda_device, int in_h, int in_w, int in_c, dyc
   if (const char* nf = getenv("DYCL_NO_FUSE")) g->no_fuse = atoi(nf);
   if (getenv("DYCL_TS")) {
     cudaMalloc(&g->dbg_ts, 8 * 16 * sizeof(long long));
+    g->dbg_ts_pick = atoi(getenv("DYCL_TS")) > 1 ? atoi(getenv("DYCL_TS")) : 0;
     cudaMemset(g->dbg_ts, 0, 8 * 16 * sizeof(long long));
   }
   cudaSetDevice(cuda_device);

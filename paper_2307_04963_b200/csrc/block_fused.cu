@@ -15,11 +15,17 @@
 // SMEM banks: the epilogue owns one pixel per thread (TMEM lane = pixel), so plain NHWC
 // fp32 rows (64 / 128 B apart) put 8 lanes of every LDS.128 phase in the same banks.  The
 // fp32 sample is therefore moved by TMA with the 64B / 128B swizzle (16-byte chunk index
-// XOR the 128-byte row index bits), read and written through swz(), and y32 leaves through
-// the same tensor map, which un-swizzles it: conflict-free shortcut reads / output writes.
+// XOR the 128-byte row index bits), read and written through swz(); y is written in place
+// over its shortcut x and leaves through a tensor map that un-swizzles it.  The producer
+// lane issues the stores and refills the buffer with the sample after next as soon as the
+// stores have read it (double-buffered fp32 samples).
+//
+// Pipeline per sample i: convert(i+1) overlaps conv2(i); conv1(i+1) is issued sub-tile by
+// sub-tile as epilogue 2(i) drains the shared TMEM accumulator (stage 1), or into its own
+// accumulator set (stage 2).  Epilogue math uses packed f32x2 ops (combine16).
 //
 // Warps: 0-7 two epilogue/converter warpgroups (sub-tiles split even / odd), 8 bulk-copy
-// producer (double-buffered fp32 sample), 9 TMEM allocator + MMA issuer.
+// producer, 9 TMEM allocator + MMA issuer.
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -38,7 +44,6 @@ struct BCfg {
   static constexpr int BH = 128 / W;                    // image rows per UMMA tile
   static constexpr int N = 3 * C;                       // row-tap MMA width
   static constexpr int X32_BYTES = HW * C * 4;
-  static constexpr int YB_BYTES = HW * C * 2;
   static constexpr int PLANE = (H + 2) * W * 16;        // one 8-channel plane with halo rows
   static constexpr int OPER = P * PLANE;                // bf16 operand image (x or T)
   static constexpr int KP_RT = (3 * C + 63) / 64 * 64;
@@ -46,9 +51,11 @@ struct BCfg {
   static constexpr int W_BYTES = WCH * N * 16;
   static constexpr int BOX_ROWS = HW < 256 ? HW : 256;  // pixels per TMA box (box dims <= 256)
   static constexpr int NBOX = HW / BOX_ROWS;
-  static constexpr int FIXED = 1024 + X32_BYTES /*y staging*/ + 2 * OPER + 2 * W_BYTES + 2 * C * 4 + 256;
-  // fp32 input buffers (2 if they fit) and a separate bf16 output staging buffer if it fits
-  static constexpr int NXB = FIXED + 2 * X32_BYTES + YB_BYTES <= 227 * 1024 ? 2 : 1;
+  static constexpr int FIXED = 1024 + 2 * OPER + 2 * W_BYTES + 2 * C * 4 + 512;
+  // fp32 sample buffers (2 if they fit: y is written in place over its own input x, which is
+  // also the shortcut) and a separate bf16 output staging buffer if it fits
+  static constexpr int NXB = FIXED + 2 * X32_BYTES <= 227 * 1024 ? 2 : 1;
+  static constexpr int YB_BYTES = HW * C * 2;
   static constexpr bool YB_SEP = FIXED + NXB * X32_BYTES + YB_BYTES <= 227 * 1024;
   static constexpr int SMEM = FIXED + NXB * X32_BYTES + (YB_SEP ? YB_BYTES : 0);
   // separate TMEM accumulators for conv1 and conv2 if two fit: conv1(s+1) overlaps epilogue 2(s)
@@ -56,6 +63,7 @@ struct BCfg {
   static_assert(HW % 128 == 0 && 128 % W == 0, "sample must tile into 128-row UMMA tiles");
   static_assert(NSUB * N <= 512, "TMEM");
   static_assert(SMEM <= 227 * 1024, "SMEM");
+  static_assert(NXB == 2, "y is staged in place over x: the next sample needs the other buffer");
 };
 
 // byte offset inside a swizzled fp32 sample buffer (1024-aligned): C=32 -> 128B swizzle,
@@ -70,6 +78,54 @@ __device__ __forceinline__ uint32_t pk(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Refill a sample buffer box by box: box q is reloaded once the bulk store group of box q
+// (committed in order, one group per box) has read it (cp.async.bulk.wait_group.read NBOX-1-q).
+template <int NB, int Q = 0, typename F>
+__device__ __forceinline__ void refill(F&& load_box) {
+  if constexpr (Q < NB) {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(NB - 1 - Q) : "memory");
+    load_box(Q);
+    refill<NB, Q + 1>(load_box);
+  }
+}
+
+// Row-tap combine of 16 channels of one pixel (TMEM lane = pixel w of an image row, lanes of a
+// warp = consecutive pixels): f = relu(D1(w) + bias [+ res] + D0(w-1) + D2(w+1)), the W
+// neighbours by warp shuffle, masked at the row ends by a 0/1 FMA factor; res(q) returns the
+// shortcut channels q..q+3 (read from SMEM just in time).  Packed f32x2 ops
+// (FADD2 / FFMA2) halve the instruction count; every term is added with one fp32 rounding.
+template <int W, typename Res>
+__device__ __forceinline__ void combine16(const uint32_t (&v)[3][16], int w, const float* bias, Res res,
+                                          float (&f)[16], bool with_res = true) {
+  const float ml = w > 0 ? 1.0f : 0.0f, mr = w < W - 1 ? 1.0f : 0.0f;
+  const float2 ml2 = make_float2(ml, ml), mr2 = make_float2(mr, mr);
+#pragma unroll
+  for (int q = 0; q < 16; q += 4) {
+    const float4 b4 = *reinterpret_cast<const float4*>(bias + q);
+    float2 t0 = __fadd2_rn(make_float2(__uint_as_float(v[1][q]), __uint_as_float(v[1][q + 1])), make_float2(b4.x, b4.y));
+    float2 t1 = __fadd2_rn(make_float2(__uint_as_float(v[1][q + 2]), __uint_as_float(v[1][q + 3])), make_float2(b4.z, b4.w));
+    if (with_res) {
+      const float4 r4 = res(q);
+      t0 = __fadd2_rn(t0, make_float2(r4.x, r4.y));
+      t1 = __fadd2_rn(t1, make_float2(r4.z, r4.w));
+    }
+    float l[4], rr[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      l[k] = __shfl_up_sync(0xffffffffu, __uint_as_float(v[0][q + k]), 1);
+      rr[k] = __shfl_down_sync(0xffffffffu, __uint_as_float(v[2][q + k]), 1);
+    }
+    t0 = __ffma2_rn(make_float2(l[0], l[1]), ml2, t0);
+    t1 = __ffma2_rn(make_float2(l[2], l[3]), ml2, t1);
+    t0 = __ffma2_rn(make_float2(rr[0], rr[1]), mr2, t0);
+    t1 = __ffma2_rn(make_float2(rr[2], rr[3]), mr2, t1);
+    f[q] = fmaxf(t0.x, 0.f);
+    f[q + 1] = fmaxf(t0.y, 0.f);
+    f[q + 2] = fmaxf(t1.x, 0.f);
+    f[q + 3] = fmaxf(t1.y, 0.f);
+  }
+}
+
 template <int C, int H>
 __global__ void __launch_bounds__(THREADS, 1)
     k_block_fused(const __grid_constant__ CUtensorMap tmW1, const __grid_constant__ CUtensorMap tmW2,
@@ -78,9 +134,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   constexpr int W = G::W, HW = G::HW, P = G::P;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* x32s = smem;                                                   // [NXB][HW][C] fp32, swizzled
-  uint8_t* ys = x32s + G::NXB * G::X32_BYTES;                             // [HW][C] fp32 y staging, swizzled
-  uint8_t* xb = ys + G::X32_BYTES;                                        // [P][H+2][W][8] bf16
+  uint8_t* x32s = smem;                                                   // [NXB][HW][C] fp32, swizzled (x, then y)
+  uint8_t* xb = x32s + G::NXB * G::X32_BYTES;                             // [P][H+2][W][8] bf16
   uint8_t* tb = xb + G::OPER;
   uint8_t* w1s = tb + G::OPER;
   uint8_t* w2s = w1s + G::W_BYTES;
@@ -88,10 +143,15 @@ __global__ void __launch_bounds__(THREADS, 1)
   float* b1s = reinterpret_cast<float*>(ybs + (G::YB_SEP ? G::YB_BYTES : 0));
   float* b2s = b1s + C;
   uint64_t* bars = reinterpret_cast<uint64_t*>(b2s + C + ((2 * C) & 1));
-  const uint32_t xfull0 = ptx::smem_u32(bars), xempty0 = xfull0 + 16;
-  const uint32_t xb_full = xempty0 + 16, xb_empty = xb_full + 8, acc1 = xb_empty + 8, tb_full = acc1 + 8;
+  // yready[b][k]: box k of buffer b holds y (both warpgroups arrived)
+  const uint32_t xfull0 = ptx::smem_u32(bars), yready0 = ptx::smem_u32(bars + 26);
+  const uint32_t xb_full = xfull0 + 16, xb_empty = xb_full + 8, acc1 = xb_empty + 8, tb_full = acc1 + 8;
   const uint32_t acc2 = tb_full + 8, acc1_empty = acc2 + 8, wfull = acc1_empty + 8, acc2_empty = wfull + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  const uint32_t tb_free = acc2_empty + 8;             // the bf16-copy store has read T / ybs
+  const uint32_t subfree0 = acc2_empty + 16;          // [NSUB] shared set: sub-tile j drained by epilogue 2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26 + 2 * 4);
+  static_assert(G::NBOX <= 4, "box barriers");
+  static_assert(G::NSUB <= 8, "sub-tile barriers");
   constexpr uint32_t SET2 = G::NSETS == 2 ? 256u : 0u;    // TMEM column of the conv2 accumulator
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -100,8 +160,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(xfull0 + 8 * i, 1);
-      ptx::mbar_init(xempty0 + 8 * i, 256);
+      for (int k = 0; k < G::NBOX; ++k) ptx::mbar_init(yready0 + 8 * (4 * i + k), 256);
     }
+    ptx::mbar_init(tb_free, 1);
+    for (int j = 0; j < G::NSUB; ++j) ptx::mbar_init(subfree0 + 8 * j, 128);
     ptx::mbar_init(xb_full, 256);
     ptx::mbar_init(xb_empty, 1);
     ptx::mbar_init(acc1, 1);
@@ -148,18 +210,57 @@ __global__ void __launch_bounds__(THREADS, 1)
           "%5}], [%2];" ::"r"(ptx::smem_u32(w2s)),
           "l"(&tmW2), "r"(wfull), "r"(0), "r"(0), "r"(0)
           : "memory");
-      int it = 0;
-      for (int smp = blockIdx.x; smp < n_live; smp += gridDim.x, ++it) {
-        const int b = it % G::NXB;
-        ptx::mbar_wait(xempty0 + 8 * b, ((it / G::NXB) & 1) ^ 1);
-        if (a.ts && blockIdx.x == 0 && it < 8) a.ts[it * 16 + 10] = clock64();
+      // The producer owns both fp32 sample buffers: it loads sample it into buffer it % 2, and
+      // once the epilogue has written y over it (yready), stores y (+ the bf16 copy), waits for
+      // the stores to have READ SMEM and refills the buffer with sample it + 2 right away.
+      auto load = [&](int k) {
+        const int smp = blockIdx.x + k * gridDim.x;
+        if (smp >= n_live) return;
+        const int b = k % G::NXB;
+        if (a.ts && blockIdx.x == 0 && k < 8) a.ts[k * 16 + 10] = clock64();
         const int src = a.list ? a.list[smp] : smp;
         ptx::mbar_arrive_expect_tx(xfull0 + 8 * b, G::X32_BYTES);
 #pragma unroll
-        for (int k = 0; k < G::NBOX; ++k)
-          ptx::tma_load_2d(ptx::smem_u32(x32s + (size_t)b * G::X32_BYTES + k * G::BOX_ROWS * C * 4), &tmX,
-                           xfull0 + 8 * b, 0, src * HW + k * G::BOX_ROWS);
+        for (int q = 0; q < G::NBOX; ++q)
+          ptx::tma_load_2d(ptx::smem_u32(x32s + (size_t)b * G::X32_BYTES + q * G::BOX_ROWS * C * 4), &tmX,
+                           xfull0 + 8 * b, 0, src * HW + q * G::BOX_ROWS);
+      };
+      load(0);
+      load(1);
+      int it = 0;
+      for (int smp = blockIdx.x; smp < n_live; smp += gridDim.x, ++it) {
+        const int b = it % G::NXB;
+        const uint8_t* xs = x32s + (size_t)b * G::X32_BYTES;
+        const int dst = smp;                           // outputs are dense in row order
+        // store box by box as epilogue 2 finishes it (one bulk group per box) ...
+#pragma unroll
+        for (int q = 0; q < G::NBOX; ++q) {
+          ptx::mbar_wait(yready0 + 8 * (4 * b + q), (it / G::NXB) & 1);
+          if (a.yb)
+            for (int p = 0; p < P; ++p)
+              ptx::bulk_store(a.yb + (size_t)dst * C * HW + (size_t)p * HW * 8 + (size_t)q * G::BOX_ROWS * 8,
+                              ptx::smem_u32((G::YB_SEP ? ybs + p * HW * 16 : tb + p * G::PLANE + W * 16) +
+                                            q * G::BOX_ROWS * 16),
+                              G::BOX_ROWS * 16);
+          ptx::tma_store_2d(&tmY, ptx::smem_u32(xs + q * G::BOX_ROWS * C * 4), 0, dst * HW + q * G::BOX_ROWS);
+          ptx::bulk_commit();
+        }
+        // ... and refill the buffer box by box with sample it + 2 as the stores read it out
+        const int nsmp = blockIdx.x + (it + 2) * gridDim.x;
+        if (nsmp < n_live) {
+          if (a.ts && blockIdx.x == 0 && it + 2 < 8) a.ts[(it + 2) * 16 + 10] = clock64();
+          const int src = a.list ? a.list[nsmp] : nsmp;
+          ptx::mbar_arrive_expect_tx(xfull0 + 8 * b, G::X32_BYTES);
+          refill<G::NBOX>([&](int q) {
+            ptx::tma_load_2d(ptx::smem_u32(x32s + (size_t)b * G::X32_BYTES + q * G::BOX_ROWS * C * 4), &tmX,
+                             xfull0 + 8 * b, 0, src * HW + q * G::BOX_ROWS);
+          });
+        } else {
+          ptx::bulk_wait_read0();
+        }
+        ptx::mbar_arrive(tb_free);                   // all stores have read T / ybs
       }
+      ptx::bulk_wait0();                             // y writes complete before the CTA retires
     }
   } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
@@ -172,14 +273,19 @@ __global__ void __launch_bounds__(THREADS, 1)
     int it = 0;
     for (int smp = blockIdx.x; smp < n_live; smp += gridDim.x, ++it) {
       const uint32_t ph = it & 1;
-      // conv1 accumulator free: drained by epilogue 1 (two sets) / epilogue 2 (shared set)
-      ptx::mbar_wait(G::NSETS == 2 ? acc1_empty : acc2_empty, ph ^ 1);
+      // conv1 accumulator free: drained by epilogue 1 (two sets) / per sub-tile by epilogue 2 of
+      // the previous sample (shared set: conv1 of sample i+1 overlaps epilogue 2 of sample i)
+      if (G::NSETS == 2) ptx::mbar_wait(acc1_empty, ph ^ 1);
       ptx::mbar_wait(xb_full, ph);                    // x operand converted
       ptx::tc_fence_after();
       const bool mstamp = a.ts && blockIdx.x == 0 && lane == 0 && it < 8;
       if (mstamp) a.ts[it * 16 + 6] = clock64();
 #pragma unroll
-      for (int j = 0; j < G::NSUB; ++j)
+      for (int j = 0; j < G::NSUB; ++j) {
+        if (G::NSETS == 1 && it > 0) {
+          ptx::mbar_wait(subfree0 + 8 * j, (it - 1) & 1);
+          ptx::tc_fence_after();
+        }
 #pragma unroll
         for (int r = 0; r < 3; ++r)
 #pragma unroll
@@ -187,6 +293,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             ptx::mma_bf16_ss_elect(tmem + j * G::N, xdesc + (uint64_t)(((j * G::BH + r) * W * 16 + 2 * q * G::PLANE) >> 4),
                                    w1d + (uint64_t)(((r * P + 2 * q) * G::N * 16) >> 4), IDESC,
                                    (uint32_t)((r | q) != 0));
+      }
       ptx::mma_commit_elect(xb_empty);
       ptx::mma_commit_elect(acc1);
       __syncwarp();
@@ -225,6 +332,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint8_t* xs = x32s + (size_t)b * G::X32_BYTES;
       ptx::mbar_wait(xfull0 + 8 * b, (itc / G::NXB) & 1);
       ptx::mbar_wait(xb_empty, (itc & 1) ^ 1);         // conv1 of the previous sample read xb
+#pragma unroll 4
       for (int u = et; u < HW * P; u += 256) {
         const int pix = u % HW, p = u / HW;            // lanes = consecutive pixels (swizzled rows)
         const float4 v0 = *reinterpret_cast<const float4*>(xs + swz<C>((uint32_t)(pix * C + p * 8) * 4));
@@ -233,23 +341,19 @@ __global__ void __launch_bounds__(THREADS, 1)
             make_uint4(pk(v0.x, v0.y), pk(v0.z, v0.w), pk(v1.x, v1.y), pk(v1.z, v1.w));
       }
       ptx::fence_proxy_async_smem();
-      ptx::mbar_arrive(xb_full);
-      ptx::mbar_arrive(xempty0 + 8 * b);
+      ptx::mbar_arrive(xb_full);              // x32s[b] stays: it is the shortcut and y's staging
     };
 
     int it = 0;
     if ((int)blockIdx.x < n_live) convert(0);
     for (int smp = blockIdx.x; smp < n_live; smp += gridDim.x, ++it) {
       const uint32_t ph = it & 1;
-      const int dst = smp;                             // outputs are dense in row order
       const bool stamp = a.ts && blockIdx.x == 0 && et == 0 && it < 8;
       // ---- epilogue 1: T = relu(conv1 + b1) -> bf16 operand image (SMEM)
       ptx::mbar_wait(acc1, ph);
       ptx::tc_fence_after();
-      if (!G::YB_SEP) {                                // T doubles as the bf16 y staging buffer
-        if (et == 0) ptx::bulk_wait_read1();          // the bf16 group (older of the two) has read T
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-      }
+      // the previous sample's bf16-copy store (from T / ybs) has read SMEM: T / ybs may be rewritten
+      if (it > 0 && a.yb) ptx::mbar_wait(tb_free, (it - 1) & 1);
       if (stamp) a.ts[it * 16 + 2] = clock64();
 #pragma unroll
       for (int g = 0; g < UPT; g += 2) {
@@ -268,13 +372,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           const int j = wg + 2 * ((g + u) / CPS), c0 = ((g + u) % CPS) * 16;
           const int pix = j * 128 + r, w = pix % W;
           float f[16];
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const float lft = __shfl_up_sync(0xffffffffu, __uint_as_float(v[u][0][q]), 1);
-            const float rgt = __shfl_down_sync(0xffffffffu, __uint_as_float(v[u][2][q]), 1);
-            f[q] = fmaxf(__uint_as_float(v[u][1][q]) + (w > 0 ? lft : 0.f) + (w < W - 1 ? rgt : 0.f) + b1s[c0 + q],
-                         0.f);
-          }
+          combine16<W>(v[u], w, b1s + c0, [](int) { return make_float4(0.f, 0.f, 0.f, 0.f); }, f, false);
 #pragma unroll
           for (int h2 = 0; h2 < 2; ++h2)
             *reinterpret_cast<uint4*>(tb + ((c0 >> 3) + h2) * G::PLANE + (W + pix) * 16) =
@@ -293,46 +391,44 @@ __global__ void __launch_bounds__(THREADS, 1)
         convert(it + 1);
         if (stamp) a.ts[(it + 1) * 16 + 1] = clock64();
       }
-      // ---- epilogue 2: y = relu(conv2 + b2 + x) -> fp32 stream (+ bf16 operand copy)
-      const float* xg = a.x32 + (size_t)(a.list ? a.list[smp] : smp) * HW * C;   // shortcut (L2-resident)
+      // ---- epilogue 2: y = relu(conv2 + b2 + x) -> fp32 stream (+ bf16 operand copy); the
+      // shortcut x is this sample's fp32 buffer in SMEM and y overwrites it in place
+      uint8_t* xs = x32s + (size_t)(it % G::NXB) * G::X32_BYTES;
       ptx::mbar_wait(acc2, ph);
       ptx::tc_fence_after();
-      if (et == 0) ptx::bulk_wait_read0();             // previous sample's y staging drained
-      asm volatile("bar.sync 1, 256;" ::: "memory");
       if (stamp) a.ts[it * 16 + 4] = clock64();
 #pragma unroll
       for (int g = 0; g < UPT; g += 2) {
         uint32_t v[2][3][16];
-        float4 rs[2][4];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const int j = wg + 2 * ((g + u) / CPS), c0 = ((g + u) % CPS) * 16;
-          const int pix = j * 128 + r;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) rs[u][q] = __ldg(reinterpret_cast<const float4*>(xg + pix * C + c0) + q);
           const uint32_t t = lane_base + SET2 + (uint32_t)(j * G::N + c0);
           ptx::tmem_ld_32x32b_x16(t, v[u][0]);
           ptx::tmem_ld_32x32b_x16(t + C, v[u][1]);
           ptx::tmem_ld_32x32b_x16(t + 2 * C, v[u][2]);
         }
         ptx::tmem_ld_wait();
+        if (G::NSETS == 1) {                           // these sub-tiles' columns are free for conv1
+          ptx::tc_fence_before();
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int j = wg + 2 * ((g + u) / CPS);
+            if (u == 0 || j != wg + 2 * (g / CPS)) ptx::mbar_arrive(subfree0 + 8 * j);
+          }
+        }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const int j = wg + 2 * ((g + u) / CPS), c0 = ((g + u) % CPS) * 16;
           const int pix = j * 128 + r, w = pix % W;
-          const float* res = reinterpret_cast<const float*>(rs[u]);
           float f[16];
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const float lft = __shfl_up_sync(0xffffffffu, __uint_as_float(v[u][0][q]), 1);
-            const float rgt = __shfl_down_sync(0xffffffffu, __uint_as_float(v[u][2][q]), 1);
-            f[q] = fmaxf(__uint_as_float(v[u][1][q]) + (w > 0 ? lft : 0.f) + (w < W - 1 ? rgt : 0.f) + b2s[c0 + q] +
-                             res[q],
-                         0.f);
-          }
+          combine16<W>(v[u], w, b2s + c0, [&](int q) {
+            return *reinterpret_cast<const float4*>(xs + swz<C>((uint32_t)(pix * C + c0 + q) * 4));
+          }, f);
+          // y overwrites its own shortcut x in place (the producer TMA-stores it)
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            *reinterpret_cast<float4*>(ys + swz<C>((uint32_t)(pix * C + c0 + 4 * q) * 4)) =
+            *reinterpret_cast<float4*>(xs + swz<C>((uint32_t)(pix * C + c0 + 4 * q) * 4)) =
                 make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
           if (a.yb) {
             uint8_t* yb_pl = G::YB_SEP ? ybs : tb + W * 16;     // plane stride: HW*16 / PLANE
@@ -343,31 +439,18 @@ __global__ void __launch_bounds__(THREADS, 1)
                   make_uint4(pk(f[8 * h2], f[8 * h2 + 1]), pk(f[8 * h2 + 2], f[8 * h2 + 3]),
                              pk(f[8 * h2 + 4], f[8 * h2 + 5]), pk(f[8 * h2 + 6], f[8 * h2 + 7]));
           }
+          if (c0 + 16 == C) {                          // sub-tile j done: hand its box to the producer
+            ptx::fence_proxy_async_smem();
+            ptx::mbar_arrive(yready0 + 8 * (4 * (it % G::NXB) + j * 128 / G::BOX_ROWS));
+          }
         }
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(acc2_empty);                    // conv2 accumulator drained
-      // staging writes visible to the async proxy, then one thread stores the sample
-      ptx::fence_proxy_async_smem();
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      if (et == 0) {
-        if (a.yb) {
-          if (G::YB_SEP)
-            ptx::bulk_store(a.yb + (size_t)dst * C * HW, ptx::smem_u32(ybs), G::YB_BYTES);
-          else
-            for (int p = 0; p < P; ++p)
-              ptx::bulk_store(a.yb + (size_t)dst * C * HW + (size_t)p * HW * 8,
-                              ptx::smem_u32(tb + p * G::PLANE + W * 16), HW * 16);
-        }
-        ptx::bulk_commit();                            // group 1: bf16 copy (T is reused first)
-#pragma unroll
-        for (int k = 0; k < G::NBOX; ++k)
-          ptx::tma_store_2d(&tmY, ptx::smem_u32(ys + k * G::BOX_ROWS * C * 4), 0, dst * HW + k * G::BOX_ROWS);
-        ptx::bulk_commit();                            // group 2: fp32 stream
-      }
+      if (stamp) a.ts[it * 16 + 5] = clock64();
       if (stamp) a.ts[it * 16 + 5] = clock64();
     }
-    if (et == 0) ptx::bulk_wait0();                    // y writes complete before the CTA retires
+
   }
   __syncthreads();
   if (warp == 9) {

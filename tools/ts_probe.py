@@ -1,7 +1,8 @@
 """Print fused-block phase timelines (CTA 0) for one block launch of config 2 (DYCL_TS=1)."""
 import os
 import sys
-os.environ["DYCL_TS"] = "1"
+
+os.environ["DYCL_TS"] = sys.argv[1] if len(sys.argv) > 1 else "1"   # k > 1: k-th fused launch
 import numpy as np
 import torch
 sys.path.insert(0, ".")
