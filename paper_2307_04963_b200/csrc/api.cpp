@@ -108,6 +108,7 @@ struct dycl_graph_s {
   int conv_path = 0;                 // 0 auto; DYCL_CONV_PATH=1 forces the cp.async kernel
   int conv_dbg = 0;                  // DYCL_CONV_DBG: timing experiments only (results invalid)
   int no_fuse = 0;                   // DYCL_NO_FUSE=1: run basic blocks as two conv launches
+  int max_fuse = 2;                  // DYCL_MAX_FUSE: basic blocks per fused launch (1..2)
   int nhwc = 0;                      // bf16 activations NHWC (decided at finalize; DYCL_NHWC=0 disables)
   int stem_s4d = 0;                  // input cast to 4x4 space-to-depth for the stem (DYCL_STEM_S4D=0 disables)
   long long* dbg_ts = nullptr;       // DYCL_TS=1: fused-block phase timestamps (development)
@@ -432,32 +433,41 @@ struct Exec {
     for (size_t li = 0; li < s.layers.size(); ++li) {
       const Layer& L = s.layers[li];
       if (L.kind == L_BLOCK && fp32_stream() && !g->no_fuse && cur.f >= 0 && fusable(s, li)) {
+        // up to MAX_FUSED_BLOCKS consecutive fusable blocks (same shape) in one launch
+        int nb = 1;
+        while (nb < dycl::MAX_FUSED_BLOCKS && nb < g->max_fuse && fusable(s, li + 3 * nb) &&
+               s.layers[li + 3 * nb + 1].in == s.layers[li + 1].in)
+          ++nb;
         const Layer &c1 = s.layers[li + 1], &c2 = s.layers[li + 2];
-        const bool last = li + 3 == s.layers.size();
-        const bool need_b = last || !fusable(s, li + 3);   // the next layer reads the bf16 copy
+        const size_t lend = li + 3 * nb;             // first layer after the fused group
+        const bool last = lend == s.layers.size();
+        const bool need_b = last || !fusable(s, lend);   // the next layer reads the bf16 copy
         Tensor o = (last && out_hint.b >= 0) ? out_hint : pick_tensor(true, {cur, busy, out_hint});
         if (o.b < 0 || o.f < 0) return fail(g, DYCL_E_STATE, "internal: out of activation buffers");
         dycl::BlockArgs ba{};
         ba.x32 = g->buf32[cur.f];
         ba.y32 = g->buf32[o.f];
         ba.yb = need_b ? g->buf[o.b] : nullptr;
-        ba.w1_rt = c1.d_wrt;
-        ba.w2_rt = c2.d_wrt;
-        ba.b1 = c1.d_b;
-        ba.b2 = c2.d_b;
+        ba.nblk = nb;
+        for (int k = 0; k < nb; ++k) {
+          ba.w1_rt[k] = s.layers[li + 3 * k + 1].d_wrt;
+          ba.w2_rt[k] = s.layers[li + 3 * k + 2].d_wrt;
+          ba.b1[k] = s.layers[li + 3 * k + 1].d_b;
+          ba.b2[k] = s.layers[li + 3 * k + 2].d_b;
+        }
         ba.n_live = cnt;
         ba.C = c1.in.C; ba.H = c1.in.H; ba.W = c1.in.W;
         ++fused_launch;
         ba.ts = (g->dbg_ts_pick == 0 || g->dbg_ts_pick == fused_launch) ? g->dbg_ts : nullptr;
         const double row_b = (4.0 + 4.0 + (need_b ? 2.0 : 0.0)) * c1.in.row_elems();
-        const double row_f = 2.0 * 2.0 * c1.out.H * c1.out.W * c1.out.C * (double)(9 * c1.in.C);
-        prof_begin(DYCL_K_CONV, cnt, row_b, row_f, 2.0 * 2 * 3 * c1.out.C * c1.Kp_rt);
+        const double row_f = nb * 2.0 * 2.0 * c1.out.H * c1.out.W * c1.out.C * (double)(9 * c1.in.C);
+        prof_begin(DYCL_K_CONV, cnt, row_b, row_f, nb * 2.0 * 2 * 3 * c1.out.C * c1.Kp_rt);
         cudaError_t e = dycl::launch_block_fused(ba, batch, g->num_sms, st);
         prof_end();
         if (e != cudaSuccess) return cuda_fail(g, e, "launch_block_fused");
         if (!need_b) o.b = -1;                        // no valid bf16 copy
         cur = o;
-        li += 2;
+        li = lend - 1;
         continue;
       }
       if (L.kind == L_BLOCK) {
@@ -768,6 +778,7 @@ dycl_status dycl_graph_create(int cuda_device, int in_h, int in_w, int in_c, dyc
   if (const char* cp = getenv("DYCL_CONV_PATH")) g->conv_path = atoi(cp);
   if (const char* cd = getenv("DYCL_CONV_DBG")) g->conv_dbg = atoi(cd);
   if (const char* nf = getenv("DYCL_NO_FUSE")) g->no_fuse = atoi(nf);
+  if (const char* mf = getenv("DYCL_MAX_FUSE")) g->max_fuse = atoi(mf);
   if (getenv("DYCL_TS")) {
     cudaMalloc(&g->dbg_ts, 8 * 16 * sizeof(long long));
     g->dbg_ts_pick = atoi(getenv("DYCL_TS")) > 1 ? atoi(getenv("DYCL_TS")) : 0;

@@ -37,7 +37,7 @@ namespace {
 
 constexpr int THREADS = 320;
 
-template <int C, int H>
+template <int C, int H, int NB>
 struct BCfg {
   static constexpr int W = H, HW = H * W, P = C / 8;
   static constexpr int NSUB = HW / 128;                 // UMMA tiles per sample
@@ -51,7 +51,7 @@ struct BCfg {
   static constexpr int W_BYTES = WCH * N * 16;
   static constexpr int BOX_ROWS = HW < 256 ? HW : 256;  // pixels per TMA box (box dims <= 256)
   static constexpr int NBOX = HW / BOX_ROWS;
-  static constexpr int FIXED = 1024 + 2 * OPER + 2 * W_BYTES + 2 * C * 4 + 512;
+  static constexpr int FIXED = 1024 + 2 * OPER + 2 * NB * W_BYTES + 2 * NB * C * 4 + 512;
   // fp32 sample buffers (2 if they fit: y is written in place over its own input x, which is
   // also the shortcut) and a separate bf16 output staging buffer if it fits
   static constexpr int NXB = FIXED + 2 * X32_BYTES <= 227 * 1024 ? 2 : 1;
@@ -126,23 +126,25 @@ __device__ __forceinline__ void combine16(const uint32_t (&v)[3][16], int w, con
   }
 }
 
-template <int C, int H>
+struct WMaps {
+  CUtensorMap m[2 * MAX_FUSED_BLOCKS];   // conv1, conv2 row-tap weights of each fused block
+};
+
+template <int C, int H, int NB>
 __global__ void __launch_bounds__(THREADS, 1)
-    k_block_fused(const __grid_constant__ CUtensorMap tmW1, const __grid_constant__ CUtensorMap tmW2,
-                  const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY, const BlockArgs a) {
-  using G = BCfg<C, H>;
+    k_block_fused(const __grid_constant__ WMaps wm, const __grid_constant__ CUtensorMap tmX,
+                  const __grid_constant__ CUtensorMap tmY, const BlockArgs a) {
+  using G = BCfg<C, H, NB>;
   constexpr int W = G::W, HW = G::HW, P = G::P;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* x32s = smem;                                                   // [NXB][HW][C] fp32, swizzled (x, then y)
   uint8_t* xb = x32s + G::NXB * G::X32_BYTES;                             // [P][H+2][W][8] bf16
   uint8_t* tb = xb + G::OPER;
-  uint8_t* w1s = tb + G::OPER;
-  uint8_t* w2s = w1s + G::W_BYTES;
-  uint8_t* ybs = w2s + G::W_BYTES;                                        // [P][HW][8] bf16 y staging
-  float* b1s = reinterpret_cast<float*>(ybs + (G::YB_SEP ? G::YB_BYTES : 0));
-  float* b2s = b1s + C;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(b2s + C + ((2 * C) & 1));
+  uint8_t* ws = tb + G::OPER;                                             // [NB][conv1, conv2] row-tap weights
+  uint8_t* ybs = ws + 2 * NB * G::W_BYTES;                                // [P][HW][8] bf16 y staging
+  float* bs = reinterpret_cast<float*>(ybs + (G::YB_SEP ? G::YB_BYTES : 0));   // [NB][b1 | b2]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bs + 2 * NB * C);
   // yready[b][k]: box k of buffer b holds y (both warpgroups arrived)
   const uint32_t xfull0 = ptx::smem_u32(bars), yready0 = ptx::smem_u32(bars + 26);
   const uint32_t xb_full = xfull0 + 16, xb_empty = xb_full + 8, acc1 = xb_empty + 8, tb_full = acc1 + 8;
@@ -182,9 +184,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint8_t* base = img ? tb : xb;
     *reinterpret_cast<uint4*>(base + p * G::PLANE + (row * W + w) * 16) = make_uint4(0, 0, 0, 0);
   }
-  for (int i = threadIdx.x; i < C; i += blockDim.x) {
-    b1s[i] = a.b1[i];
-    b2s[i] = a.b2[i];
+  for (int i = threadIdx.x; i < 2 * NB * C; i += blockDim.x) {
+    const int blk = i / (2 * C), k = (i / C) & 1, c = i % C;
+    bs[i] = (k ? a.b2[blk] : a.b1[blk])[c];
   }
   ptx::fence_proxy_async_smem();
   if (warp == 9) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), 512);
@@ -196,20 +198,15 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 8) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
-      ptx::tma_prefetch_desc(&tmW1);
-      ptx::tma_prefetch_desc(&tmW2);
       ptx::tma_prefetch_desc(&tmX);
-      ptx::mbar_arrive_expect_tx(wfull, 2 * G::W_BYTES);
-      asm volatile(
-          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
-          "%5}], [%2];" ::"r"(ptx::smem_u32(w1s)),
-          "l"(&tmW1), "r"(wfull), "r"(0), "r"(0), "r"(0)
-          : "memory");
-      asm volatile(
-          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
-          "%5}], [%2];" ::"r"(ptx::smem_u32(w2s)),
-          "l"(&tmW2), "r"(wfull), "r"(0), "r"(0), "r"(0)
-          : "memory");
+      ptx::mbar_arrive_expect_tx(wfull, 2 * NB * G::W_BYTES);
+#pragma unroll
+      for (int i = 0; i < 2 * NB; ++i)
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+            "%5}], [%2];" ::"r"(ptx::smem_u32(ws + i * G::W_BYTES)),
+            "l"(&wm.m[i]), "r"(wfull), "r"(0), "r"(0), "r"(0)
+            : "memory");
       // The producer owns both fp32 sample buffers: it loads sample it into buffer it % 2, and
       // once the epilogue has written y over it (yready), stores y (+ the bf16 copy), waits for
       // the stores to have READ SMEM and refills the buffer with sample it + 2 right away.
@@ -264,57 +261,63 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
+    // conv occurrence k = it * NB + blk: conv1 / conv2 of fused block blk of this CTA's
+    // it-th sample; every barrier below completes once per occurrence.
     constexpr uint32_t IDESC = ptx::make_idesc_bf16(128, G::N);
     const uint64_t xdesc = ptx::make_smem_desc(ptx::smem_u32(xb), 0, G::PLANE, 128);
     const uint64_t tdesc = ptx::make_smem_desc(ptx::smem_u32(tb), 0, G::PLANE, 128);
-    const uint64_t w1d = ptx::make_smem_desc(ptx::smem_u32(w1s), 0, G::N * 16, 128);
-    const uint64_t w2d = ptx::make_smem_desc(ptx::smem_u32(w2s), 0, G::N * 16, 128);
     ptx::mbar_wait(wfull, 0);
     int it = 0;
     for (int smp = blockIdx.x; smp < n_live; smp += gridDim.x, ++it) {
-      const uint32_t ph = it & 1;
-      // conv1 accumulator free: drained by epilogue 1 (two sets) / per sub-tile by epilogue 2 of
-      // the previous sample (shared set: conv1 of sample i+1 overlaps epilogue 2 of sample i)
-      if (G::NSETS == 2) ptx::mbar_wait(acc1_empty, ph ^ 1);
-      ptx::mbar_wait(xb_full, ph);                    // x operand converted
-      ptx::tc_fence_after();
       const bool mstamp = a.ts && blockIdx.x == 0 && lane == 0 && it < 8;
-      if (mstamp) a.ts[it * 16 + 6] = clock64();
+      for (int blk = 0; blk < NB; ++blk) {
+        const int k = it * NB + blk;
+        const uint32_t ph = k & 1;
+        const uint64_t w1d = ptx::make_smem_desc(ptx::smem_u32(ws + (2 * blk) * G::W_BYTES), 0, G::N * 16, 128);
+        const uint64_t w2d = ptx::make_smem_desc(ptx::smem_u32(ws + (2 * blk + 1) * G::W_BYTES), 0, G::N * 16, 128);
+        // conv1 accumulator free: drained by epilogue 1 (two sets) / per sub-tile by the previous
+        // epilogue 2 (shared set: conv1 of the next sample overlaps epilogue 2 of this one)
+        if (G::NSETS == 2) ptx::mbar_wait(acc1_empty, ph ^ 1);
+        ptx::mbar_wait(xb_full, ph);                  // x operand: converted, or the previous block's y
+        ptx::tc_fence_after();
+        if (mstamp && blk == 0) a.ts[it * 16 + 6] = clock64();
 #pragma unroll
-      for (int j = 0; j < G::NSUB; ++j) {
-        if (G::NSETS == 1 && it > 0) {
-          ptx::mbar_wait(subfree0 + 8 * j, (it - 1) & 1);
-          ptx::tc_fence_after();
+        for (int j = 0; j < G::NSUB; ++j) {
+          if (G::NSETS == 1 && k > 0) {
+            ptx::mbar_wait(subfree0 + 8 * j, (k - 1) & 1);
+            ptx::tc_fence_after();
+          }
+#pragma unroll
+          for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int q = 0; q < C / 16; ++q)
+              ptx::mma_bf16_ss_elect(tmem + j * G::N,
+                                     xdesc + (uint64_t)(((j * G::BH + r) * W * 16 + 2 * q * G::PLANE) >> 4),
+                                     w1d + (uint64_t)(((r * P + 2 * q) * G::N * 16) >> 4), IDESC,
+                                     (uint32_t)((r | q) != 0));
         }
+        ptx::mma_commit_elect(xb_empty);
+        ptx::mma_commit_elect(acc1);
+        __syncwarp();
+        if (mstamp && blk == 0) a.ts[it * 16 + 7] = clock64();
+        ptx::mbar_wait(tb_full, ph);                  // T written (and conv1 TMEM read) by epilogue 1
+        if (G::NSETS == 2) ptx::mbar_wait(acc2_empty, ph ^ 1);
+        ptx::tc_fence_after();
+        if (mstamp && blk == NB - 1) a.ts[it * 16 + 8] = clock64();
 #pragma unroll
-        for (int r = 0; r < 3; ++r)
+        for (int j = 0; j < G::NSUB; ++j)
 #pragma unroll
-          for (int q = 0; q < C / 16; ++q)
-            ptx::mma_bf16_ss_elect(tmem + j * G::N, xdesc + (uint64_t)(((j * G::BH + r) * W * 16 + 2 * q * G::PLANE) >> 4),
-                                   w1d + (uint64_t)(((r * P + 2 * q) * G::N * 16) >> 4), IDESC,
-                                   (uint32_t)((r | q) != 0));
+          for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int q = 0; q < C / 16; ++q)
+              ptx::mma_bf16_ss_elect(tmem + SET2 + j * G::N,
+                                     tdesc + (uint64_t)(((j * G::BH + r) * W * 16 + 2 * q * G::PLANE) >> 4),
+                                     w2d + (uint64_t)(((r * P + 2 * q) * G::N * 16) >> 4), IDESC,
+                                     (uint32_t)((r | q) != 0));
+        ptx::mma_commit_elect(acc2);
+        __syncwarp();
+        if (mstamp && blk == NB - 1) a.ts[it * 16 + 9] = clock64();
       }
-      ptx::mma_commit_elect(xb_empty);
-      ptx::mma_commit_elect(acc1);
-      __syncwarp();
-      if (mstamp) a.ts[it * 16 + 7] = clock64();
-      ptx::mbar_wait(tb_full, ph);                    // T written (and conv1 TMEM read) by epilogue 1
-      if (G::NSETS == 2) ptx::mbar_wait(acc2_empty, ph ^ 1);
-      ptx::tc_fence_after();
-      if (mstamp) a.ts[it * 16 + 8] = clock64();
-#pragma unroll
-      for (int j = 0; j < G::NSUB; ++j)
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-          for (int q = 0; q < C / 16; ++q)
-            ptx::mma_bf16_ss_elect(tmem + SET2 + j * G::N,
-                                   tdesc + (uint64_t)(((j * G::BH + r) * W * 16 + 2 * q * G::PLANE) >> 4),
-                                   w2d + (uint64_t)(((r * P + 2 * q) * G::N * 16) >> 4), IDESC,
-                                   (uint32_t)((r | q) != 0));
-      ptx::mma_commit_elect(acc2);
-      __syncwarp();
-      if (mstamp) a.ts[it * 16 + 9] = clock64();
     }
   } else {
     // ------------------------------------------------------------ converters / epilogues
@@ -331,7 +334,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int b = itc % G::NXB;
       const uint8_t* xs = x32s + (size_t)b * G::X32_BYTES;
       ptx::mbar_wait(xfull0 + 8 * b, (itc / G::NXB) & 1);
-      ptx::mbar_wait(xb_empty, (itc & 1) ^ 1);         // conv1 of the previous sample read xb
+      ptx::mbar_wait(xb_empty, (itc * NB - 1) & 1);    // the previous sample's last conv1 read xb
 #pragma unroll 4
       for (int u = et; u < HW * P; u += 256) {
         const int pix = u % HW, p = u / HW;            // lanes = consecutive pixels (swizzled rows)
@@ -347,14 +350,19 @@ __global__ void __launch_bounds__(THREADS, 1)
     int it = 0;
     if ((int)blockIdx.x < n_live) convert(0);
     for (int smp = blockIdx.x; smp < n_live; smp += gridDim.x, ++it) {
-      const uint32_t ph = it & 1;
+     for (int blk = 0; blk < NB; ++blk) {
+      const int kocc = it * NB + blk;
+      const uint32_t ph = kocc & 1;
+      const bool last = blk == NB - 1;
+      const float* b1s = bs + 2 * blk * C;
+      const float* b2s = b1s + C;
       const bool stamp = a.ts && blockIdx.x == 0 && et == 0 && it < 8;
       // ---- epilogue 1: T = relu(conv1 + b1) -> bf16 operand image (SMEM)
       ptx::mbar_wait(acc1, ph);
       ptx::tc_fence_after();
       // the previous sample's bf16-copy store (from T / ybs) has read SMEM: T / ybs may be rewritten
-      if (it > 0 && a.yb) ptx::mbar_wait(tb_free, (it - 1) & 1);
-      if (stamp) a.ts[it * 16 + 2] = clock64();
+      if (blk == 0 && it > 0 && a.yb) ptx::mbar_wait(tb_free, (it - 1) & 1);
+      if (stamp && blk == 0) a.ts[it * 16 + 2] = clock64();
 #pragma unroll
       for (int g = 0; g < UPT; g += 2) {
         uint32_t v[2][3][16];
@@ -382,11 +390,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       ptx::fence_proxy_async_smem();
       ptx::tc_fence_before();
-      if (stamp) a.ts[it * 16 + 3] = clock64();
+      if (stamp && blk == 0) a.ts[it * 16 + 3] = clock64();
       ptx::mbar_arrive(tb_full);
       if (G::NSETS == 2) ptx::mbar_arrive(acc1_empty);
-      // ---- next sample's operand conversion overlaps conv2 of this one
-      if (smp + (int)gridDim.x < n_live) {
+      // ---- next sample's operand conversion overlaps the last conv2 of this one
+      if (last && smp + (int)gridDim.x < n_live) {
         if (stamp) a.ts[(it + 1) * 16 + 0] = clock64();
         convert(it + 1);
         if (stamp) a.ts[(it + 1) * 16 + 1] = clock64();
@@ -396,7 +404,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint8_t* xs = x32s + (size_t)(it % G::NXB) * G::X32_BYTES;
       ptx::mbar_wait(acc2, ph);
       ptx::tc_fence_after();
-      if (stamp) a.ts[it * 16 + 4] = clock64();
+      if (stamp && last) a.ts[it * 16 + 4] = clock64();
 #pragma unroll
       for (int g = 0; g < UPT; g += 2) {
         uint32_t v[2][3][16];
@@ -430,7 +438,13 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int q = 0; q < 4; ++q)
             *reinterpret_cast<float4*>(xs + swz<C>((uint32_t)(pix * C + c0 + 4 * q) * 4)) =
                 make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
-          if (a.yb) {
+          if (!last) {                                 // the next fused block's conv1 operand
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2)
+              *reinterpret_cast<uint4*>(xb + ((c0 >> 3) + h2) * G::PLANE + (W + pix) * 16) =
+                  make_uint4(pk(f[8 * h2], f[8 * h2 + 1]), pk(f[8 * h2 + 2], f[8 * h2 + 3]),
+                             pk(f[8 * h2 + 4], f[8 * h2 + 5]), pk(f[8 * h2 + 6], f[8 * h2 + 7]));
+          } else if (a.yb) {
             uint8_t* yb_pl = G::YB_SEP ? ybs : tb + W * 16;     // plane stride: HW*16 / PLANE
             constexpr int PSTR = G::YB_SEP ? HW * 16 : G::PLANE;
 #pragma unroll
@@ -439,7 +453,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                   make_uint4(pk(f[8 * h2], f[8 * h2 + 1]), pk(f[8 * h2 + 2], f[8 * h2 + 3]),
                              pk(f[8 * h2 + 4], f[8 * h2 + 5]), pk(f[8 * h2 + 6], f[8 * h2 + 7]));
           }
-          if (c0 + 16 == C) {                          // sub-tile j done: hand its box to the producer
+          if (last && c0 + 16 == C) {                  // sub-tile j done: hand its box to the producer
             ptx::fence_proxy_async_smem();
             ptx::mbar_arrive(yready0 + 8 * (4 * (it % G::NXB) + j * 128 / G::BOX_ROWS));
           }
@@ -447,8 +461,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(acc2_empty);                    // conv2 accumulator drained
-      if (stamp) a.ts[it * 16 + 5] = clock64();
-      if (stamp) a.ts[it * 16 + 5] = clock64();
+      if (!last) {                                     // y (bf16) is the next block's conv1 operand
+        ptx::fence_proxy_async_smem();
+        ptx::mbar_arrive(xb_full);
+      }
+      if (stamp && last) a.ts[it * 16 + 5] = clock64();
+     }
     }
 
   }
@@ -474,44 +492,46 @@ EncodeTiledFn enc_fn() {
   return fn;
 }
 
-template <int C, int H>
+template <int C, int H, int NB>
 cudaError_t launch_ch(const BlockArgs& a, int max_rows, int num_sms, cudaStream_t stream) {
-  using G = BCfg<C, H>;
+  using G = BCfg<C, H, NB>;
   EncodeTiledFn enc = enc_fn();
   if (!enc) return cudaErrorNotSupported;
-  CUtensorMap tm[4];
-  const uint16_t* ws[2] = {a.w1_rt, a.w2_rt};
-  for (int i = 0; i < 2; ++i) {
+  WMaps wm;
+  for (int i = 0; i < 2 * NB; ++i) {
+    const uint16_t* w = (i & 1) ? a.w2_rt[i / 2] : a.w1_rt[i / 2];
     cuuint64_t dims[3] = {8, (cuuint64_t)G::N, (cuuint64_t)G::WCH};
     cuuint64_t strides[2] = {(cuuint64_t)G::KP_RT * 2, 16};
     cuuint32_t box[3] = {8, (cuuint32_t)G::N, (cuuint32_t)G::WCH};
     cuuint32_t es[3] = {1, 1, 1};
-    if (enc(&tm[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, (void*)ws[i], dims, strides, box, es,
+    if (enc(&wm.m[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, (void*)w, dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
   // fp32 stream in / out: [rows][C] fp32, box [BOX_ROWS][C], swizzled to the C*4-byte row
+  CUtensorMap tm[2];
   const float* xy[2] = {a.x32, a.y32};
   for (int i = 0; i < 2; ++i) {
     cuuint64_t dims[2] = {(cuuint64_t)C, (cuuint64_t)max_rows * G::HW};
     cuuint64_t strides[1] = {(cuuint64_t)C * 4};
     cuuint32_t box[2] = {(cuuint32_t)C, (cuuint32_t)G::BOX_ROWS};
     cuuint32_t es[2] = {1, 1};
-    if (enc(&tm[2 + i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)xy[i], dims, strides, box, es,
+    if (enc(&tm[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)xy[i], dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, C == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_block_fused<C, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+    cudaError_t e =
+        cudaFuncSetAttribute(k_block_fused<C, H, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   int grid = max_rows < num_sms ? max_rows : num_sms;
   if (grid < 1) grid = 1;
-  k_block_fused<C, H><<<grid, THREADS, G::SMEM, stream>>>(tm[0], tm[1], tm[2], tm[3], a);
+  k_block_fused<C, H, NB><<<grid, THREADS, G::SMEM, stream>>>(wm, tm[0], tm[1], a);
   return cudaGetLastError();
 }
 
@@ -520,8 +540,13 @@ cudaError_t launch_ch(const BlockArgs& a, int max_rows, int num_sms, cudaStream_
 bool block_fused_eligible(int C, int H, int W) { return H == W && ((C == 16 && H == 32) || (C == 32 && H == 16)); }
 
 cudaError_t launch_block_fused(const BlockArgs& a, int max_rows, int num_sms, cudaStream_t stream) {
-  if (a.C == 16 && a.H == 32 && a.W == 32) return launch_ch<16, 32>(a, max_rows, num_sms, stream);
-  if (a.C == 32 && a.H == 16 && a.W == 16) return launch_ch<32, 16>(a, max_rows, num_sms, stream);
+  if (a.nblk < 1 || a.nblk > MAX_FUSED_BLOCKS) return cudaErrorInvalidValue;
+  if (a.C == 16 && a.H == 32 && a.W == 32)
+    return a.nblk == 2 ? launch_ch<16, 32, 2>(a, max_rows, num_sms, stream)
+                       : launch_ch<16, 32, 1>(a, max_rows, num_sms, stream);
+  if (a.C == 32 && a.H == 16 && a.W == 16)
+    return a.nblk == 2 ? launch_ch<32, 16, 2>(a, max_rows, num_sms, stream)
+                       : launch_ch<32, 16, 1>(a, max_rows, num_sms, stream);
   return cudaErrorNotSupported;
 }
 

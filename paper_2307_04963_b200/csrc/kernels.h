@@ -141,17 +141,20 @@ struct PoolArgs {
 };
 cudaError_t launch_maxpool(const PoolArgs& a, int max_rows, int num_sms, cudaStream_t s);
 
-// Fused residual basic block (block_fused.cu): y = relu(conv2(relu(conv1(x))) + x), 3x3 / stride 1,
-// whole sample per CTA iteration, fp32 stream in/out (+ optional bf16 channel-planar copy).
+// Fused residual basic blocks (block_fused.cu): nblk consecutive blocks y = relu(conv2(relu(conv1(x)))
+// + x), 3x3 / stride 1, whole sample per CTA iteration kept in SMEM across the blocks, fp32 stream
+// in/out (+ optional bf16 channel-planar copy of the last block's output).
+constexpr int MAX_FUSED_BLOCKS = 2;
 struct BlockArgs {
-  const float* x32;        // fp32 NHWC [n][H][W][C] (the block input, also the shortcut)
+  const float* x32;        // fp32 NHWC [n][H][W][C] (the first block's input, also its shortcut)
   const int32_t* list;     // optional row index list (input row = list[i]), nullptr = identity
   float* y32;              // fp32 NHWC [n][H][W][C]
   uint16_t* yb;            // bf16 channel-planar copy or nullptr
-  const uint16_t* w1_rt;   // row-tap weights [3C][Kp_rt] (pack_rowtap)
-  const uint16_t* w2_rt;
-  const float* b1;
-  const float* b2;
+  int nblk;                // blocks fused in this launch (1..MAX_FUSED_BLOCKS)
+  const uint16_t* w1_rt[MAX_FUSED_BLOCKS];   // row-tap weights [3C][Kp_rt] (pack_rowtap) per block
+  const uint16_t* w2_rt[MAX_FUSED_BLOCKS];
+  const float* b1[MAX_FUSED_BLOCKS];
+  const float* b2[MAX_FUSED_BLOCKS];
   const int* n_live;
   int n_static, C, H, W;
   long long* ts;           // debug only: per-phase clock64 stamps of CTA 0 (nullptr = off)
