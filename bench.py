@@ -277,27 +277,32 @@ def run_dycl(args):
     # Pass 2 (the roofline): the same K steps again with per-launch CUDA events recorded by
     # libdycl on the launch stream around every kernel (kept out of pass 1: ~80 event pairs
     # per step perturb the step time).
-    conv_ms = conv_bytes = conv_flops = 0.0
-    conv_launches = 0
-    kind_ms = {}
+    # per-kind totals: ms, algorithmic bytes, algorithmic flops, launches
+    kind_tot = {}
     launches = 0
     if job.g is not None:
         D.dycl_set_profiling(job.g, 1)
-        for i in range(args.steps):
-            flush.zero_()
-            job.step(stream)     # profiling records the last chunk's launches; chunks are identical in shape
-            for p in D.dycl_profile_read(job.g):    # syncs the stream
-                kind_ms[p["kind"]] = kind_ms.get(p["kind"], 0.0) + p["ms"]
-                if p["kind"] == "conv":
-                    conv_ms += p["ms"]
-                    conv_bytes += p["bytes"]
-                    conv_flops += p["flops"]
-                    conv_launches += 1
-        torch.cuda.synchronize()
+        prof_read = lambda: D.dycl_profile_read(job.g)   # noqa: E731
+    else:
+        D.dycl_s2s_set_profiling(job.model.h, 1)
+        prof_read = lambda: D.dycl_s2s_profile_read(job.model.h)   # noqa: E731
+    for i in range(args.steps):
+        flush.zero_()
+        job.step(stream)     # profiling records the last chunk's launches; chunks are identical in shape
+        for p in prof_read():    # syncs the stream
+            t = kind_tot.setdefault(p["kind"], [0.0, 0.0, 0.0, 0])
+            t[0] += p["ms"]
+            t[1] += p["bytes"]
+            t[2] += p["flops"]
+            t[3] += 1
+    torch.cuda.synchronize()
+    if job.g is not None:
         D.dycl_set_profiling(job.g, 0)
         launches = D.dycl_launches_per_run(job.g) * args.steps * ((B + job.chunk - 1) // job.chunk)
     else:
+        D.dycl_s2s_set_profiling(job.model.h, 0)
         launches = D.dycl_s2s_launches(job.model.h) * args.steps
+    kind_ms = {k: v[0] for k, v in kind_tot.items()}
     hist = job.hist()
 
     # e2e: the public host-buffer call (pinned buffers; H2D + run + D2H each step)
@@ -326,30 +331,46 @@ def run_dycl(args):
     hbm, tf_burst, tf_sus, peak_src = _peaks()
     value = B * ws * args.steps / (total_ms / 1e3)
     roof = None
-    if conv_ms:
-        achieved = conv_bytes / (conv_ms / 1e3) / 1e9
-        tflops = conv_flops / (conv_ms / 1e3) / 1e12
-        traffic = None
-        tpath = os.path.join(ROOT, "profiles", "conv_traffic.json")
-        if args.config == 2 and os.path.exists(tpath):
-            try:
-                traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
-            except Exception:
-                traffic = None
-        if args.config == 5:       # ResNet-50 convs: tensor-bound
-            roof = {"kernel": "conv (a1: implicit-GEMM conv on tcgen05)", "bound": "tensor", "achieved": tflops,
-                    "peak": tf_sus, "unit": "TFLOP/s", "frac": tflops / tf_sus, "traffic": None,
-                    "peak_source": peak_src + " bf16 sustained", "hbm_GBps": achieved}
+    step_prof_ms = sum(kind_ms.values())
+    if kind_tot:
+        # the dominant kernel class of the step (largest share of the per-launch event time)
+        dom = max(kind_tot, key=lambda k: kind_tot[k][0])
+        ms_, by_, fl_, n_ = kind_tot[dom]
+        gbs = by_ / (ms_ / 1e3) / 1e9
+        tfl = fl_ / (ms_ / 1e3) / 1e12
+        names = {
+            "block": "k_block_fused (a1: 1-2 whole residual blocks per sample, SMEM-resident, row-tap tcgen05 convs)",
+            "conv": "a1 conv class (k_conv_gemm NHWC im2col GEMM / k_conv_tma / k_gemm_tma on tcgen05, fused epilogue)",
+            "gemm": "k_gemm_tma (a7/a8 decoder + encoder projections, FFN, LM head on tcgen05)",
+            "attn": "k_attn_decoder (a7 decode attention, KV-cache streaming)",
+        }
+        tensor_bound = dom in ("gemm",) or (dom == "conv" and args.config == 5)
+        if tensor_bound:
+            roof = {"kernel": names.get(dom, dom), "bound": "tensor", "achieved": tfl, "peak": tf_sus,
+                    "unit": "TFLOP/s", "frac": tfl / tf_sus, "traffic": None,
+                    "peak_source": peak_src + " bf16 sustained", "hbm_GBps": gbs}
         else:
-            roof = {"kernel": "a1 conv class: k_block_fused (whole residual block per sample, SMEM-resident) + "
-                              "k_conv_tma / k_gemm_tma (implicit-GEMM conv / dense on tcgen05, fused epilogue)",
-                    "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                    "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
-                    "tensor_tflops": tflops, "tensor_frac_of_sustained": tflops / tf_sus}
-        roof.update({"share_of_step": conv_ms / sum(kind_ms.values()) if kind_ms else None,
-                     "measured": "per-launch CUDA events (libdycl profiling) over a second pass of the same "
-                                 "K steps; achieved = algorithmic bytes (or FLOPs) / kernel time",
-                     "launches_per_step": conv_launches // max(args.steps, 1)})
+            traffic = None
+            tpath = os.path.join(ROOT, "profiles", "block_traffic.json")
+            if dom == "block" and args.config == 2 and os.path.exists(tpath):
+                try:
+                    traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+                except Exception:
+                    traffic = None
+            roof = {"kernel": names.get(dom, dom), "bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
+                    "frac": gbs / hbm, "traffic": traffic, "peak_source": peak_src,
+                    "tensor_tflops": tfl, "tensor_frac_of_sustained": tfl / tf_sus}
+        roof.update({"share_of_step": ms_ / step_prof_ms if step_prof_ms else None,
+                     "algorithmic_bytes_per_launch": by_ / max(n_, 1),
+                     "algorithmic_flops_per_launch": fl_ / max(n_, 1),
+                     "avg_launch_ms": ms_ / max(n_, 1),
+                     "launches_per_step": n_ // max(args.steps, 1),
+                     "measured": "per-launch CUDA events (libdycl profiling) on the launch stream over a second "
+                                 "pass of the same K steps; achieved = algorithmic bytes (or FLOPs) / kernel time",
+                     "classes": {k: {"ms_per_step": v[0] / args.steps, "share": v[0] / step_prof_ms,
+                                     "GBps": v[1] / (v[0] / 1e3) / 1e9 if v[0] else 0.0,
+                                     "TFLOPs": v[2] / (v[0] / 1e3) / 1e12 if v[0] else 0.0}
+                                 for k, v in sorted(kind_tot.items(), key=lambda kv: -kv[1][0])}})
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,

@@ -200,7 +200,9 @@ dycl_status dycl_num_classes(dycl_graph g, int32_t* out);
  * the launch processed, read back AFTER the run).  Arrays hold max_n entries;
  * *n_out receives the number of launches. */
 enum { DYCL_K_INPUT = 0, DYCL_K_CONV = 1, DYCL_K_HEAD = 2, DYCL_K_COMPACT = 3,
-       DYCL_K_GATHER = 4, DYCL_K_SCATTER = 5, DYCL_K_INIT = 6, DYCL_K_POOL = 7 };
+       DYCL_K_GATHER = 4, DYCL_K_SCATTER = 5, DYCL_K_INIT = 6, DYCL_K_POOL = 7,
+       DYCL_K_BLOCK = 8 /* fused residual blocks (k_block_fused) */, DYCL_K_GEMM = 9 /* dense GEMM */,
+       DYCL_K_ATTN = 10, DYCL_K_LN = 11, DYCL_K_ARGMAX = 12, DYCL_K_EMBED = 13 };
 dycl_status dycl_set_profiling(dycl_graph g, int enable);
 dycl_status dycl_profile_read(dycl_graph g, int32_t max_n, int32_t* kind, float* ms,
                               double* bytes, double* flops, int32_t* n_out);
@@ -277,6 +279,13 @@ dycl_status dycl_s2s_run_host(dycl_s2s s, const int32_t* src_host, int64_t batch
                               int32_t* lengths_host, void* stream);
 /* Number of this library's kernels the last run launched. */
 dycl_status dycl_s2s_launches(dycl_s2s s, int32_t* out);
+/* Per-launch profiling of the generative graph, same contract as dycl_set_profiling /
+ * dycl_profile_read (kinds DYCL_K_GEMM / ATTN / LN / ARGMAX / EMBED / COMPACT / INIT);
+ * while enabled, runs are issued launch by launch (no CUDA graph) with events around
+ * each launch. */
+dycl_status dycl_s2s_set_profiling(dycl_s2s s, int enable);
+dycl_status dycl_s2s_profile_read(dycl_s2s s, int32_t max_n, int32_t* kind, float* ms,
+                                  double* bytes, double* flops, int32_t* n_out);
 
 /* ------------------------------------------------------------ test hook ---- */
 /* Run ONE conv2d layer (the a1 tensor-core kernel, same code path dycl_run uses)

@@ -411,6 +411,9 @@ struct Exec {
     return o;
   }
   bool fp32_stream() const { return g->precision == DYCL_PREC_FP32_STREAM; }
+  // bf16 activation layout of a tensor with C (padded) channels: NHWC when C % 64 == 0 (the
+  // im2col GEMM's 64-channel operand boxes), channel-planar otherwise (the two coincide at C = 8)
+  bool lay(int C) const { return g->nhwc && C % 64 == 0; }
 
   // A basic block the fused kernel can run: BLOCK, conv3x3/s1/p1 ReLU (C->C),
   // conv3x3/s1/p1 ReLU + identity residual, on an eligible sample shape.
@@ -461,7 +464,7 @@ struct Exec {
         ba.ts = (g->dbg_ts_pick == 0 || g->dbg_ts_pick == fused_launch) ? g->dbg_ts : nullptr;
         const double row_b = (4.0 + 4.0 + (need_b ? 2.0 : 0.0)) * c1.in.row_elems();
         const double row_f = nb * 2.0 * 2.0 * c1.out.H * c1.out.W * c1.out.C * (double)(9 * c1.in.C);
-        prof_begin(DYCL_K_CONV, cnt, row_b, row_f, nb * 2.0 * 2 * 3 * c1.out.C * c1.Kp_rt);
+        prof_begin(DYCL_K_BLOCK, cnt, row_b, row_f, nb * 2.0 * 2 * 3 * c1.out.C * c1.Kp_rt);
         cudaError_t e = dycl::launch_block_fused(ba, batch, g->num_sms, st);
         prof_end();
         if (e != cudaSuccess) return cuda_fail(g, e, "launch_block_fused");
@@ -490,7 +493,7 @@ struct Exec {
         pa.n_live = cnt;
         pa.H = L.in.H; pa.W = L.in.W; pa.C = L.in.Cp(); pa.Ho = L.out.H; pa.Wo = L.out.W;
         pa.k = L.k; pa.stride = L.stride; pa.pad = L.pad;
-        pa.nhwc = g->nhwc;
+        pa.nhwc = lay(L.in.Cp());
         pa.s2d = L.pool_s2d;
         prof_begin(DYCL_K_POOL, cnt, (pa.x32 ? 4.0 : 2.0) * L.in.row_elems() + (o.f >= 0 ? 6.0 : 2.0) * L.out.row_elems(), 0, 0);
         cudaError_t e = dycl::launch_maxpool(pa, batch, g->num_sms, st);
@@ -520,7 +523,8 @@ struct Exec {
         a.ksz = 1; a.stride = L.stride; a.pad = 0;
         a.K = L.K; a.Kp = L.Kp;
         a.relu = 0;
-        a.nhwc = g->nhwc;
+        a.in_nhwc = lay(L.in.Cp());
+        a.nhwc = lay(L.out.C);
         a.dbg = g->conv_dbg;
         prof_begin(DYCL_K_CONV, cnt, 2.0 * L.in.row_elems() + (o.f >= 0 ? 6.0 : 2.0) * L.out.row_elems(),
                    2.0 * L.out.H * L.out.W * L.out.C * (double)L.in.C, 2.0 * L.out.C * L.Kp);
@@ -554,7 +558,9 @@ struct Exec {
       a.res_mode = L.res_mode;
       a.rH = L.res_shape.H; a.rW = L.res_shape.W; a.rC = L.res_shape.Cp();
       a.r_pad_lo = (L.out.C - L.res_shape.C) / 2;
-      a.nhwc = g->nhwc;
+      a.in_nhwc = lay(L.in.Cp());
+      a.nhwc = lay(L.out.C);
+      a.res_nhwc = lay(L.res_shape.Cp());
       double fused_b = 0.0, fused_f = 0.0;
       if (L.fuse_proj) {               // [t | x] x [W | W_proj]: no projection tensor, no shortcut read
         const Layer& Pj = s.layers[li - 1];
@@ -575,6 +581,7 @@ struct Exec {
         a.ksz = 3; a.stride = 1; a.pad = 1;
         a.K = a.Kp = 9 * 64;
         a.w_rt = nullptr;
+        a.in_nhwc = a.nhwc = 1;
       }
       a.dbg = g->conv_dbg;
       const double res_b = a.res_mode ? (a.res32 ? 4.0 : 2.0) * L.res_shape.row_elems() *
@@ -607,7 +614,7 @@ struct Exec {
     a.K = D.cout;
     a.kind = kind;
     a.thr = thr;
-    a.nhwc = g->nhwc;
+    a.nhwc = lay(s.in.Cp());
     if (D.d_wt && kind != 1 && g->d_gpool) {
       a.wt = D.d_wt;
       a.gpool = g->d_gpool;
@@ -660,6 +667,7 @@ struct Exec {
       a.mode = mode;
       a.H = sh.H; a.W = sh.W; a.C = sh.Cp();
       a.row_elems_dst = mode == 0 ? sh.row_elems() : (long long)(sh.H / 2) * (sh.W / 2) * 2 * sh.Cp();
+      a.dst_nhwc = mode == 1 && lay(2 * sh.Cp());
       const double eb = a.elem_bytes;
       prof_begin(DYCL_K_GATHER, count, eb * (mode == 0 ? a.row_elems_src : a.row_elems_dst / 2) + eb * a.row_elems_dst,
                  0, 0);
@@ -1052,16 +1060,18 @@ dycl_status dycl_finalize(dycl_graph g, int64_t max_batch) {
   // option-A skip copy; channel-planar otherwise (the CIFAR-width kernels).
   {
     bool any = false, ok = g->input.Cp() == 8;
+    // per-tensor rule (Exec::lay): C % 64 == 0 tensors are NHWC; a conv reading one runs on the
+    // im2col GEMM, so its output width must be a multiple of 64 too (else: planar graph)
     for (size_t i = 0; i < g->subnets.size() && ok; ++i)
       if (planned[i])
         for (const Layer& L : g->subnets[i].layers)
-          if ((L.kind == L_CONV || L.kind == L_PROJ) && L.in.Cp() > 8) {
+          if ((L.kind == L_CONV || L.kind == L_PROJ) && L.in.Cp() % 64 == 0 && !(L.in.H == 1 && L.in.W == 1)) {
             any = true;
-            ok = ok && L.in.C % 64 == 0 && L.out.C % 64 == 0 && L.res_mode != 2;
+            ok = ok && L.out.C % 64 == 0 && (L.res_mode != 2 || (L.res_shape.Cp() % 4 == 0));
           }
-    for (const Node& N : g->nodes) ok = ok && !(N.kind == N_GATE && N.skip_mode == 1);
     const char* env = getenv("DYCL_NHWC");
-    g->nhwc = any && ok && !(env && atoi(env) == 0);
+    g->nhwc = ok && !(env && atoi(env) == 0);
+    (void)any;
     // space-to-depth stem: the first layer run is a 7x7 / stride-2 / pad-3 conv on <= 4 input
     // channels followed by a 3x3 / stride-2 / pad-1 max pool (the ImageNet ResNet stem)
     g->stem_s4d = 0;
@@ -1262,7 +1272,7 @@ dycl_status dycl_debug_conv2d(dycl_graph g, int64_t n, int H, int W, int C, cons
   a.rH = 2 * Ho; a.rW = 2 * Wo; a.rC = c_out / 2; a.r_pad_lo = c_out / 4;
   if (res_mode == 1) { a.rH = Ho; a.rW = Wo; a.rC = c_out; a.r_pad_lo = 0; }
   if (path == 2 && dwr) a.dbg |= 32;          // path 2 exercises the row-tap mode where eligible
-  a.nhwc = path == 4;                         // path 4: NHWC tensors, im2col GEMM (8-channel stem: planar kernels)
+  a.nhwc = a.in_nhwc = a.res_nhwc = path == 4;   // path 4: NHWC tensors, im2col GEMM (8-channel stem: planar kernels)
   cudaError_t e = n > 0 ? dycl::launch_conv(a, (int)n, g->num_sms, 0, path == 3 ? 2 : path == 4 ? 0 : path)
                         : cudaSuccess;
   if (e == cudaSuccess) e = cudaDeviceSynchronize();

@@ -51,6 +51,8 @@ constexpr int EPI_WG = EPI_RES + EPI_O32 + EPI_O16;
 struct GemmPlan {
   int stages;      // mainloop ring depth
   int staged;      // 1: epilogue through SMEM + TMA stores (and TMA residual loads)
+  int bres;        // 1: all weights resident in SMEM (single N tile, loaded once per CTA); the
+                   //    ring then carries only A tiles (cuts L2->SMEM bytes by B/(A+B) per tile)
 };
 
 __device__ __forceinline__ void tma_im2col_4d(uint32_t dst, const void* tmap, uint32_t bar, int c, int w, int h, int n,
@@ -83,15 +85,17 @@ __global__ void __launch_bounds__(THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + S * G::A_BYTES;
-  uint8_t* sE = sB + S * G::B_BYTES;                       // [2 WG][res | o32 | o16] when staged
+  uint8_t* sB = smem + S * G::A_BYTES;                     // ring B tiles, or [kblocks][BN][128 B] resident
+  const int b_slots = pl.bres ? a.Kp / BKE : S;
+  uint8_t* sE = sB + b_slots * G::B_BYTES;                  // [2 WG][res | o32 | o16] when staged
   uint64_t* bars = reinterpret_cast<uint64_t*>(sE + (pl.staged ? 2 * EPI_WG : 0));
   const uint32_t full0 = ptx::smem_u32(bars);
   const uint32_t empty0 = full0 + 8 * S;
   const uint32_t tfull0 = empty0 + 8 * S;
   const uint32_t tempty0 = tfull0 + 16;
   const uint32_t rbar0 = tempty0 + 16;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 6);
+  const uint32_t bfull = rbar0 + 16;                       // resident weights landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 7);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_live = a.n_live ? *a.n_live : a.n_static;
@@ -114,6 +118,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       ptx::mbar_init(tempty0 + 8 * i, 128);
       ptx::mbar_init(rbar0 + 8 * i, 1);
     }
+    ptx::mbar_init(bfull, 1);
     ptx::fence_mbar_init();
   }
   if (warp == 9) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), G::TMEM_COLS);
@@ -128,6 +133,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       ptx::tma_prefetch_desc(&tmA);
       ptx::tma_prefetch_desc(&tmB);
       if (a.x2) ptx::tma_prefetch_desc(&tmA2);
+      if (pl.bres) {
+        ptx::mbar_arrive_expect_tx(bfull, (uint32_t)(kblocks * G::B_BYTES));
+        for (int kb = 0; kb < kblocks; ++kb)
+          ptx::tma_load_2d(ptx::smem_u32(sB + kb * G::B_BYTES), &tmB, bfull, kb * BKE, 0);
+      }
+      const uint32_t stage_tx = pl.bres ? (uint32_t)G::A_BYTES : (uint32_t)G::STAGE;
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -143,13 +154,14 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int cb = 0; cb < cblocks; ++cb, ++kb) {
               ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1);
               const uint32_t bar = full0 + 8 * stage;
-              ptx::mbar_arrive_expect_tx(bar, (uint32_t)G::STAGE);
+              ptx::mbar_arrive_expect_tx(bar, stage_tx);
               const uint32_t da = ptx::smem_u32(sA + stage * G::A_BYTES);
               if (IM2COL)
                 tma_im2col_4d(da, &tmA, bar, cb * BKE, wb, hb, n0, (uint16_t)s, (uint16_t)r);
               else
                 ptx::tma_load_2d(da, &tmA, bar, cb * BKE, (int)p0);
-              ptx::tma_load_2d(ptx::smem_u32(sB + stage * G::B_BYTES), &tmB, bar, kb * BKE, n_tile * BN);
+              if (!pl.bres)
+                ptx::tma_load_2d(ptx::smem_u32(sB + stage * G::B_BYTES), &tmB, bar, kb * BKE, n_tile * BN);
               if (++stage == S) {
                 stage = 0;
                 phase ^= 1;
@@ -159,13 +171,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int cb = 0; kb < kblocks; ++cb, ++kb) {
           ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const uint32_t bar = full0 + 8 * stage;
-          ptx::mbar_arrive_expect_tx(bar, (uint32_t)G::STAGE);
+          ptx::mbar_arrive_expect_tx(bar, stage_tx);
           const uint32_t da = ptx::smem_u32(sA + stage * G::A_BYTES);
           if (a.stride2 > 1)
             tma_im2col_4d(da, &tmA2, bar, cb * BKE, wo0 * a.stride2, ho0 * a.stride2, n0, 0, 0);
           else
             ptx::tma_load_2d(da, &tmA2, bar, cb * BKE, (int)p0);
-          ptx::tma_load_2d(ptx::smem_u32(sB + stage * G::B_BYTES), &tmB, bar, kb * BKE, n_tile * BN);
+          if (!pl.bres)
+            ptx::tma_load_2d(ptx::smem_u32(sB + stage * G::B_BYTES), &tmB, bar, kb * BKE, n_tile * BN);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -176,6 +189,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t IDESC = ptx::make_idesc_bf16(BM, BN);
+    if (pl.bres) ptx::mbar_wait(bfull, 0);
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
@@ -188,7 +202,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         ptx::mbar_wait(full0 + 8 * stage, phase);
         ptx::tc_fence_after();
         const uint64_t ad = ptx::make_smem_desc_sw128(ptx::smem_u32(sA + stage * G::A_BYTES));
-        const uint64_t bd = ptx::make_smem_desc_sw128(ptx::smem_u32(sB + stage * G::B_BYTES));
+        const uint64_t bd = ptx::make_smem_desc_sw128(ptx::smem_u32(sB + (pl.bres ? kb : stage) * G::B_BYTES));
 #pragma unroll
         for (int j = 0; j < BKE / 16; ++j)
           ptx::mma_bf16_ss_elect(d, ad + (uint64_t)(2 * j), bd + (uint64_t)(2 * j), IDESC, (uint32_t)((kb | j) != 0));
@@ -294,6 +308,30 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) f[j] += rf[j];
           if (c0 + 32 < BN) load_res_g(c0 + 32);            // next chunk's shortcut in flight
+        }
+        if (a.res_mode == 2 && ok) {
+          // option A: shortcut = block input pixel (2ho, 2wo), channel o - r_pad_lo, zero outside
+          // [0, rC); r_pad_lo and rC are multiples of 4, so every 4-channel group is all in or out
+          const long long nn = m / HWo;
+          const int pp = (int)(m - nn * HWo), ho = pp / a.Wo, wo = pp - (pp / a.Wo) * a.Wo;
+          const size_t rpix = (size_t)(2 * ho) * a.rW + 2 * wo;
+#pragma unroll
+          for (int g4 = 0; g4 < 8; ++g4) {
+            const int ci = col0 + c0 + 4 * g4 - a.r_pad_lo;
+            if (ci < 0 || ci + 4 > a.rC) continue;
+            float4 q;
+            if (a.res32) {
+              q = __ldg(reinterpret_cast<const float4*>(a.res32 + ((size_t)nn * a.rH * a.rW + rpix) * a.rC + ci));
+            } else {
+              const uint16_t* rp = a.res_nhwc ? a.res + ((size_t)nn * a.rH * a.rW + rpix) * a.rC + ci
+                                              : a.res + (size_t)nn * a.rC * a.rH * a.rW +
+                                                    (size_t)(ci >> 3) * a.rH * a.rW * 8 + rpix * 8 + (ci & 7);
+              const uint2 u = __ldg(reinterpret_cast<const uint2*>(rp));
+              q = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u),
+                              __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xFFFF0000u));
+            }
+            f[4 * g4] += q.x; f[4 * g4 + 1] += q.y; f[4 * g4 + 2] += q.z; f[4 * g4 + 3] += q.w;
+          }
         }
         if (a.relu) {
 #pragma unroll
@@ -436,7 +474,10 @@ cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t 
   const int avail_staged = SMEM_LIMIT - SMEM_MISC - 2 * EPI_WG;
   pl.staged = heavy && avail_staged / CG<BN>::STAGE >= 2 && !(a.dbg & 128);
   const int avail = pl.staged ? avail_staged : SMEM_LIMIT - SMEM_MISC;
-  pl.stages = avail / CG<BN>::STAGE;
+  // resident weights: one N tile whose K blocks all fit beside >= 3 A stages
+  pl.bres = a.Cout == BN && kblocks > 1 && avail - kblocks * CG<BN>::B_BYTES >= 3 * CG<BN>::A_BYTES &&
+            !(a.dbg & 256);
+  pl.stages = pl.bres ? (avail - kblocks * CG<BN>::B_BYTES) / CG<BN>::A_BYTES : avail / CG<BN>::STAGE;
   if (pl.stages > MAX_STAGES) pl.stages = MAX_STAGES;
   if (pl.stages > kblocks + 1 && kblocks >= 1) pl.stages = kblocks + 1 > 2 ? kblocks + 1 : 2;
   tmR = tmY32 = tmY16 = tmB;
@@ -455,7 +496,8 @@ cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t 
                       CU_TENSOR_MAP_SWIZZLE_64B))
       return cudaErrorInvalidValue;
   }
-  const int smem = SMEM_MISC + pl.stages * CG<BN>::STAGE + (pl.staged ? 2 * EPI_WG : 0);
+  const int smem = SMEM_MISC + pl.stages * CG<BN>::A_BYTES +
+                   (pl.bres ? kblocks : pl.stages) * CG<BN>::B_BYTES + (pl.staged ? 2 * EPI_WG : 0);
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_conv_gemm<BN, IM2COL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -483,8 +525,9 @@ bool conv_gemm_eligible(const ConvArgs& a) {
   if (a.x2 && (a.C2 % BKE || a.stride2 < 1 || a.stride2 > 8 || (a.H2 - 1) / a.stride2 + 1 != a.Ho ||
                (a.W2 - 1) / a.stride2 + 1 != a.Wo))
     return false;
+  if (a.res_mode == 2 && (a.r_pad_lo % 4 || a.rC % 4 || a.rH < 2 * a.Ho || a.rW < 2 * a.Wo)) return false;
   return a.nhwc && a.C % BKE == 0 && a.Cout % 64 == 0 && a.K == a.ksz * a.ksz * a.C + k2 && a.Kp == a.K &&
-         a.res_mode != 2 && a.pad <= 32 && a.stride <= 8 && (a.ksz > 1 || a.stride > 1 || a.H == a.Ho);
+         a.pad <= 32 && a.stride <= 8 && (a.ksz > 1 || a.stride > 1 || a.H == a.Ho);
 }
 
 cudaError_t launch_conv_gemm(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream) {

@@ -693,12 +693,15 @@ cudaError_t launch_conv_tma(const ConvArgs& a, int max_rows, int num_sms, cudaSt
 }
 
 cudaError_t launch_conv(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream, int path) {
-  if (a.nhwc) {
-    // NHWC graphs: the im2col GEMM for every C % 64 layer; the 8-channel stem (planar == NHWC
-    // at C = 8) keeps the planar kernels, whose epilogue writes NHWC.
-    if (conv_gemm_eligible(a)) return launch_conv_gemm(a, max_rows, num_sms, stream);
-    if (a.C != 8) return cudaErrorNotSupported;
+  if (a.in_nhwc) {
+    // NHWC input: the im2col GEMM (C, Cout % 64); a planar kernel only when the layouts coincide
+    // (8 channels, or 1x1 maps)
+    if (a.nhwc && conv_gemm_eligible(a)) return launch_conv_gemm(a, max_rows, num_sms, stream);
+    if (a.C != 8 && !(a.H == 1 && a.W == 1)) return cudaErrorNotSupported;
   }
+  // planar-input kernels: their epilogue writes y in the layout a.nhwc selects; an option-A
+  // bf16 shortcut must be planar for them
+  if (a.res_mode == 2 && a.res32 == nullptr && a.res_nhwc) return cudaErrorNotSupported;
   if (path != 1 && gemm_tma_eligible(a) && (a.dbg & 64) == 0) return launch_gemm_tma(a, max_rows, num_sms, stream);
   if (path != 1) {
     bool handled = false;

@@ -328,6 +328,22 @@ __global__ void __launch_bounds__(256) k_gather(const GatherArgs a) {
       for (int k = 0; k < 4; ++k)
         if (di[k] >= 0) dst[di[k]] = v[k];
     }
+  } else if (a.elem_bytes == 2 && a.dst_nhwc) {
+    // option A, bf16 channel-planar src [C/8][H][W][8] -> NHWC dst [H/2][W/2][2C] (2C % 64 == 0)
+    const int Wo = a.W / 2, gpp = 2 * a.C / 8, pad = a.C / 2;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total; u += stride) {
+      const int64_t j = u / U;
+      const int64_t r = u - j * U;
+      const int p = (int)(r / gpp), q = (int)(r - (int64_t)p * gpp);
+      const int ho = p / Wo, wo = p - ho * Wo;
+      const int cs = q * 8 - pad;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (cs >= 0 && cs < a.C) {
+        const int64_t e = (int64_t)a.list[j] * a.row_elems_src + ((int64_t)(cs / 8) * a.H * a.W + (2 * ho) * a.W + 2 * wo) * 8;
+        v = __ldg(src + e / 8);
+      }
+      dst[(off + j) * U + r] = v;
+    }
   } else if (a.elem_bytes == 2) {
     // option A, bf16 channel-planar: dst [2C/8][H/2][W/2][8] from src [C/8][H][W][8]
     const int Ho = a.H / 2, Wo = a.W / 2, HWo = Ho * Wo, padp = a.C / 16;   // C/2 channels = C/16 planes

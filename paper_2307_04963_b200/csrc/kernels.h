@@ -27,7 +27,9 @@ struct ConvArgs {
   int relu;
   int res_mode;          // 0 none, 1 identity [n][Ho][Wo][Cout], 2 option A from [n][rH][rW][rC]
   int rH, rW, rC, r_pad_lo;
-  int nhwc = 0;          // 1: bf16 tensors (x, y, res) are NHWC [n][H][W][C] instead of channel-planar
+  int res_nhwc = 0;      // option-A bf16 shortcut tensor is NHWC (else channel-planar)
+  int nhwc = 0;          // 1: bf16 output y and identity shortcut res are NHWC [n][H][W][C] (else channel-planar)
+  int in_nhwc = 0;       // 1: bf16 input x is NHWC (the im2col GEMM); 0: channel-planar (planar kernels)
   // conv_gemm only: a second A operand concatenated along K (the fused projection shortcut of a
   // bottleneck block: D = conv1x1(x) + proj1x1/stride2(x2)); w is then [Cout][K + C2]
   const uint16_t* x2 = nullptr;   // bf16 NHWC [n][H2][W2][C2]
@@ -123,6 +125,7 @@ struct GatherArgs {
   int64_t row_elems_src;   // elements per src row
   int64_t row_elems_dst;
   int mode, H, W, C;
+  int dst_nhwc = 0;        // mode 1, bf16: destination NHWC (else channel-planar)
 };
 cudaError_t launch_gather(const GatherArgs& a, int max_rows, int num_sms, cudaStream_t s);
 

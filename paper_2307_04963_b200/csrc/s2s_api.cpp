@@ -7,6 +7,8 @@
 // process exactly the active rows.  KV caches stay in slot order (rows carry their slot).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -47,6 +49,28 @@ struct dycl_s2s_s {
   uint8_t* flag = nullptr;
   int32_t *src_stage = nullptr, *tok_stage = nullptr, *len_stage = nullptr;
   int launches = 0;
+  // CUDA graph of one whole run (encoder + the max_len guarded decode steps, ~4.5k kernels):
+  // captured on first use for an (io pointers, batch) key, replayed on the caller's stream.
+  // Every kernel reads its live row count from device memory, so the captured sequence is
+  // valid for any data; only the pointers and the batch are baked in.
+  bool use_graph = true;             // DYCL_S2S_GRAPH=0 disables
+  // per-launch profiling (graph off while enabled)
+  struct Rec {
+    int kind;
+    cudaEvent_t e0, e1;
+    const int* cnt;                  // device live-row count, or nullptr -> rows
+    int rows;
+    double bpr, fpr, bfix;           // algorithmic bytes / flops per row, fixed bytes
+  };
+  bool profiling = false;
+  std::vector<Rec> prof;
+  size_t prof_used = 0;
+  cudaStream_t prof_stream = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  const void* gkey[6] = {};
+  int64_t gbatch = -1;
+  int glaunches = 0;
 };
 
 static thread_local std::string g_s2s_err;
@@ -114,6 +138,24 @@ struct S2SExec {
   int B;
   int n = 0;
 
+  void pb(int kind, const int* cnt, int rows, double bpr, double fpr, double bfix) {
+    if (!s->profiling) return;
+    if (s->prof_used >= s->prof.size()) {
+      dycl_s2s_s::Rec r{};
+      cudaEventCreate(&r.e0);
+      cudaEventCreate(&r.e1);
+      s->prof.push_back(r);
+    }
+    dycl_s2s_s::Rec& r = s->prof[s->prof_used];
+    r.kind = kind; r.cnt = cnt; r.rows = rows; r.bpr = bpr; r.fpr = fpr; r.bfix = bfix;
+    cudaEventRecord(r.e0, st);
+  }
+  void pe() {
+    if (!s->profiling) return;
+    cudaEventRecord(s->prof[s->prof_used].e1, st);
+    ++s->prof_used;
+  }
+
   // y = act(x W^T + b [+ res]) on rows [0, *cnt) through the tcgen05 GEMM path (a dense
   // layer = 1x1 conv on [rows][1][1][K]).
   cudaError_t gemm(const uint16_t* x, int K, const uint16_t* w, const float* b, int N, const float* res32,
@@ -125,12 +167,20 @@ struct S2SExec {
     a.K = K; a.Kp = K; a.relu = relu;
     a.rH = a.rW = 1; a.rC = N;
     ++n;
-    return dycl::launch_conv(a, max_rows, s->num_sms, st, 0);
+    pb(DYCL_K_GEMM, cnt, n_static, 2.0 * K + (yb ? 2.0 * N : 0.0) + (y32 ? 4.0 * N : 0.0) + (res32 ? 4.0 * N : 0.0),
+       2.0 * K * N, 2.0 * K * N);
+    const cudaError_t e = dycl::launch_conv(a, max_rows, s->num_sms, st, 0);
+    pe();
+    return e;
   }
   cudaError_t ln(const float* in, const float* g, const float* b, const int* cnt, int n_static, int max_rows) {
     dycl::S2SLnArgs a{in, g, b, s->x32, s->xb, cnt, n_static, s->c.d_model, 1e-5f};
     ++n;
-    return dycl::launch_layernorm(a, max_rows, st);
+    const double d = s->c.d_model;
+    pb(DYCL_K_LN, cnt, n_static, 4.0 * d + 6.0 * d, 8.0 * d, 8.0 * d);
+    const cudaError_t e = dycl::launch_layernorm(a, max_rows, st);
+    pe();
+    return e;
   }
 
   dycl_status run(const int32_t* src, int32_t* tokens, int32_t* lengths, float* top1, float* logits0) {
@@ -143,17 +193,23 @@ struct S2SExec {
     if (e != cudaSuccess) return sfail(s, DYCL_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e)); \
   } while (0)
     dycl::S2SInitArgs ia{tokens, top1, s->cur_tok, lengths, s->active[0], s->counts, B, c.max_len, c.pad, c.bos};
+    pb(DYCL_K_INIT, nullptr, B, 4.0 * (c.max_len + 3), 0, 0);
     E(dycl::launch_s2s_init(ia, st));
+    pe();
     ++n;
     // ---------------- encoder sub-network (once), rows = B*S tokens
     dycl::S2SEmbedArgs ea{s->src_emb, src, nullptr, nullptr, s->x32, s->xb, nullptr, R, d, S, 0};
+    pb(DYCL_K_EMBED, nullptr, R, 4.0 + 2.0 * d + 6.0 * d, 0, 0);
     E(dycl::launch_embed(ea, R, st));
+    pe();
     ++n;
     for (const DevLayer& L : s->enc) {
       E(gemm(s->xb, d, L.wqkv, L.bqkv, 3 * d, nullptr, s->qkv, nullptr, 0, nullptr, R, R));
       dycl::S2SAttnArgs aa{};
       aa.qkv = s->qkv; aa.out = s->att; aa.n_static = B; aa.d = d; aa.heads = c.heads; aa.S = S;
+      pb(DYCL_K_ATTN, nullptr, B, (double)S * (3.0 * d * 2 + 2.0 * d), 4.0 * S * S * d, 0);
       E(dycl::launch_attn_encoder(aa, B, st));
+      pe();
       ++n;
       E(gemm(s->att, d, L.wo, L.bo, d, s->x32, nullptr, s->pre, 0, nullptr, R, R));
       E(ln(s->pre, L.lsg, L.lsb, nullptr, R, R));
@@ -170,7 +226,9 @@ struct S2SExec {
     for (int t = 0; t < c.max_len; ++t) {
       const int32_t* slot = s->active[cur];
       dycl::S2SEmbedArgs de{s->tgt_emb, nullptr, slot, s->cur_tok, s->x32, s->xb, cnt, 0, d, S, t};
+      pb(DYCL_K_EMBED, cnt, 0, 8.0 + 2.0 * d + 6.0 * d, 0, 0);
       E(dycl::launch_embed(de, B, st));
+      pe();
       ++n;
       for (size_t l = 0; l < s->dec.size(); ++l) {
         const DevLayer& L = s->dec[l];
@@ -179,7 +237,9 @@ struct S2SExec {
         sa.qkv = s->qkv; sa.q = s->qkv; sa.q_stride = 3 * d; sa.kv = nullptr; sa.cache = s->cache[l];
         sa.out = s->att; sa.slot = slot; sa.n_live = cnt; sa.d = d; sa.heads = c.heads; sa.S = S;
         sa.max_len = c.max_len; sa.t = t;
+        pb(DYCL_K_ATTN, cnt, 0, (t + 1.0) * 2 * d * 2 + 3.0 * d * 2 + 2.0 * d * 2 + 2.0 * d * 2, 4.0 * (t + 1) * d, 0);
         E(dycl::launch_attn_decoder(sa, B, st));
+        pe();
         ++n;
         E(gemm(s->att, d, L.wo, L.bo, d, s->x32, nullptr, s->pre, 0, cnt, 0, B));
         E(ln(s->pre, L.lsg, L.lsb, cnt, 0, B));
@@ -187,7 +247,9 @@ struct S2SExec {
         dycl::S2SAttnArgs ca{};
         ca.q = s->att; ca.q_stride = d; ca.kv = s->cross[l]; ca.out = s->qkv;  // reuse qkv as scratch
         ca.slot = slot; ca.n_live = cnt; ca.d = d; ca.heads = c.heads; ca.S = S; ca.max_len = c.max_len; ca.t = t;
+        pb(DYCL_K_ATTN, cnt, 0, (double)S * 2 * d * 2 + 2.0 * d * 2 + 2.0 * d * 2, 4.0 * S * d, 0);
         E(dycl::launch_attn_decoder(ca, B, st));
+        pe();
         ++n;
         E(gemm(s->qkv, d, L.wo2, L.bo2, d, s->x32, nullptr, s->pre, 0, cnt, 0, B));
         E(ln(s->pre, L.lcg, L.lcb, cnt, 0, B));
@@ -198,12 +260,16 @@ struct S2SExec {
       E(gemm(s->xb, d, s->lm_w, s->lm_b, c.vocab, nullptr, nullptr, s->logits, 0, cnt, 0, B));
       dycl::S2SArgmaxArgs ga{s->logits, slot, src, s->len_table, s->beta, tokens, top1, logits0,
                              s->cur_tok, lengths, s->flag, cnt, c.vocab, S, c.max_len, t, c.eos};
+      pb(DYCL_K_ARGMAX, cnt, 0, 4.0 * c.vocab + 16.0, 2.0 * c.vocab, 0);
       E(dycl::launch_argmax_guard(ga, B, st));
+      pe();
       ++n;
       // the logic node's decision -> stable compaction of the still-active sequences
       int* out_counts = s->counts + 1 + 2 * t;
+      pb(DYCL_K_COMPACT, cnt, 0, 1.0 + 12.0, 0, 0);
       E(dycl::launch_compact(s->flag, cnt, slot, s->list1, s->list0, out_counts, s->active[cur ^ 1], 0,
                              nullptr, 0, st));
+      pe();
       ++n;
       cnt = out_counts + 1;
       cur ^= 1;
@@ -235,6 +301,7 @@ dycl_status dycl_s2s_create(int cuda_device, const dycl_s2s_config* cfg, dycl_s2
   if (!s) return sfail(nullptr, DYCL_E_OOM, "host allocation");
   s->c = *cfg;
   s->device = cuda_device;
+  if (const char* eg = getenv("DYCL_S2S_GRAPH")) s->use_graph = atoi(eg) != 0;
   cudaSetDevice(cuda_device);
   cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
   *out = s;
@@ -244,6 +311,12 @@ dycl_status dycl_s2s_create(int cuda_device, const dycl_s2s_config* cfg, dycl_s2
 dycl_status dycl_s2s_destroy(dycl_s2s s) {
   if (!s) return DYCL_OK;
   cudaSetDevice(s->device);
+  if (s->gexec) cudaGraphExecDestroy(s->gexec);
+  for (auto& r : s->prof) {
+    cudaEventDestroy(r.e0);
+    cudaEventDestroy(r.e1);
+  }
+  if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
   for (void* p : s->allocs) cudaFree(p);
   delete s;
   return DYCL_OK;
@@ -327,10 +400,46 @@ dycl_status dycl_s2s_run(dycl_s2s s, const int32_t* src, int64_t batch, int32_t*
   if (!src || !tokens || !lengths) return sfail(s, DYCL_E_INVALID_ARG, "null io pointer");
   SCK(cudaSetDevice(s->device));
   SCK(cudaGetLastError());
-  S2SExec ex{s, (cudaStream_t)stream, (int)batch};
-  dycl_status r = ex.run(src, tokens, lengths, top1, logits0);
-  s->launches = ex.n;
-  return r;
+  if (!s->use_graph || s->profiling) {
+    s->prof_used = 0;
+    s->prof_stream = (cudaStream_t)stream;
+    S2SExec ex{s, (cudaStream_t)stream, (int)batch};
+    dycl_status r = ex.run(src, tokens, lengths, top1, logits0);
+    s->launches = ex.n;
+    return r;
+  }
+  const void* key[6] = {src, tokens, lengths, top1, logits0, nullptr};
+  bool hit = s->gexec && s->gbatch == batch;
+  for (int i = 0; i < 6 && hit; ++i) hit = key[i] == s->gkey[i];
+  if (!hit) {
+    if (s->gexec) {
+      cudaGraphExecDestroy(s->gexec);
+      s->gexec = nullptr;
+    }
+    if (!s->cap_stream) SCK(cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
+    SCK(cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal));
+    S2SExec ex{s, s->cap_stream, (int)batch};
+    dycl_status r = ex.run(src, tokens, lengths, top1, logits0);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(s->cap_stream, &graph);
+    if (r != DYCL_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return r;
+    }
+    if (ec != cudaSuccess) return sfail(s, DYCL_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(ec));
+    const cudaError_t ei = cudaGraphInstantiate(&s->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) {
+      s->gexec = nullptr;
+      return sfail(s, DYCL_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei));
+    }
+    for (int i = 0; i < 6; ++i) s->gkey[i] = key[i];
+    s->gbatch = batch;
+    s->glaunches = ex.n;
+  }
+  SCK(cudaGraphLaunch(s->gexec, (cudaStream_t)stream));
+  s->launches = s->glaunches;
+  return DYCL_OK;
 }
 
 dycl_status dycl_s2s_run_host(dycl_s2s s, const int32_t* src_host, int64_t batch, int32_t* tokens_host,
@@ -354,6 +463,35 @@ dycl_status dycl_s2s_run_host(dycl_s2s s, const int32_t* src_host, int64_t batch
   SCK(cudaMemcpyAsync(tokens_host, s->tok_stage, (size_t)batch * s->c.max_len * 4, cudaMemcpyDeviceToHost, st));
   SCK(cudaMemcpyAsync(lengths_host, s->len_stage, (size_t)batch * 4, cudaMemcpyDeviceToHost, st));
   SCK(cudaStreamSynchronize(st));
+  return DYCL_OK;
+}
+
+dycl_status dycl_s2s_set_profiling(dycl_s2s s, int enable) {
+  if (!s) return DYCL_E_INVALID_ARG;
+  s->profiling = enable != 0;
+  return DYCL_OK;
+}
+
+dycl_status dycl_s2s_profile_read(dycl_s2s s, int32_t max_n, int32_t* kind, float* ms, double* bytes, double* flops,
+                                  int32_t* n_out) {
+  if (!s || !n_out) return DYCL_E_INVALID_ARG;
+  SCK(cudaSetDevice(s->device));
+  SCK(cudaStreamSynchronize(s->prof_stream));
+  const int nslot = 1 + 2 * s->c.max_len;
+  std::vector<int> counts(nslot, 0);
+  if (s->counts) SCK(cudaMemcpy(counts.data(), s->counts, nslot * sizeof(int), cudaMemcpyDeviceToHost));
+  const int n = (int)std::min<size_t>(s->prof_used, (size_t)std::max(max_n, 0));
+  for (int i = 0; i < n; ++i) {
+    const dycl_s2s_s::Rec& r = s->prof[i];
+    float t = 0.f;
+    SCK(cudaEventElapsedTime(&t, r.e0, r.e1));
+    const double rows = r.cnt ? (double)counts[r.cnt - s->counts] : (double)r.rows;
+    if (kind) kind[i] = r.kind;
+    if (ms) ms[i] = t;
+    if (bytes) bytes[i] = rows * r.bpr + r.bfix;
+    if (flops) flops[i] = rows * r.fpr;
+  }
+  *n_out = (int32_t)s->prof_used;
   return DYCL_OK;
 }
 

@@ -17,7 +17,8 @@ LIB_PATH = os.path.join(HERE, "libdycl.so")
 
 DYCL_ACT_NONE = 0
 DYCL_ACT_RELU = 1
-KIND_NAMES = {0: "input", 1: "conv", 2: "head", 3: "compact", 4: "gather", 5: "scatter", 6: "init", 7: "pool"}
+KIND_NAMES = {0: "input", 1: "conv", 2: "head", 3: "compact", 4: "gather", 5: "scatter", 6: "init", 7: "pool",
+              8: "block", 9: "gemm", 10: "attn", 11: "ln", 12: "argmax", 13: "embed"}
 
 _STATUS = {0: "DYCL_OK", -1: "DYCL_E_INVALID_ARG", -2: "DYCL_E_SHAPE_MISMATCH", -3: "DYCL_E_SIGNATURE",
            -4: "DYCL_E_SHAPE_JOIN", -5: "DYCL_E_STATE", -6: "DYCL_E_UNSUPPORTED", -7: "DYCL_E_OOM",
@@ -51,6 +52,7 @@ EXPORTS = [
     "dycl_s2s_create", "dycl_s2s_destroy", "dycl_s2s_last_error", "dycl_s2s_set_embeddings",
     "dycl_s2s_add_encoder_layer", "dycl_s2s_add_decoder_layer", "dycl_s2s_set_lm_head", "dycl_s2s_set_loop_guard",
     "dycl_s2s_finalize", "dycl_s2s_run", "dycl_s2s_run_host", "dycl_s2s_launches",
+    "dycl_s2s_set_profiling", "dycl_s2s_profile_read",
     "dycl_graph_create", "dycl_graph_set_precision", "dycl_graph_destroy", "dycl_last_error", "dycl_subnet_begin", "dycl_subnet_block_begin",
     "dycl_subnet_conv2d", "dycl_subnet_dense", "dycl_subnet_gap", "dycl_subnet_projection", "dycl_subnet_maxpool", "dycl_subnet_end", "dycl_seq", "dycl_exit",
     "dycl_gate", "dycl_final", "dycl_finalize", "dycl_run", "dycl_run_host", "dycl_num_count_slots",
@@ -111,6 +113,8 @@ def lib():
             "dycl_s2s_run": [vp, vp, i64, vp, vp, vp, vp, vp],
             "dycl_s2s_run_host": [vp, vp, i64, vp, vp, vp],
             "dycl_s2s_launches": [vp, Pi],
+            "dycl_s2s_set_profiling": [vp, i32],
+            "dycl_s2s_profile_read": [vp, i32, Pi, Pf, Pd, Pd, Pi],
         })
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -373,6 +377,21 @@ def dycl_s2s_run_host(s, src_host, batch, tokens_host, lengths_host, stream=None
         return ctypes.c_void_p(t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data)
     _s2s_ck(lib().dycl_s2s_run_host(s, p(src_host), int(batch), p(tokens_host), p(lengths_host),
                                     _stream_ptr(stream)), s)
+
+
+def dycl_s2s_set_profiling(s, enable):
+    _s2s_ck(lib().dycl_s2s_set_profiling(s, int(bool(enable))), s)
+
+
+def dycl_s2s_profile_read(s, max_n=8192):
+    kind = (ctypes.c_int32 * max_n)()
+    ms = (ctypes.c_float * max_n)()
+    by = (ctypes.c_double * max_n)()
+    fl = (ctypes.c_double * max_n)()
+    n = ctypes.c_int32()
+    _s2s_ck(lib().dycl_s2s_profile_read(s, max_n, kind, ms, by, fl, ctypes.byref(n)), s)
+    m = min(n.value, max_n)
+    return [dict(kind=KIND_NAMES[kind[i]], ms=ms[i], bytes=by[i], flops=fl[i]) for i in range(m)]
 
 
 def dycl_s2s_launches(s) -> int:

@@ -23,12 +23,16 @@ raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_outpu
 rr = list(csv.reader(io.StringIO(raw)))
 if len(rr) > 2:
     h = rr[0]
-    for name in ["dram__bytes_read.sum", "dram__bytes_write.sum", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
-                 "sm__inst_executed_pipe_tensor.sum", "l1tex__t_bytes.sum", "lts__t_bytes.sum",
-                 "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active"]:
-        for i, col in enumerate(h):
-            if col.startswith(name):
-                print(f"  {col:60s} {rr[2][i]:>16s} {rr[1][i]}")
+    for ki in range(2, len(rr)):
+        kn = rr[ki][h.index("Kernel Name")] if "Kernel Name" in h else f"kernel {ki - 2}"
+        print(f"  [launch {ki - 2}] {kn[:90]}")
+        for name in ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+                     "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+                     "sm__inst_executed_pipe_tensor.sum", "l1tex__t_bytes.sum", "lts__t_bytes.sum",
+                     "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active"]:
+            for i, col in enumerate(h):
+                if col.startswith(name):
+                    print(f"    {col:60s} {rr[ki][i]:>16s} {rr[1][i]}")
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))

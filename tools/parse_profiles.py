@@ -34,6 +34,31 @@ if os.path.exists(f"{src}/launches.csv"):
     out["ncu_launch_list_total_us"] = round(tot, 1)
 # 2. conv DRAM traffic per launch vs the library's algorithmic bytes
 prof = json.load(open(f"{src}/step_profile.json")) if os.path.exists(f"{src}/step_profile.json") else []
+if os.path.exists(f"{src}/block_dram.csv"):
+    by_id = defaultdict(dict)
+    for r in rows(f"{src}/block_dram.csv"):
+        by_id[int(r["ID"])][r["Metric Name"]] = (float(r["Metric Value"].replace(",", "")), r["Metric Unit"])
+    blks = [p for p in prof if p["kind"] == "block"]
+    launches = []
+    for i, (k, m) in enumerate(sorted(by_id.items())):
+        rd = m["dram__bytes_read.sum"][0]
+        wr = m["dram__bytes_write.sum"][0]
+        t = m["gpu__time_duration.sum"]
+        t_us = t[0] * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3}.get(t[1], 1.0)
+        alg = blks[i]["bytes"] if i < len(blks) else None
+        launches.append({"launch": i, "dram_bytes": rd + wr, "algorithmic_bytes": alg, "ncu_us": t_us,
+                         "event_us": blks[i]["ms"] * 1e3 if i < len(blks) else None})
+    tot_dram = sum(l["dram_bytes"] for l in launches)
+    tot_alg = sum(l["algorithmic_bytes"] or 0 for l in launches)
+    out["block_dram"] = {"launches": len(launches), "dram_bytes_per_launch": tot_dram / len(launches),
+                         "algorithmic_bytes_per_launch": tot_alg / len(launches),
+                         "dram_over_algorithmic": tot_dram / tot_alg if tot_alg else None,
+                         "per_launch": launches}
+    json.dump({"kernel": "k_block_fused", "dram_bytes_per_launch": tot_dram / len(launches),
+               "algorithmic_bytes_per_launch": tot_alg / len(launches),
+               "source": f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over the {len(launches)} "
+                         f"k_block_fused launches of one cfg2 step (profiles/{tag}_profile.json)"},
+              open("profiles/block_traffic.json", "w"), indent=1)
 if os.path.exists(f"{src}/conv_dram.csv"):
     by_id = defaultdict(dict)
     for r in rows(f"{src}/conv_dram.csv"):
