@@ -109,6 +109,7 @@ struct dycl_graph_s {
   int conv_dbg = 0;                  // DYCL_CONV_DBG: timing experiments only (results invalid)
   int no_fuse = 0;                   // DYCL_NO_FUSE=1: run basic blocks as two conv launches
   int max_fuse = 2;                  // DYCL_MAX_FUSE: basic blocks per fused launch (1..2)
+  int no_inplace = 0;                // DYCL_NO_INPLACE=1: gates gather / merge instead of running in place
   int nhwc = 0;                      // bf16 activations NHWC (decided at finalize; DYCL_NHWC=0 disables)
   int stem_s4d = 0;                  // input cast to 4x4 space-to-depth for the stem (DYCL_STEM_S4D=0 disables)
   long long* dbg_ts = nullptr;       // DYCL_TS=1: fused-block phase timestamps (development)
@@ -727,6 +728,35 @@ struct Exec {
           if ((r = head(g->subnets[N.sn], cur, cnt, 1, N.thr))) return r;
           int s;
           if ((r = compact(cnt, 1, (int32_t)1 << N.ordinal, orig_cur, &s))) return r;
+          const Subnet& T = g->subnets[N.then_sn];
+          if (N.skip_mode == 0 && fp32_stream() && cur.f >= 0 && cur.b >= 0 && !g->no_fuse && !g->no_inplace &&
+              T.layers.size() == 3 && fusable(T, 0)) {
+            // in place (the slot-table form of the skip, P:L648 identity elimination): the
+            // executed rows' block output overwrites their own rows, skipped rows are not
+            // touched -- no gather, no merge, row order and orig unchanged
+            const Layer &c1 = T.layers[1], &c2 = T.layers[2];
+            dycl::BlockArgs ba{};
+            ba.x32 = g->buf32[cur.f];
+            ba.y32 = g->buf32[cur.f];
+            ba.yb = g->buf[cur.b];
+            ba.list = g->d_list1;
+            ba.list_out = 1;
+            ba.nblk = 1;
+            ba.w1_rt[0] = c1.d_wrt;
+            ba.w2_rt[0] = c2.d_wrt;
+            ba.b1[0] = c1.d_b;
+            ba.b2[0] = c2.d_b;
+            ba.n_live = g->d_counts + s;
+            ba.C = c1.in.C; ba.H = c1.in.H; ba.W = c1.in.W;
+            ba.ts = nullptr;
+            const double row_b = (4.0 + 4.0 + 2.0) * c1.in.row_elems();
+            const double row_f = 2.0 * 2.0 * c1.out.H * c1.out.W * c1.out.C * (double)(9 * c1.in.C);
+            prof_begin(DYCL_K_BLOCK, g->d_counts + s, row_b, row_f, 2.0 * 2 * 3 * c1.out.C * c1.Kp_rt);
+            cudaError_t e = dycl::launch_block_fused(ba, batch, g->num_sms, st);
+            prof_end();
+            if (e != cudaSuccess) return cuda_fail(g, e, "launch_block_fused (in place)");
+            break;
+          }
           Tensor bt = pick_tensor(false, {cur});
           bt.f = -1;
           Tensor in_t = cur;
@@ -787,6 +817,7 @@ dycl_status dycl_graph_create(int cuda_device, int in_h, int in_w, int in_c, dyc
   if (const char* cd = getenv("DYCL_CONV_DBG")) g->conv_dbg = atoi(cd);
   if (const char* nf = getenv("DYCL_NO_FUSE")) g->no_fuse = atoi(nf);
   if (const char* mf = getenv("DYCL_MAX_FUSE")) g->max_fuse = atoi(mf);
+  if (const char* ni = getenv("DYCL_NO_INPLACE")) g->no_inplace = atoi(ni);
   if (getenv("DYCL_TS")) {
     cudaMalloc(&g->dbg_ts, 8 * 16 * sizeof(long long));
     g->dbg_ts_pick = atoi(getenv("DYCL_TS")) > 1 ? atoi(getenv("DYCL_TS")) : 0;

@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int smp = blockIdx.x; smp < n_live; smp += gridDim.x, ++it) {
         const int b = it % G::NXB;
         const uint8_t* xs = x32s + (size_t)b * G::X32_BYTES;
-        const int dst = smp;                           // outputs are dense in row order
+        const int dst = a.list && a.list_out ? a.list[smp] : smp;   // dense order, or in place
         // store box by box as epilogue 2 finishes it (one bulk group per box) ...
 #pragma unroll
         for (int q = 0; q < G::NBOX; ++q) {

@@ -151,6 +151,7 @@ constexpr int MAX_FUSED_BLOCKS = 2;
 struct BlockArgs {
   const float* x32;        // fp32 NHWC [n][H][W][C] (the first block's input, also its shortcut)
   const int32_t* list;     // optional row index list (input row = list[i]), nullptr = identity
+  int list_out = 0;        // 1: output row = list[i] too (in place over x when y32 == x32)
   float* y32;              // fp32 NHWC [n][H][W][C]
   uint16_t* yb;            // bf16 channel-planar copy or nullptr
   int nblk;                // blocks fused in this launch (1..MAX_FUSED_BLOCKS)
