@@ -51,7 +51,7 @@ struct BCfg {
   static constexpr int W_BYTES = WCH * N * 16;
   static constexpr int BOX_ROWS = HW < 256 ? HW : 256;  // pixels per TMA box (box dims <= 256)
   static constexpr int NBOX = HW / BOX_ROWS;
-  static constexpr int FIXED = 1024 + 2 * OPER + 2 * NB * W_BYTES + 2 * NB * C * 4 + 512;
+  static constexpr int FIXED = 1024 + 2 * OPER + 2 * NB * W_BYTES + 2 * NB * C * 4 + 512 + 256;
   // fp32 sample buffers (2 if they fit: y is written in place over its own input x, which is
   // also the shortcut) and a separate bf16 output staging buffer if it fits
   static constexpr int NXB = FIXED + 2 * X32_BYTES <= 227 * 1024 ? 2 : 1;
@@ -151,7 +151,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t acc2 = tb_full + 8, acc1_empty = acc2 + 8, wfull = acc1_empty + 8, acc2_empty = wfull + 8;
   const uint32_t tb_free = acc2_empty + 8;             // the bf16-copy store has read T / ybs
   const uint32_t subfree0 = acc2_empty + 16;          // [NSUB] shared set: sub-tile j drained by epilogue 2
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26 + 2 * 4);
+  // per sub-tile j: conv1 / conv2 accumulator j complete (MMA commit), and tready[j] = epilogue 1
+  // has read accumulator j and written T rows of sub-tile j (conv2 sub-tile j needs j-1..j+1)
+  const uint32_t acc1j0 = ptx::smem_u32(bars + 34), acc2j0 = ptx::smem_u32(bars + 42), tready0 = ptx::smem_u32(bars + 50);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 58);
   static_assert(G::NBOX <= 4, "box barriers");
   static_assert(G::NSUB <= 8, "sub-tile barriers");
   constexpr uint32_t SET2 = G::NSETS == 2 ? 256u : 0u;    // TMEM column of the conv2 accumulator
@@ -165,7 +168,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int k = 0; k < G::NBOX; ++k) ptx::mbar_init(yready0 + 8 * (4 * i + k), 256);
     }
     ptx::mbar_init(tb_free, 1);
-    for (int j = 0; j < G::NSUB; ++j) ptx::mbar_init(subfree0 + 8 * j, 128);
+    for (int j = 0; j < G::NSUB; ++j) {
+      ptx::mbar_init(subfree0 + 8 * j, 128);
+      ptx::mbar_init(acc1j0 + 8 * j, 1);
+      ptx::mbar_init(acc2j0 + 8 * j, 1);
+      ptx::mbar_init(tready0 + 8 * j, 128);
+    }
     ptx::mbar_init(xb_full, 256);
     ptx::mbar_init(xb_empty, 1);
     ptx::mbar_init(acc1, 1);
@@ -275,16 +283,16 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t ph = k & 1;
         const uint64_t w1d = ptx::make_smem_desc(ptx::smem_u32(ws + (2 * blk) * G::W_BYTES), 0, G::N * 16, 128);
         const uint64_t w2d = ptx::make_smem_desc(ptx::smem_u32(ws + (2 * blk + 1) * G::W_BYTES), 0, G::N * 16, 128);
-        // conv1 accumulator free: drained by epilogue 1 (two sets) / per sub-tile by the previous
-        // epilogue 2 (shared set: conv1 of the next sample overlaps epilogue 2 of this one)
-        if (G::NSETS == 2) ptx::mbar_wait(acc1_empty, ph ^ 1);
+        // conv1 sub-tile j: its columns were drained by the previous epilogue 2 (shared set) or the
+        // previous epilogue 1 (two sets); committed per sub-tile so epilogue 1 starts on sub-tile 0
+        // while the tensor core works on the rest
         ptx::mbar_wait(xb_full, ph);                  // x operand: converted, or the previous block's y
         ptx::tc_fence_after();
         if (mstamp && blk == 0) a.ts[it * 16 + 6] = clock64();
 #pragma unroll
         for (int j = 0; j < G::NSUB; ++j) {
-          if (G::NSETS == 1 && k > 0) {
-            ptx::mbar_wait(subfree0 + 8 * j, (k - 1) & 1);
+          if (k > 0) {
+            ptx::mbar_wait((G::NSETS == 1 ? subfree0 : tready0) + 8 * j, (k - 1) & 1);
             ptx::tc_fence_after();
           }
 #pragma unroll
@@ -295,17 +303,21 @@ __global__ void __launch_bounds__(THREADS, 1)
                                      xdesc + (uint64_t)(((j * G::BH + r) * W * 16 + 2 * q * G::PLANE) >> 4),
                                      w1d + (uint64_t)(((r * P + 2 * q) * G::N * 16) >> 4), IDESC,
                                      (uint32_t)((r | q) != 0));
+          ptx::mma_commit_elect(acc1j0 + 8 * j);
         }
         ptx::mma_commit_elect(xb_empty);
-        ptx::mma_commit_elect(acc1);
         __syncwarp();
         if (mstamp && blk == 0) a.ts[it * 16 + 7] = clock64();
-        ptx::mbar_wait(tb_full, ph);                  // T written (and conv1 TMEM read) by epilogue 1
-        if (G::NSETS == 2) ptx::mbar_wait(acc2_empty, ph ^ 1);
-        ptx::tc_fence_after();
         if (mstamp && blk == NB - 1) a.ts[it * 16 + 8] = clock64();
+        // conv2 sub-tile j: T rows of sub-tiles j-1..j+1 written (and, shared set, accumulator j
+        // read) by epilogue 1; two sets: SET2 columns j drained by the previous epilogue 2
 #pragma unroll
-        for (int j = 0; j < G::NSUB; ++j)
+        for (int j = 0; j < G::NSUB; ++j) {
+#pragma unroll
+          for (int jj = j - 1; jj <= j + 1; ++jj)
+            if (jj >= 0 && jj < G::NSUB) ptx::mbar_wait(tready0 + 8 * jj, ph);
+          if (G::NSETS == 2 && k > 0) ptx::mbar_wait(subfree0 + 8 * j, (k - 1) & 1);
+          ptx::tc_fence_after();
 #pragma unroll
           for (int r = 0; r < 3; ++r)
 #pragma unroll
@@ -314,7 +326,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                                      tdesc + (uint64_t)(((j * G::BH + r) * W * 16 + 2 * q * G::PLANE) >> 4),
                                      w2d + (uint64_t)(((r * P + 2 * q) * G::N * 16) >> 4), IDESC,
                                      (uint32_t)((r | q) != 0));
-        ptx::mma_commit_elect(acc2);
+          ptx::mma_commit_elect(acc2j0 + 8 * j);
+        }
         __syncwarp();
         if (mstamp && blk == NB - 1) a.ts[it * 16 + 9] = clock64();
       }
@@ -357,15 +370,18 @@ __global__ void __launch_bounds__(THREADS, 1)
       const float* b1s = bs + 2 * blk * C;
       const float* b2s = b1s + C;
       const bool stamp = a.ts && blockIdx.x == 0 && et == 0 && it < 8;
-      // ---- epilogue 1: T = relu(conv1 + b1) -> bf16 operand image (SMEM)
-      ptx::mbar_wait(acc1, ph);
-      ptx::tc_fence_after();
+      // ---- epilogue 1: T = relu(conv1 + b1) -> bf16 operand image (SMEM), sub-tile by sub-tile
+      // as the conv1 accumulators complete
       // the previous sample's bf16-copy store (from T / ybs) has read SMEM: T / ybs may be rewritten
       if (blk == 0 && it > 0 && a.yb) ptx::mbar_wait(tb_free, (it - 1) & 1);
       if (stamp && blk == 0) a.ts[it * 16 + 2] = clock64();
 #pragma unroll
       for (int g = 0; g < UPT; g += 2) {
         uint32_t v[2][3][16];
+        const int ja = wg + 2 * (g / CPS), jb = wg + 2 * ((g + 1) / CPS);   // sub-tiles of this pair
+        ptx::mbar_wait(acc1j0 + 8 * ja, ph);
+        if (jb != ja) ptx::mbar_wait(acc1j0 + 8 * jb, ph);
+        ptx::tc_fence_after();
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const int j = wg + 2 * ((g + u) / CPS), c0 = ((g + u) % CPS) * 16;
@@ -387,12 +403,13 @@ __global__ void __launch_bounds__(THREADS, 1)
                 make_uint4(pk(f[8 * h2], f[8 * h2 + 1]), pk(f[8 * h2 + 2], f[8 * h2 + 3]),
                            pk(f[8 * h2 + 4], f[8 * h2 + 5]), pk(f[8 * h2 + 6], f[8 * h2 + 7]));
         }
+        // T rows of these sub-tiles written, their accumulators read: conv2 may use / reuse them
+        ptx::fence_proxy_async_smem();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(tready0 + 8 * ja);
+        if (jb != ja) ptx::mbar_arrive(tready0 + 8 * jb);
       }
-      ptx::fence_proxy_async_smem();
-      ptx::tc_fence_before();
       if (stamp && blk == 0) a.ts[it * 16 + 3] = clock64();
-      ptx::mbar_arrive(tb_full);
-      if (G::NSETS == 2) ptx::mbar_arrive(acc1_empty);
       // ---- next sample's operand conversion overlaps the last conv2 of this one
       if (last && smp + (int)gridDim.x < n_live) {
         if (stamp) a.ts[(it + 1) * 16 + 0] = clock64();
@@ -402,12 +419,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       // ---- epilogue 2: y = relu(conv2 + b2 + x) -> fp32 stream (+ bf16 operand copy); the
       // shortcut x is this sample's fp32 buffer in SMEM and y overwrites it in place
       uint8_t* xs = x32s + (size_t)(it % G::NXB) * G::X32_BYTES;
-      ptx::mbar_wait(acc2, ph);
-      ptx::tc_fence_after();
       if (stamp && last) a.ts[it * 16 + 4] = clock64();
 #pragma unroll
       for (int g = 0; g < UPT; g += 2) {
         uint32_t v[2][3][16];
+        const int ja = wg + 2 * (g / CPS), jb = wg + 2 * ((g + 1) / CPS);
+        ptx::mbar_wait(acc2j0 + 8 * ja, ph);
+        if (jb != ja) ptx::mbar_wait(acc2j0 + 8 * jb, ph);
+        ptx::tc_fence_after();
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const int j = wg + 2 * ((g + u) / CPS), c0 = ((g + u) % CPS) * 16;
@@ -417,14 +436,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           ptx::tmem_ld_32x32b_x16(t + 2 * C, v[u][2]);
         }
         ptx::tmem_ld_wait();
-        if (G::NSETS == 1) {                           // these sub-tiles' columns are free for conv1
-          ptx::tc_fence_before();
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int j = wg + 2 * ((g + u) / CPS);
-            if (u == 0 || j != wg + 2 * (g / CPS)) ptx::mbar_arrive(subfree0 + 8 * j);
-          }
-        }
+        // these sub-tiles' conv2 columns are read: the next conv1 (shared set) / conv2 (two sets) may reuse them
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(subfree0 + 8 * ja);
+        if (jb != ja) ptx::mbar_arrive(subfree0 + 8 * jb);
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const int j = wg + 2 * ((g + u) / CPS), c0 = ((g + u) % CPS) * 16;
@@ -459,8 +474,6 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
       }
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(acc2_empty);                    // conv2 accumulator drained
       if (!last) {                                     // y (bf16) is the next block's conv1 operand
         ptx::fence_proxy_async_smem();
         ptx::mbar_arrive(xb_full);
