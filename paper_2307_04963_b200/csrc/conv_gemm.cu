@@ -532,8 +532,11 @@ bool conv_gemm_eligible(const ConvArgs& a) {
 
 cudaError_t launch_conv_gemm(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream) {
   if (!conv_gemm_eligible(a)) return cudaErrorNotSupported;
-  if (a.Cout % 256 == 0) return launch_bn<256>(a, max_rows, num_sms, stream);
-  if (a.Cout % 128 == 0) return launch_bn<128>(a, max_rows, num_sms, stream);
+  // widest N tile that still gives every SM work when M is small (decode GEMMs: M = live rows)
+  const long long m_tiles = ((long long)(max_rows > 0 ? max_rows : 1) * a.Ho * a.Wo + BM - 1) / BM;
+  if (a.Cout % 256 == 0 && m_tiles * (a.Cout / 256) >= num_sms) return launch_bn<256>(a, max_rows, num_sms, stream);
+  if (a.Cout % 128 == 0 && m_tiles * (a.Cout / 128) >= num_sms) return launch_bn<128>(a, max_rows, num_sms, stream);
+  if (a.Cout % 256 == 0 && m_tiles * (a.Cout / 64) < num_sms / 2) return launch_bn<256>(a, max_rows, num_sms, stream);
   return launch_bn<64>(a, max_rows, num_sms, stream);
 }
 

@@ -54,6 +54,7 @@ struct dycl_s2s_s {
   // Every kernel reads its live row count from device memory, so the captured sequence is
   // valid for any data; only the pointers and the batch are baked in.
   bool use_graph = true;             // DYCL_S2S_GRAPH=0 disables
+  int gemm_path = 0;                 // 0: k_gemm_tma, 1: k_conv_gemm (DYCL_S2S_GEMM=1; measured equal or slower)
   // per-launch profiling (graph off while enabled)
   struct Rec {
     int kind;
@@ -166,6 +167,7 @@ struct S2SExec {
     a.H = a.W = a.Ho = a.Wo = 1; a.C = K; a.Cout = N; a.ksz = 1; a.stride = 1; a.pad = 0;
     a.K = K; a.Kp = K; a.relu = relu;
     a.rH = a.rW = 1; a.rC = N;
+    a.nhwc = a.in_nhwc = s->gemm_path;             // [rows][K] is NHWC at 1x1: the im2col-GEMM kernel
     ++n;
     pb(DYCL_K_GEMM, cnt, n_static, 2.0 * K + (yb ? 2.0 * N : 0.0) + (y32 ? 4.0 * N : 0.0) + (res32 ? 4.0 * N : 0.0),
        2.0 * K * N, 2.0 * K * N);
@@ -302,6 +304,7 @@ dycl_status dycl_s2s_create(int cuda_device, const dycl_s2s_config* cfg, dycl_s2
   s->c = *cfg;
   s->device = cuda_device;
   if (const char* eg = getenv("DYCL_S2S_GRAPH")) s->use_graph = atoi(eg) != 0;
+  if (const char* gp = getenv("DYCL_S2S_GEMM")) s->gemm_path = atoi(gp);
   cudaSetDevice(cuda_device);
   cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
   *out = s;

@@ -153,7 +153,18 @@ __global__ void __launch_bounds__(256) k_attn_decoder(const S2SAttnArgs a) {
   const int slot = a.slot[row];
   const int d = a.d, dh = 64;
   const uint16_t* qrow = a.q + (size_t)row * a.q_stride + h * dh;
-  const float q0 = bf(qrow[lane]), q1 = bf(qrow[lane + 32]);
+  // the head's 64-dim query in every lane's registers (8 broadcast 16-byte loads)
+  float qv[64];
+#pragma unroll
+  for (int c8 = 0; c8 < 8; ++c8) {
+    const uint4 w4 = *reinterpret_cast<const uint4*>(qrow + 8 * c8);
+    const uint32_t u[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      qv[8 * c8 + 2 * e] = __uint_as_float(u[e] << 16);
+      qv[8 * c8 + 2 * e + 1] = __uint_as_float(u[e] & 0xFFFF0000u);
+    }
+  }
   const uint16_t* kv;           // [positions][2d]: K at [0, d), V at [d, 2d)
   int nk;
   if (a.kv == nullptr) {
@@ -171,26 +182,26 @@ __global__ void __launch_bounds__(256) k_attn_decoder(const S2SAttnArgs a) {
     kv = a.kv + (size_t)slot * a.S * 2 * d;
     nk = a.S;
   }
-  // scores: lane j owns keys j and j+32 (nk <= 64); q is broadcast through shuffles and
-  // each lane reads its key's 64-dim head slice as 8 x 16-byte vectors.
+  // scores: lane j owns keys j and j + 32 (nk <= 64): 8 x 16-byte loads of the key's head
+  // slice, dot product against the register-resident query (the same summation order as
+  // before: pairs of dims, c ascending)
   float s0 = -INFINITY, s1 = -INFINITY;
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
     const int j = lane + 32 * half;
-    float acc = 0.f;
     const bool valid = j < nk;
     const uint4* kp = reinterpret_cast<const uint4*>(kv + (size_t)(valid ? j : 0) * 2 * d + h * dh);
+    uint4 kk[8];
+#pragma unroll
+    for (int c8 = 0; c8 < 8; ++c8) kk[c8] = valid ? kp[c8] : make_uint4(0, 0, 0, 0);   // coherent: row t may be this warp's
+    float acc = 0.f;
 #pragma unroll
     for (int c8 = 0; c8 < 8; ++c8) {
-      // plain (coherent) load: the self cache row t was written by this warp in this kernel
-      const uint4 w4 = valid ? kp[c8] : make_uint4(0, 0, 0, 0);
-      const uint32_t u[4] = {w4.x, w4.y, w4.z, w4.w};
+      const uint32_t u[4] = {kk[c8].x, kk[c8].y, kk[c8].z, kk[c8].w};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int c = c8 * 8 + 2 * e;                    // dims c, c+1 of q live on lanes c%32 (q0 / q1)
-        const float qa = __shfl_sync(0xffffffffu, c < 32 ? q0 : q1, c & 31);
-        const float qb = __shfl_sync(0xffffffffu, c + 1 < 32 ? q0 : q1, (c + 1) & 31);
-        acc += qa * __uint_as_float(u[e] << 16) + qb * __uint_as_float(u[e] & 0xFFFF0000u);
+        const int c = c8 * 8 + 2 * e;
+        acc += qv[c] * __uint_as_float(u[e] << 16) + qv[c + 1] * __uint_as_float(u[e] & 0xFFFF0000u);
       }
     }
     if (valid) {
