@@ -124,6 +124,7 @@ struct dycl_graph_s {
   float* d_pred = nullptr;
   float* d_z = nullptr;
   float* d_gpool = nullptr;         // pooled features of wide heads [max_batch][max head C]
+  float* d_pool32[NBUF32] = {};     // fused-GAP features per fp32 stream buffer [max_batch][<= 32] (fused blocks)
   float* d_in_stage = nullptr;      // dycl_run_host staging
   float* d_logit_stage = nullptr;
   int32_t* d_path_stage = nullptr;
@@ -397,6 +398,8 @@ struct Exec {
     ++g->prof_used;
   }
 
+  bool pv[dycl_graph_s::NBUF32] = {};   // d_pool32[f] holds the GAP of every live row of buf32[f]
+
   Tensor pick_tensor(bool stream, std::initializer_list<Tensor> busy) {
     std::vector<int> bb, bf;
     for (const Tensor& t : busy) {
@@ -409,6 +412,7 @@ struct Exec {
     if (stream)
       for (int i = 0; i < dycl_graph_s::NBUF32 && o.f < 0; ++i)
         if (std::find(bf.begin(), bf.end(), i) == bf.end()) o.f = i;
+    if (o.f >= 0) pv[o.f] = false;               // about to be rewritten
     return o;
   }
   bool fp32_stream() const { return g->precision == DYCL_PREC_FP32_STREAM; }
@@ -461,6 +465,7 @@ struct Exec {
         }
         ba.n_live = cnt;
         ba.C = c1.in.C; ba.H = c1.in.H; ba.W = c1.in.W;
+        ba.pooled = last ? g->d_pool32[o.f] : nullptr;   // fused GAP for the head that follows the subnet
         ++fused_launch;
         ba.ts = (g->dbg_ts_pick == 0 || g->dbg_ts_pick == fused_launch) ? g->dbg_ts : nullptr;
         const double row_b = (4.0 + 4.0 + (need_b ? 2.0 : 0.0)) * c1.in.row_elems();
@@ -470,6 +475,7 @@ struct Exec {
         prof_end();
         if (e != cudaSuccess) return cuda_fail(g, e, "launch_block_fused");
         if (!need_b) o.b = -1;                        // no valid bf16 copy
+        pv[o.f] = ba.pooled != nullptr;
         cur = o;
         li = lend - 1;
         continue;
@@ -616,6 +622,7 @@ struct Exec {
     a.kind = kind;
     a.thr = thr;
     a.nhwc = lay(s.in.Cp());
+    if (in.f >= 0 && pv[in.f] && g->d_pool32[in.f] && s.in.H * s.in.W > 1) a.pooled = g->d_pool32[in.f];
     if (D.d_wt && kind != 1 && g->d_gpool) {
       a.wt = D.d_wt;
       a.gpool = g->d_gpool;
@@ -749,6 +756,7 @@ struct Exec {
             ba.n_live = g->d_counts + s;
             ba.C = c1.in.C; ba.H = c1.in.H; ba.W = c1.in.W;
             ba.ts = nullptr;
+            ba.pooled = pv[cur.f] ? g->d_pool32[cur.f] : nullptr;   // executed rows refresh their GAP
             const double row_b = (4.0 + 4.0 + 2.0) * c1.in.row_elems();
             const double row_f = 2.0 * 2.0 * c1.out.H * c1.out.W * c1.out.C * (double)(9 * c1.in.C);
             prof_begin(DYCL_K_BLOCK, g->d_counts + s, row_b, row_f, 2.0 * 2 * 3 * c1.out.C * c1.Kp_rt);
@@ -858,6 +866,7 @@ dycl_status dycl_graph_destroy(dycl_graph g) {
   cudaFree(g->d_pred);
   cudaFree(g->d_z);
   cudaFree(g->d_gpool);
+  for (auto* p : g->d_pool32) cudaFree(p);
   cudaFree(g->d_in_stage);
   cudaFree(g->d_logit_stage);
   cudaFree(g->d_path_stage);
@@ -1161,6 +1170,16 @@ dycl_status dycl_finalize(dycl_graph g, int64_t max_batch) {
   if (dycl_status s = dmalloc(g, &g->d_flag, nb)) return s;
   if (dycl_status s = dmalloc(g, &g->d_pred, nb * 4)) return s;
   if (dycl_status s = dmalloc(g, &g->d_z, nb * (size_t)std::max(g->K, 1) * 4)) return s;
+  if (g->precision == DYCL_PREC_FP32_STREAM) {
+    bool fused_any = false;
+    for (size_t i = 0; i < g->subnets.size(); ++i)
+      if (planned[i])
+        for (const Layer& L : g->subnets[i].layers)
+          fused_any = fused_any || (L.kind == L_CONV && L.d_wrt && dycl::block_fused_eligible(L.in.C, L.in.H, L.in.W));
+    if (fused_any)
+      for (auto& p : g->d_pool32)
+        if (dycl_status s = dmalloc(g, &p, nb * 32 * 4)) return s;
+  }
   {
     int cmax = 0;
     for (const Node& N : g->nodes)

@@ -51,7 +51,7 @@ struct BCfg {
   static constexpr int W_BYTES = WCH * N * 16;
   static constexpr int BOX_ROWS = HW < 256 ? HW : 256;  // pixels per TMA box (box dims <= 256)
   static constexpr int NBOX = HW / BOX_ROWS;
-  static constexpr int FIXED = 1024 + 2 * OPER + 2 * NB * W_BYTES + 2 * NB * C * 4 + 512 + 256;
+  static constexpr int FIXED = 1024 + 2 * OPER + 2 * NB * W_BYTES + 2 * NB * C * 4 + 512 + 256 + 8 * C * 4;
   // fp32 sample buffers (2 if they fit: y is written in place over its own input x, which is
   // also the shortcut) and a separate bf16 output staging buffer if it fits
   static constexpr int NXB = FIXED + 2 * X32_BYTES <= 227 * 1024 ? 2 : 1;
@@ -155,6 +155,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   // has read accumulator j and written T rows of sub-tile j (conv2 sub-tile j needs j-1..j+1)
   const uint32_t acc1j0 = ptx::smem_u32(bars + 34), acc2j0 = ptx::smem_u32(bars + 42), tready0 = ptx::smem_u32(bars + 50);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 58);
+  float* gred = reinterpret_cast<float*>(bars + 60);       // [8 warps][C] fused-GAP partials (C <= 32)
   static_assert(G::NBOX <= 4, "box barriers");
   static_assert(G::NSUB <= 8, "sub-tile barriers");
   constexpr uint32_t SET2 = G::NSETS == 2 ? 256u : 0u;    // TMEM column of the conv2 accumulator
@@ -468,7 +469,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                   make_uint4(pk(f[8 * h2], f[8 * h2 + 1]), pk(f[8 * h2 + 2], f[8 * h2 + 3]),
                              pk(f[8 * h2 + 4], f[8 * h2 + 5]), pk(f[8 * h2 + 6], f[8 * h2 + 7]));
           }
-          if (last && c0 + 16 == C) {                  // sub-tile j done: hand its box to the producer
+          if (last && !a.pooled && c0 + 16 == C) {     // sub-tile j done: hand its box to the producer
             ptx::fence_proxy_async_smem();
             ptx::mbar_arrive(yready0 + 8 * (4 * (it % G::NXB) + j * 128 / G::BOX_ROWS));
           }
@@ -477,6 +478,39 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (!last) {                                     // y (bf16) is the next block's conv1 operand
         ptx::fence_proxy_async_smem();
         ptx::mbar_arrive(xb_full);
+      }
+      if (last && a.pooled) {
+        // global average pool of y for the head that follows (a2 fused): y sits in SMEM; thread t
+        // sums channel quad t % (C/4) over pixels t / (C/4), + 256/(C/4), ...; lanes sharing a
+        // quad reduce by shuffles, warps through SMEM, fixed order throughout
+        constexpr int NQ = C / 4, PST = 256 / NQ;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        const int cq = et % NQ;
+        float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+        for (int pix = et / NQ; pix < HW; pix += PST) {
+          const float4 q = *reinterpret_cast<const float4*>(xs + swz<C>((uint32_t)(pix * C + 4 * cq) * 4));
+          acc4.x += q.x; acc4.y += q.y; acc4.z += q.z; acc4.w += q.w;
+        }
+#pragma unroll
+        for (int o = NQ; o < 32; o <<= 1) {
+          acc4.x += __shfl_xor_sync(0xffffffffu, acc4.x, o);
+          acc4.y += __shfl_xor_sync(0xffffffffu, acc4.y, o);
+          acc4.z += __shfl_xor_sync(0xffffffffu, acc4.z, o);
+          acc4.w += __shfl_xor_sync(0xffffffffu, acc4.w, o);
+        }
+        if (lane < NQ) *reinterpret_cast<float4*>(gred + (warp * NQ + lane) * 4) = acc4;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (et < C) {
+          float sum = 0.f;
+#pragma unroll
+          for (int w8 = 0; w8 < 8; ++w8) sum += gred[(w8 * NQ + et / 4) * 4 + (et & 3)];
+          const int dst = a.list && a.list_out ? a.list[smp] : smp;
+          a.pooled[(size_t)dst * C + et] = sum * (1.0f / HW);
+        }
+        ptx::fence_proxy_async_smem();
+#pragma unroll
+        for (int q = 0; q < G::NBOX; ++q) ptx::mbar_arrive(yready0 + 8 * (4 * (it % G::NXB) + q));
       }
       if (stamp && last) a.ts[it * 16 + 5] = clock64();
      }

@@ -67,7 +67,9 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head(const HeadArgs a) {
     const uint16_t* h = a.h + (size_t)row * a.HW * a.C;
     // GAP: thread (p0, grp) sums its 8 channels over pixels p0, p0+P, ...
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (t < G * P) {
+    if (a.pooled) {                                // fused into the producing block: just load
+      for (int c = t; c < a.C; c += HEAD_THREADS) g[c] = a.pooled[(size_t)row * a.C + c];
+    } else if (t < G * P) {
       const int grp = t % G;
       if (a.h32) {
         const float* h32 = a.h32 + (size_t)row * a.HW * a.C;
@@ -94,7 +96,7 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head(const HeadArgs a) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) part[t * 8 + j] = acc[j];
     __syncthreads();
-    for (int c = t; c < a.C; c += HEAD_THREADS) {
+    for (int c = t; c < a.C && !a.pooled; c += HEAD_THREADS) {
       const int grp = c >> 3, j = c & 7;
       float s = 0.0f;
       for (int q = 0; q < P; ++q) s += part[(q * G + grp) * 8 + j];

@@ -91,6 +91,7 @@ struct HeadArgs {
   int nhwc = 0;          // bf16 h is NHWC [n][HW][C] (else channel-planar)
   // wide heads (K >= 128): FC batched over FC_ROWS samples per CTA from the transposed weights
   const uint16_t* wt = nullptr;   // bf16 [C][K] (nullptr: per-sample FC inside the GAP kernel)
+  const float* pooled = nullptr;  // fp32 [rows][C] pooled features already computed (fused GAP): skip the GAP
   float* gpool = nullptr;         // fp32 [rows][C] pooled-feature scratch for the batched FC
 };
 cudaError_t launch_head(const HeadArgs& a, int max_rows, cudaStream_t s);
@@ -152,6 +153,7 @@ struct BlockArgs {
   const float* x32;        // fp32 NHWC [n][H][W][C] (the first block's input, also its shortcut)
   const int32_t* list;     // optional row index list (input row = list[i]), nullptr = identity
   int list_out = 0;        // 1: output row = list[i] too (in place over x when y32 == x32)
+  float* pooled = nullptr; // fp32 [rows][C]: per-sample channel means of the last block's y (fused GAP), or nullptr
   float* y32;              // fp32 NHWC [n][H][W][C]
   uint16_t* yb;            // bf16 channel-planar copy or nullptr
   int nblk;                // blocks fused in this launch (1..MAX_FUSED_BLOCKS)
