@@ -622,7 +622,10 @@ struct Exec {
     a.kind = kind;
     a.thr = thr;
     a.nhwc = lay(s.in.Cp());
-    if (in.f >= 0 && pv[in.f] && g->d_pool32[in.f] && s.in.H * s.in.W > 1) a.pooled = g->d_pool32[in.f];
+    if (in.f >= 0 && g->d_pool32[in.f] && s.in.H * s.in.W > 1 && s.in.Cp() <= 32) {
+      if (pv[in.f]) a.pooled = g->d_pool32[in.f];
+      else a.pooled_out = g->d_pool32[in.f];     // computed here, kept for the in-place gates that follow
+    }
     if (D.d_wt && kind != 1 && g->d_gpool) {
       a.wt = D.d_wt;
       a.gpool = g->d_gpool;
@@ -632,6 +635,7 @@ struct Exec {
     cudaError_t e = dycl::launch_head(a, batch, st);
     prof_end();
     if (e != cudaSuccess) return cuda_fail(g, e, "launch_head");
+    if (a.pooled_out) pv[in.f] = true;
     return DYCL_OK;
   }
 

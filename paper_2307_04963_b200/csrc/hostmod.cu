@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head(const HeadArgs a) {
       for (int q = 0; q < P; ++q) s += part[(q * G + grp) * 8 + j];
       g[c] = s / (float)a.HW;
       if (a.wt) a.gpool[(size_t)row * a.C + c] = g[c];
+      if (a.pooled_out) a.pooled_out[(size_t)row * a.C + c] = g[c];
     }
     __syncthreads();
     if (a.wt) continue;                            // wide head: FC + predicate in k_head_fc
@@ -152,6 +153,52 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head(const HeadArgs a) {
       }
     }
     __syncthreads();
+  }
+}
+
+// Head on fused-GAP features (a.pooled) with K <= 32, C <= 64: one warp per live row, lane k
+// computes logit k (sum over c ascending), then the predicate with warp reductions.
+__global__ void __launch_bounds__(256) k_head_small(const HeadArgs a) {
+  const int n_live = *a.n_live;
+  const int lane = threadIdx.x & 31;
+  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < n_live; row += (gridDim.x * blockDim.x) >> 5) {
+    const float* gp = a.pooled + (size_t)row * a.C;
+    const float g0 = lane < a.C ? gp[lane] : 0.f, g1 = lane + 32 < a.C ? gp[lane + 32] : 0.f;
+    float z = -INFINITY;
+    if (lane < a.K) {
+      const uint16_t* wr = a.w + (size_t)lane * a.C;
+      float sacc = 0.f;
+      for (int c = 0; c < a.C; ++c) {
+        const float gc = __shfl_sync(0xffffffffu, c < 32 ? g0 : g1, c & 31);
+        sacc += bf16f(wr[c]) * gc;
+      }
+      z = sacc + a.b[lane];
+      a.z[(size_t)row * a.K + lane] = z;
+    } else {
+      for (int c = 0; c < a.C; ++c) (void)__shfl_sync(0xffffffffu, c < 32 ? g0 : g1, c & 31);
+    }
+    if (a.kind == 0) {
+      float m = z;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      float e = lane < a.K ? expf(z - m) : 0.f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+      if (lane == 0) {
+        const float conf = 1.0f / e;               // max_j softmax(z)_j
+        a.flag[row] = conf >= a.thr ? 1 : 0;       // reading R1: conf >= tau exits
+        if (a.pred) a.pred[row] = conf;
+      }
+    } else if (lane == 0) {
+      if (a.kind == 1) {
+        const float pr = 1.0f / (1.0f + expf(-z));
+        a.flag[row] = pr > a.thr ? 1 : 0;          // reading R2: p > thr executes
+        if (a.pred) a.pred[row] = pr;
+      } else {
+        a.flag[row] = 1;
+        if (a.pred) a.pred[row] = 1.0f;
+      }
+    }
   }
 }
 
@@ -587,6 +634,12 @@ cudaError_t launch_init(int* counts, int n, int* orig, int32_t* path, int nmax, 
 
 cudaError_t launch_head(const HeadArgs& a, int max_rows, cudaStream_t s) {
   if (a.C % 8 != 0 || a.C / 8 > HEAD_THREADS) return cudaErrorInvalidValue;
+  if (a.pooled && !a.wt && a.K <= 32 && a.C <= 64) {
+    int grid = (max_rows + 7) / 8;
+    if (grid > 148 * 16) grid = 148 * 16;
+    k_head_small<<<grid > 0 ? grid : 1, 256, 0, s>>>(a);
+    return cudaGetLastError();
+  }
   const size_t smem = (HEAD_THREADS * 8 + a.C + a.K) * sizeof(float);
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {

@@ -92,6 +92,7 @@ struct HeadArgs {
   // wide heads (K >= 128): FC batched over FC_ROWS samples per CTA from the transposed weights
   const uint16_t* wt = nullptr;   // bf16 [C][K] (nullptr: per-sample FC inside the GAP kernel)
   const float* pooled = nullptr;  // fp32 [rows][C] pooled features already computed (fused GAP): skip the GAP
+  float* pooled_out = nullptr;    // fp32 [rows][C]: keep the GAP this kernel computes (later in-place gates reuse it)
   float* gpool = nullptr;         // fp32 [rows][C] pooled-feature scratch for the batched FC
 };
 cudaError_t launch_head(const HeadArgs& a, int max_rows, cudaStream_t s);
