@@ -64,6 +64,26 @@ __device__ __forceinline__ void conv_finish16(const ConvArgs& a, int n, int ho, 
         }
       }
     }
+  } else if (a.res_mode == 2 && a.r_pad_lo % 4 == 0 && a.rC % 4 == 0 && !a.res_nhwc) {
+    // option A, vectorised: r_pad_lo and rC are multiples of 4, so each 4-channel group is
+    // entirely inside or outside [0, rC): one 16-byte (fp32) / 8-byte (bf16) load per group
+    const size_t rHW = (size_t)a.rH * a.rW;
+    const size_t rpix = (size_t)(2 * ho) * a.rW + 2 * wo;
+#pragma unroll
+    for (int g4 = 0; g4 < 4; ++g4) {
+      const int ci = o0 + 4 * g4 - a.r_pad_lo;
+      if (ci < 0 || ci + 4 > a.rC) continue;
+      float4 q;
+      if (a.res32) {
+        q = __ldg(reinterpret_cast<const float4*>(a.res32 + ((size_t)n * rHW + rpix) * a.rC + ci));
+      } else {
+        const uint2 u = __ldg(reinterpret_cast<const uint2*>(a.res + (size_t)n * a.rC * rHW + (size_t)(ci >> 3) * rHW * 8 +
+                                                             rpix * 8 + (ci & 7)));
+        q = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u), __uint_as_float(u.y << 16),
+                        __uint_as_float(u.y & 0xFFFF0000u));
+      }
+      f[4 * g4] += q.x; f[4 * g4 + 1] += q.y; f[4 * g4 + 2] += q.z; f[4 * g4 + 3] += q.w;
+    }
   } else if (a.res_mode == 2) {
     // option A: shortcut = input pixel (2ho, 2wo), channel o - r_pad_lo (zero outside [0, rC))
     const size_t rHW = (size_t)a.rH * a.rW;
