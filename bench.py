@@ -290,11 +290,12 @@ def run_dycl(args):
         flush.zero_()
         job.step(stream)     # profiling records the last chunk's launches; chunks are identical in shape
         for p in prof_read():    # syncs the stream
-            t = kind_tot.setdefault(p["kind"], [0.0, 0.0, 0.0, 0])
+            t = kind_tot.setdefault(p["kind"], [0.0, 0.0, 0.0, 0, []])
             t[0] += p["ms"]
             t[1] += p["bytes"]
             t[2] += p["flops"]
             t[3] += 1
+            t[4].append((p["ms"], p["bytes"], p["flops"]))
     torch.cuda.synchronize()
     if job.g is not None:
         D.dycl_set_profiling(job.g, 0)
@@ -335,16 +336,25 @@ def run_dycl(args):
     if kind_tot:
         # the dominant kernel class of the step (largest share of the per-launch event time)
         dom = max(kind_tot, key=lambda k: kind_tot[k][0])
-        ms_, by_, fl_, n_ = kind_tot[dom]
+        ms_, by_, fl_, n_, recs = kind_tot[dom]
         gbs = by_ / (ms_ / 1e3) / 1e9
         tfl = fl_ / (ms_ / 1e3) / 1e12
+        # per-launch roofline: ideal = max(FLOPs / tensor peak, bytes / HBM peak); a launch is
+        # tensor- or HBM-bound by which term wins; efficiency = sum(ideal) / sum(measured)
+        split = {"tensor": [0.0, 0.0], "hbm": [0.0, 0.0]}
+        for lm, lb, lf in recs:
+            it, ib = lf / (tf_sus * 1e12) * 1e3, lb / (hbm * 1e9) * 1e3
+            k = "tensor" if it > ib else "hbm"
+            split[k][0] += max(it, ib)
+            split[k][1] += lm
+        roof_eff = (split["tensor"][0] + split["hbm"][0]) / ms_ if ms_ else None
         names = {
             "block": "k_block_fused (a1: 1-2 whole residual blocks per sample, SMEM-resident, row-tap tcgen05 convs)",
             "conv": "a1 conv class (k_conv_gemm NHWC im2col GEMM / k_conv_tma / k_gemm_tma on tcgen05, fused epilogue)",
             "gemm": "k_gemm_tma (a7/a8 decoder + encoder projections, FFN, LM head on tcgen05)",
             "attn": "k_attn_decoder (a7 decode attention, KV-cache streaming)",
         }
-        tensor_bound = dom in ("gemm",) or (dom == "conv" and args.config == 5)
+        tensor_bound = split["tensor"][1] > split["hbm"][1]   # the bound that covers most of the class's time
         if tensor_bound:
             roof = {"kernel": names.get(dom, dom), "bound": "tensor", "achieved": tfl, "peak": tf_sus,
                     "unit": "TFLOP/s", "frac": tfl / tf_sus, "traffic": None,
@@ -360,7 +370,11 @@ def run_dycl(args):
             roof = {"kernel": names.get(dom, dom), "bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
                     "frac": gbs / hbm, "traffic": traffic, "peak_source": peak_src,
                     "tensor_tflops": tfl, "tensor_frac_of_sustained": tfl / tf_sus}
-        roof.update({"share_of_step": ms_ / step_prof_ms if step_prof_ms else None,
+        roof.update({"roofline_efficiency": roof_eff,
+                     "launch_split": {k: {"ms_per_step": v[1] / args.steps,
+                                          "frac_of_own_roofline": v[0] / v[1] if v[1] else None}
+                                      for k, v in split.items()},
+                     "share_of_step": ms_ / step_prof_ms if step_prof_ms else None,
                      "algorithmic_bytes_per_launch": by_ / max(n_, 1),
                      "algorithmic_flops_per_launch": fl_ / max(n_, 1),
                      "avg_launch_ms": ms_ / max(n_, 1),
