@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(128) k_attn_encoder(const S2SAttnArgs a) {
 //   self  (kv == nullptr): append this row's k, v (from qkv) at position t of the slot's
 //         cache, then attend over positions 0..t of the cache;
 //   cross (kv != nullptr): attend over the S encoder positions of the slot's cross K/V.
-__global__ void __launch_bounds__(256) k_attn_decoder(const S2SAttnArgs a) {
+__global__ void __launch_bounds__(256, 5) k_attn_decoder(const S2SAttnArgs a) {
   const int n = a.n_live ? *a.n_live : a.n_static;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int row = gw / a.heads, h = gw % a.heads;
@@ -153,17 +153,15 @@ __global__ void __launch_bounds__(256) k_attn_decoder(const S2SAttnArgs a) {
   const int slot = a.slot[row];
   const int d = a.d, dh = 64;
   const uint16_t* qrow = a.q + (size_t)row * a.q_stride + h * dh;
-  // the head's 64-dim query in every lane's registers (8 broadcast 16-byte loads)
-  float qv[64];
-#pragma unroll
-  for (int c8 = 0; c8 < 8; ++c8) {
-    const uint4 w4 = *reinterpret_cast<const uint4*>(qrow + 8 * c8);
-    const uint32_t u[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      qv[8 * c8 + 2 * e] = __uint_as_float(u[e] << 16);
-      qv[8 * c8 + 2 * e + 1] = __uint_as_float(u[e] & 0xFFFF0000u);
-    }
+  // the head's 64-dim query in SMEM (fp32, per warp), read back as broadcasts: keeps the
+  // registers low enough for 6+ CTAs per SM (memory-level parallelism for the K/V stream)
+  __shared__ float qs_all[8][64];
+  float* qv = qs_all[threadIdx.x >> 5];
+  {
+    const uint32_t u = reinterpret_cast<const uint32_t*>(qrow)[lane];
+    qv[2 * lane] = __uint_as_float(u << 16);
+    qv[2 * lane + 1] = __uint_as_float(u & 0xFFFF0000u);
+    __syncwarp();
   }
   const uint16_t* kv;           // [positions][2d]: K at [0, d), V at [d, 2d)
   int nk;
@@ -198,11 +196,12 @@ __global__ void __launch_bounds__(256) k_attn_decoder(const S2SAttnArgs a) {
 #pragma unroll
     for (int c8 = 0; c8 < 8; ++c8) {
       const uint32_t u[4] = {kk[c8].x, kk[c8].y, kk[c8].z, kk[c8].w};
+      const float4 qa = *reinterpret_cast<const float4*>(qv + c8 * 8);
+      const float4 qb = *reinterpret_cast<const float4*>(qv + c8 * 8 + 4);
+      const float qq[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int c = c8 * 8 + 2 * e;
-        acc += qv[c] * __uint_as_float(u[e] << 16) + qv[c + 1] * __uint_as_float(u[e] & 0xFFFF0000u);
-      }
+      for (int e = 0; e < 4; ++e)
+        acc += qq[2 * e] * __uint_as_float(u[e] << 16) + qq[2 * e + 1] * __uint_as_float(u[e] & 0xFFFF0000u);
     }
     if (valid) {
       if (half == 0) s0 = acc * 0.125f;
