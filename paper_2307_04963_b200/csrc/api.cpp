@@ -725,10 +725,16 @@ struct Exec {
           // ResNet-50 stage starts with a projection block: its input is read as bf16 only)
           const bool next_seq = ni + 1 < g->nodes.size() && g->nodes[ni + 1].kind == N_SEQ;
           const bool keep32 = cur.f >= 0 && !(next_seq && !g->subnets[g->nodes[ni + 1].sn].needs_in32);
+          // ... and their bf16 copy only if the next reader is not a fused block (which reads the
+          // fp32 stream alone)
+          const bool keepb = !(next_seq && keep32 && fp32_stream() && !g->no_fuse &&
+                               fusable(g->subnets[g->nodes[ni + 1].sn], 0));
           Tensor src = cur;
           if (!keep32) src.f = -1;
+          if (!keepb) src.b = -1;
           Tensor nb = pick_tensor(keep32, {cur});
           if (!keep32) nb.f = -1;
+          if (!keepb) nb.b = -1;
           if ((r = gather(src, nb, g->d_list0, g->d_counts + s + 1, nullptr, N.in, 0))) return r;
           cur = nb;
           cnt = g->d_counts + s + 1;
