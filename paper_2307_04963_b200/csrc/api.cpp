@@ -110,6 +110,15 @@ struct dycl_graph_s {
   int no_fuse = 0;                   // DYCL_NO_FUSE=1: run basic blocks as two conv launches
   int max_fuse = 2;                  // DYCL_MAX_FUSE: basic blocks per fused launch (1..2)
   int no_inplace = 0;                // DYCL_NO_INPLACE=1: gates gather / merge instead of running in place
+  // CUDA graph of a whole run, captured on first use per (io pointers, batch) and replayed;
+  // every kernel sizes itself from device counts, so the captured launch sequence is valid for
+  // any data (DYCL_GRAPH=0 disables; profiling runs are issued launch by launch)
+  bool use_graph = true;
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  const void* gkey[3] = {};
+  int64_t gbatch = -1;
+  int glaunches = 0;
   int nhwc = 0;                      // bf16 activations NHWC (decided at finalize; DYCL_NHWC=0 disables)
   int stem_s4d = 0;                  // input cast to 4x4 space-to-depth for the stem (DYCL_STEM_S4D=0 disables)
   long long* dbg_ts = nullptr;       // DYCL_TS=1: fused-block phase timestamps (development)
@@ -836,6 +845,7 @@ dycl_status dycl_graph_create(int cuda_device, int in_h, int in_w, int in_c, dyc
   if (const char* nf = getenv("DYCL_NO_FUSE")) g->no_fuse = atoi(nf);
   if (const char* mf = getenv("DYCL_MAX_FUSE")) g->max_fuse = atoi(mf);
   if (const char* ni = getenv("DYCL_NO_INPLACE")) g->no_inplace = atoi(ni);
+  if (const char* ug = getenv("DYCL_GRAPH")) g->use_graph = atoi(ug) != 0;
   if (getenv("DYCL_TS")) {
     cudaMalloc(&g->dbg_ts, 8 * 16 * sizeof(long long));
     g->dbg_ts_pick = atoi(getenv("DYCL_TS")) > 1 ? atoi(getenv("DYCL_TS")) : 0;
@@ -881,6 +891,8 @@ dycl_status dycl_graph_destroy(dycl_graph g) {
   cudaFree(g->d_logit_stage);
   cudaFree(g->d_path_stage);
   cudaFree(g->dbg_ts);
+  if (g->gexec) cudaGraphExecDestroy(g->gexec);
+  if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
   for (auto& L : g->prof) {
     cudaEventDestroy(L.e0);
     cudaEventDestroy(L.e1);
@@ -1212,10 +1224,42 @@ static dycl_status run_impl(dycl_graph g, const float* input, int64_t batch, flo
   g->prof_stream = st;
   if (batch == 0) {
     CK(cudaMemsetAsync(g->d_counts, 0, g->n_slots * sizeof(int), st));
-  } else {
+  } else if (!g->use_graph || g->profiling || g->dbg_ts) {
     Exec ex{g, st, (int)batch, logits, path};
     if (dycl_status s = ex.run(input)) return s;
     g->launches_per_run = ex.nlaunch;
+  } else {
+    const void* key[3] = {input, logits, path};
+    bool hit = g->gexec && g->gbatch == batch;
+    for (int i = 0; i < 3 && hit; ++i) hit = key[i] == g->gkey[i];
+    if (!hit) {
+      if (g->gexec) {
+        cudaGraphExecDestroy(g->gexec);
+        g->gexec = nullptr;
+      }
+      if (!g->cap_stream) CK(cudaStreamCreateWithFlags(&g->cap_stream, cudaStreamNonBlocking));
+      CK(cudaStreamBeginCapture(g->cap_stream, cudaStreamCaptureModeThreadLocal));
+      Exec ex{g, g->cap_stream, (int)batch, logits, path};
+      const dycl_status r = ex.run(input);
+      cudaGraph_t graph = nullptr;
+      const cudaError_t ec = cudaStreamEndCapture(g->cap_stream, &graph);
+      if (r != DYCL_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return r;
+      }
+      if (ec != cudaSuccess) return cuda_fail(g, ec, "graph capture");
+      const cudaError_t ei = cudaGraphInstantiate(&g->gexec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ei != cudaSuccess) {
+        g->gexec = nullptr;
+        return cuda_fail(g, ei, "graph instantiate");
+      }
+      for (int i = 0; i < 3; ++i) g->gkey[i] = key[i];
+      g->gbatch = batch;
+      g->glaunches = ex.nlaunch;
+    }
+    CK(cudaGraphLaunch(g->gexec, st));
+    g->launches_per_run = g->glaunches;
   }
   if (node_counts) CK(cudaMemcpyAsync(node_counts, g->d_counts, g->n_slots * sizeof(int), cudaMemcpyDeviceToDevice, st));
   return DYCL_OK;
