@@ -213,14 +213,15 @@ cudaError_t launch_bn(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t
 
 bool gemm_tma_eligible(const ConvArgs& a) {
   return a.H == 1 && a.W == 1 && a.ksz == 1 && a.stride == 1 && a.pad == 0 && a.C % 64 == 0 && a.K == a.C &&
-         a.Kp == a.K && (a.Cout % 128 == 0) && a.res_mode != 2;
+         a.Kp == a.K && (a.Cout % 64 == 0) && a.res_mode != 2;
 }
 
 cudaError_t launch_gemm_tma(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream) {
   // 256-wide N tiles unless they leave more than half of the SMs idle (small-M decode GEMMs)
   const long long m_tiles = (max_rows + BM - 1) / BM;
   if (a.Cout % 256 == 0 && m_tiles * (a.Cout / 256) >= num_sms / 2) return launch_bn<256>(a, max_rows, num_sms, stream);
-  return launch_bn<128>(a, max_rows, num_sms, stream);
+  if (m_tiles * (a.Cout / 128) >= num_sms / 2) return launch_bn<128>(a, max_rows, num_sms, stream);
+  return launch_bn<64>(a, max_rows, num_sms, stream);   // small M, narrow N: twice the CTAs
 }
 
 }  // namespace dycl

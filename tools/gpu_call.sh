@@ -1,5 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu.py -x -q 2>&1 | tail -2
-timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench2.json 2> gpurun_out/bench2.err
-DYCL_GRAPH=0 timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench2b.json 2>> gpurun_out/bench2.err
-timeout 300 python bench.py --config 1 --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench1.json 2>> gpurun_out/bench2.err
-tail -n 3 gpurun_out/bench2.err
+timeout 900 python -m pytest tests/test_gpu.py -x -q -k "cfg4 or cfg1 or dense or conv_kernel" 2>&1 | tail -2
+timeout 300 python bench.py --config 4 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench4.json 2> gpurun_out/bench4.err
