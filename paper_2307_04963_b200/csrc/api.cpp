@@ -804,6 +804,7 @@ struct Exec {
           Tensor o;
           if ((r = subnet(g->subnets[N.then_sn], bt, g->d_counts + s, merged, cur, &o))) return r;
           if ((r = gather(cur, merged, g->d_list0, g->d_counts + s + 1, g->d_counts + s, N.in, N.skip_mode))) return r;
+          if (merged.f >= 0) pv[merged.f] = false;   // the skipped rows just arrived without a pooled copy
           cur = merged;
           if (!stream) cur.f = -1;
           orig_cur ^= 1;

@@ -288,6 +288,70 @@ def test_cfg2_full_batch_sampled_parity(r56):
     assert r["logit_rel_fail"] == 0 and r["outside_band_mismatch"] <= 1
 
 
+def test_cfg3_full_batch_sampled_parity():
+    """BASELINE size (B = 8192, the bench launch configuration, in-place gates): sampled rows
+    vs the oracle, plus the executed-block histogram's sanity."""
+    W = wl.skipnet_r38_weights()
+    m = P.build_skipnet_resnet38(W, 8192)
+    X = wl.image_inputs(wl.INPUT_SEED, 0, 8192)
+    lg, pg = _run_gpu(m, X)
+    assert np.isfinite(lg).all() and (pg >= 0).all() and (pg < (1 << 17)).all()
+    idx = np.random.default_rng(wl.ORACLE_SUBSET_SEED).choice(8192, 48, replace=False)
+    lo, po, pr = O.run_batch(O.skipnet_resnet38, X[idx], prg.prepare(W), "mirror")
+    r = report(lg[idx], pg[idx], lo, po, pr)
+    print("cfg3 full sampled", r, "mean executed", np.mean([bin(int(v)).count("1") for v in pg]))
+    assert r["logit_rel_fail"] == 0 and r["outside_band_mismatch"] <= 1
+
+
+def test_gates_in_place_equal_gather_merge():
+    """The in-place gate form (executed rows rewritten through the row list) and the
+    gather / merge form take the same paths; logits agree to fp32 reassociation (the
+    in-place form pools through the fused-block GAP, the other through the head's GAP)."""
+    import os
+    W = wl.skipnet_r38_weights()
+    X = wl.image_inputs(wl.INPUT_SEED, 500, 300)
+    m1 = P.build_skipnet_resnet38(W, 300)
+    lg1, pg1 = _run_gpu(m1, X)
+    os.environ["DYCL_NO_INPLACE"] = "1"
+    try:
+        m2 = P.build_skipnet_resnet38(W, 300)
+    finally:
+        del os.environ["DYCL_NO_INPLACE"]
+    lg2, pg2 = _run_gpu(m2, X)
+    print("in place vs gather: path mismatches", int((pg1 != pg2).sum()),
+          "max rel", float(np.max(np.abs(lg1 - lg2)) / np.max(np.abs(lg2))))
+    assert np.array_equal(pg1, pg2)
+    assert np.max(np.abs(lg1 - lg2)) <= 1e-5 * np.max(np.abs(lg2))
+
+
+def test_graph_replay_equals_direct_run(r56):
+    """dycl_run's captured CUDA graph and the launch-by-launch run agree bitwise, across
+    different data with the same io pointers (the graph is data-independent)."""
+    import os
+    W, m = r56
+    B = 512
+    x = torch.empty((B, 32, 32, 3), device=DEV)
+    logits = torch.empty((B, 10), device=DEV)
+    path = torch.empty(B, dtype=torch.int32, device=DEV)
+    outs = []
+    for start in (0, 7000):
+        x.copy_(torch.from_numpy(wl.image_inputs(wl.INPUT_SEED, start, B)))
+        m.run(x, logits, path)
+        torch.cuda.synchronize()
+        outs.append((logits.cpu().numpy().copy(), path.cpu().numpy().copy()))
+    os.environ["DYCL_GRAPH"] = "0"
+    try:
+        m2 = P.build_sdn_resnet56(W, 4096)
+    finally:
+        del os.environ["DYCL_GRAPH"]
+    for k, start in enumerate((0, 7000)):
+        x.copy_(torch.from_numpy(wl.image_inputs(wl.INPUT_SEED, start, B)))
+        m2.run(x, logits, path)
+        torch.cuda.synchronize()
+        assert np.array_equal(path.cpu().numpy(), outs[k][1])
+        assert np.array_equal(logits.cpu().numpy(), outs[k][0])
+
+
 # ------------------------------------------------------------------- config 5
 @pytest.fixture(scope="module")
 def r50():
@@ -308,6 +372,39 @@ def test_cfg5_resnet50_parity(r50):
     print("cfg5", r)
     assert r["logit_rel_fail"] == 0
     assert r["outside_band_mismatch"] <= 1, r
+
+
+def test_cfg5_bench_chunk_sampled_parity():
+    """The bench launch configuration (a graph finalised for 2048-sample chunks, run on a full
+    chunk of GPU-generated inputs): sampled rows vs the oracle."""
+    W = wl.resnet50_ee_weights()
+    m = P.build_resnet50_ee(W, 2048)
+    x = wl.image_inputs_torch(wl.INPUT_SEED, 10000, 2048, hw=224, device="cuda")
+    logits = torch.empty((2048, 1000), device=DEV)
+    path = torch.empty(2048, dtype=torch.int32, device=DEV)
+    m.run(x, logits, path)
+    torch.cuda.synchronize()
+    lg, pg = logits.cpu().numpy(), path.cpu().numpy()
+    assert np.isfinite(lg).all() and set(np.unique(pg)) <= {0, 1, 2, 3}
+    idx = np.sort(np.random.default_rng(wl.ORACLE_SUBSET_SEED).choice(2048, 12, replace=False))
+    X = wl.image_inputs(wl.INPUT_SEED, 0, 0, hw=224, idx=10000 + idx)
+    lo, po, pr = O.run_batch(O.resnet50_ee, X, prg.prepare(W), "mirror")
+    r = report(lg[idx], pg[idx], lo, po, pr)
+    print("cfg5 chunk sampled", r)
+    assert r["logit_rel_fail"] == 0 and r["outside_band_mismatch"] <= 1
+
+
+def test_cfg5_empty_and_single():
+    W = wl.resnet50_ee_weights()
+    m = P.build_resnet50_ee(W, 8)
+    X = wl.image_inputs(wl.INPUT_SEED, 321, 1, hw=224)
+    lg, pg = _run_gpu(m, X)
+    lo, po, pr = O.run_batch(O.resnet50_ee, X, prg.prepare(W), "mirror")
+    r = report(lg, pg, lo, po, pr)
+    assert r["logit_rel_fail"] == 0 and r["outside_band_mismatch"] == 0
+    x0 = torch.empty((0, 224, 224, 3), device=DEV)
+    m.run(x0, torch.empty((1, 1000), device=DEV), torch.empty(1, dtype=torch.int32, device=DEV))
+    torch.cuda.synchronize()
 
 
 # ------------------------------------------------------------------- config 4
