@@ -110,6 +110,7 @@ struct dycl_graph_s {
   int no_fuse = 0;                   // DYCL_NO_FUSE=1: run basic blocks as two conv launches
   int max_fuse = 2;                  // DYCL_MAX_FUSE: basic blocks per fused launch (1..2)
   int no_inplace = 0;                // DYCL_NO_INPLACE=1: gates gather / merge instead of running in place
+  int no_zero_copy = 0;              // DYCL_NO_ZERO_COPY=1: exits gather survivors even before a fused block
   // CUDA graph of a whole run, captured on first use per (io pointers, batch) and replayed;
   // every kernel sizes itself from device counts, so the captured launch sequence is valid for
   // any data (DYCL_GRAPH=0 disables; profiling runs are issued launch by launch)
@@ -408,6 +409,8 @@ struct Exec {
   }
 
   bool pv[dycl_graph_s::NBUF32] = {};   // d_pool32[f] holds the GAP of every live row of buf32[f]
+  const int* in_list = nullptr;         // zero-copy exit: the next subnet's first fused group reads its
+                                        // input rows through this list (the survivors) instead of a gather
 
   Tensor pick_tensor(bool stream, std::initializer_list<Tensor> busy) {
     std::vector<int> bb, bf;
@@ -449,6 +452,8 @@ struct Exec {
     Tensor cur = in, shortcut, proj_src;
     for (size_t li = 0; li < s.layers.size(); ++li) {
       const Layer& L = s.layers[li];
+      if (in_list && !(li == 0 && L.kind == L_BLOCK && fp32_stream() && !g->no_fuse && cur.f >= 0 && fusable(s, li)))
+        return fail(g, DYCL_E_STATE, "internal: zero-copy input on a non-fused first layer");
       if (L.kind == L_BLOCK && fp32_stream() && !g->no_fuse && cur.f >= 0 && fusable(s, li)) {
         // up to MAX_FUSED_BLOCKS consecutive fusable blocks (same shape) in one launch
         int nb = 1;
@@ -466,6 +471,8 @@ struct Exec {
         ba.y32 = g->buf32[o.f];
         ba.yb = need_b ? g->buf[o.b] : nullptr;
         ba.nblk = nb;
+        ba.list = in_list;                           // input rows = survivors of the last exit (zero-copy)
+        in_list = nullptr;
         for (int k = 0; k < nb; ++k) {
           ba.w1_rt[k] = s.layers[li + 3 * k + 1].d_wrt;
           ba.w2_rt[k] = s.layers[li + 3 * k + 2].d_wrt;
@@ -735,9 +742,17 @@ struct Exec {
           const bool next_seq = ni + 1 < g->nodes.size() && g->nodes[ni + 1].kind == N_SEQ;
           const bool keep32 = cur.f >= 0 && !(next_seq && !g->subnets[g->nodes[ni + 1].sn].needs_in32);
           // ... and their bf16 copy only if the next reader is not a fused block (which reads the
-          // fp32 stream alone)
-          const bool keepb = !(next_seq && keep32 && fp32_stream() && !g->no_fuse &&
-                               fusable(g->subnets[g->nodes[ni + 1].sn], 0));
+          // fp32 stream alone).  A fused block can even read the survivors in place through the
+          // compaction's row list: then nothing moves at all (zero-copy exit)
+          const bool next_fused = next_seq && keep32 && fp32_stream() && !g->no_fuse &&
+                                  fusable(g->subnets[g->nodes[ni + 1].sn], 0);
+          if (next_fused && !g->no_zero_copy) {
+            in_list = g->d_list0;
+            cnt = g->d_counts + s + 1;
+            orig_cur ^= 1;
+            break;
+          }
+          const bool keepb = !next_fused;
           Tensor src = cur;
           if (!keep32) src.f = -1;
           if (!keepb) src.b = -1;
@@ -846,6 +861,7 @@ dycl_status dycl_graph_create(int cuda_device, int in_h, int in_w, int in_c, dyc
   if (const char* nf = getenv("DYCL_NO_FUSE")) g->no_fuse = atoi(nf);
   if (const char* mf = getenv("DYCL_MAX_FUSE")) g->max_fuse = atoi(mf);
   if (const char* ni = getenv("DYCL_NO_INPLACE")) g->no_inplace = atoi(ni);
+  if (const char* nz = getenv("DYCL_NO_ZERO_COPY")) g->no_zero_copy = atoi(nz);
   if (const char* ug = getenv("DYCL_GRAPH")) g->use_graph = atoi(ug) != 0;
   if (getenv("DYCL_TS")) {
     cudaMalloc(&g->dbg_ts, 8 * 16 * sizeof(long long));

@@ -324,6 +324,22 @@ def test_gates_in_place_equal_gather_merge():
     assert np.max(np.abs(lg1 - lg2)) <= 1e-5 * np.max(np.abs(lg2))
 
 
+def test_zero_copy_exits_equal_gather():
+    """Exits before a fused block hand the survivors over by row list (no gather): bitwise
+    the same logits and paths as gathering them."""
+    import os
+    W = wl.sdn_r56_weights()
+    X = wl.image_inputs(wl.INPUT_SEED, 900, 333)
+    lg1, pg1 = _run_gpu(P.build_sdn_resnet56(W, 333), X)
+    os.environ["DYCL_NO_ZERO_COPY"] = "1"
+    try:
+        m2 = P.build_sdn_resnet56(W, 333)
+    finally:
+        del os.environ["DYCL_NO_ZERO_COPY"]
+    lg2, pg2 = _run_gpu(m2, X)
+    assert np.array_equal(pg1, pg2) and np.array_equal(lg1, lg2)
+
+
 def test_graph_replay_equals_direct_run(r56):
     """dycl_run's captured CUDA graph and the launch-by-launch run agree bitwise, across
     different data with the same io pointers (the graph is data-independent)."""

@@ -1,1 +1,2 @@
-timeout 1200 python -m pytest tests/test_gpu.py -x -q -s -k "full_batch or in_place or graph_replay or chunk_sampled or empty_and_single" 2>&1 | grep -E "in place vs|sampled|passed|failed|Error|assert" | head -20
+timeout 900 python -m pytest tests/test_gpu.py -x -q 2>&1 | tail -2
+timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench2.json 2> gpurun_out/bench2.err
