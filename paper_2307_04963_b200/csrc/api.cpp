@@ -446,6 +446,20 @@ struct Exec {
     return dycl::block_fused_eligible(c1.in.C, c1.in.H, c1.in.W);
   }
 
+  // A gate then-branch [block, 3x3/1/1 conv + ReLU, 3x3/1/1 conv + identity shortcut + ReLU] on
+  // NHWC tensors whose samples tile 128-row GEMM tiles whole: the in-place GEMM form applies.
+  bool inplace_gemm_ok(const Subnet& T) const {
+    if (T.layers.size() != 3 || T.layers[0].kind != L_BLOCK) return false;
+    const Layer &c1 = T.layers[1], &c2 = T.layers[2];
+    for (const Layer* c : {&c1, &c2})
+      if (c->kind != L_CONV || c->k != 3 || c->stride != 1 || c->pad != 1 || !c->relu || !(c->in == c->out) ||
+          c->fuse_proj || c->s4d)
+        return false;
+    const int hw = c1.in.H * c1.in.W;
+    return !c1.residual && c2.residual && c2.res_mode == 1 && lay(c1.in.Cp()) && lay(c1.out.C) && hw <= 128 &&
+           128 % hw == 0 && hw % 8 == 0;
+  }
+
   // Run subnet s on the rows of `in` (device count `cnt`).  The last layer writes
   // into `out_hint` when given (b >= 0).  `busy` is an outer tensor to preserve.
   dycl_status subnet(const Subnet& s, Tensor in, const int* cnt, Tensor out_hint, Tensor busy, Tensor* out) {
@@ -797,6 +811,50 @@ struct Exec {
             cudaError_t e = dycl::launch_block_fused(ba, batch, g->num_sms, st);
             prof_end();
             if (e != cudaSuccess) return cuda_fail(g, e, "launch_block_fused (in place)");
+            break;
+          }
+          if (N.skip_mode == 0 && !g->no_inplace && cur.b >= 0 && inplace_gemm_ok(T)) {
+            // in place on the NHWC GEMM (whole-sample tiles): conv1 reads the executed rows
+            // through the list into a dense scratch T, conv2 writes y (+ the fp32 stream) back
+            // over those rows, its identity shortcut read from the same rows
+            const Layer &c1 = T.layers[1], &c2 = T.layers[2];
+            const int* ecnt = g->d_counts + s;
+            const Tensor tt = pick_tensor(false, {cur});
+            if (tt.b < 0) return fail(g, DYCL_E_STATE, "internal: out of activation buffers");
+            for (int k = 0; k < 2; ++k) {
+              const Layer& L = k == 0 ? c1 : c2;
+              dycl::ConvArgs a{};
+              a.x = k == 0 ? g->buf[cur.b] : g->buf[tt.b];
+              a.w = L.d_w;
+              a.bias = L.d_b;
+              a.n_live = ecnt;
+              a.H = L.in.H; a.W = L.in.W; a.C = L.in.Cp();
+              a.Ho = L.out.H; a.Wo = L.out.W; a.Cout = L.out.C;
+              a.ksz = L.k; a.stride = L.stride; a.pad = L.pad;
+              a.K = L.K; a.Kp = L.Kp;
+              a.relu = L.relu;
+              a.in_nhwc = a.nhwc = 1;
+              if (k == 0) {
+                a.rows_in = g->d_list1;
+                a.y = g->buf[tt.b];
+              } else {
+                a.rows_out = g->d_list1;
+                a.y = g->buf[cur.b];
+                a.y32 = cur.f >= 0 ? g->buf32[cur.f] : nullptr;
+                a.res_mode = 1;
+                a.res32 = cur.f >= 0 ? g->buf32[cur.f] : nullptr;
+                a.res = g->buf[cur.b];
+                a.rH = L.out.H; a.rW = L.out.W; a.rC = L.out.C;
+              }
+              a.dbg = g->conv_dbg;
+              const double row_b = 2.0 * L.in.row_elems() + (k == 1 && cur.f >= 0 ? 10.0 : 2.0) * L.out.row_elems();
+              const double row_f = 2.0 * L.out.H * L.out.W * L.out.C * (double)(L.k * L.k * L.in.C);
+              prof_begin(DYCL_K_CONV, ecnt, row_b, row_f, 2.0 * L.out.C * L.Kp);
+              cudaError_t e = dycl::launch_conv(a, batch, g->num_sms, st, g->conv_path);
+              prof_end();
+              if (e != cudaSuccess) return cuda_fail(g, e, "launch_conv (in place)");
+            }
+            if (cur.f >= 0) pv[cur.f] = false;
             break;
           }
           Tensor bt = pick_tensor(false, {cur});

@@ -78,8 +78,8 @@ template <int BN, bool IM2COL>
 __global__ void __launch_bounds__(THREADS, 1)
     k_conv_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmY32,
-                const __grid_constant__ CUtensorMap tmY16, const __grid_constant__ CUtensorMap tmA2, const ConvArgs a,
-                const GemmPlan pl) {
+                const __grid_constant__ CUtensorMap tmY16, const __grid_constant__ CUtensorMap tmA2,
+                const __grid_constant__ CUtensorMap tmAL, const ConvArgs a, const GemmPlan pl) {
   using G = CG<BN>;
   const int S = pl.stages;
   extern __shared__ uint8_t smem_raw[];
@@ -156,7 +156,16 @@ __global__ void __launch_bounds__(THREADS, 1)
               const uint32_t bar = full0 + 8 * stage;
               ptx::mbar_arrive_expect_tx(bar, stage_tx);
               const uint32_t da = ptx::smem_u32(sA + stage * G::A_BYTES);
-              if (IM2COL)
+              if (IM2COL && a.rows_in) {
+                // whole-sample tiles through the row list: one HWo-pixel box per sample
+                const int spt = BM / HWo;
+                for (int sp = 0; sp < spt; ++sp) {
+                  const int idx = m_tile * spt + sp;
+                  const int nn = a.rows_in[idx < n_live ? idx : 0];
+                  tma_im2col_4d(da + (uint32_t)(sp * HWo * BKE * 2), &tmAL, bar, cb * BKE, -a.pad, -a.pad, nn,
+                                (uint16_t)s, (uint16_t)r);
+                }
+              } else if (IM2COL)
                 tma_im2col_4d(da, &tmA, bar, cb * BKE, wb, hb, n0, (uint16_t)s, (uint16_t)r);
               else
                 ptx::tma_load_2d(da, &tmA, bar, cb * BKE, (int)p0);
@@ -241,10 +250,17 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int m_tile = tile / n_tiles, n_tile = tile - m_tile * n_tiles;
       const long long m0 = (long long)m_tile * BM;
       const long long m = m0 + r;
-      const bool ok = m < M;
+      bool ok = m < M;
       const bool full = m0 + BM <= M;
       const int col0 = n_tile * BN;
-      const size_t rowo = (size_t)(ok ? m : 0) * a.Cout + col0;
+      long long mo = m;                                       // output row (list mode: remapped)
+      if (a.rows_in || a.rows_out) {
+        const int spt = BM / HWo;
+        const int idx = m_tile * spt + r / HWo;
+        ok = idx < n_live;
+        mo = (long long)(a.rows_out && ok ? a.rows_out[idx] : idx) * HWo + r % HWo;
+      }
+      const size_t rowo = (size_t)(ok ? mo : 0) * a.Cout + col0;
       auto res_load = [&](int c0) {
         ptx::mbar_arrive_expect_tx(rbar, res_f ? EPI_RES : EPI_RES / 2);
         ptx::tma_load_2d(ptx::smem_u32(eR), &tmR, rbar, col0 + c0, (int)m0);
@@ -449,6 +465,18 @@ cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t 
   };
   if (!mat2d(&tmB, a.w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.Kp, a.Cout, BKE, BN, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
+  CUtensorMap tmAL = tmB;
+  if (IM2COL && a.rows_in) {
+    cuuint64_t dims[4] = {(cuuint64_t)a.C, (cuuint64_t)a.W, (cuuint64_t)a.H, (cuuint64_t)rows};
+    cuuint64_t strides[3] = {(cuuint64_t)a.C * 2, (cuuint64_t)a.W * a.C * 2, (cuuint64_t)a.H * a.W * a.C * 2};
+    int lower[2] = {-a.pad, -a.pad};
+    int upper[2] = {(a.Wo - 1) * a.stride - a.pad - (a.W - 1), (a.Ho - 1) * a.stride - a.pad - (a.H - 1)};
+    cuuint32_t es[4] = {1, (cuuint32_t)a.stride, (cuuint32_t)a.stride, 1};
+    if (enc_i2c(&tmAL, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)a.x, dims, strides, lower, upper, BKE,
+                (cuuint32_t)(a.Ho * a.Wo), es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
   CUtensorMap tmA2 = tmB;
   if (a.x2) {
     if (a.stride2 > 1) {
@@ -472,7 +500,7 @@ cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t 
   const int kblocks = a.ksz * a.ksz * (a.C / BKE) + (a.x2 ? a.C2 / BKE : 0);
   const bool heavy = a.y32 != nullptr || a.res_mode == 1;
   const int avail_staged = SMEM_LIMIT - SMEM_MISC - 2 * EPI_WG;
-  pl.staged = heavy && avail_staged / CG<BN>::STAGE >= 2 && !(a.dbg & 128);
+  pl.staged = heavy && avail_staged / CG<BN>::STAGE >= 2 && !(a.dbg & 128) && !a.rows_out && !a.rows_in;
   const int avail = pl.staged ? avail_staged : SMEM_LIMIT - SMEM_MISC;
   // resident weights: one N tile whose K blocks all fit beside >= 3 A stages
   pl.bres = a.Cout == BN && kblocks > 1 && avail - kblocks * CG<BN>::B_BYTES >= 3 * CG<BN>::A_BYTES &&
@@ -508,7 +536,7 @@ cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t 
   const long long tiles = ((long long)Mmax + BM - 1) / BM * (a.Cout / BN);
   int grid = (int)(tiles < num_sms ? tiles : num_sms);
   if (grid < 1) grid = 1;
-  k_conv_gemm<BN, IM2COL><<<grid, THREADS, smem, stream>>>(tmA, tmB, tmR, tmY32, tmY16, tmA2, a, pl);
+  k_conv_gemm<BN, IM2COL><<<grid, THREADS, smem, stream>>>(tmA, tmB, tmR, tmY32, tmY16, tmA2, tmAL, a, pl);
   return cudaGetLastError();
 }
 
@@ -526,6 +554,12 @@ bool conv_gemm_eligible(const ConvArgs& a) {
                (a.W2 - 1) / a.stride2 + 1 != a.Wo))
     return false;
   if (a.res_mode == 2 && (a.r_pad_lo % 4 || a.rC % 4 || a.rH < 2 * a.Ho || a.rW < 2 * a.Wo)) return false;
+  if (a.rows_in || a.rows_out) {
+    const int hw = a.Ho * a.Wo;
+    if (hw > BM || BM % hw || hw % 8 || a.res_mode == 2 || a.x2) return false;
+    if (a.rows_in && (a.ksz == 1 && a.stride == 1 && a.pad == 0)) return false;   // tiled A path: no list form
+    if (a.rows_in && (a.H != a.Ho || a.W != a.Wo)) return false;
+  }
   return a.nhwc && a.C % BKE == 0 && a.Cout % 64 == 0 && a.K == a.ksz * a.ksz * a.C + k2 && a.Kp == a.K &&
          a.pad <= 32 && a.stride <= 8 && (a.ksz > 1 || a.stride > 1 || a.H == a.Ho);
 }

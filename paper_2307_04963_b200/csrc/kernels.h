@@ -34,6 +34,11 @@ struct ConvArgs {
   // bottleneck block: D = conv1x1(x) + proj1x1/stride2(x2)); w is then [Cout][K + C2]
   const uint16_t* x2 = nullptr;   // bf16 NHWC [n][H2][W2][C2]
   int C2 = 0, H2 = 0, W2 = 0, stride2 = 1;
+  // conv_gemm only, whole-sample tiles (128 % (Ho*Wo) == 0): sample i of the launch reads input
+  // sample rows_in[i] (im2col path) and / or writes output (and identity-shortcut) sample
+  // rows_out[i] -- the in-place form of a gate's then-branch; nullptr = dense order
+  const int* rows_in = nullptr;
+  const int* rows_out = nullptr;
   int dbg = 0;           // bit5 (32): row-tap mode opt-in; experiments only (results invalid): bit0 skip
                          // epilogue math/stores, bit1 skip MMAs, bit2 skip A loads, bit3 no residual prefetch
 };
