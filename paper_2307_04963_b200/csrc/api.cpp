@@ -116,10 +116,19 @@ struct dycl_graph_s {
   // any data (DYCL_GRAPH=0 disables; profiling runs are issued launch by launch)
   bool use_graph = true;
   cudaStream_t cap_stream = nullptr;
-  cudaGraphExec_t gexec = nullptr;
-  const void* gkey[3] = {};
-  int64_t gbatch = -1;
-  int glaunches = 0;
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    const void* key[3] = {};
+    int64_t batch = -1;
+    int launches = 0;
+    uint64_t used = 0;
+  };
+  static constexpr int NGRAPH = 4;   // dycl_run_host alternates staging slots and a tail chunk
+  GraphEntry graphs[NGRAPH];
+  uint64_t graph_clock = 0;
+  // dycl_run_host pipeline: H2D of sub-chunk k+1 and D2H of k-1 overlap the run of k
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  cudaEvent_t ev_h2d[2] = {}, ev_run[2] = {}, ev_d2h[2] = {};
   int nhwc = 0;                      // bf16 activations NHWC (decided at finalize; DYCL_NHWC=0 disables)
   int stem_s4d = 0;                  // input cast to 4x4 space-to-depth for the stem (DYCL_STEM_S4D=0 disables)
   long long* dbg_ts = nullptr;       // DYCL_TS=1: fused-block phase timestamps (development)
@@ -966,8 +975,16 @@ dycl_status dycl_graph_destroy(dycl_graph g) {
   cudaFree(g->d_logit_stage);
   cudaFree(g->d_path_stage);
   cudaFree(g->dbg_ts);
-  if (g->gexec) cudaGraphExecDestroy(g->gexec);
+  for (auto& e : g->graphs)
+    if (e.exec) cudaGraphExecDestroy(e.exec);
   if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
+  if (g->h2d_stream) cudaStreamDestroy(g->h2d_stream);
+  if (g->d2h_stream) cudaStreamDestroy(g->d2h_stream);
+  for (int i = 0; i < 2; ++i) {
+    if (g->ev_h2d[i]) cudaEventDestroy(g->ev_h2d[i]);
+    if (g->ev_run[i]) cudaEventDestroy(g->ev_run[i]);
+    if (g->ev_d2h[i]) cudaEventDestroy(g->ev_d2h[i]);
+  }
   for (auto& L : g->prof) {
     cudaEventDestroy(L.e0);
     cudaEventDestroy(L.e1);
@@ -1305,12 +1322,16 @@ static dycl_status run_impl(dycl_graph g, const float* input, int64_t batch, flo
     g->launches_per_run = ex.nlaunch;
   } else {
     const void* key[3] = {input, logits, path};
-    bool hit = g->gexec && g->gbatch == batch;
-    for (int i = 0; i < 3 && hit; ++i) hit = key[i] == g->gkey[i];
-    if (!hit) {
-      if (g->gexec) {
-        cudaGraphExecDestroy(g->gexec);
-        g->gexec = nullptr;
+    dycl_graph_s::GraphEntry* ge = nullptr;
+    for (auto& e : g->graphs)
+      if (e.exec && e.batch == batch && e.key[0] == key[0] && e.key[1] == key[1] && e.key[2] == key[2]) ge = &e;
+    if (!ge) {
+      ge = &g->graphs[0];                            // empty slot, else the least recently used
+      for (auto& e : g->graphs)
+        if (!e.exec || (ge->exec && e.used < ge->used)) ge = &e;
+      if (ge->exec) {
+        cudaGraphExecDestroy(ge->exec);
+        ge->exec = nullptr;
       }
       if (!g->cap_stream) CK(cudaStreamCreateWithFlags(&g->cap_stream, cudaStreamNonBlocking));
       CK(cudaStreamBeginCapture(g->cap_stream, cudaStreamCaptureModeThreadLocal));
@@ -1323,18 +1344,19 @@ static dycl_status run_impl(dycl_graph g, const float* input, int64_t batch, flo
         return r;
       }
       if (ec != cudaSuccess) return cuda_fail(g, ec, "graph capture");
-      const cudaError_t ei = cudaGraphInstantiate(&g->gexec, graph, 0);
+      const cudaError_t ei = cudaGraphInstantiate(&ge->exec, graph, 0);
       cudaGraphDestroy(graph);
       if (ei != cudaSuccess) {
-        g->gexec = nullptr;
+        ge->exec = nullptr;
         return cuda_fail(g, ei, "graph instantiate");
       }
-      for (int i = 0; i < 3; ++i) g->gkey[i] = key[i];
-      g->gbatch = batch;
-      g->glaunches = ex.nlaunch;
+      for (int i = 0; i < 3; ++i) ge->key[i] = key[i];
+      ge->batch = batch;
+      ge->launches = ex.nlaunch;
     }
-    CK(cudaGraphLaunch(g->gexec, st));
-    g->launches_per_run = g->glaunches;
+    ge->used = ++g->graph_clock;
+    CK(cudaGraphLaunch(ge->exec, st));
+    g->launches_per_run = ge->launches;
   }
   if (node_counts) CK(cudaMemcpyAsync(node_counts, g->d_counts, g->n_slots * sizeof(int), cudaMemcpyDeviceToDevice, st));
   return DYCL_OK;
@@ -1359,11 +1381,53 @@ dycl_status dycl_run_host(dycl_graph g, const float* input_host, int64_t batch, 
     if (dycl_status s = dmalloc(g, &g->d_logit_stage, (size_t)g->max_batch * g->K * 4)) return s;
     if (dycl_status s = dmalloc(g, &g->d_path_stage, (size_t)g->max_batch * 4)) return s;
   }
-  const size_t nin = (size_t)batch * g->input.H * g->input.W * g->input.C;
-  CK(cudaMemcpyAsync(g->d_in_stage, input_host, nin * 4, cudaMemcpyHostToDevice, st));
-  if (dycl_status s = run_impl(g, g->d_in_stage, batch, g->d_logit_stage, g->d_path_stage, nullptr, st)) return s;
-  CK(cudaMemcpyAsync(logits_host, g->d_logit_stage, (size_t)batch * g->K * 4, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(path_host, g->d_path_stage, (size_t)batch * 4, cudaMemcpyDeviceToHost, st));
+  const size_t row_in = (size_t)g->input.H * g->input.W * g->input.C;
+  // Pipelined over sub-chunks in two staging slots: H2D of sub-chunk k+1 (copy stream) and
+  // D2H of k-1 (second copy stream) overlap the run of k on the caller's stream.  Samples are
+  // independent and every kernel is batch-position independent, so the results equal one run.
+  // sub-chunk: a quarter of the batch, but >= 2048 rows for small samples (< 64 KB of input),
+  // whose runs lose efficiency below that size
+  int64_t sc = batch >= 1024 ? (batch + 3) / 4 : batch;
+  if (row_in * 4 < 64 * 1024 && sc < 2048) sc = std::min<int64_t>(batch, 2048);
+  const int64_t nsc = batch > 0 ? (batch + sc - 1) / sc : 0;
+  if (nsc <= 1) {
+    CK(cudaMemcpyAsync(g->d_in_stage, input_host, (size_t)batch * row_in * 4, cudaMemcpyHostToDevice, st));
+    if (dycl_status s = run_impl(g, g->d_in_stage, batch, g->d_logit_stage, g->d_path_stage, nullptr, st)) return s;
+    CK(cudaMemcpyAsync(logits_host, g->d_logit_stage, (size_t)batch * g->K * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(path_host, g->d_path_stage, (size_t)batch * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return DYCL_OK;
+  }
+  if (!g->h2d_stream) {
+    CK(cudaStreamCreateWithFlags(&g->h2d_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&g->d2h_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaEventCreateWithFlags(&g->ev_h2d[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&g->ev_run[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&g->ev_d2h[i], cudaEventDisableTiming));
+    }
+  }
+  for (int64_t k = 0; k < nsc; ++k) {
+    const int slot = (int)(k & 1);
+    const int64_t r0 = k * sc, rows = std::min<int64_t>(sc, batch - r0);
+    float* din = g->d_in_stage + (size_t)slot * sc * row_in;
+    float* dz = g->d_logit_stage + (size_t)slot * sc * g->K;
+    int32_t* dp = g->d_path_stage + (size_t)slot * sc;
+    if (k >= 2) CK(cudaStreamWaitEvent(g->h2d_stream, g->ev_run[slot], 0));     // run k-2 read this slot
+    CK(cudaMemcpyAsync(din, input_host + (size_t)r0 * row_in, (size_t)rows * row_in * 4, cudaMemcpyHostToDevice,
+                       g->h2d_stream));
+    CK(cudaEventRecord(g->ev_h2d[slot], g->h2d_stream));
+    CK(cudaStreamWaitEvent(st, g->ev_h2d[slot], 0));
+    if (k >= 2) CK(cudaStreamWaitEvent(st, g->ev_d2h[slot], 0));                // D2H k-2 read this slot
+    if (dycl_status s = run_impl(g, din, rows, dz, dp, nullptr, st)) return s;
+    CK(cudaEventRecord(g->ev_run[slot], st));
+    CK(cudaStreamWaitEvent(g->d2h_stream, g->ev_run[slot], 0));
+    CK(cudaMemcpyAsync(logits_host + (size_t)r0 * g->K, dz, (size_t)rows * g->K * 4, cudaMemcpyDeviceToHost,
+                       g->d2h_stream));
+    CK(cudaMemcpyAsync(path_host + r0, dp, (size_t)rows * 4, cudaMemcpyDeviceToHost, g->d2h_stream));
+    CK(cudaEventRecord(g->ev_d2h[slot], g->d2h_stream));
+  }
+  CK(cudaStreamSynchronize(g->d2h_stream));
   CK(cudaStreamSynchronize(st));
   return DYCL_OK;
 }
