@@ -143,6 +143,8 @@ struct dycl_graph_s {
   float* d_pred = nullptr;
   float* d_z = nullptr;
   float* d_gpool = nullptr;         // pooled features of wide heads [max_batch][max head C]
+  float* d_gap_part = nullptr;      // conv_gemm fused-GAP partials (sub-network outputs read by a head)
+  float* d_gap_pooled = nullptr;    // their reduction [max_batch][C]
   float* d_pool32[NBUF32] = {};     // fused-GAP features per fp32 stream buffer [max_batch][<= 32] (fused blocks)
   float* d_in_stage = nullptr;      // dycl_run_host staging
   float* d_logit_stage = nullptr;
@@ -418,6 +420,8 @@ struct Exec {
   }
 
   bool pv[dycl_graph_s::NBUF32] = {};   // d_pool32[f] holds the GAP of every live row of buf32[f]
+  int gap_f = -1;                       // buf32 index whose GAP sits in d_gap_pooled (conv_gemm fused GAP)
+  bool want_gap = false;                // the subnet being run feeds a head: fuse its GAP when possible
   const int* in_list = nullptr;         // zero-copy exit: the next subnet's first fused group reads its
                                         // input rows through this list (the survivors) instead of a gather
 
@@ -434,6 +438,7 @@ struct Exec {
       for (int i = 0; i < dycl_graph_s::NBUF32 && o.f < 0; ++i)
         if (std::find(bf.begin(), bf.end(), i) == bf.end()) o.f = i;
     if (o.f >= 0) pv[o.f] = false;               // about to be rewritten
+    if (o.f >= 0 && o.f == gap_f) gap_f = -1;
     return o;
   }
   bool fp32_stream() const { return g->precision == DYCL_PREC_FP32_STREAM; }
@@ -634,10 +639,22 @@ struct Exec {
                                             (a.res_mode == 2 ? 0.25 : 1.0) : 0.0;
       const double row_b = 2.0 * L.in.row_elems() + (o.f >= 0 ? 6.0 : 2.0) * L.out.row_elems() + res_b + fused_b;
       const double row_f = 2.0 * L.out.H * L.out.W * L.out.C * (double)(L.k * L.k * L.in.C) + fused_f;
+      // (only for wide rows: below ~128 KB of fp32 per sample the head's own GAP pass is cheaper)
+      const bool gap = want_gap && last && g->d_gap_part && a.y32 && a.nhwc && a.in_nhwc && !a.rows_out &&
+                       L.out.H * L.out.W >= 32 && 4.0 * L.out.row_elems() >= 128 * 1024 &&
+                       dycl::conv_gemm_eligible(a);
+      if (gap) a.gap_part = g->d_gap_part;
       prof_begin(DYCL_K_CONV, cnt, row_b, row_f, 2.0 * L.out.C * L.Kp);
       cudaError_t e = dycl::launch_conv(a, batch, g->num_sms, st, g->conv_path);
       prof_end();
       if (e != cudaSuccess) return cuda_fail(g, e, "launch_conv_tc");
+      if (gap) {
+        prof_begin(DYCL_K_HEAD, cnt, 4.0 * ((L.out.H * L.out.W + 31) / 32 + 1) * L.out.C + 4.0 * L.out.C, 0, 0);
+        e = dycl::launch_gap_reduce(g->d_gap_part, g->d_gap_pooled, cnt, batch, L.out.H * L.out.W, L.out.C, st);
+        prof_end();
+        if (e != cudaSuccess) return cuda_fail(g, e, "launch_gap_reduce");
+        gap_f = o.f;
+      }
       cur = o;
     }
     *out = cur;
@@ -669,6 +686,7 @@ struct Exec {
       a.wt = D.d_wt;
       a.gpool = g->d_gpool;
     }
+    if (in.f >= 0 && in.f == gap_f && g->d_gap_pooled) a.pooled = g->d_gap_pooled;   // GAP fused into the producer
     prof_begin(DYCL_K_HEAD, cnt, (a.h32 ? 4.0 : 2.0) * s.in.row_elems() + 4.0 * D.cout + 1,
                2.0 * D.cout * s.in.C + s.in.row_elems(), 2.0 * D.cout * a.C);
     cudaError_t e = dycl::launch_head(a, batch, st);
@@ -751,7 +769,11 @@ struct Exec {
       switch (N.kind) {
         case N_SEQ: {
           Tensor o;
-          if ((r = subnet(g->subnets[N.sn], cur, cnt, none, none, &o))) return r;
+          want_gap = ni + 1 < g->nodes.size() &&
+                     (g->nodes[ni + 1].kind == N_EXIT || g->nodes[ni + 1].kind == N_FINAL);
+          r = subnet(g->subnets[N.sn], cur, cnt, none, none, &o);
+          want_gap = false;
+          if (r) return r;
           cur = o;
           break;
         }
@@ -820,6 +842,7 @@ struct Exec {
             cudaError_t e = dycl::launch_block_fused(ba, batch, g->num_sms, st);
             prof_end();
             if (e != cudaSuccess) return cuda_fail(g, e, "launch_block_fused (in place)");
+            if (gap_f == cur.f) gap_f = -1;
             break;
           }
           if (N.skip_mode == 0 && !g->no_inplace && cur.b >= 0 && inplace_gemm_ok(T)) {
@@ -864,6 +887,7 @@ struct Exec {
               if (e != cudaSuccess) return cuda_fail(g, e, "launch_conv (in place)");
             }
             if (cur.f >= 0) pv[cur.f] = false;
+            if (gap_f == cur.f) gap_f = -1;
             break;
           }
           Tensor bt = pick_tensor(false, {cur});
@@ -970,6 +994,8 @@ dycl_status dycl_graph_destroy(dycl_graph g) {
   cudaFree(g->d_pred);
   cudaFree(g->d_z);
   cudaFree(g->d_gpool);
+  cudaFree(g->d_gap_part);
+  cudaFree(g->d_gap_pooled);
   for (auto* p : g->d_pool32) cudaFree(p);
   cudaFree(g->d_in_stage);
   cudaFree(g->d_logit_stage);
@@ -1300,6 +1326,25 @@ dycl_status dycl_finalize(dycl_graph g, int64_t max_batch) {
       if (N.kind != N_SEQ && g->subnets[N.sn].layers.back().d_wt) cmax = std::max(cmax, g->subnets[N.sn].in.Cp());
     if (cmax > 0)
       if (dycl_status s = dmalloc(g, &g->d_gpool, nb * (size_t)cmax * 4)) return s;
+  }
+  {
+    // conv_gemm fused GAP: the last conv of a sub-network that feeds an exit / final head
+    size_t part = 0, pooled = 0;
+    for (size_t ni = 0; ni + 1 < g->nodes.size(); ++ni) {
+      const Node& N = g->nodes[ni];
+      if (N.kind != N_SEQ || (g->nodes[ni + 1].kind != N_EXIT && g->nodes[ni + 1].kind != N_FINAL)) continue;
+      const Subnet& S = g->subnets[N.sn];
+      if (S.layers.empty() || S.layers.back().kind != L_CONV) continue;
+      const Layer& L = S.layers.back();
+      const int hw = L.out.H * L.out.W;
+      if (!g->nhwc || L.out.C % 64 || L.in.Cp() % 64 || hw < 32 || 4.0 * L.out.row_elems() < 128 * 1024) continue;
+      part = std::max(part, ((size_t)nb * hw / 32 + 2) * 2 * L.out.C);
+      pooled = std::max(pooled, (size_t)nb * L.out.C);
+    }
+    if (part && !getenv("DYCL_NO_CONV_GAP")) {
+      if (dycl_status s = dmalloc(g, &g->d_gap_part, part * 4)) return s;
+      if (dycl_status s = dmalloc(g, &g->d_gap_pooled, pooled * 4)) return s;
+    }
   }
   g->finalized = true;
   return DYCL_OK;

@@ -360,8 +360,37 @@ __global__ void __launch_bounds__(THREADS, 1)
           wg_sync(wg);
           if (res && leader && c0 + 32 < BN) res_load(c0 + 32);
         }
+        if (staged && a.gap_part) {
+          // fused GAP (a2): the chunk's fp32 y goes through the SMEM staging in every tile (the
+          // ragged last one included); thread (quarter q, column cc) sums rows 32q..32q+31 of
+          // its column in order, split at a sample boundary, into the row group's partials
+          // [rg][slot][Cout] (slot 1 = the second sample of a straddling group)
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(eO32 + sw128(r, j)) = make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
+          wg_sync(wg);
+          {
+            const int cc = lane, q = quad;
+            const long long ra = m0 + 32 * q;                  // first row of this quarter
+            const long long na = ra / HWo;
+            const long long rb = (na + 1) * HWo;              // first row of the next sample
+            float s0 = 0.f, s1 = 0.f;
+#pragma unroll 8
+            for (int i = 0; i < 32; ++i) {
+              const long long mm = ra + i;
+              if (mm >= M) break;
+              const float v = *reinterpret_cast<const float*>(eO32 + sw128(32 * q + i, cc >> 2) + (cc & 3) * 4);
+              if (mm < rb) s0 += v; else s1 += v;
+            }
+            if (ra < M) {
+              const size_t pbase = (size_t)(ra >> 5) * 2 * a.Cout + col0 + c0 + cc;
+              a.gap_part[pbase] = s0;
+              if (rb < ra + 32 && rb < M) a.gap_part[pbase + a.Cout] = s1;
+            }
+          }
+        }
         if (staged && full) {
-          if (a.y32) {
+          if (a.y32 && !a.gap_part) {
 #pragma unroll
             for (int j = 0; j < 8; ++j)
               *reinterpret_cast<float4*>(eO32 + sw128(r, j)) = make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
@@ -500,7 +529,9 @@ cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t 
   const int kblocks = a.ksz * a.ksz * (a.C / BKE) + (a.x2 ? a.C2 / BKE : 0);
   const bool heavy = a.y32 != nullptr || a.res_mode == 1;
   const int avail_staged = SMEM_LIMIT - SMEM_MISC - 2 * EPI_WG;
-  pl.staged = heavy && avail_staged / CG<BN>::STAGE >= 2 && !(a.dbg & 128) && !a.rows_out && !a.rows_in;
+  pl.staged = (heavy || a.gap_part) && avail_staged / CG<BN>::STAGE >= 2 && !(a.dbg & 128) && !a.rows_out &&
+              !a.rows_in;
+  if (a.gap_part && !pl.staged) return cudaErrorNotSupported;   // the fused GAP reads the SMEM staging
   const int avail = pl.staged ? avail_staged : SMEM_LIMIT - SMEM_MISC;
   // resident weights: one N tile whose K blocks all fit beside >= 3 A stages
   pl.bres = a.Cout == BN && kblocks > 1 && avail - kblocks * CG<BN>::B_BYTES >= 3 * CG<BN>::A_BYTES &&

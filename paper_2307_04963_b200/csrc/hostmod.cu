@@ -586,7 +586,33 @@ __global__ void k_cast_s4d(const float* __restrict__ in, uint16_t* __restrict__ 
   }
 }
 
+__global__ void k_gap_reduce(const float* __restrict__ part, float* __restrict__ pooled, const int* n_live, int HW,
+                             int C) {
+  const int n_rows = *n_live;
+  const int64_t total = (int64_t)n_rows * C;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total; u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = u / C;
+    const int c = (int)(u - n * C);
+    const int64_t r0 = n * HW, r1 = r0 + HW - 1;
+    float sum = 0.f;
+    for (int64_t rg = r0 >> 5; rg <= (r1 >> 5); ++rg) {
+      const int slot = (rg << 5) < r0 ? 1 : 0;        // group starts in the previous sample
+      sum += part[(rg * 2 + slot) * C + c];
+    }
+    pooled[n * C + c] = sum * (1.0f / HW);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_gap_reduce(const float* gap_part, float* pooled, const int* n_live, int max_rows, int HW, int C,
+                              cudaStream_t s) {
+  int64_t blocks = ((int64_t)max_rows * C + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  k_gap_reduce<<<(int)blocks, 256, 0, s>>>(gap_part, pooled, n_live, HW, C);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_cast_s4d(const float* in, uint16_t* out, int64_t n, int H, int W, int c, cudaStream_t s) {
   if (H % 4 || W % 4 || c > 4) return cudaErrorInvalidValue;
@@ -634,6 +660,28 @@ cudaError_t launch_init(int* counts, int n, int* orig, int32_t* path, int nmax, 
 
 cudaError_t launch_head(const HeadArgs& a, int max_rows, cudaStream_t s) {
   if (a.C % 8 != 0 || a.C / 8 > HEAD_THREADS) return cudaErrorInvalidValue;
+  if (a.pooled && a.wt) {                        // wide head on pooled features: FC + predicate only
+    HeadArgs b = a;
+    b.gpool = const_cast<float*>(a.pooled);
+    b.pooled = nullptr;
+    const size_t smem_fc = (size_t)FC_ROWS * b.C * sizeof(float);
+    static size_t attr_fc2 = 0;
+    if (smem_fc > 48 * 1024 && smem_fc > attr_fc2) {
+      cudaError_t e = cudaFuncSetAttribute(k_head_fc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fc);
+      if (e != cudaSuccess) return e;
+      attr_fc2 = smem_fc;
+    }
+    if (b.kind == 1 || b.C % FC_UNROLL) return cudaErrorInvalidValue;
+    int gx = (max_rows + FC_ROWS - 1) / FC_ROWS;
+    if (gx > 148 * 2) gx = 148 * 2;
+    if (gx < 1) gx = 1;
+    k_head_fc<<<dim3(gx, (b.K + HEAD_THREADS - 1) / HEAD_THREADS), HEAD_THREADS, smem_fc, s>>>(b);
+    int gp = (max_rows + 7) / 8;
+    if (gp > 148 * 8) gp = 148 * 8;
+    if (gp < 1) gp = 1;
+    k_head_pred<<<gp, 256, 0, s>>>(b);
+    return cudaGetLastError();
+  }
   if (a.pooled && !a.wt && a.K <= 32 && a.C <= 64) {
     int grid = (max_rows + 7) / 8;
     if (grid > 148 * 16) grid = 148 * 16;

@@ -39,6 +39,10 @@ struct ConvArgs {
   // rows_out[i] -- the in-place form of a gate's then-branch; nullptr = dense order
   const int* rows_in = nullptr;
   const int* rows_out = nullptr;
+  // conv_gemm only (staged epilogue): fused GAP partials, fp32 [ceil(M/32)][2][Cout] -- per
+  // 32-row group of the flat output, the column sums of y for the group's first sample (slot 0)
+  // and, when the group straddles a sample boundary, the second (slot 1); see launch_gap_reduce
+  float* gap_part = nullptr;
   int dbg = 0;           // bit5 (32): row-tap mode opt-in; experiments only (results invalid): bit0 skip
                          // epilogue math/stores, bit1 skip MMAs, bit2 skip A loads, bit3 no residual prefetch
 };
@@ -72,6 +76,11 @@ cudaError_t launch_conv(const ConvArgs& a, int max_rows, int num_sms, cudaStream
 // a0: fp32 [n][HW][C] -> bf16 [n][HW][Cp]  (Cp = roundup(C, 8), zero pad)
 cudaError_t launch_cast_pad(const float* in, uint16_t* out, int64_t n, int hw, int c, int cp,
                             cudaStream_t s);
+
+// pooled[n][c] = (sum over the 32-row groups of sample n of gap_part[group][slot][c]) / HW,
+// fixed order (the second half of conv_gemm's fused GAP)
+cudaError_t launch_gap_reduce(const float* gap_part, float* pooled, const int* n_live, int max_rows, int HW, int C,
+                              cudaStream_t s);
 
 // a0 for a space-to-depth stem: fp32 NHWC [n][H][W][c] -> bf16 [n][H/4][W/4][64], channel
 // (pr*4 + ps)*c + ci = input pixel (4P+pr, 4Q+ps) channel ci; channels >= 16c zero (c <= 4).
