@@ -592,7 +592,8 @@ bool build_plan(const ConvArgs& a, int BN, TmaPlan* P) {
 template <int BN>
 cudaError_t launch_tma_bn(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream, bool* handled) {
   *handled = false;
-  static TmaPlan P;                 // host-side scratch (the kernel parameter is copied at launch)
+  thread_local TmaPlan P;           // host-side scratch per thread (graphs may be driven from several
+                                    // host threads; the kernel parameter is copied at launch)
   P.a = a;
   if (!build_plan(a, BN, &P)) return cudaSuccess;
   EncodeTiledFn enc = get_encode();
