@@ -287,8 +287,22 @@ __global__ void __launch_bounds__(CMP_THREADS) k_compact(const uint8_t* __restri
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int ipt = (n + CMP_THREADS - 1) / CMP_THREADS;
   const int b = min(n, t * ipt), e = min(n, b + ipt);
+  // up to CMP_IPT rows per thread: flags / orig ids loaded once, unrolled (independent loads)
+  constexpr int CMP_IPT = 8;
+  const bool fast = ipt <= CMP_IPT;
+  uint8_t fr[CMP_IPT];
+  int orr[CMP_IPT];
   int c1 = 0;
-  for (int i = b; i < e; ++i) c1 += flag[i] != 0;
+  if (fast) {
+#pragma unroll
+    for (int k = 0; k < CMP_IPT; ++k) {
+      fr[k] = b + k < e ? flag[b + k] : 0;
+      orr[k] = b + k < e ? orig[b + k] : 0;
+      c1 += fr[k] != 0;
+    }
+  } else {
+    for (int i = b; i < e; ++i) c1 += flag[i] != 0;
+  }
   // block-wide exclusive scan of c1 (warp shuffles, then warp totals)
   int x = c1;
 #pragma unroll
@@ -313,7 +327,26 @@ __global__ void __launch_bounds__(CMP_THREADS) k_compact(const uint8_t* __restri
   const int total1 = total1_s;
   int o1 = excl;                                 // flag==1 rows before my chunk
   int o0 = b - excl;                             // flag==0 rows before my chunk
-  for (int i = b; i < e; ++i) {
+  if (fast) {
+#pragma unroll
+    for (int k = 0; k < CMP_IPT; ++k) {
+      if (b + k >= e) break;
+      const int i = b + k, oi = orr[k];
+      if (fr[k]) {
+        list1[o1] = i;
+        if (mode == 1) {
+          orig_next[o1] = oi;
+          path[oi] |= path_bit;
+        }
+        ++o1;
+      } else {
+        list0[o0] = i;
+        orig_next[(mode == 1 ? total1 : 0) + o0] = oi;
+        ++o0;
+      }
+    }
+  }
+  for (int i = fast ? e : b; i < e; ++i) {
     const int oi = orig[i];
     if (flag[i]) {
       list1[o1] = i;
