@@ -108,7 +108,7 @@ struct dycl_graph_s {
   int conv_path = 0;                 // 0 auto; DYCL_CONV_PATH=1 forces the cp.async kernel
   int conv_dbg = 0;                  // DYCL_CONV_DBG: timing experiments only (results invalid)
   int no_fuse = 0;                   // DYCL_NO_FUSE=1: run basic blocks as two conv launches
-  int max_fuse = 2;                  // DYCL_MAX_FUSE: basic blocks per fused launch (1..2)
+  int max_fuse = dycl::MAX_FUSED_BLOCKS;   // DYCL_MAX_FUSE: basic blocks per fused launch (1..8)
   int no_inplace = 0;                // DYCL_NO_INPLACE=1: gates gather / merge instead of running in place
   int no_zero_copy = 0;              // DYCL_NO_ZERO_COPY=1: exits gather survivors even before a fused block
   // CUDA graph of a whole run, captured on first use per (io pointers, batch) and replayed;

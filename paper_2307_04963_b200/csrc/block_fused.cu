@@ -35,9 +35,9 @@
 namespace dycl {
 namespace {
 
-constexpr int THREADS = 320;
+constexpr int THREADS = 352;          // 8 epilogue warps, sample producer, MMA, weight producer
 
-template <int C, int H, int NB>
+template <int C, int H>
 struct BCfg {
   static constexpr int W = H, HW = H * W, P = C / 8;
   static constexpr int NSUB = HW / 128;                 // UMMA tiles per sample
@@ -51,7 +51,9 @@ struct BCfg {
   static constexpr int W_BYTES = WCH * N * 16;
   static constexpr int BOX_ROWS = HW < 256 ? HW : 256;  // pixels per TMA box (box dims <= 256)
   static constexpr int NBOX = HW / BOX_ROWS;
-  static constexpr int FIXED = 1024 + 2 * OPER + 2 * NB * W_BYTES + 2 * NB * C * 4 + 512 + 256 + 8 * C * 4;
+  // two weight slots (conv1 + conv2 of one block each), streamed block by block; biases of all
+  // MAX_FUSED_BLOCKS blocks resident
+  static constexpr int FIXED = 1024 + 2 * OPER + 2 * 2 * W_BYTES + 2 * MAX_FUSED_BLOCKS * C * 4 + 512 + 256 + 8 * C * 4;
   // fp32 sample buffers (2 if they fit: y is written in place over its own input x, which is
   // also the shortcut) and a separate bf16 output staging buffer if it fits
   static constexpr int NXB = FIXED + 2 * X32_BYTES <= 227 * 1024 ? 2 : 1;
@@ -130,21 +132,22 @@ struct WMaps {
   CUtensorMap m[2 * MAX_FUSED_BLOCKS];   // conv1, conv2 row-tap weights of each fused block
 };
 
-template <int C, int H, int NB>
+template <int C, int H>
 __global__ void __launch_bounds__(THREADS, 1)
     k_block_fused(const __grid_constant__ WMaps wm, const __grid_constant__ CUtensorMap tmX,
                   const __grid_constant__ CUtensorMap tmY, const BlockArgs a) {
-  using G = BCfg<C, H, NB>;
+  using G = BCfg<C, H>;
   constexpr int W = G::W, HW = G::HW, P = G::P;
+  const int NB = a.nblk;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* x32s = smem;                                                   // [NXB][HW][C] fp32, swizzled (x, then y)
   uint8_t* xb = x32s + G::NXB * G::X32_BYTES;                             // [P][H+2][W][8] bf16
   uint8_t* tb = xb + G::OPER;
-  uint8_t* ws = tb + G::OPER;                                             // [NB][conv1, conv2] row-tap weights
-  uint8_t* ybs = ws + 2 * NB * G::W_BYTES;                                // [P][HW][8] bf16 y staging
-  float* bs = reinterpret_cast<float*>(ybs + (G::YB_SEP ? G::YB_BYTES : 0));   // [NB][b1 | b2]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(bs + 2 * NB * C);
+  uint8_t* ws = tb + G::OPER;                                             // [2 slots][conv1, conv2] row-tap weights
+  uint8_t* ybs = ws + 2 * 2 * G::W_BYTES;                                 // [P][HW][8] bf16 y staging
+  float* bs = reinterpret_cast<float*>(ybs + (G::YB_SEP ? G::YB_BYTES : 0));   // [MAX_FUSED_BLOCKS][b1 | b2]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bs + 2 * MAX_FUSED_BLOCKS * C);
   // yready[b][k]: box k of buffer b holds y (both warpgroups arrived)
   const uint32_t xfull0 = ptx::smem_u32(bars), yready0 = ptx::smem_u32(bars + 26);
   const uint32_t xb_full = xfull0 + 16, xb_empty = xb_full + 8, acc1 = xb_empty + 8, tb_full = acc1 + 8;
@@ -154,8 +157,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   // per sub-tile j: conv1 / conv2 accumulator j complete (MMA commit), and tready[j] = epilogue 1
   // has read accumulator j and written T rows of sub-tile j (conv2 sub-tile j needs j-1..j+1)
   const uint32_t acc1j0 = ptx::smem_u32(bars + 34), acc2j0 = ptx::smem_u32(bars + 42), tready0 = ptx::smem_u32(bars + 50);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 58);
-  float* gred = reinterpret_cast<float*>(bars + 60);       // [8 warps][C] fused-GAP partials (C <= 32)
+  // weight ring: wfull[s] = slot s loaded (TMA), wempty[s] = conv2 of the block in slot s done
+  const uint32_t wfull0 = ptx::smem_u32(bars + 58), wempty0 = ptx::smem_u32(bars + 60);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 62);
+  float* gred = reinterpret_cast<float*>(bars + 64);       // [8 warps][C] fused-GAP partials (C <= 32)
   static_assert(G::NBOX <= 4, "box barriers");
   static_assert(G::NSUB <= 8, "sub-tile barriers");
   constexpr uint32_t SET2 = G::NSETS == 2 ? 256u : 0u;    // TMEM column of the conv2 accumulator
@@ -182,7 +187,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     ptx::mbar_init(acc2, 1);
     ptx::mbar_init(acc1_empty, 256);
     ptx::mbar_init(acc2_empty, 256);
-    ptx::mbar_init(wfull, 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(wfull0 + 8 * i, 1);
+      ptx::mbar_init(wempty0 + 8 * i, 1);
+    }
     ptx::fence_mbar_init();
   }
   // zero the halo rows (row 0 and row H+1 of every plane) of both operand images, once
@@ -208,14 +216,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       ptx::tma_prefetch_desc(&tmX);
-      ptx::mbar_arrive_expect_tx(wfull, 2 * NB * G::W_BYTES);
-#pragma unroll
-      for (int i = 0; i < 2 * NB; ++i)
-        asm volatile(
-            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
-            "%5}], [%2];" ::"r"(ptx::smem_u32(ws + i * G::W_BYTES)),
-            "l"(&wm.m[i]), "r"(wfull), "r"(0), "r"(0), "r"(0)
-            : "memory");
       // The producer owns both fp32 sample buffers: it loads sample it into buffer it % 2, and
       // once the epilogue has written y over it (yready), stores y (+ the bf16 copy), waits for
       // the stores to have READ SMEM and refills the buffer with sample it + 2 right away.
@@ -275,15 +275,19 @@ __global__ void __launch_bounds__(THREADS, 1)
     constexpr uint32_t IDESC = ptx::make_idesc_bf16(128, G::N);
     const uint64_t xdesc = ptx::make_smem_desc(ptx::smem_u32(xb), 0, G::PLANE, 128);
     const uint64_t tdesc = ptx::make_smem_desc(ptx::smem_u32(tb), 0, G::PLANE, 128);
-    ptx::mbar_wait(wfull, 0);
     int it = 0;
     for (int smp = blockIdx.x; smp < n_live; smp += gridDim.x, ++it) {
       const bool mstamp = a.ts && blockIdx.x == 0 && lane == 0 && it < 8;
       for (int blk = 0; blk < NB; ++blk) {
         const int k = it * NB + blk;
         const uint32_t ph = k & 1;
-        const uint64_t w1d = ptx::make_smem_desc(ptx::smem_u32(ws + (2 * blk) * G::W_BYTES), 0, G::N * 16, 128);
-        const uint64_t w2d = ptx::make_smem_desc(ptx::smem_u32(ws + (2 * blk + 1) * G::W_BYTES), 0, G::N * 16, 128);
+        // weight slot of this occurrence: resident per block when NB <= 2, else the ring
+        const bool wres = NB <= 2;
+        const int ws_slot = wres ? blk : (k & 1);
+        ptx::mbar_wait(wfull0 + 8 * ws_slot, wres ? 0u : (uint32_t)((k >> 1) & 1));
+        const uint64_t w1d = ptx::make_smem_desc(ptx::smem_u32(ws + (2 * ws_slot) * G::W_BYTES), 0, G::N * 16, 128);
+        const uint64_t w2d =
+            ptx::make_smem_desc(ptx::smem_u32(ws + (2 * ws_slot + 1) * G::W_BYTES), 0, G::N * 16, 128);
         // conv1 sub-tile j: its columns were drained by the previous epilogue 2 (shared set) or the
         // previous epilogue 1 (two sets); committed per sub-tile so epilogue 1 starts on sub-tile 0
         // while the tensor core works on the rest
@@ -329,9 +333,40 @@ __global__ void __launch_bounds__(THREADS, 1)
                                      (uint32_t)((r | q) != 0));
           ptx::mma_commit_elect(acc2j0 + 8 * j);
         }
+        if (!wres) ptx::mma_commit_elect(wempty0 + 8 * ws_slot);   // free the ring slot once conv2 ends
         __syncwarp();
         if (mstamp && blk == NB - 1) a.ts[it * 16 + 9] = clock64();
       }
+    }
+  } else if (warp == 10) {
+    // ------------------------------------------------------------ weight producer
+    // the fused blocks' weights stream through two SMEM slots, one block ahead of the MMA
+    if (lane == 0 && NB <= 2) {                      // resident: each block's weights once
+      for (int blk = 0; blk < NB; ++blk) {
+        ptx::mbar_arrive_expect_tx(wfull0 + 8 * blk, 2 * G::W_BYTES);
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          asm volatile(
+              "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+              "%5}], [%2];" ::"r"(ptx::smem_u32(ws + (2 * blk + h) * G::W_BYTES)),
+              "l"(&wm.m[2 * blk + h]), "r"(wfull0 + 8 * blk), "r"(0), "r"(0), "r"(0)
+              : "memory");
+      }
+    } else if (lane == 0) {
+      int k = 0;
+      for (int smp = blockIdx.x; smp < n_live; smp += gridDim.x)
+        for (int blk = 0; blk < NB; ++blk, ++k) {
+          const int sl = k & 1;
+          if (k >= 2) ptx::mbar_wait(wempty0 + 8 * sl, ((k - 2) >> 1) & 1);
+          ptx::mbar_arrive_expect_tx(wfull0 + 8 * sl, 2 * G::W_BYTES);
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+                "%5}], [%2];" ::"r"(ptx::smem_u32(ws + (2 * sl + h) * G::W_BYTES)),
+                "l"(&wm.m[2 * blk + h]), "r"(wfull0 + 8 * sl), "r"(0), "r"(0), "r"(0)
+                : "memory");
+        }
     }
   } else {
     // ------------------------------------------------------------ converters / epilogues
@@ -539,13 +574,13 @@ EncodeTiledFn enc_fn() {
   return fn;
 }
 
-template <int C, int H, int NB>
+template <int C, int H>
 cudaError_t launch_ch(const BlockArgs& a, int max_rows, int num_sms, cudaStream_t stream) {
-  using G = BCfg<C, H, NB>;
+  using G = BCfg<C, H>;
   EncodeTiledFn enc = enc_fn();
   if (!enc) return cudaErrorNotSupported;
   WMaps wm;
-  for (int i = 0; i < 2 * NB; ++i) {
+  for (int i = 0; i < 2 * a.nblk; ++i) {
     const uint16_t* w = (i & 1) ? a.w2_rt[i / 2] : a.w1_rt[i / 2];
     cuuint64_t dims[3] = {8, (cuuint64_t)G::N, (cuuint64_t)G::WCH};
     cuuint64_t strides[2] = {(cuuint64_t)G::KP_RT * 2, 16};
@@ -571,14 +606,13 @@ cudaError_t launch_ch(const BlockArgs& a, int max_rows, int num_sms, cudaStream_
   }
   static bool attr = false;
   if (!attr) {
-    cudaError_t e =
-        cudaFuncSetAttribute(k_block_fused<C, H, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(k_block_fused<C, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   int grid = max_rows < num_sms ? max_rows : num_sms;
   if (grid < 1) grid = 1;
-  k_block_fused<C, H, NB><<<grid, THREADS, G::SMEM, stream>>>(wm, tm[0], tm[1], a);
+  k_block_fused<C, H><<<grid, THREADS, G::SMEM, stream>>>(wm, tm[0], tm[1], a);
   return cudaGetLastError();
 }
 
@@ -588,12 +622,8 @@ bool block_fused_eligible(int C, int H, int W) { return H == W && ((C == 16 && H
 
 cudaError_t launch_block_fused(const BlockArgs& a, int max_rows, int num_sms, cudaStream_t stream) {
   if (a.nblk < 1 || a.nblk > MAX_FUSED_BLOCKS) return cudaErrorInvalidValue;
-  if (a.C == 16 && a.H == 32 && a.W == 32)
-    return a.nblk == 2 ? launch_ch<16, 32, 2>(a, max_rows, num_sms, stream)
-                       : launch_ch<16, 32, 1>(a, max_rows, num_sms, stream);
-  if (a.C == 32 && a.H == 16 && a.W == 16)
-    return a.nblk == 2 ? launch_ch<32, 16, 2>(a, max_rows, num_sms, stream)
-                       : launch_ch<32, 16, 1>(a, max_rows, num_sms, stream);
+  if (a.C == 16 && a.H == 32 && a.W == 32) return launch_ch<16, 32>(a, max_rows, num_sms, stream);
+  if (a.C == 32 && a.H == 16 && a.W == 16) return launch_ch<32, 16>(a, max_rows, num_sms, stream);
   return cudaErrorNotSupported;
 }
 

@@ -163,7 +163,7 @@ cudaError_t launch_maxpool(const PoolArgs& a, int max_rows, int num_sms, cudaStr
 // Fused residual basic blocks (block_fused.cu): nblk consecutive blocks y = relu(conv2(relu(conv1(x)))
 // + x), 3x3 / stride 1, whole sample per CTA iteration kept in SMEM across the blocks, fp32 stream
 // in/out (+ optional bf16 channel-planar copy of the last block's output).
-constexpr int MAX_FUSED_BLOCKS = 2;
+constexpr int MAX_FUSED_BLOCKS = 8;
 struct BlockArgs {
   const float* x32;        // fp32 NHWC [n][H][W][C] (the first block's input, also its shortcut)
   const int32_t* list;     // optional row index list (input row = list[i]), nullptr = identity
