@@ -634,10 +634,15 @@ struct Exec {
         a.w_rt = nullptr;
         a.in_nhwc = a.nhwc = 1;
       }
+      // the fused block group that follows reads only the fp32 stream: skip the bf16 copy
+      const bool skip_b = !last && o.f >= 0 && fp32_stream() && !g->no_fuse && !L.s4d &&
+                          s.layers[li + 1].kind == L_BLOCK && fusable(s, li + 1);
+      if (skip_b) a.y = nullptr;
       a.dbg = g->conv_dbg;
       const double res_b = a.res_mode ? (a.res32 ? 4.0 : 2.0) * L.res_shape.row_elems() *
                                             (a.res_mode == 2 ? 0.25 : 1.0) : 0.0;
-      const double row_b = 2.0 * L.in.row_elems() + (o.f >= 0 ? 6.0 : 2.0) * L.out.row_elems() + res_b + fused_b;
+      const double row_b = 2.0 * L.in.row_elems() + (o.f >= 0 ? (a.y ? 6.0 : 4.0) : 2.0) * L.out.row_elems() + res_b +
+                           fused_b;
       const double row_f = 2.0 * L.out.H * L.out.W * L.out.C * (double)(L.k * L.k * L.in.C) + fused_f;
       // (only for wide rows: below ~128 KB of fp32 per sample the head's own GAP pass is cheaper)
       const bool gap = want_gap && last && g->d_gap_part && a.y32 && a.nhwc && a.in_nhwc && !a.rows_out &&
@@ -655,6 +660,7 @@ struct Exec {
         if (e != cudaSuccess) return cuda_fail(g, e, "launch_gap_reduce");
         gap_f = o.f;
       }
+      if (!a.y) o.b = -1;                            // only the fp32 copy was written
       cur = o;
     }
     *out = cur;
