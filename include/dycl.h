@@ -307,6 +307,9 @@ dycl_status dycl_s2s_profile_read(dycl_s2s s, int32_t max_n, int32_t* kind, floa
  *         4 = NHWC layout: x [n][H][W][C], res [n][Ho][Wo][c_out], y [n][Ho][Wo][c_out], run by
  *         the im2col-TMA GEMM (C % 64 == 0, c_out % 64 == 0; the 8-channel stem by the planar
  *         kernels, which coincide with NHWC at C = 8)
+ *         5 = path 4 with the row-tap weight copy supplied: 3x3 / stride 1 / pad 1 layers whose
+ *         samples tile 128-row GEMM tiles whole (W | 32, c_out = 64) take the GEMM's row-tap
+ *         form (horizontal taps along N, lane-shuffle combine)
  * g supplies the device (any created graph).  Errors: INVALID_ARG, UNSUPPORTED, CUDA. */
 dycl_status dycl_debug_conv2d(dycl_graph g, int64_t n, int H, int W, int C, const uint16_t* w, const float* bias,
                               int c_out, int k, int stride, int pad, int relu, const void* res, int res_mode,

@@ -132,6 +132,7 @@ struct dycl_graph_s {
   int nhwc = 0;                      // bf16 activations NHWC (decided at finalize; DYCL_NHWC=0 disables)
   int stem_s4d = 0;                  // input cast to 4x4 space-to-depth for the stem (DYCL_STEM_S4D=0 disables)
   long long* dbg_ts = nullptr;       // DYCL_TS=1: fused-block phase timestamps (development)
+  int dbg_ts_conv = 0;               // DYCL_TS_CONV=k: record conv_gemm phases of the k-th conv launch
   int dbg_ts_pick = 0;               // DYCL_TS=k > 1: record the k-th fused launch of a run (else the last)
   long long max_row_elems = 0;
   int* d_counts = nullptr;
@@ -394,6 +395,7 @@ struct Exec {
   int32_t* out_path;
   int slot = 1;               // next free count slot
   int fused_launch = 0;       // fused-block launches so far in this run (DYCL_TS selection)
+  int conv_launch = 0;        // conv launches so far in this run (DYCL_TS_CONV selection)
   int nlaunch = 0;
 
   void prof_begin(int kind, const int* cnt, double bpr, double fpr, double bfix) {
@@ -649,6 +651,8 @@ struct Exec {
                        L.out.H * L.out.W >= 32 && 4.0 * L.out.row_elems() >= 128 * 1024 &&
                        dycl::conv_gemm_eligible(a);
       if (gap) a.gap_part = g->d_gap_part;
+      ++conv_launch;
+      if (g->dbg_ts_conv && g->dbg_ts_conv == conv_launch) a.ts = g->dbg_ts;
       prof_begin(DYCL_K_CONV, cnt, row_b, row_f, 2.0 * L.out.C * L.Kp);
       cudaError_t e = dycl::launch_conv(a, batch, g->num_sms, st, g->conv_path);
       prof_end();
@@ -864,6 +868,8 @@ struct Exec {
               dycl::ConvArgs a{};
               a.x = k == 0 ? g->buf[cur.b] : g->buf[tt.b];
               a.w = L.d_w;
+              a.w_rt = L.d_wrt;
+              a.Kp_rt = L.Kp_rt;
               a.bias = L.d_b;
               a.n_live = ecnt;
               a.H = L.in.H; a.W = L.in.W; a.C = L.in.Cp();
@@ -963,6 +969,10 @@ dycl_status dycl_graph_create(int cuda_device, int in_h, int in_w, int in_c, dyc
   if (getenv("DYCL_TS")) {
     cudaMalloc(&g->dbg_ts, 8 * 16 * sizeof(long long));
     g->dbg_ts_pick = atoi(getenv("DYCL_TS")) > 1 ? atoi(getenv("DYCL_TS")) : 0;
+    if (getenv("DYCL_TS_CONV")) {
+      g->dbg_ts_conv = atoi(getenv("DYCL_TS_CONV"));
+      g->dbg_ts_pick = -1;                         // no fused-block launch records
+    }
     cudaMemset(g->dbg_ts, 0, 8 * 16 * sizeof(long long));
   }
   cudaSetDevice(cuda_device);
@@ -1245,19 +1255,17 @@ dycl_status dycl_finalize(dycl_graph g, int64_t max_batch) {
   // channel counts (the im2col GEMM's operand boxes are 64 channels wide) and no gate needs an
   // option-A skip copy; channel-planar otherwise (the CIFAR-width kernels).
   {
-    bool any = false, ok = g->input.Cp() == 8;
+    bool ok = g->input.Cp() == 8;
     // per-tensor rule (Exec::lay): C % 64 == 0 tensors are NHWC; a conv reading one runs on the
     // im2col GEMM, so its output width must be a multiple of 64 too (else: planar graph)
     for (size_t i = 0; i < g->subnets.size() && ok; ++i)
       if (planned[i])
         for (const Layer& L : g->subnets[i].layers)
           if ((L.kind == L_CONV || L.kind == L_PROJ) && L.in.Cp() % 64 == 0 && !(L.in.H == 1 && L.in.W == 1)) {
-            any = true;
             ok = ok && L.out.C % 64 == 0 && (L.res_mode != 2 || (L.res_shape.Cp() % 4 == 0));
           }
     const char* env = getenv("DYCL_NHWC");
     g->nhwc = ok && !(env && atoi(env) == 0);
-    (void)any;
     // space-to-depth stem: the first layer run is a 7x7 / stride-2 / pad-3 conv on <= 4 input
     // channels followed by a 3x3 / stride-2 / pad-1 max pool (the ImageNet ResNet stem)
     g->stem_s4d = 0;
@@ -1551,7 +1559,7 @@ dycl_status dycl_debug_conv2d(dycl_graph g, int64_t n, int H, int W, int C, cons
   cudaMemcpy(db, bias, (size_t)c_out * 4, cudaMemcpyHostToDevice);
   uint16_t* dwr = nullptr;
   int kp_rt = 0;
-  if (k == 3 && stride == 1 && pad == 1 && path != 3 && path != 4) {
+  if (k == 3 && stride == 1 && pad == 1 && path != 3 && path != 4) {   // (path 5 included)
     kp_rt = (3 * C + 63) / 64 * 64;
     std::vector<uint16_t> wr((size_t)3 * c_out * kp_rt);
     dycl::pack_rowtap(wp.data(), c_out, Kp, C, wr.data(), kp_rt);
@@ -1566,8 +1574,10 @@ dycl_status dycl_debug_conv2d(dycl_graph g, int64_t n, int H, int W, int C, cons
   a.rH = 2 * Ho; a.rW = 2 * Wo; a.rC = c_out / 2; a.r_pad_lo = c_out / 4;
   if (res_mode == 1) { a.rH = Ho; a.rW = Wo; a.rC = c_out; a.r_pad_lo = 0; }
   if (path == 2 && dwr) a.dbg |= 32;          // path 2 exercises the row-tap mode where eligible
-  a.nhwc = a.in_nhwc = a.res_nhwc = path == 4;   // path 4: NHWC tensors, im2col GEMM (8-channel stem: planar kernels)
-  cudaError_t e = n > 0 ? dycl::launch_conv(a, (int)n, g->num_sms, 0, path == 3 ? 2 : path == 4 ? 0 : path)
+  // path 4: NHWC tensors, im2col GEMM (8-channel stem: planar kernels); 5: the same with row-tap
+  // weights supplied (the GEMM's row-tap form where eligible)
+  a.nhwc = a.in_nhwc = a.res_nhwc = path == 4 || path == 5;
+  cudaError_t e = n > 0 ? dycl::launch_conv(a, (int)n, g->num_sms, 0, path == 3 ? 2 : path >= 4 ? 0 : path)
                         : cudaSuccess;
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   cudaFree(dwr);

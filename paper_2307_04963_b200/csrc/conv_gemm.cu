@@ -14,7 +14,7 @@
 // ordered (r, s, c)): a 2-D tiled box.  Both land in SMEM in the 128-byte-swizzled K-major
 // layout; tcgen05.mma 128 x BN x 16 reads them by descriptor.
 //
-// Persistent warp-specialised CTA (one per SM): warp 8 = TMA producer (one lane), warp 9 =
+// Persistent warp-specialised CTA (one per SM): warps 8, 10, 11 = TMA producers (k-blocks round-robin), warp 9 =
 // TMEM allocator + MMA issuer (one lane), warps 0-7 = two epilogue warpgroups alternating
 // tiles over two TMEM accumulators.  The fused epilogue adds bias (+ identity shortcut from
 // the fp32 residual stream or the bf16 tensor), applies ReLU and writes bf16 NHWC (+ the fp32
@@ -31,13 +31,12 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BKE = 64;                 // K elements per stage: one 128-byte swizzle row
-constexpr int THREADS = 320;
+constexpr int THREADS = 384;   // warps 0-7 epilogue, 8/10/11 TMA producers, 9 MMA
+constexpr int NPROD = 3;
 
 template <int BN>
 struct CG {
   static constexpr int A_BYTES = BM * BKE * 2;
-  static constexpr int B_BYTES = BN * BKE * 2;
-  static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
 };
 constexpr int MAX_STAGES = 8;
@@ -53,6 +52,9 @@ struct GemmPlan {
   int staged;      // 1: epilogue through SMEM + TMA stores (and TMA residual loads)
   int bres;        // 1: all weights resident in SMEM (single N tile, loaded once per CTA); the
                    //    ring then carries only A tiles (cuts L2->SMEM bytes by B/(A+B) per tile)
+  int tshift;      // 1: stride-1 'same' conv whose whole samples tile BM: tap (r, s) of the A tile is
+                   //    one TILED 4-d box {BKE, W, H, samples} at (c, s - pad, r - pad, n0) with zero
+                   //    out-of-bounds fill -- same SMEM image as the im2col box, far fewer TMA requests
 };
 
 __device__ __forceinline__ void tma_im2col_4d(uint32_t dst, const void* tmap, uint32_t bar, int c, int w, int h, int n,
@@ -64,6 +66,13 @@ __device__ __forceinline__ void tma_im2col_4d(uint32_t dst, const void* tmap, ui
       : "memory");
 }
 
+__device__ __forceinline__ void ts_mark(const ConvArgs& a, int k) {   // development timeline
+  if (a.ts && blockIdx.x < 8) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.ts[blockIdx.x * 16 + k] = (long long)t;
+  }
+}
 __device__ __forceinline__ uint32_t pk2(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -74,20 +83,29 @@ __device__ __forceinline__ uint32_t sw128(int r, int j) { return (uint32_t)(r * 
 // 16-byte chunk j of row r with 64-byte rows, 64B swizzle (chunk bits XOR address bits [7,9))
 __device__ __forceinline__ uint32_t sw64(int r, int j) { return (uint32_t)(r * 64 + ((j ^ ((r >> 1) & 3)) << 4)); }
 
-template <int BN, bool IM2COL>
+// RT ("row-tap"): 3x3 / stride-1 'same' conv on whole-sample tiles (GemmPlan::tshift) with
+// the three horizontal taps stacked along N (weights pack_rowtap, N = 3 * BN) and only the
+// three vertical taps along K: a third of the A-operand traffic; the epilogue combines
+// out(x) = T0(x-1) + T1(x) + T2(x+1) with lane shuffles (image rows never straddle a warp).
+template <int BN, bool IM2COL, bool RT = false>
 __global__ void __launch_bounds__(THREADS, 1)
     k_conv_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmY32,
                 const __grid_constant__ CUtensorMap tmY16, const __grid_constant__ CUtensorMap tmA2,
                 const __grid_constant__ CUtensorMap tmAL, const ConvArgs a, const GemmPlan pl) {
   using G = CG<BN>;
+  constexpr int NA = RT ? 3 * BN : BN;                     // MMA N = accumulator columns per tile
+  constexpr int BB = NA * BKE * 2;                         // B bytes per k-block
+  constexpr int TCOLS = RT ? 512 : G::TMEM_COLS;
   const int S = pl.stages;
+  const int kblocks1 = (RT ? a.ksz : a.ksz * a.ksz) * (a.C / BKE);
+  const int kblocks = kblocks1 + (a.x2 ? a.C2 / BKE : 0);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * G::A_BYTES;                     // ring B tiles, or [kblocks][BN][128 B] resident
-  const int b_slots = pl.bres ? a.Kp / BKE : S;
-  uint8_t* sE = sB + b_slots * G::B_BYTES;                  // [2 WG][res | o32 | o16] when staged
+  const int b_slots = pl.bres ? kblocks : S;
+  uint8_t* sE = sB + b_slots * BB;                  // [2 WG][res | o32 | o16] when staged
   uint64_t* bars = reinterpret_cast<uint64_t*>(sE + (pl.staged ? 2 * EPI_WG : 0));
   const uint32_t full0 = ptx::smem_u32(bars);
   const uint32_t empty0 = full0 + 8 * S;
@@ -99,16 +117,28 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_live = a.n_live ? *a.n_live : a.n_static;
+  // loop-invariant arguments laundered into registers: the asm "memory" clobbers in the
+  // pipeline loops otherwise make the compiler re-read them from the parameter bank on every
+  // iteration (constant-cache latency on the producer / MMA critical path)
+  auto reg = [](int v) {
+    int r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+    return r;
+  };
+  const int dbg = reg(a.dbg), pad = reg(a.pad), cstride = reg(a.stride), Wo = reg(a.Wo), ksz = reg(a.ksz);
+  const int stride2 = reg(a.stride2);
+  const int* const rows_in = reinterpret_cast<const int*>(
+      (uintptr_t)(((unsigned long long)reg((int)((uintptr_t)a.rows_in >> 32)) << 32) |
+                  (unsigned)reg((int)(uintptr_t)a.rows_in)));
   const int HWo = a.Ho * a.Wo;
   const long long M = (long long)n_live * HWo;
   const int m_tiles = (int)((M + BM - 1) / BM);
   const int n_tiles = a.Cout / BN;
   const int num_tiles = m_tiles * n_tiles;
   const int cblocks = a.C / BKE;
-  const int kblocks1 = a.ksz * a.ksz * cblocks;
-  const int kblocks = kblocks1 + (a.x2 ? a.C2 / BKE : 0);
 
   if (threadIdx.x == 0) {
+    ts_mark(a, 0);
     for (int i = 0; i < S; ++i) {
       ptx::mbar_init(full0 + 8 * i, 1);
       ptx::mbar_init(empty0 + 8 * i, 1);
@@ -121,84 +151,123 @@ __global__ void __launch_bounds__(THREADS, 1)
     ptx::mbar_init(bfull, 1);
     ptx::fence_mbar_init();
   }
-  if (warp == 9) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), G::TMEM_COLS);
+  if (warp == 9) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), TCOLS);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) ts_mark(a, 1);
 
-  if (warp == 8) {
-    // ------------------------------------------------------------ TMA producer
+  if (warp == 8 || warp >= 10) {
+    // ------------------------------------------------------------ TMA producers
+    // A single issuing warp runs at ~9 cycles per instruction (one dependent stream), i.e.
+    // ~400-600 cycles per k-block -- slower than the tensor core eats a 128x64x64 block
+    // (measured with a globaltimer timeline).  NPROD warps on different SM sub-partitions take
+    // the k-blocks round-robin; each walks the whole loop (waits by all lanes, issue by lane 0).
+    const int prod = warp == 8 ? 0 : warp - 9;
     if (lane == 0) {
       ptx::tma_prefetch_desc(&tmA);
       ptx::tma_prefetch_desc(&tmB);
       if (a.x2) ptx::tma_prefetch_desc(&tmA2);
-      if (pl.bres) {
-        ptx::mbar_arrive_expect_tx(bfull, (uint32_t)(kblocks * G::B_BYTES));
+      if (pl.bres && prod == 0) {
+        ptx::mbar_arrive_expect_tx(bfull, (uint32_t)(kblocks * BB));
         for (int kb = 0; kb < kblocks; ++kb)
-          ptx::tma_load_2d(ptx::smem_u32(sB + kb * G::B_BYTES), &tmB, bfull, kb * BKE, 0);
+          ptx::tma_load_2d(ptx::smem_u32(sB + kb * BB), &tmB, bfull, kb * BKE, 0);
       }
-      const uint32_t stage_tx = pl.bres ? (uint32_t)G::A_BYTES : (uint32_t)G::STAGE;
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m_tile = tile / n_tiles, n_tile = tile - m_tile * n_tiles;
-        const long long p0 = (long long)m_tile * BM;
-        const int n0 = (int)(p0 / HWo);
-        const int rem = (int)(p0 - (long long)n0 * HWo);
-        const int ho0 = rem / a.Wo, wo0 = rem - (rem / a.Wo) * a.Wo;
-        const int wb = wo0 * a.stride - a.pad, hb = ho0 * a.stride - a.pad;
-        int kb = 0;
-        for (int r = 0; r < a.ksz; ++r)
-          for (int s = 0; s < a.ksz; ++s)
-            for (int cb = 0; cb < cblocks; ++cb, ++kb) {
-              ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1);
+    }
+    __syncwarp();
+    const uint32_t stage_tx = pl.bres ? (uint32_t)G::A_BYTES : (uint32_t)(G::A_BYTES + BB);
+    // this producer's k-blocks: global sequence numbers prod, prod + NPROD, ...
+    // at most S producers: a producer then never runs two ring rounds ahead of a stage's
+    // empty barrier, which a parity wait could not tell apart
+    const int np = NPROD < S ? NPROD : S;
+    int stage = prod;
+    uint32_t phase = 0;
+    int rr = 0;                                    // round-robin owner of the next k-block
+    auto advance = [&]() {
+      stage += np;
+      while (stage >= S) {
+        stage -= S;
+        phase ^= 1;
+      }
+    };
+    for (int tile = blockIdx.x; tile < (prod >= np ? 0 : num_tiles); tile += gridDim.x) {
+      if (lane == 0 && prod == 0 && tile == (int)blockIdx.x + (int)gridDim.x) ts_mark(a, 5);
+      const int m_tile = tile / n_tiles, n_tile = tile - m_tile * n_tiles;
+      const long long p0 = (long long)m_tile * BM;
+      const int n0 = (int)(p0 / HWo);
+      const int rem = (int)(p0 - (long long)n0 * HWo);
+      const int ho0 = rem / Wo, wo0 = rem - (rem / Wo) * Wo;
+      const int wb = wo0 * cstride - pad, hb = ho0 * cstride - pad;
+      int kb = 0;
+      for (int r = 0; r < ksz; ++r)
+        for (int s = RT ? 1 : 0; s < (RT ? 2 : ksz); ++s)
+          for (int cb = 0; cb < cblocks; ++cb, ++kb) {
+            const bool mine = rr == prod;
+            rr = rr + 1 == np ? 0 : rr + 1;
+            if (!mine) continue;
+            ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1);
+            if (lane == 0) {
               const uint32_t bar = full0 + 8 * stage;
-              ptx::mbar_arrive_expect_tx(bar, stage_tx);
               const uint32_t da = ptx::smem_u32(sA + stage * G::A_BYTES);
-              if (IM2COL && a.rows_in) {
-                // whole-sample tiles through the row list: one HWo-pixel box per sample
-                const int spt = BM / HWo;
-                for (int sp = 0; sp < spt; ++sp) {
-                  const int idx = m_tile * spt + sp;
-                  const int nn = a.rows_in[idx < n_live ? idx : 0];
-                  tma_im2col_4d(da + (uint32_t)(sp * HWo * BKE * 2), &tmAL, bar, cb * BKE, -a.pad, -a.pad, nn,
-                                (uint16_t)s, (uint16_t)r);
+              if (dbg & 1024) {                    // timing experiment: no operand loads
+                ptx::mbar_arrive(bar);
+              } else {
+                ptx::mbar_arrive_expect_tx(bar, stage_tx);
+                if (IM2COL && rows_in) {
+                  // whole-sample tiles through the row list: one HWo-pixel box per sample
+                  const int spt = BM / HWo;
+                  for (int sp = 0; sp < spt; ++sp) {
+                    const int idx = m_tile * spt + sp;
+                    const int nn = rows_in[idx < n_live ? idx : 0];
+                    if (pl.tshift)
+                      ptx::tma_load_4d(da + (uint32_t)(sp * HWo * BKE * 2), &tmAL, bar, cb * BKE, s - pad,
+                                       r - pad, nn);
+                    else
+                      tma_im2col_4d(da + (uint32_t)(sp * HWo * BKE * 2), &tmAL, bar, cb * BKE, -pad, -pad, nn,
+                                    (uint16_t)s, (uint16_t)r);
+                  }
+                } else if (IM2COL && pl.tshift) {
+                  ptx::tma_load_4d(da, &tmA, bar, cb * BKE, s - pad, r - pad, n0);
+                } else if (IM2COL) {
+                  tma_im2col_4d(da, &tmA, bar, cb * BKE, wb, hb, n0, (uint16_t)s, (uint16_t)r);
+                } else {
+                  ptx::tma_load_2d(da, &tmA, bar, cb * BKE, (int)p0);
                 }
-              } else if (IM2COL)
-                tma_im2col_4d(da, &tmA, bar, cb * BKE, wb, hb, n0, (uint16_t)s, (uint16_t)r);
-              else
-                ptx::tma_load_2d(da, &tmA, bar, cb * BKE, (int)p0);
-              if (!pl.bres)
-                ptx::tma_load_2d(ptx::smem_u32(sB + stage * G::B_BYTES), &tmB, bar, kb * BKE, n_tile * BN);
-              if (++stage == S) {
-                stage = 0;
-                phase ^= 1;
+                if (!pl.bres)
+                  ptx::tma_load_2d(ptx::smem_u32(sB + stage * BB), &tmB, bar, kb * BKE, n_tile * NA);
               }
             }
-        // fused projection shortcut: K blocks of the second operand (1x1, stride2)
-        for (int cb = 0; kb < kblocks; ++cb, ++kb) {
-          ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1);
+            __syncwarp();
+            advance();
+          }
+      // fused projection shortcut: K blocks of the second operand (1x1, stride2)
+      for (int cb = 0; kb < kblocks; ++cb, ++kb) {
+        const bool mine = rr == prod;
+        rr = rr + 1 == np ? 0 : rr + 1;
+        if (!mine) continue;
+        ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1);
+        if (lane == 0) {
           const uint32_t bar = full0 + 8 * stage;
           ptx::mbar_arrive_expect_tx(bar, stage_tx);
           const uint32_t da = ptx::smem_u32(sA + stage * G::A_BYTES);
-          if (a.stride2 > 1)
-            tma_im2col_4d(da, &tmA2, bar, cb * BKE, wo0 * a.stride2, ho0 * a.stride2, n0, 0, 0);
+          if (stride2 > 1)
+            tma_im2col_4d(da, &tmA2, bar, cb * BKE, wo0 * stride2, ho0 * stride2, n0, 0, 0);
           else
             ptx::tma_load_2d(da, &tmA2, bar, cb * BKE, (int)p0);
           if (!pl.bres)
-            ptx::tma_load_2d(ptx::smem_u32(sB + stage * G::B_BYTES), &tmB, bar, kb * BKE, n_tile * BN);
-          if (++stage == S) {
-            stage = 0;
-            phase ^= 1;
-          }
+            ptx::tma_load_2d(ptx::smem_u32(sB + stage * BB), &tmB, bar, kb * BKE, n_tile * NA);
         }
+        __syncwarp();
+        advance();
       }
     }
+    if (lane == 0 && prod == 0) ts_mark(a, 6);
   } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t IDESC = ptx::make_idesc_bf16(BM, BN);
+    constexpr uint32_t IDESC = ptx::make_idesc_bf16(BM, NA);
     if (pl.bres) ptx::mbar_wait(bfull, 0);
+    if (lane == 0) ts_mark(a, 2);
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
@@ -206,15 +275,17 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int acc = it & 1;
       ptx::mbar_wait(tempty0 + 8 * acc, ((it >> 1) & 1) ^ 1);
       ptx::tc_fence_after();
-      const uint32_t d = tmem_base + (uint32_t)(acc * BN);
+      const uint32_t d = tmem_base + (uint32_t)(acc * NA);
       for (int kb = 0; kb < kblocks; ++kb) {
         ptx::mbar_wait(full0 + 8 * stage, phase);
         ptx::tc_fence_after();
         const uint64_t ad = ptx::make_smem_desc_sw128(ptx::smem_u32(sA + stage * G::A_BYTES));
-        const uint64_t bd = ptx::make_smem_desc_sw128(ptx::smem_u32(sB + (pl.bres ? kb : stage) * G::B_BYTES));
+        const uint64_t bd = ptx::make_smem_desc_sw128(ptx::smem_u32(sB + (pl.bres ? kb : stage) * BB));
 #pragma unroll
         for (int j = 0; j < BKE / 16; ++j)
-          ptx::mma_bf16_ss_elect(d, ad + (uint64_t)(2 * j), bd + (uint64_t)(2 * j), IDESC, (uint32_t)((kb | j) != 0));
+          if (!(dbg & 2048))                       // timing experiment: no MMAs
+            ptx::mma_bf16_ss_elect(d, ad + (uint64_t)(2 * j), bd + (uint64_t)(2 * j), IDESC,
+                                   (uint32_t)((kb | j) != 0));
         ptx::mma_commit_elect(empty0 + 8 * stage);
         __syncwarp();
         if (++stage == S) {
@@ -224,6 +295,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       ptx::mma_commit_elect(tfull0 + 8 * acc);
       __syncwarp();
+      if (lane == 0 && it == 0) ts_mark(a, 3);
+    }
+    if (lane == 0) {
+      ts_mark(a, 4);
+      if (a.ts && blockIdx.x < 8) a.ts[blockIdx.x * 16 + 10] = it;
     }
   } else {
     // ------------------------------------------------------------ epilogue (2 warpgroups)
@@ -247,6 +323,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       if ((it & 1) != wg) continue;
       const int acc = it & 1;
+      if (a.dbg & 4096) {                            // timing experiment: no epilogue work
+        ptx::mbar_wait(tfull0 + 8 * acc, (it >> 1) & 1);
+        ptx::tc_fence_after();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(tempty0 + 8 * acc);
+        continue;
+      }
       const int m_tile = tile / n_tiles, n_tile = tile - m_tile * n_tiles;
       const long long m0 = (long long)m_tile * BM;
       const long long m = m0 + r;
@@ -288,13 +371,35 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (!staged && res) load_res_g(0);
       ptx::mbar_wait(tfull0 + 8 * acc, (it >> 1) & 1);
       ptx::tc_fence_after();
-      const uint32_t t_base = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN);
+      const uint32_t t_base = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * NA);
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t v[32];
-        ptx::tmem_ld_32x32b_x16(t_base + (uint32_t)c0, *reinterpret_cast<uint32_t(*)[16]>(v));
-        ptx::tmem_ld_32x32b_x16(t_base + (uint32_t)c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
-        ptx::tmem_ld_wait();
+        if constexpr (RT) {
+          // out(x) = T0(x-1) + T1(x) + T2(x+1); x = tile row mod W (whole samples per tile)
+          const int xr = r % Wo;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint32_t t0[16], t2[16];
+            ptx::tmem_ld_32x32b_x16(t_base + (uint32_t)(c0 + 16 * h), t0);
+            ptx::tmem_ld_32x32b_x16(t_base + (uint32_t)(BN + c0 + 16 * h), *reinterpret_cast<uint32_t(*)[16]>(v + 16 * h));
+            ptx::tmem_ld_32x32b_x16(t_base + (uint32_t)(2 * BN + c0 + 16 * h), t2);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float lft = __shfl_up_sync(0xffffffffu, __uint_as_float(t0[j]), 1);
+              const float rgt = __shfl_down_sync(0xffffffffu, __uint_as_float(t2[j]), 1);
+              float f = __uint_as_float(v[16 * h + j]);
+              if (xr > 0) f += lft;
+              if (xr < Wo - 1) f += rgt;
+              v[16 * h + j] = __float_as_uint(f);
+            }
+          }
+        } else {
+          ptx::tmem_ld_32x32b_x16(t_base + (uint32_t)c0, *reinterpret_cast<uint32_t(*)[16]>(v));
+          ptx::tmem_ld_32x32b_x16(t_base + (uint32_t)c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
+          ptx::tmem_ld_wait();
+        }
         float f[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]) + __ldg(a.bias + col0 + c0 + j);
@@ -426,13 +531,16 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(tempty0 + 8 * acc);
+      if (threadIdx.x == 0 && it == 0) ts_mark(a, 7);
     }
-    if (staged && leader) ptx::bulk_wait0();                 // stores done reading SMEM before exit
+    if (staged && leader) ptx::bulk_wait0();
+    if (threadIdx.x == 0) ts_mark(a, 8);                 // stores done reading SMEM before exit
   }
   __syncthreads();
+  if (threadIdx.x == 0) ts_mark(a, 9);
   if (warp == 9) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, G::TMEM_COLS);
+    ptx::tmem_dealloc(tmem_base, TCOLS);
   }
 }
 
@@ -454,8 +562,10 @@ F driver_fn(const char* name) {
   return nullptr;
 }
 
-template <int BN, bool IM2COL>
+template <int BN, bool IM2COL, bool RT = false>
 cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream) {
+  constexpr int NA = RT ? 3 * BN : BN;
+  constexpr int BB = NA * BKE * 2;
   static EncodeTiledFn enc = driver_fn<EncodeTiledFn>("cuTensorMapEncodeTiled");
   static EncodeIm2colFn enc_i2c = driver_fn<EncodeIm2colFn>("cuTensorMapEncodeIm2col");
   if (!enc || !enc_i2c) return cudaErrorNotSupported;
@@ -492,7 +602,9 @@ cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t 
     return enc(t, dt, 2, (void*)p, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   };
-  if (!mat2d(&tmB, a.w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.Kp, a.Cout, BKE, BN, CU_TENSOR_MAP_SWIZZLE_128B))
+  if (RT ? !mat2d(&tmB, a.w_rt, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.Kp_rt, 3 * a.Cout, BKE, NA,
+                  CU_TENSOR_MAP_SWIZZLE_128B)
+         : !mat2d(&tmB, a.w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.Kp, a.Cout, BKE, BN, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   CUtensorMap tmAL = tmB;
   if (IM2COL && a.rows_in) {
@@ -505,6 +617,27 @@ cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t 
                 (cuuint32_t)(a.Ho * a.Wo), es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
+  }
+  // tiled-shift A operand (GemmPlan::tshift)
+  const int HW = a.H * a.W;
+  const bool tshift = IM2COL && a.stride == 1 && a.Ho == a.H && a.Wo == a.W && 2 * a.pad + 1 == a.ksz && HW <= BM &&
+                      BM % HW == 0 && !(a.dbg & 512);
+  if (tshift) {
+    cuuint64_t dims[4] = {(cuuint64_t)a.C, (cuuint64_t)a.W, (cuuint64_t)a.H, (cuuint64_t)rows};
+    cuuint64_t strides[3] = {(cuuint64_t)a.C * 2, (cuuint64_t)a.W * a.C * 2, (cuuint64_t)a.H * a.W * a.C * 2};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    cuuint32_t box[4] = {BKE, (cuuint32_t)a.W, (cuuint32_t)a.H, (cuuint32_t)(BM / HW)};
+    if (enc(&tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)a.x, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+    if (a.rows_in) {
+      box[3] = 1;
+      if (enc(&tmAL, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)a.x, dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    }
   }
   CUtensorMap tmA2 = tmB;
   if (a.x2) {
@@ -526,17 +659,18 @@ cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t 
   // epilogue plan: SMEM-staged TMA stores when the epilogue moves more than a bf16 tile
   // (fp32 stream copy and / or a shortcut) and the ring keeps >= 2 stages beside the staging
   GemmPlan pl{};
-  const int kblocks = a.ksz * a.ksz * (a.C / BKE) + (a.x2 ? a.C2 / BKE : 0);
+  pl.tshift = tshift;
+  if (RT && !tshift) return cudaErrorInvalidValue;
+  const int kblocks = (RT ? a.ksz : a.ksz * a.ksz) * (a.C / BKE) + (a.x2 ? a.C2 / BKE : 0);
   const bool heavy = a.y32 != nullptr || a.res_mode == 1;
   const int avail_staged = SMEM_LIMIT - SMEM_MISC - 2 * EPI_WG;
-  pl.staged = (heavy || a.gap_part) && avail_staged / CG<BN>::STAGE >= 2 && !(a.dbg & 128) && !a.rows_out &&
+  pl.staged = (heavy || a.gap_part) && avail_staged / (CG<BN>::A_BYTES + BB) >= 2 && !(a.dbg & 128) && !a.rows_out &&
               !a.rows_in;
   if (a.gap_part && !pl.staged) return cudaErrorNotSupported;   // the fused GAP reads the SMEM staging
   const int avail = pl.staged ? avail_staged : SMEM_LIMIT - SMEM_MISC;
   // resident weights: one N tile whose K blocks all fit beside >= 3 A stages
-  pl.bres = a.Cout == BN && kblocks > 1 && avail - kblocks * CG<BN>::B_BYTES >= 3 * CG<BN>::A_BYTES &&
-            !(a.dbg & 256);
-  pl.stages = pl.bres ? (avail - kblocks * CG<BN>::B_BYTES) / CG<BN>::A_BYTES : avail / CG<BN>::STAGE;
+  pl.bres = a.Cout == BN && kblocks > 1 && avail - kblocks * BB >= 3 * CG<BN>::A_BYTES && !(a.dbg & 256);
+  pl.stages = pl.bres ? (avail - kblocks * BB) / CG<BN>::A_BYTES : avail / (CG<BN>::A_BYTES + BB);
   if (pl.stages > MAX_STAGES) pl.stages = MAX_STAGES;
   if (pl.stages > kblocks + 1 && kblocks >= 1) pl.stages = kblocks + 1 > 2 ? kblocks + 1 : 2;
   tmR = tmY32 = tmY16 = tmB;
@@ -556,10 +690,10 @@ cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t 
       return cudaErrorInvalidValue;
   }
   const int smem = SMEM_MISC + pl.stages * CG<BN>::A_BYTES +
-                   (pl.bres ? kblocks : pl.stages) * CG<BN>::B_BYTES + (pl.staged ? 2 * EPI_WG : 0);
+                   (pl.bres ? kblocks : pl.stages) * BB + (pl.staged ? 2 * EPI_WG : 0);
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_conv_gemm<BN, IM2COL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_conv_gemm<BN, IM2COL, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          SMEM_LIMIT);
     if (e != cudaSuccess) return e;
     attr = true;
@@ -567,12 +701,22 @@ cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t 
   const long long tiles = ((long long)Mmax + BM - 1) / BM * (a.Cout / BN);
   int grid = (int)(tiles < num_sms ? tiles : num_sms);
   if (grid < 1) grid = 1;
-  k_conv_gemm<BN, IM2COL><<<grid, THREADS, smem, stream>>>(tmA, tmB, tmR, tmY32, tmY16, tmA2, tmAL, a, pl);
+  k_conv_gemm<BN, IM2COL, RT><<<grid, THREADS, smem, stream>>>(tmA, tmB, tmR, tmY32, tmY16, tmA2, tmAL, a, pl);
   return cudaGetLastError();
+}
+
+// row-tap form (k_conv_gemm RT): 3x3 / stride 1 / pad 1, whole samples per 128-row tile,
+// image rows inside a warp, one 64-wide N tile (3 x 64 accumulator columns)
+bool rowtap_ok(const ConvArgs& a) {
+  const int hw = a.H * a.W;
+  return a.ksz == 3 && a.stride == 1 && a.pad == 1 && a.Ho == a.H && a.Wo == a.W && hw <= BM && BM % hw == 0 &&
+         32 % a.W == 0 && a.Cout == 64 && a.w_rt && a.Kp_rt == 3 * a.C && !a.x2 && !(a.dbg & (512 | 4194304));
 }
 
 template <int BN>
 cudaError_t launch_bn(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream) {
+  if constexpr (BN == 64)
+    if (rowtap_ok(a)) return launch_t<64, true, true>(a, max_rows, num_sms, stream);
   const bool tiled = a.ksz == 1 && a.stride == 1 && a.pad == 0;
   return tiled ? launch_t<BN, false>(a, max_rows, num_sms, stream) : launch_t<BN, true>(a, max_rows, num_sms, stream);
 }

@@ -43,8 +43,12 @@ struct ConvArgs {
   // 32-row group of the flat output, the column sums of y for the group's first sample (slot 0)
   // and, when the group straddles a sample boundary, the second (slot 1); see launch_gap_reduce
   float* gap_part = nullptr;
+  long long* ts = nullptr;   // development: conv_gemm phase timestamps (DYCL_TS_CONV)
   int dbg = 0;           // bit5 (32): row-tap mode opt-in; experiments only (results invalid): bit0 skip
-                         // epilogue math/stores, bit1 skip MMAs, bit2 skip A loads, bit3 no residual prefetch
+                         // epilogue math/stores, bit1 skip MMAs, bit2 skip A loads, bit3 no residual prefetch.
+                         // conv_gemm: 128 no staged epilogue, 256 no resident weights, 512 no tiled-shift
+                         // A boxes (nor row-tap), 4194304 no row-tap; timing only: 1024 skip A loads,
+                         // 2048 skip MMAs, 4096 skip the epilogue
 };
 // Launch on `stream`; grid is sized for max_rows samples (persistent CTAs loop
 // over the tiles the live count needs).  Returns cudaSuccess or the launch error.

@@ -127,10 +127,18 @@ NHWC_CASES = [
     (4, 16, 16, 8, 64, 7, 2, 3, 1, 0),       # stem (C = 8): planar kernels, NHWC output
     (1, 1, 1, 64, 64, 1, 1, 0, 1, 0),        # single row
 ]
+# row-tap GEMM form (path 5): 3x3 / s1 / p1, whole samples per 128-row tile, W | 32, Cout 64
+ROWTAP_NHWC_CASES = [
+    (5, 8, 8, 64, 64, 3, 1, 1, 1, 1),        # CIFAR stage 3 + identity shortcut, ragged last tile
+    (7, 8, 8, 64, 64, 3, 1, 1, 0, 0),        # odd sample count, no ReLU
+    (9, 4, 4, 128, 64, 3, 1, 1, 1, 0),       # 8 samples per tile, two channel blocks per tap
+    (3, 8, 16, 64, 64, 3, 1, 1, 1, 1),       # non-square, W = 16
+]
 
 
-@pytest.mark.parametrize("case", NHWC_CASES, ids=[f"nhwc-{c}" for c in NHWC_CASES])
-def test_conv_gemm_nhwc_matches_oracle_conv(any_graph, case):
+@pytest.mark.parametrize("path,case", [(4, c) for c in NHWC_CASES] + [(5, c) for c in ROWTAP_NHWC_CASES],
+                         ids=[f"nhwc-{c}" for c in NHWC_CASES] + [f"nhwc-rowtap-{c}" for c in ROWTAP_NHWC_CASES])
+def test_conv_gemm_nhwc_matches_oracle_conv(any_graph, path, case):
     n, H, W, C, Co, k, st, pad, relu, res_mode = case
     rng = np.random.default_rng(abs(hash(case)) % 2**32)
     x = wl.f32_to_bf16_bits(rng.standard_normal((n, H, W, C)))
@@ -140,7 +148,7 @@ def test_conv_gemm_nhwc_matches_oracle_conv(any_graph, case):
     res = wl.f32_to_bf16_bits(rng.standard_normal((n, Ho, Wo, Co))) if res_mode == 1 else None
     y = torch.zeros((n, Ho, Wo, Co), dtype=torch.int16, device=DEV)
     D.dycl_debug_conv2d(any_graph, _bits_to_t(x), n, H, W, C, w, b, Co, k, st, pad, relu,
-                        _bits_to_t(res) if res is not None else None, res_mode, y, 4)
+                        _bits_to_t(res) if res is not None else None, res_mode, y, path)
     got = _t_to_f64(y)
     xf, wf = prg._bf16_to_f64(x), prg._bf16_to_f64(w)
     for i in range(n):
