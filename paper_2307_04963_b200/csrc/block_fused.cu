@@ -318,9 +318,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         // read) by epilogue 1; two sets: SET2 columns j drained by the previous epilogue 2
 #pragma unroll
         for (int j = 0; j < G::NSUB; ++j) {
-#pragma unroll
-          for (int jj = j - 1; jj <= j + 1; ++jj)
-            if (jj >= 0 && jj < G::NSUB) ptx::mbar_wait(tready0 + 8 * jj, ph);
+          // T rows j-1..j+1: j-1 and j were already awaited for sub-tile j-1 (each barrier
+          // completes once per occurrence), so only the new neighbour j+1 is waited on
+          if (j == 0) ptx::mbar_wait(tready0, ph);
+          if (j + 1 < G::NSUB) ptx::mbar_wait(tready0 + 8 * (j + 1), ph);
           if (G::NSETS == 2 && k > 0) ptx::mbar_wait(subfree0 + 8 * j, (k - 1) & 1);
           ptx::tc_fence_after();
 #pragma unroll

@@ -9,7 +9,7 @@
 // Blackwell GEMM: 128 x 64 A boxes and BN x 64 W boxes (TMA, SWIZZLE_128B) into a
 // 4-stage ring, one elected lane issues 128 x BN x 16 tcgen05.mma (BN = 256 or 128)
 // into one of two TMEM accumulators, two epilogue warpgroups alternate tiles and run
-// the shared fused epilogue (conv_finish16).  Warps: 0-7 epilogue, 8 TMA, 9 MMA.
+// the shared fused epilogue (conv_finish16).  Warps: 0-7 epilogue, 8/10/11 TMA (k-blocks round-robin), 9 MMA.
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -22,8 +22,9 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BKE = 64;                  // K elements per stage (one 128-byte swizzle row)
-constexpr int THREADS = 320;
+constexpr int THREADS = 384;             // warps 0-7 epilogue, 8/10/11 TMA producers, 9 MMA
 constexpr int STAGES = 4;
+constexpr int NPROD = 3;                 // <= STAGES (a parity wait never spans two ring rounds)
 
 template <int BN>
 struct GCfg {
@@ -72,24 +73,35 @@ __global__ void __launch_bounds__(THREADS, 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 8) {
+  if (warp == 8 || warp >= 10) {
+    // k-blocks round-robin over NPROD producer warps: one issuing warp runs ~9 cycles per
+    // instruction, slower than the tensor core consumes a 128 x BN x 64 block (conv_gemm.cu)
+    const int prod = warp == 8 ? 0 : warp - 9;
     if (lane == 0) {
       ptx::tma_prefetch_desc(&tmA);
       ptx::tma_prefetch_desc(&tmB);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m_tile = tile / n_tiles, n_tile = tile - m_tile * n_tiles;
-        for (int kb = 0; kb < kblocks; ++kb) {
-          ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1);
+    }
+    int stage = prod;
+    uint32_t phase = 0;
+    int rr = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int m_tile = tile / n_tiles, n_tile = tile - m_tile * n_tiles;
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const bool mine = rr == prod;
+        rr = rr + 1 == NPROD ? 0 : rr + 1;
+        if (!mine) continue;
+        ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1);
+        if (lane == 0) {
           const uint32_t bar = full0 + 8 * stage;
           ptx::mbar_arrive_expect_tx(bar, (uint32_t)C::STAGE);
           ptx::tma_load_2d(ptx::smem_u32(sA + stage * C::A_BYTES), &tmA, bar, kb * BKE, m_tile * BM);
           ptx::tma_load_2d(ptx::smem_u32(sB + stage * C::B_BYTES), &tmB, bar, kb * BKE, n_tile * BN);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
+        }
+        __syncwarp();
+        stage += NPROD;
+        if (stage >= STAGES) {
+          stage -= STAGES;
+          phase ^= 1;
         }
       }
     }
