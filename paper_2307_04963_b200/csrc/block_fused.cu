@@ -160,7 +160,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   // weight ring: wfull[s] = slot s loaded (TMA), wempty[s] = conv2 of the block in slot s done
   const uint32_t wfull0 = ptx::smem_u32(bars + 58), wempty0 = ptx::smem_u32(bars + 60);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 62);
-  float* gred = reinterpret_cast<float*>(bars + 64);       // [8 warps][C] fused-GAP partials (C <= 32)
+  // xready[j]: between fused blocks, epilogue 2 wrote the bf16 operand rows of sub-tile j (the
+  // next conv1 sub-tile j needs j-1..j+1): the next block starts before this one's epilogue ends
+  const uint32_t xready0 = ptx::smem_u32(bars + 66);
+  float* gred = reinterpret_cast<float*>(bars + 74);       // [8 warps][C] fused-GAP partials (C <= 32)
   static_assert(G::NBOX <= 4, "box barriers");
   static_assert(G::NSUB <= 8, "sub-tile barriers");
   constexpr uint32_t SET2 = G::NSETS == 2 ? 256u : 0u;    // TMEM column of the conv2 accumulator
@@ -179,6 +182,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       ptx::mbar_init(acc1j0 + 8 * j, 1);
       ptx::mbar_init(acc2j0 + 8 * j, 1);
       ptx::mbar_init(tready0 + 8 * j, 128);
+      ptx::mbar_init(xready0 + 8 * j, 128);
     }
     ptx::mbar_init(xb_full, 256);
     ptx::mbar_init(xb_empty, 1);
@@ -291,15 +295,20 @@ __global__ void __launch_bounds__(THREADS, 1)
         // conv1 sub-tile j: its columns were drained by the previous epilogue 2 (shared set) or the
         // previous epilogue 1 (two sets); committed per sub-tile so epilogue 1 starts on sub-tile 0
         // while the tensor core works on the rest
-        ptx::mbar_wait(xb_full, ph);                  // x operand: converted, or the previous block's y
+        // x operand: the converted sample (first block) or, sub-tile by sub-tile below, the
+        // previous block's y
+        const uint32_t pxr = (uint32_t)((it * (NB - 1) + blk - 1) & 1);
+        if (blk == 0) ptx::mbar_wait(xb_full, it & 1);
         ptx::tc_fence_after();
         if (mstamp && blk == 0) a.ts[it * 16 + 6] = clock64();
 #pragma unroll
         for (int j = 0; j < G::NSUB; ++j) {
-          if (k > 0) {
-            ptx::mbar_wait((G::NSETS == 1 ? subfree0 : tready0) + 8 * j, (k - 1) & 1);
-            ptx::tc_fence_after();
+          if (blk > 0) {
+            if (j == 0) ptx::mbar_wait(xready0, pxr);
+            if (j + 1 < G::NSUB) ptx::mbar_wait(xready0 + 8 * (j + 1), pxr);
           }
+          if (k > 0) ptx::mbar_wait((G::NSETS == 1 ? subfree0 : tready0) + 8 * j, (k - 1) & 1);
+          if (k > 0 || blk > 0) ptx::tc_fence_after();
 #pragma unroll
           for (int r = 0; r < 3; ++r)
 #pragma unroll
@@ -510,10 +519,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             ptx::mbar_arrive(yready0 + 8 * (4 * (it % G::NXB) + j * 128 / G::BOX_ROWS));
           }
         }
-      }
-      if (!last) {                                     // y (bf16) is the next block's conv1 operand
-        ptx::fence_proxy_async_smem();
-        ptx::mbar_arrive(xb_full);
+        if (!last) {                                   // y (bf16) rows: the next block's conv1 operand
+          ptx::fence_proxy_async_smem();
+          ptx::mbar_arrive(xready0 + 8 * ja);
+          if (jb != ja) ptx::mbar_arrive(xready0 + 8 * jb);
+        }
       }
       if (last && a.pooled) {
         // global average pool of y for the head that follows (a2 fused): y sits in SMEM; thread t
