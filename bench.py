@@ -349,7 +349,7 @@ def run_dycl(args):
             split[k][1] += lm
         roof_eff = (split["tensor"][0] + split["hbm"][0]) / ms_ if ms_ else None
         names = {
-            "block": "k_block_fused (a1: 1-2 whole residual blocks per sample, SMEM-resident, row-tap tcgen05 convs)",
+            "block": "k_block_fused (a1: 1-8 whole residual blocks per sample, SMEM-resident, row-tap tcgen05 convs)",
             "conv": "a1 conv class (k_conv_gemm NHWC im2col GEMM / k_conv_tma / k_gemm_tma on tcgen05, fused epilogue)",
             "gemm": "k_gemm_tma (a7/a8 decoder + encoder projections, FFN, LM head on tcgen05)",
             "attn": "k_attn_decoder (a7 decode attention, KV-cache streaming)",
