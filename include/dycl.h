@@ -182,8 +182,9 @@ dycl_status dycl_run(dycl_graph g, const dycl_io* io, void* stream);
 /* Same, with HOST buffers (pinned or pageable): copies the input host->device,
  * runs, copies logits and path device->host, and synchronises `stream` before
  * returning -- the deployment-style call of Listing 2 (set_input/run/get_output).
- * Batches of >= 1024 rows are pipelined in sub-chunks (a quarter of the batch, >= 2048 rows
- * for samples under 64 KB) over two library-owned
+ * Batches of >= 1024 rows are pipelined in sub-chunks (a quarter of the batch; for samples
+ * under 64 KB, batches of >= 2048 rows run as two chunks, a quarter then the rest, so only
+ * the first chunk's copy is exposed) over two library-owned
  * staging slots: the host->device copy of sub-chunk k+1 and the device->host copy of
  * k-1 run on two internal copy streams while sub-chunk k runs on `stream` (results
  * equal one run: samples are independent). */

@@ -1444,11 +1444,22 @@ dycl_status dycl_run_host(dycl_graph g, const float* input_host, int64_t batch, 
   // Pipelined over sub-chunks in two staging slots: H2D of sub-chunk k+1 (copy stream) and
   // D2H of k-1 (second copy stream) overlap the run of k on the caller's stream.  Samples are
   // independent and every kernel is batch-position independent, so the results equal one run.
-  // sub-chunk: a quarter of the batch, but >= 2048 rows for small samples (< 64 KB of input),
-  // whose runs lose efficiency below that size
+  // sub-chunk: a quarter of the batch.  Small samples (< 64 KB of input), whose runs lose
+  // efficiency below ~2048 rows: two uneven chunks, a quarter then the rest -- only the first
+  // chunk's copy is exposed, the second one's hides under the first run
   int64_t sc = batch >= 1024 ? (batch + 3) / 4 : batch;
-  if (row_in * 4 < 64 * 1024 && sc < 2048) sc = std::min<int64_t>(batch, 2048);
-  const int64_t nsc = batch > 0 ? (batch + sc - 1) / sc : 0;
+  int64_t first = sc;                              // rows of chunk 0
+  const bool small = row_in * 4 < 64 * 1024;
+  if (small) {
+    if (batch >= 2048 && !getenv("DYCL_E2E_EVEN")) {
+      first = ((batch + 3) / 4 + 255) / 256 * 256;
+      sc = batch - first;                          // chunk 1 (slot 1 starts at row `first`)
+    } else if (sc < 2048) {
+      sc = first = std::min<int64_t>(batch, 2048);
+    }
+  }
+  const bool uneven = small && first != sc && batch >= 2048 && first < batch;
+  const int64_t nsc = batch <= 0 ? 0 : uneven ? 2 : (batch + sc - 1) / sc;
   if (nsc <= 1) {
     CK(cudaMemcpyAsync(g->d_in_stage, input_host, (size_t)batch * row_in * 4, cudaMemcpyHostToDevice, st));
     if (dycl_status s = run_impl(g, g->d_in_stage, batch, g->d_logit_stage, g->d_path_stage, nullptr, st)) return s;
@@ -1468,10 +1479,12 @@ dycl_status dycl_run_host(dycl_graph g, const float* input_host, int64_t batch, 
   }
   for (int64_t k = 0; k < nsc; ++k) {
     const int slot = (int)(k & 1);
-    const int64_t r0 = k * sc, rows = std::min<int64_t>(sc, batch - r0);
-    float* din = g->d_in_stage + (size_t)slot * sc * row_in;
-    float* dz = g->d_logit_stage + (size_t)slot * sc * g->K;
-    int32_t* dp = g->d_path_stage + (size_t)slot * sc;
+    const int64_t r0 = uneven ? (k == 0 ? 0 : first) : k * sc;
+    const int64_t rows = uneven ? (k == 0 ? first : batch - first) : std::min<int64_t>(sc, batch - r0);
+    const size_t off = uneven ? (size_t)r0 : (size_t)slot * sc;    // staging rows of this slot
+    float* din = g->d_in_stage + off * row_in;
+    float* dz = g->d_logit_stage + off * g->K;
+    int32_t* dp = g->d_path_stage + off;
     if (k >= 2) CK(cudaStreamWaitEvent(g->h2d_stream, g->ev_run[slot], 0));     // run k-2 read this slot
     CK(cudaMemcpyAsync(din, input_host + (size_t)r0 * row_in, (size_t)rows * row_in * 4, cudaMemcpyHostToDevice,
                        g->h2d_stream));

@@ -283,6 +283,18 @@ def test_run_host_equals_run(r56):
     assert np.array_equal(lh, l1) and np.array_equal(ph, p1)
 
 
+def test_run_host_pipelined_equals_run(r56):
+    """A batch the host-buffer path splits into two uneven chunks (768 + 1732 rows): bitwise
+    the device run's results, in input order."""
+    W, m = r56
+    X = wl.image_inputs(wl.INPUT_SEED, 3000, 2500)
+    l1, p1 = _run_gpu(m, X)
+    lh = np.zeros((2500, 10), np.float32)
+    ph = np.zeros(2500, np.int32)
+    m.run_host(X, lh, ph)
+    assert np.array_equal(lh, l1) and np.array_equal(ph, p1)
+
+
 def test_cfg2_full_batch_sampled_parity(r56):
     """BASELINE size (B = 4096, the bench launch configuration): sampled rows vs oracle."""
     W, m = r56
