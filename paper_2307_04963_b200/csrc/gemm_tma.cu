@@ -50,10 +50,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int M = a.n_live ? *a.n_live : a.n_static;
-  const int m_tiles = (M + BM - 1) / BM;
   const int n_tiles = a.Cout / BN;
-  const int num_tiles = m_tiles * n_tiles;
   const int kblocks = a.K / BKE;
 
   if (threadIdx.x == 0) {
@@ -68,19 +65,26 @@ __global__ void __launch_bounds__(THREADS, 1)
     ptx::fence_mbar_init();
   }
   if (warp == 9) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), 512);
+  if (warp == 8 && lane == 0) {
+    ptx::tma_prefetch_desc(&tmA);
+    ptx::tma_prefetch_desc(&tmB);
+  }
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // PDL: the prologue above (barriers, TMEM, descriptors) overlaps the predecessor's tail;
+  // the live count and every operand are read after it completes
+  ptx::pdl_wait();
+  ptx::pdl_trigger();
+  const int M = a.n_live ? *a.n_live : a.n_static;
+  const int m_tiles = (M + BM - 1) / BM;
+  const int num_tiles = m_tiles * n_tiles;
 
   if (warp == 8 || warp >= 10) {
     // k-blocks round-robin over NPROD producer warps: one issuing warp runs ~9 cycles per
     // instruction, slower than the tensor core consumes a 128 x BN x 64 block (conv_gemm.cu)
     const int prod = warp == 8 ? 0 : warp - 9;
-    if (lane == 0) {
-      ptx::tma_prefetch_desc(&tmA);
-      ptx::tma_prefetch_desc(&tmB);
-    }
     int stage = prod;
     uint32_t phase = 0;
     int rr = 0;
@@ -217,8 +221,7 @@ cudaError_t launch_bn(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t
   const long long tiles = (long long)((max_rows + BM - 1) / BM) * (a.Cout / BN);
   int grid = (int)(tiles < num_sms ? tiles : num_sms);
   if (grid < 1) grid = 1;
-  k_gemm_tma<BN><<<grid, THREADS, GCfg<BN>::SMEM, stream>>>(tmA, tmB, a);
-  return cudaGetLastError();
+  return launch_k(k_gemm_tma<BN>, dim3(grid), dim3(THREADS), GCfg<BN>::SMEM, stream, tmA, tmB, a);
 }
 
 }  // namespace

@@ -11,6 +11,7 @@
 #include <cuda_bf16.h>
 
 #include "kernels.h"
+#include "ptx.cuh"
 
 namespace dycl {
 namespace {
@@ -283,6 +284,8 @@ __global__ void __launch_bounds__(CMP_THREADS) k_compact(const uint8_t* __restri
                                                          int32_t path_bit) {
   __shared__ int wsum[CMP_THREADS / 32];
   __shared__ int total1_s;
+  ptx::pdl_wait();
+  ptx::pdl_trigger();
   const int n = *n_live;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int ipt = (n + CMP_THREADS - 1) / CMP_THREADS;
@@ -755,8 +758,8 @@ cudaError_t launch_head(const HeadArgs& a, int max_rows, cudaStream_t s) {
 cudaError_t launch_compact(const uint8_t* flag, const int* n_live, const int* orig, int* list1, int* list0,
                            int* counts_out, int* orig_next, int mode, int32_t* path, int32_t path_bit,
                            cudaStream_t s) {
-  k_compact<<<1, CMP_THREADS, 0, s>>>(flag, n_live, orig, list1, list0, counts_out, orig_next, mode, path, path_bit);
-  return cudaGetLastError();
+  return launch_k(k_compact, dim3(1), dim3(CMP_THREADS), 0, s, flag, n_live, orig, list1, list0, counts_out, orig_next,
+                  mode, path, path_bit);
 }
 
 cudaError_t launch_scatter(const float* z, int K, const int* list, const int* count, const int* orig,
@@ -775,6 +778,11 @@ cudaError_t launch_gather(const GatherArgs& a, int max_rows, int num_sms, cudaSt
   if (blocks < 1) blocks = 1;
   k_gather<<<(int)blocks, 256, 0, s>>>(a);
   return cudaGetLastError();
+}
+
+bool& pdl_flag() {
+  thread_local bool on = false;
+  return on;
 }
 
 }  // namespace dycl

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 namespace dycl {
 
 // Implicit-GEMM convolution / dense layer on tcgen05 (conv_tc.cu).
@@ -50,6 +52,35 @@ struct ConvArgs {
                          // A boxes (nor row-tap), 4194304 no row-tap; timing only: 1024 skip A loads,
                          // 2048 skip MMAs, 4096 skip the epilogue
 };
+// Programmatic dependent launch (PDL) for the launches the calling host thread enqueues
+// while a PdlScope is alive (the config-4 decode loop: ~70 dependent small kernels per step).
+// A PDL launch may start while its predecessor kernel is still running; every kernel that
+// can be launched this way executes griddepcontrol.wait (ptx::pdl_wait / s2s pdl_wait)
+// before its first read of predecessor output and before any early return, so completion
+// stays transitive along the stream.  Thread-local: graphs are driven from several threads.
+bool& pdl_flag();
+struct PdlScope {
+  bool prev;
+  explicit PdlScope(bool on) : prev(pdl_flag()) { pdl_flag() = on; }
+  ~PdlScope() { pdl_flag() = prev; }
+};
+// Kernel launch honouring pdl_flag() (cudaLaunchKernelEx + programmatic stream serialization).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_flag() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 // Launch on `stream`; grid is sized for max_rows samples (persistent CTAs loop
 // over the tiles the live count needs).  Returns cudaSuccess or the launch error.
 cudaError_t launch_conv_tc(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream);

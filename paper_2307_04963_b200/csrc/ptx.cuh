@@ -7,6 +7,11 @@
 namespace dycl {
 namespace ptx {
 
+// PDL (kernels.h PdlScope): wait for the predecessor grid's completion and memory flush;
+// allow the successor grid to be scheduled.  Both are no-ops in a non-PDL launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -54,6 +54,7 @@ struct dycl_s2s_s {
   // Every kernel reads its live row count from device memory, so the captured sequence is
   // valid for any data; only the pointers and the batch are baked in.
   bool use_graph = true;             // DYCL_S2S_GRAPH=0 disables
+  bool pdl = true;                   // programmatic dependent launch in the run (DYCL_S2S_PDL=0 disables)
   int gemm_path = 0;                 // 0: k_gemm_tma, 1: k_conv_gemm (DYCL_S2S_GEMM=1; measured equal or slower)
   // per-launch profiling (graph off while enabled)
   struct Rec {
@@ -188,6 +189,9 @@ struct S2SExec {
   dycl_status run(const int32_t* src, int32_t* tokens, int32_t* lengths, float* top1, float* logits0) {
     const dycl_s2s_config& c = s->c;
     const int d = c.d_model, S = c.src_len, R = B * S;
+    // the decode loop is ~70 dependent launches per step: each kernel's launch and prologue
+    // overlap its predecessor's tail (per-launch profiling events would break the chain)
+    dycl::PdlScope pdl_scope(s->pdl && !s->profiling);
     cudaError_t e;
 #define E(x)                                                                        \
   do {                                                                              \
@@ -305,6 +309,7 @@ dycl_status dycl_s2s_create(int cuda_device, const dycl_s2s_config* cfg, dycl_s2
   s->device = cuda_device;
   if (const char* eg = getenv("DYCL_S2S_GRAPH")) s->use_graph = atoi(eg) != 0;
   if (const char* gp = getenv("DYCL_S2S_GEMM")) s->gemm_path = atoi(gp);
+  if (const char* pp = getenv("DYCL_S2S_PDL")) s->pdl = atoi(pp) != 0;
   cudaSetDevice(cuda_device);
   cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
   *out = s;

@@ -7,6 +7,8 @@
 // All reductions are fixed-order warp trees (batch-position independent).
 #include <cuda_bf16.h>
 
+#include "kernels.h"
+#include "ptx.cuh"
 #include "s2s_kernels.h"
 
 namespace dycl {
@@ -30,6 +32,18 @@ __device__ __forceinline__ float warp_max(float v) {
 
 // x = emb[tok] * sqrt(d) + PE(pos); one warp per row, d / 32 elements per lane.
 __global__ void k_embed(const S2SEmbedArgs a) {
+  ptx::pdl_wait();      // PDL (kernels.h): before any read of predecessor output / early return
+  ptx::pdl_trigger();
+  // decoder step: every row sits at position t -- the PE row is computed once per CTA
+  // (same expression, same values as the per-element form below)
+  __shared__ float pe_t[1024];
+  if (!a.src) {
+    for (int c = threadIdx.x; c < a.d; c += blockDim.x) {
+      const float ang = (float)a.t / powf(10000.0f, (float)(c & ~1) / (float)a.d);
+      pe_t[c] = (c & 1) ? cosf(ang) : sinf(ang);
+    }
+    __syncthreads();
+  }
   const int n = a.n_live ? *a.n_live : a.n_static;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= n) return;
@@ -45,9 +59,14 @@ __global__ void k_embed(const S2SEmbedArgs a) {
   const uint16_t* e = a.table + (size_t)tok * a.d;
   const float sd = sqrtf((float)a.d);
   for (int c = lane; c < a.d; c += 32) {
-    const int i2 = c & ~1;
-    const float ang = (float)pos / powf(10000.0f, (float)i2 / (float)a.d);
-    const float pe = (c & 1) ? cosf(ang) : sinf(ang);
+    float pe;
+    if (a.src) {
+      const int i2 = c & ~1;
+      const float ang = (float)pos / powf(10000.0f, (float)i2 / (float)a.d);
+      pe = (c & 1) ? cosf(ang) : sinf(ang);
+    } else {
+      pe = pe_t[c];
+    }
     const float v = bf(e[c]) * sd + pe;
     a.x32[(size_t)warp * a.d + c] = v;
     a.xb[(size_t)warp * a.d + c] = to_bf(v);
@@ -57,6 +76,8 @@ __global__ void k_embed(const S2SEmbedArgs a) {
 // LayerNorm of [rows][d] fp32 (d <= 1024, d % 32 == 0): warp per row, the row in registers
 // (compile-time unrolled, guarded), biased variance, eps.
 __global__ void k_layernorm(const S2SLnArgs a) {
+  ptx::pdl_wait();      // PDL (kernels.h): before any read of predecessor output / early return
+  ptx::pdl_trigger();
   const int n = a.n_live ? *a.n_live : a.n_static;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= n) return;
@@ -91,6 +112,8 @@ __global__ void k_layernorm(const S2SLnArgs a) {
 // Encoder self-attention: one CTA per (sequence, head), S <= 64 tokens, head dim 64.
 // qkv: bf16 [B*S][3d] (q | k | v), out: bf16 [B*S][d].
 __global__ void __launch_bounds__(128) k_attn_encoder(const S2SAttnArgs a) {
+  ptx::pdl_wait();      // PDL (kernels.h): before any read of predecessor output / early return
+  ptx::pdl_trigger();
   __shared__ float sk[64][65];
   __shared__ float sv[64][65];
   __shared__ float sq[4][64];
@@ -146,6 +169,8 @@ __global__ void __launch_bounds__(128) k_attn_encoder(const S2SAttnArgs a) {
 //         cache, then attend over positions 0..t of the cache;
 //   cross (kv != nullptr): attend over the S encoder positions of the slot's cross K/V.
 __global__ void __launch_bounds__(256, 5) k_attn_decoder(const S2SAttnArgs a) {
+  ptx::pdl_wait();      // PDL (kernels.h): before any read of predecessor output / early return
+  ptx::pdl_trigger();
   const int n = a.n_live ? *a.n_live : a.n_static;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int row = gw / a.heads, h = gw % a.heads;
@@ -229,6 +254,8 @@ __global__ void __launch_bounds__(256, 5) k_attn_decoder(const S2SAttnArgs a) {
 //   z[EOS] += beta * (t + 1 - LEN[src[slot][0]]);  tok = argmax z (lowest index on ties)
 //   tokens[slot][t] = tok; top1[slot][t] = z[tok]; done -> length = t + 1, flag = 1
 __global__ void __launch_bounds__(256) k_argmax_guard(const S2SArgmaxArgs a) {
+  ptx::pdl_wait();      // PDL (kernels.h): before any read of predecessor output / early return
+  ptx::pdl_trigger();
   __shared__ float sv[8];
   __shared__ int si[8];
   const int n = *a.n_live;
@@ -239,14 +266,29 @@ __global__ void __launch_bounds__(256) k_argmax_guard(const S2SArgmaxArgs a) {
   const float bias = a.beta * ((float)(a.t + 1) - a.len_table[a.src[(size_t)slot * a.S]]);
   float best = -INFINITY;
   int bi = 0x7fffffff;
-  for (int j = threadIdx.x; j < a.V; j += blockDim.x) {
-    float v = z[j];
-    if (j == a.eos) v += bias;
-    if (a.logits0 && a.t == 0) a.logits0[(size_t)slot * a.V + j] = v;
-    if (v > best || (v == best && j < bi)) {
-      best = v;
-      bi = j;
+  // 16-byte loads (V % 4 == 0, enforced at create), 4 in flight per thread; each thread
+  // scans its indices in ascending order
+  const float4* z4 = reinterpret_cast<const float4*>(z);
+  float4* l0 = (a.logits0 && a.t == 0) ? reinterpret_cast<float4*>(a.logits0 + (size_t)slot * a.V) : nullptr;
+  const int V4 = a.V >> 2;
+#pragma unroll 4
+  for (int j4 = threadIdx.x; j4 < V4; j4 += blockDim.x) {
+    float4 q = z4[j4];
+    const int j = 4 * j4;
+    if ((unsigned)(a.eos - j) < 4u) {
+      if (a.eos == j) q.x += bias;
+      else if (a.eos == j + 1) q.y += bias;
+      else if (a.eos == j + 2) q.z += bias;
+      else q.w += bias;
     }
+    if (l0) l0[j4] = q;
+    const float vv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (vv[e] > best || (vv[e] == best && j + e < bi)) {
+        best = vv[e];
+        bi = j + e;
+      }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -280,6 +322,8 @@ __global__ void __launch_bounds__(256) k_argmax_guard(const S2SArgmaxArgs a) {
 
 // run start: tokens = PAD, lengths = max_len, top1 = NaN, cur_tok = BOS, active = iota, count.
 __global__ void k_s2s_init(S2SInitArgs a) {
+  ptx::pdl_wait();      // PDL (kernels.h): before any read of predecessor output / early return
+  ptx::pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0) a.count[0] = a.B;
   if (i < a.B) {
@@ -297,34 +341,28 @@ __global__ void k_s2s_init(S2SInitArgs a) {
 
 cudaError_t launch_embed(const S2SEmbedArgs& a, int max_rows, cudaStream_t s) {
   const int blocks = (max_rows * 32 + 255) / 256;
-  k_embed<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(a);
-  return cudaGetLastError();
+  return launch_k(k_embed, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, s, a);
 }
 cudaError_t launch_layernorm(const S2SLnArgs& a, int max_rows, cudaStream_t s) {
   if (a.d % 32 || a.d > 1024) return cudaErrorInvalidValue;
   const int blocks = (max_rows * 32 + 255) / 256;
-  k_layernorm<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(a);
-  return cudaGetLastError();
+  return launch_k(k_layernorm, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, s, a);
 }
 cudaError_t launch_attn_encoder(const S2SAttnArgs& a, int max_seqs, cudaStream_t s) {
   if (a.S > 64 || a.d / a.heads != 64) return cudaErrorInvalidValue;
-  k_attn_encoder<<<max_seqs * a.heads > 0 ? max_seqs * a.heads : 1, 128, 0, s>>>(a);
-  return cudaGetLastError();
+  return launch_k(k_attn_encoder, dim3(max_seqs * a.heads > 0 ? max_seqs * a.heads : 1), dim3(128), 0, s, a);
 }
 cudaError_t launch_attn_decoder(const S2SAttnArgs& a, int max_rows, cudaStream_t s) {
   if (a.S > 64 || a.max_len > 64 || a.d / a.heads != 64) return cudaErrorInvalidValue;
   const int warps = max_rows * a.heads;
   const int blocks = (warps * 32 + 255) / 256;
-  k_attn_decoder<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(a);
-  return cudaGetLastError();
+  return launch_k(k_attn_decoder, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, s, a);
 }
 cudaError_t launch_argmax_guard(const S2SArgmaxArgs& a, int max_rows, cudaStream_t s) {
-  k_argmax_guard<<<max_rows > 0 ? max_rows : 1, 256, 0, s>>>(a);
-  return cudaGetLastError();
+  return launch_k(k_argmax_guard, dim3(max_rows > 0 ? max_rows : 1), dim3(256), 0, s, a);
 }
 cudaError_t launch_s2s_init(const S2SInitArgs& a, cudaStream_t s) {
-  k_s2s_init<<<(a.B + 255) / 256 > 0 ? (a.B + 255) / 256 : 1, 256, 0, s>>>(a);
-  return cudaGetLastError();
+  return launch_k(k_s2s_init, dim3((a.B + 255) / 256 > 0 ? (a.B + 255) / 256 : 1), dim3(256), 0, s, a);
 }
 
 }  // namespace dycl
