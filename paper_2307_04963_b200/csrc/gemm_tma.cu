@@ -23,7 +23,6 @@ namespace {
 constexpr int BM = 128;
 constexpr int BKE = 64;                  // K elements per stage (one 128-byte swizzle row)
 constexpr int THREADS = 384;             // warps 0-7 epilogue, 8/10/11 TMA producers, 9 MMA
-constexpr int STAGES = 4;
 constexpr int NPROD = 3;                 // <= STAGES (a parity wait never spans two ring rounds)
 
 template <int BN>
@@ -31,6 +30,9 @@ struct GCfg {
   static constexpr int A_BYTES = BM * BKE * 2;
   static constexpr int B_BYTES = BN * BKE * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
+  // ~190 KB of ring whatever BN: the small-M decode GEMMs are bound by the bytes one CTA
+  // keeps in flight (Little's law on the L2 -> SMEM path), not by the tensor core
+  static constexpr int STAGES = BN == 64 ? 8 : BN == 128 ? 6 : 4;
   static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
 };
 
@@ -41,20 +43,20 @@ __global__ void __launch_bounds__(THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * C::A_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES);
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
   const uint32_t full0 = ptx::smem_u32(bars);
-  const uint32_t empty0 = full0 + 8 * STAGES;
-  const uint32_t tfull0 = empty0 + 8 * STAGES;
+  const uint32_t empty0 = full0 + 8 * C::STAGES;
+  const uint32_t tfull0 = empty0 + 8 * C::STAGES;
   const uint32_t tempty0 = tfull0 + 16;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = a.Cout / BN;
   const int kblocks = a.K / BKE;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < STAGES; ++i) {
+    for (int i = 0; i < C::STAGES; ++i) {
       ptx::mbar_init(full0 + 8 * i, 1);
       ptx::mbar_init(empty0 + 8 * i, 1);
     }
@@ -103,8 +105,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         __syncwarp();
         stage += NPROD;
-        if (stage >= STAGES) {
-          stage -= STAGES;
+        if (stage >= C::STAGES) {
+          stage -= C::STAGES;
           phase ^= 1;
         }
       }
@@ -129,7 +131,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           ptx::mma_bf16_ss_elect(d, ad + (uint64_t)(2 * j), bd + (uint64_t)(2 * j), IDESC, (uint32_t)((kb | j) != 0));
         ptx::mma_commit_elect(empty0 + 8 * stage);
         __syncwarp();
-        if (++stage == STAGES) {
+        if (++stage == C::STAGES) {
           stage = 0;
           phase ^= 1;
         }
