@@ -1,9 +1,8 @@
 #!/bin/bash
-# cfg4 launch list + ncu --set full on the decode kernels
+# smoke() + compute-sanitizer memcheck / racecheck on the config-4 parity tests (PDL chain, new kernels)
 mkdir -p gpurun_out
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/s2s_launches.csv python tools/s2s_probe.py 1024 1 > gpurun_out/s2s_probe.log 2>&1
-echo "launch list rc=$?"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_attn_decoder -c 2 -o gpurun_out/s2s_attn -f python tools/s2s_probe.py 1024 1 > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_layernorm -s 20 -c 1 -o gpurun_out/s2s_ln -f python tools/s2s_probe.py 1024 1 > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_gemm_tma -s 40 -c 8 -o gpurun_out/s2s_gemm -f python tools/s2s_probe.py 1024 1 > /dev/null 2>&1
-ls -la gpurun_out/
+timeout 600 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -2
+timeout 1200 compute-sanitizer --tool memcheck --log-file gpurun_out/memcheck_s2s.log python -m pytest tests/test_gpu.py -m gpu -x -q -k "cfg4_seq2seq_parity or cfg1" 2>&1 | tail -2
+tail -2 gpurun_out/memcheck_s2s.log
+timeout 1200 compute-sanitizer --tool racecheck --log-file gpurun_out/racecheck_s2s.log python -m pytest tests/test_gpu.py -m gpu -x -q -k "cfg4_seq2seq_parity and 8" 2>&1 | tail -2
+tail -2 gpurun_out/racecheck_s2s.log
