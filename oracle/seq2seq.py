@@ -94,10 +94,14 @@ def encoder(src, P, cfg, mode):
     return x
 
 
-def greedy_decode(src, P, cfg, mode="mirror", eos_bias=None, max_steps=None):
+def greedy_decode(src, P, cfg, mode="mirror", eos_bias=None, max_steps=None, forced=None):
     """One sequence.  Returns (tokens [max_len] int, length, top1 logit per step [max_len]
     (nan after done), step-0 logits [V], preds).  eos_bias(t, src) overrides the length
-    guard bias (e.g. -inf to force fixed-length decoding)."""
+    guard bias (e.g. -inf to force fixed-length decoding).
+
+    forced (teacher forcing, SURVEY 8(c) "the oracle recomputes each step from the GPU's own
+    prefix"): a token sequence fed as the decoder input instead of the oracle's own choice;
+    out[t] is still the oracle's argmax at step t, the loop stops after forced[t] == EOS."""
     d, H, L = cfg["d"], cfg["heads"], cfg["max_len"]
     pad, bos, eos = cfg["pad"], cfg["bos"], cfg["eos"]
     m = encoder(src, P, cfg, mode)
@@ -146,8 +150,8 @@ def greedy_decode(src, P, cfg, mode="mirror", eos_bias=None, max_steps=None):
         preds.append(("token", (srt[1] - srt[0]) / max(1.0, abs(srt[1])), 0.0))
         out[t] = tok
         top1[t] = z[tok]
-        tok_in = tok
-        if tok == eos:                                          # the If node on the output token (L265)
+        tok_in = tok if forced is None else int(forced[t])
+        if tok_in == eos:                                          # the If node on the output token (L265)
             done = True
             length = t + 1
     return out, length, top1, z0, preds

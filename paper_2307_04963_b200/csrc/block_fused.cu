@@ -615,12 +615,7 @@ cudaError_t launch_ch(const BlockArgs& a, int max_rows, int num_sms, cudaStream_
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_block_fused<C, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  if (cudaError_t e = ensure_smem(k_block_fused<C, H>, G::SMEM)) return e;
   int grid = max_rows < num_sms ? max_rows : num_sms;
   if (grid < 1) grid = 1;
   k_block_fused<C, H><<<grid, THREADS, G::SMEM, stream>>>(wm, tm[0], tm[1], a);

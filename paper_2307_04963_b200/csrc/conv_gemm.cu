@@ -691,13 +691,7 @@ cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t 
   }
   const int smem = SMEM_MISC + pl.stages * CG<BN>::A_BYTES +
                    (pl.bres ? kblocks : pl.stages) * BB + (pl.staged ? 2 * EPI_WG : 0);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_conv_gemm<BN, IM2COL, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         SMEM_LIMIT);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  if (cudaError_t e = ensure_smem(k_conv_gemm<BN, IM2COL, RT>, SMEM_LIMIT)) return e;
   const long long tiles = ((long long)Mmax + BM - 1) / BM * (a.Cout / BN);
   int grid = (int)(tiles < num_sms ? tiles : num_sms);
   if (grid < 1) grid = 1;

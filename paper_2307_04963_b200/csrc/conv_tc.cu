@@ -270,12 +270,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_conv_tc(const ConvArgs a) {
 template <int BN>
 cudaError_t launch_bn(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream) {
   using C = Cfg<BN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_conv_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  if (cudaError_t e = ensure_smem(k_conv_tc<BN>, C::SMEM_BYTES)) return e;
   const long long max_m = (long long)max_rows * a.Ho * a.Wo;
   const long long tiles = ((max_m + BM - 1) / BM) * (a.Cout / BN);
   int grid = (int)(tiles < num_sms ? tiles : num_sms);

@@ -665,12 +665,7 @@ cudaError_t launch_tma_bn(const ConvArgs& a, int max_rows, int num_sms, cudaStre
     case 8: kern = k_conv_tma<BN, 8>; break;
     default: return cudaSuccess;
   }
-  static bool attr[9] = {false};
-  if (!attr[a.C / 16]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr[a.C / 16] = true;
-  }
+  if (cudaError_t e = ensure_smem(kern, 227 * 1024)) return e;
   const long long groups = (max_rows + P.samples_per_group - 1) / P.samples_per_group;
   const long long tiles = groups * P.tiles_per_group * n_tiles;
   int grid = (int)(tiles < num_sms ? tiles : num_sms);

@@ -214,12 +214,7 @@ cudaError_t launch_bn(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_tma<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, GCfg<BN>::SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  if (cudaError_t e = ensure_smem(k_gemm_tma<BN>, GCfg<BN>::SMEM)) return e;
   const long long tiles = (long long)((max_rows + BM - 1) / BM) * (a.Cout / BN);
   int grid = (int)(tiles < num_sms ? tiles : num_sms);
   if (grid < 1) grid = 1;
@@ -237,7 +232,7 @@ cudaError_t launch_gemm_tma(const ConvArgs& a, int max_rows, int num_sms, cudaSt
   // 256-wide N tiles unless they leave more than half of the SMs idle (small-M decode GEMMs)
   const long long m_tiles = (max_rows + BM - 1) / BM;
   if (a.Cout % 256 == 0 && m_tiles * (a.Cout / 256) >= num_sms / 2) return launch_bn<256>(a, max_rows, num_sms, stream);
-  if (m_tiles * (a.Cout / 128) >= num_sms / 2) return launch_bn<128>(a, max_rows, num_sms, stream);
+  if (a.Cout % 128 == 0 && m_tiles * (a.Cout / 128) >= num_sms / 2) return launch_bn<128>(a, max_rows, num_sms, stream);
   return launch_bn<64>(a, max_rows, num_sms, stream);   // small M, narrow N: twice the CTAs
 }
 

@@ -10,10 +10,29 @@
 // of batch size and of the position of a sample in the batch.
 #include <cuda_bf16.h>
 
+#include <map>
+#include <mutex>
+
 #include "kernels.h"
 #include "ptx.cuh"
 
 namespace dycl {
+
+cudaError_t ensure_smem(const void* func, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = done[{dev, func}];
+  if (cur >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) cur = bytes;
+  return e;
+}
+
 namespace {
 
 __device__ __forceinline__ float bf16f(uint16_t u) { return __uint_as_float((uint32_t)u << 16); }
@@ -701,12 +720,7 @@ cudaError_t launch_head(const HeadArgs& a, int max_rows, cudaStream_t s) {
     b.gpool = const_cast<float*>(a.pooled);
     b.pooled = nullptr;
     const size_t smem_fc = (size_t)FC_ROWS * b.C * sizeof(float);
-    static size_t attr_fc2 = 0;
-    if (smem_fc > 48 * 1024 && smem_fc > attr_fc2) {
-      cudaError_t e = cudaFuncSetAttribute(k_head_fc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fc);
-      if (e != cudaSuccess) return e;
-      attr_fc2 = smem_fc;
-    }
+    if (cudaError_t e = ensure_smem(k_head_fc, smem_fc)) return e;
     if (b.kind == 1 || b.C % FC_UNROLL) return cudaErrorInvalidValue;
     int gx = (max_rows + FC_ROWS - 1) / FC_ROWS;
     if (gx > 148 * 2) gx = 148 * 2;
@@ -725,24 +739,14 @@ cudaError_t launch_head(const HeadArgs& a, int max_rows, cudaStream_t s) {
     return cudaGetLastError();
   }
   const size_t smem = (HEAD_THREADS * 8 + a.C + a.K) * sizeof(float);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_head, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
+  if (cudaError_t e = ensure_smem(k_head, smem)) return e;
   int grid = max_rows < 148 * 8 ? max_rows : 148 * 8;
   if (grid < 1) grid = 1;
   k_head<<<grid, HEAD_THREADS, smem, s>>>(a);
   if (!a.wt) return cudaGetLastError();
   if (a.kind == 1 || !a.gpool) return cudaErrorInvalidValue;
   const size_t smem_fc = (size_t)FC_ROWS * a.C * sizeof(float);
-  static size_t attr_fc = 0;
-  if (smem_fc > 48 * 1024 && smem_fc > attr_fc) {
-    cudaError_t e = cudaFuncSetAttribute(k_head_fc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fc);
-    if (e != cudaSuccess) return e;
-    attr_fc = smem_fc;
-  }
+  if (cudaError_t e = ensure_smem(k_head_fc, smem_fc)) return e;
   if (a.C % FC_UNROLL) return cudaErrorInvalidValue;
   int gx = (max_rows + FC_ROWS - 1) / FC_ROWS;
   if (gx > 148 * 2) gx = 148 * 2;

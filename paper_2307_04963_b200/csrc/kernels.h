@@ -64,6 +64,14 @@ struct PdlScope {
   explicit PdlScope(bool on) : prev(pdl_flag()) { pdl_flag() = on; }
   ~PdlScope() { pdl_flag() = prev; }
 };
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) for `func` on the CURRENT device, once per
+// (device, function, size): function attributes are per device context, so a process that
+// drives graphs on several devices must set them on each (thread-safe; hostmod.cu).
+cudaError_t ensure_smem(const void* func, size_t bytes);
+template <typename... KArgs>
+inline cudaError_t ensure_smem(void (*kernel)(KArgs...), size_t bytes) {
+  return ensure_smem(reinterpret_cast<const void*>(kernel), bytes);
+}
 // Kernel launch honouring pdl_flag() (cudaLaunchKernelEx + programmatic stream serialization).
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,

@@ -91,6 +91,9 @@ def test_gate_at_half_skips():
     assert O.sigmoid(0.0) == 0.5
     assert not (O.sigmoid(0.0) > 0.5)
     assert O.sigmoid(1e-9) > 0.5
+    # the slope: sigma(ln 3) = 3/4, sigma(-ln 3) = 1/4 (closed form 1/(1+e^-z))
+    assert O.sigmoid(np.log(3.0)) == pytest.approx(0.75, abs=1e-15)
+    assert O.sigmoid(-np.log(3.0)) == pytest.approx(0.25, abs=1e-15)
 
 
 def test_metrics_golden():
@@ -431,3 +434,80 @@ def test_seq2seq_length_guard(s2s):
         assert L == int(np.floor(P["len_table"][src[i][0]])) + 1
         assert out[L - 1] == cfg["eos"] and np.all(out[L:] == cfg["pad"]) and cfg["eos"] not in out[:L - 1]
         assert len(preds) == L
+
+
+def test_seq2seq_mirror_rounding_points(s2s, monkeypatch):
+    """Mirror mode rounds exactly at the GPU's bf16 storage points (SURVEY 8(c) 'mirror'):
+    every linear's operand, q/k/v (self and cross), attention outputs and the FFN hidden;
+    residual stream, LayerNorm, softmax and logits unrounded.  Pinned against an independent
+    composition of torch fp64 primitives (F.linear, F.scaled_dot_product_attention,
+    F.layer_norm) with torch's own bf16 cast at those points, full-prefix recompute under a
+    causal mask (so the K/V cache is the rounded k/v of earlier positions).  This pins the
+    rounding POINTS: both sides use torch's cast as the rounding function (it rounds fp64 via
+    fp32, a double rounding that differs from round_bf16's direct rounding on rare ties;
+    round_bf16 itself is pinned by test_round_bf16_matches_torch_cast_and_ties)."""
+    import torch.nn.functional as F
+    from oracle import seq2seq as S
+    W, P = s2s
+    real_round = S.round_bf16
+    monkeypatch.setattr(S, "round_bf16",
+                        lambda v: torch.tensor(np.asarray(v, np.float64)).to(torch.bfloat16).double().numpy())
+    cfg = dict(wl.S2S)
+    d, H = cfg["d"], cfg["heads"]
+    src = wl.token_inputs(wl.INPUT_SEED, 21, 1)[0]
+    steps = 3
+    out, _, top1, z0, _ = S.greedy_decode(src, P, cfg, "mirror", eos_bias=lambda t, s: -np.inf, max_steps=steps)
+    T = lambda a: torch.tensor(np.asarray(a, np.float64))  # noqa: E731
+    rb = lambda t: t.to(torch.bfloat16).to(torch.float64)  # noqa: E731
+
+    def lin(x, w, b):
+        return F.linear(rb(x), T(P[w]), T(P[b]))
+
+    def mha(q, k, v, causal):
+        sp = lambda t: t.reshape(t.shape[0], H, d // H).transpose(0, 1)  # noqa: E731
+        o = F.scaled_dot_product_attention(sp(q)[None], sp(k)[None], sp(v)[None], is_causal=causal)[0]
+        return rb(o.transpose(0, 1).reshape(q.shape[0], d))
+
+    def ln(x, p):
+        return F.layer_norm(x, (d,), T(P[p + ".g"]), T(P[p + ".b"]), eps=1e-5)
+
+    pe = T(S.positional_encoding(64, d))
+    with torch.no_grad():
+        m = T(P["src_emb"][src]) * np.sqrt(d) + pe[:len(src)]
+        for l in range(cfg["enc_layers"]):
+            p = f"enc{l}"
+            qkv = rb(lin(m, p + ".wqkv", p + ".bqkv"))
+            a = mha(qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:], False)
+            m = ln(lin(a, p + ".wo", p + ".bo") + m, p + ".ln1")
+            h = rb(F.relu(lin(m, p + ".w1", p + ".b1")))
+            m = ln(lin(h, p + ".w2", p + ".b2") + m, p + ".ln2")
+        y = [cfg["bos"]]
+        for t in range(steps):
+            x = T(P["tgt_emb"][np.array(y)]) * np.sqrt(d) + pe[:len(y)]
+            for l in range(cfg["dec_layers"]):
+                p = f"dec{l}"
+                qkv = rb(lin(x, p + ".wqkv", p + ".bqkv"))
+                a = mha(qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:], True)
+                x = ln(lin(a, p + ".wo", p + ".bo") + x, p + ".ln1")
+                q2 = rb(lin(x, p + ".wq2", p + ".bq2"))
+                kv = rb(lin(m, p + ".wkv2", p + ".bkv2"))
+                a2 = mha(q2, kv[:, :d], kv[:, d:], False)
+                x = ln(lin(a2, p + ".wo2", p + ".bo2") + x, p + ".ln2")
+                h = rb(F.relu(lin(x, p + ".w1", p + ".b1")))
+                x = ln(lin(h, p + ".w2", p + ".b2") + x, p + ".ln3")
+            z = lin(x[-1:], "lm.w", "lm.b")[0]
+            z[cfg["eos"]] = -np.inf
+            tok = int(torch.argmax(z))
+            assert tok == out[t]
+            assert abs(float(z[tok]) - top1[t]) <= 1e-9 * max(1.0, abs(top1[t]))
+            if t == 0:
+                zz, z0c = z.numpy().copy(), z0.copy()
+                zz[cfg["eos"]] = z0c[cfg["eos"]] = 0
+                np.testing.assert_allclose(z0c, zz, rtol=1e-9, atol=1e-9)
+            y.append(tok)
+    # and the rounding really happens: mirror differs from exact
+    monkeypatch.setattr(S, "round_bf16", real_round)
+    _, _, top1e, z0e, _ = S.greedy_decode(src, P, cfg, "exact", eos_bias=lambda t, s: -np.inf, max_steps=1)
+    z0m = z0.copy()
+    z0m[cfg["eos"]] = z0e[cfg["eos"]] = 0
+    assert np.max(np.abs(z0m - z0e)) > 1e-6
