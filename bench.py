@@ -1,19 +1,21 @@
 """Benchmark: batched dynamic-NN inference (DyCL, arXiv 2307.04963) on B200.
 
-Workload (BASELINE.json configs[1], the configuration its metric is quoted on):
-ShallowDeep-style early-exit ResNet-56 on synthetic 32x32x3 CIFAR-shaped inputs,
-batch 4096 per GPU, 4 internal classifiers + final head, tau = 0.9, calibrated
-heads (workloads/calib/cfg2.json).  One step = one full pass of the hot path
-(input cast, every sub-network, predicates, compaction, gathers, scatters) over
-one batch, through the C ABI (dycl_run).
+Headline workload (BASELINE.json configs[4], the largest configuration and the one its
+multi-GPU metric "samples/sec at 1/2/4/8 B200" is sharded on): early-exit ResNet-50 v1.5 on
+synthetic 224x224x3 inputs, exits after stages 1/2/3 + final head (1000 classes), tau = 0.9,
+calibrated heads (workloads/calib/cfg5.json), GLOBAL batch 65536 sharded over the ranks
+(rank r takes samples [r*B/G, (r+1)*B/G): strong scaling), each rank's shard resident in
+HBM and processed in chunks of 2048 through the C ABI (dycl_run).  One step = one full
+pass of the hot path (input cast, every sub-network, predicates, compaction, gathers,
+scatters) over the whole global batch.  With G > 1 the survivors of exit 0 are rebalanced
+across ranks inside dycl_run over NCCL (dycl_set_comm; --no-rebalance disables).
 
-  python bench.py [--gpus N --steps K --warmup W]            # our arm
-  python bench.py --impl reference ...                        # the CPU oracle arm
-  torchrun --nproc-per-node N bench.py --gpus N ...           # N > 1: one rank per GPU
+  python bench.py [--gpus N --steps K --warmup W] [--config 2]   # our arm (default config 5)
+  python bench.py --impl reference ...                          # the CPU oracle arm
+  torchrun --nproc-per-node N bench.py --gpus N ...             # N > 1: one rank per GPU
 
-Multi-GPU: samples are independent (Eq. 2 is per-x), so each rank processes its
-own 4096-sample slice of the global batch (weak scaling) with no collective on
-the data path; timing = max over ranks of the per-rank device time.
+Other configs (--config 1..4) are secondary lines: per-GPU batches as BASELINE.json states
+them (weak scaling).  Timing = max over ranks of the per-rank device time (CUDA events).
 """
 from __future__ import annotations
 
@@ -31,16 +33,16 @@ sys.path.insert(0, ROOT)
 
 METRIC = "dynamic-inference samples/sec"
 UNIT = "samples/s"
-BATCH = 4096
-WORKLOAD = ("cfg2: ShallowDeep-style early-exit ResNet-56, synthetic 32x32x3 CIFAR-shaped inputs, "
-            "4 ICs after blocks 5/11/16/22 + final head, tau=0.9, calibrated heads")
+DEFAULT_CONFIG = 5
+GLOBAL_BATCH_CONFIGS = {5}         # BASELINE configs[4]: "batch 65536 sharded over 1/2/4/8 B200"
+CHUNK = {5: 2048}                  # per-dycl_run chunk (graph finalised for this many rows)
 
 
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return p["hbm_gbs"], p["bf16_tflops"], p["bf16_tflops_sustained"], "measured"
+        return p["hbm_gbs"], p["bf16_tflops"], p["bf16_tflops_sustained"], "measured (MEASURED_PEAKS.json)"
     except Exception:
         return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
 
@@ -50,6 +52,11 @@ def _dist():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def shard(B, ws, rank):
+    """Rank r's contiguous slice [r*B/G, (r+1)*B/G) of a global batch."""
+    return rank * B // ws, (rank + 1) * B // ws
 
 
 class ClockSampler:
@@ -100,29 +107,69 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_oracle_rate(n_samples: int, seed_offset: int = 0):
-    """The oracle (as it stands) on this host's cores: per-sample interpreter, mirror mode."""
+WORKLOADS = {
+    1: "cfg1: tiny early-exit MLP, 3 blocks width 64, 2 exit heads + final, tau=0.9, batch 32 random fp32 inputs",
+    2: "cfg2: ShallowDeep-style early-exit ResNet-56, synthetic 32x32x3 CIFAR-shaped inputs, 4 ICs after blocks "
+       "5/11/16/22 + final head, tau=0.9, calibrated heads, batch 4096 per GPU",
+    3: "cfg3: SkipNet-style gated ResNet-38, 17 feed-forward gates, synthetic 32x32x3, batch 8192 per GPU",
+    4: "cfg4: 6+6 post-LN Transformer d=512, greedy decode with per-sequence EOS / max-len 64 loop guard, "
+       "batch 1024 random-token sequences (src len 64) per GPU",
+    5: "cfg5: early-exit ResNet-50 v1.5, synthetic 224x224x3, exits after stages 1/2/3 + final (1000 classes), "
+       "tau=0.9, global batch 65536 sharded over the GPUs (inputs resident in HBM, chunks of 2048 per dycl_run)",
+}
+BATCHES = {1: 32, 2: 4096, 3: 8192, 4: 1024, 5: 65536}
+KERNEL_NAMES = {
+    "block": "k_block_fused (a1: 1-8 whole residual blocks per sample, SMEM-resident, row-tap tcgen05 convs)",
+    "conv": "a1 conv class (k_conv_gemm NHWC TMA-im2col GEMM / k_conv_tma / k_gemm_tma on tcgen05, fused epilogue)",
+    "gemm": "k_gemm_tma (a7/a8 decoder + encoder projections, FFN, LM head on tcgen05)",
+    "attn": "a7/a8 attention (decode KV streaming / encoder)",
+}
+
+
+def oracle_sample(cfg, n, start=0):
+    """The oracle (as it stands, mirror mode, all host cores) on n seeded samples of config cfg.
+    Returns (samples/s, cores, seconds, description)."""
     import oracle as O
     import workloads as wl
     from oracle import programs as prg
-    P = prg.prepare(wl.sdn_r56_weights())
-    X = wl.image_inputs(wl.INPUT_SEED, seed_offset, n_samples)
     cores = len(os.sched_getaffinity(0))
+    if cfg == 4:
+        from concurrent.futures import ThreadPoolExecutor
+        from oracle import seq2seq as S
+        P = S.prepare_s2s(wl.seq2seq_weights())
+        src = wl.token_inputs(wl.INPUT_SEED, start, n)
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(cores) as ex:
+            list(ex.map(lambda i: S.greedy_decode(src[i], P, wl.S2S, "mirror"), range(n)))
+        dt = time.perf_counter() - t0
+        return n / dt, cores, dt, (f"{n} cfg4 sequences (seeded tokens {start}..{start + n - 1}), per-sequence fp64 "
+                                   f"greedy decode, mirror mode")
+    W = {1: wl.mlp_weights, 2: wl.sdn_r56_weights, 3: wl.skipnet_r38_weights, 5: wl.resnet50_ee_weights}[cfg]()
+    P = prg.prepare(W)
+    X = (wl.mlp_inputs(wl.INPUT_SEED, start, n) if cfg == 1 else
+         wl.image_inputs(wl.INPUT_SEED, start, n, hw=224 if cfg == 5 else 32))
     t0 = time.perf_counter()
-    O.run_batch(O.sdn_resnet56, X, P, "mirror", threads=cores)
+    O.run_batch(O.PROGRAMS[cfg], X, P, "mirror", threads=cores)
     dt = time.perf_counter() - t0
-    return n_samples / dt, cores, dt
+    return n / dt, cores, dt, (f"{n} cfg{cfg} samples (seeded inputs {start}..{start + n - 1}), per-sample fp64 "
+                               f"interpreter, mirror mode")
+
+
+REF_SAMPLES = {1: 4096, 2: 32, 3: 32, 4: 4, 5: 8}
 
 
 def run_reference(args):
+    """The base contract's reference arm for this tier: the CPU oracle timed as it stands on the
+    host cores, each step a bounded sample of the same workload (rank 0 only)."""
     ws, rank, _ = _dist()
     if rank != 0:
         return
-    per_step = args.ref_samples
+    per_step = args.ref_samples or REF_SAMPLES[args.config]
     times = []
+    what = ""
     cores = len(os.sched_getaffinity(0))
     for i in range(args.warmup + args.steps):
-        rate, cores, dt = cpu_oracle_rate(per_step, seed_offset=i * per_step)
+        _, cores, dt, what = oracle_sample(args.config, per_step, start=i * per_step)
         if i >= args.warmup:
             times.append(dt)
     tot = sum(times)
@@ -130,39 +177,44 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": WORKLOAD, "samples_per_step": per_step},
+        "higher_is_better": True, "scaling": "strong" if args.config in GLOBAL_BATCH_CONFIGS else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.config], "samples_per_step": per_step},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"{per_step} samples of cfg2 per step (seeded inputs), per-sample fp64 interpreter"},
+                         "sample": f"per step: {what}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-WORKLOADS = {
-    1: "cfg1: tiny early-exit MLP, 3 blocks width 64, 2 exit heads + final, tau=0.9, batch 32 random fp32 inputs",
-    2: WORKLOAD,
-    3: "cfg3: SkipNet-style gated ResNet-38, 17 feed-forward gates, synthetic 32x32x3, batch 8192",
-    4: "cfg4: 6+6 post-LN Transformer d=512, greedy decode with per-sequence EOS / max-len 64 loop guard, "
-       "batch 1024 random-token sequences (src len 64)",
-    5: "cfg5: early-exit ResNet-50 v1.5, synthetic 224x224x3, exits after stages 1/2/3 + final, batch 65536 per GPU "
-       "(processed in chunks of 2048, all inputs resident in HBM)",
-}
-BATCHES = {1: 32, 2: 4096, 3: 8192, 4: 1024, 5: 65536}
-
-
 class ImageJob:
-    """configs 1/2/3/5: one step = dycl_run over every chunk of the per-rank batch."""
+    """configs 1/2/3/5: one step = dycl_run over every chunk of this rank's samples."""
 
-    def __init__(self, cfg, rank, dev, torch):
+    def __init__(self, cfg, rank, ws, dev, torch, rebalance):
         import workloads as wl
         from paper_2307_04963_b200 import programs as P
         self.cfg, self.torch = cfg, torch
-        self.B = BATCHES[cfg]
-        self.chunk = 2048 if cfg == 5 else self.B
+        if cfg in GLOBAL_BATCH_CONFIGS:
+            g0, g1 = shard(BATCHES[cfg], ws, rank)
+            self.B = g1 - g0
+            per_rank_max = max(shard(BATCHES[cfg], ws, r)[1] - shard(BATCHES[cfg], ws, r)[0] for r in range(ws))
+        else:
+            g0, self.B = rank * BATCHES[cfg], BATCHES[cfg]
+            per_rank_max = self.B
+        self.g0 = g0
+        chunk = CHUNK.get(cfg, per_rank_max)
+        # the same number of chunks on every rank (rebalancing runs them in lock step)
+        self.n_chunks = max(1, (per_rank_max + chunk - 1) // chunk)
+        self.bounds = [self.B * i // self.n_chunks for i in range(self.n_chunks + 1)]
+        self.chunk = max(b - a for a, b in zip(self.bounds, self.bounds[1:]))
         W = {1: wl.mlp_weights, 2: wl.sdn_r56_weights, 3: wl.skipnet_r38_weights, 5: wl.resnet50_ee_weights}[cfg]()
-        self.model = P.BUILDERS[cfg](W, self.chunk, device=dev.index or 0)
-        g0 = rank * self.B
+        self.model = P.BUILDERS[cfg](W, (per_rank_max + self.n_chunks - 1) // self.n_chunks + 1,
+                                     device=dev.index or 0)
+        self.rebalance = False
+        if rebalance and ws > 1:
+            from paper_2307_04963_b200 import dist as DI
+            DI.attach(self.model, rank, ws)
+            self.rebalance = True
         if cfg == 1:
             X = torch.from_numpy(wl.mlp_inputs(wl.INPUT_SEED, g0, self.B)).to(dev)
         elif cfg == 5:
@@ -177,10 +229,15 @@ class ImageJob:
         self.h2d = int(X.numel() * 4)
         self.d2h = int(self.B * (K * 4 + 4))
 
-    def step(self, stream):
-        for c0 in range(0, self.B, self.chunk):
-            c1 = min(self.B, c0 + self.chunk)
-            self.model.run(self.x[c0:c1], self.logits[c0:c1], self.path[c0:c1], stream=stream)
+    def chunks(self):
+        return zip(self.bounds, self.bounds[1:])
+
+    def step(self, stream, after_chunk=None):
+        for c0, c1 in self.chunks():
+            self.model.run(self.x[c0:c1], self.logits[c0:c1], self.path[c0:c1], stream=stream,
+                           global_offset=self.g0 + c0)
+            if after_chunk:
+                after_chunk()
 
     def host_setup(self):
         torch = self.torch
@@ -189,9 +246,9 @@ class ImageJob:
         self.ph = torch.empty(self.B, dtype=torch.int32).pin_memory()
 
     def step_host(self, stream):
-        for c0 in range(0, self.B, self.chunk):
-            c1 = min(self.B, c0 + self.chunk)
-            self.model.run_host(self.xh[c0:c1], self.lh[c0:c1], self.ph[c0:c1], stream=stream)
+        for c0, c1 in self.chunks():
+            self.model.run_host(self.xh[c0:c1], self.lh[c0:c1], self.ph[c0:c1], stream=stream,
+                                global_offset=self.g0 + c0)
 
     def check_host(self):
         return bool(np.array_equal(self.ph.numpy(), self.path.cpu().numpy()))
@@ -205,11 +262,13 @@ class ImageJob:
 class S2SJob:
     """config 4: one step = encoder + guarded greedy decode of the per-rank batch."""
 
-    def __init__(self, cfg, rank, dev, torch):
+    def __init__(self, cfg, rank, ws, dev, torch, rebalance):
         import workloads as wl
         from paper_2307_04963_b200 import programs as P
         self.cfg, self.torch = cfg, torch
         self.B = BATCHES[4]
+        self.n_chunks = 1
+        self.rebalance = False
         c = wl.S2S
         self.model = P.build_seq2seq(wl.seq2seq_weights(), c, self.B, device=dev.index or 0)
         self.g = None
@@ -220,8 +279,10 @@ class S2SJob:
         self.h2d = int(src.nbytes)
         self.d2h = int(self.B * (c["max_len"] + 1) * 4)
 
-    def step(self, stream):
+    def step(self, stream, after_chunk=None):
         self.model.run(self.src, self.tok, self.len, stream=stream)
+        if after_chunk:
+            after_chunk()
 
     def host_setup(self):
         torch = self.torch
@@ -240,6 +301,16 @@ class S2SJob:
         return {"mean_length": float(ln.mean()), "tokens": int(ln.sum())}
 
 
+def _traffic(cfg, kind):
+    """ncu DRAM bytes per launch of the dominant kernel class (profiles/r02_traffic.json, one
+    `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum` capture of one step / chunk)."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "r02_traffic.json")))
+        return t[f"cfg{cfg}"][kind]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def run_dycl(args):
     import torch
     from paper_2307_04963_b200 import dycl as D
@@ -251,8 +322,7 @@ def run_dycl(args):
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     stream = torch.cuda.current_stream()
-    job = (S2SJob if args.config == 4 else ImageJob)(args.config, rank, dev, torch)
-    B = job.B
+    job = (S2SJob if args.config == 4 else ImageJob)(args.config, rank, ws, dev, torch, not args.no_rebalance)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > L2 (126 MB)
 
     for _ in range(args.warmup):
@@ -273,36 +343,39 @@ def run_dycl(args):
         ev[i][1].record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
-    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
     # Pass 2 (the roofline): the same K steps again with per-launch CUDA events recorded by
-    # libdycl on the launch stream around every kernel (kept out of pass 1: ~80 event pairs
-    # per step perturb the step time).
-    # per-kind totals: ms, algorithmic bytes, algorithmic flops, launches
-    kind_tot = {}
-    launches = 0
+    # libdycl on the launch stream around every kernel, read back after every chunk (kept out
+    # of pass 1: the event pairs perturb the step time).
+    kind_tot = {}                              # kind -> [ms, bytes, flops, launches, records]
+    n_prof = [0]
     if job.g is not None:
         D.dycl_set_profiling(job.g, 1)
         prof_read = lambda: D.dycl_profile_read(job.g)   # noqa: E731
     else:
         D.dycl_s2s_set_profiling(job.model.h, 1)
         prof_read = lambda: D.dycl_s2s_profile_read(job.model.h)   # noqa: E731
-    for i in range(args.steps):
-        flush.zero_()
-        job.step(stream)     # profiling records the last chunk's launches; chunks are identical in shape
-        for p in prof_read():    # syncs the stream
+
+    def collect():
+        for p in prof_read():                  # syncs the stream
+            n_prof[0] += 1
             t = kind_tot.setdefault(p["kind"], [0.0, 0.0, 0.0, 0, []])
             t[0] += p["ms"]
             t[1] += p["bytes"]
             t[2] += p["flops"]
             t[3] += 1
             t[4].append((p["ms"], p["bytes"], p["flops"]))
+
+    for i in range(args.steps):
+        flush.zero_()
+        job.step(stream, after_chunk=collect)
     torch.cuda.synchronize()
     if job.g is not None:
         D.dycl_set_profiling(job.g, 0)
-        launches = D.dycl_launches_per_run(job.g) * args.steps * ((B + job.chunk - 1) // job.chunk)
     else:
         D.dycl_s2s_set_profiling(job.model.h, 0)
-        launches = D.dycl_s2s_launches(job.model.h) * args.steps
+    launches = n_prof[0]                       # this library's kernels in K steps (profiled pass)
     kind_ms = {k: v[0] for k, v in kind_tot.items()}
     hist = job.hist()
 
@@ -314,6 +387,8 @@ def run_dycl(args):
     for i in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
         t0 = time.perf_counter()
         job.step_host(stream)
         e2e_ms += (time.perf_counter() - t0) * 1e3
@@ -330,46 +405,38 @@ def run_dycl(args):
         return
 
     hbm, tf_burst, tf_sus, peak_src = _peaks()
-    value = B * ws * args.steps / (total_ms / 1e3)
+    global_samples = BATCHES[args.config] if args.config in GLOBAL_BATCH_CONFIGS else BATCHES[args.config] * ws
+    value = global_samples * args.steps / (total_ms / 1e3)
+    # a step of >= 100 ms keeps the tensor pipe busy long enough to reach the sustained
+    # (power-limited) clock: the sustained peak applies; shorter steps: the burst peak
+    long_step = total_ms / args.steps >= 100.0
+    tf_peak = tf_sus if long_step else tf_burst
     roof = None
     step_prof_ms = sum(kind_ms.values())
     if kind_tot:
-        # the dominant kernel class of the step (largest share of the per-launch event time)
         dom = max(kind_tot, key=lambda k: kind_tot[k][0])
         ms_, by_, fl_, n_, recs = kind_tot[dom]
         gbs = by_ / (ms_ / 1e3) / 1e9
         tfl = fl_ / (ms_ / 1e3) / 1e12
-        # per-launch roofline: ideal = max(FLOPs / tensor peak, bytes / HBM peak); a launch is
-        # tensor- or HBM-bound by which term wins; efficiency = sum(ideal) / sum(measured)
+        # per-launch roofline: ideal = max(FLOPs / tensor peak, bytes / HBM peak)
         split = {"tensor": [0.0, 0.0], "hbm": [0.0, 0.0]}
         for lm, lb, lf in recs:
-            it, ib = lf / (tf_sus * 1e12) * 1e3, lb / (hbm * 1e9) * 1e3
+            it, ib = lf / (tf_peak * 1e12) * 1e3, lb / (hbm * 1e9) * 1e3
             k = "tensor" if it > ib else "hbm"
             split[k][0] += max(it, ib)
             split[k][1] += lm
         roof_eff = (split["tensor"][0] + split["hbm"][0]) / ms_ if ms_ else None
-        names = {
-            "block": "k_block_fused (a1: 1-8 whole residual blocks per sample, SMEM-resident, row-tap tcgen05 convs)",
-            "conv": "a1 conv class (k_conv_gemm NHWC im2col GEMM / k_conv_tma / k_gemm_tma on tcgen05, fused epilogue)",
-            "gemm": "k_gemm_tma (a7/a8 decoder + encoder projections, FFN, LM head on tcgen05)",
-            "attn": "k_attn_decoder (a7 decode attention, KV-cache streaming)",
-        }
-        tensor_bound = split["tensor"][1] > split["hbm"][1]   # the bound that covers most of the class's time
+        tensor_bound = split["tensor"][1] > split["hbm"][1]
+        traffic = _traffic(args.config, dom)
         if tensor_bound:
-            roof = {"kernel": names.get(dom, dom), "bound": "tensor", "achieved": tfl, "peak": tf_sus,
-                    "unit": "TFLOP/s", "frac": tfl / tf_sus, "traffic": None,
-                    "peak_source": peak_src + " bf16 sustained", "hbm_GBps": gbs}
+            roof = {"kernel": KERNEL_NAMES.get(dom, dom), "bound": "tensor", "achieved": tfl, "peak": tf_peak,
+                    "unit": "TFLOP/s", "frac": tfl / tf_peak, "traffic": traffic,
+                    "peak_source": peak_src + (" bf16 sustained (step >= 100 ms)" if long_step else " bf16 burst"),
+                    "frac_of_burst": tfl / tf_burst, "frac_of_sustained": tfl / tf_sus, "hbm_GBps": gbs}
         else:
-            traffic = None
-            tpath = os.path.join(ROOT, "profiles", "block_traffic.json")
-            if dom == "block" and args.config == 2 and os.path.exists(tpath):
-                try:
-                    traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
-                except Exception:
-                    traffic = None
-            roof = {"kernel": names.get(dom, dom), "bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
+            roof = {"kernel": KERNEL_NAMES.get(dom, dom), "bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
                     "frac": gbs / hbm, "traffic": traffic, "peak_source": peak_src,
-                    "tensor_tflops": tfl, "tensor_frac_of_sustained": tfl / tf_sus}
+                    "tensor_tflops": tfl, "tensor_frac_of_burst": tfl / tf_burst}
         roof.update({"roofline_efficiency": roof_eff,
                      "launch_split": {k: {"ms_per_step": v[1] / args.steps,
                                           "frac_of_own_roofline": v[0] / v[1] if v[1] else None}
@@ -380,22 +447,30 @@ def run_dycl(args):
                      "avg_launch_ms": ms_ / max(n_, 1),
                      "launches_per_step": n_ // max(args.steps, 1),
                      "measured": "per-launch CUDA events (libdycl profiling) on the launch stream over a second "
-                                 "pass of the same K steps; achieved = algorithmic bytes (or FLOPs) / kernel time",
+                                 "pass of the same K steps (every chunk); achieved = algorithmic bytes (or FLOPs) "
+                                 "/ kernel time; traffic = ncu DRAM read+write bytes per launch "
+                                 "(profiles/r02_traffic.json)",
                      "classes": {k: {"ms_per_step": v[0] / args.steps, "share": v[0] / step_prof_ms,
                                      "GBps": v[1] / (v[0] / 1e3) / 1e9 if v[0] else 0.0,
                                      "TFLOPs": v[2] / (v[0] / 1e3) / 1e12 if v[0] else 0.0}
                                  for k, v in sorted(kind_tot.items(), key=lambda kv: -kv[1][0])}})
+    strong = args.config in GLOBAL_BATCH_CONFIGS
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": total_ms / args.steps, "ms_per_step_std": float(np.std(step_ms)),
+        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config], "batch_per_gpu": B, "global_batch": B * ws,
+        "config": {"workload": WORKLOADS[args.config], "global_batch": global_samples,
+                   "batch_per_gpu": job.B, "chunks_per_gpu": job.n_chunks,
                    "precision": "bf16 tensor-core operands, fp32 accumulate, fp32 residual stream",
-                   "l2": "flushed (256 MB write) before every timed step, flush not timed",
-                   "parallelism": f"dp{ws} (independent shards, no collective)",
+                   "l2": "flushed (256 MB write) before every timed step, flush not timed; inputs > L2",
+                   "parallelism": (f"dp{ws}: contiguous shards of the global batch" if strong else
+                                   f"dp{ws}: independent per-GPU batches") +
+                                  ("; survivors of exit 0 rebalanced over NCCL inside dycl_run" if job.rebalance
+                                   else "; no collective on the data path"),
                    "decisions_rank0": hist},
         "clocks": clk,
-        "e2e": {"value": B * ws * args.steps / (e2e_ms / 1e3), "unit": UNIT,
+        "e2e": {"value": global_samples * args.steps / (e2e_ms / 1e3), "unit": UNIT,
                 "h2d_bytes_per_step": job.h2d, "d2h_bytes_per_step": job.d2h},
         "gpu_launches": launches,
         "roofline": roof,
@@ -404,8 +479,8 @@ def run_dycl(args):
     if args.config == 4:
         line["tokens_per_s"] = hist["tokens"] * ws * args.steps / (total_ms / 1e3)
     if ws == 1 and not args.no_cpu_baseline:
-        n_cpu = {1: 4096, 2: args.cpu_samples, 3: 2048, 4: 48, 5: 32}[args.config]
-        rate, cores, dt, what = cpu_oracle_rate_cfg(args.config, n_cpu)
+        n_cpu = args.cpu_samples or {1: 4096, 2: 4096, 3: 2048, 4: 48, 5: 64}[args.config]
+        rate, cores, dt, what = oracle_sample(args.config, n_cpu)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
                                 "sample": f"{what}, {dt:.1f} s wall"}
     print(json.dumps(line), flush=True)
@@ -413,49 +488,24 @@ def run_dycl(args):
         torch.distributed.destroy_process_group()
 
 
-def cpu_oracle_rate_cfg(cfg, n):
-    """The oracle on this host's cores for a bounded sample of config `cfg`."""
-    import oracle as O
-    import workloads as wl
-    from oracle import programs as prg
-    cores = len(os.sched_getaffinity(0))
-    if cfg == 2:
-        rate, cores, dt = cpu_oracle_rate(n)
-        return rate, cores, dt, f"{n} cfg2 samples (seeded inputs 0..{n - 1}), per-sample fp64 interpreter, mirror mode"
-    if cfg == 4:
-        from concurrent.futures import ThreadPoolExecutor
-        from oracle import seq2seq as S
-        P = S.prepare_s2s(wl.seq2seq_weights())
-        src = wl.token_inputs(wl.INPUT_SEED, 0, n)
-        t0 = time.perf_counter()
-        with ThreadPoolExecutor(cores) as ex:
-            list(ex.map(lambda i: S.greedy_decode(src[i], P, wl.S2S, "mirror"), range(n)))
-        dt = time.perf_counter() - t0
-        return n / dt, cores, dt, f"{n} cfg4 sequences (seeded tokens), per-sequence fp64 greedy decode, mirror mode"
-    W = {1: wl.mlp_weights, 3: wl.skipnet_r38_weights, 5: wl.resnet50_ee_weights}[cfg]()
-    P = prg.prepare(W)
-    X = (wl.mlp_inputs(wl.INPUT_SEED, 0, n) if cfg == 1 else
-         wl.image_inputs(wl.INPUT_SEED, 0, n, hw=224 if cfg == 5 else 32))
-    t0 = time.perf_counter()
-    O.run_batch(O.PROGRAMS[cfg], X, P, "mirror", threads=cores)
-    dt = time.perf_counter() - t0
-    return n / dt, cores, dt, f"{n} cfg{cfg} samples (seeded inputs), per-sample fp64 interpreter, mirror mode"
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=None, help="default: 10 for config 5, 50 otherwise")
+    ap.add_argument("--warmup", type=int, default=None, help="default: 3 for config 5, 5 otherwise")
     ap.add_argument("--impl", default="dycl", choices=["dycl", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5],
-                    help="BASELINE.json config (default 2: the configuration the metric is quoted on)")
-    ap.add_argument("--cpu-samples", type=int, default=4096)
-    ap.add_argument("--ref-samples", type=int, default=32)
+    ap.add_argument("--config", type=int, default=DEFAULT_CONFIG, choices=[1, 2, 3, 4, 5],
+                    help="BASELINE.json config (default 5: the largest, global batch 65536 sharded over the GPUs)")
+    ap.add_argument("--cpu-samples", type=int, default=None)
+    ap.add_argument("--ref-samples", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-rebalance", action="store_true", help="N > 1: no survivor rebalancing")
     args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
+    if args.steps is None:
+        args.steps = 10 if args.config == 5 else 50
+    if args.warmup is None:
+        args.warmup = 3 if args.config == 5 else 5
+    args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -72,8 +72,11 @@ dycl_status dycl_graph_create(int cuda_device, int in_h, int in_w, int in_c, dyc
  *     sub-network outputs) are kept in fp32; each conv/dense reads a bf16 (RNE)
  *     copy of its input; intermediates inside a block are bf16.
  *   DYCL_PREC_BF16: every activation is stored bf16 (half the bytes; logits drift
- *     ~2.5e-2 relative after 27 blocks -- see DESIGN.md §2 reading R13). */
-enum { DYCL_PREC_BF16 = 0, DYCL_PREC_FP32_STREAM = 1 };
+ *     ~4e-2 relative after 27 blocks, past the 2e-2 bar -- see DESIGN.md §2 reading R13).
+ *   DYCL_PREC_BF16X3_PARITY: DYCL_E_UNSUPPORTED for image graphs (implemented for the
+ *     generative graph, dycl_s2s_set_precision; image graphs show 0 outside-band decision
+ *     mismatches in FP32_STREAM on 512 / 512 / 256 oracle samples, R13). */
+enum { DYCL_PREC_BF16 = 0, DYCL_PREC_FP32_STREAM = 1, DYCL_PREC_BF16X3_PARITY = 2 };
 dycl_status dycl_graph_set_precision(dycl_graph g, int precision);
 
 /* Free the graph and all device memory it owns.  NULL is accepted. */
@@ -172,6 +175,13 @@ typedef struct {
   float* logits;          /* device fp32 [batch][K]   (output, original order)        */
   int32_t* path;          /* device int32 [batch]     exit index or gate mask word     */
   int32_t* node_counts;   /* device int32 [dycl_num_count_slots] live-row counts, or NULL */
+  int64_t global_offset;  /* global index of row 0 when the batch is one shard of a larger one
+                             (rank r holds [r*B/G, (r+1)*B/G)); rows handed to other
+                             ranks by rebalancing carry global_offset + row as their id.  >= 0.  */
+  float* min_margin;      /* device fp32 [batch] or NULL: per sample, the minimum over the exit /
+                             gate predicates evaluated along its path of |p - threshold| (p = max
+                             softmax for exits, sigmoid for gates; +inf if none) -- the quantity the
+                             north star's "within 1e-3 of its threshold" band is defined on (R12) */
 } dycl_io;
 
 /* Enqueue one batched inference on `stream` (a cudaStream_t, NULL = default stream).
@@ -190,6 +200,10 @@ dycl_status dycl_run(dycl_graph g, const dycl_io* io, void* stream);
  * equal one run: samples are independent). */
 dycl_status dycl_run_host(dycl_graph g, const float* input_host, int64_t batch,
                           float* logits_host, int32_t* path_host, void* stream);
+/* dycl_run_host with the dycl_io extensions: global_offset (a shard of a global batch; every
+ * sub-chunk run carries global_offset + its first row) and an optional host min_margin [batch]. */
+dycl_status dycl_run_host_ex(dycl_graph g, const float* input_host, int64_t batch, int64_t global_offset,
+                             float* logits_host, int32_t* path_host, float* min_margin_host, void* stream);
 
 /* --------------------------------------------------------- introspection --- */
 /* Number of device count slots a run writes (for dycl_io.node_counts). */
@@ -214,6 +228,47 @@ dycl_status dycl_profile_read(dycl_graph g, int32_t max_n, int32_t* kind, float*
                               double* bytes, double* flops, int32_t* n_out);
 
 /* ------------------------------------------------- multi-GPU rebalancing ---- */
+/* Samples are independent (Eq. 2 is per x), so a global batch shards across
+ * ranks with no collective: each rank runs its contiguous slice with dycl_io.global_offset.
+ * Optional survivor rebalancing: after the exits selected by the policy, the
+ * ranks all-gather their survivor counts (one int32 each; the run's one host synchronisation
+ * per rebalanced exit), every rank computes the same plan (dycl_rebalance_plan below), and
+ * surplus rows -- the bf16 / fp32 activation rows the next sub-network reads, plus 16 bytes of
+ * metadata (path word, min margin, 64-bit global id) -- move in one grouped point-to-point step
+ * on the run's stream.  Received rows are appended after the local survivors and run through
+ * the rest of the chain with them.  At the end the results of rows computed away from home go
+ * back by the reverse plans (last level first) and are scattered to their original rows by a
+ * kernel.  Every kernel is batch-position independent, so the outputs are bitwise those of the
+ * unbalanced run (tested).  A rebalancing run is issued launch by launch (no CUDA graph: it
+ * reads the counts on the host); all ranks must call dycl_run the same number of times (lock
+ * step), each with its own shard (batch may be 0).
+ *
+ * Policy: bit k set = rebalance after exit k; DYCL_REBALANCE_ALL = every exit; 0 = none
+ * (shards only).  Graphs without exits (gates only) never rebalance. */
+enum { DYCL_REBALANCE_NONE = 0, DYCL_REBALANCE_ALL = -1 };
+/* nccl_comm: an ncclComm_t spanning the `world` ranks, this process being `rank` (borrowed, not
+ * destroyed; e.g. torch's ProcessGroupNCCL._comm_ptr(), or dycl_nccl_comm_init_rank).  NCCL is
+ * resolved at run time from the libnccl.so.2 mapped in the process.  nccl_comm == NULL with
+ * world == 1 detaches (a world-1 communicator is kept: its runs all-gather and never move rows).
+ * Call after dycl_finalize (allocates the result space: (1 + #exits) x max_batch rows).
+ * Errors: INVALID_ARG, STATE, NCCL (library not found), OOM.  Run-time transport failures
+ * surface from dycl_run as DYCL_E_NCCL. */
+dycl_status dycl_set_comm(dycl_graph g, void* nccl_comm, int rank, int world, int rebalance_policy);
+/* In-process transport: `world` graphs of one process (same or different devices), each driven
+ * by its own host thread, exchange rows by device-to-device copies behind a host barrier.  Same
+ * protocol and plan as the NCCL transport; used to test rebalancing on a single GPU. */
+typedef struct dycl_local_group_s* dycl_local_group;
+dycl_status dycl_local_group_create(int world, dycl_local_group* out);
+dycl_status dycl_local_group_destroy(dycl_local_group grp);
+dycl_status dycl_set_comm_local(dycl_graph g, dycl_local_group grp, int rank, int rebalance_policy);
+/* Rows this rank sent to / received from other ranks during its last dycl_run. */
+dycl_status dycl_rebalance_stats(dycl_graph g, int64_t* rows_sent, int64_t* rows_received);
+/* NCCL bootstrap for callers without a communicator: rank 0 gets a 128-byte unique id, shares
+ * it out of band, every rank calls dycl_nccl_comm_init_rank (collective). */
+dycl_status dycl_nccl_get_unique_id(uint8_t out[128]);
+dycl_status dycl_nccl_comm_init_rank(const uint8_t id[128], int rank, int world, int cuda_device, void** comm);
+dycl_status dycl_nccl_comm_destroy(void* comm);
+
 /* Survivor rebalancing plan after an exit point: given every rank's
  * survivor count counts[0..world-1], the target is T = ceil(S / world), S = sum(counts).
  * Ranks with more than T survivors send their LAST (count - T) rows, in order, to the
@@ -273,6 +328,17 @@ dycl_status dycl_s2s_set_lm_head(dycl_s2s s, const uint16_t* w, const float* b);
  * plain argmax guard); tok = argmax (lowest index on ties); a sequence is done after it
  * emits EOS (EOS counted in its length) or after max_len steps; PAD fills the rest. */
 dycl_status dycl_s2s_set_loop_guard(dycl_s2s s, const float* len_table, float beta);
+/* Numerics (before finalize).  DYCL_PREC_BF16 (default): bf16 tensor-core operands, bf16
+ * q/k/v, K/V caches, attention outputs and FFN hidden, fp32 residual stream / LayerNorm /
+ * softmax / logits -- graded against the oracle's mirror mode.  DYCL_PREC_BF16X3_PARITY
+ * (SURVEY 8(c) "precision modes"): every bf16 tensor is kept as a split pair hi + lo (hi =
+ * bf16(v), lo = bf16(v - hi), ~16 significant bits) and every GEMM runs on the tensor cores over
+ * K-concatenated operands [A_hi | A_lo] x [W | W] -- the split-bf16 3-pass product, whose
+ * A_hi x W_lo term is identically zero because the weights are exact bf16 -- so products are
+ * fp32-accurate; graded against the oracle's exact (fp64) mode, where decisions must be
+ * bit-exact outside the 1e-3 band.  Twice the GEMM work and the bf16 bytes.  Errors:
+ * INVALID_ARG, STATE. */
+dycl_status dycl_s2s_set_precision(dycl_s2s s, int precision);
 dycl_status dycl_s2s_finalize(dycl_s2s s, int64_t max_batch);
 /* Device buffers: src int32 [batch][src_len]; tokens int32 [batch][max_len] (out);
  * lengths int32 [batch] (out); top1 fp32 [batch][max_len] (out, the chosen token's logit,

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "../../include/dycl.h"
+#include "comm.h"
 #include "kernels.h"
 
 namespace {
@@ -118,7 +119,7 @@ struct dycl_graph_s {
   cudaStream_t cap_stream = nullptr;
   struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
-    const void* key[3] = {};
+    const void* key[4] = {};
     int64_t batch = -1;
     int launches = 0;
     uint64_t used = 0;
@@ -144,18 +145,35 @@ struct dycl_graph_s {
   float* d_pred = nullptr;
   float* d_z = nullptr;
   float* d_gpool = nullptr;         // pooled features of wide heads [max_batch][max head C]
-  float* d_gap_part = nullptr;      // conv_gemm fused-GAP partials (sub-network outputs read by a head)
+  long long* d_gap_part = nullptr;  // conv_gemm fused-GAP partials (int64 fixed point) (sub-network outputs read by a head)
   float* d_gap_pooled = nullptr;    // their reduction [max_batch][C]
   float* d_pool32[NBUF32] = {};     // fused-GAP features per fp32 stream buffer [max_batch][<= 32] (fused blocks)
   float* d_in_stage = nullptr;      // dycl_run_host staging
   float* d_logit_stage = nullptr;
   int32_t* d_path_stage = nullptr;
+  float* d_margin_stage = nullptr;
   int launches_per_run = 0;
   // profiling
   bool profiling = false;
   std::vector<Launch> prof;
   size_t prof_used = 0;
   cudaStream_t prof_stream = nullptr;
+  // multi-GPU survivor rebalancing (dycl_set_comm / dycl_set_comm_local)
+  dycl::Transport* tr = nullptr;
+  int rb_policy = 0;                 // bit k: rebalance after exit k (-1: every exit)
+  // result space of a rebalancing run: rows [0, batch) are the rank's own samples, rows
+  // [batch, batch + ext) the samples other ranks handed over (returned to them at the end)
+  float* d_res_logits = nullptr;
+  int32_t* d_res_path = nullptr;
+  float* d_res_margin = nullptr;
+  long long* d_ext_gid = nullptr;
+  int* d_sent_orig = nullptr;        // result-space ids of the rows sent away, per level
+  int32_t* d_meta = nullptr;         // [rows][4] path, margin bits, global id lo / hi (send | recv)
+  float* d_ret_logits = nullptr;     // returned results of rows sent away
+  int32_t* d_ret_path = nullptr;
+  float* d_ret_margin = nullptr;
+  int64_t rb_rows = 0;               // capacity of the result space / sent tables (rows)
+  long long rb_sent = 0, rb_recv = 0;   // rows moved by the last run (dycl_rebalance_stats)
 };
 
 static thread_local std::string g_create_err;
@@ -393,6 +411,9 @@ struct Exec {
   int batch;
   float* out_logits;
   int32_t* out_path;
+  float* out_margin = nullptr;       // per-sample min |predicate - threshold| (or nullptr)
+  long long global_offset = 0;       // global index of row 0 (rebalanced rows carry their id)
+  int own = 0;                       // the rank's own rows (result space rows [0, own))
   int slot = 1;               // next free count slot
   int fused_launch = 0;       // fused-block launches so far in this run (DYCL_TS selection)
   int conv_launch = 0;        // conv launches so far in this run (DYCL_TS_CONV selection)
@@ -706,12 +727,13 @@ struct Exec {
     return DYCL_OK;
   }
 
-  dycl_status compact(const int* cnt, int mode, int32_t bit, int orig_cur, int* s_out) {
+  dycl_status compact(const int* cnt, int mode, int32_t bit, int orig_cur, int* s_out, bool pred, float thr) {
     *s_out = slot;
     if (slot + 2 > g->n_slots) return fail(g, DYCL_E_STATE, "count slots exhausted");
-    prof_begin(DYCL_K_COMPACT, cnt, 1.0 + 4 * 4, 0, 0);
+    prof_begin(DYCL_K_COMPACT, cnt, 1.0 + 4 * 4 + (pred && out_margin ? 12.0 : 0.0), 0, 0);
     cudaError_t e = dycl::launch_compact(g->d_flag, cnt, g->d_orig[orig_cur], g->d_list1, g->d_list0,
-                                         g->d_counts + slot, g->d_orig[orig_cur ^ 1], mode, out_path, bit, st);
+                                         g->d_counts + slot, g->d_orig[orig_cur ^ 1], mode, out_path, bit,
+                                         g->d_pred, thr, pred ? out_margin : nullptr, st);
     prof_end();
     slot += 2;
     if (e != cudaSuccess) return cuda_fail(g, e, "launch_compact");
@@ -761,13 +783,14 @@ struct Exec {
     dycl_status r;
     int orig_cur = 0;
     prof_begin(DYCL_K_INIT, nullptr, 0, 0, 12.0 * batch);
-    cudaError_t e = dycl::launch_init(g->d_counts, batch, g->d_orig[0], out_path, batch, st);
+    cudaError_t e = dycl::launch_init(g->d_counts, own, g->d_orig[0], out_path, out_margin, batch, st);
     prof_end();
     if (e != cudaSuccess) return cuda_fail(g, e, "launch_init");
     const Shape& in = g->input;
     prof_begin(DYCL_K_INPUT, nullptr, 0, 0, (double)batch * in.H * in.W * (4.0 * in.C + 2.0 * in.Cp()));
-    e = g->stem_s4d ? dycl::launch_cast_s4d(input, g->buf[0], batch, in.H, in.W, in.C, st)
-                    : dycl::launch_cast_pad(input, g->buf[0], batch, in.H * in.W, in.C, in.Cp(), st);
+    e = own == 0 ? cudaSuccess
+        : g->stem_s4d ? dycl::launch_cast_s4d(input, g->buf[0], own, in.H, in.W, in.C, st)
+                      : dycl::launch_cast_pad(input, g->buf[0], own, in.H * in.W, in.C, in.Cp(), st);
     prof_end();
     if (e != cudaSuccess) return cuda_fail(g, e, "launch_cast_pad");
     Tensor cur;
@@ -790,8 +813,9 @@ struct Exec {
         case N_EXIT: {
           if ((r = head(g->subnets[N.sn], cur, cnt, 0, N.thr))) return r;
           int s;
-          if ((r = compact(cnt, 0, 0, orig_cur, &s))) return r;
+          if ((r = compact(cnt, 0, 0, orig_cur, &s, true, N.thr))) return r;
           if ((r = scatter(g->d_list1, g->d_counts + s, orig_cur, N.ordinal))) return r;
+          const bool rebal = rebalance_here(N.ordinal);
           // survivors move on; their fp32 stream copy only if the next reader uses it (a
           // ResNet-50 stage starts with a projection block: its input is read as bf16 only)
           const bool next_seq = ni + 1 < g->nodes.size() && g->nodes[ni + 1].kind == N_SEQ;
@@ -801,7 +825,7 @@ struct Exec {
           // compaction's row list: then nothing moves at all (zero-copy exit)
           const bool next_fused = next_seq && keep32 && fp32_stream() && !g->no_fuse &&
                                   fusable(g->subnets[g->nodes[ni + 1].sn], 0);
-          if (next_fused && !g->no_zero_copy) {
+          if (next_fused && !g->no_zero_copy && !rebal) {
             in_list = g->d_list0;
             cnt = g->d_counts + s + 1;
             orig_cur ^= 1;
@@ -818,12 +842,13 @@ struct Exec {
           cur = nb;
           cnt = g->d_counts + s + 1;
           orig_cur ^= 1;
+          if (rebal && (r = rebalance(cur, g->d_counts + s + 1, N.in, orig_cur))) return r;
           break;
         }
         case N_GATE: {
           if ((r = head(g->subnets[N.sn], cur, cnt, 1, N.thr))) return r;
           int s;
-          if ((r = compact(cnt, 1, (int32_t)1 << N.ordinal, orig_cur, &s))) return r;
+          if ((r = compact(cnt, 1, (int32_t)1 << N.ordinal, orig_cur, &s, true, N.thr))) return r;
           const Subnet& T = g->subnets[N.then_sn];
           if (N.skip_mode == 0 && fp32_stream() && cur.f >= 0 && cur.b >= 0 && !g->no_fuse && !g->no_inplace &&
               T.layers.size() == 3 && fusable(T, 0)) {
@@ -931,12 +956,138 @@ struct Exec {
         case N_FINAL: {
           if ((r = head(g->subnets[N.sn], cur, cnt, 2, 0.f))) return r;
           int s;
-          if ((r = compact(cnt, 0, 0, orig_cur, &s))) return r;
+          if ((r = compact(cnt, 0, 0, orig_cur, &s, false, 0.f))) return r;
           const int32_t pv = g->n_exits > 0 ? g->n_exits : -1;
           if ((r = scatter(g->d_list1, g->d_counts + s, orig_cur, pv))) return r;
           break;
         }
       }
+    }
+    return return_results();
+  }
+
+  // ---------------------------------------------------------------- a9 rebalancing
+  struct Level {
+    std::vector<int> send, recv;     // rows to / from each rank
+    int ext0 = 0;                    // result-space id of the first row received at this level
+    long long sent0 = 0;             // offset of this level's rows in d_sent_orig / d_ret_*
+    int n_send = 0, n_recv = 0;
+    bool moved_any = false;          // some rank moved rows at this level (all ranks agree)
+  };
+  std::vector<Level> levels;
+  int ext_used = 0;
+  long long sent_used = 0;
+
+  bool rebalance_here(int exit_ordinal) const {
+    return g->tr && exit_ordinal < 31 && (g->rb_policy >> exit_ordinal) & 1;
+  }
+
+  // After an exit: the survivors sit dense in rows [0, s) of t.  All ranks agree on the counts
+  // (all-gather), compute the same deterministic plan (dycl_rebalance_plan), and exchange the
+  // surplus rows -- the LAST rows of a surplus rank, in order -- with their metadata; arrivals
+  // are appended after the local survivors and get result-space ids past the own rows.
+  dycl_status rebalance(Tensor t, int* cnt_slot, const Shape& sh, int orig_cur) {
+    dycl::Transport* T = g->tr;
+    const int W = T->world, me = T->rank;
+    std::vector<int> counts(W);
+    std::string err;
+    if (!T->allgather_int(cnt_slot, counts.data(), st, &err)) return fail(g, DYCL_E_NCCL, err);
+    Level L;
+    L.send.assign(W, 0);
+    L.recv.assign(W, 0);
+    int newc = 0;
+    if (dycl_rebalance_plan(counts.data(), W, me, L.send.data(), L.recv.data(), &newc) != DYCL_OK)
+      return fail(g, DYCL_E_INVALID_ARG, "rebalance plan");
+    long long moved = 0;
+    for (int r = 0; r < W; ++r) {
+      std::vector<int> sd(W), rc(W);
+      int nc = 0;
+      dycl_rebalance_plan(counts.data(), W, r, sd.data(), rc.data(), &nc);
+      for (int j = 0; j < W; ++j) moved += sd[j];
+    }
+    for (int j = 0; j < W; ++j) {
+      L.n_send += L.send[j];
+      L.n_recv += L.recv[j];
+    }
+    if (newc > g->max_batch) return fail(g, DYCL_E_SHAPE_MISMATCH, "rebalance: rows held exceed max_batch");
+    L.ext0 = own + ext_used;
+    L.sent0 = sent_used;
+    L.moved_any = moved > 0;
+    if (moved == 0) {                                // nobody moves: no exchange, no return
+      levels.push_back(L);
+      return DYCL_OK;
+    }
+    if (ext_used + L.n_recv > g->rb_rows - own || sent_used + L.n_send > g->rb_rows)
+      return fail(g, DYCL_E_STATE, "rebalance: result space exhausted");
+    const int s_own = counts[me], keep = s_own - L.n_send;
+    int32_t* meta_send = g->d_meta;
+    int32_t* meta_recv = g->d_meta + 4 * (size_t)g->max_batch;
+    int* orig = g->d_orig[orig_cur];
+    cudaError_t e = dycl::launch_rb_pack(orig, keep, L.n_send, out_path, out_margin, g->d_ext_gid, global_offset, own,
+                                         g->d_sent_orig + sent_used, meta_send, st);
+    if (e != cudaSuccess) return cuda_fail(g, e, "launch_rb_pack");
+    std::vector<dycl::Transport::Msg> sends, recvs;
+    const size_t rb = (size_t)sh.row_elems() * 2, rf = (size_t)sh.row_elems() * 4;
+    int so = keep, ro = s_own;                       // row cursors (destination / source rank ascending)
+    for (int j = 0; j < W; ++j) {
+      if (L.send[j]) {
+        if (t.b >= 0) sends.push_back({j, (char*)g->buf[t.b] + so * rb, L.send[j] * rb});
+        if (t.f >= 0) sends.push_back({j, (char*)g->buf32[t.f] + so * rf, L.send[j] * rf});
+        sends.push_back({j, meta_send + 4 * (size_t)(so - keep), (size_t)L.send[j] * 16});
+        so += L.send[j];
+      }
+      if (L.recv[j]) {
+        if (t.b >= 0) recvs.push_back({j, (char*)g->buf[t.b] + ro * rb, L.recv[j] * rb});
+        if (t.f >= 0) recvs.push_back({j, (char*)g->buf32[t.f] + ro * rf, L.recv[j] * rf});
+        recvs.push_back({j, meta_recv + 4 * (size_t)(ro - s_own), (size_t)L.recv[j] * 16});
+        ro += L.recv[j];
+      }
+    }
+    if (!T->exchange(sends, recvs, st, &err)) return fail(g, DYCL_E_NCCL, err);
+    e = dycl::launch_rb_unpack(orig, s_own, L.n_recv, L.ext0, own, meta_recv, out_path, out_margin, g->d_ext_gid, st);
+    if (e == cudaSuccess) e = dycl::launch_set_int(cnt_slot, newc, st);
+    if (e != cudaSuccess) return cuda_fail(g, e, "rebalance unpack");
+    ext_used += L.n_recv;
+    sent_used += L.n_send;
+    g->rb_sent += L.n_send;
+    g->rb_recv += L.n_recv;
+    if (newc > batch) batch = newc;                  // grid sizing for the rows now held
+    levels.push_back(L);
+    return DYCL_OK;
+  }
+
+  // End of run: results of rows computed away from home go back by the reverse plans, last
+  // level first (a row forwarded twice returns through its intermediate rank), and are
+  // scattered to their result-space id; own rows then reach the caller's buffers.
+  dycl_status return_results() {
+    if (!g->tr || levels.empty()) return DYCL_OK;
+    const int K = g->K, W = g->tr->world;
+    std::string err;
+    for (int li = (int)levels.size() - 1; li >= 0; --li) {
+      const Level& L = levels[li];
+      if (!L.moved_any) continue;                    // every rank knows every plan: all skip together
+      std::vector<dycl::Transport::Msg> sends, recvs;
+      int ro = L.ext0;
+      long long so = L.sent0;
+      for (int j = 0; j < W; ++j) {
+        if (L.recv[j]) {                             // results of rows received from j go back to j
+          sends.push_back({j, out_logits + (size_t)ro * K, (size_t)L.recv[j] * K * 4});
+          sends.push_back({j, out_path + ro, (size_t)L.recv[j] * 4});
+          sends.push_back({j, out_margin + ro, (size_t)L.recv[j] * 4});
+          ro += L.recv[j];
+        }
+        if (L.send[j]) {
+          const long long k = so - L.sent0;
+          recvs.push_back({j, g->d_ret_logits + (size_t)k * K, (size_t)L.send[j] * K * 4});
+          recvs.push_back({j, g->d_ret_path + k, (size_t)L.send[j] * 4});
+          recvs.push_back({j, g->d_ret_margin + k, (size_t)L.send[j] * 4});
+          so += L.send[j];
+        }
+      }
+      if (!g->tr->exchange(sends, recvs, st, &err)) return fail(g, DYCL_E_NCCL, err);
+      cudaError_t e = dycl::launch_rb_return(g->d_sent_orig + L.sent0, L.n_send, K, g->d_ret_logits, g->d_ret_path,
+                                             g->d_ret_margin, out_logits, out_path, out_margin, st);
+      if (e != cudaSuccess) return cuda_fail(g, e, "launch_rb_return");
     }
     return DYCL_OK;
   }
@@ -1016,7 +1167,18 @@ dycl_status dycl_graph_destroy(dycl_graph g) {
   cudaFree(g->d_in_stage);
   cudaFree(g->d_logit_stage);
   cudaFree(g->d_path_stage);
+  cudaFree(g->d_margin_stage);
   cudaFree(g->dbg_ts);
+  cudaFree(g->d_res_logits);
+  cudaFree(g->d_res_path);
+  cudaFree(g->d_res_margin);
+  cudaFree(g->d_ext_gid);
+  cudaFree(g->d_sent_orig);
+  cudaFree(g->d_meta);
+  cudaFree(g->d_ret_logits);
+  cudaFree(g->d_ret_path);
+  cudaFree(g->d_ret_margin);
+  delete g->tr;
   for (auto& e : g->graphs)
     if (e.exec) cudaGraphExecDestroy(e.exec);
   if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
@@ -1040,6 +1202,9 @@ const char* dycl_last_error(dycl_graph g) { return g ? g->err.c_str() : g_create
 dycl_status dycl_graph_set_precision(dycl_graph g, int precision) {
   if (!g) return DYCL_E_INVALID_ARG;
   if (g->finalized) return fail(g, DYCL_E_STATE, "graph already finalized");
+  if (precision == DYCL_PREC_BF16X3_PARITY)
+    return fail(g, DYCL_E_UNSUPPORTED, "BF16X3 parity mode is implemented for the generative graph (dycl_s2s); "
+                                       "image graphs meet decision parity in FP32_STREAM (DESIGN.md R13)");
   if (precision != DYCL_PREC_BF16 && precision != DYCL_PREC_FP32_STREAM)
     return fail(g, DYCL_E_INVALID_ARG, "unknown precision mode");
   g->precision = precision;
@@ -1356,7 +1521,7 @@ dycl_status dycl_finalize(dycl_graph g, int64_t max_batch) {
       pooled = std::max(pooled, (size_t)nb * L.out.C);
     }
     if (part && !getenv("DYCL_NO_CONV_GAP")) {
-      if (dycl_status s = dmalloc(g, &g->d_gap_part, part * 4)) return s;
+      if (dycl_status s = dmalloc(g, &g->d_gap_part, part * 8)) return s;
       if (dycl_status s = dmalloc(g, &g->d_gap_pooled, pooled * 4)) return s;
     }
   }
@@ -1365,25 +1530,48 @@ dycl_status dycl_finalize(dycl_graph g, int64_t max_batch) {
 }
 
 static dycl_status run_impl(dycl_graph g, const float* input, int64_t batch, float* logits, int32_t* path,
-                            int32_t* node_counts, cudaStream_t st) {
+                            int32_t* node_counts, cudaStream_t st, long long global_offset = 0,
+                            float* min_margin = nullptr) {
   if (!g->finalized) return fail(g, DYCL_E_STATE, "graph not finalized");
   if (batch < 0 || batch > g->max_batch) return fail(g, DYCL_E_SHAPE_MISMATCH, "batch > max_batch");
   if (batch > 0 && (!input || !logits || !path)) return fail(g, DYCL_E_INVALID_ARG, "null io pointer");
+  if (global_offset < 0) return fail(g, DYCL_E_INVALID_ARG, "negative global_offset");
   CK(cudaSetDevice(g->device));
   CK(cudaGetLastError());                      // surface async faults of earlier work
   g->prof_used = 0;
   g->prof_stream = st;
-  if (batch == 0) {
+  g->rb_sent = g->rb_recv = 0;
+  const bool rebal = g->tr && g->rb_policy != 0 && g->n_exits > 0;
+  if (rebal) {
+    // lock step with the other ranks (even with no rows of its own: it may receive some);
+    // results land in the library's result space first, then own rows go to the caller
+    Exec ex{g, st, (int)std::max<int64_t>(batch, 1), g->d_res_logits, g->d_res_path};
+    ex.out_margin = g->d_res_margin;
+    ex.global_offset = global_offset;
+    ex.own = (int)batch;
+    if (dycl_status s = ex.run(input)) return s;
+    g->launches_per_run = ex.nlaunch;
+    if (batch > 0) {
+      CK(cudaMemcpyAsync(logits, g->d_res_logits, (size_t)batch * g->K * 4, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(path, g->d_res_path, (size_t)batch * 4, cudaMemcpyDeviceToDevice, st));
+      if (min_margin)
+        CK(cudaMemcpyAsync(min_margin, g->d_res_margin, (size_t)batch * 4, cudaMemcpyDeviceToDevice, st));
+    }
+  } else if (batch == 0) {
     CK(cudaMemsetAsync(g->d_counts, 0, g->n_slots * sizeof(int), st));
   } else if (!g->use_graph || g->profiling || g->dbg_ts) {
     Exec ex{g, st, (int)batch, logits, path};
+    ex.out_margin = min_margin;
+    ex.own = (int)batch;
     if (dycl_status s = ex.run(input)) return s;
     g->launches_per_run = ex.nlaunch;
   } else {
-    const void* key[3] = {input, logits, path};
+    const void* key[4] = {input, logits, path, min_margin};
     dycl_graph_s::GraphEntry* ge = nullptr;
     for (auto& e : g->graphs)
-      if (e.exec && e.batch == batch && e.key[0] == key[0] && e.key[1] == key[1] && e.key[2] == key[2]) ge = &e;
+      if (e.exec && e.batch == batch && e.key[0] == key[0] && e.key[1] == key[1] && e.key[2] == key[2] &&
+          e.key[3] == key[3])
+        ge = &e;
     if (!ge) {
       ge = &g->graphs[0];                            // empty slot, else the least recently used
       for (auto& e : g->graphs)
@@ -1395,6 +1583,8 @@ static dycl_status run_impl(dycl_graph g, const float* input, int64_t batch, flo
       if (!g->cap_stream) CK(cudaStreamCreateWithFlags(&g->cap_stream, cudaStreamNonBlocking));
       CK(cudaStreamBeginCapture(g->cap_stream, cudaStreamCaptureModeThreadLocal));
       Exec ex{g, g->cap_stream, (int)batch, logits, path};
+      ex.out_margin = min_margin;
+      ex.own = (int)batch;
       const dycl_status r = ex.run(input);
       cudaGraph_t graph = nullptr;
       const cudaError_t ec = cudaStreamEndCapture(g->cap_stream, &graph);
@@ -1409,7 +1599,7 @@ static dycl_status run_impl(dycl_graph g, const float* input, int64_t batch, flo
         ge->exec = nullptr;
         return cuda_fail(g, ei, "graph instantiate");
       }
-      for (int i = 0; i < 3; ++i) ge->key[i] = key[i];
+      for (int i = 0; i < 4; ++i) ge->key[i] = key[i];
       ge->batch = batch;
       ge->launches = ex.nlaunch;
     }
@@ -1423,11 +1613,12 @@ static dycl_status run_impl(dycl_graph g, const float* input, int64_t batch, flo
 
 dycl_status dycl_run(dycl_graph g, const dycl_io* io, void* stream) {
   if (!g || !io) return DYCL_E_INVALID_ARG;
-  return run_impl(g, io->input, io->batch, io->logits, io->path, io->node_counts, (cudaStream_t)stream);
+  return run_impl(g, io->input, io->batch, io->logits, io->path, io->node_counts, (cudaStream_t)stream,
+                  io->global_offset, io->min_margin);
 }
 
-dycl_status dycl_run_host(dycl_graph g, const float* input_host, int64_t batch, float* logits_host,
-                          int32_t* path_host, void* stream) {
+static dycl_status run_host_impl(dycl_graph g, const float* input_host, int64_t batch, long long global_offset,
+                                 float* logits_host, int32_t* path_host, float* margin_host, void* stream) {
   if (!g) return DYCL_E_INVALID_ARG;
   if (!g->finalized) return fail(g, DYCL_E_STATE, "graph not finalized");
   if (batch < 0 || batch > g->max_batch) return fail(g, DYCL_E_SHAPE_MISMATCH, "batch > max_batch");
@@ -1439,6 +1630,7 @@ dycl_status dycl_run_host(dycl_graph g, const float* input_host, int64_t batch, 
     if (dycl_status s = dmalloc(g, &g->d_in_stage, in_elems * 4)) return s;
     if (dycl_status s = dmalloc(g, &g->d_logit_stage, (size_t)g->max_batch * g->K * 4)) return s;
     if (dycl_status s = dmalloc(g, &g->d_path_stage, (size_t)g->max_batch * 4)) return s;
+    if (dycl_status s = dmalloc(g, &g->d_margin_stage, (size_t)g->max_batch * 4)) return s;
   }
   const size_t row_in = (size_t)g->input.H * g->input.W * g->input.C;
   // Pipelined over sub-chunks in two staging slots: H2D of sub-chunk k+1 (copy stream) and
@@ -1462,9 +1654,13 @@ dycl_status dycl_run_host(dycl_graph g, const float* input_host, int64_t batch, 
   const int64_t nsc = batch <= 0 ? 0 : uneven ? 2 : (batch + sc - 1) / sc;
   if (nsc <= 1) {
     CK(cudaMemcpyAsync(g->d_in_stage, input_host, (size_t)batch * row_in * 4, cudaMemcpyHostToDevice, st));
-    if (dycl_status s = run_impl(g, g->d_in_stage, batch, g->d_logit_stage, g->d_path_stage, nullptr, st)) return s;
+    if (dycl_status s = run_impl(g, g->d_in_stage, batch, g->d_logit_stage, g->d_path_stage, nullptr, st,
+                                 global_offset, margin_host ? g->d_margin_stage : nullptr))
+      return s;
     CK(cudaMemcpyAsync(logits_host, g->d_logit_stage, (size_t)batch * g->K * 4, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(path_host, g->d_path_stage, (size_t)batch * 4, cudaMemcpyDeviceToHost, st));
+    if (margin_host)
+      CK(cudaMemcpyAsync(margin_host, g->d_margin_stage, (size_t)batch * 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return DYCL_OK;
   }
@@ -1485,23 +1681,35 @@ dycl_status dycl_run_host(dycl_graph g, const float* input_host, int64_t batch, 
     float* din = g->d_in_stage + off * row_in;
     float* dz = g->d_logit_stage + off * g->K;
     int32_t* dp = g->d_path_stage + off;
+    float* dm = margin_host ? g->d_margin_stage + off : nullptr;
     if (k >= 2) CK(cudaStreamWaitEvent(g->h2d_stream, g->ev_run[slot], 0));     // run k-2 read this slot
     CK(cudaMemcpyAsync(din, input_host + (size_t)r0 * row_in, (size_t)rows * row_in * 4, cudaMemcpyHostToDevice,
                        g->h2d_stream));
     CK(cudaEventRecord(g->ev_h2d[slot], g->h2d_stream));
     CK(cudaStreamWaitEvent(st, g->ev_h2d[slot], 0));
     if (k >= 2) CK(cudaStreamWaitEvent(st, g->ev_d2h[slot], 0));                // D2H k-2 read this slot
-    if (dycl_status s = run_impl(g, din, rows, dz, dp, nullptr, st)) return s;
+    if (dycl_status s = run_impl(g, din, rows, dz, dp, nullptr, st, global_offset + r0, dm)) return s;
     CK(cudaEventRecord(g->ev_run[slot], st));
     CK(cudaStreamWaitEvent(g->d2h_stream, g->ev_run[slot], 0));
     CK(cudaMemcpyAsync(logits_host + (size_t)r0 * g->K, dz, (size_t)rows * g->K * 4, cudaMemcpyDeviceToHost,
                        g->d2h_stream));
     CK(cudaMemcpyAsync(path_host + r0, dp, (size_t)rows * 4, cudaMemcpyDeviceToHost, g->d2h_stream));
+    if (margin_host) CK(cudaMemcpyAsync(margin_host + r0, dm, (size_t)rows * 4, cudaMemcpyDeviceToHost, g->d2h_stream));
     CK(cudaEventRecord(g->ev_d2h[slot], g->d2h_stream));
   }
   CK(cudaStreamSynchronize(g->d2h_stream));
   CK(cudaStreamSynchronize(st));
   return DYCL_OK;
+}
+
+dycl_status dycl_run_host(dycl_graph g, const float* input_host, int64_t batch, float* logits_host,
+                          int32_t* path_host, void* stream) {
+  return run_host_impl(g, input_host, batch, 0, logits_host, path_host, nullptr, stream);
+}
+
+dycl_status dycl_run_host_ex(dycl_graph g, const float* input_host, int64_t batch, int64_t global_offset,
+                             float* logits_host, int32_t* path_host, float* min_margin_host, void* stream) {
+  return run_host_impl(g, input_host, batch, global_offset, logits_host, path_host, min_margin_host, stream);
 }
 
 dycl_status dycl_num_count_slots(dycl_graph g, int32_t* out) {
@@ -1597,6 +1805,97 @@ dycl_status dycl_debug_conv2d(dycl_graph g, int64_t n, int H, int W, int C, cons
   cudaFree(dw);
   cudaFree(db);
   if (e != cudaSuccess) return cuda_fail(g, e, "debug_conv2d");
+  return DYCL_OK;
+}
+
+// Result space + exchange staging for rebalancing runs (allocated when a transport is set).
+static dycl_status alloc_rebalance(dycl_graph g) {
+  const int levels = std::max(1, std::min(g->n_exits, 31));
+  const int64_t rows = (int64_t)g->max_batch * (1 + levels);
+  const size_t K = (size_t)std::max(g->K, 1), mb = (size_t)g->max_batch;
+  dycl_status s;
+  if ((s = dmalloc(g, &g->d_res_logits, (size_t)rows * K * 4)) || (s = dmalloc(g, &g->d_res_path, rows * 4)) ||
+      (s = dmalloc(g, &g->d_res_margin, rows * 4)) || (s = dmalloc(g, &g->d_ext_gid, rows * 8)) ||
+      (s = dmalloc(g, &g->d_sent_orig, rows * 4)) || (s = dmalloc(g, &g->d_meta, 2 * mb * 16)) ||
+      (s = dmalloc(g, &g->d_ret_logits, (size_t)rows * K * 4)) || (s = dmalloc(g, &g->d_ret_path, rows * 4)) ||
+      (s = dmalloc(g, &g->d_ret_margin, rows * 4)))
+    return s;
+  g->rb_rows = rows;
+  return DYCL_OK;
+}
+
+static dycl_status set_transport(dycl_graph g, dycl::Transport* t, int policy) {
+  CK(cudaSetDevice(g->device));
+  delete g->tr;
+  g->tr = t;
+  g->rb_policy = policy;
+  if (t && policy != 0 && !g->d_res_logits) return alloc_rebalance(g);
+  return DYCL_OK;
+}
+
+dycl_status dycl_set_comm(dycl_graph g, void* nccl_comm, int rank, int world, int rebalance_policy) {
+  if (!g) return DYCL_E_INVALID_ARG;
+  if (!g->finalized) return fail(g, DYCL_E_STATE, "dycl_set_comm: finalize the graph first");
+  if (world < 1 || rank < 0 || rank >= world || (world > 1 && !nccl_comm))
+    return fail(g, DYCL_E_INVALID_ARG, "dycl_set_comm: bad rank / world / communicator");
+  if (world == 1 && !nccl_comm) return set_transport(g, nullptr, 0);
+  std::string err;
+  dycl::Transport* t = dycl::make_nccl_transport(nccl_comm, rank, world, &err);
+  if (!t) return fail(g, DYCL_E_NCCL, err);
+  return set_transport(g, t, rebalance_policy);
+}
+
+struct dycl_local_group_s {
+  dycl::LocalGroup* g;
+};
+
+dycl_status dycl_local_group_create(int world, dycl_local_group* out) {
+  if (world < 1 || !out) return fail(nullptr, DYCL_E_INVALID_ARG, "bad world");
+  *out = new (std::nothrow) dycl_local_group_s{dycl::local_group_create(world)};
+  return *out ? DYCL_OK : DYCL_E_OOM;
+}
+
+dycl_status dycl_local_group_destroy(dycl_local_group grp) {
+  if (grp) {
+    dycl::local_group_destroy(grp->g);
+    delete grp;
+  }
+  return DYCL_OK;
+}
+
+dycl_status dycl_set_comm_local(dycl_graph g, dycl_local_group grp, int rank, int rebalance_policy) {
+  if (!g || !grp) return DYCL_E_INVALID_ARG;
+  if (!g->finalized) return fail(g, DYCL_E_STATE, "dycl_set_comm_local: finalize the graph first");
+  if (rank < 0 || rank >= dycl::local_group_world(grp->g)) return fail(g, DYCL_E_INVALID_ARG, "bad rank");
+  return set_transport(g, dycl::make_local_transport(grp->g, rank), rebalance_policy);
+}
+
+dycl_status dycl_rebalance_stats(dycl_graph g, int64_t* rows_sent, int64_t* rows_received) {
+  if (!g || !rows_sent || !rows_received) return DYCL_E_INVALID_ARG;
+  *rows_sent = g->rb_sent;
+  *rows_received = g->rb_recv;
+  return DYCL_OK;
+}
+
+dycl_status dycl_nccl_get_unique_id(uint8_t out[128]) {
+  if (!out) return fail(nullptr, DYCL_E_INVALID_ARG, "null");
+  std::string err;
+  if (!dycl::nccl_get_unique_id(out, &err)) return fail(nullptr, DYCL_E_NCCL, err);
+  return DYCL_OK;
+}
+
+dycl_status dycl_nccl_comm_init_rank(const uint8_t id[128], int rank, int world, int cuda_device, void** comm) {
+  if (!id || !comm || world < 1 || rank < 0 || rank >= world) return fail(nullptr, DYCL_E_INVALID_ARG, "bad argument");
+  if (cudaSetDevice(cuda_device) != cudaSuccess) return fail(nullptr, DYCL_E_CUDA, "cudaSetDevice");
+  std::string err;
+  if (!dycl::nccl_comm_init_rank(id, rank, world, comm, &err)) return fail(nullptr, DYCL_E_NCCL, err);
+  return DYCL_OK;
+}
+
+dycl_status dycl_nccl_comm_destroy(void* comm) {
+  if (!comm) return DYCL_OK;
+  std::string err;
+  if (!dycl::nccl_comm_destroy(comm, &err)) return fail(nullptr, DYCL_E_NCCL, err);
   return DYCL_OK;
 }
 

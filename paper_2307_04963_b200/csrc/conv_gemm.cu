@@ -479,13 +479,14 @@ __global__ void __launch_bounds__(THREADS, 1)
             const long long ra = m0 + 32 * q;                  // first row of this quarter
             const long long na = ra / HWo;
             const long long rb = (na + 1) * HWo;              // first row of the next sample
-            float s0 = 0.f, s1 = 0.f;
+            long long s0 = 0, s1 = 0;                         // fixed point x 2^32 (kernels.h)
 #pragma unroll 8
             for (int i = 0; i < 32; ++i) {
               const long long mm = ra + i;
               if (mm >= M) break;
               const float v = *reinterpret_cast<const float*>(eO32 + sw128(32 * q + i, cc >> 2) + (cc & 3) * 4);
-              if (mm < rb) s0 += v; else s1 += v;
+              const long long iv = __double2ll_rn((double)v * 4294967296.0);
+              if (mm < rb) s0 += iv; else s1 += iv;
             }
             if (ra < M) {
               const size_t pbase = (size_t)(ra >> 5) * 2 * a.Cout + col0 + c0 + cc;

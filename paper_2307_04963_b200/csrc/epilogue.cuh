@@ -102,8 +102,25 @@ __device__ __forceinline__ void conv_finish16(const ConvArgs& a, int n, int ho, 
 #pragma unroll
     for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.0f);
   }
+  if (a.split && a.y) {                 // dense split pair: hi at [row][o], lo at [row][Cout + o]
+    uint16_t* yr = a.y + (size_t)n * 2 * a.Cout + o0;
 #pragma unroll
-  for (int h = 0; h < 2 && a.y; ++h) {
+    for (int h = 0; h < 2; ++h) {
+      uint4 hi, lo;
+      uint32_t* hp = &hi.x;
+      uint32_t* lp = &lo.x;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float v0 = f[8 * h + 2 * j], v1 = f[8 * h + 2 * j + 1];
+        hp[j] = pack_bf16x2_rn(v0, v1);
+        lp[j] = pack_bf16x2_rn(v0 - __uint_as_float(hp[j] << 16), v1 - __uint_as_float(hp[j] & 0xFFFF0000u));
+      }
+      *reinterpret_cast<uint4*>(yr + 8 * h) = hi;
+      *reinterpret_cast<uint4*>(yr + a.Cout + 8 * h) = lo;
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < 2 && a.y && !a.split; ++h) {
     uint4 o;
     o.x = pack_bf16x2_rn(f[8 * h + 0], f[8 * h + 1]);
     o.y = pack_bf16x2_rn(f[8 * h + 2], f[8 * h + 3]);

@@ -61,12 +61,13 @@ __global__ void k_cast_pad(const float* __restrict__ in, uint16_t* __restrict__ 
   }
 }
 
-__global__ void k_init(int* counts, int n, int* orig, int32_t* path, int nmax) {
+__global__ void k_init(int* counts, int n, int* orig, int32_t* path, float* margin, int nmax) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0) counts[0] = n;
   if (i < n) {
     orig[i] = i;
     if (path) path[i] = 0;
+    if (margin) margin[i] = __int_as_float(0x7f800000);   // +inf: no predicate evaluated yet
   }
 }
 
@@ -300,7 +301,8 @@ constexpr int CMP_THREADS = 1024;
 __global__ void __launch_bounds__(CMP_THREADS) k_compact(const uint8_t* __restrict__ flag, const int* n_live,
                                                          const int* __restrict__ orig, int* list1, int* list0,
                                                          int* counts_out, int* orig_next, int mode, int32_t* path,
-                                                         int32_t path_bit) {
+                                                         int32_t path_bit, const float* __restrict__ pred, float thr,
+                                                         float* margin) {
   __shared__ int wsum[CMP_THREADS / 32];
   __shared__ int total1_s;
   ptx::pdl_wait();
@@ -354,6 +356,7 @@ __global__ void __launch_bounds__(CMP_THREADS) k_compact(const uint8_t* __restri
     for (int k = 0; k < CMP_IPT; ++k) {
       if (b + k >= e) break;
       const int i = b + k, oi = orr[k];
+      if (margin) margin[oi] = fminf(margin[oi], fabsf(pred[i] - thr));   // per-sample min |pred - thr|
       if (fr[k]) {
         list1[o1] = i;
         if (mode == 1) {
@@ -370,6 +373,7 @@ __global__ void __launch_bounds__(CMP_THREADS) k_compact(const uint8_t* __restri
   }
   for (int i = fast ? e : b; i < e; ++i) {
     const int oi = orig[i];
+    if (margin) margin[oi] = fminf(margin[oi], fabsf(pred[i] - thr));
     if (flag[i]) {
       list1[o1] = i;
       if (mode == 1) {
@@ -641,26 +645,26 @@ __global__ void k_cast_s4d(const float* __restrict__ in, uint16_t* __restrict__ 
   }
 }
 
-__global__ void k_gap_reduce(const float* __restrict__ part, float* __restrict__ pooled, const int* n_live, int HW,
-                             int C) {
+__global__ void k_gap_reduce(const long long* __restrict__ part, float* __restrict__ pooled, const int* n_live,
+                             int HW, int C) {
   const int n_rows = *n_live;
   const int64_t total = (int64_t)n_rows * C;
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total; u += (int64_t)gridDim.x * blockDim.x) {
     const int64_t n = u / C;
     const int c = (int)(u - n * C);
     const int64_t r0 = n * HW, r1 = r0 + HW - 1;
-    float sum = 0.f;
+    long long sum = 0;                               // exact: order and grouping free
     for (int64_t rg = r0 >> 5; rg <= (r1 >> 5); ++rg) {
       const int slot = (rg << 5) < r0 ? 1 : 0;        // group starts in the previous sample
       sum += part[(rg * 2 + slot) * C + c];
     }
-    pooled[n * C + c] = sum * (1.0f / HW);
+    pooled[n * C + c] = (float)((double)sum * (1.0 / 4294967296.0) / (double)HW);
   }
 }
 
 }  // namespace
 
-cudaError_t launch_gap_reduce(const float* gap_part, float* pooled, const int* n_live, int max_rows, int HW, int C,
+cudaError_t launch_gap_reduce(const long long* gap_part, float* pooled, const int* n_live, int max_rows, int HW, int C,
                               cudaStream_t s) {
   int64_t blocks = ((int64_t)max_rows * C + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
@@ -707,9 +711,9 @@ cudaError_t launch_cast_pad(const float* in, uint16_t* out, int64_t n, int hw, i
   return cudaGetLastError();
 }
 
-cudaError_t launch_init(int* counts, int n, int* orig, int32_t* path, int nmax, cudaStream_t s) {
+cudaError_t launch_init(int* counts, int n, int* orig, int32_t* path, float* margin, int nmax, cudaStream_t s) {
   const int blocks = (n + 255) / 256 > 0 ? (n + 255) / 256 : 1;
-  k_init<<<blocks, 256, 0, s>>>(counts, n, orig, path, nmax);
+  k_init<<<blocks, 256, 0, s>>>(counts, n, orig, path, margin, nmax);
   return cudaGetLastError();
 }
 
@@ -761,9 +765,9 @@ cudaError_t launch_head(const HeadArgs& a, int max_rows, cudaStream_t s) {
 
 cudaError_t launch_compact(const uint8_t* flag, const int* n_live, const int* orig, int* list1, int* list0,
                            int* counts_out, int* orig_next, int mode, int32_t* path, int32_t path_bit,
-                           cudaStream_t s) {
+                           const float* pred, float thr, float* margin, cudaStream_t s) {
   return launch_k(k_compact, dim3(1), dim3(CMP_THREADS), 0, s, flag, n_live, orig, list1, list0, counts_out, orig_next,
-                  mode, path, path_bit);
+                  mode, path, path_bit, pred, thr, margin);
 }
 
 cudaError_t launch_scatter(const float* z, int K, const int* list, const int* count, const int* orig,
@@ -781,6 +785,81 @@ cudaError_t launch_gather(const GatherArgs& a, int max_rows, int num_sms, cudaSt
   if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
   if (blocks < 1) blocks = 1;
   k_gather<<<(int)blocks, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------ a9 survivor rebalancing
+// Rows [first, first + n) of the dense survivor tensor leave this rank: record their row ids
+// in the run's result space (orig) and their metadata (path word, min margin, global id).
+__global__ void k_rb_pack(const int* __restrict__ orig, int first, int n, const int32_t* __restrict__ res_path,
+                          const float* __restrict__ res_margin, const long long* __restrict__ ext_gid,
+                          long long gid_base, int batch, int* sent_orig, int32_t* meta) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const int o = orig[first + j];
+    sent_orig[j] = o;
+    const long long gid = o < batch ? gid_base + o : ext_gid[o - batch];
+    meta[4 * j + 0] = res_path[o];
+    meta[4 * j + 1] = res_margin ? __float_as_int(res_margin[o]) : 0x7f800000;
+    meta[4 * j + 2] = (int32_t)(gid & 0xffffffffll);
+    meta[4 * j + 3] = (int32_t)(gid >> 32);
+  }
+}
+// Rows received from peers were appended at rows [first, first + n): they get result-space
+// ids ext0 + j (past the rank's own rows) and their path word / margin / global id.
+__global__ void k_rb_unpack(int* orig, int first, int n, int ext0, int batch, const int32_t* __restrict__ meta,
+                            int32_t* res_path, float* res_margin, long long* ext_gid) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const int o = ext0 + j;
+    orig[first + j] = o;
+    res_path[o] = meta[4 * j + 0];
+    if (res_margin) res_margin[o] = __int_as_float(meta[4 * j + 1]);
+    ext_gid[o - batch] = (long long)(uint32_t)meta[4 * j + 2] | ((long long)meta[4 * j + 3] << 32);
+  }
+}
+// Results of the rows this rank sent, returned by the reverse plan, scattered home by id.
+__global__ void k_rb_return(const int* __restrict__ sent_orig, int n, int K, const float* __restrict__ ret_logits,
+                            const int32_t* __restrict__ ret_path, const float* __restrict__ ret_margin,
+                            float* res_logits, int32_t* res_path, float* res_margin) {
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  for (int j = blockIdx.x * wpb + (threadIdx.x >> 5); j < n; j += gridDim.x * wpb) {
+    const int o = sent_orig[j];
+    for (int c = lane; c < K; c += 32) res_logits[(size_t)o * K + c] = ret_logits[(size_t)j * K + c];
+    if (lane == 0) {
+      res_path[o] = ret_path[j];
+      if (res_margin) res_margin[o] = ret_margin[j];
+    }
+  }
+}
+__global__ void k_set_int(int* p, int v) { *p = v; }
+
+cudaError_t launch_rb_pack(const int* orig, int first, int n, const int32_t* res_path, const float* res_margin,
+                           const long long* ext_gid, long long gid_base, int batch, int* sent_orig, int32_t* meta,
+                           cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  k_rb_pack<<<(n + 255) / 256 < 148 ? (n + 255) / 256 : 148, 256, 0, s>>>(orig, first, n, res_path, res_margin,
+                                                                          ext_gid, gid_base, batch, sent_orig, meta);
+  return cudaGetLastError();
+}
+cudaError_t launch_rb_unpack(int* orig, int first, int n, int ext0, int batch, const int32_t* meta,
+                             int32_t* res_path, float* res_margin, long long* ext_gid, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  k_rb_unpack<<<(n + 255) / 256 < 148 ? (n + 255) / 256 : 148, 256, 0, s>>>(orig, first, n, ext0, batch, meta,
+                                                                            res_path, res_margin, ext_gid);
+  return cudaGetLastError();
+}
+cudaError_t launch_rb_return(const int* sent_orig, int n, int K, const float* ret_logits, const int32_t* ret_path,
+                             const float* ret_margin, float* res_logits, int32_t* res_path, float* res_margin,
+                             cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  int blocks = (n + 7) / 8;
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  k_rb_return<<<blocks, 256, 0, s>>>(sent_orig, n, K, ret_logits, ret_path, ret_margin, res_logits, res_path,
+                                     res_margin);
+  return cudaGetLastError();
+}
+cudaError_t launch_set_int(int* p, int v, cudaStream_t s) {
+  k_set_int<<<1, 1, 0, s>>>(p, v);
   return cudaGetLastError();
 }
 

@@ -41,10 +41,15 @@ struct ConvArgs {
   // rows_out[i] -- the in-place form of a gate's then-branch; nullptr = dense order
   const int* rows_in = nullptr;
   const int* rows_out = nullptr;
-  // conv_gemm only (staged epilogue): fused GAP partials, fp32 [ceil(M/32)][2][Cout] -- per
+  // conv_gemm only (staged epilogue): fused GAP partials [ceil(M/32)][2][Cout] -- per
   // 32-row group of the flat output, the column sums of y for the group's first sample (slot 0)
   // and, when the group straddles a sample boundary, the second (slot 1); see launch_gap_reduce
-  float* gap_part = nullptr;
+  // int64 fixed point (value x 2^32, llrint): integer sums are exact, so the pooled features do
+  // not depend on where a sample's rows fall in the 32-row groups (batch-position independence)
+  long long* gap_part = nullptr;
+  // dense rows only (Ho = Wo = 1): write y as a split pair [hi | lo] per row (row stride 2*Cout,
+  // hi = bf16(v), lo = bf16(v - hi)) -- the operand format of the BF16X3 parity mode
+  int split = 0;
   long long* ts = nullptr;   // development: conv_gemm phase timestamps (DYCL_TS_CONV)
   int dbg = 0;           // bit5 (32): row-tap mode opt-in; experiments only (results invalid): bit0 skip
                          // epilogue math/stores, bit1 skip MMAs, bit2 skip A loads, bit3 no residual prefetch.
@@ -122,7 +127,7 @@ cudaError_t launch_cast_pad(const float* in, uint16_t* out, int64_t n, int hw, i
 
 // pooled[n][c] = (sum over the 32-row groups of sample n of gap_part[group][slot][c]) / HW,
 // fixed order (the second half of conv_gemm's fused GAP)
-cudaError_t launch_gap_reduce(const float* gap_part, float* pooled, const int* n_live, int max_rows, int HW, int C,
+cudaError_t launch_gap_reduce(const long long* gap_part, float* pooled, const int* n_live, int max_rows, int HW, int C,
                               cudaStream_t s);
 
 // a0 for a space-to-depth stem: fp32 NHWC [n][H][W][c] -> bf16 [n][H/4][W/4][64], channel
@@ -130,7 +135,18 @@ cudaError_t launch_gap_reduce(const float* gap_part, float* pooled, const int* n
 cudaError_t launch_cast_s4d(const float* in, uint16_t* out, int64_t n, int H, int W, int c, cudaStream_t s);
 
 // Run-start init: counts[0] = n ; orig[i] = i ; path[i] = 0.
-cudaError_t launch_init(int* counts, int n, int* orig, int32_t* path, int nmax, cudaStream_t s);
+cudaError_t launch_init(int* counts, int n, int* orig, int32_t* path, float* margin, int nmax, cudaStream_t s);
+// a9 survivor rebalancing (hostmod.cu): pack the metadata of rows leaving the rank, unpack the
+// rows that arrived, scatter returned results home by id, set a device count
+cudaError_t launch_rb_pack(const int* orig, int first, int n, const int32_t* res_path, const float* res_margin,
+                           const long long* ext_gid, long long gid_base, int batch, int* sent_orig, int32_t* meta,
+                           cudaStream_t s);
+cudaError_t launch_rb_unpack(int* orig, int first, int n, int ext0, int batch, const int32_t* meta,
+                             int32_t* res_path, float* res_margin, long long* ext_gid, cudaStream_t s);
+cudaError_t launch_rb_return(const int* sent_orig, int n, int K, const float* ret_logits, const int32_t* ret_path,
+                             const float* ret_margin, float* res_logits, int32_t* res_path, float* res_margin,
+                             cudaStream_t s);
+cudaError_t launch_set_int(int* p, int v, cudaStream_t s);
 
 // GAP + FC head + predicate, one CTA per live sample.
 //   kind 0 = exit (flag = max softmax >= thr), 1 = gate (flag = sigmoid(z0) > thr), 2 = final (flag = 1)
@@ -160,9 +176,12 @@ cudaError_t launch_head(const HeadArgs& a, int max_rows, cudaStream_t s);
 //   orig_next = [orig[list0...]]  (mode 0: survivors continue; exit)
 //             = [orig[list1...], orig[list0...]]  (mode 1: gate; then-rows first)
 //   mode 1 also ORs path_bit into path[orig[i]] for flag==1 rows.
+//   margin (optional): margin[orig[i]] = min(margin[orig[i]], |pred[i] - thr|), the per-sample
+//   distance of its predicates from their thresholds along its path (band reporting, R12).
 cudaError_t launch_compact(const uint8_t* flag, const int* n_live, const int* orig,
                            int* list1, int* list0, int* counts_out, int* orig_next,
-                           int mode, int32_t* path, int32_t path_bit, cudaStream_t s);
+                           int mode, int32_t* path, int32_t path_bit, const float* pred, float thr, float* margin,
+                           cudaStream_t s);
 
 // out_logits[orig[list[j]]] = z[list[j]], out_path[orig[list[j]]] = path_val (if path_val >= 0)
 // for j < *count.

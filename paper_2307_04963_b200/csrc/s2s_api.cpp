@@ -56,6 +56,10 @@ struct dycl_s2s_s {
   bool use_graph = true;             // DYCL_S2S_GRAPH=0 disables
   bool pdl = true;                   // programmatic dependent launch in the run (DYCL_S2S_PDL=0 disables)
   int gemm_path = 0;                 // 0: k_gemm_tma, 1: k_conv_gemm (DYCL_S2S_GEMM=1; measured equal or slower)
+  // DYCL_PREC_BF16X3_PARITY: every bf16 tensor is a split pair [hi | lo] and every GEMM runs
+  // on K-concatenated operands [A_hi | A_lo] x [W | W] (weights are exact bf16, so the
+  // W_lo terms of the 3-pass product vanish): fp32-accurate products on the tensor cores
+  int pair = 0;
   // per-launch profiling (graph off while enabled)
   struct Rec {
     int kind;
@@ -163,6 +167,10 @@ struct S2SExec {
   cudaError_t gemm(const uint16_t* x, int K, const uint16_t* w, const float* b, int N, const float* res32,
                    uint16_t* yb, float* y32, int relu, const int* cnt, int n_static, int max_rows) {
     dycl::ConvArgs a{};
+    if (s->pair) {                     // [A_hi | A_lo] x [W | W], bf16 outputs written as pairs
+      K *= 2;
+      a.split = yb != nullptr;
+    }
     a.x = x; a.w = w; a.bias = b; a.res32 = res32; a.res_mode = res32 ? 1 : 0;
     a.y = yb; a.y32 = y32; a.n_live = cnt; a.n_static = n_static;
     a.H = a.W = a.Ho = a.Wo = 1; a.C = K; a.Cout = N; a.ksz = 1; a.stride = 1; a.pad = 0;
@@ -178,6 +186,7 @@ struct S2SExec {
   }
   cudaError_t ln(const float* in, const float* g, const float* b, const int* cnt, int n_static, int max_rows) {
     dycl::S2SLnArgs a{in, g, b, s->x32, s->xb, cnt, n_static, s->c.d_model, 1e-5f};
+    a.pair = s->pair;
     ++n;
     const double d = s->c.d_model;
     pb(DYCL_K_LN, cnt, n_static, 4.0 * d + 6.0 * d, 8.0 * d, 8.0 * d);
@@ -205,6 +214,7 @@ struct S2SExec {
     ++n;
     // ---------------- encoder sub-network (once), rows = B*S tokens
     dycl::S2SEmbedArgs ea{s->src_emb, src, nullptr, nullptr, s->x32, s->xb, nullptr, R, d, S, 0};
+    ea.pair = s->pair;
     pb(DYCL_K_EMBED, nullptr, R, 4.0 + 2.0 * d + 6.0 * d, 0, 0);
     E(dycl::launch_embed(ea, R, st));
     pe();
@@ -213,6 +223,7 @@ struct S2SExec {
       E(gemm(s->xb, d, L.wqkv, L.bqkv, 3 * d, nullptr, s->qkv, nullptr, 0, nullptr, R, R));
       dycl::S2SAttnArgs aa{};
       aa.qkv = s->qkv; aa.out = s->att; aa.n_static = B; aa.d = d; aa.heads = c.heads; aa.S = S;
+      aa.pair = s->pair;
       pb(DYCL_K_ATTN, nullptr, B, (double)S * (3.0 * d * 2 + 2.0 * d), 4.0 * S * S * d, 0);
       E(dycl::launch_attn_encoder(aa, B, st));
       pe();
@@ -232,6 +243,7 @@ struct S2SExec {
     for (int t = 0; t < c.max_len; ++t) {
       const int32_t* slot = s->active[cur];
       dycl::S2SEmbedArgs de{s->tgt_emb, nullptr, slot, s->cur_tok, s->x32, s->xb, cnt, 0, d, S, t};
+      de.pair = s->pair;
       pb(DYCL_K_EMBED, cnt, 0, 8.0 + 2.0 * d + 6.0 * d, 0, 0);
       E(dycl::launch_embed(de, B, st));
       pe();
@@ -240,7 +252,8 @@ struct S2SExec {
         const DevLayer& L = s->dec[l];
         E(gemm(s->xb, d, L.wqkv, L.bqkv, 3 * d, nullptr, s->qkv, nullptr, 0, cnt, 0, B));
         dycl::S2SAttnArgs sa{};
-        sa.qkv = s->qkv; sa.q = s->qkv; sa.q_stride = 3 * d; sa.kv = nullptr; sa.cache = s->cache[l];
+        sa.qkv = s->qkv; sa.q = s->qkv; sa.q_stride = (s->pair ? 6 : 3) * d; sa.kv = nullptr; sa.cache = s->cache[l];
+        sa.pair = s->pair; sa.q_lo = 3 * d;
         sa.out = s->att; sa.slot = slot; sa.n_live = cnt; sa.d = d; sa.heads = c.heads; sa.S = S;
         sa.max_len = c.max_len; sa.t = t;
         pb(DYCL_K_ATTN, cnt, 0, (t + 1.0) * 2 * d * 2 + 3.0 * d * 2 + 2.0 * d * 2 + 2.0 * d * 2, 4.0 * (t + 1) * d, 0);
@@ -251,7 +264,8 @@ struct S2SExec {
         E(ln(s->pre, L.lsg, L.lsb, cnt, 0, B));
         E(gemm(s->xb, d, L.wq2, L.bq2, d, nullptr, s->att, nullptr, 0, cnt, 0, B));
         dycl::S2SAttnArgs ca{};
-        ca.q = s->att; ca.q_stride = d; ca.kv = s->cross[l]; ca.out = s->qkv;  // reuse qkv as scratch
+        ca.q = s->att; ca.q_stride = (s->pair ? 2 : 1) * d; ca.kv = s->cross[l]; ca.out = s->qkv;  // reuse qkv as scratch
+        ca.pair = s->pair; ca.q_lo = d;
         ca.slot = slot; ca.n_live = cnt; ca.d = d; ca.heads = c.heads; ca.S = S; ca.max_len = c.max_len; ca.t = t;
         pb(DYCL_K_ATTN, cnt, 0, (double)S * 2 * d * 2 + 2.0 * d * 2 + 2.0 * d * 2, 4.0 * S * d, 0);
         E(dycl::launch_attn_decoder(ca, B, st));
@@ -274,7 +288,7 @@ struct S2SExec {
       int* out_counts = s->counts + 1 + 2 * t;
       pb(DYCL_K_COMPACT, cnt, 0, 1.0 + 12.0, 0, 0);
       E(dycl::launch_compact(s->flag, cnt, slot, s->list1, s->list0, out_counts, s->active[cur ^ 1], 0,
-                             nullptr, 0, st));
+                             nullptr, 0, nullptr, 0.f, nullptr, st));
       pe();
       ++n;
       cnt = out_counts + 1;
@@ -371,6 +385,15 @@ dycl_status dycl_s2s_set_loop_guard(dycl_s2s s, const float* len_table, float be
   return upload(s, &s->len_table, len_table, (size_t)s->c.vocab);
 }
 
+dycl_status dycl_s2s_set_precision(dycl_s2s s, int precision) {
+  if (!s) return DYCL_E_INVALID_ARG;
+  if (s->finalized) return sfail(s, DYCL_E_STATE, "already finalized");
+  if (precision != DYCL_PREC_BF16 && precision != DYCL_PREC_BF16X3_PARITY)
+    return sfail(s, DYCL_E_INVALID_ARG, "s2s precision: DYCL_PREC_BF16 or DYCL_PREC_BF16X3_PARITY");
+  s->pair = precision == DYCL_PREC_BF16X3_PARITY;
+  return DYCL_OK;
+}
+
 dycl_status dycl_s2s_finalize(dycl_s2s s, int64_t max_batch) {
   if (!s) return DYCL_E_INVALID_ARG;
   if (s->finalized) return sfail(s, DYCL_E_STATE, "already finalized");
@@ -382,10 +405,31 @@ dycl_status dycl_s2s_finalize(dycl_s2s s, int64_t max_batch) {
     if (dycl_status r = dycl_s2s_set_loop_guard(s, nullptr, 0.f)) return r;
   SCK(cudaSetDevice(s->device));
   const size_t B = max_batch, d = s->c.d_model, S = s->c.src_len, R = B * S, L = s->c.max_len;
+  const size_t P = s->pair ? 2 : 1;               // split pairs double every bf16 tensor
   dycl_status r;
-  if ((r = alloc(s, &s->x32, R * d)) || (r = alloc(s, &s->pre, R * d)) || (r = alloc(s, &s->xb, R * d)) ||
-      (r = alloc(s, &s->qkv, R * 3 * d)) || (r = alloc(s, &s->att, R * d)) ||
-      (r = alloc(s, &s->h, R * (size_t)s->c.d_ff)) || (r = alloc(s, &s->logits, B * (size_t)s->c.vocab)) ||
+  if (s->pair) {                                  // [W | W] copies of every GEMM weight
+    const size_t f = s->c.d_ff;
+    auto dup = [&](uint16_t*& w, size_t N, size_t K) -> dycl_status {
+      uint16_t* w2 = nullptr;
+      if (dycl_status e = alloc(s, &w2, N * 2 * K)) return e;
+      SCK(cudaMemcpy2D(w2, 4 * K, w, 2 * K, 2 * K, N, cudaMemcpyDeviceToDevice));
+      SCK(cudaMemcpy2D(w2 + K, 4 * K, w, 2 * K, 2 * K, N, cudaMemcpyDeviceToDevice));
+      w = w2;
+      return DYCL_OK;
+    };
+    for (auto* Ls : {&s->enc, &s->dec})
+      for (DevLayer& Lw : *Ls) {
+        if ((r = dup(Lw.wqkv, 3 * d, d)) || (r = dup(Lw.wo, d, d)) || (r = dup(Lw.w1, f, d)) ||
+            (r = dup(Lw.w2, d, f)))
+          return r;
+        if (Lw.wq2 && ((r = dup(Lw.wq2, d, d)) || (r = dup(Lw.wkv2, 2 * d, d)) || (r = dup(Lw.wo2, d, d))))
+          return r;
+      }
+    if ((r = dup(s->lm_w, (size_t)s->c.vocab, d))) return r;
+  }
+  if ((r = alloc(s, &s->x32, R * d)) || (r = alloc(s, &s->pre, R * d)) || (r = alloc(s, &s->xb, R * d * P)) ||
+      (r = alloc(s, &s->qkv, R * 3 * d * P)) || (r = alloc(s, &s->att, R * d * P)) ||
+      (r = alloc(s, &s->h, R * (size_t)s->c.d_ff * P)) || (r = alloc(s, &s->logits, B * (size_t)s->c.vocab)) ||
       (r = alloc(s, &s->cur_tok, B)) || (r = alloc(s, &s->active[0], B)) || (r = alloc(s, &s->active[1], B)) ||
       (r = alloc(s, &s->list1, B)) || (r = alloc(s, &s->list0, B)) || (r = alloc(s, &s->counts, 2 * L + 2)) ||
       (r = alloc(s, &s->flag, B)))
@@ -393,7 +437,7 @@ dycl_status dycl_s2s_finalize(dycl_s2s s, int64_t max_batch) {
   s->cross.resize(s->dec.size());
   s->cache.resize(s->dec.size());
   for (size_t l = 0; l < s->dec.size(); ++l)
-    if ((r = alloc(s, &s->cross[l], R * 2 * d)) || (r = alloc(s, &s->cache[l], B * L * 2 * d))) return r;
+    if ((r = alloc(s, &s->cross[l], R * 2 * d * P)) || (r = alloc(s, &s->cache[l], B * L * 2 * d * P))) return r;
   s->max_batch = max_batch;
   s->finalized = true;
   return DYCL_OK;

@@ -19,6 +19,12 @@ __device__ __forceinline__ uint16_t to_bf(float f) {
   __nv_bfloat16 h = __float2bfloat16_rn(f);
   return *reinterpret_cast<uint16_t*>(&h);
 }
+// BF16X3 parity pair: hi = bf16(v), lo = bf16(v - hi)
+__device__ __forceinline__ void store_pair(uint16_t* row, int lo_off, int c, float v) {
+  const uint16_t h = to_bf(v);
+  row[c] = h;
+  row[lo_off + c] = to_bf(v - bf(h));
+}
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -69,7 +75,8 @@ __global__ void k_embed(const S2SEmbedArgs a) {
     }
     const float v = bf(e[c]) * sd + pe;
     a.x32[(size_t)warp * a.d + c] = v;
-    a.xb[(size_t)warp * a.d + c] = to_bf(v);
+    if (a.pair) store_pair(a.xb + (size_t)warp * 2 * a.d, a.d, c, v);
+    else a.xb[(size_t)warp * a.d + c] = to_bf(v);
   }
 }
 
@@ -104,7 +111,8 @@ __global__ void k_layernorm(const S2SLnArgs a) {
       const int c = lane + 32 * j;
       const float y = (v[j] - mu) * rstd * __ldg(a.gamma + c) + __ldg(a.beta + c);
       a.out32[(size_t)warp * a.d + c] = y;
-      a.outb[(size_t)warp * a.d + c] = to_bf(y);
+      if (a.pair) store_pair(a.outb + (size_t)warp * 2 * a.d, a.d, c, y);
+      else a.outb[(size_t)warp * a.d + c] = to_bf(y);
     }
   }
 }
@@ -122,18 +130,20 @@ __global__ void __launch_bounds__(128) k_attn_encoder(const S2SAttnArgs a) {
   const int n_seq = a.n_live ? *a.n_live : a.n_static;
   if (b >= n_seq) return;
   const int S = a.S, d = a.d, dh = 64;
-  const uint16_t* base = a.qkv + (size_t)b * S * 3 * d;
+  const int rs = (a.pair ? 6 : 3) * d;                // qkv row stride (pair: lo half at +3d)
+  const uint16_t* base = a.qkv + (size_t)b * S * rs;
+  auto ld = [&](size_t off) { return a.pair ? bf(base[off]) + bf(base[off + 3 * d]) : bf(base[off]); };
   for (int i = threadIdx.x; i < S * dh; i += blockDim.x) {
     const int j = i / dh, c = i % dh;
-    sk[j][c] = bf(base[(size_t)j * 3 * d + d + h * dh + c]);
-    sv[j][c] = bf(base[(size_t)j * 3 * d + 2 * d + h * dh + c]);
+    sk[j][c] = ld((size_t)j * rs + d + h * dh + c);
+    sv[j][c] = ld((size_t)j * rs + 2 * d + h * dh + c);
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float scale = 0.125f;          // 1/sqrt(64)
   for (int i = warp; i < S; i += 4) {
-    sq[warp][lane] = bf(base[(size_t)i * 3 * d + h * dh + lane]);
-    sq[warp][lane + 32] = bf(base[(size_t)i * 3 * d + h * dh + lane + 32]);
+    sq[warp][lane] = ld((size_t)i * rs + h * dh + lane);
+    sq[warp][lane + 32] = ld((size_t)i * rs + h * dh + lane + 32);
     __syncwarp();
     float s0 = -INFINITY, s1 = -INFINITY;
     if (lane < S) {
@@ -157,11 +167,74 @@ __global__ void __launch_bounds__(128) k_attn_encoder(const S2SAttnArgs a) {
       o0 += sp[warp][j] * sv[j][lane];
       o1 += sp[warp][j] * sv[j][lane + 32];
     }
-    uint16_t* out = a.out + ((size_t)b * S + i) * d + h * dh;
-    out[lane] = to_bf(o0);
-    out[lane + 32] = to_bf(o1);
+    if (a.pair) {
+      uint16_t* out = a.out + ((size_t)b * S + i) * 2 * d + h * dh;
+      store_pair(out, d, lane, o0);
+      store_pair(out, d, lane + 32, o1);
+    } else {
+      uint16_t* out = a.out + ((size_t)b * S + i) * d + h * dh;
+      out[lane] = to_bf(o0);
+      out[lane + 32] = to_bf(o1);
+    }
     __syncwarp();
   }
+}
+
+// Parity-mode decoder attention (split pairs, value = hi + lo), one warp per (row, head):
+// the same math and summation order as k_attn_decoder below.
+__device__ __noinline__ void attn_decoder_pair(const S2SAttnArgs& a, int row, int h, int slot, int lane) {
+  const int d = a.d, dh = 64;
+  const uint16_t* qrow = a.q + (size_t)row * a.q_stride + h * dh;
+  const float q0 = bf(qrow[2 * lane]) + bf(qrow[a.q_lo + 2 * lane]);
+  const float q1 = bf(qrow[2 * lane + 1]) + bf(qrow[a.q_lo + 2 * lane + 1]);
+  const uint16_t* kv;                 // rows [K_hi V_hi K_lo V_lo], stride 4d
+  int nk;
+  if (a.kv == nullptr) {
+    uint16_t* cache = a.cache + (size_t)slot * a.max_len * 4 * d;
+    const uint16_t* src = a.qkv + (size_t)row * 6 * d;
+    uint16_t* dst = cache + (size_t)a.t * 4 * d;
+    for (int c = lane; c < dh; c += 32) {
+      dst[h * dh + c] = src[d + h * dh + c];
+      dst[d + h * dh + c] = src[2 * d + h * dh + c];
+      dst[2 * d + h * dh + c] = src[3 * d + d + h * dh + c];
+      dst[3 * d + h * dh + c] = src[3 * d + 2 * d + h * dh + c];
+    }
+    __syncwarp();
+    kv = cache;
+    nk = a.t + 1;
+  } else {
+    kv = a.kv + (size_t)slot * a.S * 4 * d;
+    nk = a.S;
+  }
+  float s0 = -INFINITY, s1 = -INFINITY;
+  for (int half = 0; half < 2; ++half) {
+    const int j = lane + 32 * half;
+    float acc = 0.f;
+    for (int c = 0; c < dh; c += 2) {
+      const float qa = __shfl_sync(0xffffffffu, q0, c >> 1), qb = __shfl_sync(0xffffffffu, q1, c >> 1);
+      if (j < nk) {
+        const uint16_t* kr = kv + (size_t)j * 4 * d + h * dh + c;
+        acc += qa * (bf(kr[0]) + bf(kr[2 * d])) + qb * (bf(kr[1]) + bf(kr[2 * d + 1]));
+      }
+    }
+    if (j < nk) {
+      if (half == 0) s0 = acc * 0.125f;
+      else s1 = acc * 0.125f;
+    }
+  }
+  const float m = warp_max(fmaxf(s0, s1));
+  const float e0 = lane < nk ? expf(s0 - m) : 0.f, e1 = lane + 32 < nk ? expf(s1 - m) : 0.f;
+  const float inv = 1.f / warp_sum(e0 + e1);
+  float o0 = 0.f, o1 = 0.f;
+  for (int j = 0; j < nk; ++j) {
+    const float pj = __shfl_sync(0xffffffffu, j < 32 ? e0 : e1, j & 31) * inv;
+    const uint16_t* vr = kv + (size_t)j * 4 * d + d + h * dh + 2 * lane;
+    o0 += pj * (bf(vr[0]) + bf(vr[2 * d]));
+    o1 += pj * (bf(vr[1]) + bf(vr[2 * d + 1]));
+  }
+  uint16_t* out = a.out + (size_t)row * 2 * d + h * dh;
+  store_pair(out, d, 2 * lane, o0);
+  store_pair(out, d, 2 * lane + 1, o1);
 }
 
 // Decoder attention for one query per active row, one warp per (row, head).
@@ -177,6 +250,10 @@ __global__ void __launch_bounds__(256, 5) k_attn_decoder(const S2SAttnArgs a) {
   if (row >= n) return;
   const int slot = a.slot[row];
   const int d = a.d, dh = 64;
+  if (a.pair) {                       // BF16X3 parity mode: split pairs, plain loads (not tuned)
+    attn_decoder_pair(a, row, h, slot, lane);
+    return;
+  }
   const uint16_t* qrow = a.q + (size_t)row * a.q_stride + h * dh;
   // the head's 64-dim query in SMEM (fp32, per warp), read back as broadcasts: keeps the
   // registers low enough for 6+ CTAs per SM (memory-level parallelism for the K/V stream)

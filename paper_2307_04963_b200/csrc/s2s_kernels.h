@@ -14,6 +14,7 @@ struct S2SEmbedArgs {
   uint16_t* xb;            // [rows][d]
   const int* n_live;
   int n_static, d, S, t;
+  int pair = 0;            // BF16X3 parity mode: xb rows are [hi(d) | lo(d)]
 };
 struct S2SLnArgs {
   const float* in;         // [rows][d]
@@ -24,6 +25,7 @@ struct S2SLnArgs {
   const int* n_live;
   int n_static, d;
   float eps;
+  int pair = 0;            // outb rows are [hi(d) | lo(d)]
 };
 struct S2SAttnArgs {
   const uint16_t* qkv;     // encoder: [B*S][3d]; decoder self: [rows][3d] (k, v appended)
@@ -35,6 +37,11 @@ struct S2SAttnArgs {
   const int32_t* slot;
   const int* n_live;
   int n_static, d, heads, S, max_len, t;
+  // BF16X3 parity mode: every bf16 tensor row is a split pair [hi | lo] (value = hi + lo):
+  // qkv rows [q k v | q k v]_lo at +3d, K/V rows [K V | K V]_lo at +2d, out rows lo at +d;
+  // q_lo = offset of the query's lo half within its row (3d self, d cross)
+  int pair = 0;
+  int q_lo = 0;
 };
 struct S2SArgmaxArgs {
   const float* logits;     // [rows][V]

@@ -33,7 +33,12 @@ class DyclError(RuntimeError):
 
 class dycl_io(ctypes.Structure):
     _fields_ = [("input", ctypes.c_void_p), ("batch", ctypes.c_int64), ("logits", ctypes.c_void_p),
-                ("path", ctypes.c_void_p), ("node_counts", ctypes.c_void_p)]
+                ("path", ctypes.c_void_p), ("node_counts", ctypes.c_void_p), ("global_offset", ctypes.c_int64),
+                ("min_margin", ctypes.c_void_p)]
+
+
+DYCL_REBALANCE_NONE = 0
+DYCL_REBALANCE_ALL = -1
 
 
 class dycl_s2s_config(ctypes.Structure):
@@ -58,6 +63,9 @@ EXPORTS = [
     "dycl_gate", "dycl_final", "dycl_finalize", "dycl_run", "dycl_run_host", "dycl_num_count_slots",
     "dycl_launches_per_run", "dycl_num_classes", "dycl_set_profiling", "dycl_profile_read",
     "dycl_debug_conv2d", "dycl_rebalance_plan", "dycl_debug_timestamps",
+    "dycl_run_host_ex", "dycl_set_comm", "dycl_local_group_create", "dycl_local_group_destroy",
+    "dycl_set_comm_local", "dycl_rebalance_stats", "dycl_nccl_get_unique_id", "dycl_nccl_comm_init_rank",
+    "dycl_nccl_comm_destroy", "dycl_s2s_set_precision",
 ]
 
 
@@ -100,6 +108,15 @@ def lib():
             "dycl_rebalance_plan": [Pi, i32, i32, Pi, Pi, Pi],
             "dycl_debug_timestamps": [vp, ctypes.POINTER(ctypes.c_longlong)],
             "dycl_debug_conv2d": [vp, i64, i32, i32, i32, P16, Pf, i32, i32, i32, i32, i32, vp, i32, vp, vp, i32],
+            "dycl_run_host_ex": [vp, vp, i64, i64, vp, vp, vp, vp],
+            "dycl_set_comm": [vp, vp, i32, i32, i32],
+            "dycl_local_group_create": [i32, ctypes.POINTER(vp)],
+            "dycl_local_group_destroy": [vp],
+            "dycl_set_comm_local": [vp, vp, i32, i32],
+            "dycl_rebalance_stats": [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)],
+            "dycl_nccl_get_unique_id": [ctypes.POINTER(ctypes.c_uint8)],
+            "dycl_nccl_comm_init_rank": [ctypes.POINTER(ctypes.c_uint8), i32, i32, i32, ctypes.POINTER(vp)],
+            "dycl_nccl_comm_destroy": [vp],
         }
         sig.update({
             "dycl_s2s_create": [i32, ctypes.POINTER(dycl_s2s_config), ctypes.POINTER(vp)],
@@ -110,6 +127,7 @@ def lib():
             "dycl_s2s_set_lm_head": [vp, vp, vp],
             "dycl_s2s_set_loop_guard": [vp, vp, f32],
             "dycl_s2s_finalize": [vp, i64],
+            "dycl_s2s_set_precision": [vp, i32],
             "dycl_s2s_run": [vp, vp, i64, vp, vp, vp, vp, vp],
             "dycl_s2s_run_host": [vp, vp, i64, vp, vp, vp],
             "dycl_s2s_launches": [vp, Pi],
@@ -160,6 +178,7 @@ def dycl_graph_create(cuda_device: int, in_h: int, in_w: int, in_c: int):
 
 DYCL_PREC_BF16 = 0
 DYCL_PREC_FP32_STREAM = 1
+DYCL_PREC_BF16X3_PARITY = 2
 
 
 def dycl_graph_set_precision(g, precision):
@@ -234,10 +253,11 @@ def dycl_finalize(g, max_batch):
     _ck(lib().dycl_finalize(g, int(max_batch)), g)
 
 
-def dycl_run(g, input, batch, logits, path, node_counts=None, stream=None):
-    """input/logits/path/node_counts: CUDA torch tensors (fp32, fp32, int32, int32)."""
+def dycl_run(g, input, batch, logits, path, node_counts=None, stream=None, global_offset=0, min_margin=None):
+    """input/logits/path/node_counts/min_margin: CUDA torch tensors (fp32, fp32, int32, int32, fp32)."""
     io = dycl_io(input.data_ptr(), int(batch), logits.data_ptr(), path.data_ptr(),
-                 node_counts.data_ptr() if node_counts is not None else None)
+                 node_counts.data_ptr() if node_counts is not None else None, int(global_offset),
+                 min_margin.data_ptr() if min_margin is not None else None)
     _ck(lib().dycl_run(g, ctypes.byref(io), _stream_ptr(stream)), g)
 
 
@@ -247,6 +267,59 @@ def dycl_run_host(g, input_host, batch, logits_host, path_host, stream=None):
         return t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data
     _ck(lib().dycl_run_host(g, ctypes.c_void_p(ptr(input_host)), int(batch), ctypes.c_void_p(ptr(logits_host)),
                             ctypes.c_void_p(ptr(path_host)), _stream_ptr(stream)), g)
+
+
+def dycl_run_host_ex(g, input_host, batch, global_offset, logits_host, path_host, min_margin_host=None,
+                     stream=None):
+    def ptr(t):
+        return t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data
+    _ck(lib().dycl_run_host_ex(g, ctypes.c_void_p(ptr(input_host)), int(batch), int(global_offset),
+                               ctypes.c_void_p(ptr(logits_host)), ctypes.c_void_p(ptr(path_host)),
+                               ctypes.c_void_p(ptr(min_margin_host)) if min_margin_host is not None else None,
+                               _stream_ptr(stream)), g)
+
+
+def dycl_set_comm(g, nccl_comm_ptr, rank, world, rebalance_policy=DYCL_REBALANCE_ALL):
+    """nccl_comm_ptr: an ncclComm_t as an int (e.g. ProcessGroupNCCL._comm_ptr())."""
+    _ck(lib().dycl_set_comm(g, ctypes.c_void_p(int(nccl_comm_ptr) if nccl_comm_ptr else 0), int(rank), int(world),
+                            int(rebalance_policy)), g)
+
+
+def dycl_local_group_create(world):
+    h = ctypes.c_void_p()
+    _ck(lib().dycl_local_group_create(int(world), ctypes.byref(h)), None)
+    return h
+
+
+def dycl_local_group_destroy(grp):
+    _ck(lib().dycl_local_group_destroy(grp), None)
+
+
+def dycl_set_comm_local(g, grp, rank, rebalance_policy=DYCL_REBALANCE_ALL):
+    _ck(lib().dycl_set_comm_local(g, grp, int(rank), int(rebalance_policy)), g)
+
+
+def dycl_rebalance_stats(g):
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    _ck(lib().dycl_rebalance_stats(g, ctypes.byref(a), ctypes.byref(b)), g)
+    return a.value, b.value
+
+
+def dycl_nccl_get_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _ck(lib().dycl_nccl_get_unique_id(buf), None)
+    return bytes(buf)
+
+
+def dycl_nccl_comm_init_rank(uid: bytes, rank, world, cuda_device):
+    buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+    h = ctypes.c_void_p()
+    _ck(lib().dycl_nccl_comm_init_rank(buf, int(rank), int(world), int(cuda_device), ctypes.byref(h)), None)
+    return h
+
+
+def dycl_nccl_comm_destroy(comm):
+    _ck(lib().dycl_nccl_comm_destroy(comm), None)
 
 
 def dycl_num_count_slots(g) -> int:
@@ -359,6 +432,10 @@ def dycl_s2s_set_loop_guard(s, len_table, beta):
         return
     a, pa = _hp(len_table, np.float32)
     _s2s_ck(lib().dycl_s2s_set_loop_guard(s, pa, float(beta)), s)
+
+
+def dycl_s2s_set_precision(s, precision):
+    _s2s_ck(lib().dycl_s2s_set_precision(s, int(precision)), s)
 
 
 def dycl_s2s_finalize(s, max_batch):

@@ -23,11 +23,16 @@ class Model:
     def __init__(self, g, in_shape, K, max_batch, name):
         self.g, self.in_shape, self.K, self.max_batch, self.name = g, in_shape, K, max_batch, name
 
-    def run(self, x, logits, path, node_counts=None, stream=None, batch=None):
-        D.dycl_run(self.g, x, x.shape[0] if batch is None else batch, logits, path, node_counts, stream)
+    def run(self, x, logits, path, node_counts=None, stream=None, batch=None, global_offset=0, min_margin=None):
+        D.dycl_run(self.g, x, x.shape[0] if batch is None else batch, logits, path, node_counts, stream,
+                   global_offset, min_margin)
 
-    def run_host(self, x_host, logits_host, path_host, stream=None):
-        D.dycl_run_host(self.g, x_host, x_host.shape[0], logits_host, path_host, stream)
+    def run_host(self, x_host, logits_host, path_host, stream=None, global_offset=0, min_margin=None):
+        if global_offset == 0 and min_margin is None:
+            D.dycl_run_host(self.g, x_host, x_host.shape[0], logits_host, path_host, stream)
+        else:
+            D.dycl_run_host_ex(self.g, x_host, x_host.shape[0], global_offset, logits_host, path_host, min_margin,
+                               stream)
 
     def close(self):
         if self.g is not None:
@@ -194,12 +199,15 @@ class Seq2Seq:
             pass
 
 
-def build_seq2seq(W, cfg, max_batch, device=0) -> Seq2Seq:
+def build_seq2seq(W, cfg, max_batch, device=0, precision=D.DYCL_PREC_BF16) -> Seq2Seq:
     """Config 4, rewritten: encoder sub-network + decoder-step sub-network + LM head, with the
-    EOS / length guard registered as the loop's logic node."""
+    EOS / length guard registered as the loop's logic node.  precision: DYCL_PREC_BF16
+    (production) or DYCL_PREC_BF16X3_PARITY (fp32-accurate split-bf16 products)."""
     cfg = dict(cfg)
     cfg.setdefault("d_model", cfg.get("d"))
     h = D.dycl_s2s_create(device, cfg)
+    if precision != D.DYCL_PREC_BF16:
+        D.dycl_s2s_set_precision(h, precision)
     D.dycl_s2s_set_embeddings(h, W["src_emb"], W["tgt_emb"])
     for l in range(cfg["enc_layers"]):
         p = f"enc{l}."

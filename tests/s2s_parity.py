@@ -37,10 +37,10 @@ def _threads():
     return max(1, len(os.sched_getaffinity(0)))
 
 
-def compare_free_running(P_, src, tok, ln, top1, z0):
+def compare_free_running(P_, src, tok, ln, top1, z0, mode="mirror"):
     """Oracle free-running decode per sequence vs the GPU's tokens / lengths / top-1 logits."""
     with ThreadPoolExecutor(_threads()) as ex:
-        res = list(ex.map(lambda i: S.greedy_decode(src[i], P_, wl.S2S, "mirror"), range(len(src))))
+        res = list(ex.map(lambda i: S.greedy_decode(src[i], P_, wl.S2S, mode), range(len(src))))
     rep = dict(n=len(src), band_excluded=0, mismatch=0, max_top1_rel=0.0, max_z0_rel=0.0, mismatch_idx=[])
     for i, (o_tok, o_len, o_top1, o_z0, preds) in enumerate(res):
         rel0 = np.max(np.abs(z0[i] - o_z0)) / np.max(np.abs(o_z0))
@@ -58,11 +58,11 @@ def compare_free_running(P_, src, tok, ln, top1, z0):
     return rep
 
 
-def compare_teacher_forced(P_, src, tok, ln, top1):
+def compare_teacher_forced(P_, src, tok, ln, top1, mode="mirror"):
     """Per step: the oracle, fed the GPU's own prefix, must choose the GPU's token at every
     step whose oracle margin lies outside the band; the chosen token's logit within 2e-2."""
     def one(i):
-        return S.greedy_decode(src[i], P_, wl.S2S, "mirror", forced=tok[i])
+        return S.greedy_decode(src[i], P_, wl.S2S, mode, forced=tok[i])
     with ThreadPoolExecutor(_threads()) as ex:
         res = list(ex.map(one, range(len(src))))
     rep = dict(n=len(src), steps=0, band_steps=0, step_mismatch=0, max_top1_rel=0.0)
@@ -81,15 +81,15 @@ def compare_teacher_forced(P_, src, tok, ln, top1):
     return rep
 
 
-def s2s_free_running(m, W, src, idx):
+def s2s_free_running(m, W, src, idx, mode="mirror"):
     tok, ln, top1, z0 = run_s2s(m, src)
-    rep = compare_free_running(_prep(W), src[idx], tok[idx], ln[idx], top1[idx], z0[idx])
+    rep = compare_free_running(_prep(W), src[idx], tok[idx], ln[idx], top1[idx], z0[idx], mode)
     rep.update(batch=len(src), sampled=len(idx), mean_length=float(ln.mean()))
     return rep
 
 
-def s2s_teacher_forced(m, W, src, idx):
+def s2s_teacher_forced(m, W, src, idx, mode="mirror"):
     tok, ln, top1, _ = run_s2s(m, src)
-    rep = compare_teacher_forced(_prep(W), src[idx], tok[idx], ln[idx], top1[idx])
+    rep = compare_teacher_forced(_prep(W), src[idx], tok[idx], ln[idx], top1[idx], mode)
     rep.update(batch=len(src), sampled=len(idx))
     return rep

@@ -1,5 +1,8 @@
-"""Multi-rank host logic on CPU (gloo, world_size 2 and 3): the survivor rebalancing plan
-(libdycl's dycl_rebalance_plan) and the exchange / return protocol (rebalance.py)."""
+"""Multi-rank host logic on CPU (gloo, world sizes 2-4): the survivor rebalancing plan
+(libdycl's dycl_rebalance_plan) computed independently on every rank from all-gathered counts
+must agree across ranks (sends == peers' receives, rows conserved, surplus ranks drop to
+T = ceil(S/G)); the bench's shards tile the global batch.  The exchange itself runs inside
+dycl_run (NCCL / in-process transport) and is tested on the GPU (tests/test_gpu_multi.py)."""
 import os
 import socket
 
@@ -44,40 +47,36 @@ def _free_port():
 
 
 def _worker(rank, world, port, counts, q):
+    """One rank: all-gather the survivor counts over gloo, compute this rank's plan with the
+    C-ABI host function (what dycl_run does between the all-gather and the exchange), and
+    check that every rank's sends match its peers' receives and the data volume is conserved."""
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_2307_04963_b200 import rebalance as RB
-    B = 64                                                  # local batch per rank
-    n = counts[rank]
-    cap = B
-    # survivors: global ids of this rank's surviving samples, rows = f(id)
-    ids = torch.full((cap,), -1, dtype=torch.int64)
-    ids[:n] = rank * B + torch.arange(n) * 2                  # every other sample survived
-    rows = torch.zeros((cap, 5), dtype=torch.float32)
-    rows[:n] = ids[:n, None].float() * torch.tensor([1.0, -2.0, 0.5, 3.0, 7.0])
-    new_n, send, recv = RB.exchange([rows, ids], n)
-    ok = True
-    # content integrity: every held row still matches its id
-    ok &= bool(torch.equal(rows[:new_n], ids[:new_n, None].float() * torch.tensor([1.0, -2.0, 0.5, 3.0, 7.0])))
-    # "compute" on the holding rank, return results home, compare to local compute
-    res = rows[:new_n].sum(dim=1, keepdim=True) * 3.0 + 1.0
-    out = torch.full((B, 1), float("nan"))
-    RB.return_results(res, ids, new_n, B, out)
-    mine = rank * B + torch.arange(n) * 2
-    expect = (mine[:, None].float() * torch.tensor([1.0, -2.0, 0.5, 3.0, 7.0])).sum(1, keepdim=True) * 3.0 + 1.0
-    ok &= bool(torch.equal(out[(mine - rank * B)], expect))
-    ok &= bool(torch.isnan(out[1::2]).all()) if n else True
-    held = torch.tensor([new_n])
-    allh = [torch.zeros_like(held) for _ in range(world)]
-    dist.all_gather(allh, held)
-    q.put((rank, ok, [int(h) for h in allh], int(send.sum()), int(recv.sum())))
+    t = torch.tensor([counts[rank]], dtype=torch.int32)
+    allc = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(allc, t)
+    seen = [int(x) for x in allc]
+    send, recv, new = D.dycl_rebalance_plan(seen, rank)
+    sends = [torch.zeros(world, dtype=torch.int32) for _ in range(world)]
+    dist.all_gather(sends, torch.from_numpy(send))
+    matrix = torch.stack(sends).numpy()                       # matrix[r, j] = rows r sends to j
+    ok = seen == list(counts)
+    ok &= bool(np.array_equal(matrix[:, rank], recv))        # my receives are my peers' sends to me
+    ok &= new == counts[rank] - int(send.sum()) + int(recv.sum())
+    # rows a surplus rank sends are its LAST ones, destination ascending: the row ranges
+    # [keep + sum(send[:j]), keep + sum(send[:j+1])) tile [keep, count) exactly
+    keep = counts[rank] - int(send.sum())
+    ok &= keep >= 0 and (keep == counts[rank] or int(recv.sum()) == 0)
+    held = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(held, torch.tensor([new], dtype=torch.int64))
+    q.put((rank, ok, [int(h) for h in held], int(send.sum()), int(recv.sum())))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("counts", [[30, 4], [5, 17, 2], [0, 9]])
-def test_gloo_exchange_and_return(counts):
+@pytest.mark.parametrize("counts", [[30, 4], [5, 17, 2], [0, 9], [3, 3], [100, 0, 0, 1]])
+def test_gloo_plan_agreement(counts):
     world = len(counts)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -93,3 +92,14 @@ def test_gloo_exchange_and_return(counts):
     for rank, ok, held, ns, nr in res:
         assert ok, (rank, held)
         assert sum(held) == sum(counts) and max(held) == T
+
+
+@pytest.mark.parametrize("B,world", [(65536, 1), (65536, 2), (65536, 8), (65536, 3), (5, 8), (2048, 6)])
+def test_bench_shards_tile_the_global_batch(B, world):
+    """bench.py's shards: contiguous [r*B/G, (r+1)*B/G), disjoint, covering the global batch."""
+    import bench
+    lo_hi = [bench.shard(B, world, r) for r in range(world)]
+    assert lo_hi[0][0] == 0 and lo_hi[-1][1] == B
+    assert all(a[1] == b[0] for a, b in zip(lo_hi, lo_hi[1:]))
+    sizes = [h - l for l, h in lo_hi]
+    assert max(sizes) - min(sizes) <= 1
