@@ -21,12 +21,12 @@ pin beyond library cross-checks are marked "parity unpinned" where defined.
 """
 from .core import (round_bf16, conv2d, dense, gap, relu, max_softmax, sigmoid,
                    argmax_lowest, option_a, maxpool2d)
-from .programs import (mlp_ee, sdn_resnet56, skipnet_resnet38, resnet50_ee, run_batch,
+from .programs import (mlp_ee, sdn_resnet56, skipnet_resnet38, skipnet_rnn_resnet38, resnet50_ee, run_batch,
                        PROGRAMS)
 from .metrics import delta, eta
 
 __all__ = [
     "round_bf16", "conv2d", "dense", "gap", "relu", "max_softmax", "sigmoid",
-    "argmax_lowest", "option_a", "maxpool2d", "mlp_ee", "sdn_resnet56", "skipnet_resnet38", "resnet50_ee",
+    "argmax_lowest", "option_a", "maxpool2d", "mlp_ee", "sdn_resnet56", "skipnet_resnet38", "skipnet_rnn_resnet38", "resnet50_ee",
     "run_batch", "PROGRAMS", "delta", "eta",
 ]

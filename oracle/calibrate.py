@@ -18,7 +18,10 @@ samples drawn with seed CALIB_SEED=2 (disjoint from the measured inputs):
   raw r = H_i . g, a_i = median(r), s_i = 2 / std(r); gate logit
   z = bf16(s_i H_i) . g - s_i a_i  (~50 % execute); final head s = 4, centred.
 
-Usage:  python -m oracle.calibrate [--n 512]
+* SkipNet with recurrent gates (cfg3r, reading R19): as config 3 but on the raw LSTM output
+  r = w_out . h after each gate's cell step; out_i = (s_i w_out, -s_i a_i) in fp32.
+
+Usage:  python -m oracle.calibrate [--n 512] [--cfg 2 3 3r 5]
 """
 from __future__ import annotations
 
@@ -124,6 +127,48 @@ def calibrate_cfg3(n: int, mode: str = "mirror") -> dict:
     return out
 
 
+def calibrate_cfg3r(n: int, mode: str = "mirror") -> dict:
+    """SkipNet with the recurrent gate (reading R19): gates in path order; per gate the raw
+    output r = w_out . hs of the LSTM state after this gate's step, a = median(r), s = 2/std(r);
+    the program's gate logit is then (s w_out)_fp32 . hs + (-s a)_fp32 (~50 % execute)."""
+    X = wl.image_inputs(wl.CALIB_SEED, 0, n)
+    W = wl.skipnet_rnn_r38_weights(calib=None)
+    P = prg.prepare(W)
+    raw = wl.skipnet_rnn_r38_raw()
+    Hd = int(P["rnn.hidden"])
+    with _pool() as ex:
+        H = list(ex.map(lambda i: prg.basic_block(prg.stem(X[i], P, mode), P, 1, 6, mode), range(n)))
+        hs = [np.zeros(Hd) for _ in range(n)]
+        cs = [np.zeros(Hd) for _ in range(n)]
+        out = {}
+        executed = []
+        for i in wl.SKIP_GATED:
+            for j in range(n):
+                u = dense(P[f"proj{i}.w"], P[f"proj{i}.b"], gap(H[j]))
+                hs[j], cs[j] = prg.lstm_cell(u, hs[j], cs[j], P)
+            r = np.array([raw["w_out"] @ h for h in hs])
+            a = float(np.median(r))
+            s = float(2.0 / r.std())
+            w = np.float32(s * raw["w_out"]).astype(np.float64)
+            b = float(np.float32(-s * a))
+            run = np.array([sigmoid(w @ h + b) > 0.5 for h in hs])
+            executed.append(float(run.mean()))
+            out[f"gate{i}"] = {"scale": s, "median": a, "exec_frac": float(run.mean())}
+            ci, co, stride = prg._block_io(i, 6)
+
+            def step(j, i=i, run=run, co=co, stride=stride):
+                if run[j]:
+                    return prg.basic_block(H[j], P, i, 6, mode)
+                return prg.option_a(H[j], co) if stride == 2 else H[j]
+
+            H = list(ex.map(step, range(n)))
+    out["final"] = {"scale": 4.0, "mu": [float(v) for v in np.stack([gap(h) for h in H]).mean(axis=0)]}
+    out["_recipe"] = ("oracle/calibrate.py calibrate_cfg3r: n=%d calibration samples (seed %d), "
+                      "mode=%s, recurrent gates in path order, a=median, s=2/std of w_out . h; mean executed "
+                      "%.2f/17" % (n, wl.CALIB_SEED, mode, sum(executed)))
+    return out
+
+
 def calibrate_cfg5(n: int, mode: str = "mirror") -> dict:
     """Config 5 heads (exits after stages 1-3, 1000 classes): same recipe as config 2."""
     X = wl.image_inputs(wl.CALIB_SEED, 0, n, hw=224)
@@ -174,12 +219,13 @@ def calibrate_cfg5(n: int, mode: str = "mirror") -> dict:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=512)
-    ap.add_argument("--cfg", type=int, nargs="*", default=[2, 3])
+    ap.add_argument("--cfg", nargs="*", default=["2", "3"], help="2 3 3r 5")
     ap.add_argument("--n5", type=int, default=128)
     a = ap.parse_args()
     os.makedirs(os.path.join(wl.HERE, "calib"), exist_ok=True)
     for c in a.cfg:
-        res = calibrate_cfg2(a.n) if c == 2 else calibrate_cfg3(a.n) if c == 3 else calibrate_cfg5(a.n5)
+        res = {"2": lambda: calibrate_cfg2(a.n), "3": lambda: calibrate_cfg3(a.n), "3r": lambda: calibrate_cfg3r(a.n),
+               "5": lambda: calibrate_cfg5(a.n5)}[str(c)]()
         path = os.path.join(wl.HERE, "calib", f"cfg{c}.json")
         with open(path, "w") as f:
             json.dump(res, f, indent=1)

@@ -173,6 +173,53 @@ def skipnet_resnet38(x, P, mode="mirror", thr=0.5, gate_hook=None):
 
 
 # ---------------------------------------------------------------------------
+# SkipNet with the recurrent gate (Table 3 ID 5 "ResNet38 + RNN"; SURVEY 8(f)3;
+# reading R19).  Same trunk, same Listing-3 control flow as config 3; the gate of block i is
+#   u = proj_i(GAP(h))                       (dense C_i -> n_in, bf16 weights, fp32 logits)
+#   (hs, cs) = LSTMCell(u, (hs, cs))          (one cell shared by all gates, state carried across
+#                                             gates in program order, zero before gate 2; torch
+#                                             gate order i, f, g, o)
+#   p = sigmoid(w_out_i . hs + b_out_i)       (per-gate calibrated output, fp32)
+# and the cell steps at EVERY gate, whether the block then runs or not.
+# ---------------------------------------------------------------------------
+def lstm_cell(u, hs, cs, P):
+    """One LSTM step (torch.nn.LSTMCell semantics), fp64."""
+    gates = P["rnn.w_ih"] @ u + P["rnn.b_ih"] + P["rnn.w_hh"] @ hs + P["rnn.b_hh"]
+    H = hs.shape[0]
+    i_ = sigmoid(gates[0:H])
+    f_ = sigmoid(gates[H:2 * H])
+    g_ = np.tanh(gates[2 * H:3 * H])
+    o_ = sigmoid(gates[3 * H:4 * H])
+    cs = f_ * cs + i_ * g_
+    return o_ * np.tanh(cs), cs
+
+
+def skipnet_rnn_resnet38(x, P, mode="mirror", thr=0.5, gate_hook=None):
+    preds = []
+    h = stem(x, P, mode)
+    h = basic_block(h, P, 1, 6, mode)
+    H = int(P["rnn.hidden"])
+    hs, cs = np.zeros(H), np.zeros(H)
+    mask = 0
+    for i in range(2, 19):
+        g = gap(h)
+        u = dense(P[f"proj{i}.w"], P[f"proj{i}.b"], g)
+        hs, cs = lstm_cell(u, hs, cs, P)
+        z = float(P[f"out{i}.w"] @ hs + P[f"out{i}.b"][0])
+        if gate_hook is not None:
+            gate_hook(i, g, hs, z)
+        p = sigmoid(z)
+        preds.append(("gate", p, thr))
+        if p > thr:
+            h = basic_block(h, P, i, 6, mode)
+            mask |= 1 << (i - 2)
+        else:
+            ci, co, stride = _block_io(i, 6)
+            h = option_a(h, co) if stride == 2 else h
+    return dense(P["final.w"], P["final.b"], gap(h)), mask, preds
+
+
+# ---------------------------------------------------------------------------
 # Config 5: early-exit ResNet-50 v1.5 (BASELINE configs[4]).
 #   h = maxpool(relu(conv7x7/2(x)))
 #   for stage s in 1..4: for each bottleneck b: h = bottleneck(h)

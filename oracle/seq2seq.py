@@ -25,7 +25,8 @@ Decoding is incremental (cached K/V of earlier positions), which equals recomput
 the whole prefix for a causal decoder (tests pin it against torch's full recompute).
 
 Modes as in programs.py: 'mirror' rounds every tensor-core operand and every
-bf16-stored tensor (q/k/v, K/V caches, attention outputs, FFN hidden) to bf16,
+bf16-stored tensor (q/k/v, K/V caches, attention outputs, FFN hidden, the encoder's
+attention probabilities P) to bf16,
 keeps the residual stream, LayerNorm, softmax and logits unrounded; 'exact' rounds
 nothing.  Matrix products use numpy's matmul (fp64) as the library primitive.
 """
@@ -65,14 +66,18 @@ def _softmax_rows(s):
     return e / e.sum(axis=-1, keepdims=True)
 
 
-def attention(q, k, v, heads, mode):
-    """Multi-head scaled dot-product attention: q [nq, d], k/v [nk, d] (already bf16 in mirror)."""
+def attention(q, k, v, heads, mode, p_operand=False):
+    """Multi-head scaled dot-product attention: q [nq, d], k/v [nk, d] (already bf16 in mirror).
+    p_operand: the probabilities P are a tensor-core operand (the encoder's P x V runs on
+    tcgen05), so mirror mode rounds P = softmax(.) to bf16 before P @ V (reading R18)."""
     nq, d = q.shape
     dh = d // heads
     out = np.empty((nq, d))
     for h in range(heads):
         sl = slice(h * dh, (h + 1) * dh)
         p = _softmax_rows(q[:, sl] @ k[:, sl].T / math.sqrt(dh))
+        if p_operand:
+            p = _r(p, mode)
         out[:, sl] = p @ v[:, sl]
     return _r(out, mode)                      # stored bf16: the out-projection's operand
 
@@ -87,7 +92,7 @@ def encoder(src, P, cfg, mode):
     for l in range(cfg["enc_layers"]):
         p = f"enc{l}"
         qkv = _r(_linear(x, P, p + ".wqkv", p + ".bqkv", mode), mode)
-        a = attention(qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:], H, mode)
+        a = attention(qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:], H, mode, p_operand=True)
         x = layer_norm(_linear(a, P, p + ".wo", p + ".bo", mode) + x, P[p + ".ln1.g"], P[p + ".ln1.b"])
         h = _r(np.maximum(_linear(x, P, p + ".w1", p + ".b1", mode), 0.0), mode)
         x = layer_norm(_linear(h, P, p + ".w2", p + ".b2", mode) + x, P[p + ".ln2.g"], P[p + ".ln2.b"])

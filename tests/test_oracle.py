@@ -468,6 +468,13 @@ def test_seq2seq_mirror_rounding_points(s2s, monkeypatch):
         o = F.scaled_dot_product_attention(sp(q)[None], sp(k)[None], sp(v)[None], is_causal=causal)[0]
         return rb(o.transpose(0, 1).reshape(q.shape[0], d))
 
+    def mha_enc(q, k, v):
+        # encoder: P x V on the tensor cores, so P itself is a bf16 operand (reading R18)
+        sp = lambda t: t.reshape(t.shape[0], H, d // H).transpose(0, 1)  # noqa: E731
+        p = torch.softmax(sp(q) @ sp(k).transpose(1, 2) / np.sqrt(d // H), dim=-1)
+        o = rb(p) @ sp(v)
+        return rb(o.transpose(0, 1).reshape(q.shape[0], d))
+
     def ln(x, p):
         return F.layer_norm(x, (d,), T(P[p + ".g"]), T(P[p + ".b"]), eps=1e-5)
 
@@ -477,7 +484,7 @@ def test_seq2seq_mirror_rounding_points(s2s, monkeypatch):
         for l in range(cfg["enc_layers"]):
             p = f"enc{l}"
             qkv = rb(lin(m, p + ".wqkv", p + ".bqkv"))
-            a = mha(qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:], False)
+            a = mha_enc(qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:])
             m = ln(lin(a, p + ".wo", p + ".bo") + m, p + ".ln1")
             h = rb(F.relu(lin(m, p + ".w1", p + ".b1")))
             m = ln(lin(h, p + ".w2", p + ".b2") + m, p + ".ln2")

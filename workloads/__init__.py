@@ -282,6 +282,58 @@ def skipnet_r38_weights(seed: int = WEIGHT_SEED, calib=None) -> dict:
 
 
 # ----------------------------------------------------------------------------
+# SkipNet with the recurrent gate (Table 3 ID 5 "ResNet38 + RNN"; reading R19):
+# the config-3 trunk, per-gate projections proj_i (C_i -> RNN_IN, N(0, 1/C_i), bf16) feeding one
+# shared LSTM cell (hidden RNN_HIDDEN, torch.nn.LSTMCell's U(-1/sqrt(H), 1/sqrt(H)) init, fp32),
+# and a raw output vector w_out ~ N(0, 1/H); per-gate calibration (oracle/calibrate.py) gives
+# out_i.w = s_i w_out, out_i.b = -s_i a_i (a_i = median, s_i = 2/std of the raw w_out . h).
+# ----------------------------------------------------------------------------
+RNN_IN = 10
+RNN_HIDDEN = 10
+
+
+def skipnet_rnn_r38_raw(seed: int = WEIGHT_SEED) -> dict:
+    rng = np.random.default_rng([seed, 3000])
+    out = {}
+    for i in SKIP_GATED:
+        c = R38.block_io(i)[0]
+        out[f"proj{i}.w"] = rng.standard_normal((RNN_IN, c)) / math.sqrt(c)
+        out[f"proj{i}.b"] = rng.uniform(-0.05, 0.05, RNN_IN)
+    k = 1.0 / math.sqrt(RNN_HIDDEN)
+    H4 = 4 * RNN_HIDDEN
+    out["rnn.w_ih"] = rng.uniform(-k, k, (H4, RNN_IN))
+    out["rnn.w_hh"] = rng.uniform(-k, k, (H4, RNN_HIDDEN))
+    out["rnn.b_ih"] = rng.uniform(-k, k, H4)
+    out["rnn.b_hh"] = rng.uniform(-k, k, H4)
+    out["w_out"] = rng.standard_normal(RNN_HIDDEN) / math.sqrt(RNN_HIDDEN)
+    out["final"] = rng.standard_normal((NUM_CLASSES, 64)) / math.sqrt(64)
+    return out
+
+
+def skipnet_rnn_r38_weights(seed: int = WEIGHT_SEED, calib=None) -> dict:
+    """SkipNet-style ResNet-38 with 17 recurrent (LSTM) gates on blocks 2..18."""
+    W, _ = resnet_cifar_trunk(R38, seed)
+    if calib is None:
+        calib = load_calib("cfg3r")
+    raw = skipnet_rnn_r38_raw(seed)
+    for i in SKIP_GATED:
+        W[f"proj{i}.w"] = _bf16(raw[f"proj{i}.w"])
+        W[f"proj{i}.b"] = raw[f"proj{i}.b"].astype(np.float32)
+        s, a = (calib[f"gate{i}"]["scale"], calib[f"gate{i}"]["median"]) if calib is not None else (1.0, 0.0)
+        W[f"out{i}.w"] = (s * raw["w_out"]).astype(np.float32)
+        W[f"out{i}.b"] = np.array([-s * a], dtype=np.float32)
+    for k in ("rnn.w_ih", "rnn.w_hh", "rnn.b_ih", "rnn.b_hh"):
+        W[k] = raw[k].astype(np.float32)
+    W["rnn.n_in"] = np.int32(RNN_IN)
+    W["rnn.hidden"] = np.int32(RNN_HIDDEN)
+    fin = raw["final"]
+    mu = np.array(calib["final"]["mu"]) if calib is not None else np.zeros(64)
+    W["final.w"], W["final.b"] = _centered_head(fin, 4.0, mu)
+    W["thr"] = np.float32(0.5)
+    return W
+
+
+# ----------------------------------------------------------------------------
 # Config 5: early-exit ResNet-50 v1.5 (torchvision topology, BN folded into biases).
 # ----------------------------------------------------------------------------
 R50_LAYERS = (3, 4, 6, 3)
