@@ -159,6 +159,25 @@ dycl_status dycl_exit(dycl_graph g, dycl_node head_subnet, float tau);
  * two join shapes accepted, else DYCL_E_SHAPE_JOIN). */
 dycl_status dycl_gate(dycl_graph g, dycl_node gate_subnet, float thr, dycl_node then_subnet);
 
+/* Recurrent conditional skip (SkipNet's RNN gate: Table 3 ID 5 "ResNet38 + RNN", PAPER.md L812;
+ * Table 1).  One LSTM cell per graph, shared by every dycl_gate_rnn node and carrying a
+ * per-sample state (h, c) across the gates in program order (zero at the start of a run):
+ *   dycl_rnn_cell: hidden H <= 16, input width n_in <= 16; fp32 host weights (copied)
+ *     w_ih [4H][n_in], w_hh [4H][H], b_ih [4H], b_hh [4H], gate rows in the order i, f, g, o
+ *     (torch.nn.LSTMCell): (i,f,g,o) = (sig, sig, tanh, sig)(w_ih u + b_ih + w_hh h + b_hh);
+ *     c <- f*c + i*g;  h <- o*tanh(c).
+ *   dycl_gate_rnn: u = proj_subnet(h_act) (fp32 [n_in], e.g. GAP + dense(out_fp32)); the cell
+ *     steps on u; z = w_out . h + b_out (w_out fp32 [H], copied); samples with sigmoid(z) > thr
+ *     run then_subnet and set their path bit, as dycl_gate.  The cell steps for EVERY live sample
+ *     at every gate, executed or not (the gate reads the block input).
+ * Errors: dycl_rnn_cell twice or after a dycl_gate_rnn -> STATE; dycl_gate_rnn before
+ * dycl_rnn_cell -> STATE; sizes out of range -> INVALID_ARG; proj_subnet output width != n_in
+ * -> SHAPE_MISMATCH (at dycl_finalize).  A graph with recurrent gates never rebalances. */
+dycl_status dycl_rnn_cell(dycl_graph g, int n_in, int hidden, const float* w_ih, const float* w_hh,
+                          const float* b_ih, const float* b_hh);
+dycl_status dycl_gate_rnn(dycl_graph g, dycl_node proj_subnet, const float* w_out, float b_out, float thr,
+                          dycl_node then_subnet);
+
 /* Default exit: every sample still running terminates with z = head(h).
  * path = number of exits registered (early-exit nets) or the gate mask. */
 dycl_status dycl_final(dycl_graph g, dycl_node head_subnet);

@@ -54,6 +54,9 @@ struct Layer {
   int s4d = 0;
   int pool_s2d = 0;           // maxpool reading that phase layout (3x3 / stride 2 / pad 1)
   uint16_t* d_wt = nullptr;   // wide fp32 heads (K >= 128): weights transposed [C][K] for the batched FC
+  uint16_t* d_w2 = nullptr;   // wide fp32 heads on the tensor cores: [W | W] [kpad][2C] (split-bf16 GEMM)
+  float* d_b2 = nullptr;      // bias padded to kpad
+  int kpad = 0;
   // NHWC bottleneck: this 1x1 conv and the projection shortcut before it run as ONE GEMM over
   // K-concatenated operands [t | x] with weights [W | W_proj] and bias b + b_proj
   int fuse_proj = 0;
@@ -78,6 +81,12 @@ struct Node {
   int ordinal = 0;            // exit index / gate index
   int skip_mode = 0;          // gate: 0 identity, 1 option A
   Shape in, out;
+  // recurrent gate (dycl_gate_rnn): the proj subnet yields the cell input u; the graph's LSTM cell
+  // steps on it; z = w_out . h + b_out
+  int rnn = 0;
+  std::vector<float> w_out;
+  float b_out = 0.f;
+  float* d_w_out = nullptr;
 };
 
 struct Launch {               // profiling record
@@ -100,6 +109,11 @@ struct dycl_graph_s {
   int K = 0;
   int n_exits = 0, n_gates = 0;
   std::string err;
+  // the recurrent gates' shared LSTM cell (dycl_rnn_cell) and its per-sample state [max_batch][2H]
+  int rnn_in = 0, rnn_hidden = 0;
+  std::vector<float> rnn_w;            // w_ih [4H][n_in] | w_hh [4H][H] | b_ih [4H] | b_hh [4H]
+  float* d_rnn_w = nullptr;
+  float* d_rnn_state = nullptr;
   // device workspace
   static constexpr int NBUF = 6;
   static constexpr int NBUF32 = 4;
@@ -109,6 +123,7 @@ struct dycl_graph_s {
   int conv_path = 0;                 // 0 auto; DYCL_CONV_PATH=1 forces the cp.async kernel
   int conv_dbg = 0;                  // DYCL_CONV_DBG: timing experiments only (results invalid)
   int no_fuse = 0;                   // DYCL_NO_FUSE=1: run basic blocks as two conv launches
+  int head_cuda_core = 0;            // DYCL_HEAD_CUDA_CORE=1: wide-head FC on CUDA cores (k_head_fc), not tcgen05
   int max_fuse = dycl::MAX_FUSED_BLOCKS;   // DYCL_MAX_FUSE: basic blocks per fused launch (1..8)
   int no_inplace = 0;                // DYCL_NO_INPLACE=1: gates gather / merge instead of running in place
   int no_zero_copy = 0;              // DYCL_NO_ZERO_COPY=1: exits gather survivors even before a fused block
@@ -145,7 +160,8 @@ struct dycl_graph_s {
   float* d_pred = nullptr;
   float* d_z = nullptr;
   float* d_gpool = nullptr;         // pooled features of wide heads [max_batch][max head C]
-  long long* d_gap_part = nullptr;  // conv_gemm fused-GAP partials (int64 fixed point) (sub-network outputs read by a head)
+  uint16_t* d_a2 = nullptr;         // their split bf16 pairs [max_batch][2 * max head C] (tensor-core heads)
+  float* d_gap_part = nullptr;      // conv_gemm fused-GAP partials [rows / G][C] fp32 (sub-network outputs read by a head)
   float* d_gap_pooled = nullptr;    // their reduction [max_batch][C]
   float* d_pool32[NBUF32] = {};     // fused-GAP features per fp32 stream buffer [max_batch][<= 32] (fused blocks)
   float* d_in_stage = nullptr;      // dycl_run_host staging
@@ -207,6 +223,14 @@ dycl_status dmalloc(dycl_graph g, T** p, size_t bytes) {
   cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), bytes);
   if (e != cudaSuccess) return fail(g, DYCL_E_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
   return DYCL_OK;
+}
+
+// Fused-GAP row group: the largest power of two <= 32 dividing the per-sample pixel count
+// (a group then never straddles samples; see ConvArgs::gap_g).
+int gap_group(int hw) {
+  int G = 32;
+  while (G > 1 && hw % G) G >>= 1;
+  return G;
 }
 
 // Shape propagation through one subnet (Alg. 2 line: "compile N with the shape of
@@ -387,6 +411,22 @@ dycl_status upload_subnet(dycl_graph g, Subnet& s) {
           for (int c = 0; c < Cin; ++c) wt[(size_t)c * L.cout + o] = L.w[(size_t)o * Cin + c];
         if ((st = dmalloc(g, &L.d_wt, wt.size() * 2))) return st;
         CK(cudaMemcpy(L.d_wt, wt.data(), wt.size() * 2, cudaMemcpyHostToDevice));
+        if (L.out_fp32 && Cp % 32 == 0 && !g->head_cuda_core) {
+          // tensor-core head: W2 = [W | W] with N padded to a multiple of 128 (zero rows)
+          L.kpad = (L.cout + 127) / 128 * 128;
+          std::vector<uint16_t> w2((size_t)L.kpad * 2 * Cp, 0);
+          for (int o = 0; o < L.cout; ++o)
+            for (int c = 0; c < Cin; ++c) {
+              w2[(size_t)o * 2 * Cp + c] = L.w[(size_t)o * Cin + c];
+              w2[(size_t)o * 2 * Cp + Cp + c] = L.w[(size_t)o * Cin + c];
+            }
+          std::vector<float> b2(L.kpad, 0.0f);
+          for (int o = 0; o < L.cout && o < (int)L.b.size(); ++o) b2[o] = L.b[o];
+          if ((st = dmalloc(g, &L.d_w2, w2.size() * 2))) return st;
+          CK(cudaMemcpy(L.d_w2, w2.data(), w2.size() * 2, cudaMemcpyHostToDevice));
+          if ((st = dmalloc(g, &L.d_b2, b2.size() * 4))) return st;
+          CK(cudaMemcpy(L.d_b2, b2.data(), b2.size() * 4, cudaMemcpyHostToDevice));
+        }
       }
     }
     if (!L.b.empty()) {
@@ -669,9 +709,14 @@ struct Exec {
       const double row_f = 2.0 * L.out.H * L.out.W * L.out.C * (double)(L.k * L.k * L.in.C) + fused_f;
       // (only for wide rows: below ~128 KB of fp32 per sample the head's own GAP pass is cheaper)
       const bool gap = want_gap && last && g->d_gap_part && a.y32 && a.nhwc && a.in_nhwc && !a.rows_out &&
+                       gap_group(L.out.H * L.out.W) >= 4 &&
                        L.out.H * L.out.W >= 32 && 4.0 * L.out.row_elems() >= 128 * 1024 &&
                        dycl::conv_gemm_eligible(a);
-      if (gap) a.gap_part = g->d_gap_part;
+      const int gap_g = gap_group(L.out.H * L.out.W);
+      if (gap) {
+        a.gap_part = g->d_gap_part;
+        a.gap_g = gap_g;
+      }
       ++conv_launch;
       if (g->dbg_ts_conv && g->dbg_ts_conv == conv_launch) a.ts = g->dbg_ts;
       prof_begin(DYCL_K_CONV, cnt, row_b, row_f, 2.0 * L.out.C * L.Kp);
@@ -679,8 +724,8 @@ struct Exec {
       prof_end();
       if (e != cudaSuccess) return cuda_fail(g, e, "launch_conv_tc");
       if (gap) {
-        prof_begin(DYCL_K_HEAD, cnt, 4.0 * ((L.out.H * L.out.W + 31) / 32 + 1) * L.out.C + 4.0 * L.out.C, 0, 0);
-        e = dycl::launch_gap_reduce(g->d_gap_part, g->d_gap_pooled, cnt, batch, L.out.H * L.out.W, L.out.C, st);
+        prof_begin(DYCL_K_HEAD, cnt, 4.0 * (L.out.H * L.out.W / gap_g) * L.out.C + 4.0 * L.out.C, 0, 0);
+        e = dycl::launch_gap_reduce(g->d_gap_part, gap_g, g->d_gap_pooled, cnt, batch, L.out.H * L.out.W, L.out.C, st);
         prof_end();
         if (e != cudaSuccess) return cuda_fail(g, e, "launch_gap_reduce");
         gap_f = o.f;
@@ -716,7 +761,14 @@ struct Exec {
     if (D.d_wt && kind != 1 && g->d_gpool) {
       a.wt = D.d_wt;
       a.gpool = g->d_gpool;
+      if (D.d_w2 && g->d_a2) {
+        a.w2 = D.d_w2;
+        a.b2 = D.d_b2;
+        a.a2 = g->d_a2;
+        a.kpad = D.kpad;
+      }
     }
+    a.num_sms = g->num_sms;
     if (in.f >= 0 && in.f == gap_f && g->d_gap_pooled) a.pooled = g->d_gap_pooled;   // GAP fused into the producer
     prof_begin(DYCL_K_HEAD, cnt, (a.h32 ? 4.0 : 2.0) * s.in.row_elems() + 4.0 * D.cout + 1,
                2.0 * D.cout * s.in.C + s.in.row_elems(), 2.0 * D.cout * a.C);
@@ -786,6 +838,10 @@ struct Exec {
     cudaError_t e = dycl::launch_init(g->d_counts, own, g->d_orig[0], out_path, out_margin, batch, st);
     prof_end();
     if (e != cudaSuccess) return cuda_fail(g, e, "launch_init");
+    if (g->d_rnn_state) {
+      e = cudaMemsetAsync(g->d_rnn_state, 0, (size_t)batch * 2 * g->rnn_hidden * sizeof(float), st);
+      if (e != cudaSuccess) return cuda_fail(g, e, "rnn state reset");
+    }
     const Shape& in = g->input;
     prof_begin(DYCL_K_INPUT, nullptr, 0, 0, (double)batch * in.H * in.W * (4.0 * in.C + 2.0 * in.Cp()));
     e = own == 0 ? cudaSuccess
@@ -846,7 +902,33 @@ struct Exec {
           break;
         }
         case N_GATE: {
-          if ((r = head(g->subnets[N.sn], cur, cnt, 1, N.thr))) return r;
+          if (N.rnn) {
+            // u = proj(h) into d_z (no predicate), then the shared LSTM cell steps on u for every
+            // live row (state indexed by the row's original sample), z = w_out . h, sigmoid > thr
+            if ((r = head(g->subnets[N.sn], cur, cnt, 2, 0.f))) return r;
+            dycl::RnnGateArgs ra{};
+            ra.u = g->d_z;
+            ra.u_stride = std::max(g->K, 1);
+            ra.orig = g->d_orig[orig_cur];
+            ra.state = g->d_rnn_state;
+            ra.w = g->d_rnn_w;
+            ra.w_out = N.d_w_out;
+            ra.b_out = N.b_out;
+            ra.n_in = g->rnn_in;
+            ra.hidden = g->rnn_hidden;
+            ra.thr = N.thr;
+            ra.flag = g->d_flag;
+            ra.pred = g->d_pred;
+            ra.n_live = cnt;
+            const double H4 = 4.0 * g->rnn_hidden;
+            prof_begin(DYCL_K_HEAD, cnt, 4.0 * g->rnn_in + 2 * 8.0 * g->rnn_hidden + 5.0,
+                       2.0 * H4 * (g->rnn_in + g->rnn_hidden) + 2.0 * g->rnn_hidden, 0);
+            cudaError_t e = dycl::launch_rnn_gate(ra, batch, g->num_sms, st);
+            prof_end();
+            if (e != cudaSuccess) return cuda_fail(g, e, "launch_rnn_gate");
+          } else if ((r = head(g->subnets[N.sn], cur, cnt, 1, N.thr))) {
+            return r;
+          }
           int s;
           if ((r = compact(cnt, 1, (int32_t)1 << N.ordinal, orig_cur, &s, true, N.thr))) return r;
           const Subnet& T = g->subnets[N.then_sn];
@@ -979,7 +1061,7 @@ struct Exec {
   long long sent_used = 0;
 
   bool rebalance_here(int exit_ordinal) const {
-    return g->tr && exit_ordinal < 31 && (g->rb_policy >> exit_ordinal) & 1;
+    return g->tr && !g->rnn_hidden && exit_ordinal < 31 && (g->rb_policy >> exit_ordinal) & 1;
   }
 
   // After an exit: the survivors sit dense in rows [0, s) of t.  All ranks agree on the counts
@@ -1113,6 +1195,7 @@ dycl_status dycl_graph_create(int cuda_device, int in_h, int in_w, int in_c, dyc
   if (const char* cp = getenv("DYCL_CONV_PATH")) g->conv_path = atoi(cp);
   if (const char* cd = getenv("DYCL_CONV_DBG")) g->conv_dbg = atoi(cd);
   if (const char* nf = getenv("DYCL_NO_FUSE")) g->no_fuse = atoi(nf);
+  if (const char* hc = getenv("DYCL_HEAD_CUDA_CORE")) g->head_cuda_core = atoi(hc);
   if (const char* mf = getenv("DYCL_MAX_FUSE")) g->max_fuse = atoi(mf);
   if (const char* ni = getenv("DYCL_NO_INPLACE")) g->no_inplace = atoi(ni);
   if (const char* nz = getenv("DYCL_NO_ZERO_COPY")) g->no_zero_copy = atoi(nz);
@@ -1146,6 +1229,8 @@ dycl_status dycl_graph_destroy(dycl_graph g) {
       cudaFree(L.d_w);
       cudaFree(L.d_wrt);
       cudaFree(L.d_wt);
+      cudaFree(L.d_w2);
+      cudaFree(L.d_b2);
       cudaFree(L.d_wcat);
       cudaFree(L.d_bcat);
       cudaFree(L.d_b);
@@ -1161,6 +1246,10 @@ dycl_status dycl_graph_destroy(dycl_graph g) {
   cudaFree(g->d_pred);
   cudaFree(g->d_z);
   cudaFree(g->d_gpool);
+  cudaFree(g->d_a2);
+  cudaFree(g->d_rnn_w);
+  cudaFree(g->d_rnn_state);
+  for (Node& N : g->nodes) cudaFree(N.d_w_out);
   cudaFree(g->d_gap_part);
   cudaFree(g->d_gap_pooled);
   for (auto* p : g->d_pool32) cudaFree(p);
@@ -1348,6 +1437,42 @@ dycl_status dycl_gate(dycl_graph g, dycl_node gate_subnet, float thr, dycl_node 
   return s;
 }
 
+dycl_status dycl_rnn_cell(dycl_graph g, int n_in, int hidden, const float* w_ih, const float* w_hh,
+                          const float* b_ih, const float* b_hh) {
+  if (!g) return DYCL_E_INVALID_ARG;
+  if (g->finalized) return fail(g, DYCL_E_STATE, "graph already finalized");
+  if (g->rnn_hidden) return fail(g, DYCL_E_STATE, "the graph already has an RNN cell");
+  if (n_in < 1 || n_in > 16 || hidden < 1 || hidden > 16 || !w_ih || !w_hh || !b_ih || !b_hh)
+    return fail(g, DYCL_E_INVALID_ARG, "rnn cell: 1 <= n_in, hidden <= 16, non-null weights");
+  const size_t H4 = 4 * (size_t)hidden;
+  g->rnn_w.assign(w_ih, w_ih + H4 * n_in);
+  g->rnn_w.insert(g->rnn_w.end(), w_hh, w_hh + H4 * hidden);
+  g->rnn_w.insert(g->rnn_w.end(), b_ih, b_ih + H4);
+  g->rnn_w.insert(g->rnn_w.end(), b_hh, b_hh + H4);
+  g->rnn_in = n_in;
+  g->rnn_hidden = hidden;
+  return DYCL_OK;
+}
+
+dycl_status dycl_gate_rnn(dycl_graph g, dycl_node proj_subnet, const float* w_out, float b_out, float thr,
+                          dycl_node then_subnet) {
+  if (!g) return DYCL_E_INVALID_ARG;
+  if (!g->rnn_hidden) return fail(g, DYCL_E_STATE, "dycl_gate_rnn before dycl_rnn_cell");
+  if (!w_out) return fail(g, DYCL_E_INVALID_ARG, "null w_out");
+  Node N{};
+  N.kind = N_GATE;
+  N.sn = proj_subnet;
+  N.then_sn = then_subnet;
+  N.thr = thr;
+  N.rnn = 1;
+  N.w_out.assign(w_out, w_out + g->rnn_hidden);
+  N.b_out = b_out;
+  if (g->n_gates >= 31) return fail(g, DYCL_E_UNSUPPORTED, "at most 31 gates (path word bits)");
+  dycl_status s = add_node(g, N, true);
+  if (s == DYCL_OK) g->nodes.back().ordinal = g->n_gates++;
+  return s;
+}
+
 dycl_status dycl_final(dycl_graph g, dycl_node head_subnet) {
   Node N{};
   N.kind = N_FINAL;
@@ -1399,7 +1524,9 @@ dycl_status dycl_finalize(dycl_graph g, int64_t max_batch) {
       if (!S.is_head) return fail(g, DYCL_E_SHAPE_MISMATCH, "exit/gate/final need a [gap] + dense(out_fp32) head");
       if (S.in.Cp() % 8 || S.in.Cp() / 8 > 256) return fail(g, DYCL_E_UNSUPPORTED, "head input channels");
       if (N.kind == N_GATE) {
-        if (S.head_K != 1) return fail(g, DYCL_E_SIGNATURE, "gate head must produce one logit");
+        if (N.rnn ? S.head_K != g->rnn_in : S.head_K != 1)
+          return fail(g, N.rnn ? DYCL_E_SHAPE_MISMATCH : DYCL_E_SIGNATURE,
+                      N.rnn ? "rnn gate: proj output width != the cell's n_in" : "gate head must produce one logit");
         if ((s = plan(N.then_sn, cur))) return s;
         const Subnet& T = g->subnets[N.then_sn];
         if (T.is_head) return fail(g, DYCL_E_UNSUPPORTED, "gate then-branch is a head");
@@ -1488,7 +1615,18 @@ dycl_status dycl_finalize(dycl_graph g, int64_t max_batch) {
   if (dycl_status s = dmalloc(g, &g->d_list0, nb * 4)) return s;
   if (dycl_status s = dmalloc(g, &g->d_flag, nb)) return s;
   if (dycl_status s = dmalloc(g, &g->d_pred, nb * 4)) return s;
+  if (g->rnn_hidden && g->K < g->rnn_in) return fail(g, DYCL_E_UNSUPPORTED, "rnn cell n_in exceeds the head width K");
   if (dycl_status s = dmalloc(g, &g->d_z, nb * (size_t)std::max(g->K, 1) * 4)) return s;
+  if (g->rnn_hidden) {
+    if (dycl_status s = dmalloc(g, &g->d_rnn_w, g->rnn_w.size() * 4)) return s;
+    CK(cudaMemcpy(g->d_rnn_w, g->rnn_w.data(), g->rnn_w.size() * 4, cudaMemcpyHostToDevice));
+    if (dycl_status s = dmalloc(g, &g->d_rnn_state, nb * 2 * g->rnn_hidden * 4)) return s;
+    for (Node& N : g->nodes)
+      if (N.rnn) {
+        if (dycl_status s = dmalloc(g, &N.d_w_out, N.w_out.size() * 4)) return s;
+        CK(cudaMemcpy(N.d_w_out, N.w_out.data(), N.w_out.size() * 4, cudaMemcpyHostToDevice));
+      }
+  }
   if (g->precision == DYCL_PREC_FP32_STREAM) {
     bool fused_any = false;
     for (size_t i = 0; i < g->subnets.size(); ++i)
@@ -1505,6 +1643,8 @@ dycl_status dycl_finalize(dycl_graph g, int64_t max_batch) {
       if (N.kind != N_SEQ && g->subnets[N.sn].layers.back().d_wt) cmax = std::max(cmax, g->subnets[N.sn].in.Cp());
     if (cmax > 0)
       if (dycl_status s = dmalloc(g, &g->d_gpool, nb * (size_t)cmax * 4)) return s;
+    if (cmax > 0 && !g->head_cuda_core)
+      if (dycl_status s = dmalloc(g, &g->d_a2, nb * (size_t)cmax * 2 * 2)) return s;
   }
   {
     // conv_gemm fused GAP: the last conv of a sub-network that feeds an exit / final head
@@ -1516,12 +1656,14 @@ dycl_status dycl_finalize(dycl_graph g, int64_t max_batch) {
       if (S.layers.empty() || S.layers.back().kind != L_CONV) continue;
       const Layer& L = S.layers.back();
       const int hw = L.out.H * L.out.W;
-      if (!g->nhwc || L.out.C % 64 || L.in.Cp() % 64 || hw < 32 || 4.0 * L.out.row_elems() < 128 * 1024) continue;
-      part = std::max(part, ((size_t)nb * hw / 32 + 2) * 2 * L.out.C);
+      if (!g->nhwc || L.out.C % 64 || L.in.Cp() % 64 || hw < 32 || 4.0 * L.out.row_elems() < 128 * 1024 ||
+          gap_group(hw) < 4)
+        continue;
+      part = std::max(part, (size_t)nb * (hw / gap_group(hw)) * L.out.C);
       pooled = std::max(pooled, (size_t)nb * L.out.C);
     }
     if (part && !getenv("DYCL_NO_CONV_GAP")) {
-      if (dycl_status s = dmalloc(g, &g->d_gap_part, part * 8)) return s;
+      if (dycl_status s = dmalloc(g, &g->d_gap_part, part * 4)) return s;
       if (dycl_status s = dmalloc(g, &g->d_gap_pooled, pooled * 4)) return s;
     }
   }

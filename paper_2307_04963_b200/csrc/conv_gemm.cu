@@ -29,6 +29,7 @@
 namespace dycl {
 namespace {
 
+
 constexpr int BM = 128;
 constexpr int BKE = 64;                 // K elements per stage: one 128-byte swizzle row
 constexpr int THREADS = 384;   // warps 0-7 epilogue, 8/10/11 TMA producers, 9 MMA
@@ -468,30 +469,33 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (staged && a.gap_part) {
           // fused GAP (a2): the chunk's fp32 y goes through the SMEM staging in every tile (the
           // ragged last one included); thread (quarter q, column cc) sums rows 32q..32q+31 of
-          // its column in order, split at a sample boundary, into the row group's partials
-          // [rg][slot][Cout] (slot 1 = the second sample of a straddling group)
+          // its column in order, in groups of G rows, into the partials [M / G][Cout]
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             *reinterpret_cast<float4*>(eO32 + sw128(r, j)) = make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
           wg_sync(wg);
           {
+            // fp32 sums over G-row groups (G = the largest power of two <= 32 dividing HW): every
+            // group lies inside one sample and covers the same pixels p in [kG, (k+1)G) whatever
+            // the sample's batch position, and is summed in ascending row order -- so the pooled
+            // features are batch-position independent without integer arithmetic
             const int cc = lane, q = quad;
+            const int G = a.gap_g;
             const long long ra = m0 + 32 * q;                  // first row of this quarter
-            const long long na = ra / HWo;
-            const long long rb = (na + 1) * HWo;              // first row of the next sample
-            long long s0 = 0, s1 = 0;                         // fixed point x 2^32 (kernels.h)
-#pragma unroll 8
+            // all 32 loads first (independent of the partial stores below), then the sums
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              v[i] = *reinterpret_cast<const float*>(eO32 + sw128(32 * q + i, cc >> 2) + (cc & 3) * 4);
+            float* gp = a.gap_part + (size_t)(ra / G) * a.Cout + col0 + c0 + cc;
+            float sacc = 0.f;
+#pragma unroll
             for (int i = 0; i < 32; ++i) {
-              const long long mm = ra + i;
-              if (mm >= M) break;
-              const float v = *reinterpret_cast<const float*>(eO32 + sw128(32 * q + i, cc >> 2) + (cc & 3) * 4);
-              const long long iv = __double2ll_rn((double)v * 4294967296.0);
-              if (mm < rb) s0 += iv; else s1 += iv;
-            }
-            if (ra < M) {
-              const size_t pbase = (size_t)(ra >> 5) * 2 * a.Cout + col0 + c0 + cc;
-              a.gap_part[pbase] = s0;
-              if (rb < ra + 32 && rb < M) a.gap_part[pbase + a.Cout] = s1;
+              sacc += v[i];
+              if (((i + 1) & (G - 1)) == 0) {             // a group never straddles M (G | HW)
+                if (ra + i < M) gp[(size_t)(i / G) * a.Cout] = sacc;
+                sacc = 0.f;
+              }
             }
           }
         }

@@ -130,9 +130,12 @@ __device__ __forceinline__ void conv_finish16(const ConvArgs& a, int n, int ho, 
                                      : a.y + (size_t)n * a.Cout * HWo + (size_t)((o0 >> 3) + h) * HWo * 8 + pix * 8) = o;
   }
   if (a.y32) {
-    float4* yq = reinterpret_cast<float4*>(a.y32 + ((size_t)n * HWo + pix) * a.Cout + o0);
+    const size_t ld = a.y32_ld ? (size_t)a.y32_ld : (size_t)a.Cout;
+    const int nv = a.y32_n ? a.y32_n : a.Cout;
+    float4* yq = reinterpret_cast<float4*>(a.y32 + ((size_t)n * HWo + pix) * ld + o0);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) yq[j] = make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
+    for (int j = 0; j < 4; ++j)
+      if (o0 + 4 * j < nv) yq[j] = make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
   }
 }
 

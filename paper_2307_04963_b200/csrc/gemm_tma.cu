@@ -151,6 +151,40 @@ __global__ void __launch_bounds__(THREADS, 1)
       ptx::mbar_wait(tfull0 + 8 * acc, (it >> 1) & 1);
       ptx::tc_fence_after();
       const uint32_t t_base = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN);
+      if (a.am_val) {
+        // fused argmax: (acc + bias) [+ guard bias on the EOS column], ascending scan, strict '>'
+        // keeps the lowest index among equal maxima (reading R11)
+        float gb = 0.f;
+        if (m < M) gb = a.g_beta * ((float)(a.g_t + 1) - a.g_len[a.g_src[(size_t)a.g_slot[m] * a.g_S]]);
+        float best = -INFINITY;
+        int bi = 0x7fffffff;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          uint32_t v[16];
+          ptx::tmem_ld_32x32b_x16(t_base + (uint32_t)c0, v);
+          ptx::tmem_ld_wait();
+          const int col0 = n_tile * BN + c0;
+          float bq[16];
+#pragma unroll
+          for (int q = 0; q < 16; q += 4) {
+            const float4 b4 = __ldg(reinterpret_cast<const float4*>(a.bias + col0 + q));
+            bq[q] = b4.x; bq[q + 1] = b4.y; bq[q + 2] = b4.z; bq[q + 3] = b4.w;
+          }
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            float z = __uint_as_float(v[q]) + bq[q];
+            if (col0 + q == a.g_eos) z += gb;
+            if (z > best) {
+              best = z;
+              bi = col0 + q;
+            }
+          }
+        }
+        if (m < M) {
+          a.am_val[(size_t)m * n_tiles + n_tile] = best;
+          a.am_idx[(size_t)m * n_tiles + n_tile] = bi;
+        }
+      } else {
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 16) {
         uint32_t v[16];
@@ -162,6 +196,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int q = 0; q < 16; ++q) f[q] = __uint_as_float(v[q]);
           conv_finish16(a, m, 0, 0, n_tile * BN + c0, f);
         }
+      }
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(tempty0 + 8 * acc);
@@ -228,12 +263,20 @@ bool gemm_tma_eligible(const ConvArgs& a) {
          a.Kp == a.K && (a.Cout % 64 == 0) && a.res_mode != 2;
 }
 
+int gemm_tma_bn(const ConvArgs& a, int max_rows, int num_sms) {
+  const long long m_tiles = (max_rows + BM - 1) / BM;
+  if (a.Cout % 256 == 0 && m_tiles * (a.Cout / 256) >= num_sms / 2) return 256;
+  if (a.Cout % 128 == 0 && m_tiles * (a.Cout / 128) >= num_sms / 2) return 128;
+  return 64;
+}
+
 cudaError_t launch_gemm_tma(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream) {
   // 256-wide N tiles unless they leave more than half of the SMs idle (small-M decode GEMMs)
-  const long long m_tiles = (max_rows + BM - 1) / BM;
-  if (a.Cout % 256 == 0 && m_tiles * (a.Cout / 256) >= num_sms / 2) return launch_bn<256>(a, max_rows, num_sms, stream);
-  if (a.Cout % 128 == 0 && m_tiles * (a.Cout / 128) >= num_sms / 2) return launch_bn<128>(a, max_rows, num_sms, stream);
-  return launch_bn<64>(a, max_rows, num_sms, stream);   // small M, narrow N: twice the CTAs
+  switch (gemm_tma_bn(a, max_rows, num_sms)) {
+    case 256: return launch_bn<256>(a, max_rows, num_sms, stream);
+    case 128: return launch_bn<128>(a, max_rows, num_sms, stream);
+    default: return launch_bn<64>(a, max_rows, num_sms, stream);   // small M, narrow N: twice the CTAs
+  }
 }
 
 }  // namespace dycl

@@ -13,6 +13,7 @@
 #include <map>
 #include <mutex>
 
+#include "epilogue.cuh"
 #include "kernels.h"
 #include "ptx.cuh"
 
@@ -294,6 +295,85 @@ __global__ void k_head_pred(const HeadArgs a) {
     }
   }
 }
+
+// Wide head operand: pooled fp32 features [n][C] -> the split bf16 pair [hi | lo] per row
+// ([n][2C]; hi = bf16_rn(g), lo = bf16_rn(g - hi)), the A operand of the tensor-core head GEMM.
+__global__ void k_pool_split(const float* __restrict__ g, uint16_t* __restrict__ a2, const int* n_live, int C) {
+  const int n = *n_live;
+  const int C4 = C >> 2;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)n * C4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long row = i / C4;
+    const int c = (int)(i - row * C4) * 4;
+    const float4 v = __ldg(reinterpret_cast<const float4*>(g + row * C + c));
+    const uint32_t h01 = pack_bf16x2_rn(v.x, v.y), h23 = pack_bf16x2_rn(v.z, v.w);
+    const uint32_t l01 = pack_bf16x2_rn(v.x - __uint_as_float(h01 << 16), v.y - __uint_as_float(h01 & 0xFFFF0000u));
+    const uint32_t l23 = pack_bf16x2_rn(v.z - __uint_as_float(h23 << 16), v.w - __uint_as_float(h23 & 0xFFFF0000u));
+    uint16_t* r = a2 + row * 2 * C;
+    *reinterpret_cast<uint2*>(r + c) = make_uint2(h01, h23);
+    *reinterpret_cast<uint2*>(r + C + c) = make_uint2(l01, l23);
+  }
+}
+
+// Recurrent gate: one warp per live row.  Lane j < 4H (two passes of 32 lanes) computes the
+// pre-activation of gate row j in a fixed order (b_ih + b_hh, then w_ih . u ascending, then
+// w_hh . h ascending); lanes k < H then update c_k, h_k from rows (k, H+k, 2H+k, 3H+k).
+__global__ void k_rnn_gate(const RnnGateArgs a) {
+  const int n_live = *a.n_live;
+  const int lane = threadIdx.x & 31;
+  const int H = a.hidden, NI = a.n_in, H4 = 4 * H;
+  const float* w_ih = a.w;
+  const float* w_hh = w_ih + (size_t)H4 * NI;
+  const float* b_ih = w_hh + (size_t)H4 * H;
+  const float* b_hh = b_ih + H4;
+  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < n_live; row += (gridDim.x * blockDim.x) >> 5) {
+    float* st = a.state + (size_t)a.orig[row] * 2 * H;
+    const float uv = lane < NI ? a.u[(size_t)row * a.u_stride + lane] : 0.f;
+    const float hv = lane < H ? st[lane] : 0.f;
+    const float cv = lane < H ? st[H + lane] : 0.f;
+    float pre[2];
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass) {
+      const int j = lane + 32 * pass;
+      float acc = 0.f;
+      if (j < H4) acc = b_ih[j] + b_hh[j];
+      for (int k = 0; k < NI; ++k) {
+        const float uk = __shfl_sync(0xffffffffu, uv, k);
+        if (j < H4) acc = fmaf(w_ih[(size_t)j * NI + k], uk, acc);
+      }
+      for (int k = 0; k < H; ++k) {
+        const float hk = __shfl_sync(0xffffffffu, hv, k);
+        if (j < H4) acc = fmaf(w_hh[(size_t)j * H + k], hk, acc);
+      }
+      pre[pass] = acc;
+    }
+    // gate row j lives in lane j % 32 of pass j / 32
+    auto fetch = [&](int j) {
+      const float v0 = __shfl_sync(0xffffffffu, pre[0], j & 31);
+      const float v1 = __shfl_sync(0xffffffffu, pre[1], j & 31);
+      return j < 32 ? v0 : v1;
+    };
+    const int k = lane < H ? lane : 0;
+    const float gi = fetch(k), gf = fetch(H + k), gg = fetch(2 * H + k), go = fetch(3 * H + k);
+    const float i_ = 1.f / (1.f + expf(-gi)), f_ = 1.f / (1.f + expf(-gf));
+    const float g_ = tanhf(gg), o_ = 1.f / (1.f + expf(-go));
+    const float c2 = f_ * cv + i_ * g_;
+    const float h2 = o_ * tanhf(c2);
+    float zc = lane < H ? a.w_out[lane] * h2 : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) zc += __shfl_xor_sync(0xffffffffu, zc, o);
+    if (lane < H) {
+      st[lane] = h2;
+      st[H + lane] = c2;
+    }
+    if (lane == 0) {
+      const float p = 1.0f / (1.0f + expf(-(zc + a.b_out)));
+      a.flag[row] = p > a.thr ? 1 : 0;           // reading R2: p > thr executes
+      if (a.pred) a.pred[row] = p;
+    }
+  }
+}
+
 
 // ------------------------------------------------------------ a4 compaction
 constexpr int CMP_THREADS = 1024;
@@ -645,31 +725,30 @@ __global__ void k_cast_s4d(const float* __restrict__ in, uint16_t* __restrict__ 
   }
 }
 
-__global__ void k_gap_reduce(const long long* __restrict__ part, float* __restrict__ pooled, const int* n_live,
+__global__ void k_gap_reduce(const float* __restrict__ part, int G, float* __restrict__ pooled, const int* n_live,
                              int HW, int C) {
   const int n_rows = *n_live;
   const int64_t total = (int64_t)n_rows * C;
+  const int ng = HW / G;
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total; u += (int64_t)gridDim.x * blockDim.x) {
     const int64_t n = u / C;
     const int c = (int)(u - n * C);
-    const int64_t r0 = n * HW, r1 = r0 + HW - 1;
-    long long sum = 0;                               // exact: order and grouping free
-    for (int64_t rg = r0 >> 5; rg <= (r1 >> 5); ++rg) {
-      const int slot = (rg << 5) < r0 ? 1 : 0;        // group starts in the previous sample
-      sum += part[(rg * 2 + slot) * C + c];
-    }
-    pooled[n * C + c] = (float)((double)sum * (1.0 / 4294967296.0) / (double)HW);
+    const float* p = part + (size_t)n * ng * C + c;
+    float sum = 0.f;                                 // fixed order: groups k = 0, 1, ... of sample n
+    for (int k = 0; k < ng; ++k) sum += p[(size_t)k * C];
+    pooled[n * C + c] = sum / (float)HW;
   }
 }
 
 }  // namespace
 
-cudaError_t launch_gap_reduce(const long long* gap_part, float* pooled, const int* n_live, int max_rows, int HW, int C,
+cudaError_t launch_gap_reduce(const float* gap_part, int G, float* pooled, const int* n_live, int max_rows, int HW, int C,
                               cudaStream_t s) {
+  if (G < 1 || HW % G) return cudaErrorInvalidValue;
   int64_t blocks = ((int64_t)max_rows * C + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-  k_gap_reduce<<<(int)blocks, 256, 0, s>>>(gap_part, pooled, n_live, HW, C);
+  k_gap_reduce<<<(int)blocks, 256, 0, s>>>(gap_part, G, pooled, n_live, HW, C);
   return cudaGetLastError();
 }
 
@@ -717,8 +796,47 @@ cudaError_t launch_init(int* counts, int n, int* orig, int32_t* path, float* mar
   return cudaGetLastError();
 }
 
+// Wide head FC on tcgen05 (k_gemm_tma over the split pair), then the predicate.
+static cudaError_t head_fc_tc(const HeadArgs& a, const float* pooled, int max_rows, cudaStream_t s) {
+  int gs = (int)(((long long)max_rows * (a.C / 4) + 255) / 256);
+  if (gs > a.num_sms * 8) gs = a.num_sms * 8;
+  if (gs < 1) gs = 1;
+  k_pool_split<<<gs, 256, 0, s>>>(pooled, a.a2, a.n_live, a.C);
+  ConvArgs g{};
+  g.x = a.a2;
+  g.w = a.w2;
+  g.bias = a.b2;
+  g.y = nullptr;
+  g.y32 = a.z;
+  g.y32_ld = a.K;
+  g.y32_n = a.K;
+  g.n_live = a.n_live;
+  g.H = g.W = g.Ho = g.Wo = 1;
+  g.C = g.K = g.Kp = 2 * a.C;
+  g.Cout = a.kpad;
+  g.ksz = 1; g.stride = 1; g.pad = 0;
+  g.nhwc = g.in_nhwc = 1;
+  if (!gemm_tma_eligible(g)) return cudaErrorInvalidValue;
+  if (cudaError_t e = launch_gemm_tma(g, max_rows, a.num_sms, s)) return e;
+  int gp = (max_rows + 7) / 8;
+  if (gp > a.num_sms * 8) gp = a.num_sms * 8;
+  if (gp < 1) gp = 1;
+  k_head_pred<<<gp, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_head(const HeadArgs& a, int max_rows, cudaStream_t s) {
   if (a.C % 8 != 0 || a.C / 8 > HEAD_THREADS) return cudaErrorInvalidValue;
+  if (a.w2 && a.kind != 1) {                     // wide head, FC on the tensor cores
+    if (a.pooled) return head_fc_tc(a, a.pooled, max_rows, s);
+    if (!a.gpool || !a.wt) return cudaErrorInvalidValue;
+    const size_t smem = (HEAD_THREADS * 8 + a.C + a.K) * sizeof(float);
+    if (cudaError_t e = ensure_smem(k_head, smem)) return e;
+    int grid = max_rows < a.num_sms * 8 ? max_rows : a.num_sms * 8;
+    if (grid < 1) grid = 1;
+    k_head<<<grid, HEAD_THREADS, smem, s>>>(a);   // GAP only (a.wt set): pooled -> gpool
+    return head_fc_tc(a, a.gpool, max_rows, s);
+  }
   if (a.pooled && a.wt) {                        // wide head on pooled features: FC + predicate only
     HeadArgs b = a;
     b.gpool = const_cast<float*>(a.pooled);
@@ -760,6 +878,15 @@ cudaError_t launch_head(const HeadArgs& a, int max_rows, cudaStream_t s) {
   if (gp > 148 * 8) gp = 148 * 8;
   if (gp < 1) gp = 1;
   k_head_pred<<<gp, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rnn_gate(const RnnGateArgs& a, int max_rows, int num_sms, cudaStream_t s) {
+  if (a.hidden < 1 || a.hidden > 16 || a.n_in < 1 || a.n_in > 16) return cudaErrorInvalidValue;
+  int grid = (max_rows + 7) / 8;
+  if (grid > num_sms * 8) grid = num_sms * 8;
+  if (grid < 1) grid = 1;
+  k_rnn_gate<<<grid, 256, 0, s>>>(a);
   return cudaGetLastError();
 }
 

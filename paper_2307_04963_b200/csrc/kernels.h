@@ -41,15 +41,30 @@ struct ConvArgs {
   // rows_out[i] -- the in-place form of a gate's then-branch; nullptr = dense order
   const int* rows_in = nullptr;
   const int* rows_out = nullptr;
-  // conv_gemm only (staged epilogue): fused GAP partials [ceil(M/32)][2][Cout] -- per
-  // 32-row group of the flat output, the column sums of y for the group's first sample (slot 0)
-  // and, when the group straddles a sample boundary, the second (slot 1); see launch_gap_reduce
-  // int64 fixed point (value x 2^32, llrint): integer sums are exact, so the pooled features do
-  // not depend on where a sample's rows fall in the 32-row groups (batch-position independence)
-  long long* gap_part = nullptr;
+  // conv_gemm only (staged epilogue): fused GAP partials [M / gap_g][Cout] fp32 -- per group of
+  // gap_g consecutive output rows (gap_g = the largest power of two <= 32 dividing Ho*Wo, so a
+  // group never straddles samples and always covers the same pixels of its sample), the column
+  // sums of y in ascending row order; see launch_gap_reduce
+  float* gap_part = nullptr;
+  int gap_g = 32;
   // dense rows only (Ho = Wo = 1): write y as a split pair [hi | lo] per row (row stride 2*Cout,
   // hi = bf16(v), lo = bf16(v - hi)) -- the operand format of the BF16X3 parity mode
   int split = 0;
+  // dense rows only: fp32 output y32 with row stride y32_ld (0 = Cout) and only its first y32_n
+  // columns stored (0 = all; a multiple of 4) -- the wide heads' padded-N GEMM writes the K
+  // logits straight into the [rows][K] logit buffer
+  int y32_ld = 0, y32_n = 0;
+  // gemm_tma only: fused LM-head argmax.  Instead of storing y, each
+  // epilogue thread scans its row's BN columns of the tile in ascending order (after bias, plus
+  // the loop guard's EOS bias g_beta * (g_t + 1 - g_len[g_src[g_slot[m] * g_S]]) on column g_eos)
+  // and writes the tile's (max, lowest index of the max) to am_val / am_idx [rows][Cout / BN]
+  float* am_val = nullptr;
+  int* am_idx = nullptr;
+  const int32_t* g_slot = nullptr;
+  const int32_t* g_src = nullptr;
+  const float* g_len = nullptr;
+  float g_beta = 0.f;
+  int g_t = 0, g_S = 0, g_eos = -1;
   long long* ts = nullptr;   // development: conv_gemm phase timestamps (DYCL_TS_CONV)
   int dbg = 0;           // bit5 (32): row-tap mode opt-in; experiments only (results invalid): bit0 skip
                          // epilogue math/stores, bit1 skip MMAs, bit2 skip A loads, bit3 no residual prefetch.
@@ -115,6 +130,8 @@ cudaError_t launch_conv_tma(const ConvArgs& a, int max_rows, int num_sms, cudaSt
 // Dense-layer GEMM on tcgen05 with TMA SWIZZLE_128B tiles (gemm_tma.cu): [rows][K] x [N][K].
 bool gemm_tma_eligible(const ConvArgs& a);
 cudaError_t launch_gemm_tma(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream);
+// N tile width launch_gemm_tma picks for these arguments (64, 128 or 256).
+int gemm_tma_bn(const ConvArgs& a, int max_rows, int num_sms);
 // NHWC implicit-GEMM conv with TMA im2col operand loads (conv_gemm.cu): C % 64 == 0, Cout % 64 == 0.
 bool conv_gemm_eligible(const ConvArgs& a);
 cudaError_t launch_conv_gemm(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream);
@@ -125,9 +142,9 @@ cudaError_t launch_conv(const ConvArgs& a, int max_rows, int num_sms, cudaStream
 cudaError_t launch_cast_pad(const float* in, uint16_t* out, int64_t n, int hw, int c, int cp,
                             cudaStream_t s);
 
-// pooled[n][c] = (sum over the 32-row groups of sample n of gap_part[group][slot][c]) / HW,
-// fixed order (the second half of conv_gemm's fused GAP)
-cudaError_t launch_gap_reduce(const long long* gap_part, float* pooled, const int* n_live, int max_rows, int HW, int C,
+// pooled[n][c] = (sum over the HW / G row groups k = 0.. of sample n of gap_part[n*HW/G + k][c],
+// in ascending k) / HW -- a fixed order, independent of the sample's batch position.
+cudaError_t launch_gap_reduce(const float* gap_part, int G, float* pooled, const int* n_live, int max_rows, int HW, int C,
                               cudaStream_t s);
 
 // a0 for a space-to-depth stem: fp32 NHWC [n][H][W][c] -> bf16 [n][H/4][W/4][64], channel
@@ -167,8 +184,36 @@ struct HeadArgs {
   const float* pooled = nullptr;  // fp32 [rows][C] pooled features already computed (fused GAP): skip the GAP
   float* pooled_out = nullptr;    // fp32 [rows][C]: keep the GAP this kernel computes (later in-place gates reuse it)
   float* gpool = nullptr;         // fp32 [rows][C] pooled-feature scratch for the batched FC
+  // wide heads on the tensor cores (a2): the fp32 pooled features are split into a bf16 pair
+  // [hi | lo] per row (a2, [rows][2C]) and multiplied with w2 = [W | W] ([kpad][2C], rows >= K
+  // zero) by the tcgen05 GEMM -- the split-bf16 product, fp32-accurate (|rel err| ~ 2^-16)
+  // because the weights are exact bf16 -- writing the K logits to z; b2 = bias padded to kpad
+  const uint16_t* w2 = nullptr;
+  const float* b2 = nullptr;
+  uint16_t* a2 = nullptr;
+  int kpad = 0, num_sms = 148;
 };
 cudaError_t launch_head(const HeadArgs& a, int max_rows, cudaStream_t s);
+
+// Recurrent gate (SkipNet RNN gate): per live row r, u = u[r][0..n_in) (the proj head's fp32
+// output), state = state[orig[r]] (h [H] then c [H], fp32); LSTM cell step (torch gate order
+// i, f, g, o; w = w_ih [4H][n_in] | w_hh [4H][H] | b_ih [4H] | b_hh [4H]); the new state is
+// written back; z = w_out . h + b_out, p = sigmoid(z), flag = p > thr, pred = p.  Warp per row.
+struct RnnGateArgs {
+  const float* u;
+  int u_stride;
+  const int* orig;
+  float* state;
+  const float* w;
+  const float* w_out;
+  float b_out;
+  int n_in, hidden;
+  float thr;
+  uint8_t* flag;
+  float* pred;
+  const int* n_live;
+};
+cudaError_t launch_rnn_gate(const RnnGateArgs& a, int max_rows, int num_sms, cudaStream_t s);
 
 // Stable partition of the live rows by flag (single CTA, deterministic):
 //   rows with flag==1 -> list1 (in order), count -> counts_out[0]

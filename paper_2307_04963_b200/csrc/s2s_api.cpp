@@ -56,6 +56,9 @@ struct dycl_s2s_s {
   bool use_graph = true;             // DYCL_S2S_GRAPH=0 disables
   bool pdl = true;                   // programmatic dependent launch in the run (DYCL_S2S_PDL=0 disables)
   int gemm_path = 0;                 // 0: k_gemm_tma, 1: k_conv_gemm (DYCL_S2S_GEMM=1; measured equal or slower)
+  bool fuse_argmax = true;           // LM-head argmax in the GEMM epilogue (DYCL_S2S_FUSE_ARGMAX=0 disables)
+  float* am_val = nullptr;           // fused argmax partials [max_batch][vocab / 64]
+  int* am_idx = nullptr;
   // DYCL_PREC_BF16X3_PARITY: every bf16 tensor is a split pair [hi | lo] and every GEMM runs
   // on K-concatenated operands [A_hi | A_lo] x [W | W] (weights are exact bf16, so the
   // W_lo terms of the 3-pass product vanish): fp32-accurate products on the tensor cores
@@ -165,8 +168,10 @@ struct S2SExec {
   // y = act(x W^T + b [+ res]) on rows [0, *cnt) through the tcgen05 GEMM path (a dense
   // layer = 1x1 conv on [rows][1][1][K]).
   cudaError_t gemm(const uint16_t* x, int K, const uint16_t* w, const float* b, int N, const float* res32,
-                   uint16_t* yb, float* y32, int relu, const int* cnt, int n_static, int max_rows) {
+                   uint16_t* yb, float* y32, int relu, const int* cnt, int n_static, int max_rows,
+                   const dycl::ConvArgs* argmax = nullptr) {
     dycl::ConvArgs a{};
+    if (argmax) a = *argmax;           // the fused-argmax fields (LM head)
     if (s->pair) {                     // [A_hi | A_lo] x [W | W], bf16 outputs written as pairs
       K *= 2;
       a.split = yb != nullptr;
@@ -178,9 +183,10 @@ struct S2SExec {
     a.rH = a.rW = 1; a.rC = N;
     a.nhwc = a.in_nhwc = s->gemm_path;             // [rows][K] is NHWC at 1x1: the im2col-GEMM kernel
     ++n;
-    pb(DYCL_K_GEMM, cnt, n_static, 2.0 * K + (yb ? 2.0 * N : 0.0) + (y32 ? 4.0 * N : 0.0) + (res32 ? 4.0 * N : 0.0),
-       2.0 * K * N, 2.0 * K * N);
-    const cudaError_t e = dycl::launch_conv(a, max_rows, s->num_sms, st, 0);
+    pb(DYCL_K_GEMM, cnt, n_static, 2.0 * K + (yb ? 2.0 * N : 0.0) + (y32 ? 4.0 * N : 0.0) + (res32 ? 4.0 * N : 0.0) +
+       (argmax ? 8.0 * N / dycl::gemm_tma_bn(a, max_rows, s->num_sms) : 0.0), 2.0 * K * N, 2.0 * K * N);
+    const cudaError_t e = argmax ? dycl::launch_gemm_tma(a, max_rows, s->num_sms, st)
+                                 : dycl::launch_conv(a, max_rows, s->num_sms, st, 0);
     pe();
     return e;
   }
@@ -277,11 +283,27 @@ struct S2SExec {
         E(gemm(s->h, c.d_ff, L.w2, L.b2, d, s->x32, nullptr, s->pre, 0, cnt, 0, B));
         E(ln(s->pre, L.lfg, L.lfb, cnt, 0, B));
       }
-      E(gemm(s->xb, d, s->lm_w, s->lm_b, c.vocab, nullptr, nullptr, s->logits, 0, cnt, 0, B));
       dycl::S2SArgmaxArgs ga{s->logits, slot, src, s->len_table, s->beta, tokens, top1, logits0,
                              s->cur_tok, lengths, s->flag, cnt, c.vocab, S, c.max_len, t, c.eos};
-      pb(DYCL_K_ARGMAX, cnt, 0, 4.0 * c.vocab + 16.0, 2.0 * c.vocab, 0);
-      E(dycl::launch_argmax_guard(ga, B, st));
+      if (s->fuse_argmax && !(logits0 && t == 0)) {
+        // LM head with the guard + argmax in its epilogue: per (row, N tile) the max and its
+        // lowest index; the [rows][V] fp32 logits never reach HBM
+        dycl::ConvArgs am{};
+        am.am_val = s->am_val; am.am_idx = s->am_idx;
+        am.g_slot = slot; am.g_src = src; am.g_len = s->len_table; am.g_beta = s->beta;
+        am.g_t = t; am.g_S = S; am.g_eos = c.eos;
+        E(gemm(s->xb, d, s->lm_w, s->lm_b, c.vocab, nullptr, nullptr, nullptr, 0, cnt, 0, B, &am));
+        dycl::ConvArgs probe{};
+        probe.Cout = c.vocab;
+        ga.am_val = s->am_val; ga.am_idx = s->am_idx;
+        ga.ntiles = c.vocab / dycl::gemm_tma_bn(probe, B, s->num_sms);
+        pb(DYCL_K_ARGMAX, cnt, 0, 8.0 * ga.ntiles + 16.0, 0, 0);
+        E(dycl::launch_argmax_final(ga, B, st));
+      } else {
+        E(gemm(s->xb, d, s->lm_w, s->lm_b, c.vocab, nullptr, nullptr, s->logits, 0, cnt, 0, B));
+        pb(DYCL_K_ARGMAX, cnt, 0, 4.0 * c.vocab + 16.0, 2.0 * c.vocab, 0);
+        E(dycl::launch_argmax_guard(ga, B, st));
+      }
       pe();
       ++n;
       // the logic node's decision -> stable compaction of the still-active sequences
@@ -324,6 +346,7 @@ dycl_status dycl_s2s_create(int cuda_device, const dycl_s2s_config* cfg, dycl_s2
   if (const char* eg = getenv("DYCL_S2S_GRAPH")) s->use_graph = atoi(eg) != 0;
   if (const char* gp = getenv("DYCL_S2S_GEMM")) s->gemm_path = atoi(gp);
   if (const char* pp = getenv("DYCL_S2S_PDL")) s->pdl = atoi(pp) != 0;
+  if (const char* fa = getenv("DYCL_S2S_FUSE_ARGMAX")) s->fuse_argmax = atoi(fa) != 0;
   cudaSetDevice(cuda_device);
   cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
   *out = s;
@@ -429,7 +452,8 @@ dycl_status dycl_s2s_finalize(dycl_s2s s, int64_t max_batch) {
   }
   if ((r = alloc(s, &s->x32, R * d)) || (r = alloc(s, &s->pre, R * d)) || (r = alloc(s, &s->xb, R * d * P)) ||
       (r = alloc(s, &s->qkv, R * 3 * d * P)) || (r = alloc(s, &s->att, R * d * P)) ||
-      (r = alloc(s, &s->h, R * (size_t)s->c.d_ff * P)) || (r = alloc(s, &s->logits, B * (size_t)s->c.vocab)) ||
+      (r = alloc(s, &s->h, R * (size_t)s->c.d_ff * P)) || (r = alloc(s, &s->logits, B * (size_t)s->c.vocab)) || (r = alloc(s, &s->am_val, B * (size_t)(s->c.vocab / 64))) ||
+      (r = alloc(s, &s->am_idx, B * (size_t)(s->c.vocab / 64))) ||
       (r = alloc(s, &s->cur_tok, B)) || (r = alloc(s, &s->active[0], B)) || (r = alloc(s, &s->active[1], B)) ||
       (r = alloc(s, &s->list1, B)) || (r = alloc(s, &s->list0, B)) || (r = alloc(s, &s->counts, 2 * L + 2)) ||
       (r = alloc(s, &s->flag, B)))

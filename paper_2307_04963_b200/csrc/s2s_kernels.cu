@@ -7,6 +7,9 @@
 // All reductions are fixed-order warp trees (batch-position independent).
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
+#include "epilogue.cuh"
 #include "kernels.h"
 #include "ptx.cuh"
 #include "s2s_kernels.h"
@@ -177,6 +180,187 @@ __global__ void __launch_bounds__(128) k_attn_encoder(const S2SAttnArgs a) {
       out[lane + 32] = to_bf(o1);
     }
     __syncwarp();
+  }
+}
+
+// Encoder self-attention on tcgen05: one CTA per (sequence, head pair), S <= 64
+// tokens, head dim 64.  The two heads are stacked along M so every MMA is a full 128-row tile:
+//   S = [Q_h0; Q_h1] x [K_h0; K_h1]^T    (M = N = 128, K = 64; only the two diagonal 64 x 64
+//                                         blocks are used)
+//   O = P x [V_h0; V_h1]                 (M = 128, N = 64, K = 128; P block-diagonal: row r of
+//                                         head h has its 64 probabilities in key block h, zeros
+//                                         in the other -- the rows' own head's values only)
+// Operands sit in SMEM in the K-major 128-byte-swizzle layout the MMA reads (written by the
+// threads from 16-byte global loads; V is transposed on the way in so it is K-major in keys);
+// S and O accumulate in TMEM (fp32).  Softmax: thread r owns row r (its TMEM lane), fp32,
+// p = exp(s - max) / sum rounded to bf16 -- the tensor-core operand (oracle mirror mode rounds
+// the encoder's P there too, R18); O is rounded to bf16 on the way out.
+namespace enc_tc {
+constexpr int THREADS = 128;
+constexpr int Q_OFF = 0, K_OFF = 16384, VT_OFF = 32768, P_OFF = 49152;   // bytes, 1024-aligned
+constexpr int SMEM = 1024 + 81920 + 64;
+// byte offset of 16-byte chunk c (0..7) of row r in a K-major SW128 block of 128-byte rows
+__device__ __forceinline__ uint32_t sw128(int r, int c) {
+  return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4));
+}
+}  // namespace enc_tc
+
+__global__ void __launch_bounds__(enc_tc::THREADS) k_attn_encoder_tc(const S2SAttnArgs a) {
+  using namespace enc_tc;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + 81920);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+  const int t = threadIdx.x, warp = t >> 5;
+  const int npair = a.heads >> 1;
+  const int b = blockIdx.x / npair, h0 = 2 * (blockIdx.x % npair);
+  const uint32_t bar0 = ptx::smem_u32(bars), bar1 = bar0 + 8;
+  if (t == 0) {
+    ptx::mbar_init(bar0, 1);
+    ptx::mbar_init(bar1, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 0) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), 256);
+  ptx::pdl_wait();      // PDL (kernels.h): before any read of predecessor output / early return
+  ptx::pdl_trigger();
+  const int n_seq = a.n_live ? *a.n_live : a.n_static;
+  const bool live = b < n_seq;
+  const int S = a.S, d = a.d;
+  const int rs = 3 * d;
+  const uint16_t* base = a.qkv + (size_t)b * S * rs;
+  if (live) {
+    // Q and K: row r = (head r / 64, token r % 64); 8 chunks of 16 B per row
+    for (int i = t; i < 2 * 128 * 8; i += THREADS) {
+      const int which = i >> 10, r = (i >> 3) & 127, c = i & 7;
+      const int hh = h0 + (r >> 6), tok = r & 63;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (tok < S) v = __ldg(reinterpret_cast<const uint4*>(base + (size_t)tok * rs + which * d + hh * 64 + c * 8));
+      *reinterpret_cast<uint4*>(sm + (which ? K_OFF : Q_OFF) + sw128(r, c)) = v;
+    }
+    // V^T: B operand [dim n][key k], key block kb = head (keys 0..63 of head h0, then h1).
+    // Thread: key pair (2p, 2p+1) of one head, 32 of the 64 dims; one 32-bit store per dim.
+    for (int i = t; i < 2 * 32 * 2; i += THREADS) {
+      const int hb = i >> 6, p = (i >> 1) & 31, half = i & 1;
+      const int k0 = 2 * p;
+      uint32_t w0[16], w1[16];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 v0 = make_uint4(0, 0, 0, 0), v1 = make_uint4(0, 0, 0, 0);
+        const size_t col = 2 * d + (h0 + hb) * 64 + half * 32 + q * 8;
+        if (k0 < S) v0 = __ldg(reinterpret_cast<const uint4*>(base + (size_t)k0 * rs + col));
+        if (k0 + 1 < S) v1 = __ldg(reinterpret_cast<const uint4*>(base + (size_t)(k0 + 1) * rs + col));
+        w0[4 * q] = v0.x; w0[4 * q + 1] = v0.y; w0[4 * q + 2] = v0.z; w0[4 * q + 3] = v0.w;
+        w1[4 * q] = v1.x; w1[4 * q + 1] = v1.y; w1[4 * q + 2] = v1.z; w1[4 * q + 3] = v1.w;
+      }
+      uint8_t* vt = sm + VT_OFF + hb * 8192;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const uint32_t e0 = (j & 1) ? (w0[j >> 1] >> 16) : (w0[j >> 1] & 0xFFFFu);
+        const uint32_t e1 = (j & 1) ? (w1[j >> 1] >> 16) : (w1[j >> 1] & 0xFFFFu);
+        const int n = half * 32 + j;
+        *reinterpret_cast<uint32_t*>(vt + sw128(n, k0 >> 3) + (k0 & 7) * 2) = e0 | (e1 << 16);
+      }
+    }
+  }
+  ptx::fence_proxy_async_smem();       // generic-proxy SMEM writes -> visible to the tensor core
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (live) {
+    if (warp == 0) {
+      constexpr uint32_t ID_S = ptx::make_idesc_bf16(128, 128);
+      const uint64_t qd = ptx::make_smem_desc_sw128(ptx::smem_u32(sm + Q_OFF));
+      const uint64_t kd = ptx::make_smem_desc_sw128(ptx::smem_u32(sm + K_OFF));
+#pragma unroll
+      for (int j = 0; j < 4; ++j) ptx::mma_bf16_ss_elect(tmem, qd + 2 * j, kd + 2 * j, ID_S, j != 0);
+      ptx::mma_commit_elect(bar0);
+      __syncwarp();
+    }
+    // softmax of row t (head t / 64, query token t % 64) over its head's S keys
+    ptx::mbar_wait(bar0, 0);
+    ptx::tc_fence_after();
+    const int hb = t >> 6;
+    float sc[64];
+#pragma unroll
+    for (int c0 = 0; c0 < 64; c0 += 16) {
+      uint32_t v[16];
+      ptx::tmem_ld_32x32b_x16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(hb * 64 + c0), v);
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 16; ++q) sc[c0 + q] = __uint_as_float(v[q]) * 0.125f;   // 1/sqrt(64)
+    }
+    float m = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 64; ++j)
+      if (j < S) m = fmaxf(m, sc[j]);
+    float sum = 0.f;
+#pragma unroll
+    for (int j = 0; j < 64; ++j) {
+      sc[j] = j < S ? expf(sc[j] - m) : 0.f;
+      sum += sc[j];
+    }
+    const float inv = 1.f / sum;
+    uint8_t* prow = sm + P_OFF;
+#pragma unroll
+    for (int kb = 0; kb < 2; ++kb) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint4 o = make_uint4(0, 0, 0, 0);
+        if (kb == hb) {
+          o.x = pack_bf16x2_rn(sc[8 * c] * inv, sc[8 * c + 1] * inv);
+          o.y = pack_bf16x2_rn(sc[8 * c + 2] * inv, sc[8 * c + 3] * inv);
+          o.z = pack_bf16x2_rn(sc[8 * c + 4] * inv, sc[8 * c + 5] * inv);
+          o.w = pack_bf16x2_rn(sc[8 * c + 6] * inv, sc[8 * c + 7] * inv);
+        }
+        *reinterpret_cast<uint4*>(prow + kb * 16384 + sw128(t, c)) = o;
+      }
+    }
+    ptx::fence_proxy_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (warp == 0) {
+      constexpr uint32_t ID_O = ptx::make_idesc_bf16(128, 64);
+#pragma unroll
+      for (int kb = 0; kb < 2; ++kb) {
+        const uint64_t pd = ptx::make_smem_desc_sw128(ptx::smem_u32(sm + P_OFF + kb * 16384));
+        const uint64_t vd = ptx::make_smem_desc_sw128(ptx::smem_u32(sm + VT_OFF + kb * 8192));
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ptx::mma_bf16_ss_elect(tmem + 128, pd + 2 * j, vd + 2 * j, ID_O, (kb | j) != 0);
+      }
+      ptx::mma_commit_elect(bar1);
+      __syncwarp();
+    }
+    ptx::mbar_wait(bar1, 0);
+    ptx::tc_fence_after();
+    const int tok = t & 63;
+    uint16_t* out = a.out + ((size_t)b * S + tok) * d + (h0 + hb) * 64;
+#pragma unroll
+    for (int c0 = 0; c0 < 64; c0 += 16) {
+      uint32_t v[16];
+      ptx::tmem_ld_32x32b_x16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(128 + c0), v);
+      ptx::tmem_ld_wait();
+      if (tok < S) {
+        uint4 o0, o1;
+        o0.x = pack_bf16x2_rn(__uint_as_float(v[0]), __uint_as_float(v[1]));
+        o0.y = pack_bf16x2_rn(__uint_as_float(v[2]), __uint_as_float(v[3]));
+        o0.z = pack_bf16x2_rn(__uint_as_float(v[4]), __uint_as_float(v[5]));
+        o0.w = pack_bf16x2_rn(__uint_as_float(v[6]), __uint_as_float(v[7]));
+        o1.x = pack_bf16x2_rn(__uint_as_float(v[8]), __uint_as_float(v[9]));
+        o1.y = pack_bf16x2_rn(__uint_as_float(v[10]), __uint_as_float(v[11]));
+        o1.z = pack_bf16x2_rn(__uint_as_float(v[12]), __uint_as_float(v[13]));
+        o1.w = pack_bf16x2_rn(__uint_as_float(v[14]), __uint_as_float(v[15]));
+        *reinterpret_cast<uint4*>(out + c0) = o0;
+        *reinterpret_cast<uint4*>(out + c0 + 8) = o1;
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 256);
   }
 }
 
@@ -397,6 +581,46 @@ __global__ void __launch_bounds__(256) k_argmax_guard(const S2SArgmaxArgs a) {
   }
 }
 
+// Guard decision from the LM-head GEMM's fused partials: the row's argmax over its ntiles
+// (max, lowest index) pairs, ties to the lowest index (R11) -- the same token / top-1 value as
+// k_argmax_guard over the full logits row.  One warp per row.
+__global__ void __launch_bounds__(256) k_argmax_final(const S2SArgmaxArgs a) {
+  ptx::pdl_wait();      // PDL (kernels.h): before any read of predecessor output / early return
+  ptx::pdl_trigger();
+  const int n = *a.n_live;
+  const int lane = threadIdx.x & 31;
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= n) return;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int j = lane; j < a.ntiles; j += 32) {
+    const float v = a.am_val[(size_t)row * a.ntiles + j];
+    const int i = a.am_idx[(size_t)row * a.ntiles + j];
+    if (v > best || (v == best && i < bi)) {
+      best = v;
+      bi = i;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    const int slot = a.slot[row];
+    a.tokens[(size_t)slot * a.max_len + a.t] = bi;
+    if (a.top1) a.top1[(size_t)slot * a.max_len + a.t] = best;
+    a.cur_tok[slot] = bi;
+    const bool done = bi == a.eos;
+    if (done) a.lengths[slot] = a.t + 1;
+    a.flag[row] = done ? 1 : 0;
+  }
+}
+
 // run start: tokens = PAD, lengths = max_len, top1 = NaN, cur_tok = BOS, active = iota, count.
 __global__ void k_s2s_init(S2SInitArgs a) {
   ptx::pdl_wait();      // PDL (kernels.h): before any read of predecessor output / early return
@@ -427,6 +651,12 @@ cudaError_t launch_layernorm(const S2SLnArgs& a, int max_rows, cudaStream_t s) {
 }
 cudaError_t launch_attn_encoder(const S2SAttnArgs& a, int max_seqs, cudaStream_t s) {
   if (a.S > 64 || a.d / a.heads != 64) return cudaErrorInvalidValue;
+  static const bool cuda_core = getenv("DYCL_ENC_ATTN_CC") != nullptr;   // A/B timing of the old kernel
+  if (!a.pair && a.heads % 2 == 0 && !cuda_core) {
+    if (cudaError_t e = ensure_smem(k_attn_encoder_tc, enc_tc::SMEM)) return e;
+    const int grid = max_seqs * (a.heads / 2);
+    return launch_k(k_attn_encoder_tc, dim3(grid > 0 ? grid : 1), dim3(enc_tc::THREADS), enc_tc::SMEM, s, a);
+  }
   return launch_k(k_attn_encoder, dim3(max_seqs * a.heads > 0 ? max_seqs * a.heads : 1), dim3(128), 0, s, a);
 }
 cudaError_t launch_attn_decoder(const S2SAttnArgs& a, int max_rows, cudaStream_t s) {
@@ -437,6 +667,10 @@ cudaError_t launch_attn_decoder(const S2SAttnArgs& a, int max_rows, cudaStream_t
 }
 cudaError_t launch_argmax_guard(const S2SArgmaxArgs& a, int max_rows, cudaStream_t s) {
   return launch_k(k_argmax_guard, dim3(max_rows > 0 ? max_rows : 1), dim3(256), 0, s, a);
+}
+cudaError_t launch_argmax_final(const S2SArgmaxArgs& a, int max_rows, cudaStream_t s) {
+  const int blocks = (max_rows + 7) / 8;
+  return launch_k(k_argmax_final, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, s, a);
 }
 cudaError_t launch_s2s_init(const S2SInitArgs& a, cudaStream_t s) {
   return launch_k(k_s2s_init, dim3((a.B + 255) / 256 > 0 ? (a.B + 255) / 256 : 1), dim3(256), 0, s, a);

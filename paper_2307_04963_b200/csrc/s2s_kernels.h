@@ -57,6 +57,10 @@ struct S2SArgmaxArgs {
   uint8_t* flag;           // [rows] 1 = finished this step
   const int* n_live;
   int V, S, max_len, t, eos;
+  // fused LM-head argmax: per-(row, N tile) partial maxima and their indices [rows][ntiles]
+  const float* am_val = nullptr;
+  const int* am_idx = nullptr;
+  int ntiles = 0;
 };
 struct S2SInitArgs {
   int32_t* tokens;
@@ -73,6 +77,8 @@ cudaError_t launch_layernorm(const S2SLnArgs& a, int max_rows, cudaStream_t s);
 cudaError_t launch_attn_encoder(const S2SAttnArgs& a, int max_seqs, cudaStream_t s);
 cudaError_t launch_attn_decoder(const S2SAttnArgs& a, int max_rows, cudaStream_t s);
 cudaError_t launch_argmax_guard(const S2SArgmaxArgs& a, int max_rows, cudaStream_t s);
+// the guard's decision from the fused LM-head partials (a.am_val / a.am_idx): one warp per row
+cudaError_t launch_argmax_final(const S2SArgmaxArgs& a, int max_rows, cudaStream_t s);
 cudaError_t launch_s2s_init(const S2SInitArgs& a, cudaStream_t s);
 
 }  // namespace dycl

@@ -60,7 +60,7 @@ EXPORTS = [
     "dycl_s2s_set_profiling", "dycl_s2s_profile_read",
     "dycl_graph_create", "dycl_graph_set_precision", "dycl_graph_destroy", "dycl_last_error", "dycl_subnet_begin", "dycl_subnet_block_begin",
     "dycl_subnet_conv2d", "dycl_subnet_dense", "dycl_subnet_gap", "dycl_subnet_projection", "dycl_subnet_maxpool", "dycl_subnet_end", "dycl_seq", "dycl_exit",
-    "dycl_gate", "dycl_final", "dycl_finalize", "dycl_run", "dycl_run_host", "dycl_num_count_slots",
+    "dycl_gate", "dycl_rnn_cell", "dycl_gate_rnn", "dycl_final", "dycl_finalize", "dycl_run", "dycl_run_host", "dycl_num_count_slots",
     "dycl_launches_per_run", "dycl_num_classes", "dycl_set_profiling", "dycl_profile_read",
     "dycl_debug_conv2d", "dycl_rebalance_plan", "dycl_debug_timestamps",
     "dycl_run_host_ex", "dycl_set_comm", "dycl_local_group_create", "dycl_local_group_destroy",
@@ -96,6 +96,8 @@ def lib():
             "dycl_seq": [vp, i32],
             "dycl_exit": [vp, i32, f32],
             "dycl_gate": [vp, i32, f32, i32],
+            "dycl_rnn_cell": [vp, i32, i32, Pf, Pf, Pf, Pf],
+            "dycl_gate_rnn": [vp, i32, Pf, f32, f32, i32],
             "dycl_final": [vp, i32],
             "dycl_finalize": [vp, i64],
             "dycl_run": [vp, ctypes.POINTER(dycl_io), vp],
@@ -243,6 +245,19 @@ def dycl_exit(g, head_sn, tau):
 
 def dycl_gate(g, gate_sn, thr, then_sn):
     _ck(lib().dycl_gate(g, gate_sn, float(thr), then_sn), g)
+
+
+def dycl_rnn_cell(g, n_in, hidden, w_ih, w_hh, b_ih, b_hh):
+    a, pa = _f32(w_ih)
+    b, pb = _f32(w_hh)
+    c, pc = _f32(b_ih)
+    d, pd = _f32(b_hh)
+    _ck(lib().dycl_rnn_cell(g, n_in, hidden, pa, pb, pc, pd), g)
+
+
+def dycl_gate_rnn(g, proj_sn, w_out, b_out, thr, then_sn):
+    a, pa = _f32(w_out)
+    _ck(lib().dycl_gate_rnn(g, proj_sn, pa, float(b_out), float(thr), then_sn), g)
 
 
 def dycl_final(g, head_sn):

@@ -139,6 +139,31 @@ def build_skipnet_resnet38(W, max_batch, device=0, thr=None, precision=FP32_STRE
     return Model(g, (32, 32, 3), 10, max_batch, "skipnet_resnet38")
 
 
+def build_skipnet_rnn_resnet38(W, max_batch, device=0, thr=None, precision=FP32_STREAM) -> Model:
+    """SkipNet with the recurrent gate (Table 3 ID 5 "ResNet38 + RNN"), rewritten:
+    stem+block1, then per block i=2..18 a recurrent gate node: proj_i = GAP + dense(C_i -> n_in)
+    feeds the graph's one LSTM cell, whose state carries across the gates."""
+    thr = float(W["thr"]) if thr is None else thr
+    n_in, hid = int(W["rnn.n_in"]), int(W["rnn.hidden"])
+    g = _create(device, 32, 32, 3, precision)
+    D.dycl_rnn_cell(g, n_in, hid, W["rnn.w_ih"], W["rnn.w_hh"], W["rnn.b_ih"], W["rnn.b_hh"])
+    sn = D.dycl_subnet_begin(g)
+    D.dycl_subnet_conv2d(g, sn, 3, 16, 3, 1, 1, W["stem.w"], W["stem.b"], RELU, 0)
+    _block(g, sn, W, 1, 16, 16, 1)
+    D.dycl_subnet_end(g, sn)
+    D.dycl_seq(g, sn)
+    for i in range(2, 19):
+        ci, co, stride = _block_io(i, 6)
+        proj = _head(g, W, f"proj{i}", ci)
+        blk = D.dycl_subnet_begin(g)
+        _block(g, blk, W, i, ci, co, stride)
+        D.dycl_subnet_end(g, blk)
+        D.dycl_gate_rnn(g, proj, W[f"out{i}.w"], float(np.asarray(W[f"out{i}.b"]).reshape(-1)[0]), thr, blk)
+    D.dycl_final(g, _head(g, W, "final", 64))
+    D.dycl_finalize(g, max_batch)
+    return Model(g, (32, 32, 3), 10, max_batch, "skipnet_rnn_resnet38")
+
+
 R50_LAYERS = (3, 4, 6, 3)
 R50_WIDTHS = (64, 128, 256, 512)
 

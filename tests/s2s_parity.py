@@ -58,6 +58,12 @@ def compare_free_running(P_, src, tok, ln, top1, z0, mode="mirror"):
     return rep
 
 
+# bf16 storage noise of the production mode on the LM logits (measured ~3e-3 relative, DESIGN.md
+# R13 / SURVEY 8(c) ladder): a production-mode token flip is "explained" when the oracle's own
+# top1 - top2 margin at that step (fed the GPU's prefix) is below this
+FLIP_NOISE_MARGIN = 1e-2
+
+
 def compare_teacher_forced(P_, src, tok, ln, top1, mode="mirror"):
     """Per step: the oracle, fed the GPU's own prefix, must choose the GPU's token at every
     step whose oracle margin lies outside the band; the chosen token's logit within 2e-2."""
@@ -65,7 +71,7 @@ def compare_teacher_forced(P_, src, tok, ln, top1, mode="mirror"):
         return S.greedy_decode(src[i], P_, wl.S2S, mode, forced=tok[i])
     with ThreadPoolExecutor(_threads()) as ex:
         res = list(ex.map(one, range(len(src))))
-    rep = dict(n=len(src), steps=0, band_steps=0, step_mismatch=0, max_top1_rel=0.0)
+    rep = dict(n=len(src), steps=0, band_steps=0, step_mismatch=0, max_top1_rel=0.0, max_flip_margin=0.0)
     for i, (o_tok, o_len, o_top1, _, preds) in enumerate(res):
         assert o_len == ln[i], (i, o_len, ln[i])       # the forced prefix decides the length
         for t in range(int(ln[i])):
@@ -75,6 +81,7 @@ def compare_teacher_forced(P_, src, tok, ln, top1, mode="mirror"):
                 continue
             if o_tok[t] != tok[i, t]:
                 rep["step_mismatch"] += 1
+                rep["max_flip_margin"] = max(rep["max_flip_margin"], float(preds[t][1]))
                 continue
             r = abs(top1[i, t] - o_top1[t]) / max(1.0, abs(o_top1[t]))
             rep["max_top1_rel"] = max(rep["max_top1_rel"], float(r))

@@ -10,7 +10,7 @@ import oracle as O
 import workloads as wl
 from oracle import programs as prg
 from tests.parity import report
-from tests.s2s_parity import compare_free_running, compare_teacher_forced, run_s2s
+from tests.s2s_parity import FLIP_NOISE_MARGIN, compare_free_running, compare_teacher_forced, run_s2s
 
 pytestmark = pytest.mark.gpu
 
@@ -476,7 +476,15 @@ def test_cfg4_seq2seq_parity(s2s_model, B):
             assert tok[i, ln[i] - 1] == wl.S2S["eos"]
     rep = compare_free_running(P_, src, tok, ln, top1, z0)
     print("cfg4", B, rep)
-    assert rep["mismatch"] == 0 and rep["max_top1_rel"] <= 2e-2 and rep["max_z0_rel"] <= 2e-2, rep
+    assert rep["max_top1_rel"] <= 2e-2 and rep["max_z0_rel"] <= 2e-2, rep
+    # production mode: a free-running divergence must come from a counted token flip whose
+    # oracle margin (the oracle fed the GPU's own prefix) is inside the bf16 storage-noise floor;
+    # every other teacher-forced step matches (bit-exact decisions are the BF16X3 mode's bar)
+    if rep["mismatch"]:
+        bad = rep["mismatch_idx"]
+        tf = compare_teacher_forced(P_, src[bad], tok[bad], ln[bad], top1[bad])
+        print("cfg4", B, "teacher-forced on the diverged sequences", tf)
+        assert tf["step_mismatch"] >= 1 and tf["max_flip_margin"] < FLIP_NOISE_MARGIN, tf
 
 
 def test_cfg4_full_batch_sampled_parity(s2s_model):
@@ -498,6 +506,7 @@ def test_cfg4_full_batch_sampled_parity(s2s_model):
     tf = compare_teacher_forced(P_, src[idx[:32]], tok[idx[:32]], ln[idx[:32]], top1[idx[:32]])
     print("cfg4 teacher forced", tf)
     assert tf["step_mismatch"] <= 0.02 * tf["steps"] and tf["max_top1_rel"] <= 2e-2, tf
+    assert tf["max_flip_margin"] < FLIP_NOISE_MARGIN, tf
     # batch-position independence: a permuted sub-batch decodes identically
     perm = np.random.default_rng(1).permutation(64)
     tok2, ln2, _, _ = _run_s2s(m, src[:64][perm])
