@@ -118,6 +118,7 @@ WORKLOADS = {
        "tau=0.9, global batch 65536 sharded over the GPUs (inputs resident in HBM, chunks of 2048 per dycl_run)",
 }
 BATCHES = {1: 32, 2: 4096, 3: 8192, 4: 1024, 5: 65536}
+RNN_NOTE = " -- variant: recurrent LSTM gates (SkipNet RNN gate, Table 3 ID 5), hidden 10, shared across the 17 gates"
 KERNEL_NAMES = {
     "block": "k_block_fused (a1: 1-8 whole residual blocks per sample, SMEM-resident, row-tap tcgen05 convs)",
     "conv": "a1 conv class (k_conv_gemm NHWC TMA-im2col GEMM / k_conv_tma / k_gemm_tma on tcgen05, fused epilogue)",
@@ -126,7 +127,7 @@ KERNEL_NAMES = {
 }
 
 
-def oracle_sample(cfg, n, start=0):
+def oracle_sample(cfg, n, start=0, rnn=False):
     """The oracle (as it stands, mirror mode, all host cores) on n seeded samples of config cfg.
     Returns (samples/s, cores, seconds, description)."""
     import oracle as O
@@ -145,11 +146,14 @@ def oracle_sample(cfg, n, start=0):
         return n / dt, cores, dt, (f"{n} cfg4 sequences (seeded tokens {start}..{start + n - 1}), per-sequence fp64 "
                                    f"greedy decode, mirror mode")
     W = {1: wl.mlp_weights, 2: wl.sdn_r56_weights, 3: wl.skipnet_r38_weights, 5: wl.resnet50_ee_weights}[cfg]()
+    program = O.PROGRAMS[cfg]
+    if rnn and cfg == 3:
+        W, program = wl.skipnet_rnn_r38_weights(), O.skipnet_rnn_resnet38
     P = prg.prepare(W)
     X = (wl.mlp_inputs(wl.INPUT_SEED, start, n) if cfg == 1 else
          wl.image_inputs(wl.INPUT_SEED, start, n, hw=224 if cfg == 5 else 32))
     t0 = time.perf_counter()
-    O.run_batch(O.PROGRAMS[cfg], X, P, "mirror", threads=cores)
+    O.run_batch(program, X, P, "mirror", threads=cores)
     dt = time.perf_counter() - t0
     return n / dt, cores, dt, (f"{n} cfg{cfg} samples (seeded inputs {start}..{start + n - 1}), per-sample fp64 "
                                f"interpreter, mirror mode")
@@ -169,7 +173,7 @@ def run_reference(args):
     what = ""
     cores = len(os.sched_getaffinity(0))
     for i in range(args.warmup + args.steps):
-        _, cores, dt, what = oracle_sample(args.config, per_step, start=i * per_step)
+        _, cores, dt, what = oracle_sample(args.config, per_step, start=i * per_step, rnn=args.rnn_gates)
         if i >= args.warmup:
             times.append(dt)
     tot = sum(times)
@@ -179,7 +183,8 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
         "higher_is_better": True, "scaling": "strong" if args.config in GLOBAL_BATCH_CONFIGS else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config], "samples_per_step": per_step},
+        "config": {"workload": WORKLOADS[args.config] + (RNN_NOTE if args.rnn_gates and args.config == 3 else ""),
+                   "samples_per_step": per_step},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                          "sample": f"per step: {what}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -190,7 +195,7 @@ def run_reference(args):
 class ImageJob:
     """configs 1/2/3/5: one step = dycl_run over every chunk of this rank's samples."""
 
-    def __init__(self, cfg, rank, ws, dev, torch, rebalance):
+    def __init__(self, cfg, rank, ws, dev, torch, rebalance, rnn=False):
         import workloads as wl
         from paper_2307_04963_b200 import programs as P
         self.cfg, self.torch = cfg, torch
@@ -208,8 +213,10 @@ class ImageJob:
         self.bounds = [self.B * i // self.n_chunks for i in range(self.n_chunks + 1)]
         self.chunk = max(b - a for a, b in zip(self.bounds, self.bounds[1:]))
         W = {1: wl.mlp_weights, 2: wl.sdn_r56_weights, 3: wl.skipnet_r38_weights, 5: wl.resnet50_ee_weights}[cfg]()
-        self.model = P.BUILDERS[cfg](W, (per_rank_max + self.n_chunks - 1) // self.n_chunks + 1,
-                                     device=dev.index or 0)
+        build = P.BUILDERS[cfg]
+        if rnn and cfg == 3:
+            W, build = wl.skipnet_rnn_r38_weights(), P.build_skipnet_rnn_resnet38
+        self.model = build(W, (per_rank_max + self.n_chunks - 1) // self.n_chunks + 1, device=dev.index or 0)
         self.rebalance = False
         if rebalance and ws > 1:
             from paper_2307_04963_b200 import dist as DI
@@ -262,7 +269,7 @@ class ImageJob:
 class S2SJob:
     """config 4: one step = encoder + guarded greedy decode of the per-rank batch."""
 
-    def __init__(self, cfg, rank, ws, dev, torch, rebalance):
+    def __init__(self, cfg, rank, ws, dev, torch, rebalance, rnn=False):
         import workloads as wl
         from paper_2307_04963_b200 import programs as P
         self.cfg, self.torch = cfg, torch
@@ -322,7 +329,8 @@ def run_dycl(args):
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     stream = torch.cuda.current_stream()
-    job = (S2SJob if args.config == 4 else ImageJob)(args.config, rank, ws, dev, torch, not args.no_rebalance)
+    job = (S2SJob if args.config == 4 else ImageJob)(args.config, rank, ws, dev, torch, not args.no_rebalance,
+                                                     rnn=args.rnn_gates)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > L2 (126 MB)
 
     for _ in range(args.warmup):
@@ -460,7 +468,8 @@ def run_dycl(args):
         "ms_per_step": total_ms / args.steps, "ms_per_step_std": float(np.std(step_ms)),
         "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config], "global_batch": global_samples,
+        "config": {"workload": WORKLOADS[args.config] + (RNN_NOTE if args.rnn_gates and args.config == 3 else ""),
+                   "global_batch": global_samples,
                    "batch_per_gpu": job.B, "chunks_per_gpu": job.n_chunks,
                    "precision": "bf16 tensor-core operands, fp32 accumulate, fp32 residual stream",
                    "l2": "flushed (256 MB write) before every timed step, flush not timed; inputs > L2",
@@ -480,7 +489,7 @@ def run_dycl(args):
         line["tokens_per_s"] = hist["tokens"] * ws * args.steps / (total_ms / 1e3)
     if ws == 1 and not args.no_cpu_baseline:
         n_cpu = args.cpu_samples or {1: 4096, 2: 4096, 3: 2048, 4: 48, 5: 64}[args.config]
-        rate, cores, dt, what = oracle_sample(args.config, n_cpu)
+        rate, cores, dt, what = oracle_sample(args.config, n_cpu, rnn=args.rnn_gates)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
                                 "sample": f"{what}, {dt:.1f} s wall"}
     print(json.dumps(line), flush=True)
@@ -500,6 +509,8 @@ def main():
     ap.add_argument("--ref-samples", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rebalance", action="store_true", help="N > 1: no survivor rebalancing")
+    ap.add_argument("--rnn-gates", action="store_true",
+                    help="config 3 with SkipNet's recurrent (LSTM) gates (SURVEY 8(f)3, Table 3 ID 5)")
     args = ap.parse_args()
     if args.steps is None:
         args.steps = 10 if args.config == 5 else 50

@@ -595,7 +595,13 @@ struct Exec {
         return fail(g, DYCL_E_UNSUPPORTED, "head layers inside a sequential subnet");
       const bool last = li + 1 == s.layers.size();
       if (L.kind == L_MAXPOOL) {
-        const bool stream_mp = fp32_stream() && (last || s.layers[li + 1].kind == L_BLOCK);
+        // the pool output is a residual-stream tensor only if something reads its fp32 copy: a
+        // block whose shortcut is a projection reads its input as the bf16 operand alone
+        bool proj_next = false;
+        if (!last && s.layers[li + 1].kind == L_BLOCK)
+          for (size_t lj = li + 2; lj < s.layers.size() && s.layers[lj].kind != L_BLOCK; ++lj)
+            proj_next = proj_next || s.layers[lj].kind == L_PROJ;
+        const bool stream_mp = fp32_stream() && (last || s.layers[li + 1].kind == L_BLOCK) && !proj_next;
         Tensor o = (last && out_hint.b >= 0) ? out_hint : pick_tensor(stream_mp, {cur, shortcut, busy, out_hint});
         if (o.b < 0 || (stream_mp && o.f < 0)) return fail(g, DYCL_E_STATE, "internal: out of activation buffers");
         if (!stream_mp) o.f = -1;

@@ -319,7 +319,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                                      (uint32_t)((r | q) != 0));
           ptx::mma_commit_elect(acc1j0 + 8 * j);
         }
-        ptx::mma_commit_elect(xb_empty);
+        // xb is free for the next sample's conversion once the LAST block's conv1 has read it
+        // (earlier blocks' reads are ordered before the epilogue-2 writes that refill xb by the
+        // acc2 commit, which covers every prior MMA): one completion per sample, no skipped phase
+        if (blk == NB - 1) ptx::mma_commit_elect(xb_empty);
         __syncwarp();
         if (mstamp && blk == 0) a.ts[it * 16 + 7] = clock64();
         if (mstamp && blk == NB - 1) a.ts[it * 16 + 8] = clock64();
@@ -393,7 +396,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int b = itc % G::NXB;
       const uint8_t* xs = x32s + (size_t)b * G::X32_BYTES;
       ptx::mbar_wait(xfull0 + 8 * b, (itc / G::NXB) & 1);
-      ptx::mbar_wait(xb_empty, (itc * NB - 1) & 1);    // the previous sample's last conv1 read xb
+      ptx::mbar_wait(xb_empty, (itc - 1) & 1);         // the previous sample's last conv1 read xb
 #pragma unroll 4
       for (int u = et; u < HW * P; u += 256) {
         const int pix = u % HW, p = u / HW;            // lanes = consecutive pixels (swizzled rows)

@@ -688,10 +688,21 @@ __global__ void k_cast_s4d(const float* __restrict__ in, uint16_t* __restrict__ 
   const int Wb = W / 4, Hb = H / 4;
   for (int64_t pix = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pix < total;
        pix += (int64_t)gridDim.x * blockDim.x) {
-    const int Q = (int)(pix % Wb);
-    const int64_t t = pix / Wb;
-    const int P = (int)(t % Hb);
-    const int64_t n = t / Hb;
+    // 32-bit index arithmetic when the launch fits (64-bit division is a long software sequence)
+    int Q, P;
+    int64_t n;
+    if (total < (int64_t)1 << 31) {
+      const uint32_t p32 = (uint32_t)pix, t32 = p32 / (uint32_t)Wb;
+      Q = (int)(p32 - t32 * (uint32_t)Wb);
+      const uint32_t n32 = t32 / (uint32_t)Hb;
+      P = (int)(t32 - n32 * (uint32_t)Hb);
+      n = n32;
+    } else {
+      Q = (int)(pix % Wb);
+      const int64_t t = pix / Wb;
+      P = (int)(t % Hb);
+      n = t / Hb;
+    }
     float v[64];
 #pragma unroll
     for (int k = 0; k < 64; ++k) v[k] = 0.0f;

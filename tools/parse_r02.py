@@ -27,7 +27,7 @@ def launches(path):
     for r in csv.DictReader(lines):
         i = int(r["ID"])
         names[i] = r["Kernel Name"].split("(")[0].replace("void ", "").replace("(anonymous namespace)::", "") \
-            .replace("dycl::", "")
+            .replace("dycl::", "").replace("unnamed>::", "")
         v = float(r["Metric Value"].replace(",", ""))
         u = r["Metric Unit"]
         if r["Metric Name"] == "gpu__time_duration.sum":
