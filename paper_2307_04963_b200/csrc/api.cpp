@@ -124,6 +124,10 @@ struct dycl_graph_s {
   int conv_dbg = 0;                  // DYCL_CONV_DBG: timing experiments only (results invalid)
   int no_fuse = 0;                   // DYCL_NO_FUSE=1: run basic blocks as two conv launches
   int head_cuda_core = 0;            // DYCL_HEAD_CUDA_CORE=1: wide-head FC on CUDA cores (k_head_fc), not tcgen05
+  // pair residual stream (set at finalize; DYCL_NO_PAIR=1 disables): in NHWC graphs without gates,
+  // fused blocks or dense trunk layers the fp32 stream copy is replaced by a bf16 "lo" plane
+  // (value = bf16 operand copy + lo; ConvArgs::y32_pair): 4 instead of 6 bytes per element
+  bool stream_pair = false;
   int max_fuse = dycl::MAX_FUSED_BLOCKS;   // DYCL_MAX_FUSE: basic blocks per fused launch (1..8)
   int no_inplace = 0;                // DYCL_NO_INPLACE=1: gates gather / merge instead of running in place
   int no_zero_copy = 0;              // DYCL_NO_ZERO_COPY=1: exits gather survivors even before a fused block
@@ -646,7 +650,8 @@ struct Exec {
         a.in_nhwc = lay(L.in.Cp());
         a.nhwc = lay(L.out.C);
         a.dbg = g->conv_dbg;
-        prof_begin(DYCL_K_CONV, cnt, 2.0 * L.in.row_elems() + (o.f >= 0 ? 6.0 : 2.0) * L.out.row_elems(),
+        a.y32_pair = g->stream_pair;
+        prof_begin(DYCL_K_CONV, cnt, 2.0 * L.in.row_elems() + (o.f >= 0 ? (g->stream_pair ? 4.0 : 6.0) : 2.0) * L.out.row_elems(),
                    2.0 * L.out.H * L.out.W * L.out.C * (double)L.in.C, 2.0 * L.out.C * L.Kp);
         cudaError_t e = dycl::launch_conv(a, batch, g->num_sms, st, g->conv_path);
         prof_end();
@@ -708,9 +713,11 @@ struct Exec {
                           s.layers[li + 1].kind == L_BLOCK && fusable(s, li + 1);
       if (skip_b) a.y = nullptr;
       a.dbg = g->conv_dbg;
+      a.y32_pair = g->stream_pair;
       const double res_b = a.res_mode ? (a.res32 ? 4.0 : 2.0) * L.res_shape.row_elems() *
                                             (a.res_mode == 2 ? 0.25 : 1.0) : 0.0;
-      const double row_b = 2.0 * L.in.row_elems() + (o.f >= 0 ? (a.y ? 6.0 : 4.0) : 2.0) * L.out.row_elems() + res_b +
+      const double row_b = 2.0 * L.in.row_elems() +
+                           (o.f >= 0 ? (a.y ? 2.0 : 0.0) + (g->stream_pair ? 2.0 : 4.0) : 2.0) * L.out.row_elems() + res_b +
                            fused_b;
       const double row_f = 2.0 * L.out.H * L.out.W * L.out.C * (double)(L.k * L.k * L.in.C) + fused_f;
       // (only for wide rows: below ~128 KB of fp32 per sample the head's own GAP pass is cheaper)
@@ -748,6 +755,8 @@ struct Exec {
     dycl::HeadArgs a{};
     a.h = in.b >= 0 ? g->buf[in.b] : nullptr;
     a.h32 = in.f >= 0 ? g->buf32[in.f] : nullptr;
+    a.h32_pair = g->stream_pair;
+    if (a.h32_pair && a.h32 && !a.h) return fail(g, DYCL_E_STATE, "internal: pair stream head without its hi plane");
     a.w = D.d_w;
     a.b = D.d_b;
     a.z = g->d_z;
@@ -816,7 +825,7 @@ struct Exec {
       if (si < 0) continue;
       if (di < 0) return fail(g, DYCL_E_STATE, "internal: gather destination lacks a copy");
       dycl::GatherArgs a{};
-      a.elem_bytes = pass == 0 ? 2 : 4;
+      a.elem_bytes = pass == 0 || g->stream_pair ? 2 : 4;
       a.src = pass == 0 ? (const void*)g->buf[si] : (const void*)g->buf32[si];
       a.dst = pass == 0 ? (void*)g->buf[di] : (void*)g->buf32[di];
       a.list = list;
@@ -1115,7 +1124,7 @@ struct Exec {
                                          g->d_sent_orig + sent_used, meta_send, st);
     if (e != cudaSuccess) return cuda_fail(g, e, "launch_rb_pack");
     std::vector<dycl::Transport::Msg> sends, recvs;
-    const size_t rb = (size_t)sh.row_elems() * 2, rf = (size_t)sh.row_elems() * 4;
+    const size_t rb = (size_t)sh.row_elems() * 2, rf = (size_t)sh.row_elems() * (g->stream_pair ? 2 : 4);
     int so = keep, ro = s_own;                       // row cursors (destination / source rank ascending)
     for (int j = 0; j < W; ++j) {
       if (L.send[j]) {
@@ -1564,6 +1573,29 @@ dycl_status dycl_finalize(dycl_graph g, int64_t max_batch) {
           }
     const char* env = getenv("DYCL_NHWC");
     g->nhwc = ok && !(env && atoi(env) == 0);
+    // pair residual stream (see stream_pair): NHWC, fp32-stream precision, no gates (in-place gate
+    // forms read the fp32 copy), no dense trunk layers or SMEM-fused basic blocks, and no max pool
+    // whose fp32 output copy a block would read as its identity shortcut
+    bool pair = g->nhwc && g->precision == DYCL_PREC_FP32_STREAM && g->n_gates == 0 && !getenv("DYCL_NO_PAIR");
+    for (size_t i = 0; i < g->subnets.size() && pair; ++i) {
+      if (!planned[i]) continue;
+      const auto& Ls = g->subnets[i].layers;
+      for (size_t li = 0; li < Ls.size() && pair; ++li) {
+        const Layer& L = Ls[li];
+        if (L.kind == L_DENSE && !L.out_fp32) pair = false;
+        if (L.kind == L_BLOCK && li + 2 < Ls.size() && Ls[li + 1].kind == L_CONV && Ls[li + 1].k == 3 &&
+            Ls[li + 2].kind == L_CONV && Ls[li + 2].k == 3 &&
+            dycl::block_fused_eligible(Ls[li + 1].in.C, Ls[li + 1].in.H, Ls[li + 1].in.W))
+          pair = false;
+        if (L.kind == L_MAXPOOL) {
+          bool proj = false;
+          if (li + 1 < Ls.size() && Ls[li + 1].kind == L_BLOCK)
+            for (size_t lj = li + 2; lj < Ls.size() && Ls[lj].kind != L_BLOCK; ++lj) proj = proj || Ls[lj].kind == L_PROJ;
+          if (li + 1 == Ls.size() || (Ls[li + 1].kind == L_BLOCK && !proj)) pair = false;
+        }
+      }
+    }
+    g->stream_pair = pair;
     // space-to-depth stem: the first layer run is a 7x7 / stride-2 / pad-3 conv on <= 4 input
     // channels followed by a 3x3 / stride-2 / pad-1 max pool (the ImageNet ResNet stem)
     g->stem_s4d = 0;

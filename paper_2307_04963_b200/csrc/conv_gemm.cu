@@ -78,6 +78,11 @@ __device__ __forceinline__ uint32_t pk2(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
 }
+// the lo halves of the pair stream: bf16_rn(v - bf16_rn(v)) for two values
+__device__ __forceinline__ uint32_t pk2lo(float a, float b) {
+  const uint32_t h = pk2(a, b);
+  return pk2(a - __uint_as_float(h << 16), b - __uint_as_float(h & 0xFFFF0000u));
+}
 __device__ __forceinline__ void wg_sync(int wg) { asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory"); }
 // 16-byte chunk j of row r in a 1024-B-aligned buffer with 128-byte rows, 128B swizzle
 __device__ __forceinline__ uint32_t sw128(int r, int j) { return (uint32_t)(r * 128 + ((j ^ (r & 7)) << 4)); }
@@ -93,7 +98,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     k_conv_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmY32,
                 const __grid_constant__ CUtensorMap tmY16, const __grid_constant__ CUtensorMap tmA2,
-                const __grid_constant__ CUtensorMap tmAL, const ConvArgs a, const GemmPlan pl) {
+                const __grid_constant__ CUtensorMap tmAL, const __grid_constant__ CUtensorMap tmRL,
+                const ConvArgs a, const GemmPlan pl) {
   using G = CG<BN>;
   constexpr int NA = RT ? 3 * BN : BN;                     // MMA N = accumulator columns per tile
   constexpr int BB = NA * BKE * 2;                         // B bytes per k-block
@@ -309,6 +315,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     const bool leader = (threadIdx.x & 127) == 0;
     const bool res = a.res_mode == 1;
     const bool res_f = res && a.res32 != nullptr;
+    // pair stream (ConvArgs::y32_pair): the residual stream is bf16 hi (the operand copy a.res /
+    // a.y) + bf16 lo (the planes behind res32 / y32), value = hi + lo
+    const bool pair = a.y32_pair != 0;
+    const uint16_t* res_lo = reinterpret_cast<const uint16_t*>(a.res32);
+    uint16_t* y_lo = reinterpret_cast<uint16_t*>(a.y32);
     const bool staged = pl.staged != 0;
     uint8_t* eR = sE + wg * EPI_WG;
     uint8_t* eO32 = eR + EPI_RES;
@@ -318,6 +329,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (staged && leader) {
       if (res) ptx::tma_prefetch_desc(&tmR);
       if (a.y32) ptx::tma_prefetch_desc(&tmY32);
+      if (res_f && pair) ptx::tma_prefetch_desc(&tmRL);
       if (a.y) ptx::tma_prefetch_desc(&tmY16);
     }
     int it = 0;
@@ -348,12 +360,29 @@ __global__ void __launch_bounds__(THREADS, 1)
       auto res_load = [&](int c0) {
         ptx::mbar_arrive_expect_tx(rbar, res_f ? EPI_RES : EPI_RES / 2);
         ptx::tma_load_2d(ptx::smem_u32(eR), &tmR, rbar, col0 + c0, (int)m0);
+        if (res_f && pair) ptx::tma_load_2d(ptx::smem_u32(eR + EPI_RES / 2), &tmRL, rbar, col0 + c0, (int)m0);
       };
       if (staged && res && leader) res_load(0);
       // unstaged shortcut chunk (32 channels) prefetch, issued before the accumulator wait
       float4 rs[8];
       auto load_res_g = [&](int c0) {
-        if (res_f) {
+        if (res_f && pair) {
+          const uint4* qh = reinterpret_cast<const uint4*>(a.res + rowo + c0);
+          const uint4* ql = reinterpret_cast<const uint4*>(res_lo + rowo + c0);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint4 h = ok ? __ldg(qh + j) : make_uint4(0, 0, 0, 0);
+            const uint4 l = ok ? __ldg(ql + j) : make_uint4(0, 0, 0, 0);
+            rs[2 * j] = make_float4(__uint_as_float(h.x << 16) + __uint_as_float(l.x << 16),
+                                    __uint_as_float(h.x & 0xFFFF0000u) + __uint_as_float(l.x & 0xFFFF0000u),
+                                    __uint_as_float(h.y << 16) + __uint_as_float(l.y << 16),
+                                    __uint_as_float(h.y & 0xFFFF0000u) + __uint_as_float(l.y & 0xFFFF0000u));
+            rs[2 * j + 1] = make_float4(__uint_as_float(h.z << 16) + __uint_as_float(l.z << 16),
+                                        __uint_as_float(h.z & 0xFFFF0000u) + __uint_as_float(l.z & 0xFFFF0000u),
+                                        __uint_as_float(h.w << 16) + __uint_as_float(l.w << 16),
+                                        __uint_as_float(h.w & 0xFFFF0000u) + __uint_as_float(l.w & 0xFFFF0000u));
+          }
+        } else if (res_f) {
           const float4* q = reinterpret_cast<const float4*>(a.res32 + rowo + c0);
 #pragma unroll
           for (int j = 0; j < 8; ++j) rs[j] = ok ? __ldg(q + j) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -407,7 +436,19 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (staged && res) {
           ptx::mbar_wait(rbar, rphase);
           rphase ^= 1;
-          if (res_f) {
+          if (res_f && pair) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint4 uh = *reinterpret_cast<const uint4*>(eR + sw64(r, j));
+              const uint4 ul = *reinterpret_cast<const uint4*>(eR + EPI_RES / 2 + sw64(r, j));
+              const uint32_t h4[4] = {uh.x, uh.y, uh.z, uh.w}, l4[4] = {ul.x, ul.y, ul.z, ul.w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                f[8 * j + 2 * q] += __uint_as_float(h4[q] << 16) + __uint_as_float(l4[q] << 16);
+                f[8 * j + 2 * q + 1] += __uint_as_float(h4[q] & 0xFFFF0000u) + __uint_as_float(l4[q] & 0xFFFF0000u);
+              }
+            }
+          } else if (res_f) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const float4 q = *reinterpret_cast<const float4*>(eR + sw128(r, j));
@@ -482,25 +523,35 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int cc = lane, q = quad;
             const int G = a.gap_g;
             const long long ra = m0 + 32 * q;                  // first row of this quarter
-            // all 32 loads first (independent of the partial stores below), then the sums
-            float v[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              v[i] = *reinterpret_cast<const float*>(eO32 + sw128(32 * q + i, cc >> 2) + (cc & 3) * 4);
+            // 8 shared loads in flight at a time (a 32-value batch spilled the epilogue's registers)
             float* gp = a.gap_part + (size_t)(ra / G) * a.Cout + col0 + c0 + cc;
+            const uint8_t* col = eO32 + (cc & 3) * 4;
             float sacc = 0.f;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              sacc += v[i];
-              if (((i + 1) & (G - 1)) == 0) {             // a group never straddles M (G | HW)
-                if (ra + i < M) gp[(size_t)(i / G) * a.Cout] = sacc;
-                sacc = 0.f;
+            for (int i0 = 0; i0 < 32; i0 += 8) {
+              float v[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[i] = *reinterpret_cast<const float*>(col + sw128(32 * q + i0 + i, cc >> 2));
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                sacc += v[i];
+                if (((i0 + i + 1) & (G - 1)) == 0) {     // a group never straddles M (G | HW)
+                  if (ra + i0 + i < M) gp[(size_t)((i0 + i) / G) * a.Cout] = sacc;
+                  sacc = 0.f;
+                }
               }
             }
           }
         }
         if (staged && full) {
-          if (a.y32 && !a.gap_part) {
+          if (a.y32 && pair) {
+            if (a.gap_part) wg_sync(wg);                // the GAP has read the fp32 staging
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              *reinterpret_cast<uint4*>(eO32 + sw64(r, j)) =
+                  make_uint4(pk2lo(f[8 * j], f[8 * j + 1]), pk2lo(f[8 * j + 2], f[8 * j + 3]),
+                             pk2lo(f[8 * j + 4], f[8 * j + 5]), pk2lo(f[8 * j + 6], f[8 * j + 7]));
+          } else if (a.y32 && !a.gap_part) {
 #pragma unroll
             for (int j = 0; j < 8; ++j)
               *reinterpret_cast<float4*>(eO32 + sw128(r, j)) = make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
@@ -527,7 +578,13 @@ __global__ void __launch_bounds__(THREADS, 1)
               yq[j] = make_uint4(pk2(f[8 * j], f[8 * j + 1]), pk2(f[8 * j + 2], f[8 * j + 3]),
                                  pk2(f[8 * j + 4], f[8 * j + 5]), pk2(f[8 * j + 6], f[8 * j + 7]));
           }
-          if (a.y32) {
+          if (a.y32 && pair) {
+            uint4* lq = reinterpret_cast<uint4*>(y_lo + rowo + c0);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              lq[j] = make_uint4(pk2lo(f[8 * j], f[8 * j + 1]), pk2lo(f[8 * j + 2], f[8 * j + 3]),
+                                 pk2lo(f[8 * j + 4], f[8 * j + 5]), pk2lo(f[8 * j + 6], f[8 * j + 7]));
+          } else if (a.y32) {
             float4* zq = reinterpret_cast<float4*>(a.y32 + rowo + c0);
 #pragma unroll
             for (int j = 0; j < 8; ++j) zq[j] = make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
@@ -678,17 +735,26 @@ cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t 
   pl.stages = pl.bres ? (avail - kblocks * BB) / CG<BN>::A_BYTES : avail / (CG<BN>::A_BYTES + BB);
   if (pl.stages > MAX_STAGES) pl.stages = MAX_STAGES;
   if (pl.stages > kblocks + 1 && kblocks >= 1) pl.stages = kblocks + 1 > 2 ? kblocks + 1 : 2;
+  CUtensorMap tmRL = tmB;
   tmR = tmY32 = tmY16 = tmB;
+  const bool pair = a.y32_pair != 0;
+  if (pair && a.res_mode == 1 && a.res32 && !a.res) return cudaErrorInvalidValue;   // the hi plane
   if (pl.staged) {
-    if (a.res_mode == 1) {
+    if (a.res_mode == 1 && a.res32 && pair) {
+      if (!mat2d(&tmR, a.res, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.Cout, Mmax, 32, BM, CU_TENSOR_MAP_SWIZZLE_64B) ||
+          !mat2d(&tmRL, a.res32, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.Cout, Mmax, 32, BM, CU_TENSOR_MAP_SWIZZLE_64B))
+        return cudaErrorInvalidValue;
+    } else if (a.res_mode == 1) {
       const bool f32 = a.res32 != nullptr;
       if (!mat2d(&tmR, f32 ? (const void*)a.res32 : (const void*)a.res,
                  f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, f32 ? 4 : 2, a.Cout, Mmax,
                  32, BM, f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B))
         return cudaErrorInvalidValue;
     }
-    if (a.y32 && !mat2d(&tmY32, a.y32, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.Cout, Mmax, 32, BM,
-                        CU_TENSOR_MAP_SWIZZLE_128B))
+    if (a.y32 && !(pair ? mat2d(&tmY32, a.y32, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.Cout, Mmax, 32, BM,
+                                CU_TENSOR_MAP_SWIZZLE_64B)
+                         : mat2d(&tmY32, a.y32, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.Cout, Mmax, 32, BM,
+                                 CU_TENSOR_MAP_SWIZZLE_128B)))
       return cudaErrorInvalidValue;
     if (a.y && !mat2d(&tmY16, a.y, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.Cout, Mmax, 32, BM,
                       CU_TENSOR_MAP_SWIZZLE_64B))
@@ -700,7 +766,7 @@ cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t 
   const long long tiles = ((long long)Mmax + BM - 1) / BM * (a.Cout / BN);
   int grid = (int)(tiles < num_sms ? tiles : num_sms);
   if (grid < 1) grid = 1;
-  k_conv_gemm<BN, IM2COL, RT><<<grid, THREADS, smem, stream>>>(tmA, tmB, tmR, tmY32, tmY16, tmA2, tmAL, a, pl);
+  k_conv_gemm<BN, IM2COL, RT><<<grid, THREADS, smem, stream>>>(tmA, tmB, tmR, tmY32, tmY16, tmA2, tmAL, tmRL, a, pl);
   return cudaGetLastError();
 }
 

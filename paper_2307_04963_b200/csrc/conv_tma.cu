@@ -689,9 +689,12 @@ cudaError_t launch_conv_tma(const ConvArgs& a, int max_rows, int num_sms, cudaSt
 }
 
 cudaError_t launch_conv(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream, int path) {
+  // the pair stream exists only on the NHWC im2col GEMM
+  if (a.y32_pair && !(a.in_nhwc && a.nhwc && conv_gemm_eligible(a))) return cudaErrorNotSupported;
   if (a.in_nhwc) {
     // NHWC input: the im2col GEMM (C, Cout % 64); a planar kernel only when the layouts coincide
     // (8 channels, or 1x1 maps)
+    if (a.nhwc && conv_halo_eligible(a)) return launch_conv_halo(a, max_rows, num_sms, stream);
     if (a.nhwc && conv_gemm_eligible(a)) return launch_conv_gemm(a, max_rows, num_sms, stream);
     if (a.C != 8 && !(a.H == 1 && a.W == 1)) return cudaErrorNotSupported;
   }

@@ -93,7 +93,20 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head(const HeadArgs a) {
       for (int c = t; c < a.C; c += HEAD_THREADS) g[c] = a.pooled[(size_t)row * a.C + c];
     } else if (t < G * P) {
       const int grp = t % G;
-      if (a.h32) {
+      if (a.h32 && a.h32_pair) {
+        // pair stream: value = bf16 hi (the NHWC operand copy) + bf16 lo
+        const uint16_t* lo = reinterpret_cast<const uint16_t*>(a.h32) + (size_t)row * a.HW * a.C;
+        for (int p = t / G; p < a.HW; p += P) {
+          const uint4 vh = __ldg(reinterpret_cast<const uint4*>(h + (size_t)p * a.C + grp * 8));
+          const uint4 vl = __ldg(reinterpret_cast<const uint4*>(lo + (size_t)p * a.C + grp * 8));
+          const uint32_t uh[4] = {vh.x, vh.y, vh.z, vh.w}, ul[4] = {vl.x, vl.y, vl.z, vl.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            acc[2 * j] += __uint_as_float(uh[j] << 16) + __uint_as_float(ul[j] << 16);
+            acc[2 * j + 1] += __uint_as_float(uh[j] & 0xFFFF0000u) + __uint_as_float(ul[j] & 0xFFFF0000u);
+          }
+        }
+      } else if (a.h32) {
         const float* h32 = a.h32 + (size_t)row * a.HW * a.C;
         for (int p = t / G; p < a.HW; p += P) {
           const float4* q = reinterpret_cast<const float4*>(h32 + (size_t)p * a.C + grp * 8);

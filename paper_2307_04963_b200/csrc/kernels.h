@@ -54,6 +54,10 @@ struct ConvArgs {
   // columns stored (0 = all; a multiple of 4) -- the wide heads' padded-N GEMM writes the K
   // logits straight into the [rows][K] logit buffer
   int y32_ld = 0, y32_n = 0;
+  // conv_gemm only: the "pair" residual stream -- y32 / res32 point to bf16 LO planes and the
+  // stream value is bf16(hi) + bf16(lo) with hi = the bf16 operand copy (y / res) and
+  // lo = bf16_rn(v - hi): 4 bytes per element instead of fp32 + bf16 copy (6), |rel err| < 2^-16
+  int y32_pair = 0;
   // gemm_tma only: fused LM-head argmax.  Instead of storing y, each
   // epilogue thread scans its row's BN columns of the tile in ascending order (after bias, plus
   // the loop guard's EOS bias g_beta * (g_t + 1 - g_len[g_src[g_slot[m] * g_S]]) on column g_eos)
@@ -128,10 +132,15 @@ inline void pack_rowtap(const uint16_t* wp, int cout, int kp, int cp, uint16_t* 
 // boxes; *handled = false (and nothing launched) when the shape does not qualify.
 cudaError_t launch_conv_tma(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream, bool* handled);
 // Dense-layer GEMM on tcgen05 with TMA SWIZZLE_128B tiles (gemm_tma.cu): [rows][K] x [N][K].
+// 3x3 / s1 / p1 NHWC conv, 64 -> 64 channels, W + 2 <= 128, bf16 output only: TMA halo tile +
+// shifted UMMA descriptors (conv_halo.cu)
+bool conv_halo_eligible(const ConvArgs& a);
+cudaError_t launch_conv_halo(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream);
 bool gemm_tma_eligible(const ConvArgs& a);
 cudaError_t launch_gemm_tma(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream);
 // N tile width launch_gemm_tma picks for these arguments (64, 128 or 256).
 int gemm_tma_bn(const ConvArgs& a, int max_rows, int num_sms);
+
 // NHWC implicit-GEMM conv with TMA im2col operand loads (conv_gemm.cu): C % 64 == 0, Cout % 64 == 0.
 bool conv_gemm_eligible(const ConvArgs& a);
 cudaError_t launch_conv_gemm(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream);
@@ -184,6 +193,7 @@ struct HeadArgs {
   const float* pooled = nullptr;  // fp32 [rows][C] pooled features already computed (fused GAP): skip the GAP
   float* pooled_out = nullptr;    // fp32 [rows][C]: keep the GAP this kernel computes (later in-place gates reuse it)
   float* gpool = nullptr;         // fp32 [rows][C] pooled-feature scratch for the batched FC
+  int h32_pair = 0;               // h32 is the pair stream's bf16 lo plane (value = h + lo), NHWC
   // wide heads on the tensor cores (a2): the fp32 pooled features are split into a bf16 pair
   // [hi | lo] per row (a2, [rows][2C]) and multiplied with w2 = [W | W] ([kpad][2C], rows >= K
   // zero) by the tcgen05 GEMM -- the split-bf16 product, fp32-accurate (|rel err| ~ 2^-16)

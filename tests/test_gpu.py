@@ -128,6 +128,11 @@ NHWC_CASES = [
     (2, 9, 9, 64, 64, 7, 2, 3, 1, 0),        # 7x7 stride 2 pad 3
     (4, 16, 16, 8, 64, 7, 2, 3, 1, 0),       # stem (C = 8): planar kernels, NHWC output
     (1, 1, 1, 64, 64, 1, 1, 0, 1, 0),        # single row
+    # 3x3 / s1 / p1, 64 -> 64: the halo-tile kernel (conv_halo.cu; R output rows per tile, pitch W + 2)
+    (2, 56, 56, 64, 64, 3, 1, 1, 1, 0),      # ResNet-50 stage 1: R = 2, P = 58
+    (3, 14, 14, 64, 64, 3, 1, 1, 1, 0),      # R = 7, P = 16
+    (2, 5, 7, 64, 64, 3, 1, 1, 0, 0),        # non-square, whole sample in one tile, no ReLU
+    (1, 9, 30, 64, 64, 3, 1, 1, 1, 0),       # R = 3 (9 / 3), P = 32
 ]
 # row-tap GEMM form (path 5): 3x3 / s1 / p1, whole samples per 128-row tile, W | 32, Cout 64
 ROWTAP_NHWC_CASES = [
