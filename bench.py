@@ -253,9 +253,9 @@ class ImageJob:
         self.ph = torch.empty(self.B, dtype=torch.int32).pin_memory()
 
     def step_host(self, stream):
-        for c0, c1 in self.chunks():
-            self.model.run_host(self.xh[c0:c1], self.lh[c0:c1], self.ph[c0:c1], stream=stream,
-                                global_offset=self.g0 + c0)
+        # one public call for the rank's whole shard: the library streams it through in
+        # max_batch-row sub-chunks with the copies of sub-chunk k +- 1 under the run of k
+        self.model.run_host(self.xh, self.lh, self.ph, stream=stream, global_offset=self.g0)
 
     def check_host(self):
         return bool(np.array_equal(self.ph.numpy(), self.path.cpu().numpy()))

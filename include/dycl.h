@@ -211,6 +211,8 @@ dycl_status dycl_run(dycl_graph g, const dycl_io* io, void* stream);
 /* Same, with HOST buffers (pinned or pageable): copies the input host->device,
  * runs, copies logits and path device->host, and synchronises `stream` before
  * returning -- the deployment-style call of Listing 2 (set_input/run/get_output).
+ * Any batch >= 0 is accepted: a batch larger than max_batch streams through in
+ * max_batch-row sub-chunks (library-owned staging of 2 x max_batch rows).
  * Batches of >= 1024 rows are pipelined in sub-chunks (a quarter of the batch; for samples
  * under 64 KB, batches of >= 2048 rows run as two chunks, a quarter then the rest, so only
  * the first chunk's copy is exposed) over two library-owned

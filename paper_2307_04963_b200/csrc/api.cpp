@@ -168,7 +168,8 @@ struct dycl_graph_s {
   float* d_gap_part = nullptr;      // conv_gemm fused-GAP partials [rows / G][C] fp32 (sub-network outputs read by a head)
   float* d_gap_pooled = nullptr;    // their reduction [max_batch][C]
   float* d_pool32[NBUF32] = {};     // fused-GAP features per fp32 stream buffer [max_batch][<= 32] (fused blocks)
-  float* d_in_stage = nullptr;      // dycl_run_host staging
+  float* d_in_stage = nullptr;      // dycl_run_host staging (stage_rows rows)
+  int64_t stage_rows = 0;
   float* d_logit_stage = nullptr;
   int32_t* d_path_stage = nullptr;
   float* d_margin_stage = nullptr;
@@ -1801,16 +1802,27 @@ static dycl_status run_host_impl(dycl_graph g, const float* input_host, int64_t 
                                  float* logits_host, int32_t* path_host, float* margin_host, void* stream) {
   if (!g) return DYCL_E_INVALID_ARG;
   if (!g->finalized) return fail(g, DYCL_E_STATE, "graph not finalized");
-  if (batch < 0 || batch > g->max_batch) return fail(g, DYCL_E_SHAPE_MISMATCH, "batch > max_batch");
+  if (batch < 0) return fail(g, DYCL_E_SHAPE_MISMATCH, "negative batch");
   if (batch > 0 && (!input_host || !logits_host || !path_host)) return fail(g, DYCL_E_INVALID_ARG, "null pointer");
   CK(cudaSetDevice(g->device));
   cudaStream_t st = (cudaStream_t)stream;
-  const size_t in_elems = (size_t)g->max_batch * g->input.H * g->input.W * g->input.C;
-  if (!g->d_in_stage) {
+  // a batch larger than the graph's max_batch streams through in max_batch-row sub-chunks, two
+  // staging slots of max_batch rows each (only the first sub-chunk's copy is exposed)
+  const bool big = batch > g->max_batch;
+  const int64_t need = big ? 2 * g->max_batch : g->max_batch;
+  if (g->stage_rows < need) {
+    cudaFree(g->d_in_stage);
+    cudaFree(g->d_logit_stage);
+    cudaFree(g->d_path_stage);
+    cudaFree(g->d_margin_stage);
+    g->d_in_stage = nullptr; g->d_logit_stage = nullptr; g->d_path_stage = nullptr; g->d_margin_stage = nullptr;
+    g->stage_rows = 0;
+    const size_t in_elems = (size_t)need * g->input.H * g->input.W * g->input.C;
     if (dycl_status s = dmalloc(g, &g->d_in_stage, in_elems * 4)) return s;
-    if (dycl_status s = dmalloc(g, &g->d_logit_stage, (size_t)g->max_batch * g->K * 4)) return s;
-    if (dycl_status s = dmalloc(g, &g->d_path_stage, (size_t)g->max_batch * 4)) return s;
-    if (dycl_status s = dmalloc(g, &g->d_margin_stage, (size_t)g->max_batch * 4)) return s;
+    if (dycl_status s = dmalloc(g, &g->d_logit_stage, (size_t)need * g->K * 4)) return s;
+    if (dycl_status s = dmalloc(g, &g->d_path_stage, (size_t)need * 4)) return s;
+    if (dycl_status s = dmalloc(g, &g->d_margin_stage, (size_t)need * 4)) return s;
+    g->stage_rows = need;
   }
   const size_t row_in = (size_t)g->input.H * g->input.W * g->input.C;
   // Pipelined over sub-chunks in two staging slots: H2D of sub-chunk k+1 (copy stream) and
@@ -1819,9 +1831,9 @@ static dycl_status run_host_impl(dycl_graph g, const float* input_host, int64_t 
   // sub-chunk: a quarter of the batch.  Small samples (< 64 KB of input), whose runs lose
   // efficiency below ~2048 rows: two uneven chunks, a quarter then the rest -- only the first
   // chunk's copy is exposed, the second one's hides under the first run
-  int64_t sc = batch >= 1024 ? (batch + 3) / 4 : batch;
+  int64_t sc = big ? g->max_batch : batch >= 1024 ? (batch + 3) / 4 : batch;
   int64_t first = sc;                              // rows of chunk 0
-  const bool small = row_in * 4 < 64 * 1024;
+  const bool small = row_in * 4 < 64 * 1024 && !big;
   if (small) {
     if (batch >= 2048 && !getenv("DYCL_E2E_EVEN")) {
       first = ((batch + 3) / 4 + 255) / 256 * 256;

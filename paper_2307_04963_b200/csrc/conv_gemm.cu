@@ -523,23 +523,39 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int cc = lane, q = quad;
             const int G = a.gap_g;
             const long long ra = m0 + 32 * q;                  // first row of this quarter
-            // 8 shared loads in flight at a time (a 32-value batch spilled the epilogue's registers)
+            // sums of 4-row groups (fixed tree), then combined into G-row groups (G in {4, 8, 16,
+            // 32}, one uniform branch per chunk); the 8 swizzle phases of the shared loads are
+            // hoisted so each load is a base register + immediate
             float* gp = a.gap_part + (size_t)(ra / G) * a.Cout + col0 + c0 + cc;
-            const uint8_t* col = eO32 + (cc & 3) * 4;
-            float sacc = 0.f;
+            const uint8_t* colb = eO32 + (size_t)(32 * q) * 128 + (cc & 3) * 4;
+            uint32_t ph[8];
 #pragma unroll
-            for (int i0 = 0; i0 < 32; i0 += 8) {
-              float v[8];
+            for (int k = 0; k < 8; ++k) ph[k] = (uint32_t)(k * 128 + (((cc >> 2) ^ k) << 4));
+            float s4[8];
 #pragma unroll
-              for (int i = 0; i < 8; ++i) v[i] = *reinterpret_cast<const float*>(col + sw128(32 * q + i0 + i, cc >> 2));
+            for (int g4 = 0; g4 < 8; ++g4) {
+              float v[4];
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                sacc += v[i];
-                if (((i0 + i + 1) & (G - 1)) == 0) {     // a group never straddles M (G | HW)
-                  if (ra + i0 + i < M) gp[(size_t)((i0 + i) / G) * a.Cout] = sacc;
-                  sacc = 0.f;
-                }
+              for (int i = 0; i < 4; ++i) {
+                const int rr = 4 * g4 + i;                  // row within the quarter
+                v[i] = *reinterpret_cast<const float*>(colb + (rr >> 3) * 1024 + ph[rr & 7]);
               }
+              s4[g4] = ((v[0] + v[1]) + v[2]) + v[3];
+            }
+            if (G == 4) {
+#pragma unroll
+              for (int k = 0; k < 8; ++k)
+                if (ra + 4 * k < M) gp[(size_t)k * a.Cout] = s4[k];
+            } else if (G == 8) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                if (ra + 8 * k < M) gp[(size_t)k * a.Cout] = s4[2 * k] + s4[2 * k + 1];
+            } else if (G == 16) {
+#pragma unroll
+              for (int k = 0; k < 2; ++k)
+                if (ra + 16 * k < M) gp[(size_t)k * a.Cout] = (s4[4 * k] + s4[4 * k + 1]) + (s4[4 * k + 2] + s4[4 * k + 3]);
+            } else if (ra < M) {
+              gp[0] = ((s4[0] + s4[1]) + (s4[2] + s4[3])) + ((s4[4] + s4[5]) + (s4[6] + s4[7]));
             }
           }
         }

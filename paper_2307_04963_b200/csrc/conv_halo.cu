@@ -207,6 +207,9 @@ bool halo_plan(const ConvArgs& a, HaloPlan* hp) {
     if (a.H % r == 0 && r * P <= BM) R = r;
   // the halo rows and the furthest row any MMA row reads (tap (1, 1) of virtual row 127) fit a plane
   if (R == 0 || LEAD + (R + 2) * P > PLANE_ROWS || LEAD + 2 * P + BM >= PLANE_ROWS) return false;
+  // >= 75 % of the 128 MMA rows real (small maps -- e.g. 8 x 8, 80 of 128 -- keep the GEMM's
+  // whole-sample row-tap form)
+  if (R * a.W < 96) return false;
   hp->R = R;
   hp->P = P;
   hp->tiles_per_sample = a.H / R;

@@ -131,8 +131,9 @@ NHWC_CASES = [
     # 3x3 / s1 / p1, 64 -> 64: the halo-tile kernel (conv_halo.cu; R output rows per tile, pitch W + 2)
     (2, 56, 56, 64, 64, 3, 1, 1, 1, 0),      # ResNet-50 stage 1: R = 2, P = 58
     (3, 14, 14, 64, 64, 3, 1, 1, 1, 0),      # R = 7, P = 16
-    (2, 5, 7, 64, 64, 3, 1, 1, 0, 0),        # non-square, whole sample in one tile, no ReLU
+    (2, 12, 30, 64, 64, 3, 1, 1, 0, 0),      # non-square, R = 4, P = 32 (128 rows), no ReLU
     (1, 9, 30, 64, 64, 3, 1, 1, 1, 0),       # R = 3 (9 / 3), P = 32
+    (2, 8, 8, 64, 64, 3, 1, 1, 1, 0),        # 8 x 8: 80 of 128 rows real -> the im2col GEMM instead
 ]
 # row-tap GEMM form (path 5): 3x3 / s1 / p1, whole samples per 128-row tile, W | 32, Cout 64
 ROWTAP_NHWC_CASES = [
@@ -292,6 +293,26 @@ def test_run_host_equals_run(r56):
     ph = np.zeros(128, np.int32)
     m.run_host(X, lh, ph)
     assert np.array_equal(lh, l1) and np.array_equal(ph, p1)
+
+
+def test_run_host_batch_above_max_batch():
+    """dycl_run_host with a batch 2.5x the graph's max_batch streams through in max_batch-row
+    sub-chunks: bitwise the device runs' results (each sub-chunk run on its own), in input order,
+    with global offsets carried (min margins identical)."""
+    W = wl.sdn_r56_weights()
+    m = P.build_sdn_resnet56(W, 200)
+    X = wl.image_inputs(wl.INPUT_SEED, 5000, 500)
+    l1, p1 = np.zeros((500, 10), np.float32), np.zeros(500, np.int32)
+    for c0 in range(0, 500, 200):
+        lg, pg = _run_gpu(m, X[c0:c0 + 200])
+        l1[c0:c0 + 200], p1[c0:c0 + 200] = lg, pg
+    lh = np.zeros((500, 10), np.float32)
+    ph = np.zeros(500, np.int32)
+    m.run_host(X, lh, ph)
+    assert np.array_equal(lh, l1) and np.array_equal(ph, p1)
+    mh = np.zeros(500, np.float32)
+    m.run_host(X, lh, ph, global_offset=1000, min_margin=mh)
+    assert np.array_equal(lh, l1) and np.array_equal(ph, p1) and np.isfinite(mh).any()
 
 
 def test_run_host_pipelined_equals_run(r56):
