@@ -490,6 +490,8 @@ struct Exec {
   bool pv[dycl_graph_s::NBUF32] = {};   // d_pool32[f] holds the GAP of every live row of buf32[f]
   int gap_f = -1;                       // buf32 index whose GAP sits in d_gap_pooled (conv_gemm fused GAP)
   bool want_gap = false;                // the subnet being run feeds a head: fuse its GAP when possible
+  const int* in_rows_gemm = nullptr;    // zero-copy exit into an NHWC bottleneck stage: its first 1x1 conv and
+                                        // fused projection read the survivors through this list (no gather)
   const int* in_list = nullptr;         // zero-copy exit: the next subnet's first fused group reads its
                                         // input rows through this list (the survivors) instead of a gather
 
@@ -540,6 +542,25 @@ struct Exec {
     const int hw = c1.in.H * c1.in.W;
     return !c1.residual && c2.residual && c2.res_mode == 1 && lay(c1.in.Cp()) && lay(c1.out.C) && hw <= 128 &&
            128 % hw == 0 && hw % 8 == 0;
+  }
+
+  // A sub-network the NHWC GEMM can enter zero-copy: [block, 1x1/s1 conv (HW % 64 == 0), ...,
+  // projection fused into the block's last conv (output HW % 16 == 0)] -- the block input is read
+  // only by the first conv and by the projection, both through the row list.
+  bool gemm_list_entry(const Subnet& S) const {
+    if (S.layers.size() < 5 || S.layers[0].kind != L_BLOCK) return false;
+    const Layer& c1 = S.layers[1];
+    if (c1.kind != L_CONV || c1.k != 1 || c1.stride != 1 || c1.residual || c1.s4d || !lay(c1.in.Cp()) ||
+        !lay(c1.out.C) || (c1.in.H * c1.in.W) % 64 || c1.in.Cp() % 64 || c1.out.C % 64)
+      return false;
+    for (size_t li = 2; li < S.layers.size() && S.layers[li].kind != L_BLOCK; ++li) {
+      const Layer& L = S.layers[li];
+      if (L.kind == L_PROJ)
+        return li + 1 < S.layers.size() && S.layers[li + 1].fuse_proj &&
+               (S.layers[li + 1].out.H * S.layers[li + 1].out.W) % 16 == 0;
+      if (L.residual) return false;
+    }
+    return false;
   }
 
   // Run subnet s on the rows of `in` (device count `cnt`).  The last layer writes
@@ -715,6 +736,11 @@ struct Exec {
       if (skip_b) a.y = nullptr;
       a.dbg = g->conv_dbg;
       a.y32_pair = g->stream_pair;
+      if (in_rows_gemm && li == 1) a.rows_gather = in_rows_gemm;     // zero-copy entry (gemm_list_entry)
+      if (in_rows_gemm && L.fuse_proj) {
+        a.x2_rows = in_rows_gemm;
+        in_rows_gemm = nullptr;                      // the block input has no other reader
+      }
       const double res_b = a.res_mode ? (a.res32 ? 4.0 : 2.0) * L.res_shape.row_elems() *
                                             (a.res_mode == 2 ? 0.25 : 1.0) : 0.0;
       const double row_b = 2.0 * L.in.row_elems() +
@@ -899,6 +925,12 @@ struct Exec {
                                   fusable(g->subnets[g->nodes[ni + 1].sn], 0);
           if (next_fused && !g->no_zero_copy && !rebal) {
             in_list = g->d_list0;
+            cnt = g->d_counts + s + 1;
+            orig_cur ^= 1;
+            break;
+          }
+          if (next_seq && !g->no_zero_copy && !rebal && gemm_list_entry(g->subnets[g->nodes[ni + 1].sn])) {
+            in_rows_gemm = g->d_list0;                 // the next stage reads the survivors in place
             cnt = g->d_counts + s + 1;
             orig_cur ^= 1;
             break;

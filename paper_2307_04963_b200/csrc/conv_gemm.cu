@@ -234,6 +234,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                       tma_im2col_4d(da + (uint32_t)(sp * HWo * BKE * 2), &tmAL, bar, cb * BKE, -pad, -pad, nn,
                                     (uint16_t)s, (uint16_t)r);
                   }
+                } else if (!IM2COL && a.rows_gather) {
+                  // zero-copy entry: two 64-row boxes, each inside one input sample (HWo % 64 == 0)
+#pragma unroll
+                  for (int h = 0; h < 2; ++h) {
+                    const long long row = p0 + 64 * h;
+                    const int idx = (int)(row / HWo);             // 1x1 / stride 1: HW == HWo
+                    const int src = a.rows_gather[idx < n_live ? idx : (n_live > 0 ? n_live - 1 : 0)];
+                    ptx::tma_load_3d(da + (uint32_t)(h * 64 * BKE * 2), &tmAL, bar, cb * BKE,
+                                     (int)(row - (long long)idx * HWo), src);
+                  }
                 } else if (IM2COL && pl.tshift) {
                   ptx::tma_load_4d(da, &tmA, bar, cb * BKE, s - pad, r - pad, n0);
                 } else if (IM2COL) {
@@ -258,7 +268,18 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint32_t bar = full0 + 8 * stage;
           ptx::mbar_arrive_expect_tx(bar, stage_tx);
           const uint32_t da = ptx::smem_u32(sA + stage * G::A_BYTES);
-          if (stride2 > 1)
+          if (a.x2_rows) {
+            // zero-copy entry: eight 16-pixel im2col boxes, each inside one sample (HWo % 16 == 0)
+#pragma unroll
+            for (int q = 0; q < BM / 16; ++q) {
+              const long long row = p0 + 16 * q;
+              const int idx = (int)(row / HWo);
+              const int pq = (int)(row - (long long)idx * HWo);
+              const int src = a.x2_rows[idx < n_live ? idx : (n_live > 0 ? n_live - 1 : 0)];
+              tma_im2col_4d(da + (uint32_t)(q * 16 * BKE * 2), &tmA2, bar, cb * BKE, (pq % Wo) * stride2,
+                            (pq / Wo) * stride2, src, 0, 0);
+            }
+          } else if (stride2 > 1)
             tma_im2col_4d(da, &tmA2, bar, cb * BKE, wo0 * stride2, ho0 * stride2, n0, 0, 0);
           else
             ptx::tma_load_2d(da, &tmA2, bar, cb * BKE, (int)p0);
@@ -696,6 +717,17 @@ cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t 
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
+  if (!IM2COL && a.rows_gather) {
+    if ((a.H * a.W) % 64) return cudaErrorInvalidValue;
+    cuuint64_t dims[3] = {(cuuint64_t)a.C, (cuuint64_t)a.H * a.W, (cuuint64_t)rows};
+    cuuint64_t strides[2] = {(cuuint64_t)a.C * 2, (cuuint64_t)a.H * a.W * a.C * 2};
+    cuuint32_t box[3] = {BKE, 64, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (enc(&tmAL, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, (void*)a.x, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
   // tiled-shift A operand (GemmPlan::tshift)
   const int HW = a.H * a.W;
   const bool tshift = IM2COL && a.stride == 1 && a.Ho == a.H && a.Wo == a.W && 2 * a.pad + 1 == a.ksz && HW <= BM &&
@@ -718,7 +750,19 @@ cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t 
     }
   }
   CUtensorMap tmA2 = tmB;
-  if (a.x2) {
+  if (a.x2 && a.x2_rows) {
+    // 16-pixel strided im2col boxes of the projection operand (zero-copy entry)
+    if ((a.Ho * a.Wo) % 16) return cudaErrorInvalidValue;
+    cuuint64_t dims[4] = {(cuuint64_t)a.C2, (cuuint64_t)a.W2, (cuuint64_t)a.H2, (cuuint64_t)rows};
+    cuuint64_t strides[3] = {(cuuint64_t)a.C2 * 2, (cuuint64_t)a.W2 * a.C2 * 2, (cuuint64_t)a.H2 * a.W2 * a.C2 * 2};
+    int lower[2] = {0, 0};
+    int upper[2] = {(a.Wo - 1) * a.stride2 - (a.W2 - 1), (a.Ho - 1) * a.stride2 - (a.H2 - 1)};
+    cuuint32_t es[4] = {1, (cuuint32_t)a.stride2, (cuuint32_t)a.stride2, 1};
+    if (enc_i2c(&tmA2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)a.x2, dims, strides, lower, upper, BKE, 16, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  } else if (a.x2) {
     if (a.stride2 > 1) {
       cuuint64_t dims[4] = {(cuuint64_t)a.C2, (cuuint64_t)a.W2, (cuuint64_t)a.H2, (cuuint64_t)rows};
       cuuint64_t strides[3] = {(cuuint64_t)a.C2 * 2, (cuuint64_t)a.W2 * a.C2 * 2, (cuuint64_t)a.H2 * a.W2 * a.C2 * 2};

@@ -41,6 +41,12 @@ struct ConvArgs {
   // rows_out[i] -- the in-place form of a gate's then-branch; nullptr = dense order
   const int* rows_in = nullptr;
   const int* rows_out = nullptr;
+  // conv_gemm only, zero-copy sub-network entry: the rows of the flat A operand
+  // (a 1x1 / stride-1 conv, HW % 64 == 0) belong to input samples rows_gather[m / HW] -- loaded
+  // as 64-row boxes at (pixel, sample) -- and the fused projection operand x2 (HWo % 16 == 0)
+  // to samples x2_rows[m / HWo], loaded as 16-pixel im2col boxes; the output stays dense
+  const int* rows_gather = nullptr;
+  const int* x2_rows = nullptr;
   // conv_gemm only (staged epilogue): fused GAP partials [M / gap_g][Cout] fp32 -- per group of
   // gap_g consecutive output rows (gap_g = the largest power of two <= 32 dividing Ho*Wo, so a
   // group never straddles samples and always covers the same pixels of its sample), the column
