@@ -21,7 +21,9 @@ samples drawn with seed CALIB_SEED=2 (disjoint from the measured inputs):
 * SkipNet with recurrent gates (cfg3r, reading R19): as config 3 but on the raw LSTM output
   r = w_out . h after each gate's cell step; out_i = (s_i w_out, -s_i a_i) in fp32.
 
-Usage:  python -m oracle.calibrate [--n 512] [--cfg 2 3 3r 5]
+* captioning En-Decoder (cfg4c, reading R20): EOS output bias by bisection, mean length ~12.
+
+Usage:  python -m oracle.calibrate [--n 512] [--cfg 2 3 3r 4c 5]
 """
 from __future__ import annotations
 
@@ -169,6 +171,33 @@ def calibrate_cfg3r(n: int, mode: str = "mirror") -> dict:
     return out
 
 
+def calibrate_cfg4c(n: int, mode: str = "mirror", target: float = 12.0) -> dict:
+    """Captioning En-Decoder (reading R20): the EOS output bias by bisection so the mean
+    greedy caption length of n calibration images is ~target (of max_len 32)."""
+    from . import caption as C
+    X = wl.image_inputs(wl.CALIB_SEED, 0, n)
+    P = prg.prepare(wl.caption_weights(calib={"eos_bias": 0.0}))
+    with _pool() as ex:
+        A = list(ex.map(lambda i: C.encode(X[i], P, mode), range(n)))
+
+        def mean_len(b):
+            return float(np.mean(list(ex.map(lambda a: C.decode(a, P, wl.CAP, mode, eos_bias=b)[1], A))))
+
+        lo, hi = -20.0, 40.0                    # mean length decreases with the bias
+        for _ in range(30):
+            mid = 0.5 * (lo + hi)
+            if mean_len(mid) > target:
+                lo = mid
+            else:
+                hi = mid
+        b = float(np.float32(0.5 * (lo + hi)))
+        ml = mean_len(b)
+    return {"eos_bias": b, "mean_length": ml,
+            "_recipe": "oracle/calibrate.py calibrate_cfg4c: n=%d calibration images (seed %d), mode=%s, EOS "
+                       "output bias by bisection to a mean greedy caption length of %.1f" % (n, wl.CALIB_SEED, mode,
+                                                                                          target)}
+
+
 def calibrate_cfg5(n: int, mode: str = "mirror") -> dict:
     """Config 5 heads (exits after stages 1-3, 1000 classes): same recipe as config 2."""
     X = wl.image_inputs(wl.CALIB_SEED, 0, n, hw=224)
@@ -224,7 +253,7 @@ def main():
     a = ap.parse_args()
     os.makedirs(os.path.join(wl.HERE, "calib"), exist_ok=True)
     for c in a.cfg:
-        res = {"2": lambda: calibrate_cfg2(a.n), "3": lambda: calibrate_cfg3(a.n), "3r": lambda: calibrate_cfg3r(a.n),
+        res = {"2": lambda: calibrate_cfg2(a.n), "3": lambda: calibrate_cfg3(a.n), "3r": lambda: calibrate_cfg3r(a.n), "4c": lambda: calibrate_cfg4c(64),
                "5": lambda: calibrate_cfg5(a.n5)}[str(c)]()
         path = os.path.join(wl.HERE, "calib", f"cfg{c}.json")
         with open(path, "w") as f:

@@ -499,6 +499,38 @@ def seq2seq_weights(seed: int = WEIGHT_SEED) -> dict:
     return W
 
 
+# ----------------------------------------------------------------------------
+# Image-captioning En-Decoder (reading R20): CIFAR ResNet-38 trunk encoder (its
+# 8x8x64 output = 64 annotation vectors), soft-attention LSTM decoder (hidden 256, word
+# embeddings 256, vocabulary 4096), greedy, EOS / max-len 32 guard.  EOS output bias calibrated
+# (oracle/calibrate.py cfg4c) to a mean caption length of ~12.
+# ----------------------------------------------------------------------------
+CAP = dict(vocab=4096, emb=256, hidden=256, max_len=32, pad=0, bos=1, eos=2, L=64, D=64)
+CAP_SEED_OFFSET = 6000
+
+
+def caption_weights(seed: int = WEIGHT_SEED, calib=None) -> dict:
+    W, _ = resnet_cifar_trunk(R38, seed + CAP_SEED_OFFSET)
+    c = CAP
+    V, E, H, D = c["vocab"], c["emb"], c["hidden"], c["D"]
+    rng = _Rng([seed, 7000])
+    k = 1.0 / math.sqrt(H)
+    W["init.w"] = _bf16(rng.next().standard_normal((2 * H, D)) / math.sqrt(D) * 2.0)
+    W["init.b"] = rng.next().uniform(-0.1, 0.1, 2 * H).astype(np.float32)
+    W["att.w"] = _bf16(rng.next().standard_normal((D, H)) / math.sqrt(H) * 4.0)
+    W["att.b"] = rng.next().uniform(-0.1, 0.1, D).astype(np.float32)
+    W["emb"] = _bf16(rng.next().standard_normal((V, E)))
+    W["lstm.w"] = _bf16(rng.next().uniform(-k, k, (4 * H, E + D + H)))
+    W["lstm.b"] = rng.next().uniform(-2 * k, 2 * k, 4 * H).astype(np.float32)
+    W["out.w"] = _bf16(rng.next().standard_normal((V, H)) / math.sqrt(H) * 8.0)
+    W["out.b"] = rng.next().uniform(-0.1, 0.1, V).astype(np.float32)
+    if calib is None:
+        calib = load_calib("cfg4c")
+    if calib is not None:
+        W["out.b"][c["eos"]] = np.float32(calib["eos_bias"])
+    return W
+
+
 CONFIGS = {
     1: dict(name="mlp_ee", batch=32, desc="tiny early-exit MLP: 3 blocks width 64, 2 exit heads, tau 0.9, batch 32"),
     2: dict(name="sdn_resnet56", batch=4096, desc="ShallowDeep-style early-exit ResNet-56, 32x32x3, batch 4096, 4 ICs"),
