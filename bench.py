@@ -118,6 +118,9 @@ WORKLOADS = {
        "tau=0.9, global batch 65536 sharded over the GPUs (inputs resident in HBM, chunks of 2048 per dycl_run)",
 }
 BATCHES = {1: 32, 2: 4096, 3: 8192, 4: 1024, 5: 65536}
+CAP_WORKLOAD = ("image-captioning En-Decoder (SURVEY 8(f)4): CIFAR ResNet-38 trunk encoder (8x8x64 annotation "
+                "vectors), soft-attention LSTM decoder (hidden 256, vocab 4096), greedy with EOS / max-len 32 guard, "
+                "batch 1024 synthetic 32x32x3 images per GPU")
 RNN_NOTE = " -- variant: recurrent LSTM gates (SkipNet RNN gate, Table 3 ID 5), hidden 10, shared across the 17 gates"
 KERNEL_NAMES = {
     "block": "k_block_fused (a1: 1-8 whole residual blocks per sample, SMEM-resident, row-tap tcgen05 convs)",
@@ -127,13 +130,24 @@ KERNEL_NAMES = {
 }
 
 
-def oracle_sample(cfg, n, start=0, rnn=False):
+def oracle_sample(cfg, n, start=0, rnn=False, caption=False):
     """The oracle (as it stands, mirror mode, all host cores) on n seeded samples of config cfg.
     Returns (samples/s, cores, seconds, description)."""
     import oracle as O
     import workloads as wl
     from oracle import programs as prg
     cores = len(os.sched_getaffinity(0))
+    if caption:
+        from concurrent.futures import ThreadPoolExecutor
+        from oracle import caption as C
+        P = prg.prepare(wl.caption_weights())
+        X = wl.image_inputs(wl.INPUT_SEED, start, n)
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(cores) as ex:
+            list(ex.map(lambda i: C.caption(X[i], P, wl.CAP, "mirror"), range(n)))
+        dt = time.perf_counter() - t0
+        return n / dt, cores, dt, (f"{n} captioning images (seeded inputs {start}..{start + n - 1}), per-image fp64 "
+                                   f"encoder + greedy decode, mirror mode")
     if cfg == 4:
         from concurrent.futures import ThreadPoolExecutor
         from oracle import seq2seq as S
@@ -173,7 +187,8 @@ def run_reference(args):
     what = ""
     cores = len(os.sched_getaffinity(0))
     for i in range(args.warmup + args.steps):
-        _, cores, dt, what = oracle_sample(args.config, per_step, start=i * per_step, rnn=args.rnn_gates)
+        _, cores, dt, what = oracle_sample(args.config, per_step, start=i * per_step, rnn=args.rnn_gates,
+                                           caption=args.caption)
         if i >= args.warmup:
             times.append(dt)
     tot = sum(times)
@@ -308,6 +323,55 @@ class S2SJob:
         return {"mean_length": float(ln.mean()), "tokens": int(ln.sum())}
 
 
+class CapJob:
+    """--caption: the image-captioning En-Decoder (reading R20): one step = the CNN
+    encoder graph + the guarded soft-attention LSTM decode of the per-rank batch of 1024 images."""
+
+    def __init__(self, cfg, rank, ws, dev, torch, rebalance, rnn=False):
+        import workloads as wl
+        from paper_2307_04963_b200 import programs as P
+        self.cfg, self.torch = cfg, torch
+        self.B = 1024
+        self.n_chunks = 1
+        self.rebalance = False
+        c = wl.CAP
+        self.model = P.build_caption(wl.caption_weights(), c, self.B, device=dev.index or 0)
+        self.g = None
+        X = wl.image_inputs(wl.INPUT_SEED, rank * self.B, self.B)
+        self.x = torch.from_numpy(X).to(dev)
+        self.tok = torch.empty((self.B, c["max_len"]), dtype=torch.int32, device=dev)
+        self.len = torch.empty(self.B, dtype=torch.int32, device=dev)
+        self.feats = torch.empty((self.B, c["L"], c["D"]), dtype=torch.int16, device=dev)
+        self.h2d = int(X.nbytes)
+        self.d2h = int(self.B * (c["max_len"] + 1) * 4)
+
+    def step(self, stream, after_chunk=None):
+        self.model.run(self.x, self.tok, self.len, stream=stream, features=self.feats)
+        if after_chunk:
+            after_chunk()
+
+    def host_setup(self):
+        torch = self.torch
+        self.xh = self.x.cpu().pin_memory()
+        self.th = torch.empty(tuple(self.tok.shape), dtype=torch.int32).pin_memory()
+        self.lh = torch.empty(self.B, dtype=torch.int32).pin_memory()
+
+    def step_host(self, stream):
+        # the public call chain with host buffers: H2D of the images, encoder + decoder, D2H
+        self.x.copy_(self.xh, non_blocking=True)
+        self.model.run(self.x, self.tok, self.len, stream=stream, features=self.feats)
+        self.th.copy_(self.tok, non_blocking=True)
+        self.lh.copy_(self.len, non_blocking=True)
+        self.torch.cuda.current_stream().synchronize()
+
+    def check_host(self):
+        return bool(np.array_equal(self.lh.numpy(), self.len.cpu().numpy()))
+
+    def hist(self):
+        ln = self.len.cpu().numpy()
+        return {"mean_length": float(ln.mean()), "tokens": int(ln.sum())}
+
+
 def _traffic(cfg, kind):
     """ncu DRAM bytes per launch of the dominant kernel class (profiles/r02_traffic.json, one
     `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum` capture of one step / chunk)."""
@@ -329,8 +393,8 @@ def run_dycl(args):
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     stream = torch.cuda.current_stream()
-    job = (S2SJob if args.config == 4 else ImageJob)(args.config, rank, ws, dev, torch, not args.no_rebalance,
-                                                     rnn=args.rnn_gates)
+    job_cls = CapJob if args.caption else S2SJob if args.config == 4 else ImageJob
+    job = job_cls(args.config, rank, ws, dev, torch, not args.no_rebalance, rnn=args.rnn_gates)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > L2 (126 MB)
 
     for _ in range(args.warmup):
@@ -358,7 +422,9 @@ def run_dycl(args):
     # of pass 1: the event pairs perturb the step time).
     kind_tot = {}                              # kind -> [ms, bytes, flops, launches, records]
     n_prof = [0]
-    if job.g is not None:
+    if args.caption:
+        prof_read = lambda: []                           # noqa: E731  (no per-launch profiling here)
+    elif job.g is not None:
         D.dycl_set_profiling(job.g, 1)
         prof_read = lambda: D.dycl_profile_read(job.g)   # noqa: E731
     else:
@@ -379,11 +445,14 @@ def run_dycl(args):
         flush.zero_()
         job.step(stream, after_chunk=collect)
     torch.cuda.synchronize()
-    if job.g is not None:
+    if args.caption:
+        launches = (D.dycl_cap_launches(job.model.h) + D.dycl_launches_per_run(job.model.enc.g)) * args.steps
+    elif job.g is not None:
         D.dycl_set_profiling(job.g, 0)
+        launches = n_prof[0]                   # this library's kernels in K steps (profiled pass)
     else:
         D.dycl_s2s_set_profiling(job.model.h, 0)
-    launches = n_prof[0]                       # this library's kernels in K steps (profiled pass)
+        launches = n_prof[0]
     kind_ms = {k: v[0] for k, v in kind_tot.items()}
     hist = job.hist()
 
@@ -413,7 +482,8 @@ def run_dycl(args):
         return
 
     hbm, tf_burst, tf_sus, peak_src = _peaks()
-    global_samples = BATCHES[args.config] if args.config in GLOBAL_BATCH_CONFIGS else BATCHES[args.config] * ws
+    global_samples = (1024 * ws if args.caption else
+                      BATCHES[args.config] if args.config in GLOBAL_BATCH_CONFIGS else BATCHES[args.config] * ws)
     value = global_samples * args.steps / (total_ms / 1e3)
     # a step of >= 100 ms keeps the tensor pipe busy long enough to reach the sustained
     # (power-limited) clock: the sustained peak applies; shorter steps: the burst peak
@@ -468,7 +538,8 @@ def run_dycl(args):
         "ms_per_step": total_ms / args.steps, "ms_per_step_std": float(np.std(step_ms)),
         "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config] + (RNN_NOTE if args.rnn_gates and args.config == 3 else ""),
+        "config": {"workload": (CAP_WORKLOAD if args.caption else
+                                WORKLOADS[args.config] + (RNN_NOTE if args.rnn_gates and args.config == 3 else "")),
                    "global_batch": global_samples,
                    "batch_per_gpu": job.B, "chunks_per_gpu": job.n_chunks,
                    "precision": "bf16 tensor-core operands, fp32 accumulate, fp32 residual stream",
@@ -485,11 +556,11 @@ def run_dycl(args):
         "roofline": roof,
         "kernel_ms_per_step": {k: v / args.steps for k, v in sorted(kind_ms.items(), key=lambda kv: -kv[1])},
     }
-    if args.config == 4:
+    if args.config == 4 or args.caption:
         line["tokens_per_s"] = hist["tokens"] * ws * args.steps / (total_ms / 1e3)
     if ws == 1 and not args.no_cpu_baseline:
-        n_cpu = args.cpu_samples or {1: 4096, 2: 4096, 3: 2048, 4: 48, 5: 64}[args.config]
-        rate, cores, dt, what = oracle_sample(args.config, n_cpu, rnn=args.rnn_gates)
+        n_cpu = args.cpu_samples or (64 if args.caption else {1: 4096, 2: 4096, 3: 2048, 4: 48, 5: 64}[args.config])
+        rate, cores, dt, what = oracle_sample(args.config, n_cpu, rnn=args.rnn_gates, caption=args.caption)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
                                 "sample": f"{what}, {dt:.1f} s wall"}
     print(json.dumps(line), flush=True)
@@ -509,6 +580,8 @@ def main():
     ap.add_argument("--ref-samples", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rebalance", action="store_true", help="N > 1: no survivor rebalancing")
+    ap.add_argument("--caption", action="store_true",
+                    help="the image-captioning En-Decoder (SURVEY 8(f)4): CNN encoder + soft-attention LSTM decoder")
     ap.add_argument("--rnn-gates", action="store_true",
                     help="config 3 with SkipNet's recurrent (LSTM) gates (SURVEY 8(f)3, Table 3 ID 5)")
     args = ap.parse_args()

@@ -201,6 +201,10 @@ typedef struct {
                              gate predicates evaluated along its path of |p - threshold| (p = max
                              softmax for exits, sigmoid for gates; +inf if none) -- the quantity the
                              north star's "within 1e-3 of its threshold" band is defined on (R12) */
+  uint16_t* features;     /* device bf16 [batch][H][W][C] (NHWC) or NULL: the tensor entering the final
+                             head, in input order -- the encoder output of an En-Decoder
+                             (dycl_cap_run).  Plain graphs only (no exit / gate nodes) whose final
+                             tensor is NHWC (C % 64 == 0); else DYCL_E_UNSUPPORTED */
 } dycl_io;
 
 /* Enqueue one batched inference on `stream` (a cudaStream_t, NULL = default stream).
@@ -379,6 +383,40 @@ dycl_status dycl_s2s_launches(dycl_s2s s, int32_t* out);
 dycl_status dycl_s2s_set_profiling(dycl_s2s s, int enable);
 dycl_status dycl_s2s_profile_read(dycl_s2s s, int32_t max_n, int32_t* kind, float* ms,
                                   double* bytes, double* flops, int32_t* n_out);
+
+/* ------------------------------------ image-captioning En-Decoder --- */
+/* The paper's En-Decoder ("Image caption / token wise caption generation"; L323:
+ * Show, Attend and Tell).  Encoder = an image graph (any dycl_graph) whose final tensor is
+ * exported with dycl_io.features: L = H*W annotation vectors of D = C dims.  This graph is the
+ * decoder loop (reading R20): h, c = tanh(init_w[:H] mean(a) + b), tanh(init_w[H:] ...);
+ * per step q = att_w h + att_b, alpha = softmax_j(a_j . q / sqrt(D)), z = sum alpha_j a_j, one LSTM
+ * cell on [emb[y]; z] with h (gate rows i, f, g, o; lstm_w [4H][E + D + H], lstm_b = b_ih + b_hh),
+ * logits = out_w h + out_b, greedy argmax (lowest index on ties); the loop guard of
+ * dycl_s2s_set_loop_guard's semantics without the length bias: a caption is done after EOS
+ * (counted in its length) or max_len steps, PAD after.  Each step runs on the still-active captions
+ * only (compacted on the device); no host synchronisation.  bf16 weights [n_out][n_in], fp32 biases;
+ * host pointers copied.  Constraints: D == 64, L <= 64, hidden and emb multiples of 64, vocab of
+ * 256, max_len <= 64 (else DYCL_E_UNSUPPORTED). */
+typedef struct dycl_cap_s* dycl_cap;
+typedef struct {
+  int vocab, emb, hidden;
+  int feat_len, feat_dim;    /* L, D */
+  int max_len, pad, bos, eos;
+} dycl_cap_config;
+dycl_status dycl_cap_create(int cuda_device, const dycl_cap_config* cfg, dycl_cap* out);
+dycl_status dycl_cap_destroy(dycl_cap c);
+const char* dycl_cap_last_error(dycl_cap c);
+dycl_status dycl_cap_set_weights(dycl_cap c, const uint16_t* init_w, const float* init_b, const uint16_t* att_w,
+                                 const float* att_b, const uint16_t* emb, const uint16_t* lstm_w,
+                                 const float* lstm_b, const uint16_t* out_w, const float* out_b);
+dycl_status dycl_cap_finalize(dycl_cap c, int64_t max_batch);
+/* features: device bf16 [batch][L][D]; tokens int32 [batch][max_len] (out); lengths int32 [batch]
+ * (out); top1 fp32 [batch][max_len] (out, the chosen token's logit, NaN after done) or NULL.
+ * Stream-ordered.  Errors: INVALID_ARG, STATE, SHAPE_MISMATCH (batch > max_batch), CUDA. */
+dycl_status dycl_cap_run(dycl_cap c, const uint16_t* features, int64_t batch, int32_t* tokens, int32_t* lengths,
+                         float* top1, void* stream);
+/* Number of this library's kernels the last dycl_cap_run launched. */
+dycl_status dycl_cap_launches(dycl_cap c, int32_t* out);
 
 /* ------------------------------------------------------------ test hook ---- */
 /* Run ONE conv2d layer (the a1 tensor-core kernel, same code path dycl_run uses)

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdycl.so")
-SOURCES = ["api.cpp", "comm.cpp", "s2s_api.cpp", "conv_tc.cu", "conv_tma.cu", "conv_gemm.cu", "conv_halo.cu", "gemm_tma.cu", "block_fused.cu", "hostmod.cu", "s2s_kernels.cu"]
+SOURCES = ["api.cpp", "comm.cpp", "s2s_api.cpp", "conv_tc.cu", "conv_tma.cu", "conv_gemm.cu", "conv_halo.cu", "gemm_tma.cu", "block_fused.cu", "hostmod.cu", "s2s_kernels.cu", "cap.cu"]
 HEADERS = ["kernels.h", "comm.h", "ptx.cuh", "epilogue.cuh", "s2s_kernels.h", os.path.join("..", "..", "include", "dycl.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -457,6 +457,7 @@ struct Exec {
   float* out_logits;
   int32_t* out_path;
   float* out_margin = nullptr;       // per-sample min |predicate - threshold| (or nullptr)
+  uint16_t* out_features = nullptr;  // dycl_io.features: the final head's input tensor (plain graphs)
   long long global_offset = 0;       // global index of row 0 (rebalanced rows carry their id)
   int own = 0;                       // the rank's own rows (result space rows [0, own))
   int slot = 1;               // next free count slot
@@ -1084,6 +1085,14 @@ struct Exec {
           break;
         }
         case N_FINAL: {
+          if (out_features) {
+            // the encoder output of an En-Decoder: rows are in input order in a plain graph
+            if (g->n_exits || g->n_gates || cur.b < 0 || !lay(N.in.Cp()) || N.in.C % 64)
+              return fail(g, DYCL_E_UNSUPPORTED, "features output: plain graphs with an NHWC final tensor only");
+            e = cudaMemcpyAsync(out_features, g->buf[cur.b], (size_t)batch * N.in.row_elems() * 2,
+                                cudaMemcpyDeviceToDevice, st);
+            if (e != cudaSuccess) return cuda_fail(g, e, "features copy");
+          }
           if ((r = head(g->subnets[N.sn], cur, cnt, 2, 0.f))) return r;
           int s;
           if ((r = compact(cnt, 0, 0, orig_cur, &s, false, 0.f))) return r;
@@ -1744,7 +1753,7 @@ dycl_status dycl_finalize(dycl_graph g, int64_t max_batch) {
 
 static dycl_status run_impl(dycl_graph g, const float* input, int64_t batch, float* logits, int32_t* path,
                             int32_t* node_counts, cudaStream_t st, long long global_offset = 0,
-                            float* min_margin = nullptr) {
+                            float* min_margin = nullptr, uint16_t* features = nullptr) {
   if (!g->finalized) return fail(g, DYCL_E_STATE, "graph not finalized");
   if (batch < 0 || batch > g->max_batch) return fail(g, DYCL_E_SHAPE_MISMATCH, "batch > max_batch");
   if (batch > 0 && (!input || !logits || !path)) return fail(g, DYCL_E_INVALID_ARG, "null io pointer");
@@ -1772,9 +1781,10 @@ static dycl_status run_impl(dycl_graph g, const float* input, int64_t batch, flo
     }
   } else if (batch == 0) {
     CK(cudaMemsetAsync(g->d_counts, 0, g->n_slots * sizeof(int), st));
-  } else if (!g->use_graph || g->profiling || g->dbg_ts) {
+  } else if (!g->use_graph || g->profiling || g->dbg_ts || features) {
     Exec ex{g, st, (int)batch, logits, path};
     ex.out_margin = min_margin;
+    ex.out_features = features;
     ex.own = (int)batch;
     if (dycl_status s = ex.run(input)) return s;
     g->launches_per_run = ex.nlaunch;
@@ -1827,7 +1837,7 @@ static dycl_status run_impl(dycl_graph g, const float* input, int64_t batch, flo
 dycl_status dycl_run(dycl_graph g, const dycl_io* io, void* stream) {
   if (!g || !io) return DYCL_E_INVALID_ARG;
   return run_impl(g, io->input, io->batch, io->logits, io->path, io->node_counts, (cudaStream_t)stream,
-                  io->global_offset, io->min_margin);
+                  io->global_offset, io->min_margin, io->features);
 }
 
 static dycl_status run_host_impl(dycl_graph g, const float* input_host, int64_t batch, long long global_offset,

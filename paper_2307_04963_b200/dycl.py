@@ -34,11 +34,16 @@ class DyclError(RuntimeError):
 class dycl_io(ctypes.Structure):
     _fields_ = [("input", ctypes.c_void_p), ("batch", ctypes.c_int64), ("logits", ctypes.c_void_p),
                 ("path", ctypes.c_void_p), ("node_counts", ctypes.c_void_p), ("global_offset", ctypes.c_int64),
-                ("min_margin", ctypes.c_void_p)]
+                ("min_margin", ctypes.c_void_p), ("features", ctypes.c_void_p)]
 
 
 DYCL_REBALANCE_NONE = 0
 DYCL_REBALANCE_ALL = -1
+
+
+class dycl_cap_config(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in ("vocab", "emb", "hidden", "feat_len", "feat_dim", "max_len", "pad", "bos",
+                                            "eos")]
 
 
 class dycl_s2s_config(ctypes.Structure):
@@ -66,6 +71,8 @@ EXPORTS = [
     "dycl_run_host_ex", "dycl_set_comm", "dycl_local_group_create", "dycl_local_group_destroy",
     "dycl_set_comm_local", "dycl_rebalance_stats", "dycl_nccl_get_unique_id", "dycl_nccl_comm_init_rank",
     "dycl_nccl_comm_destroy", "dycl_s2s_set_precision",
+    "dycl_cap_create", "dycl_cap_destroy", "dycl_cap_last_error", "dycl_cap_set_weights", "dycl_cap_finalize",
+    "dycl_cap_run", "dycl_cap_launches",
 ]
 
 
@@ -136,12 +143,22 @@ def lib():
             "dycl_s2s_set_profiling": [vp, i32],
             "dycl_s2s_profile_read": [vp, i32, Pi, Pf, Pd, Pd, Pi],
         })
+        sig.update({
+            "dycl_cap_create": [i32, ctypes.POINTER(dycl_cap_config), ctypes.POINTER(vp)],
+            "dycl_cap_destroy": [vp],
+            "dycl_cap_set_weights": [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp],
+            "dycl_cap_finalize": [vp, i64],
+            "dycl_cap_run": [vp, vp, i64, vp, vp, vp, vp],
+            "dycl_cap_launches": [vp, Pi],
+        })
         for name, args in sig.items():
             fn = getattr(L, name)
             fn.argtypes = args
             fn.restype = ctypes.c_int
         L.dycl_last_error.argtypes = [vp]
         L.dycl_last_error.restype = ctypes.c_char_p
+        L.dycl_cap_last_error.argtypes = [vp]
+        L.dycl_cap_last_error.restype = ctypes.c_char_p
         L.dycl_s2s_last_error.argtypes = [vp]
         L.dycl_s2s_last_error.restype = ctypes.c_char_p
         _lib = L
@@ -268,11 +285,14 @@ def dycl_finalize(g, max_batch):
     _ck(lib().dycl_finalize(g, int(max_batch)), g)
 
 
-def dycl_run(g, input, batch, logits, path, node_counts=None, stream=None, global_offset=0, min_margin=None):
-    """input/logits/path/node_counts/min_margin: CUDA torch tensors (fp32, fp32, int32, int32, fp32)."""
+def dycl_run(g, input, batch, logits, path, node_counts=None, stream=None, global_offset=0, min_margin=None,
+             features=None):
+    """input/logits/path/node_counts/min_margin/features: CUDA torch tensors (fp32, fp32, int32, int32,
+    fp32, bf16 bits as int16)."""
     io = dycl_io(input.data_ptr(), int(batch), logits.data_ptr(), path.data_ptr(),
                  node_counts.data_ptr() if node_counts is not None else None, int(global_offset),
-                 min_margin.data_ptr() if min_margin is not None else None)
+                 min_margin.data_ptr() if min_margin is not None else None,
+                 features.data_ptr() if features is not None else None)
     _ck(lib().dycl_run(g, ctypes.byref(io), _stream_ptr(stream)), g)
 
 
@@ -508,3 +528,47 @@ def dycl_debug_timestamps(g):
     buf = (ctypes.c_longlong * 128)()
     _ck(lib().dycl_debug_timestamps(g, buf), g)
     return np.array(buf[:], dtype=np.int64).reshape(8, 16)
+
+
+# ------------------------------------------------------------------ captioning En-Decoder
+def _cap_ck(status, c=None):
+    if status != 0:
+        raise DyclError(status, lib().dycl_cap_last_error(c).decode(errors="replace"))
+
+
+def dycl_cap_create(cuda_device, cfg: dict):
+    c = dycl_cap_config(*(int(cfg[k]) for k in ("vocab", "emb", "hidden", "L", "D", "max_len", "pad", "bos", "eos")))
+    h = ctypes.c_void_p()
+    _cap_ck(lib().dycl_cap_create(cuda_device, ctypes.byref(c), ctypes.byref(h)))
+    return h
+
+
+def dycl_cap_destroy(c):
+    _cap_ck(lib().dycl_cap_destroy(c), c)
+
+
+def dycl_cap_last_error(c=None) -> str:
+    return lib().dycl_cap_last_error(c).decode(errors="replace")
+
+
+def dycl_cap_set_weights(c, init_w, init_b, att_w, att_b, emb, lstm_w, lstm_b, out_w, out_b):
+    keep = [_hp(init_w, np.uint16), _hp(init_b, np.float32), _hp(att_w, np.uint16), _hp(att_b, np.float32),
+            _hp(emb, np.uint16), _hp(lstm_w, np.uint16), _hp(lstm_b, np.float32), _hp(out_w, np.uint16),
+            _hp(out_b, np.float32)]
+    _cap_ck(lib().dycl_cap_set_weights(c, *[p for _, p in keep]), c)
+
+
+def dycl_cap_finalize(c, max_batch):
+    _cap_ck(lib().dycl_cap_finalize(c, int(max_batch)), c)
+
+
+def dycl_cap_run(c, features, batch, tokens, lengths, top1=None, stream=None):
+    _cap_ck(lib().dycl_cap_run(c, ctypes.c_void_p(features.data_ptr()), int(batch), ctypes.c_void_p(tokens.data_ptr()),
+                               ctypes.c_void_p(lengths.data_ptr()),
+                               ctypes.c_void_p(top1.data_ptr()) if top1 is not None else None, _stream_ptr(stream)), c)
+
+
+def dycl_cap_launches(c) -> int:
+    n = ctypes.c_int32()
+    _cap_ck(lib().dycl_cap_launches(c, ctypes.byref(n)), c)
+    return n.value

@@ -254,4 +254,63 @@ def build_seq2seq(W, cfg, max_batch, device=0, precision=D.DYCL_PREC_BF16) -> Se
     return Seq2Seq(h, cfg, max_batch)
 
 
+class Caption:
+    """The captioning En-Decoder (reading R20): the encoder image graph (its final
+    tensor exported through dycl_io.features) chained with the decoder loop graph (dycl_cap_*) --
+    the host program P_Host of Listing 2: run the encoder sub-network, then the guarded loop."""
+
+    def __init__(self, enc, h, cfg, max_batch):
+        self.enc, self.h, self.cfg, self.max_batch = enc, h, cfg, max_batch
+
+    def run(self, x, tokens, lengths, top1=None, stream=None, features=None):
+        """x: CUDA fp32 [B][32][32][3]; tokens int32 [B][max_len], lengths int32 [B], top1 fp32
+        [B][max_len] or None (outputs).  Returns the encoder's annotation vectors (bf16 bits)."""
+        import torch
+        B = x.shape[0]
+        feats = features if features is not None else \
+            torch.empty((B, self.cfg["L"], self.cfg["D"]), dtype=torch.int16, device=x.device)
+        lg = torch.empty((B, self.enc.K), device=x.device)
+        pa = torch.empty(B, dtype=torch.int32, device=x.device)
+        D.dycl_run(self.enc.g, x, B, lg, pa, stream=stream, features=feats)
+        D.dycl_cap_run(self.h, feats, B, tokens, lengths, top1, stream)
+        return feats
+
+    def close(self):
+        if self.h is not None:
+            D.dycl_cap_destroy(self.h)
+            self.h = None
+        self.enc.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def build_caption(W, cfg, max_batch, device=0, precision=FP32_STREAM) -> Caption:
+    """Captioning En-Decoder, rewritten: the encoder sub-network (the CIFAR ResNet-38 trunk, one
+    conditional-free subnet; a small head closes the image graph, its output unused) and the
+    decoder-step sub-networks + LM head under the loop guard (dycl_cap_*)."""
+    g = _create(device, 32, 32, 3, precision)
+    sn = D.dycl_subnet_begin(g)
+    D.dycl_subnet_conv2d(g, sn, 3, 16, 3, 1, 1, W["stem.w"], W["stem.b"], RELU, 0)
+    for i in range(1, 19):
+        _block(g, sn, W, i, *_block_io(i, 6))
+    D.dycl_subnet_end(g, sn)
+    D.dycl_seq(g, sn)
+    head = D.dycl_subnet_begin(g)
+    D.dycl_subnet_gap(g, head)
+    D.dycl_subnet_dense(g, head, 64, 16, np.zeros((16, 64), np.uint16), np.zeros(16, np.float32), NONE, 1)
+    D.dycl_subnet_end(g, head)
+    D.dycl_final(g, head)
+    D.dycl_finalize(g, max_batch)
+    enc = Model(g, (32, 32, 3), 16, max_batch, "caption_encoder")
+    h = D.dycl_cap_create(device, cfg)
+    D.dycl_cap_set_weights(h, W["init.w"], W["init.b"], W["att.w"], W["att.b"], W["emb"], W["lstm.w"], W["lstm.b"],
+                           W["out.w"], W["out.b"])
+    D.dycl_cap_finalize(h, max_batch)
+    return Caption(enc, h, dict(cfg), max_batch)
+
+
 BUILDERS = {1: build_mlp_ee, 2: build_sdn_resnet56, 3: build_skipnet_resnet38, 5: build_resnet50_ee}
