@@ -53,6 +53,10 @@ struct Layer {
   // 4*cout channels; d_w / d_b then hold that packed form ([4*cout][9*64], [4*cout])
   int s4d = 0;
   int pool_s2d = 0;           // maxpool reading that phase layout (3x3 / stride 2 / pad 1)
+  // 2x2 space-to-depth stem (opt-in, measured slower than s4d): the 7x7 / stride-2 conv on <= 4 channels as a 4x4 /
+  // stride-1 conv over 2x2 pixel blocks (16 channels) with padding 2 before / 1 after, on the
+  // halo-tile kernel (conv_halo.cu); d_w holds [cout][16 taps x 16] ; output plain NHWC
+  int s2d2 = 0;
   uint16_t* d_wt = nullptr;   // wide fp32 heads (K >= 128): weights transposed [C][K] for the batched FC
   uint16_t* d_w2 = nullptr;   // wide fp32 heads on the tensor cores: [W | W] [kpad][2C] (split-bf16 GEMM)
   float* d_b2 = nullptr;      // bias padded to kpad
@@ -151,6 +155,7 @@ struct dycl_graph_s {
   cudaEvent_t ev_h2d[2] = {}, ev_run[2] = {}, ev_d2h[2] = {};
   int nhwc = 0;                      // bf16 activations NHWC (decided at finalize; DYCL_NHWC=0 disables)
   int stem_s4d = 0;                  // input cast to 4x4 space-to-depth for the stem (DYCL_STEM_S4D=0 disables)
+  int stem_s2d2 = 0;                 // input cast to 2x2 space-to-depth, 16 channels (opt-in DYCL_STEM_S2D2=1)
   long long* dbg_ts = nullptr;       // DYCL_TS=1: fused-block phase timestamps (development)
   int dbg_ts_conv = 0;               // DYCL_TS_CONV=k: record conv_gemm phases of the k-th conv launch
   int dbg_ts_pick = 0;               // DYCL_TS=k > 1: record the k-th fused launch of a run (else the last)
@@ -355,6 +360,29 @@ dycl_status upload_subnet(dycl_graph g, Subnet& s) {
       CK(cudaMemcpy(L.d_bcat, bc.data(), bc.size() * 4, cudaMemcpyHostToDevice));
       L.fuse_proj = 1;
     }
+    if (L.kind == L_CONV && L.s2d2) {
+      // W'[o][(R*4+S)*16 + (dy*2+dx)*Cin + c] = w[o][2R+dy-1][2S+dx-1][c] (zero outside the 7x7
+      // window): output pixel y reads input rows 2y-3 .. 2y+3 = blocks y-2 .. y+1 (tap R = block - y + 2)
+      const int Cin = L.in.C, co = L.cout, K2 = 16 * 16;
+      std::vector<uint16_t> w2((size_t)co * K2, 0);
+      for (int o = 0; o < co; ++o)
+        for (int R = 0; R < 4; ++R)
+          for (int S = 0; S < 4; ++S)
+            for (int dy = 0; dy < 2; ++dy)
+              for (int dx = 0; dx < 2; ++dx) {
+                const int r = 2 * R + dy - 1, s2 = 2 * S + dx - 1;
+                if (r < 0 || r >= L.k || s2 < 0 || s2 >= L.k) continue;
+                for (int c = 0; c < Cin; ++c)
+                  w2[(size_t)o * K2 + (R * 4 + S) * 16 + (dy * 2 + dx) * Cin + c] =
+                      L.w[(((size_t)o * L.k + r) * L.k + s2) * Cin + c];
+              }
+      dycl_status st = dmalloc(g, &L.d_w, w2.size() * 2);
+      if (st) return st;
+      CK(cudaMemcpy(L.d_w, w2.data(), w2.size() * 2, cudaMemcpyHostToDevice));
+      if ((st = dmalloc(g, &L.d_b, L.b.size() * 4))) return st;
+      CK(cudaMemcpy(L.d_b, L.b.data(), L.b.size() * 4, cudaMemcpyHostToDevice));
+      continue;
+    }
     if (L.kind == L_CONV && L.s4d) {
       // W'[(b*2+b')*cout + o][(R*3+S)*64 + (pr*4+ps)*Cin + c] = w[o][r][s][c] with
       // r = 4(R-1) + pr - 2b + pad, s = 4(S-1) + ps - 2b' + pad (zero outside the 7x7 window):
@@ -538,7 +566,7 @@ struct Exec {
     const Layer &c1 = T.layers[1], &c2 = T.layers[2];
     for (const Layer* c : {&c1, &c2})
       if (c->kind != L_CONV || c->k != 3 || c->stride != 1 || c->pad != 1 || !c->relu || !(c->in == c->out) ||
-          c->fuse_proj || c->s4d)
+          c->fuse_proj || c->s4d || c->s2d2)
         return false;
     const int hw = c1.in.H * c1.in.W;
     return !c1.residual && c2.residual && c2.res_mode == 1 && lay(c1.in.Cp()) && lay(c1.out.C) && hw <= 128 &&
@@ -551,7 +579,7 @@ struct Exec {
   bool gemm_list_entry(const Subnet& S) const {
     if (S.layers.size() < 5 || S.layers[0].kind != L_BLOCK) return false;
     const Layer& c1 = S.layers[1];
-    if (c1.kind != L_CONV || c1.k != 1 || c1.stride != 1 || c1.residual || c1.s4d || !lay(c1.in.Cp()) ||
+    if (c1.kind != L_CONV || c1.k != 1 || c1.stride != 1 || c1.residual || c1.s4d || c1.s2d2 || !lay(c1.in.Cp()) ||
         !lay(c1.out.C) || (c1.in.H * c1.in.W) % 64 || c1.in.Cp() % 64 || c1.out.C % 64)
       return false;
     for (size_t li = 2; li < S.layers.size() && S.layers[li].kind != L_BLOCK; ++li) {
@@ -723,6 +751,14 @@ struct Exec {
         fused_b = 2.0 * L.out.H * L.out.W * Pj.in.C;   // the strided pixels of x the GEMM reads
         fused_f = 2.0 * L.out.H * L.out.W * L.out.C * (double)Pj.in.C;
       }
+      if (L.s2d2) {                    // 4x4 / stride 1 over 2x2 blocks (pad 2 before, 1 after)
+        a.H = L.in.H / 2; a.W = L.in.W / 2; a.C = 16;
+        a.Ho = L.out.H; a.Wo = L.out.W; a.Cout = L.out.C;
+        a.ksz = 4; a.stride = 1; a.pad = 2;
+        a.K = a.Kp = 16 * 16;
+        a.w_rt = nullptr;
+        a.in_nhwc = a.nhwc = 1;
+      }
       if (L.s4d) {                     // 3x3 / stride 1 over 4x4 blocks, 2x2 output phases in N
         a.H = L.in.H / 4; a.W = L.in.W / 4; a.C = 64;
         a.Ho = L.out.H / 2; a.Wo = L.out.W / 2; a.Cout = 4 * L.out.C;
@@ -888,6 +924,7 @@ struct Exec {
     const Shape& in = g->input;
     prof_begin(DYCL_K_INPUT, nullptr, 0, 0, (double)batch * in.H * in.W * (4.0 * in.C + 2.0 * in.Cp()));
     e = own == 0 ? cudaSuccess
+        : g->stem_s2d2 ? dycl::launch_cast_s2d2(input, g->buf[0], own, in.H, in.W, in.C, st)
         : g->stem_s4d ? dycl::launch_cast_s4d(input, g->buf[0], own, in.H, in.W, in.C, st)
                       : dycl::launch_cast_pad(input, g->buf[0], own, in.H * in.W, in.C, in.Cp(), st);
     prof_end();
@@ -1649,9 +1686,17 @@ dycl_status dycl_finalize(dycl_graph g, int64_t max_batch) {
         if (L0.kind == L_CONV && L0.k == 7 && L0.stride == 2 && L0.pad == 3 && L0.in.C <= 4 && !L0.residual &&
             L0.relu && L0.in.H % 4 == 0 && L0.in.W % 4 == 0 && L0.out.H * 2 == L0.in.H && L0.out.W * 2 == L0.in.W &&
             L1.kind == L_MAXPOOL && L1.k == 3 && L1.stride == 2 && L1.pad == 1 && L0.cout % 16 == 0) {
-          L0.s4d = 1;
-          L1.pool_s2d = 1;
-          g->stem_s4d = 1;
+          // the 2x2 form on the halo kernel measured slower end to end (stem 2.37 vs 2.2 ms, and the
+          // plain NHWC max pool 1.9 vs 0.9 ms per 2048-row chunk): opt-in DYCL_STEM_S2D2=1
+          const char* env2 = getenv("DYCL_STEM_S2D2");
+          if (env2 && atoi(env2) == 1 && L0.cout == 64 && L0.in.C <= 4) {
+            L0.s2d2 = 1;                    // the halo-tile form; the max pool reads plain NHWC
+            g->stem_s2d2 = 1;
+          } else {
+            L0.s4d = 1;
+            L1.pool_s2d = 1;
+            g->stem_s4d = 1;
+          }
         }
       }
     }

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <new>
 #include <string>
 #include <vector>
@@ -50,7 +51,6 @@ struct CapStepArgs {
   uint16_t* hb;              // [rows][H] bf16 h (row order)
   const float* q;            // [rows][D]
   const float* gates;        // [rows][4H]
-  const float* hc0;          // [B][2H] init pre-activations (t = 0 only)
   int E, D, H, L;
 };
 
@@ -189,6 +189,14 @@ struct dycl_cap_s {
   float* zero_f = nullptr;
   uint8_t* flag = nullptr;
   int launches = 0;
+  // CUDA graph of a whole run (init + max_len guarded steps), captured on first use per
+  // (io pointers, batch) and replayed: every kernel sizes itself from device counts
+  bool use_graph = true;             // DYCL_CAP_GRAPH=0 disables
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  const void* gkey[4] = {};
+  int64_t gbatch = -1;
+  int glaunches = 0;
 };
 
 static thread_local std::string g_cap_err;
@@ -254,6 +262,7 @@ dycl_status dycl_cap_create(int cuda_device, const dycl_cap_config* cfg, dycl_ca
   if (!c) return cfail(nullptr, DYCL_E_OOM, "host allocation");
   c->c = *cfg;
   c->device = cuda_device;
+  if (const char* eg = getenv("DYCL_CAP_GRAPH")) c->use_graph = atoi(eg) != 0;
   cudaSetDevice(cuda_device);
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
   *out = c;
@@ -263,6 +272,8 @@ dycl_status dycl_cap_create(int cuda_device, const dycl_cap_config* cfg, dycl_ca
 dycl_status dycl_cap_destroy(dycl_cap c) {
   if (!c) return DYCL_OK;
   cudaSetDevice(c->device);
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   for (void* p : c->allocs) cudaFree(p);
   delete c;
   return DYCL_OK;
@@ -312,15 +323,10 @@ dycl_status dycl_cap_finalize(dycl_cap c, int64_t max_batch) {
   return DYCL_OK;
 }
 
-dycl_status dycl_cap_run(dycl_cap c, const uint16_t* features, int64_t batch, int32_t* tokens, int32_t* lengths,
-                         float* top1, void* stream) {
-  if (!c) return DYCL_E_INVALID_ARG;
-  if (!c->finalized) return cfail(c, DYCL_E_STATE, "not finalized");
-  if (batch < 0 || batch > c->max_batch) return cfail(c, DYCL_E_SHAPE_MISMATCH, "batch > max_batch");
-  if (batch == 0) return DYCL_OK;
-  if (!features || !tokens || !lengths) return cfail(c, DYCL_E_INVALID_ARG, "null io pointer");
-  cudaSetDevice(c->device);
-  cudaStream_t st = (cudaStream_t)stream;
+}  // extern "C"
+
+static dycl_status cap_enqueue(dycl_cap c, const uint16_t* features, int64_t batch, int32_t* tokens, int32_t* lengths,
+                               float* top1, cudaStream_t st) {
   const dycl_cap_config& k = c->c;
   const int B = (int)batch, E = k.emb, H = k.hidden, D = k.feat_dim, L = k.feat_len, V = k.vocab;
   const int K = E + D + H;
@@ -376,6 +382,54 @@ dycl_status dycl_cap_run(dycl_cap c, const uint16_t* features, int64_t batch, in
     cur ^= 1;
   }
 #undef CE
+  return DYCL_OK;
+}
+
+extern "C" {
+
+dycl_status dycl_cap_run(dycl_cap c, const uint16_t* features, int64_t batch, int32_t* tokens, int32_t* lengths,
+                         float* top1, void* stream) {
+  if (!c) return DYCL_E_INVALID_ARG;
+  if (!c->finalized) return cfail(c, DYCL_E_STATE, "not finalized");
+  if (batch < 0 || batch > c->max_batch) return cfail(c, DYCL_E_SHAPE_MISMATCH, "batch > max_batch");
+  if (batch == 0) return DYCL_OK;
+  if (!features || !tokens || !lengths) return cfail(c, DYCL_E_INVALID_ARG, "null io pointer");
+  if (cudaSetDevice(c->device) != cudaSuccess) return cfail(c, DYCL_E_CUDA, "cudaSetDevice");
+  if (cudaError_t e = cudaGetLastError()) return cfail(c, DYCL_E_CUDA, cudaGetErrorString(e));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!c->use_graph) return cap_enqueue(c, features, batch, tokens, lengths, top1, st);
+  const void* key[4] = {features, tokens, lengths, top1};
+  bool hit = c->gexec && c->gbatch == batch;
+  for (int i = 0; i < 4 && hit; ++i) hit = key[i] == c->gkey[i];
+  if (!hit) {
+    if (c->gexec) {
+      cudaGraphExecDestroy(c->gexec);
+      c->gexec = nullptr;
+    }
+    if (!c->cap_stream && cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
+      return cfail(c, DYCL_E_CUDA, "stream create");
+    if (cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+      return cfail(c, DYCL_E_CUDA, "begin capture");
+    dycl_status r = cap_enqueue(c, features, batch, tokens, lengths, top1, c->cap_stream);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(c->cap_stream, &graph);
+    if (r != DYCL_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return r;
+    }
+    if (ec != cudaSuccess) return cfail(c, DYCL_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(ec));
+    const cudaError_t ei = cudaGraphInstantiate(&c->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) {
+      c->gexec = nullptr;
+      return cfail(c, DYCL_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei));
+    }
+    for (int i = 0; i < 4; ++i) c->gkey[i] = key[i];
+    c->gbatch = batch;
+    c->glaunches = c->launches;
+  }
+  if (cudaError_t e = cudaGraphLaunch(c->gexec, st)) return cfail(c, DYCL_E_CUDA, cudaGetErrorString(e));
+  c->launches = c->glaunches;
   return DYCL_OK;
 }
 

@@ -690,7 +690,8 @@ cudaError_t launch_conv_tma(const ConvArgs& a, int max_rows, int num_sms, cudaSt
 
 cudaError_t launch_conv(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream, int path) {
   // the pair stream exists only on the NHWC im2col GEMM
-  if (a.y32_pair && !(a.in_nhwc && a.nhwc && conv_gemm_eligible(a))) return cudaErrorNotSupported;
+  if (a.y32_pair && (a.y32 || a.res32) && !(a.in_nhwc && a.nhwc && conv_gemm_eligible(a)))
+    return cudaErrorNotSupported;
   if (a.in_nhwc) {
     // NHWC input: the im2col GEMM (C, Cout % 64); a planar kernel only when the layouts coincide
     // (8 channels, or 1x1 maps)

@@ -696,6 +696,36 @@ __global__ void k_maxpool_s2d(const PoolArgs a) {
 // fp32 NHWC [n][H][W][c] -> bf16 4x4 space-to-depth [n][H/4][W/4][64]; one thread per output
 // pixel: the 4 input rows of its block are 4 contiguous runs of 4*c floats (c == 3: 3 float4
 // each; lanes = consecutive blocks, so a warp reads contiguous 1.5 KB rows), 128 B out.
+// a0, 2x2 space-to-depth: thread per output block (32-bit index math: the launcher bounds the
+// block count); channel (dy*2+dx)*c + ci, zeros up to 16
+__global__ void k_cast_s2d2(const float* __restrict__ in, uint16_t* __restrict__ out, int64_t total, int H, int W,
+                            int c) {
+  const uint32_t Wb = (uint32_t)(W / 2), Hb = (uint32_t)(H / 2);
+  for (uint32_t blk = blockIdx.x * blockDim.x + threadIdx.x; blk < (uint32_t)total; blk += gridDim.x * blockDim.x) {
+    const uint32_t t = blk / Wb, Q = blk - t * Wb;
+    const uint32_t n = t / Hb, Pr = t - n * Hb;
+    float v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = 0.0f;
+    for (int dy = 0; dy < 2; ++dy)
+      for (int dx = 0; dx < 2; ++dx)
+        for (int ci = 0; ci < c; ++ci)
+          v[(dy * 2 + dx) * c + ci] =
+              __ldg(in + (((size_t)n * H + 2 * Pr + dy) * (size_t)W + 2 * Q + dx) * c + ci);
+    uint4* dst = reinterpret_cast<uint4*>(out + (size_t)blk * 16);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      uint32_t o[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        __nv_bfloat162 b = __floats2bfloat162_rn(v[8 * j + 2 * k], v[8 * j + 2 * k + 1]);
+        o[k] = *reinterpret_cast<uint32_t*>(&b);
+      }
+      dst[j] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
 __global__ void k_cast_s4d(const float* __restrict__ in, uint16_t* __restrict__ out, int64_t total, int H, int W,
                            int c, int vec) {
   const int Wb = W / 4, Hb = H / 4;
@@ -773,6 +803,16 @@ cudaError_t launch_gap_reduce(const float* gap_part, int G, float* pooled, const
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
   k_gap_reduce<<<(int)blocks, 256, 0, s>>>(gap_part, G, pooled, n_live, HW, C);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cast_s2d2(const float* in, uint16_t* out, int64_t n, int H, int W, int c, cudaStream_t s) {
+  if (H % 2 || W % 2 || c > 4 || n * (H / 2) * (W / 2) >= ((int64_t)1 << 31)) return cudaErrorInvalidValue;
+  const int64_t total = n * (H / 2) * (W / 2);
+  if (total == 0) return cudaSuccess;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  k_cast_s2d2<<<(int)blocks, 256, 0, s>>>(in, out, total, H, W, c);
   return cudaGetLastError();
 }
 

@@ -165,6 +165,9 @@ cudaError_t launch_gap_reduce(const float* gap_part, int G, float* pooled, const
 // a0 for a space-to-depth stem: fp32 NHWC [n][H][W][c] -> bf16 [n][H/4][W/4][64], channel
 // (pr*4 + ps)*c + ci = input pixel (4P+pr, 4Q+ps) channel ci; channels >= 16c zero (c <= 4).
 cudaError_t launch_cast_s4d(const float* in, uint16_t* out, int64_t n, int H, int W, int c, cudaStream_t s);
+// a0 for the 2x2 space-to-depth stem: fp32 [n][H][W][c] (c <= 4) -> bf16 [n][H/2][W/2][16],
+// channel (dy*2+dx)*c + ci, zero-padded to 16
+cudaError_t launch_cast_s2d2(const float* in, uint16_t* out, int64_t n, int H, int W, int c, cudaStream_t s);
 
 // Run-start init: counts[0] = n ; orig[i] = i ; path[i] = 0.
 cudaError_t launch_init(int* counts, int n, int* orig, int32_t* path, float* margin, int nmax, cudaStream_t s);
