@@ -236,6 +236,9 @@ class ImageJob:
         if rebalance and ws > 1:
             from paper_2307_04963_b200 import dist as DI
             DI.attach(self.model, rank, ws)
+            if rebalance == "device":
+                from paper_2307_04963_b200 import dycl as D
+                D.dycl_set_rebalance_mode(self.model.g, D.DYCL_REBALANCE_MODE_DEVICE)
             self.rebalance = True
         if cfg == 1:
             X = torch.from_numpy(wl.mlp_inputs(wl.INPUT_SEED, g0, self.B)).to(dev)
@@ -394,7 +397,8 @@ def run_dycl(args):
     dev = torch.device(f"cuda:{local}")
     stream = torch.cuda.current_stream()
     job_cls = CapJob if args.caption else S2SJob if args.config == 4 else ImageJob
-    job = job_cls(args.config, rank, ws, dev, torch, not args.no_rebalance, rnn=args.rnn_gates)
+    job = job_cls(args.config, rank, ws, dev, torch, False if args.no_rebalance else args.rebalance_mode,
+                  rnn=args.rnn_gates)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > L2 (126 MB)
 
     for _ in range(args.warmup):
@@ -546,7 +550,8 @@ def run_dycl(args):
                    "l2": "flushed (256 MB write) before every timed step, flush not timed; inputs > L2",
                    "parallelism": (f"dp{ws}: contiguous shards of the global batch" if strong else
                                    f"dp{ws}: independent per-GPU batches") +
-                                  ("; survivors of exit 0 rebalanced over NCCL inside dycl_run" if job.rebalance
+                                  (f"; survivors rebalanced after every exit inside dycl_run ({args.rebalance_mode}-initiated)"
+                                   if job.rebalance
                                    else "; no collective on the data path"),
                    "decisions_rank0": hist},
         "clocks": clk,
@@ -580,6 +585,9 @@ def main():
     ap.add_argument("--ref-samples", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rebalance", action="store_true", help="N > 1: no survivor rebalancing")
+    ap.add_argument("--rebalance-mode", default="host", choices=["host", "device"],
+                    help="N > 1: survivor exchange via the host plan + NCCL send/recv, or device-initiated "
+                         "through NCCL symmetric windows (SURVEY 8(f)1)")
     ap.add_argument("--caption", action="store_true",
                     help="the image-captioning En-Decoder (SURVEY 8(f)4): CNN encoder + soft-attention LSTM decoder")
     ap.add_argument("--rnn-gates", action="store_true",

@@ -286,6 +286,25 @@ typedef struct dycl_local_group_s* dycl_local_group;
 dycl_status dycl_local_group_create(int world, dycl_local_group* out);
 dycl_status dycl_local_group_destroy(dycl_local_group grp);
 dycl_status dycl_set_comm_local(dycl_graph g, dycl_local_group grp, int rank, int rebalance_policy);
+/* Where the exchange runs (call after dycl_set_comm / dycl_set_comm_local; default HOST):
+ *   DYCL_REBALANCE_MODE_HOST   as described above: count all-gather read on the host, host plan,
+ *                              grouped point-to-point step (NCCL send / recv or local copies);
+ *   DYCL_REBALANCE_MODE_DEVICE device-initiated: every rank owns a symmetric device
+ *                              window (NCCL: ncclMemAlloc + ncclCommWindowRegister, peers reached
+ *                              through their LSA pointers over NVLink / NVSwitch; in-process: the
+ *                              graphs' buffers) and kernels do the exchange -- publish the survivor
+ *                              count into every peer's window, compute every rank's plan on the
+ *                              device (the same plan as dycl_rebalance_plan), store the surplus
+ *                              rows straight into the receivers' windows, release / acquire flags
+ *                              per level and epoch -- with no host synchronisation; results come
+ *                              home the same way.  Same outputs, bitwise.  The window (allocated at
+ *                              the first rebalanced exit, collectively) holds max_batch rows of the
+ *                              largest exit input plus per-level results; at most 8 ranks and 8
+ *                              rebalanced exits; a peer that never arrives is reported (after
+ *                              ~20 s) by dycl_rebalance_stats as DYCL_E_NCCL instead of hanging.
+ * Errors: INVALID_ARG, STATE (no communicator), UNSUPPORTED (world > 8), OOM. */
+enum { DYCL_REBALANCE_MODE_HOST = 0, DYCL_REBALANCE_MODE_DEVICE = 1 };
+dycl_status dycl_set_rebalance_mode(dycl_graph g, int mode);
 /* Rows this rank sent to / received from other ranks during its last dycl_run. */
 dycl_status dycl_rebalance_stats(dycl_graph g, int64_t* rows_sent, int64_t* rows_received);
 /* NCCL bootstrap for callers without a communicator: rank 0 gets a 128-byte unique id, shares

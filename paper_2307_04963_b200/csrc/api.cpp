@@ -22,6 +22,7 @@
 
 #include "../../include/dycl.h"
 #include "comm.h"
+#include "drb.h"
 #include "kernels.h"
 
 namespace {
@@ -200,6 +201,16 @@ struct dycl_graph_s {
   float* d_ret_margin = nullptr;
   int64_t rb_rows = 0;               // capacity of the result space / sent tables (rows)
   long long rb_sent = 0, rb_recv = 0;   // rows moved by the last run (dycl_rebalance_stats)
+  // device-initiated rebalancing (dycl_set_rebalance_mode DEVICE; drb.cu)
+  bool rb_device = false;
+  void* drb_win = nullptr;           // this rank's window (transport-owned)
+  void** drb_peers = nullptr;        // device [world] window bases
+  size_t drb_bytes = 0, drb_rows_off = 0, drb_ret_off = 0;
+  dycl::DrbPlan* d_drb_plan = nullptr;
+  unsigned* d_drb_epoch = nullptr;
+  int* d_drb_err = nullptr;
+  int* d_drb_ticket = nullptr;
+  int drb_levels_last = 0;           // levels the last run rebalanced (stats)
 };
 
 static thread_local std::string g_create_err;
@@ -516,6 +527,7 @@ struct Exec {
     ++g->prof_used;
   }
 
+  std::vector<dycl::DrbArgs> drb;       // device-rebalanced levels of this run (return path)
   bool pv[dycl_graph_s::NBUF32] = {};   // d_pool32[f] holds the GAP of every live row of buf32[f]
   int gap_f = -1;                       // buf32 index whose GAP sits in d_gap_pooled (conv_gemm fused GAP)
   bool want_gap = false;                // the subnet being run feeds a head: fuse its GAP when possible
@@ -917,6 +929,10 @@ struct Exec {
     cudaError_t e = dycl::launch_init(g->d_counts, own, g->d_orig[0], out_path, out_margin, batch, st);
     prof_end();
     if (e != cudaSuccess) return cuda_fail(g, e, "launch_init");
+    if (g->tr && g->rb_device && g->rb_policy != 0 && g->n_exits > 0) {
+      e = dycl::drb_begin(g->d_drb_epoch, st);           // this run's exchange epoch (every rank)
+      if (e != cudaSuccess) return cuda_fail(g, e, "drb_begin");
+    }
     if (g->d_rnn_state) {
       e = cudaMemsetAsync(g->d_rnn_state, 0, (size_t)batch * 2 * g->rnn_hidden * sizeof(float), st);
       if (e != cudaSuccess) return cuda_fail(g, e, "rnn state reset");
@@ -1162,7 +1178,72 @@ struct Exec {
   // (all-gather), compute the same deterministic plan (dycl_rebalance_plan), and exchange the
   // surplus rows -- the LAST rows of a surplus rank, in order -- with their metadata; arrivals
   // are appended after the local survivors and get result-space ids past the own rows.
+  // Device-initiated form: counts, plan, row transfer and bookkeeping all on the
+  // device (drb.cu); level k's received rows get result ids [max_batch * (1 + k), ...), its sent
+  // rows' ids go to d_sent_orig + k * max_batch -- fixed regions, so the host needs no plan.
+  dycl_status rebalance_device(Tensor t, int* cnt_slot, const Shape& sh, int orig_cur) {
+    const int k = (int)drb.size();
+    if (k >= dycl::DRB_MAX_LEVELS) return fail(g, DYCL_E_UNSUPPORTED, "device rebalancing: too many levels");
+    if (!g->drb_win) {
+      std::string err;
+      if (!g->tr->window(g->drb_bytes, &g->drb_win, &g->drb_peers, &err)) return fail(g, DYCL_E_NCCL, err);
+    }
+    dycl::DrbArgs a{};
+    a.rank = g->tr->rank;
+    a.world = g->tr->world;
+    a.level = k;
+    a.max_rows = (int)g->max_batch;
+    a.K = g->K;
+    a.peers = g->drb_peers;
+    a.rows_off = g->drb_rows_off;
+    a.ret_off = g->drb_ret_off;
+    a.epoch = g->d_drb_epoch;
+    a.err = g->d_drb_err;
+    a.ticket = g->d_drb_ticket;
+    a.plan = g->d_drb_plan;
+    a.cnt = cnt_slot;
+    a.plane_b = t.b >= 0 ? reinterpret_cast<uint8_t*>(g->buf[t.b]) : nullptr;
+    a.plane_f = t.f >= 0 ? reinterpret_cast<uint8_t*>(g->buf32[t.f]) : nullptr;
+    a.plane_b_bytes = t.b >= 0 ? sh.row_elems() * 2 : 0;
+    a.plane_f_bytes = t.f >= 0 ? sh.row_elems() * (g->stream_pair ? 2 : 4) : 0;
+    a.row_bytes = a.plane_b_bytes + a.plane_f_bytes;
+    if (a.row_bytes + 16 > (long long)((g->drb_ret_off - g->drb_rows_off) / g->max_batch))
+      return fail(g, DYCL_E_STATE, "device rebalancing: row larger than the window's row slots");
+    a.orig = g->d_orig[orig_cur];
+    a.sent_orig = g->d_sent_orig + (size_t)k * g->max_batch;
+    a.gid_base = global_offset;
+    a.own = own;
+    a.ext0 = (int)(g->max_batch * (1 + k));
+    a.ext_gid = g->d_ext_gid;
+    a.res_path = out_path;
+    a.res_margin = out_margin;
+    a.res_logits = out_logits;
+    cudaError_t e = dycl::drb_counts(a, st);
+    if (e == cudaSuccess) e = dycl::drb_push(a, g->num_sms, st);
+    if (e == cudaSuccess) e = dycl::drb_wait(a, 0, st);
+    if (e == cudaSuccess) e = dycl::drb_pull(a, g->num_sms, st);
+    if (e != cudaSuccess) return cuda_fail(g, e, "device rebalancing");
+    nlaunch += 4;
+    drb.push_back(a);
+    batch = (int)g->max_batch;                     // rows held are known on the device only
+    return DYCL_OK;
+  }
+
+  dycl_status return_results_device() {
+    for (int k = (int)drb.size() - 1; k >= 0; --k) {
+      const dycl::DrbArgs& a = drb[k];
+      cudaError_t e = dycl::drb_ret_push(a, g->num_sms, st);
+      if (e == cudaSuccess) e = dycl::drb_wait(a, 1, st);
+      if (e == cudaSuccess) e = dycl::drb_ret_pull(a, g->num_sms, st);
+      if (e != cudaSuccess) return cuda_fail(g, e, "device rebalancing (return)");
+      nlaunch += 3;
+    }
+    g->drb_levels_last = (int)drb.size();
+    return DYCL_OK;
+  }
+
   dycl_status rebalance(Tensor t, int* cnt_slot, const Shape& sh, int orig_cur) {
+    if (g->rb_device) return rebalance_device(t, cnt_slot, sh, orig_cur);
     dycl::Transport* T = g->tr;
     const int W = T->world, me = T->rank;
     std::vector<int> counts(W);
@@ -1236,6 +1317,7 @@ struct Exec {
   // level first (a row forwarded twice returns through its intermediate rank), and are
   // scattered to their result-space id; own rows then reach the caller's buffers.
   dycl_status return_results() {
+    if (g->tr && g->rb_device) return return_results_device();
     if (!g->tr || levels.empty()) return DYCL_OK;
     const int K = g->K, W = g->tr->world;
     std::string err;
@@ -1352,6 +1434,10 @@ dycl_status dycl_graph_destroy(dycl_graph g) {
   cudaFree(g->d_path_stage);
   cudaFree(g->d_margin_stage);
   cudaFree(g->dbg_ts);
+  cudaFree(g->d_drb_plan);
+  cudaFree(g->d_drb_epoch);
+  cudaFree(g->d_drb_err);
+  cudaFree(g->d_drb_ticket);
   cudaFree(g->d_res_logits);
   cudaFree(g->d_res_path);
   cudaFree(g->d_res_margin);
@@ -2124,6 +2210,41 @@ dycl_status dycl_set_comm(dycl_graph g, void* nccl_comm, int rank, int world, in
   return set_transport(g, t, rebalance_policy);
 }
 
+dycl_status dycl_set_rebalance_mode(dycl_graph g, int mode) {
+  if (!g) return DYCL_E_INVALID_ARG;
+  if (mode != DYCL_REBALANCE_MODE_HOST && mode != DYCL_REBALANCE_MODE_DEVICE)
+    return fail(g, DYCL_E_INVALID_ARG, "rebalance mode");
+  if (!g->tr || !g->d_res_logits) return fail(g, DYCL_E_STATE, "dycl_set_rebalance_mode: attach a communicator first");
+  if (mode == DYCL_REBALANCE_MODE_DEVICE && g->tr->world > dycl::DRB_MAX_WORLD)
+    return fail(g, DYCL_E_UNSUPPORTED, "device rebalancing: at most 8 ranks (one NVLink domain)");
+  CK(cudaSetDevice(g->device));
+  g->rb_device = mode == DYCL_REBALANCE_MODE_DEVICE;
+  if (g->rb_device && !g->d_drb_plan) {
+    dycl_status s;
+    if ((s = dmalloc(g, &g->d_drb_plan, dycl::DRB_MAX_LEVELS * sizeof(dycl::DrbPlan))) ||
+        (s = dmalloc(g, &g->d_drb_epoch, sizeof(unsigned))) || (s = dmalloc(g, &g->d_drb_err, sizeof(int))) ||
+        (s = dmalloc(g, &g->d_drb_ticket, sizeof(int))))
+      return s;
+    CK(cudaMemset(g->d_drb_plan, 0, dycl::DRB_MAX_LEVELS * sizeof(dycl::DrbPlan)));
+    CK(cudaMemset(g->d_drb_epoch, 0, sizeof(unsigned)));
+    CK(cudaMemset(g->d_drb_err, 0, sizeof(int)));
+    CK(cudaMemset(g->d_drb_ticket, 0, sizeof(int)));
+    // window: control words | max_batch row slots (the largest exit input: bf16 + fp32 planes +
+    // 16 B) | per level max_batch returned results (K logits, path, margin, pad)
+    long long row = 16;
+    for (const Node& N : g->nodes)
+      if (N.kind == N_EXIT) row = std::max(row, N.in.row_elems() * 6 + 16);
+    const size_t ctrl = (sizeof(dycl::DrbCtrl) + 255) / 256 * 256;
+    const size_t rows = ((size_t)g->max_batch * row + 255) / 256 * 256;
+    const size_t levels = (size_t)std::max(1, std::min(g->n_exits, dycl::DRB_MAX_LEVELS));
+    const size_t ret = levels * (size_t)g->max_batch * ((size_t)g->K + 4) * 4;
+    g->drb_rows_off = ctrl;
+    g->drb_ret_off = ctrl + rows;
+    g->drb_bytes = (ctrl + rows + ret + 4095) / 4096 * 4096;
+  }
+  return DYCL_OK;
+}
+
 struct dycl_local_group_s {
   dycl::LocalGroup* g;
 };
@@ -2151,6 +2272,25 @@ dycl_status dycl_set_comm_local(dycl_graph g, dycl_local_group grp, int rank, in
 
 dycl_status dycl_rebalance_stats(dycl_graph g, int64_t* rows_sent, int64_t* rows_received) {
   if (!g || !rows_sent || !rows_received) return DYCL_E_INVALID_ARG;
+  if (g->rb_device && g->d_drb_plan) {
+    // the plans live on the device: read the last run's levels (and its error word)
+    CK(cudaSetDevice(g->device));
+    CK(cudaDeviceSynchronize());
+    int err = 0;
+    CK(cudaMemcpy(&err, g->d_drb_err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (err) return fail(g, DYCL_E_NCCL, "device rebalancing: " +
+                                             std::string(err == 2 ? "rows held exceed max_batch" : "peer wait timed out"));
+    std::vector<dycl::DrbPlan> P(dycl::DRB_MAX_LEVELS);
+    CK(cudaMemcpy(P.data(), g->d_drb_plan, P.size() * sizeof(dycl::DrbPlan), cudaMemcpyDeviceToHost));
+    long long sent = 0, recv = 0;
+    for (int k = 0; k < g->drb_levels_last; ++k) {
+      sent += P[k].n_send;
+      recv += P[k].n_recv;
+    }
+    *rows_sent = sent;
+    *rows_received = recv;
+    return DYCL_OK;
+  }
   *rows_sent = g->rb_sent;
   *rows_received = g->rb_recv;
   return DYCL_OK;

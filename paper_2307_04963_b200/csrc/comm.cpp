@@ -3,6 +3,8 @@
 
 #include <dlfcn.h>
 
+#include "drb.h"
+
 #include <condition_variable>
 #include <map>
 #include <mutex>
@@ -30,6 +32,11 @@ struct NcclApi {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, NcclUid, int) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  // symmetric windows (NCCL >= 2.27; optional: only the device-initiated rebalancing needs them)
+  ncclResult_t (*MemAlloc)(void**, size_t) = nullptr;
+  ncclResult_t (*MemFree)(void*) = nullptr;
+  ncclResult_t (*WindowRegister)(ncclComm_t, void*, size_t, void**, int) = nullptr;
+  ncclResult_t (*WindowDeregister)(ncclComm_t, void*) = nullptr;
 };
 
 const NcclApi& nccl() {
@@ -60,6 +67,10 @@ const NcclApi& nccl() {
     SYM(CommDestroy, "ncclCommDestroy");
     SYM(GetErrorString, "ncclGetErrorString");
 #undef SYM
+    api.MemAlloc = reinterpret_cast<decltype(api.MemAlloc)>(dlsym(h, "ncclMemAlloc"));
+    api.MemFree = reinterpret_cast<decltype(api.MemFree)>(dlsym(h, "ncclMemFree"));
+    api.WindowRegister = reinterpret_cast<decltype(api.WindowRegister)>(dlsym(h, "ncclCommWindowRegister"));
+    api.WindowDeregister = reinterpret_cast<decltype(api.WindowDeregister)>(dlsym(h, "ncclCommWindowDeregister"));
     api.ok = true;
   });
   return api;
@@ -75,10 +86,46 @@ struct NcclTransport : Transport {
   ncclComm_t comm = nullptr;
   int* d_all = nullptr;
   int* h_all = nullptr;
+  void* win_buf = nullptr;                         // ncclMemAlloc'd symmetric window
+  void* win = nullptr;                             // its ncclWindow_t
+  void** peers = nullptr;                          // device [world] LSA peer pointers
+  size_t win_bytes = 0;
 
   ~NcclTransport() override {
     if (d_all) cudaFree(d_all);
     if (h_all) cudaFreeHost(h_all);
+    if (win && nccl().WindowDeregister) nccl().WindowDeregister(comm, win);
+    if (win_buf && nccl().MemFree) nccl().MemFree(win_buf);
+    if (peers) cudaFree(peers);
+  }
+  bool window(size_t bytes, void** local, void*** peers_dev, std::string* err) override {
+    const NcclApi& A = nccl();
+    if (!win) {
+      if (!A.MemAlloc || !A.WindowRegister) {
+        *err = "device rebalancing needs NCCL symmetric windows (ncclMemAlloc / ncclCommWindowRegister)";
+        return false;
+      }
+      if (!nccl_err(A.MemAlloc(&win_buf, bytes), "ncclMemAlloc", err)) return false;
+      if (cudaMemset(win_buf, 0, bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+        *err = "window clear failed";
+        return false;
+      }
+      if (!nccl_err(A.WindowRegister(comm, win_buf, bytes, &win, 1 /* NCCL_WIN_COLL_SYMMETRIC */),
+                    "ncclCommWindowRegister", err))
+        return false;
+      if (cudaMalloc(reinterpret_cast<void**>(&peers), world * sizeof(void*)) != cudaSuccess ||
+          drb_nccl_peers(win, world, peers, 0) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+        *err = "window peer table failed";
+        return false;
+      }
+      win_bytes = bytes;
+    } else if (bytes > win_bytes) {
+      *err = "window size changed";
+      return false;
+    }
+    *local = win_buf;
+    *peers_dev = peers;
+    return true;
   }
   bool allgather_int(const int* dev_val, int* host_out, cudaStream_t st, std::string* err) override {
     const NcclApi& A = nccl();
@@ -130,6 +177,8 @@ struct LocalGroup {
   // (src, dst) -> that step's send buffers in posting order (matched to receives in order,
   // as NCCL matches several sends between one pair of ranks)
   std::map<std::pair<int, int>, std::vector<Transport::Msg>> posted;
+  std::vector<void*> wins;                         // device windows (device-initiated rebalancing)
+  std::vector<int> win_dev;
   void barrier() {
     std::unique_lock<std::mutex> lk(mu);
     const long long gen = generation;
@@ -146,6 +195,59 @@ struct LocalGroup {
 namespace {
 struct LocalTransport : Transport {
   LocalGroup* g = nullptr;
+  void* win = nullptr;
+  void** peers = nullptr;
+  size_t win_bytes = 0;
+  ~LocalTransport() override {
+    if (win) cudaFree(win);
+    if (peers) cudaFree(peers);
+  }
+  bool window(size_t bytes, void** local, void*** peers_dev, std::string* err) override {
+    if (!win) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (cudaMalloc(&win, bytes) != cudaSuccess || cudaMemset(win, 0, bytes) != cudaSuccess ||
+          cudaDeviceSynchronize() != cudaSuccess) {
+        *err = "local window allocation failed";
+        return false;
+      }
+      {
+        std::lock_guard<std::mutex> lk(g->mu);
+        g->wins[rank] = win;
+        g->win_dev[rank] = dev;
+      }
+      g->barrier();
+      std::vector<void*> all;
+      std::vector<int> devs;
+      {
+        std::lock_guard<std::mutex> lk(g->mu);
+        all = g->wins;
+        devs = g->win_dev;
+      }
+      for (int r = 0; r < world; ++r)
+        if (devs[r] != dev) {
+          const cudaError_t e = cudaDeviceEnablePeerAccess(devs[r], 0);
+          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+            *err = "local window: peer access";
+            return false;
+          }
+          cudaGetLastError();
+        }
+      if (cudaMalloc(reinterpret_cast<void**>(&peers), world * sizeof(void*)) != cudaSuccess ||
+          cudaMemcpy(peers, all.data(), world * sizeof(void*), cudaMemcpyHostToDevice) != cudaSuccess) {
+        *err = "local window: peer table";
+        return false;
+      }
+      win_bytes = bytes;
+      g->barrier();
+    } else if (bytes > win_bytes) {
+      *err = "window size changed";
+      return false;
+    }
+    *local = win;
+    *peers_dev = peers;
+    return true;
+  }
   bool allgather_int(const int* dev_val, int* host_out, cudaStream_t st, std::string* err) override {
     int v = 0;
     cudaError_t e = cudaMemcpyAsync(&v, dev_val, sizeof(int), cudaMemcpyDeviceToHost, st);
@@ -231,6 +333,8 @@ LocalGroup* local_group_create(int world) {
   LocalGroup* g = new LocalGroup();
   g->world = world;
   g->ints.assign(world, 0);
+  g->wins.assign(world, nullptr);
+  g->win_dev.assign(world, 0);
   return g;
 }
 void local_group_destroy(LocalGroup* g) { delete g; }

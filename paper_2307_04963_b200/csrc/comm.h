@@ -33,6 +33,12 @@ struct Transport {
   // Post all sends and receives of one step; completion is stream-ordered on `st`.
   virtual bool exchange(const std::vector<Msg>& sends, const std::vector<Msg>& recvs, cudaStream_t st,
                         std::string* err) = 0;
+  // Device windows for device-initiated rebalancing (drb.cu).  Collective: every
+  // rank calls it with the same size at the same point of its run sequence (the first device-
+  // rebalanced exit).  *local = this rank's window (zeroed), *peers_dev = device array [world] of
+  // every rank's window base as addressable from this rank's kernels (NCCL: the LSA pointers of a
+  // registered symmetric window over NVLink; in-process: the graphs' own buffers).
+  virtual bool window(size_t bytes, void** local, void*** peers_dev, std::string* err) = 0;
 };
 
 // nccl_comm: an ncclComm_t (borrowed, not destroyed).  nullptr + *err on failure.

@@ -39,6 +39,8 @@ class dycl_io(ctypes.Structure):
 
 DYCL_REBALANCE_NONE = 0
 DYCL_REBALANCE_ALL = -1
+DYCL_REBALANCE_MODE_HOST = 0
+DYCL_REBALANCE_MODE_DEVICE = 1
 
 
 class dycl_cap_config(ctypes.Structure):
@@ -69,7 +71,7 @@ EXPORTS = [
     "dycl_launches_per_run", "dycl_num_classes", "dycl_set_profiling", "dycl_profile_read",
     "dycl_debug_conv2d", "dycl_rebalance_plan", "dycl_debug_timestamps",
     "dycl_run_host_ex", "dycl_set_comm", "dycl_local_group_create", "dycl_local_group_destroy",
-    "dycl_set_comm_local", "dycl_rebalance_stats", "dycl_nccl_get_unique_id", "dycl_nccl_comm_init_rank",
+    "dycl_set_comm_local", "dycl_set_rebalance_mode", "dycl_rebalance_stats", "dycl_nccl_get_unique_id", "dycl_nccl_comm_init_rank",
     "dycl_nccl_comm_destroy", "dycl_s2s_set_precision",
     "dycl_cap_create", "dycl_cap_destroy", "dycl_cap_last_error", "dycl_cap_set_weights", "dycl_cap_finalize",
     "dycl_cap_run", "dycl_cap_launches",
@@ -122,6 +124,7 @@ def lib():
             "dycl_local_group_create": [i32, ctypes.POINTER(vp)],
             "dycl_local_group_destroy": [vp],
             "dycl_set_comm_local": [vp, vp, i32, i32],
+            "dycl_set_rebalance_mode": [vp, i32],
             "dycl_rebalance_stats": [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)],
             "dycl_nccl_get_unique_id": [ctypes.POINTER(ctypes.c_uint8)],
             "dycl_nccl_comm_init_rank": [ctypes.POINTER(ctypes.c_uint8), i32, i32, i32, ctypes.POINTER(vp)],
@@ -332,6 +335,10 @@ def dycl_local_group_destroy(grp):
 
 def dycl_set_comm_local(g, grp, rank, rebalance_policy=DYCL_REBALANCE_ALL):
     _ck(lib().dycl_set_comm_local(g, grp, int(rank), int(rebalance_policy)), g)
+
+
+def dycl_set_rebalance_mode(g, mode):
+    _ck(lib().dycl_set_rebalance_mode(g, int(mode)), g)
 
 
 def dycl_rebalance_stats(g):

@@ -5,7 +5,11 @@
   world 2 / 3 graphs on this GPU, one host thread each -- the same plan, exchange, metadata and
   return code as the NCCL transport): rebalance on == off, bitwise, with rows actually moved,
   including a rank with an empty shard and a skewed split;
-* the NCCL transport over torch's own communicator (world 1: the all-gather runs, no rows move);
+* the same with the exchange device-initiated (dycl_set_rebalance_mode DEVICE, SURVEY 8(f)1:
+  counts, plan, row stores and results through the ranks' device windows, no host sync), over
+  repeated runs (epochs / parity slots);
+* the NCCL transport over torch's own communicator (world 1: the all-gather runs, no rows move),
+  host and device modes (the latter registers an NCCL symmetric window and reads its LSA pointer);
 * the min_margin output against the oracle's predicates.
 """
 import os
@@ -55,14 +59,18 @@ def test_shards_with_offsets_equal_one_run(r56w):
     assert np.array_equal(np.concatenate([la, lb]), l1) and np.array_equal(np.concatenate([pa, pb]), p1)
 
 
-def _rebalanced(builder, W, shards, policy=D.DYCL_REBALANCE_ALL, max_batch=None):
-    """Run len(shards) graphs as ranks of one in-process group, one host thread each."""
+def _rebalanced(builder, W, shards, policy=D.DYCL_REBALANCE_ALL, max_batch=None, mode=D.DYCL_REBALANCE_MODE_HOST,
+                runs=1):
+    """Run len(shards) graphs as ranks of one in-process group, one host thread each (device
+    mode: the ranks' exchange kernels wait for one another through their windows, so every
+    rank's run is in flight at once -- one stream per rank)."""
     world = len(shards)
     mb = max_batch or max(1, max(s.shape[0] for s in shards))
     models = [builder(W, mb) for _ in range(world)]
     grp = D.dycl_local_group_create(world)
     for r, m in enumerate(models):
         D.dycl_set_comm_local(m.g, grp, r, policy)
+        D.dycl_set_rebalance_mode(m.g, mode)
     outs = [None] * world
     errs = []
     g0 = np.cumsum([0] + [s.shape[0] for s in shards])
@@ -75,7 +83,8 @@ def _rebalanced(builder, W, shards, policy=D.DYCL_REBALANCE_ALL, max_batch=None)
                 lg = torch.full((max(B, 1), models[r].K), float("nan"), device=DEV)
                 pa = torch.full((max(B, 1),), -7, dtype=torch.int32, device=DEV)
                 mm = torch.full((max(B, 1),), float("nan"), device=DEV)
-                models[r].run(shards[r], lg, pa, stream=st, global_offset=int(g0[r]), min_margin=mm)
+                for _ in range(runs):                 # repeated runs: epochs / parity slots advance
+                    models[r].run(shards[r], lg, pa, stream=st, global_offset=int(g0[r]), min_margin=mm)
                 st.synchronize()
                 outs[r] = (lg[:B].cpu().numpy(), pa[:B].cpu().numpy(), mm[:B].cpu().numpy(),
                            D.dycl_rebalance_stats(models[r].g))
@@ -98,8 +107,12 @@ def _skewed(X, paths, first_exit_share):
     return X[torch.from_numpy(order).to(DEV)], order
 
 
+MODES = [D.DYCL_REBALANCE_MODE_HOST, D.DYCL_REBALANCE_MODE_DEVICE]
+
+
+@pytest.mark.parametrize("mode", MODES, ids=["host", "device"])
 @pytest.mark.parametrize("world,split", [(2, "equal"), (2, "skewed"), (3, "one_empty")])
-def test_cfg2_rebalance_on_equals_off(r56w, world, split):
+def test_cfg2_rebalance_on_equals_off(r56w, world, split, mode):
     n = 900
     X = torch.from_numpy(wl.image_inputs(wl.INPUT_SEED, 5000, n)).to(DEV)
     ref = P.build_sdn_resnet56(r56w, n)
@@ -112,7 +125,8 @@ def test_cfg2_rebalance_on_equals_off(r56w, world, split):
     else:
         cuts = [n * r // world for r in range(world + 1)]
     shards = [X[cuts[r]:cuts[r + 1]].contiguous() for r in range(world)]
-    outs = _rebalanced(P.build_sdn_resnet56, r56w, shards, max_batch=max(c1 - c0 for c0, c1 in zip(cuts, cuts[1:])))
+    outs = _rebalanced(P.build_sdn_resnet56, r56w, shards, max_batch=max(c1 - c0 for c0, c1 in zip(cuts, cuts[1:])),
+                       mode=mode, runs=3 if mode == D.DYCL_REBALANCE_MODE_DEVICE else 1)
     lg = np.concatenate([o[0] for o in outs])
     pg = np.concatenate([o[1] for o in outs])
     mg = np.concatenate([o[2] for o in outs])
@@ -126,7 +140,8 @@ def test_cfg2_rebalance_on_equals_off(r56w, world, split):
     assert np.array_equal(mg, m_ref)
 
 
-def test_cfg5_rebalance_on_equals_off():
+@pytest.mark.parametrize("mode", MODES, ids=["host", "device"])
+def test_cfg5_rebalance_on_equals_off(mode):
     W = wl.resnet50_ee_weights()
     n = 96
     X = wl.image_inputs_torch(wl.INPUT_SEED, 900, n, hw=224, device="cuda")
@@ -135,7 +150,7 @@ def test_cfg5_rebalance_on_equals_off():
     X, order = _skewed(X, p_ref, 0.5)
     l_ref, p_ref = l_ref[order], p_ref[order]
     shards = [X[:n // 2].contiguous(), X[n // 2:].contiguous()]
-    outs = _rebalanced(P.build_resnet50_ee, W, shards, max_batch=n // 2)
+    outs = _rebalanced(P.build_resnet50_ee, W, shards, max_batch=n // 2, mode=mode)
     moved = sum(o[3][0] for o in outs)
     print("cfg5 rows moved", moved)
     assert moved > 0
@@ -143,18 +158,20 @@ def test_cfg5_rebalance_on_equals_off():
     assert np.array_equal(np.concatenate([o[0] for o in outs]), l_ref)
 
 
-def test_rebalance_policy_first_exit_only(r56w):
+@pytest.mark.parametrize("mode", MODES, ids=["host", "device"])
+def test_rebalance_policy_first_exit_only(r56w, mode):
     n = 400
     X = torch.from_numpy(wl.image_inputs(wl.INPUT_SEED, 7000, n)).to(DEV)
     l_ref, p_ref = _run(P.build_sdn_resnet56(r56w, n), X)
     X, order = _skewed(X, p_ref, 0.5)
     outs = _rebalanced(P.build_sdn_resnet56, r56w, [X[:200].contiguous(), X[200:].contiguous()], policy=1,
-                       max_batch=200)
+                       max_batch=200, mode=mode)
     assert np.array_equal(np.concatenate([o[1] for o in outs]), p_ref[order])
     assert np.array_equal(np.concatenate([o[0] for o in outs]), l_ref[order])
 
 
-def test_nccl_transport_world1(r56w):
+@pytest.mark.parametrize("mode", MODES, ids=["host", "device"])
+def test_nccl_transport_world1(r56w, mode):
     """dycl_set_comm with torch's own NCCL communicator (world 1: the count all-gather runs on
     NCCL every exit, no rows move); results equal the plain run."""
     import torch.distributed as dist
@@ -171,6 +188,8 @@ def test_nccl_transport_world1(r56w):
         l_ref, p_ref = _run(P.build_sdn_resnet56(r56w, n), X)
         m = P.build_sdn_resnet56(r56w, n)
         D.dycl_set_comm(m.g, DI.nccl_comm_ptr(), 0, 1, D.DYCL_REBALANCE_ALL)
+        D.dycl_set_rebalance_mode(m.g, mode)
+        l1, p1 = _run(m, X)
         l1, p1 = _run(m, X)
         assert np.array_equal(p1, p_ref) and np.array_equal(l1, l_ref)
         assert D.dycl_rebalance_stats(m.g) == (0, 0)
