@@ -127,6 +127,7 @@ struct dycl_graph_s {
   int precision = DYCL_PREC_FP32_STREAM;
   int conv_path = 0;                 // 0 auto; DYCL_CONV_PATH=1 forces the cp.async kernel
   int conv_dbg = 0;                  // DYCL_CONV_DBG: timing experiments only (results invalid)
+  int halo_kskip = 1;                // DYCL_HALO_KSKIP=0: the s4d stem multiplies its zero channels too
   int no_fuse = 0;                   // DYCL_NO_FUSE=1: run basic blocks as two conv launches
   int head_cuda_core = 0;            // DYCL_HEAD_CUDA_CORE=1: wide-head FC on CUDA cores (k_head_fc), not tcgen05
   // pair residual stream (set at finalize; DYCL_NO_PAIR=1 disables): in NHWC graphs without gates,
@@ -776,6 +777,7 @@ struct Exec {
         a.Ho = L.out.H / 2; a.Wo = L.out.W / 2; a.Cout = 4 * L.out.C;
         a.ksz = 3; a.stride = 1; a.pad = 1;
         a.K = a.Kp = 9 * 64;
+        a.c_live = g->halo_kskip ? 16 * L.in.C : 0;   // 4x4 pixels x C real channels per block; the rest zero
         a.w_rt = nullptr;
         a.in_nhwc = a.nhwc = 1;
       }
@@ -1370,6 +1372,7 @@ dycl_status dycl_graph_create(int cuda_device, int in_h, int in_w, int in_c, dyc
   g->input = Shape{in_h, in_w, in_c};
   if (const char* cp = getenv("DYCL_CONV_PATH")) g->conv_path = atoi(cp);
   if (const char* cd = getenv("DYCL_CONV_DBG")) g->conv_dbg = atoi(cd);
+  if (const char* hk = getenv("DYCL_HALO_KSKIP")) g->halo_kskip = atoi(hk);
   if (const char* nf = getenv("DYCL_NO_FUSE")) g->no_fuse = atoi(nf);
   if (const char* hc = getenv("DYCL_HEAD_CUDA_CORE")) g->head_cuda_core = atoi(hc);
   if (const char* mf = getenv("DYCL_MAX_FUSE")) g->max_fuse = atoi(mf);

@@ -26,6 +26,7 @@ struct ConvArgs {
   int n_static;
   int H, W, C, Ho, Wo, Cout, ksz, stride, pad;
   int K, Kp;
+  int c_live = 0;       // input channels that can be nonzero (a prefix of C; 0 = all): the s4d stem's 48 of 64
   int relu;
   int res_mode;          // 0 none, 1 identity [n][Ho][Wo][Cout], 2 option A from [n][rH][rW][rC]
   int rH, rW, rC, r_pad_lo;
@@ -138,8 +139,8 @@ inline void pack_rowtap(const uint16_t* wp, int cout, int kp, int cp, uint16_t* 
 // boxes; *handled = false (and nothing launched) when the shape does not qualify.
 cudaError_t launch_conv_tma(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream, bool* handled);
 // Dense-layer GEMM on tcgen05 with TMA SWIZZLE_128B tiles (gemm_tma.cu): [rows][K] x [N][K].
-// 3x3 / s1 / p1 NHWC conv, 64 -> 64 channels, W + 2 <= 128, bf16 output only: TMA halo tile +
-// shifted UMMA descriptors (conv_halo.cu)
+// 3x3 / 4x4 stride-1 NHWC conv, 64 -> 64 / 128 / 256 or 16 -> 64 channels, whole output rows per
+// 128-row tile, bf16 output only: TMA halo tile + shifted UMMA descriptors (conv_halo.cu)
 bool conv_halo_eligible(const ConvArgs& a);
 cudaError_t launch_conv_halo(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream);
 bool gemm_tma_eligible(const ConvArgs& a);

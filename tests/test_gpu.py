@@ -135,6 +135,9 @@ NHWC_CASES = [
     (1, 9, 30, 64, 64, 3, 1, 1, 1, 0),       # R = 3 (9 / 3), P = 32
     (2, 8, 8, 64, 64, 3, 1, 1, 1, 0),        # 8 x 8: 80 of 128 rows real -> the im2col GEMM instead
     (2, 11, 47, 16, 64, 4, 1, 2, 1, 0),      # 4x4 / pad 2 over 16 channels (the 2x2 s2d stem's form): R = 2
+    (2, 56, 56, 64, 256, 3, 1, 1, 1, 0),     # the 4x4 space-to-depth stem: N = 256 split over CTA pairs
+    (3, 14, 14, 64, 128, 3, 1, 1, 0, 0),     # N = 128 in one CTA, R = 7
+    (1, 9, 30, 64, 256, 3, 1, 1, 1, 0),      # N split, R = 3, a single sample
 ]
 # row-tap GEMM form (path 5): 3x3 / s1 / p1, whole samples per 128-row tile, W | 32, Cout 64
 ROWTAP_NHWC_CASES = [
