@@ -309,14 +309,21 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
           if (k > 0) ptx::mbar_wait((G::NSETS == 1 ? subfree0 : tready0) + 8 * j, (k - 1) & 1);
           if (k > 0 || blk > 0) ptx::tc_fence_after();
+          // one elected lane issues the sub-tile's MMAs; descriptors advance by 32-bit adds on
+          // their start-address word (a per-MMA elect + 64-bit descriptor build cost more issue
+          // slots than a 128 x 3C x 16 MMA runs)
+          if (ptx::elect_one()) {
 #pragma unroll
-          for (int r = 0; r < 3; ++r)
+            for (int r = 0; r < 3; ++r)
 #pragma unroll
-            for (int q = 0; q < C / 16; ++q)
-              ptx::mma_bf16_ss_elect(tmem + j * G::N,
-                                     xdesc + (uint64_t)(((j * G::BH + r) * W * 16 + 2 * q * G::PLANE) >> 4),
-                                     w1d + (uint64_t)(((r * P + 2 * q) * G::N * 16) >> 4), IDESC,
-                                     (uint32_t)((r | q) != 0));
+              for (int q = 0; q < C / 16; ++q)
+                ptx::mma_bf16_ss_lohi(tmem + j * G::N,
+                                      (uint32_t)xdesc + (uint32_t)(((j * G::BH + r) * W * 16 + 2 * q * G::PLANE) >> 4),
+                                      (uint32_t)(xdesc >> 32),
+                                      (uint32_t)w1d + (uint32_t)(((r * P + 2 * q) * G::N * 16) >> 4),
+                                      (uint32_t)(w1d >> 32), IDESC, (uint32_t)((r | q) != 0));
+          }
+          __syncwarp();
           ptx::mma_commit_elect(acc1j0 + 8 * j);
         }
         // xb is free for the next sample's conversion once the LAST block's conv1 has read it
@@ -336,14 +343,18 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (j + 1 < G::NSUB) ptx::mbar_wait(tready0 + 8 * (j + 1), ph);
           if (G::NSETS == 2 && k > 0) ptx::mbar_wait(subfree0 + 8 * j, (k - 1) & 1);
           ptx::tc_fence_after();
+          if (ptx::elect_one()) {
 #pragma unroll
-          for (int r = 0; r < 3; ++r)
+            for (int r = 0; r < 3; ++r)
 #pragma unroll
-            for (int q = 0; q < C / 16; ++q)
-              ptx::mma_bf16_ss_elect(tmem + SET2 + j * G::N,
-                                     tdesc + (uint64_t)(((j * G::BH + r) * W * 16 + 2 * q * G::PLANE) >> 4),
-                                     w2d + (uint64_t)(((r * P + 2 * q) * G::N * 16) >> 4), IDESC,
-                                     (uint32_t)((r | q) != 0));
+              for (int q = 0; q < C / 16; ++q)
+                ptx::mma_bf16_ss_lohi(tmem + SET2 + j * G::N,
+                                      (uint32_t)tdesc + (uint32_t)(((j * G::BH + r) * W * 16 + 2 * q * G::PLANE) >> 4),
+                                      (uint32_t)(tdesc >> 32),
+                                      (uint32_t)w2d + (uint32_t)(((r * P + 2 * q) * G::N * 16) >> 4),
+                                      (uint32_t)(w2d >> 32), IDESC, (uint32_t)((r | q) != 0));
+          }
+          __syncwarp();
           ptx::mma_commit_elect(acc2j0 + 8 * j);
         }
         if (!wres) ptx::mma_commit_elect(wempty0 + 8 * ws_slot);   // free the ring slot once conv2 ends

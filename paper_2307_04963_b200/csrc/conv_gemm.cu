@@ -309,11 +309,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         ptx::tc_fence_after();
         const uint64_t ad = ptx::make_smem_desc_sw128(ptx::smem_u32(sA + stage * G::A_BYTES));
         const uint64_t bd = ptx::make_smem_desc_sw128(ptx::smem_u32(sB + (pl.bres ? kb : stage) * BB));
+        if (ptx::elect_one() && !(dbg & 2048)) {   // dbg 2048: timing experiment, no MMAs
 #pragma unroll
-        for (int j = 0; j < BKE / 16; ++j)
-          if (!(dbg & 2048))                       // timing experiment: no MMAs
-            ptx::mma_bf16_ss_elect(d, ad + (uint64_t)(2 * j), bd + (uint64_t)(2 * j), IDESC,
-                                   (uint32_t)((kb | j) != 0));
+          for (int j = 0; j < BKE / 16; ++j)
+            ptx::mma_bf16_ss_lohi(d, (uint32_t)ad + 2 * j, (uint32_t)(ad >> 32), (uint32_t)bd + 2 * j,
+                                  (uint32_t)(bd >> 32), IDESC, (uint32_t)((kb | j) != 0));
+        }
+        __syncwarp();
         ptx::mma_commit_elect(empty0 + 8 * stage);
         __syncwarp();
         if (++stage == S) {

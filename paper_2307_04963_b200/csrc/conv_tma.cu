@@ -230,9 +230,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int ks = 0; ks < P.nks; ++ks) {
         ptx::mbar_wait(full0 + 8 * stage, phase);
         ptx::tc_fence_after();
-        if (!(a.dbg & 2)) {
-          // Warp-uniform, compile-time-unrolled issue: descriptor offsets stay in
-          // uniform registers, one elected lane issues each tcgen05.mma.
+        if (!(a.dbg & 2) && ptx::elect_one()) {
+          // compile-time-unrolled issue by one elected lane (descriptor offsets in uniform registers)
           const uint64_t ad0 = adesc0 + ((uint32_t)(stage * P.stage_bytes) >> 4);
           const uint64_t bd0 = bdesc0 + (b_nt >> 4);
           const uint32_t plane16 = (uint32_t)P.a_lbo >> 4;            // 16-byte units
@@ -249,7 +248,7 @@ __global__ void __launch_bounds__(THREADS, 1)
               for (int r = 0; r < 3; ++r) {
 #pragma unroll
                 for (int q = 0; q < KCH; ++q)
-                  ptx::mma_bf16_ss_elect(dj, aj + (uint32_t)r * row16 + 2 * q * plane16,
+                  ptx::mma_bf16_ss(dj, aj + (uint32_t)r * row16 + 2 * q * plane16,
                                          bd0 + (uint32_t)(r * (a.C / 8) + 2 * q) * chunk16, IDESC,
                                          (uint32_t)((r | q) != 0));
               }
@@ -266,7 +265,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const uint32_t ao = (uint32_t)(t % 3) * shift16 + (uint32_t)(t / 3) * row16;
 #pragma unroll
                 for (int q = 0; q < KCH; ++q)
-                  ptx::mma_bf16_ss_elect(dj, aj + ao + 2 * q * plane16, bd0 + t * tapb16 + (uint32_t)(2 * q * BN),
+                  ptx::mma_bf16_ss(dj, aj + ao + 2 * q * plane16, bd0 + t * tapb16 + (uint32_t)(2 * q * BN),
                                          IDESC, (uint32_t)((t | q) != 0));
               }
             }
@@ -282,18 +281,19 @@ __global__ void __launch_bounds__(THREADS, 1)
               uint64_t bt = bd0 + (uint32_t)t0 * tapb16;
               if (KCH == 0) {                       // C == 8: K step = a pair of taps (LBO = one tap)
                 for (int t = t0; t < t1; t += 2, at += 2 * tap16, bt += 2 * tapb16)
-                  ptx::mma_bf16_ss_elect(dj, at, bt, IDESC, (uint32_t)(t != 0));
+                  ptx::mma_bf16_ss(dj, at, bt, IDESC, (uint32_t)(t != 0));
               } else {
                 for (int t = t0; t < t1; ++t, at += tap16, bt += tapb16) {
 #pragma unroll
                   for (int q = 0; q < KCH; ++q)
-                    ptx::mma_bf16_ss_elect(dj, at + 2 * q * plane16, bt + (uint32_t)(2 * q * BN), IDESC,
+                    ptx::mma_bf16_ss(dj, at + 2 * q * plane16, bt + (uint32_t)(2 * q * BN), IDESC,
                                            (uint32_t)((t | q) != 0));
                 }
               }
             }
           }
         }
+        __syncwarp();
         ptx::mma_commit_elect(empty0 + 8 * stage);
         __syncwarp();
         if (++stage == S) {
