@@ -2269,7 +2269,12 @@ dycl_status dycl_local_group_destroy(dycl_local_group grp) {
 dycl_status dycl_set_comm_local(dycl_graph g, dycl_local_group grp, int rank, int rebalance_policy) {
   if (!g || !grp) return DYCL_E_INVALID_ARG;
   if (!g->finalized) return fail(g, DYCL_E_STATE, "dycl_set_comm_local: finalize the graph first");
-  if (rank < 0 || rank >= dycl::local_group_world(grp->g)) return fail(g, DYCL_E_INVALID_ARG, "bad rank");
+  const int world = dycl::local_group_world(grp->g);
+  if (rank < 0 || rank >= world) return fail(g, DYCL_E_INVALID_ARG, "bad rank");
+  // in-process ranks share one GPU: with device-initiated rebalancing a rank's wait kernels spin
+  // on an SM while the others compute, so compute grids leave `world` SMs free (a persistent
+  // grid of one CTA per SM could otherwise never start its last CTA behind a spinner)
+  if (world > 1 && g->num_sms > world) g->num_sms -= world;
   return set_transport(g, dycl::make_local_transport(grp->g, rank), rebalance_policy);
 }
 

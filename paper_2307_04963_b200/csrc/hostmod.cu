@@ -651,44 +651,46 @@ __global__ void k_maxpool(const PoolArgs a) {
 // rows 2P-1..2P+1 x cols 2Q-1..2Q+1 = its own 4 phases, phases b = 1 of block P-1, b' = 1 of
 // block Q-1 and phase (1,1) of block (P-1, Q-1).  One thread per (sample, pixel, 8-channel group).
 __global__ void k_maxpool_s2d(const PoolArgs a) {
+  // grid: x over (pixel, group) items of one sample, y over samples; 32-bit index math (the
+  // 64-bit divisions of a flat index made this kernel ALU-bound)
   const int n_live = *a.n_live;
   const int G = a.C / 8, C4 = 4 * a.C;
-  const int HWo = a.Ho * a.Wo;
-  const int64_t total = (int64_t)n_live * HWo * G;
-  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total; u += (int64_t)gridDim.x * blockDim.x) {
-    const int g = (int)(u % G);
-    const int64_t t = u / G;
-    const int p = (int)(t % HWo);
-    const int64_t n = t / HWo;
-    const int P = p / a.Wo, Q = p - (p / a.Wo) * a.Wo;
-    float m[8];
+  const int items = a.Ho * a.Wo * G;
+  for (int n = blockIdx.y; n < n_live; n += gridDim.y) {
+    const uint16_t* xs = a.x + (size_t)n * a.Ho * a.Wo * C4;
+    uint16_t* ys = a.y + (size_t)n * a.Ho * a.Wo * a.C;
+    for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < items; w += gridDim.x * blockDim.x) {
+      const int p = w / G, g = w - (w / G) * G;
+      const int P = p / a.Wo, Q = p - (p / a.Wo) * a.Wo;
+      float m[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) m[j] = -INFINITY;
-    auto take = [&](int pp, int qq, int ph) {
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.x + ((n * a.Ho + pp) * a.Wo + qq) * C4 + ph * a.C + g * 8));
-      const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+      for (int j = 0; j < 8; ++j) m[j] = -INFINITY;
+      auto take = [&](int pp, int qq, int ph) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(xs + (pp * a.Wo + qq) * C4 + ph * a.C + g * 8));
+        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          m[2 * j] = fmaxf(m[2 * j], __uint_as_float(w4[j] << 16));
+          m[2 * j + 1] = fmaxf(m[2 * j + 1], __uint_as_float(w4[j] & 0xFFFF0000u));
+        }
+      };
+#pragma unroll
+      for (int ph = 0; ph < 4; ++ph) take(P, Q, ph);
+      if (P > 0) { take(P - 1, Q, 2); take(P - 1, Q, 3); }
+      if (Q > 0) { take(P, Q - 1, 1); take(P, Q - 1, 3); }
+      if (P > 0 && Q > 0) take(P - 1, Q - 1, 3);
+      uint32_t o[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        m[2 * j] = fmaxf(m[2 * j], __uint_as_float(w4[j] << 16));
-        m[2 * j + 1] = fmaxf(m[2 * j + 1], __uint_as_float(w4[j] & 0xFFFF0000u));
+        __nv_bfloat162 v = __floats2bfloat162_rn(m[2 * j], m[2 * j + 1]);
+        o[j] = *reinterpret_cast<uint32_t*>(&v);
       }
-    };
-#pragma unroll
-    for (int ph = 0; ph < 4; ++ph) take(P, Q, ph);
-    if (P > 0) { take(P - 1, Q, 2); take(P - 1, Q, 3); }
-    if (Q > 0) { take(P, Q - 1, 1); take(P, Q - 1, 3); }
-    if (P > 0 && Q > 0) take(P - 1, Q - 1, 3);
-    uint32_t o[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      __nv_bfloat162 v = __floats2bfloat162_rn(m[2 * j], m[2 * j + 1]);
-      o[j] = *reinterpret_cast<uint32_t*>(&v);
-    }
-    *reinterpret_cast<uint4*>(a.y + (n * HWo + p) * a.C + g * 8) = make_uint4(o[0], o[1], o[2], o[3]);
-    if (a.y32) {
-      float4* q = reinterpret_cast<float4*>(a.y32 + (n * HWo + p) * a.C + g * 8);
-      q[0] = make_float4(m[0], m[1], m[2], m[3]);
-      q[1] = make_float4(m[4], m[5], m[6], m[7]);
+      *reinterpret_cast<uint4*>(ys + (size_t)p * a.C + g * 8) = make_uint4(o[0], o[1], o[2], o[3]);
+      if (a.y32) {
+        float4* q = reinterpret_cast<float4*>(a.y32 + ((size_t)n * a.Ho * a.Wo + p) * a.C + g * 8);
+        q[0] = make_float4(m[0], m[1], m[2], m[3]);
+        q[1] = make_float4(m[4], m[5], m[6], m[7]);
+      }
     }
   }
 }
@@ -726,11 +728,19 @@ __global__ void k_cast_s2d2(const float* __restrict__ in, uint16_t* __restrict__
   }
 }
 
-__global__ void k_cast_s4d(const float* __restrict__ in, uint16_t* __restrict__ out, int64_t total, int H, int W,
-                           int c, int vec) {
+__global__ void __launch_bounds__(256) k_cast_s4d(const float* __restrict__ in, uint16_t* __restrict__ out,
+                                                   int64_t total, int H, int W, int c, int vec) {
+  // a warp converts 32 consecutive output pixels (4 KB of output) and stores them through SMEM
+  // as contiguous 512-byte rows (direct 16-byte stores at a 128-byte lane stride left the
+  // kernel at ~3.4 TB/s)
+  __shared__ uint4 stage[8][256];
   const int Wb = W / 4, Hb = H / 4;
-  for (int64_t pix = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pix < total;
-       pix += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  uint4* sw = stage[threadIdx.x >> 5];
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < total;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pix = base + lane;
+    const bool ok = pix < total;
     // 32-bit index arithmetic when the launch fits (64-bit division is a long software sequence)
     int Q, P;
     int64_t n;
@@ -749,7 +759,7 @@ __global__ void k_cast_s4d(const float* __restrict__ in, uint16_t* __restrict__ 
     float v[64];
 #pragma unroll
     for (int k = 0; k < 64; ++k) v[k] = 0.0f;
-    if (vec) {
+    if (ok && vec) {
 #pragma unroll
       for (int pr = 0; pr < 4; ++pr) {
         const float4* src = reinterpret_cast<const float4*>(in + ((n * H + 4 * P + pr) * (int64_t)W + 4 * Q) * 3);
@@ -759,13 +769,12 @@ __global__ void k_cast_s4d(const float* __restrict__ in, uint16_t* __restrict__ 
           v[pr * 12 + 4 * q] = f.x; v[pr * 12 + 4 * q + 1] = f.y; v[pr * 12 + 4 * q + 2] = f.z; v[pr * 12 + 4 * q + 3] = f.w;
         }
       }
-    } else {
+    } else if (ok) {
       for (int ch = 0; ch < 16 * c; ++ch) {
         const int ph = ch / c, ci = ch - ph * c;
         v[ch] = __ldg(in + ((n * H + 4 * P + (ph >> 2)) * (int64_t)W + 4 * Q + (ph & 3)) * c + ci);
       }
     }
-    uint4* dst = reinterpret_cast<uint4*>(out + pix * 64);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       uint32_t o[4];
@@ -774,8 +783,16 @@ __global__ void k_cast_s4d(const float* __restrict__ in, uint16_t* __restrict__ 
         __nv_bfloat162 b = __floats2bfloat162_rn(v[8 * j + 2 * k], v[8 * j + 2 * k + 1]);
         o[k] = *reinterpret_cast<uint32_t*>(&b);
       }
-      dst[j] = make_uint4(o[0], o[1], o[2], o[3]);
+      sw[lane * 8 + (j ^ (lane & 7))] = make_uint4(o[0], o[1], o[2], o[3]);   // XOR: conflict-free
     }
+    __syncwarp();
+    uint4* dst = reinterpret_cast<uint4*>(out + base * 64);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int e = k * 32 + lane, pe = e >> 3;
+      if (base + pe < total) dst[e] = sw[pe * 8 + ((e & 7) ^ (pe & 7))];
+    }
+    __syncwarp();
   }
 }
 
@@ -830,11 +847,10 @@ cudaError_t launch_cast_s4d(const float* in, uint16_t* out, int64_t n, int H, in
 cudaError_t launch_maxpool(const PoolArgs& a, int max_rows, int num_sms, cudaStream_t s) {
   if (a.s2d) {
     if (!a.nhwc || a.k != 3 || a.stride != 2 || a.pad != 1) return cudaErrorInvalidValue;
-    const int64_t total = (int64_t)max_rows * (a.C / 8) * a.Ho * a.Wo;
-    int64_t blocks = (total + 255) / 256;
-    if (blocks > (int64_t)num_sms * 16) blocks = (int64_t)num_sms * 16;
-    if (blocks < 1) blocks = 1;
-    k_maxpool_s2d<<<(int)blocks, 256, 0, s>>>(a);
+    const int items = (a.C / 8) * a.Ho * a.Wo;
+    const int bx = (items + 255) / 256;
+    const int by = max_rows < 1 ? 1 : max_rows > 65535 ? 65535 : max_rows;
+    k_maxpool_s2d<<<dim3(bx, by), 256, 0, s>>>(a);
     return cudaGetLastError();
   }
   const int64_t total = (int64_t)max_rows * (a.C / 8) * a.Ho * a.Wo;
