@@ -36,6 +36,26 @@ struct GCfg {
   static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
 };
 
+__device__ __forceinline__ void named_bar(int id) { asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory"); }
+
+// The N-tile CTAs of one M tile meet (fused LayerNorm): the calling warpgroup's stores are
+// published, its leader counts in and spins until `target` CTAs have (the counter only grows
+// until the last CTA re-arms it after the final meeting). Every CTA of the grid is resident
+// (one tile per CTA, grid <= SMs), so the wait is bounded by the slowest tile.
+__device__ __forceinline__ void ln_meet(int* cnt, int target, int wg, bool leader) {
+  __threadfence();
+  named_bar(1 + wg);
+  if (leader) {
+    atomicAdd(cnt, 1);
+    int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+    } while (v < target);
+    __threadfence();
+  }
+  named_bar(1 + wg);
+}
+
 template <int BN>
 __global__ void __launch_bounds__(THREADS, 1)
     k_gemm_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const ConvArgs a) {
@@ -188,6 +208,71 @@ __global__ void __launch_bounds__(THREADS, 1)
           a.am_val[(size_t)m * n_tiles + n_tile] = best;
           a.am_idx[(size_t)m * n_tiles + n_tile] = bi;
         }
+      } else if (BN == 64 && a.ln_gamma) {
+        // residual + LayerNorm over the whole row (ConvArgs.ln_*): this CTA's 64 columns stay
+        // in registers; the row's mean and centred sum of squares are assembled from the
+        // N tiles' partials (ascending tile order) after two meetings on ln_cnt[m_tile]
+        const int col0 = n_tile * BN;
+        float v[BN];
+#pragma unroll
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          uint32_t u[16];
+          ptx::tmem_ld_32x32b_x16(t_base + (uint32_t)c0, u);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int q = 0; q < 16; ++q) v[c0 + q] = __uint_as_float(u[q]) + __ldg(a.bias + col0 + c0 + q);
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(tempty0 + 8 * acc);           // the accumulator is in registers now
+        if (m < M) {
+          const float4* rp = reinterpret_cast<const float4*>(a.res32 + (size_t)m * a.Cout + col0);
+#pragma unroll
+          for (int j = 0; j < BN / 4; ++j) {
+            const float4 q = rp[j];                      // coherent load: y32 may alias res32
+            v[4 * j] += q.x; v[4 * j + 1] += q.y; v[4 * j + 2] += q.z; v[4 * j + 3] += q.w;
+          }
+        }
+        float* part = a.ln_part + (size_t)(m < M ? m : 0) * 2 * n_tiles;
+        float s1 = 0.f;
+#pragma unroll
+        for (int q = 0; q < BN; ++q) s1 += v[q];
+        if (m < M) __stcg(part + n_tile, s1);
+        ln_meet(a.ln_cnt + m_tile, n_tiles, wg, r == 0);
+        float mu = 0.f;
+        for (int t = 0; t < n_tiles; ++t) mu += __ldcg(part + t);
+        mu /= (float)a.Cout;
+        float s2 = 0.f;
+#pragma unroll
+        for (int q = 0; q < BN; ++q) {
+          const float dd = v[q] - mu;
+          s2 += dd * dd;
+        }
+        if (m < M) __stcg(part + n_tiles + n_tile, s2);
+        ln_meet(a.ln_cnt + m_tile, 2 * n_tiles, wg, r == 0);
+        float q2 = 0.f;
+        for (int t = 0; t < n_tiles; ++t) q2 += __ldcg(part + n_tiles + t);
+        const float rstd = rsqrtf(q2 / (float)a.Cout + a.ln_eps);
+        // last meeting: every CTA of the M tile is past its reads; the last one re-arms the counter
+        named_bar(1 + wg);
+        if (r == 0 && atomicAdd(a.ln_cnt + m_tile, 1) == 3 * n_tiles - 1) atomicExch(a.ln_cnt + m_tile, 0);
+        if (m < M) {
+          float4* yq = reinterpret_cast<float4*>(a.y32 + (size_t)m * a.Cout + col0);
+          uint4* yb = reinterpret_cast<uint4*>(a.y + (size_t)m * a.Cout + col0);
+#pragma unroll
+          for (int j = 0; j < BN / 8; ++j) {
+            float y[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int c = col0 + 8 * j + e;
+              y[e] = (v[8 * j + e] - mu) * rstd * __ldg(a.ln_gamma + c) + __ldg(a.ln_beta + c);
+            }
+            yq[2 * j] = make_float4(y[0], y[1], y[2], y[3]);
+            yq[2 * j + 1] = make_float4(y[4], y[5], y[6], y[7]);
+            yb[j] = make_uint4(pack_bf16x2_rn(y[0], y[1]), pack_bf16x2_rn(y[2], y[3]), pack_bf16x2_rn(y[4], y[5]),
+                               pack_bf16x2_rn(y[6], y[7]));
+          }
+        }
+        continue;
       } else {
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 16) {
@@ -267,6 +352,11 @@ bool gemm_tma_eligible(const ConvArgs& a) {
          a.Kp == a.K && (a.Cout % 64 == 0) && a.res_mode != 2;
 }
 
+bool gemm_tma_ln_ok(const ConvArgs& a, int max_rows, int num_sms) {
+  const long long tiles = (long long)((max_rows + BM - 1) / BM) * (a.Cout / 64);
+  return gemm_tma_eligible(a) && a.Cout % 64 == 0 && a.res_mode == 1 && a.res32 && tiles <= num_sms;
+}
+
 int gemm_tma_bn(const ConvArgs& a, int max_rows, int num_sms) {
   const long long m_tiles = (max_rows + BM - 1) / BM;
   if (a.Cout % 256 == 0 && m_tiles * (a.Cout / 256) >= num_sms / 2) return 256;
@@ -275,6 +365,12 @@ int gemm_tma_bn(const ConvArgs& a, int max_rows, int num_sms) {
 }
 
 cudaError_t launch_gemm_tma(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream) {
+  if (a.ln_gamma) {
+    // fused LayerNorm: 64-wide N tiles, every tile its own CTA (the tiles of an M tile meet)
+    if (!gemm_tma_ln_ok(a, max_rows, num_sms) || !a.ln_part || !a.ln_cnt || !a.y || !a.y32 || a.split || a.relu)
+      return cudaErrorInvalidValue;
+    return launch_bn<64>(a, max_rows, num_sms, stream);
+  }
   // 256-wide N tiles unless they leave more than half of the SMs idle (small-M decode GEMMs)
   switch (gemm_tma_bn(a, max_rows, num_sms)) {
     case 256: return launch_bn<256>(a, max_rows, num_sms, stream);

@@ -59,6 +59,11 @@ struct dycl_s2s_s {
   bool fuse_argmax = true;           // LM-head argmax in the GEMM epilogue (DYCL_S2S_FUSE_ARGMAX=0 disables)
   float* am_val = nullptr;           // fused argmax partials [max_batch][vocab / 64]
   int* am_idx = nullptr;
+  // residual + LayerNorm in the epilogue of the out-proj / FFN-down GEMMs of the decode step
+  // (ConvArgs.ln_*; DYCL_S2S_FUSE_LN=0 disables): row partials and per-M-tile meeting counters
+  bool fuse_ln = true;
+  float* ln_part = nullptr;          // [max_batch][2][d / 64]
+  int* ln_cnt = nullptr;             // [max_batch / 128 + 1], zero between launches
   // DYCL_PREC_BF16X3_PARITY: every bf16 tensor is a split pair [hi | lo] and every GEMM runs
   // on K-concatenated operands [A_hi | A_lo] x [W | W] (weights are exact bf16, so the
   // W_lo terms of the 3-pass product vanish): fp32-accurate products on the tensor cores
@@ -190,6 +195,29 @@ struct S2SExec {
     pe();
     return e;
   }
+  // x32 <- LN(x32 + x W^T + b), xb <- bf16 of it: one GEMM with the LayerNorm in its epilogue
+  // when it applies (decode steps), else the GEMM into `pre` followed by k_layernorm
+  cudaError_t gemm_res_ln(const uint16_t* x, int K, const uint16_t* w, const float* b, const float* g,
+                          const float* be, const int* cnt, int n_static, int max_rows) {
+    const int d = s->c.d_model;
+    dycl::ConvArgs a{};
+    a.x = x; a.w = w; a.bias = b; a.res32 = s->x32; a.res_mode = 1;
+    a.y = s->xb; a.y32 = s->x32; a.n_live = cnt; a.n_static = n_static;
+    a.H = a.W = a.Ho = a.Wo = 1; a.C = K; a.Cout = d; a.ksz = 1; a.stride = 1; a.pad = 0;
+    a.K = K; a.Kp = K; a.relu = 0;
+    a.rH = a.rW = 1; a.rC = d;
+    a.nhwc = a.in_nhwc = 1;
+    if (!s->fuse_ln || s->pair || s->gemm_path || !dycl::gemm_tma_ln_ok(a, max_rows, s->num_sms)) {
+      cudaError_t e = gemm(x, K, w, b, d, s->x32, nullptr, s->pre, 0, cnt, n_static, max_rows);
+      return e != cudaSuccess ? e : ln(s->pre, g, be, cnt, n_static, max_rows);
+    }
+    a.ln_gamma = g; a.ln_beta = be; a.ln_part = s->ln_part; a.ln_cnt = s->ln_cnt; a.ln_eps = 1e-5f;
+    ++n;
+    pb(DYCL_K_GEMM, cnt, n_static, 2.0 * K + 2.0 * d + 4.0 * d + 4.0 * d, 2.0 * K * d + 8.0 * d, 2.0 * K * d);
+    const cudaError_t e = dycl::launch_gemm_tma(a, max_rows, s->num_sms, st);
+    pe();
+    return e;
+  }
   cudaError_t ln(const float* in, const float* g, const float* b, const int* cnt, int n_static, int max_rows) {
     dycl::S2SLnArgs a{in, g, b, s->x32, s->xb, cnt, n_static, s->c.d_model, 1e-5f};
     a.pair = s->pair;
@@ -266,8 +294,7 @@ struct S2SExec {
         E(dycl::launch_attn_decoder(sa, B, st));
         pe();
         ++n;
-        E(gemm(s->att, d, L.wo, L.bo, d, s->x32, nullptr, s->pre, 0, cnt, 0, B));
-        E(ln(s->pre, L.lsg, L.lsb, cnt, 0, B));
+        E(gemm_res_ln(s->att, d, L.wo, L.bo, L.lsg, L.lsb, cnt, 0, B));
         E(gemm(s->xb, d, L.wq2, L.bq2, d, nullptr, s->att, nullptr, 0, cnt, 0, B));
         dycl::S2SAttnArgs ca{};
         ca.q = s->att; ca.q_stride = (s->pair ? 2 : 1) * d; ca.kv = s->cross[l]; ca.out = s->qkv;  // reuse qkv as scratch
@@ -277,11 +304,9 @@ struct S2SExec {
         E(dycl::launch_attn_decoder(ca, B, st));
         pe();
         ++n;
-        E(gemm(s->qkv, d, L.wo2, L.bo2, d, s->x32, nullptr, s->pre, 0, cnt, 0, B));
-        E(ln(s->pre, L.lcg, L.lcb, cnt, 0, B));
+        E(gemm_res_ln(s->qkv, d, L.wo2, L.bo2, L.lcg, L.lcb, cnt, 0, B));
         E(gemm(s->xb, d, L.w1, L.b1, c.d_ff, nullptr, s->h, nullptr, 1, cnt, 0, B));
-        E(gemm(s->h, c.d_ff, L.w2, L.b2, d, s->x32, nullptr, s->pre, 0, cnt, 0, B));
-        E(ln(s->pre, L.lfg, L.lfb, cnt, 0, B));
+        E(gemm_res_ln(s->h, c.d_ff, L.w2, L.b2, L.lfg, L.lfb, cnt, 0, B));
       }
       dycl::S2SArgmaxArgs ga{s->logits, slot, src, s->len_table, s->beta, tokens, top1, logits0,
                              s->cur_tok, lengths, s->flag, cnt, c.vocab, S, c.max_len, t, c.eos};
@@ -347,6 +372,7 @@ dycl_status dycl_s2s_create(int cuda_device, const dycl_s2s_config* cfg, dycl_s2
   if (const char* gp = getenv("DYCL_S2S_GEMM")) s->gemm_path = atoi(gp);
   if (const char* pp = getenv("DYCL_S2S_PDL")) s->pdl = atoi(pp) != 0;
   if (const char* fa = getenv("DYCL_S2S_FUSE_ARGMAX")) s->fuse_argmax = atoi(fa) != 0;
+  if (const char* fl = getenv("DYCL_S2S_FUSE_LN")) s->fuse_ln = atoi(fl) != 0;
   cudaSetDevice(cuda_device);
   cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
   *out = s;
@@ -456,8 +482,10 @@ dycl_status dycl_s2s_finalize(dycl_s2s s, int64_t max_batch) {
       (r = alloc(s, &s->am_idx, B * (size_t)(s->c.vocab / 64))) ||
       (r = alloc(s, &s->cur_tok, B)) || (r = alloc(s, &s->active[0], B)) || (r = alloc(s, &s->active[1], B)) ||
       (r = alloc(s, &s->list1, B)) || (r = alloc(s, &s->list0, B)) || (r = alloc(s, &s->counts, 2 * L + 2)) ||
-      (r = alloc(s, &s->flag, B)))
+      (r = alloc(s, &s->flag, B)) || (r = alloc(s, &s->ln_part, B * 2 * (size_t)(d / 64 + 1))) ||
+      (r = alloc(s, &s->ln_cnt, B / 128 + 2)))
     return r;
+  SCK(cudaMemset(s->ln_cnt, 0, (B / 128 + 2) * sizeof(int)));
   s->cross.resize(s->dec.size());
   s->cache.resize(s->dec.size());
   for (size_t l = 0; l < s->dec.size(); ++l)

@@ -5,6 +5,7 @@
 // Numerics (R13): residual stream fp32; every tensor-core operand and the
 // q/k/v, K/V caches, attention outputs bf16 (RNE); softmax / LayerNorm / logits fp32.
 // All reductions are fixed-order warp trees (batch-position independent).
+#include <cuda.h>
 #include <cuda_bf16.h>
 
 #include <cstdlib>
@@ -16,6 +17,10 @@
 
 namespace dycl {
 namespace {
+
+typedef CUresult (*XEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 __device__ __forceinline__ float bf(uint16_t u) { return __uint_as_float((uint32_t)u << 16); }
 __device__ __forceinline__ uint16_t to_bf(float f) {
@@ -511,6 +516,138 @@ __global__ void __launch_bounds__(256, 5) k_attn_decoder(const S2SAttnArgs a) {
   *out = (uint32_t)to_bf(o0) | ((uint32_t)to_bf(o1) << 16);
 }
 
+// Cross attention with the encoder K/V streamed by TMA. The per-warp form above
+// issues its K/V reads from the same warp that consumes them (scores, then softmax, then the
+// V sweep) and leaves its last wave a third full: ~3 TB/s on the 134 MB one decoder layer
+// reads. Here one persistent CTA per SM walks the active rows; a producer lane streams each
+// row's K block and then its V block (heads x S x 128 B each, one 128-byte-swizzled
+// {64, S} box per head) into a 3-stage ring, so two blocks are in flight while the head warps
+// (warp h = head h) consume a third from SMEM. Same arithmetic, same order as k_attn_decoder:
+// scores over dims in pairs ascending, * 1/8, softmax in fp32 with expf, P.V over keys ascending.
+namespace xattn {
+constexpr int NST = 3;
+constexpr int STAGE = 64 * 1024;           // heads * S * 128 B <= 8 * 64 * 128
+constexpr int THREADS = 288;               // warps 0-7 heads, warp 8 producer
+constexpr int SMEM = 1024 + NST * STAGE + 64;
+}  // namespace xattn
+
+__global__ void __launch_bounds__(xattn::THREADS, 1)
+    k_attn_cross_tma(const __grid_constant__ CUtensorMap tmKV, const S2SAttnArgs a) {
+  using namespace xattn;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t full0 = ptx::smem_u32(smem + NST * STAGE);
+  const uint32_t empty0 = full0 + 8 * NST;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NST; ++i) {
+      ptx::mbar_init(full0 + 8 * i, 1);
+      ptx::mbar_init(empty0 + 8 * i, a.heads);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 8 && lane == 0) ptx::tma_prefetch_desc(&tmKV);
+  __syncthreads();
+  ptx::pdl_wait();      // PDL (kernels.h): the live count, slots and queries come from predecessors
+  ptx::pdl_trigger();
+  const int n = a.n_live ? *a.n_live : a.n_static;
+  const int d = a.d, S = a.S;
+  const uint32_t hbytes = (uint32_t)S * 128;          // one head's {64, S} box
+  if (warp == 8) {
+    if (lane == 0) {
+      int st = 0;
+      uint32_t ph = 0;
+      for (int row = blockIdx.x; row < n; row += gridDim.x) {
+        const int slot = a.slot[row];
+        for (int kvh = 0; kvh < 2; ++kvh) {          // K block, then V block
+          ptx::mbar_wait(empty0 + 8 * st, ph ^ 1);
+          const uint32_t bar = full0 + 8 * st;
+          ptx::mbar_arrive_expect_tx(bar, hbytes * (uint32_t)a.heads);
+          for (int h = 0; h < a.heads; ++h)
+            ptx::tma_load_2d(ptx::smem_u32(smem + st * STAGE + h * hbytes), &tmKV, bar, kvh * d + h * 64, slot * S);
+          if (++st == NST) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+    return;
+  }
+  if (warp >= a.heads) return;
+  const int h = warp;
+  int st = 0;
+  uint32_t ph = 0;
+  for (int row = blockIdx.x; row < n; row += gridDim.x) {
+    // the head's 64-dim query, fp32, in registers (every lane holds all of it: broadcast loads)
+    float qv[64];
+    {
+      const uint4* qp = reinterpret_cast<const uint4*>(a.q + (size_t)row * a.q_stride + h * 64);
+#pragma unroll
+      for (int c8 = 0; c8 < 8; ++c8) {
+        const uint4 u4 = qp[c8];
+        const uint32_t u[4] = {u4.x, u4.y, u4.z, u4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          qv[c8 * 8 + 2 * e] = __uint_as_float(u[e] << 16);
+          qv[c8 * 8 + 2 * e + 1] = __uint_as_float(u[e] & 0xFFFF0000u);
+        }
+      }
+    }
+    ptx::mbar_wait(full0 + 8 * st, ph);
+    const uint8_t* kb = smem + st * STAGE + h * hbytes;
+    float s0 = -INFINITY, s1 = -INFINITY;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int j = lane + 32 * half;
+      const bool valid = j < S;
+      const uint8_t* kr = kb + (valid ? j : 0) * 128;
+      const int sw = (valid ? j : 0) & 7;
+      float acc = 0.f;
+#pragma unroll
+      for (int c8 = 0; c8 < 8; ++c8) {
+        const uint4 kk = *reinterpret_cast<const uint4*>(kr + ((c8 ^ sw) << 4));
+        const uint32_t u[4] = {kk.x, kk.y, kk.z, kk.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          acc += qv[c8 * 8 + 2 * e] * __uint_as_float(u[e] << 16) +
+                 qv[c8 * 8 + 2 * e + 1] * __uint_as_float(u[e] & 0xFFFF0000u);
+      }
+      if (valid) {
+        if (half == 0) s0 = acc * 0.125f;
+        else s1 = acc * 0.125f;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(empty0 + 8 * st);
+    if (++st == NST) {
+      st = 0;
+      ph ^= 1;
+    }
+    const float m = warp_max(fmaxf(s0, s1));
+    const float e0 = lane < S ? expf(s0 - m) : 0.f, e1 = lane + 32 < S ? expf(s1 - m) : 0.f;
+    const float inv = 1.f / warp_sum(e0 + e1);
+    ptx::mbar_wait(full0 + 8 * st, ph);
+    const uint8_t* vb = smem + st * STAGE + h * hbytes + ((lane & 3) << 2);
+    float o0 = 0.f, o1 = 0.f;
+#pragma unroll 8
+    for (int j = 0; j < S; ++j) {
+      const float pj = __shfl_sync(0xffffffffu, j < 32 ? e0 : e1, j & 31) * inv;
+      const uint32_t vv = *reinterpret_cast<const uint32_t*>(vb + j * 128 + (((lane >> 2) ^ (j & 7)) << 4));
+      o0 += pj * __uint_as_float(vv << 16);
+      o1 += pj * __uint_as_float(vv & 0xFFFF0000u);
+    }
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(empty0 + 8 * st);
+    if (++st == NST) {
+      st = 0;
+      ph ^= 1;
+    }
+    uint32_t* out = reinterpret_cast<uint32_t*>(a.out + (size_t)row * d + h * 64) + lane;
+    *out = (uint32_t)to_bf(o0) | ((uint32_t)to_bf(o1) << 16);
+  }
+}
+
 // LM-head argmax + EOS / length loop guard, one CTA per active row:
 //   z[EOS] += beta * (t + 1 - LEN[src[slot][0]]);  tok = argmax z (lowest index on ties)
 //   tokens[slot][t] = tok; top1[slot][t] = z[tok]; done -> length = t + 1, flag = 1
@@ -661,6 +798,34 @@ cudaError_t launch_attn_encoder(const S2SAttnArgs& a, int max_seqs, cudaStream_t
 }
 cudaError_t launch_attn_decoder(const S2SAttnArgs& a, int max_rows, cudaStream_t s) {
   if (a.S > 64 || a.max_len > 64 || a.d / a.heads != 64) return cudaErrorInvalidValue;
+  static const bool warp_form = getenv("DYCL_XATTN_WARP") != nullptr;   // A/B timing of the per-warp form
+  if (a.kv && !a.pair && a.heads <= 8 && a.S % 8 == 0 && a.d == 64 * a.heads && !warp_form) {
+    static XEncodeFn enc = nullptr;
+    if (!enc) {
+      void* p = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+          q == cudaDriverEntryPointSuccess)
+        enc = reinterpret_cast<XEncodeFn>(p);
+      if (!enc) return cudaErrorNotSupported;
+    }
+    // K/V of every slot as a [B*S][2d] bf16 matrix; box = one head's 64 dims x S positions
+    CUtensorMap tm;
+    cuuint64_t dims[2] = {(cuuint64_t)(2 * a.d), (cuuint64_t)max_rows * a.S};
+    cuuint64_t strides[1] = {(cuuint64_t)a.d * 4};
+    cuuint32_t box[2] = {64, (cuuint32_t)a.S};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)a.kv, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+    if (cudaError_t e = ensure_smem(k_attn_cross_tma, xattn::SMEM)) return e;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = max_rows < sms ? max_rows : sms;
+    return launch_k(k_attn_cross_tma, dim3(grid > 0 ? grid : 1), dim3(xattn::THREADS), xattn::SMEM, s, tm, a);
+  }
   const int warps = max_rows * a.heads;
   const int blocks = (warps * 32 + 255) / 256;
   return launch_k(k_attn_decoder, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, s, a);
