@@ -56,6 +56,9 @@ struct GemmPlan {
   int tshift;      // 1: stride-1 'same' conv whose whole samples tile BM: tap (r, s) of the A tile is
                    //    one TILED 4-d box {BKE, W, H, samples} at (c, s - pad, r - pad, n0) with zero
                    //    out-of-bounds fill -- same SMEM image as the im2col box, far fewer TMA requests
+  int g1;          // zero-copy entry: rows per A box (the largest power of two <= 64 dividing HW)
+  int g2;          // zero-copy entry: pixels per projection im2col box (largest power of two <= 16
+                   //    dividing Ho*Wo); a box never straddles two samples
 };
 
 __device__ __forceinline__ void tma_im2col_4d(uint32_t dst, const void* tmap, uint32_t bar, int c, int w, int h, int n,
@@ -235,13 +238,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                                     (uint16_t)s, (uint16_t)r);
                   }
                 } else if (!IM2COL && a.rows_gather) {
-                  // zero-copy entry: two 64-row boxes, each inside one input sample (HWo % 64 == 0)
-#pragma unroll
-                  for (int h = 0; h < 2; ++h) {
-                    const long long row = p0 + 64 * h;
+                  // zero-copy entry: BM / g1 boxes of g1 rows, each inside one input sample
+                  for (int h = 0; h < BM / pl.g1; ++h) {
+                    const long long row = p0 + pl.g1 * h;
                     const int idx = (int)(row / HWo);             // 1x1 / stride 1: HW == HWo
                     const int src = a.rows_gather[idx < n_live ? idx : (n_live > 0 ? n_live - 1 : 0)];
-                    ptx::tma_load_3d(da + (uint32_t)(h * 64 * BKE * 2), &tmAL, bar, cb * BKE,
+                    ptx::tma_load_3d(da + (uint32_t)(h * pl.g1 * BKE * 2), &tmAL, bar, cb * BKE,
                                      (int)(row - (long long)idx * HWo), src);
                   }
                 } else if (IM2COL && pl.tshift) {
@@ -269,14 +271,13 @@ __global__ void __launch_bounds__(THREADS, 1)
           ptx::mbar_arrive_expect_tx(bar, stage_tx);
           const uint32_t da = ptx::smem_u32(sA + stage * G::A_BYTES);
           if (a.x2_rows) {
-            // zero-copy entry: eight 16-pixel im2col boxes, each inside one sample (HWo % 16 == 0)
-#pragma unroll
-            for (int q = 0; q < BM / 16; ++q) {
-              const long long row = p0 + 16 * q;
+            // zero-copy entry: BM / g2 im2col boxes of g2 pixels, each inside one sample
+            for (int q = 0; q < BM / pl.g2; ++q) {
+              const long long row = p0 + pl.g2 * q;
               const int idx = (int)(row / HWo);
               const int pq = (int)(row - (long long)idx * HWo);
               const int src = a.x2_rows[idx < n_live ? idx : (n_live > 0 ? n_live - 1 : 0)];
-              tma_im2col_4d(da + (uint32_t)(q * 16 * BKE * 2), &tmA2, bar, cb * BKE, (pq % Wo) * stride2,
+              tma_im2col_4d(da + (uint32_t)(q * pl.g2 * BKE * 2), &tmA2, bar, cb * BKE, (pq % Wo) * stride2,
                             (pq / Wo) * stride2, src, 0, 0);
             }
           } else if (stride2 > 1)
@@ -719,11 +720,12 @@ cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t 
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
+  const int g1 = zero_copy_rows(a.H * a.W, 64), g2 = zero_copy_rows(a.Ho * a.Wo, 16);
   if (!IM2COL && a.rows_gather) {
-    if ((a.H * a.W) % 64) return cudaErrorInvalidValue;
+    if (g1 < ZC_MIN_ROWS) return cudaErrorInvalidValue;
     cuuint64_t dims[3] = {(cuuint64_t)a.C, (cuuint64_t)a.H * a.W, (cuuint64_t)rows};
     cuuint64_t strides[2] = {(cuuint64_t)a.C * 2, (cuuint64_t)a.H * a.W * a.C * 2};
-    cuuint32_t box[3] = {BKE, 64, 1};
+    cuuint32_t box[3] = {BKE, (cuuint32_t)g1, 1};
     cuuint32_t es[3] = {1, 1, 1};
     if (enc(&tmAL, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, (void*)a.x, dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -753,14 +755,14 @@ cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t 
   }
   CUtensorMap tmA2 = tmB;
   if (a.x2 && a.x2_rows) {
-    // 16-pixel strided im2col boxes of the projection operand (zero-copy entry)
-    if ((a.Ho * a.Wo) % 16) return cudaErrorInvalidValue;
+    // g2-pixel strided im2col boxes of the projection operand (zero-copy entry)
+    if (g2 < ZC_MIN_ROWS) return cudaErrorInvalidValue;
     cuuint64_t dims[4] = {(cuuint64_t)a.C2, (cuuint64_t)a.W2, (cuuint64_t)a.H2, (cuuint64_t)rows};
     cuuint64_t strides[3] = {(cuuint64_t)a.C2 * 2, (cuuint64_t)a.W2 * a.C2 * 2, (cuuint64_t)a.H2 * a.W2 * a.C2 * 2};
     int lower[2] = {0, 0};
     int upper[2] = {(a.Wo - 1) * a.stride2 - (a.W2 - 1), (a.Ho - 1) * a.stride2 - (a.H2 - 1)};
     cuuint32_t es[4] = {1, (cuuint32_t)a.stride2, (cuuint32_t)a.stride2, 1};
-    if (enc_i2c(&tmA2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)a.x2, dims, strides, lower, upper, BKE, 16, es,
+    if (enc_i2c(&tmA2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)a.x2, dims, strides, lower, upper, BKE, (cuuint32_t)g2, es,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
@@ -784,6 +786,8 @@ cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t 
   // (fp32 stream copy and / or a shortcut) and the ring keeps >= 2 stages beside the staging
   GemmPlan pl{};
   pl.tshift = tshift;
+  pl.g1 = g1;
+  pl.g2 = g2;
   if (RT && !tshift) return cudaErrorInvalidValue;
   const int kblocks = (RT ? a.ksz : a.ksz * a.ksz) * (a.C / BKE) + (a.x2 ? a.C2 / BKE : 0);
   const bool heavy = a.y32 != nullptr || a.res_mode == 1;

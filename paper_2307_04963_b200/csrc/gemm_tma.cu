@@ -172,8 +172,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int acc = it & 1;
       const int m_tile = tile / n_tiles, n_tile = tile - m_tile * n_tiles;
       const int m = m_tile * BM + r;
-      ptx::mbar_wait(tfull0 + 8 * acc, (it >> 1) & 1);
-      ptx::tc_fence_after();
+      const bool ln = BN == 64 && a.ln_gamma;           // waits for the accumulator itself
+      if (!ln) {
+        ptx::mbar_wait(tfull0 + 8 * acc, (it >> 1) & 1);
+        ptx::tc_fence_after();
+      }
       const uint32_t t_base = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN);
       if (a.am_val) {
         // fused argmax: (acc + bias) [+ guard bias on the EOS column], ascending scan, strict '>'
@@ -210,51 +213,68 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       } else if (BN == 64 && a.ln_gamma) {
         // residual + LayerNorm over the whole row (ConvArgs.ln_*): this CTA's 64 columns stay
-        // in registers; the row's mean and centred sum of squares are assembled from the
-        // N tiles' partials (ascending tile order) after two meetings on ln_cnt[m_tile]
+        // in registers; each N tile publishes its slice's (sum, centred sum of squares) per row
+        // and after ONE meeting every tile merges the d/64 slices in ascending order
+        // (Chan et al.: M2 = sum_i [M2_i + 64 (mean_i - mean)^2], as stable as two passes)
         const int col0 = n_tile * BN;
         float v[BN];
+#pragma unroll
+        for (int j = 0; j < BN; ++j) v[j] = 0.f;
+        if (m < M) {                                    // the residual, while the MMA runs
+          const float4* rp = reinterpret_cast<const float4*>(a.res32 + (size_t)m * a.Cout + col0);
+#pragma unroll
+          for (int j = 0; j < BN / 4; ++j) {
+            const float4 q = rp[j];                      // coherent load: y32 may alias res32
+            v[4 * j] = q.x; v[4 * j + 1] = q.y; v[4 * j + 2] = q.z; v[4 * j + 3] = q.w;
+          }
+        }
+        ptx::mbar_wait(tfull0 + 8 * acc, (it >> 1) & 1);
+        ptx::tc_fence_after();
 #pragma unroll
         for (int c0 = 0; c0 < BN; c0 += 16) {
           uint32_t u[16];
           ptx::tmem_ld_32x32b_x16(t_base + (uint32_t)c0, u);
           ptx::tmem_ld_wait();
 #pragma unroll
-          for (int q = 0; q < 16; ++q) v[c0 + q] = __uint_as_float(u[q]) + __ldg(a.bias + col0 + c0 + q);
+          for (int q = 0; q < 16; ++q)
+            v[c0 + q] = (__uint_as_float(u[q]) + __ldg(a.bias + col0 + c0 + q)) + v[c0 + q];
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive(tempty0 + 8 * acc);           // the accumulator is in registers now
-        if (m < M) {
-          const float4* rp = reinterpret_cast<const float4*>(a.res32 + (size_t)m * a.Cout + col0);
-#pragma unroll
-          for (int j = 0; j < BN / 4; ++j) {
-            const float4 q = rp[j];                      // coherent load: y32 may alias res32
-            v[4 * j] += q.x; v[4 * j + 1] += q.y; v[4 * j + 2] += q.z; v[4 * j + 3] += q.w;
-          }
-        }
-        float* part = a.ln_part + (size_t)(m < M ? m : 0) * 2 * n_tiles;
         float s1 = 0.f;
 #pragma unroll
         for (int q = 0; q < BN; ++q) s1 += v[q];
-        if (m < M) __stcg(part + n_tile, s1);
-        ln_meet(a.ln_cnt + m_tile, n_tiles, wg, r == 0);
-        float mu = 0.f;
-        for (int t = 0; t < n_tiles; ++t) mu += __ldcg(part + t);
-        mu /= (float)a.Cout;
-        float s2 = 0.f;
+        const float mi = s1 * (1.f / BN);
+        float m2 = 0.f;
 #pragma unroll
         for (int q = 0; q < BN; ++q) {
-          const float dd = v[q] - mu;
-          s2 += dd * dd;
+          const float dd = v[q] - mi;
+          m2 += dd * dd;
         }
-        if (m < M) __stcg(part + n_tiles + n_tile, s2);
-        ln_meet(a.ln_cnt + m_tile, 2 * n_tiles, wg, r == 0);
+        float2* part = reinterpret_cast<float2*>(a.ln_part) + (size_t)(m < M ? m : 0) * n_tiles;
+        if (m < M) __stcg(part + n_tile, make_float2(s1, m2));
+        ln_meet(a.ln_cnt + m_tile, n_tiles, wg, r == 0);
+        float2 pt[16];                                  // d <= 1024
+        float sum = 0.f;
+#pragma unroll
+        for (int t = 0; t < 16; ++t)
+          if (t < n_tiles) {
+            pt[t] = __ldcg(part + t);
+            sum += pt[t].x;
+          }
+        const float mu = sum / (float)a.Cout;
         float q2 = 0.f;
-        for (int t = 0; t < n_tiles; ++t) q2 += __ldcg(part + n_tiles + t);
+#pragma unroll
+        for (int t = 0; t < 16; ++t)
+          if (t < n_tiles) {
+            const float dm = pt[t].x * (1.f / BN) - mu;
+            q2 += pt[t].y + (float)BN * dm * dm;
+          }
         const float rstd = rsqrtf(q2 / (float)a.Cout + a.ln_eps);
-        // last meeting: every CTA of the M tile is past its reads; the last one re-arms the counter
+        // every CTA of the M tile is past its reads once all have counted in twice: the last
+        // one re-arms the counter
         named_bar(1 + wg);
-        if (r == 0 && atomicAdd(a.ln_cnt + m_tile, 1) == 3 * n_tiles - 1) atomicExch(a.ln_cnt + m_tile, 0);
+        if (r == 0 && atomicAdd(a.ln_cnt + m_tile, 1) == 2 * n_tiles - 1) atomicExch(a.ln_cnt + m_tile, 0);
         if (m < M) {
           float4* yq = reinterpret_cast<float4*>(a.y32 + (size_t)m * a.Cout + col0);
           uint4* yb = reinterpret_cast<uint4*>(a.y + (size_t)m * a.Cout + col0);

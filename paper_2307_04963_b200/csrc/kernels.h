@@ -43,9 +43,10 @@ struct ConvArgs {
   const int* rows_in = nullptr;
   const int* rows_out = nullptr;
   // conv_gemm only, zero-copy sub-network entry: the rows of the flat A operand
-  // (a 1x1 / stride-1 conv, HW % 64 == 0) belong to input samples rows_gather[m / HW] -- loaded
-  // as 64-row boxes at (pixel, sample) -- and the fused projection operand x2 (HWo % 16 == 0)
-  // to samples x2_rows[m / HWo], loaded as 16-pixel im2col boxes; the output stays dense
+  // (a 1x1 / stride-1 conv) belong to input samples rows_gather[m / HW] -- loaded as boxes of
+  // zero_copy_rows(HW, 64) rows at (pixel, sample) -- and the fused projection operand x2 to
+  // samples x2_rows[m / HWo], loaded as im2col boxes of zero_copy_rows(HWo, 16) pixels; the
+  // output stays dense
   const int* rows_gather = nullptr;
   const int* x2_rows = nullptr;
   // conv_gemm only (staged epilogue): fused GAP partials [M / gap_g][Cout] fp32 -- per group of
@@ -164,6 +165,14 @@ bool gemm_tma_ln_ok(const ConvArgs& a, int max_rows, int num_sms);
 
 // NHWC implicit-GEMM conv with TMA im2col operand loads (conv_gemm.cu): C % 64 == 0, Cout % 64 == 0.
 bool conv_gemm_eligible(const ConvArgs& a);
+// Zero-copy entry box height for samples of `hw` rows: the largest power of two <= cap that
+// divides hw (a box then never straddles two samples); usable when >= ZC_MIN_ROWS (56x56: 64,
+// 28x28: 16, 14x14: 4; 7x7: 1, not usable).
+constexpr int ZC_MIN_ROWS = 4;
+inline int zero_copy_rows(int hw, int cap) {
+  const int g = hw & -hw;
+  return g < cap ? g : cap;
+}
 cudaError_t launch_conv_gemm(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream);
 // Dispatch: path 0 = auto (TMA when possible), 1 = cp.async kernel, 2 = TMA only.
 cudaError_t launch_conv(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream, int path = 0);
