@@ -137,7 +137,7 @@ struct dycl_graph_s {
   int max_fuse = dycl::MAX_FUSED_BLOCKS;   // DYCL_MAX_FUSE: basic blocks per fused launch (1..8)
   int no_inplace = 0;                // DYCL_NO_INPLACE=1: gates gather / merge instead of running in place
   int no_zero_copy = 0;              // DYCL_NO_ZERO_COPY=1: exits gather survivors even before a fused block
-  int zc_min_hw = 0;                 // DYCL_ZC_MIN_HW=n: zero-copy GEMM entries only for samples of >= n rows (A/B)
+  int zc_proj_min = 8;               // smallest projection box (pixels) of a zero-copy GEMM entry (DYCL_ZC_PROJ_MIN)
   // CUDA graph of a whole run, captured on first use per (io pointers, batch) and replayed;
   // every kernel sizes itself from device counts, so the captured launch sequence is valid for
   // any data (DYCL_GRAPH=0 disables; profiling runs are issued launch by launch)
@@ -588,21 +588,24 @@ struct Exec {
   }
 
   // A sub-network the NHWC GEMM can enter zero-copy: [block, 1x1/s1 conv, ..., projection fused
-  // into the block's last conv] whose samples split into row-list boxes of >= ZC_MIN_ROWS rows
-  // (dycl::zero_copy_rows: 56x56 -> 64 / 16, 28x28 -> 16 / 4; not 14x14 -> 7x7) -- the block
+  // into the block's last conv] whose samples split into row-list boxes (dycl::zero_copy_rows:
+  // 56x56 -> 64-row A / 16-pixel projection boxes; 28x28 -> 16 / 4, 14x14 -> 4 / 1) -- the block
   // input is read only by the first conv and by the projection, both through the row list.
+  // Projection boxes below zc_proj_min pixels (default 8) are not used: at 28x28 the 4-pixel
+  // boxes (32 TMA requests per k-block) slow the stage's first conv3 + projection GEMM by more
+  // than the gather they save (cfg 5: 931 -> 944 ms per step; DYCL_ZC_PROJ_MIN=4 enables them).
   bool gemm_list_entry(const Subnet& S) const {
     if (S.layers.size() < 5 || S.layers[0].kind != L_BLOCK) return false;
     const Layer& c1 = S.layers[1];
     if (c1.kind != L_CONV || c1.k != 1 || c1.stride != 1 || c1.residual || c1.s4d || c1.s2d2 || !lay(c1.in.Cp()) ||
         !lay(c1.out.C) || dycl::zero_copy_rows(c1.in.H * c1.in.W, 64) < dycl::ZC_MIN_ROWS || c1.in.Cp() % 64 ||
-        c1.out.C % 64 || (g->zc_min_hw && c1.in.H * c1.in.W < g->zc_min_hw))
+        c1.out.C % 64)
       return false;
     for (size_t li = 2; li < S.layers.size() && S.layers[li].kind != L_BLOCK; ++li) {
       const Layer& L = S.layers[li];
       if (L.kind == L_PROJ)
         return li + 1 < S.layers.size() && S.layers[li + 1].fuse_proj &&
-               dycl::zero_copy_rows(S.layers[li + 1].out.H * S.layers[li + 1].out.W, 16) >= dycl::ZC_MIN_ROWS;
+               dycl::zero_copy_rows(S.layers[li + 1].out.H * S.layers[li + 1].out.W, 16) >= g->zc_proj_min;
       if (L.residual) return false;
     }
     return false;
@@ -1381,7 +1384,7 @@ dycl_status dycl_graph_create(int cuda_device, int in_h, int in_w, int in_c, dyc
   if (const char* mf = getenv("DYCL_MAX_FUSE")) g->max_fuse = atoi(mf);
   if (const char* ni = getenv("DYCL_NO_INPLACE")) g->no_inplace = atoi(ni);
   if (const char* nz = getenv("DYCL_NO_ZERO_COPY")) g->no_zero_copy = atoi(nz);
-  if (const char* zm = getenv("DYCL_ZC_MIN_HW")) g->zc_min_hw = atoi(zm);
+  if (const char* zm = getenv("DYCL_ZC_PROJ_MIN")) g->zc_proj_min = std::max(dycl::ZC_MIN_ROWS, atoi(zm));
   if (const char* ug = getenv("DYCL_GRAPH")) g->use_graph = atoi(ug) != 0;
   if (getenv("DYCL_TS")) {
     cudaMalloc(&g->dbg_ts, 8 * 16 * sizeof(long long));

@@ -86,7 +86,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 9) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), 512);
+  // two BN-column fp32 accumulators: allocate only those (a PDL-launched successor on this SM
+  // can then take its own columns while this CTA still runs, instead of spinning in its prologue)
+  constexpr uint32_t TCOLS = 2 * BN < 32 ? 32 : 2 * BN;
+  if (warp == 9) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), TCOLS);
   if (warp == 8 && lane == 0) {
     ptx::tma_prefetch_desc(&tmA);
     ptx::tma_prefetch_desc(&tmB);
@@ -314,7 +317,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   if (warp == 9) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, 512);
+    ptx::tmem_dealloc(tmem_base, TCOLS);
   }
 }
 

@@ -516,23 +516,27 @@ __global__ void __launch_bounds__(256, 5) k_attn_decoder(const S2SAttnArgs a) {
   *out = (uint32_t)to_bf(o0) | ((uint32_t)to_bf(o1) << 16);
 }
 
-// Cross attention with the encoder K/V streamed by TMA. The per-warp form above
-// issues its K/V reads from the same warp that consumes them (scores, then softmax, then the
-// V sweep) and leaves its last wave a third full: ~3 TB/s on the 134 MB one decoder layer
-// reads. Here one persistent CTA per SM walks the active rows; a producer lane streams each
-// row's K block and then its V block (heads x S x 128 B each, one 128-byte-swizzled
-// {64, S} box per head) into a 3-stage ring, so two blocks are in flight while the head warps
-// (warp h = head h) consume a third from SMEM. Same arithmetic, same order as k_attn_decoder:
-// scores over dims in pairs ascending, * 1/8, softmax in fp32 with expf, P.V over keys ascending.
+// Decoder attention with the K/V streamed by TMA. The per-warp form above issues
+// its K/V reads from the same warp that consumes them (scores, then softmax, then the V sweep)
+// and leaves its last wave a third full: ~3 TB/s on the 134 MB one cross-attention layer reads.
+// Here one persistent CTA per SM walks the active rows; a producer lane streams each row's K
+// block and then its V block (heads x R x 128 B each, one 128-byte-swizzled {64, R} box per
+// head) into a 3-stage ring, so two blocks are in flight while the head warps (warp h = head h)
+// consume a third from SMEM. Same arithmetic, same order as k_attn_decoder: scores over dims in
+// pairs ascending, * 1/8, softmax in fp32 with expf, P.V over keys ascending.
+//   cross (a.kv):  R = S encoder positions of the slot's K/V ([B*S][2d]), nk = S;
+//   self (a.cache): R = round_up(t + 1, 8) positions of the slot's cache ([B*max_len][2d]),
+//                  nk = t + 1; position t is this step's k, v (from qkv): each head warp appends
+//                  it to the cache and writes it over the (stale) row t of its SMEM blocks.
 namespace xattn {
 constexpr int NST = 3;
-constexpr int STAGE = 64 * 1024;           // heads * S * 128 B <= 8 * 64 * 128
+constexpr int STAGE = 64 * 1024;           // heads * R * 128 B <= 8 * 64 * 128
 constexpr int THREADS = 288;               // warps 0-7 heads, warp 8 producer
 constexpr int SMEM = 1024 + NST * STAGE + 64;
 }  // namespace xattn
 
 __global__ void __launch_bounds__(xattn::THREADS, 1)
-    k_attn_cross_tma(const __grid_constant__ CUtensorMap tmKV, const S2SAttnArgs a) {
+    k_attn_tma(const __grid_constant__ CUtensorMap tmKV, const S2SAttnArgs a, const int R) {
   using namespace xattn;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -551,8 +555,11 @@ __global__ void __launch_bounds__(xattn::THREADS, 1)
   ptx::pdl_wait();      // PDL (kernels.h): the live count, slots and queries come from predecessors
   ptx::pdl_trigger();
   const int n = a.n_live ? *a.n_live : a.n_static;
-  const int d = a.d, S = a.S;
-  const uint32_t hbytes = (uint32_t)S * 128;          // one head's {64, S} box
+  const int d = a.d;
+  const bool self = a.kv == nullptr;
+  const int nk = self ? a.t + 1 : a.S;                 // keys attended
+  const int rps = self ? a.max_len : a.S;              // K/V rows per slot
+  const uint32_t hbytes = (uint32_t)R * 128;           // one head's {64, R} box
   if (warp == 8) {
     if (lane == 0) {
       int st = 0;
@@ -564,7 +571,7 @@ __global__ void __launch_bounds__(xattn::THREADS, 1)
           const uint32_t bar = full0 + 8 * st;
           ptx::mbar_arrive_expect_tx(bar, hbytes * (uint32_t)a.heads);
           for (int h = 0; h < a.heads; ++h)
-            ptx::tma_load_2d(ptx::smem_u32(smem + st * STAGE + h * hbytes), &tmKV, bar, kvh * d + h * 64, slot * S);
+            ptx::tma_load_2d(ptx::smem_u32(smem + st * STAGE + h * hbytes), &tmKV, bar, kvh * d + h * 64, slot * rps);
           if (++st == NST) {
             st = 0;
             ph ^= 1;
@@ -578,6 +585,7 @@ __global__ void __launch_bounds__(xattn::THREADS, 1)
   const int h = warp;
   int st = 0;
   uint32_t ph = 0;
+  const int tsw = (a.t & 7) << 4;                      // self: swizzle of SMEM row t
   for (int row = blockIdx.x; row < n; row += gridDim.x) {
     // the head's 64-dim query, fp32, in registers (every lane holds all of it: broadcast loads)
     float qv[64];
@@ -594,13 +602,26 @@ __global__ void __launch_bounds__(xattn::THREADS, 1)
         }
       }
     }
+    uint32_t kt = 0, vt = 0;                           // self: this lane's 2 dims of k_t, v_t
+    if (self) {
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(a.qkv + (size_t)row * 3 * d);
+      kt = src[(d + h * 64) / 2 + lane];
+      vt = src[(2 * d + h * 64) / 2 + lane];
+      uint32_t* dst = reinterpret_cast<uint32_t*>(a.cache + ((size_t)a.slot[row] * a.max_len + a.t) * 2 * d);
+      dst[(h * 64) / 2 + lane] = kt;                   // append for the later steps
+      dst[(d + h * 64) / 2 + lane] = vt;
+    }
     ptx::mbar_wait(full0 + 8 * st, ph);
-    const uint8_t* kb = smem + st * STAGE + h * hbytes;
+    uint8_t* kb = smem + st * STAGE + h * hbytes;
+    if (self) {
+      *reinterpret_cast<uint32_t*>(kb + a.t * 128 + ((((lane >> 2) << 4) ^ tsw)) + ((lane & 3) << 2)) = kt;
+      __syncwarp();
+    }
     float s0 = -INFINITY, s1 = -INFINITY;
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
       const int j = lane + 32 * half;
-      const bool valid = j < S;
+      const bool valid = j < nk;
       const uint8_t* kr = kb + (valid ? j : 0) * 128;
       const int sw = (valid ? j : 0) & 7;
       float acc = 0.f;
@@ -618,6 +639,7 @@ __global__ void __launch_bounds__(xattn::THREADS, 1)
         else s1 = acc * 0.125f;
       }
     }
+    if (self) ptx::fence_proxy_async_smem();          // our row-t store before the ring's next TMA write
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(empty0 + 8 * st);
     if (++st == NST) {
@@ -625,18 +647,24 @@ __global__ void __launch_bounds__(xattn::THREADS, 1)
       ph ^= 1;
     }
     const float m = warp_max(fmaxf(s0, s1));
-    const float e0 = lane < S ? expf(s0 - m) : 0.f, e1 = lane + 32 < S ? expf(s1 - m) : 0.f;
+    const float e0 = lane < nk ? expf(s0 - m) : 0.f, e1 = lane + 32 < nk ? expf(s1 - m) : 0.f;
     const float inv = 1.f / warp_sum(e0 + e1);
     ptx::mbar_wait(full0 + 8 * st, ph);
-    const uint8_t* vb = smem + st * STAGE + h * hbytes + ((lane & 3) << 2);
+    uint8_t* vb0 = smem + st * STAGE + h * hbytes;
+    if (self) {
+      *reinterpret_cast<uint32_t*>(vb0 + a.t * 128 + ((((lane >> 2) << 4) ^ tsw)) + ((lane & 3) << 2)) = vt;
+      __syncwarp();
+    }
+    const uint8_t* vb = vb0 + ((lane & 3) << 2);
     float o0 = 0.f, o1 = 0.f;
 #pragma unroll 8
-    for (int j = 0; j < S; ++j) {
+    for (int j = 0; j < nk; ++j) {
       const float pj = __shfl_sync(0xffffffffu, j < 32 ? e0 : e1, j & 31) * inv;
       const uint32_t vv = *reinterpret_cast<const uint32_t*>(vb + j * 128 + (((lane >> 2) ^ (j & 7)) << 4));
       o0 += pj * __uint_as_float(vv << 16);
       o1 += pj * __uint_as_float(vv & 0xFFFF0000u);
     }
+    if (self) ptx::fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(empty0 + 8 * st);
     if (++st == NST) {
@@ -799,7 +827,7 @@ cudaError_t launch_attn_encoder(const S2SAttnArgs& a, int max_seqs, cudaStream_t
 cudaError_t launch_attn_decoder(const S2SAttnArgs& a, int max_rows, cudaStream_t s) {
   if (a.S > 64 || a.max_len > 64 || a.d / a.heads != 64) return cudaErrorInvalidValue;
   static const bool warp_form = getenv("DYCL_XATTN_WARP") != nullptr;   // A/B timing of the per-warp form
-  if (a.kv && !a.pair && a.heads <= 8 && a.S % 8 == 0 && a.d == 64 * a.heads && !warp_form) {
+  if (!a.pair && a.heads <= 8 && a.d == 64 * a.heads && !warp_form && (a.kv ? a.S % 8 == 0 : a.max_len % 8 == 0)) {
     static XEncodeFn enc = nullptr;
     if (!enc) {
       void* p = nullptr;
@@ -809,22 +837,25 @@ cudaError_t launch_attn_decoder(const S2SAttnArgs& a, int max_rows, cudaStream_t
         enc = reinterpret_cast<XEncodeFn>(p);
       if (!enc) return cudaErrorNotSupported;
     }
-    // K/V of every slot as a [B*S][2d] bf16 matrix; box = one head's 64 dims x S positions
+    // K/V of every slot as a [B * rows per slot][2d] bf16 matrix; box = one head's 64 dims x R
+    // positions (cross: the S encoder positions; self: positions 0..t rounded up to 8)
+    const int rps = a.kv ? a.S : a.max_len;
+    const int R = a.kv ? a.S : (a.t + 1 + 7) / 8 * 8;
     CUtensorMap tm;
-    cuuint64_t dims[2] = {(cuuint64_t)(2 * a.d), (cuuint64_t)max_rows * a.S};
+    cuuint64_t dims[2] = {(cuuint64_t)(2 * a.d), (cuuint64_t)max_rows * rps};
     cuuint64_t strides[1] = {(cuuint64_t)a.d * 4};
-    cuuint32_t box[2] = {64, (cuuint32_t)a.S};
+    cuuint32_t box[2] = {64, (cuuint32_t)R};
     cuuint32_t es[2] = {1, 1};
-    if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)a.kv, dims, strides, box, es,
+    if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)(a.kv ? a.kv : a.cache), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
-    if (cudaError_t e = ensure_smem(k_attn_cross_tma, xattn::SMEM)) return e;
+    if (cudaError_t e = ensure_smem(k_attn_tma, xattn::SMEM)) return e;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int grid = max_rows < sms ? max_rows : sms;
-    return launch_k(k_attn_cross_tma, dim3(grid > 0 ? grid : 1), dim3(xattn::THREADS), xattn::SMEM, s, tm, a);
+    return launch_k(k_attn_tma, dim3(grid > 0 ? grid : 1), dim3(xattn::THREADS), xattn::SMEM, s, tm, a, R);
   }
   const int warps = max_rows * a.heads;
   const int blocks = (warps * 32 + 255) / 256;

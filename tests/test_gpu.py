@@ -470,16 +470,17 @@ def test_cfg5_bench_chunk_sampled_parity():
 
 
 def test_cfg5_zero_copy_stage_entries_equal_gather():
-    """cfg5 exits hand their survivors to the next stage by row list (56x56 and 28x28 stage
-    entries: 64/16-row A boxes, 16/4-pixel projection boxes): bitwise the same
-    logits and paths as gathering them, and fewer launches."""
+    """cfg5 exits hand their survivors to the next stage by row list (default: the
+    56x56 stage entry, 64-row A / 16-pixel projection boxes; DYCL_ZC_PROJ_MIN=4 adds the 28x28
+    entry, 16-row A / 4-pixel projection boxes): bitwise the same logits and paths as gathering
+    them, and fewer launches."""
     import os
     from paper_2307_04963_b200 import dycl as D
     W = wl.resnet50_ee_weights()
     B = 384
     x = wl.image_inputs_torch(wl.INPUT_SEED, 20000, B, hw=224, device="cuda")
     outs, launches = [], []
-    for env in ({}, {"DYCL_ZC_MIN_HW": "1000"}, {"DYCL_NO_ZERO_COPY": "1"}):
+    for env in ({"DYCL_ZC_PROJ_MIN": "4"}, {}, {"DYCL_NO_ZERO_COPY": "1"}):
         os.environ.update(env)
         try:
             m = P.build_resnet50_ee(W, B)
@@ -493,7 +494,7 @@ def test_cfg5_zero_copy_stage_entries_equal_gather():
         outs.append((logits.cpu().numpy(), path.cpu().numpy()))
         launches.append(D.dycl_launches_per_run(m.g))
         m.close()
-    print("cfg5 paths", np.bincount(outs[0][1], minlength=4).tolist(), "launches (all / 56x56 only / none)", launches)
+    print("cfg5 paths", np.bincount(outs[0][1], minlength=4).tolist(), "launches (56x56 + 28x28 / 56x56 / none)", launches)
     assert all((outs[0][1] == k).sum() > 0 for k in range(4))
     for lg, pg in outs[1:]:
         assert np.array_equal(pg, outs[0][1]) and np.array_equal(lg, outs[0][0])
