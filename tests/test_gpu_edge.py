@@ -72,6 +72,24 @@ def test_cfg2_degenerate_tau(tau, expect):
         assert cnt[2] == 0, cnt[:12]
 
 
+def test_cfg2_traced_program_differs_from_dynamic():
+    """The trace baseline on the GPU path (Table 2): the program with every
+    exit predicate frozen to "stay" (tau > 1, a trace of an input that ran to the final head)
+    reproduces the dynamic run BITWISE for the inputs that take the final head in it -- the
+    kernels are batch-position independent, so the compaction in between changes nothing --
+    and differs for every input that exits early (eta > 0)."""
+    from oracle.metrics import eta
+    W = wl.sdn_r56_weights()
+    X = wl.image_inputs(wl.INPUT_SEED, 4000, 256)
+    ld, pd, _ = _run(P.build_sdn_resnet56(W, 256), X)
+    lt, pt, _ = _run(P.build_sdn_resnet56(W, 256, tau=1.5), X)
+    assert (pt == 4).all() and (pd < 4).any() and (pd == 4).any(), np.bincount(pd)
+    fin = pd == 4
+    assert np.array_equal(lt[fin], ld[fin])
+    assert np.all(np.max(np.abs(lt[~fin] - ld[~fin]), axis=1) > 0)
+    assert eta(list(np.argmax(lt, 1)), list(np.argmax(ld, 1))) > 0.0
+
+
 @pytest.mark.parametrize("tau,expect", [(1.5, 3), (0.1, 0)])
 def test_cfg5_degenerate_tau(tau, expect):
     W = wl.resnet50_ee_weights()
