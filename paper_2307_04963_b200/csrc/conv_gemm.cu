@@ -239,12 +239,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                   }
                 } else if (!IM2COL && a.rows_gather) {
                   // zero-copy entry: BM / g1 boxes of g1 rows, each inside one input sample
+                  // (1x1 / stride 1: HW == HWo; sample and pixel advanced incrementally, no divisions)
+                  int idx = n0, prow = rem;
                   for (int h = 0; h < BM / pl.g1; ++h) {
-                    const long long row = p0 + pl.g1 * h;
-                    const int idx = (int)(row / HWo);             // 1x1 / stride 1: HW == HWo
                     const int src = a.rows_gather[idx < n_live ? idx : (n_live > 0 ? n_live - 1 : 0)];
-                    ptx::tma_load_3d(da + (uint32_t)(h * pl.g1 * BKE * 2), &tmAL, bar, cb * BKE,
-                                     (int)(row - (long long)idx * HWo), src);
+                    ptx::tma_load_3d(da + (uint32_t)(h * pl.g1 * BKE * 2), &tmAL, bar, cb * BKE, prow, src);
+                    prow += pl.g1;
+                    if (prow >= HWo) {
+                      prow -= HWo;
+                      ++idx;
+                    }
                   }
                 } else if (IM2COL && pl.tshift) {
                   ptx::tma_load_4d(da, &tmA, bar, cb * BKE, s - pad, r - pad, n0);
@@ -271,14 +275,21 @@ __global__ void __launch_bounds__(THREADS, 1)
           ptx::mbar_arrive_expect_tx(bar, stage_tx);
           const uint32_t da = ptx::smem_u32(sA + stage * G::A_BYTES);
           if (a.x2_rows) {
-            // zero-copy entry: BM / g2 im2col boxes of g2 pixels, each inside one sample
+            // zero-copy entry: BM / g2 im2col boxes of g2 pixels, each inside one sample; the
+            // (sample, output row, output column) of each box advanced incrementally, no divisions
+            int idx = n0, ho = ho0, wo = wo0;
             for (int q = 0; q < BM / pl.g2; ++q) {
-              const long long row = p0 + pl.g2 * q;
-              const int idx = (int)(row / HWo);
-              const int pq = (int)(row - (long long)idx * HWo);
               const int src = a.x2_rows[idx < n_live ? idx : (n_live > 0 ? n_live - 1 : 0)];
-              tma_im2col_4d(da + (uint32_t)(q * pl.g2 * BKE * 2), &tmA2, bar, cb * BKE, (pq % Wo) * stride2,
-                            (pq / Wo) * stride2, src, 0, 0);
+              tma_im2col_4d(da + (uint32_t)(q * pl.g2 * BKE * 2), &tmA2, bar, cb * BKE, wo * stride2, ho * stride2,
+                            src, 0, 0);
+              wo += pl.g2;
+              while (wo >= Wo) {
+                wo -= Wo;
+                if (++ho == a.Ho) {
+                  ho = 0;
+                  ++idx;
+                }
+              }
             }
           } else if (stride2 > 1)
             tma_im2col_4d(da, &tmA2, bar, cb * BKE, wo0 * stride2, ho0 * stride2, n0, 0, 0);
@@ -455,8 +466,19 @@ __global__ void __launch_bounds__(THREADS, 1)
           ptx::tmem_ld_wait();
         }
         float f[32];
+        {
+          // bias as 8 broadcast 16-byte loads (col0 + c0 is a multiple of 32): the scalar form was
+          // 32 loads per chunk, a fifth of the epilogue's instructions on the K = 64 convs
+          const float4* b4 = reinterpret_cast<const float4*>(a.bias + col0 + c0);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]) + __ldg(a.bias + col0 + c0 + j);
+          for (int j = 0; j < 8; ++j) {
+            const float4 q = __ldg(b4 + j);
+            f[4 * j] = __uint_as_float(v[4 * j]) + q.x;
+            f[4 * j + 1] = __uint_as_float(v[4 * j + 1]) + q.y;
+            f[4 * j + 2] = __uint_as_float(v[4 * j + 2]) + q.z;
+            f[4 * j + 3] = __uint_as_float(v[4 * j + 3]) + q.w;
+          }
+        }
         if (staged && res) {
           ptx::mbar_wait(rbar, rphase);
           rphase ^= 1;

@@ -33,8 +33,13 @@ __device__ __forceinline__ void conv_finish16(const ConvArgs& a, int n, int ho, 
       f[j] += q.x; f[j + 1] += q.y; f[j + 2] += q.z; f[j + 3] += q.w;
     }
   } else {
+    // four broadcast 16-byte loads (o0 is a multiple of 16) instead of sixteen scalar ones
+    const float4* b4 = reinterpret_cast<const float4*>(a.bias + o0);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) f[j] += __ldg(a.bias + o0 + j);
+    for (int j = 0; j < 4; ++j) {
+      const float4 q = __ldg(b4 + j);
+      f[4 * j] += q.x; f[4 * j + 1] += q.y; f[4 * j + 2] += q.z; f[4 * j + 3] += q.w;
+    }
   }
   if (a.res_mode == 1 && res_s) {
 #pragma unroll

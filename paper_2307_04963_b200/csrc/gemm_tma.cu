@@ -239,8 +239,13 @@ __global__ void __launch_bounds__(THREADS, 1)
           ptx::tmem_ld_32x32b_x16(t_base + (uint32_t)c0, u);
           ptx::tmem_ld_wait();
 #pragma unroll
-          for (int q = 0; q < 16; ++q)
-            v[c0 + q] = (__uint_as_float(u[q]) + __ldg(a.bias + col0 + c0 + q)) + v[c0 + q];
+          for (int q = 0; q < 16; q += 4) {
+            const float4 b4 = __ldg(reinterpret_cast<const float4*>(a.bias + col0 + c0 + q));
+            v[c0 + q] = (__uint_as_float(u[q]) + b4.x) + v[c0 + q];
+            v[c0 + q + 1] = (__uint_as_float(u[q + 1]) + b4.y) + v[c0 + q + 1];
+            v[c0 + q + 2] = (__uint_as_float(u[q + 2]) + b4.z) + v[c0 + q + 2];
+            v[c0 + q + 3] = (__uint_as_float(u[q + 3]) + b4.w) + v[c0 + q + 3];
+          }
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive(tempty0 + 8 * acc);           // the accumulator is in registers now
