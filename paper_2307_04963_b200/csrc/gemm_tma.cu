@@ -200,14 +200,26 @@ __global__ void __launch_bounds__(THREADS, 1)
             const float4 b4 = __ldg(reinterpret_cast<const float4*>(a.bias + col0 + q));
             bq[q] = b4.x; bq[q + 1] = b4.y; bq[q + 2] = b4.z; bq[q + 3] = b4.w;
           }
+          float z[16];
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            float z = __uint_as_float(v[q]) + bq[q];
-            if (col0 + q == a.g_eos) z += gb;
-            if (z > best) {
-              best = z;
-              bi = col0 + q;
-            }
+          for (int q = 0; q < 16; ++q) z[q] = __uint_as_float(v[q]) + bq[q];
+          if (a.g_eos >= col0 && a.g_eos < col0 + 16) {   // uniform: the EOS column's chunk
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              if (col0 + q == a.g_eos) z[q] += gb;
+          }
+          // the chunk's maximum first (15 max ops), its lowest index only when it beats the
+          // running best: the same (max, lowest index) as the element-wise strict-'>' scan
+          float cm = z[0];
+#pragma unroll
+          for (int q = 1; q < 16; ++q) cm = fmaxf(cm, z[q]);
+          if (cm > best) {
+            int qi = 15;
+#pragma unroll
+            for (int q = 15; q >= 0; --q)
+              if (z[q] == cm) qi = q;
+            best = cm;
+            bi = col0 + qi;
           }
         }
         if (m < M) {

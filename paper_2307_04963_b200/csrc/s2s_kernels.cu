@@ -210,22 +210,26 @@ __device__ __forceinline__ uint32_t sw128(int r, int c) {
 }
 }  // namespace enc_tc
 
-__global__ void __launch_bounds__(enc_tc::THREADS) k_attn_encoder_tc(const S2SAttnArgs a) {
+__global__ void __launch_bounds__(enc_tc::THREADS)
+    k_attn_encoder_tc(const __grid_constant__ CUtensorMap tmQK, const S2SAttnArgs a) {
   using namespace enc_tc;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + 81920);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3);
   const int t = threadIdx.x, warp = t >> 5;
   const int npair = a.heads >> 1;
   const int b = blockIdx.x / npair, h0 = 2 * (blockIdx.x % npair);
-  const uint32_t bar0 = ptx::smem_u32(bars), bar1 = bar0 + 8;
+  const uint32_t bar0 = ptx::smem_u32(bars), bar1 = bar0 + 8, barq = bar0 + 16;
   if (t == 0) {
     ptx::mbar_init(bar0, 1);
     ptx::mbar_init(bar1, 1);
+    ptx::mbar_init(barq, 1);
     ptx::fence_mbar_init();
+    ptx::tma_prefetch_desc(&tmQK);
   }
   if (warp == 0) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), 256);
+  __syncthreads();
   ptx::pdl_wait();      // PDL (kernels.h): before any read of predecessor output / early return
   ptx::pdl_trigger();
   const int n_seq = a.n_live ? *a.n_live : a.n_static;
@@ -233,15 +237,20 @@ __global__ void __launch_bounds__(enc_tc::THREADS) k_attn_encoder_tc(const S2SAt
   const int S = a.S, d = a.d;
   const int rs = 3 * d;
   const uint16_t* base = a.qkv + (size_t)b * S * rs;
+  if (live && t == 0) {
+    // Q and K by TMA: row r = (head r / 64, token r % 64), one {64 dims, 64 tokens} 128-byte-
+    // swizzled box per head -- the K-major SW128 image the MMA reads (sw128 below). Tokens past
+    // S belong to the next sequence (or are zero past the batch): their score rows are never
+    // stored, their score columns are masked in the softmax.
+    ptx::mbar_arrive_expect_tx(barq, 4 * 8192);
+#pragma unroll
+    for (int w = 0; w < 2; ++w)
+#pragma unroll
+      for (int hb = 0; hb < 2; ++hb)
+        ptx::tma_load_2d(ptx::smem_u32(sm + (w ? K_OFF : Q_OFF) + hb * 8192), &tmQK, barq, w * d + (h0 + hb) * 64,
+                         b * S);
+  }
   if (live) {
-    // Q and K: row r = (head r / 64, token r % 64); 8 chunks of 16 B per row
-    for (int i = t; i < 2 * 128 * 8; i += THREADS) {
-      const int which = i >> 10, r = (i >> 3) & 127, c = i & 7;
-      const int hh = h0 + (r >> 6), tok = r & 63;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (tok < S) v = __ldg(reinterpret_cast<const uint4*>(base + (size_t)tok * rs + which * d + hh * 64 + c * 8));
-      *reinterpret_cast<uint4*>(sm + (which ? K_OFF : Q_OFF) + sw128(r, c)) = v;
-    }
     // V^T: B operand [dim n][key k], key block kb = head (keys 0..63 of head h0, then h1).
     // Thread: key pair (2p, 2p+1) of one head, 32 of the 64 dims; one 32-bit store per dim.
     for (int i = t; i < 2 * 32 * 2; i += THREADS) {
@@ -268,6 +277,7 @@ __global__ void __launch_bounds__(enc_tc::THREADS) k_attn_encoder_tc(const S2SAt
     }
   }
   ptx::fence_proxy_async_smem();       // generic-proxy SMEM writes -> visible to the tensor core
+  if (live) ptx::mbar_wait(barq, 0);   // Q, K landed
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -819,8 +829,27 @@ cudaError_t launch_attn_encoder(const S2SAttnArgs& a, int max_seqs, cudaStream_t
   static const bool cuda_core = getenv("DYCL_ENC_ATTN_CC") != nullptr;   // A/B timing of the old kernel
   if (!a.pair && a.heads % 2 == 0 && !cuda_core) {
     if (cudaError_t e = ensure_smem(k_attn_encoder_tc, enc_tc::SMEM)) return e;
+    static XEncodeFn enc = nullptr;
+    if (!enc) {
+      void* p = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+          q == cudaDriverEntryPointSuccess)
+        enc = reinterpret_cast<XEncodeFn>(p);
+      if (!enc) return cudaErrorNotSupported;
+    }
+    // qkv as a [B*S][3d] bf16 matrix; box = one head's 64 dims x 64 tokens
+    CUtensorMap tm;
+    cuuint64_t dims[2] = {(cuuint64_t)(3 * a.d), (cuuint64_t)max_seqs * a.S};
+    cuuint64_t strides[1] = {(cuuint64_t)a.d * 6};
+    cuuint32_t box[2] = {64, 64};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)a.qkv, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
     const int grid = max_seqs * (a.heads / 2);
-    return launch_k(k_attn_encoder_tc, dim3(grid > 0 ? grid : 1), dim3(enc_tc::THREADS), enc_tc::SMEM, s, a);
+    return launch_k(k_attn_encoder_tc, dim3(grid > 0 ? grid : 1), dim3(enc_tc::THREADS), enc_tc::SMEM, s, tm, a);
   }
   return launch_k(k_attn_encoder, dim3(max_seqs * a.heads > 0 ? max_seqs * a.heads : 1), dim3(128), 0, s, a);
 }
