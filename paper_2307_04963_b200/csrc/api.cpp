@@ -2229,6 +2229,9 @@ dycl_status dycl_set_rebalance_mode(dycl_graph g, int mode) {
     return fail(g, DYCL_E_UNSUPPORTED, "device rebalancing: at most 8 ranks (one NVLink domain)");
   CK(cudaSetDevice(g->device));
   g->rb_device = mode == DYCL_REBALANCE_MODE_DEVICE;
+  // every kernel loaded before the first exchange: a lazy load during a run could wait for a
+  // context that one of this process's spinning exchange kernels keeps busy (kernels.h)
+  if (g->rb_device) CK(dycl::preload_kernels());
   if (g->rb_device && !g->d_drb_plan) {
     dycl_status s;
     if ((s = dmalloc(g, &g->d_drb_plan, dycl::DRB_MAX_LEVELS * sizeof(dycl::DrbPlan))) ||
@@ -2282,6 +2285,8 @@ dycl_status dycl_set_comm_local(dycl_graph g, dycl_local_group grp, int rank, in
   // on an SM while the others compute, so compute grids leave `world` SMs free (a persistent
   // grid of one CTA per SM could otherwise never start its last CTA behind a spinner)
   if (world > 1 && g->num_sms > world) g->num_sms -= world;
+  CK(cudaSetDevice(g->device));
+  CK(dycl::preload_kernels());                 // ranks of one process share one context (kernels.h)
   return set_transport(g, dycl::make_local_transport(grp->g, rank), rebalance_policy);
 }
 

@@ -647,4 +647,8 @@ cudaError_t launch_block_fused(const BlockArgs& a, int max_rows, int num_sms, cu
   return cudaErrorNotSupported;
 }
 
+// Lazy-loading anchor: a kernel of this translation unit's module (preload_kernels, hostmod.cu).
+__global__ void k_tu_anchor_block_fused() {}
+const void* tu_anchor_block_fused() { return reinterpret_cast<const void*>(&k_tu_anchor_block_fused); }
+
 }  // namespace dycl

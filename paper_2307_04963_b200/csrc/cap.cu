@@ -170,6 +170,10 @@ int blocks_for(long long work, int threads, int num_sms) {
 }
 
 }  // namespace
+// Lazy-loading anchor: a kernel of this translation unit's module (preload_kernels, hostmod.cu).
+__global__ void k_tu_anchor_cap() {}
+const void* tu_anchor_cap() { return reinterpret_cast<const void*>(&k_tu_anchor_cap); }
+
 }  // namespace dycl
 
 struct dycl_cap_s {

@@ -902,4 +902,8 @@ cudaError_t launch_conv_gemm(const ConvArgs& a, int max_rows, int num_sms, cudaS
   return launch_bn<64>(a, max_rows, num_sms, stream);
 }
 
+// Lazy-loading anchor: a kernel of this translation unit's module (preload_kernels, hostmod.cu).
+__global__ void k_tu_anchor_conv_gemm() {}
+const void* tu_anchor_conv_gemm() { return reinterpret_cast<const void*>(&k_tu_anchor_conv_gemm); }
+
 }  // namespace dycl

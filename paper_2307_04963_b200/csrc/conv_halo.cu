@@ -354,4 +354,8 @@ cudaError_t launch_conv_halo(const ConvArgs& a, int max_rows, int num_sms, cudaS
   return launch_ch<64, 128, 3>(a, hp, max_rows, num_sms, stream);
 }
 
+// Lazy-loading anchor: a kernel of this translation unit's module (preload_kernels, hostmod.cu).
+__global__ void k_tu_anchor_conv_halo() {}
+const void* tu_anchor_conv_halo() { return reinterpret_cast<const void*>(&k_tu_anchor_conv_halo); }
+
 }  // namespace dycl

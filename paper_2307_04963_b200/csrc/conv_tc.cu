@@ -304,4 +304,8 @@ cudaError_t launch_conv_tc(const ConvArgs& a, int max_rows, int num_sms, cudaStr
   return cudaErrorInvalidValue;
 }
 
+// Lazy-loading anchor: a kernel of this translation unit's module (preload_kernels, hostmod.cu).
+__global__ void k_tu_anchor_conv_tc() {}
+const void* tu_anchor_conv_tc() { return reinterpret_cast<const void*>(&k_tu_anchor_conv_tc); }
+
 }  // namespace dycl

@@ -712,4 +712,8 @@ cudaError_t launch_conv(const ConvArgs& a, int max_rows, int num_sms, cudaStream
   return launch_conv_tc(a, max_rows, num_sms, stream);
 }
 
+// Lazy-loading anchor: a kernel of this translation unit's module (preload_kernels, hostmod.cu).
+__global__ void k_tu_anchor_conv_tma() {}
+const void* tu_anchor_conv_tma() { return reinterpret_cast<const void*>(&k_tu_anchor_conv_tma); }
+
 }  // namespace dycl

@@ -312,4 +312,8 @@ cudaError_t drb_nccl_peers(void* nccl_window, int world, void** table_dev, cudaS
   return cudaGetLastError();
 }
 
+// Lazy-loading anchor: a kernel of this translation unit's module (preload_kernels, hostmod.cu).
+__global__ void k_tu_anchor_drb() {}
+const void* tu_anchor_drb() { return reinterpret_cast<const void*>(&k_tu_anchor_drb); }
+
 }  // namespace dycl

@@ -419,4 +419,8 @@ cudaError_t launch_gemm_tma(const ConvArgs& a, int max_rows, int num_sms, cudaSt
   }
 }
 
+// Lazy-loading anchor: a kernel of this translation unit's module (preload_kernels, hostmod.cu).
+__global__ void k_tu_anchor_gemm_tma() {}
+const void* tu_anchor_gemm_tma() { return reinterpret_cast<const void*>(&k_tu_anchor_gemm_tma); }
+
 }  // namespace dycl

@@ -8,10 +8,13 @@
 // that the next kernels read, so a whole batched run needs no host round trip.
 // All reductions use fixed-order trees (no atomics), so results are independent
 // of batch size and of the position of a sample in the batch.
+#include <cuda.h>
 #include <cuda_bf16.h>
 
 #include <map>
 #include <mutex>
+#include <set>
+#include <vector>
 
 #include "epilogue.cuh"
 #include "kernels.h"
@@ -32,6 +35,50 @@ cudaError_t ensure_smem(const void* func, size_t bytes) {
   e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e == cudaSuccess) cur = bytes;
   return e;
+}
+
+cudaError_t preload_kernels() {
+  typedef CUresult (*FuncGetModule)(CUmodule*, CUfunction);
+  typedef CUresult (*ModuleGetFunctionCount)(unsigned int*, CUmodule);
+  typedef CUresult (*ModuleEnumerateFunctions)(CUfunction*, unsigned int, CUmodule);
+  typedef CUresult (*FuncLoad)(CUfunction);
+  static std::mutex mu;
+  static std::set<int> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count(dev)) return cudaSuccess;
+  auto sym = [](const char* name) -> void* {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    return cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess &&
+                   q == cudaDriverEntryPointSuccess
+               ? p
+               : nullptr;
+  };
+  auto get_module = reinterpret_cast<FuncGetModule>(sym("cuFuncGetModule"));
+  auto count = reinterpret_cast<ModuleGetFunctionCount>(sym("cuModuleGetFunctionCount"));
+  auto enumerate = reinterpret_cast<ModuleEnumerateFunctions>(sym("cuModuleEnumerateFunctions"));
+  auto load = reinterpret_cast<FuncLoad>(sym("cuFuncLoad"));
+  if (!get_module || !count || !enumerate || !load) return cudaErrorNotSupported;
+  const void* anchors[] = {tu_anchor_conv_tc(), tu_anchor_conv_tma(),   tu_anchor_conv_gemm(), tu_anchor_conv_halo(),
+                           tu_anchor_gemm_tma(), tu_anchor_block_fused(), tu_anchor_hostmod(),  tu_anchor_s2s_kernels(),
+                           tu_anchor_cap(),      tu_anchor_drb()};
+  for (const void* a : anchors) {
+    cudaFunction_t f = nullptr;
+    if ((e = cudaGetFuncBySymbol(&f, a)) != cudaSuccess) return e;
+    CUmodule m = nullptr;
+    unsigned n = 0;
+    if (get_module(&m, reinterpret_cast<CUfunction>(f)) != CUDA_SUCCESS || count(&n, m) != CUDA_SUCCESS)
+      return cudaErrorNotSupported;
+    std::vector<CUfunction> fs(n);
+    if (n && enumerate(fs.data(), n, m) != CUDA_SUCCESS) return cudaErrorNotSupported;
+    for (CUfunction fn : fs)
+      if (load(fn) != CUDA_SUCCESS) return cudaErrorNotSupported;
+  }
+  done.insert(dev);
+  return cudaSuccess;
 }
 
 namespace {
@@ -1074,5 +1121,9 @@ bool& pdl_flag() {
   thread_local bool on = false;
   return on;
 }
+
+// Lazy-loading anchor: a kernel of this translation unit's module (preload_kernels, hostmod.cu).
+__global__ void k_tu_anchor_hostmod() {}
+const void* tu_anchor_hostmod() { return reinterpret_cast<const void*>(&k_tu_anchor_hostmod); }
 
 }  // namespace dycl

@@ -111,6 +111,22 @@ struct PdlScope {
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) for `func` on the CURRENT device, once per
 // (device, function, size): function attributes are per device context, so a process that
 // drives graphs on several devices must set them on each (thread-safe; hostmod.cu).
+// One kernel of each translation unit's module (lazy-loading anchors, see preload_kernels).
+const void* tu_anchor_conv_tc();
+const void* tu_anchor_conv_tma();
+const void* tu_anchor_conv_gemm();
+const void* tu_anchor_conv_halo();
+const void* tu_anchor_gemm_tma();
+const void* tu_anchor_block_fused();
+const void* tu_anchor_hostmod();
+const void* tu_anchor_s2s_kernels();
+const void* tu_anchor_cap();
+const void* tu_anchor_drb();
+// Load every kernel of libdycl now (CUDA lazy loading otherwise loads a kernel at its first
+// launch, and loading can wait for the whole context to go idle: with device-initiated
+// rebalancing between ranks of ONE process, a rank's spinning exchange kernel would then wait
+// for a peer whose host thread is blocked loading its next kernel). Once per device.
+cudaError_t preload_kernels();
 cudaError_t ensure_smem(const void* func, size_t bytes);
 template <typename... KArgs>
 inline cudaError_t ensure_smem(void (*kernel)(KArgs...), size_t bytes) {

@@ -901,4 +901,8 @@ cudaError_t launch_s2s_init(const S2SInitArgs& a, cudaStream_t s) {
   return launch_k(k_s2s_init, dim3((a.B + 255) / 256 > 0 ? (a.B + 255) / 256 : 1), dim3(256), 0, s, a);
 }
 
+// Lazy-loading anchor: a kernel of this translation unit's module (preload_kernels, hostmod.cu).
+__global__ void k_tu_anchor_s2s_kernels() {}
+const void* tu_anchor_s2s_kernels() { return reinterpret_cast<const void*>(&k_tu_anchor_s2s_kernels); }
+
 }  // namespace dycl
