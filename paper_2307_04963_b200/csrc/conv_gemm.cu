@@ -553,67 +553,52 @@ __global__ void __launch_bounds__(THREADS, 1)
           wg_sync(wg);
           if (res && leader && c0 + 32 < BN) res_load(c0 + 32);
         }
-        if (staged && a.gap_part) {
-          // fused GAP (a2): the chunk's fp32 y goes through the SMEM staging in every tile (the
-          // ragged last one included); thread (quarter q, column cc) sums rows 32q..32q+31 of
-          // its column in order, in groups of G rows, into the partials [M / G][Cout]
+        if (a.gap_part) {
+          // fused GAP (a2): column sums of the chunk's fp32 y over groups of G consecutive rows
+          // (G = the largest power of two <= 32 dividing HW: a group lies inside one sample and
+          // covers the same pixels p in [kG, (k+1)G) whatever the sample's batch position) into
+          // the partials [M / G][Cout]. A transpose-reduce over the warp's 32 rows (= lanes):
+          // at level o = 1, 2, .., G/2 lanes l and l^o swap halves of their column sets and add,
+          // so after log2(G) levels lane l holds 32/G column sums over its aligned G-row group --
+          // a fixed pairwise tree (batch-position independent), no SMEM staging, no barrier
+          const int G = a.gap_g;
+          float g[32];
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            *reinterpret_cast<float4*>(eO32 + sw128(r, j)) = make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
-          wg_sync(wg);
-          {
-            // fp32 sums over G-row groups (G = the largest power of two <= 32 dividing HW): every
-            // group lies inside one sample and covers the same pixels p in [kG, (k+1)G) whatever
-            // the sample's batch position, and is summed in ascending row order -- so the pooled
-            // features are batch-position independent without integer arithmetic
-            const int cc = lane, q = quad;
-            const int G = a.gap_g;
-            const long long ra = m0 + 32 * q;                  // first row of this quarter
-            // sums of 4-row groups (fixed tree), then combined into G-row groups (G in {4, 8, 16,
-            // 32}, one uniform branch per chunk); the 8 swizzle phases of the shared loads are
-            // hoisted so each load is a base register + immediate
-            float* gp = a.gap_part + (size_t)(ra / G) * a.Cout + col0 + c0 + cc;
-            const uint8_t* colb = eO32 + (size_t)(32 * q) * 128 + (cc & 3) * 4;
-            uint32_t ph[8];
+          for (int j = 0; j < 32; ++j) g[j] = f[j];
+          int colbase = 0;                                  // first column of this lane's set
 #pragma unroll
-            for (int k = 0; k < 8; ++k) ph[k] = (uint32_t)(k * 128 + (((cc >> 2) ^ k) << 4));
-            float s4[8];
+          for (int lvl = 0; lvl < 5; ++lvl) {
+            const int o = 1 << lvl;
+            if (o >= G) break;
+            const int n = 16 >> lvl;                         // columns kept after this level
+            const bool upper = (lane & o) != 0;
 #pragma unroll
-            for (int g4 = 0; g4 < 8; ++g4) {
-              float v[4];
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const int rr = 4 * g4 + i;                  // row within the quarter
-                v[i] = *reinterpret_cast<const float*>(colb + (rr >> 3) * 1024 + ph[rr & 7]);
+            for (int j = 0; j < 16; ++j) {
+              if (j < n) {
+                const float send = upper ? g[j] : g[n + j];
+                const float recv = __shfl_xor_sync(0xffffffffu, send, o);
+                g[j] = (upper ? g[n + j] : g[j]) + recv;
               }
-              s4[g4] = ((v[0] + v[1]) + v[2]) + v[3];
             }
-            if (G == 4) {
+            if (upper) colbase += n;
+          }
+          const int ncol = 32 / G;                           // column sums held by this lane
+          const long long grow = m0 + 32 * quad + (lane & ~(G - 1));   // first row of the group
+          if (grow < M) {
+            float* gp = a.gap_part + (size_t)(grow / G) * a.Cout + col0 + c0 + colbase;
 #pragma unroll
-              for (int k = 0; k < 8; ++k)
-                if (ra + 4 * k < M) gp[(size_t)k * a.Cout] = s4[k];
-            } else if (G == 8) {
-#pragma unroll
-              for (int k = 0; k < 4; ++k)
-                if (ra + 8 * k < M) gp[(size_t)k * a.Cout] = s4[2 * k] + s4[2 * k + 1];
-            } else if (G == 16) {
-#pragma unroll
-              for (int k = 0; k < 2; ++k)
-                if (ra + 16 * k < M) gp[(size_t)k * a.Cout] = (s4[4 * k] + s4[4 * k + 1]) + (s4[4 * k + 2] + s4[4 * k + 3]);
-            } else if (ra < M) {
-              gp[0] = ((s4[0] + s4[1]) + (s4[2] + s4[3])) + ((s4[4] + s4[5]) + (s4[6] + s4[7]));
-            }
+            for (int j = 0; j < 8; ++j)
+              if (j < ncol) gp[j] = g[j];
           }
         }
         if (staged && full) {
           if (a.y32 && pair) {
-            if (a.gap_part) wg_sync(wg);                // the GAP has read the fp32 staging
 #pragma unroll
             for (int j = 0; j < 4; ++j)
               *reinterpret_cast<uint4*>(eO32 + sw64(r, j)) =
                   make_uint4(pk2lo(f[8 * j], f[8 * j + 1]), pk2lo(f[8 * j + 2], f[8 * j + 3]),
                              pk2lo(f[8 * j + 4], f[8 * j + 5]), pk2lo(f[8 * j + 6], f[8 * j + 7]));
-          } else if (a.y32 && !a.gap_part) {
+          } else if (a.y32) {
 #pragma unroll
             for (int j = 0; j < 8; ++j)
               *reinterpret_cast<float4*>(eO32 + sw128(r, j)) = make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
@@ -816,7 +801,7 @@ cudaError_t launch_t(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t 
   const int avail_staged = SMEM_LIMIT - SMEM_MISC - 2 * EPI_WG;
   pl.staged = (heavy || a.gap_part) && avail_staged / (CG<BN>::A_BYTES + BB) >= 2 && !(a.dbg & 128) && !a.rows_out &&
               !a.rows_in;
-  if (a.gap_part && !pl.staged) return cudaErrorNotSupported;   // the fused GAP reads the SMEM staging
+  if (a.gap_part && !pl.staged) return cudaErrorNotSupported;   // (the fused GAP is planned with the staged epilogue)
   const int avail = pl.staged ? avail_staged : SMEM_LIMIT - SMEM_MISC;
   // resident weights: one N tile whose K blocks all fit beside >= 3 A stages
   pl.bres = a.Cout == BN && kblocks > 1 && avail - kblocks * BB >= 3 * CG<BN>::A_BYTES && !(a.dbg & 256);

@@ -2,7 +2,7 @@
 # cfg5: conv kernel tests + cfg5 parity/zero-copy tests + 2 bench runs + launch list of one chunk
 mkdir -p gpurun_out
 python -c "from paper_2307_04963_b200 import build as B; B.build()" > gpurun_out/build.txt 2>&1
-timeout 900 python -m pytest tests/test_gpu.py -m gpu -q -x -k "nhwc or cfg5 or zero_copy" 2>&1 | tail -3 > gpurun_out/c5ab_tests.txt
+timeout 900 python -m pytest tests/test_gpu.py tests/test_gpu_multi.py tests/test_gpu_edge.py -m gpu -q -x -k "nhwc or cfg5 or zero_copy" 2>&1 | tail -3 > gpurun_out/c5ab_tests.txt
 for i in 1 2; do
 timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/c5ab_$i.json 2> gpurun_out/c5ab.err
 done
