@@ -41,7 +41,8 @@ __device__ __forceinline__ void named_bar(int id) { asm volatile("bar.sync %0, 1
 // The N-tile CTAs of one M tile meet (fused LayerNorm): the calling warpgroup's stores are
 // published, its leader counts in and spins until `target` CTAs have (the counter only grows
 // until the last CTA re-arms it after the final meeting). Every CTA of the grid is resident
-// (one tile per CTA, grid <= SMs), so the wait is bounded by the slowest tile.
+// (grid <= SMs, one CTA per SM) and the partners of a tile are processed in the same round of
+// the persistent loop (grid a multiple of the N-tile count), so the wait is bounded.
 __device__ __forceinline__ void ln_meet(int* cnt, int target, int wg, bool leader) {
   __threadfence();
   named_bar(1 + wg);
@@ -393,8 +394,12 @@ bool gemm_tma_eligible(const ConvArgs& a) {
 }
 
 bool gemm_tma_ln_ok(const ConvArgs& a, int max_rows, int num_sms) {
-  const long long tiles = (long long)((max_rows + BM - 1) / BM) * (a.Cout / 64);
-  return gemm_tma_eligible(a) && a.Cout % 64 == 0 && a.res_mode == 1 && a.res32 && tiles <= num_sms;
+  // the N tiles of an M tile must run in the same round of the persistent loop: the grid is a
+  // multiple of the N-tile count, <= the SMs (one CTA per SM, all resident), so tile t and its
+  // partners are processed by neighbouring CTAs in round t / grid
+  const int n_tiles = a.Cout / 64;
+  return gemm_tma_eligible(a) && a.Cout % 64 == 0 && a.res_mode == 1 && a.res32 && n_tiles >= 1 &&
+         n_tiles <= 16 && n_tiles <= num_sms;
 }
 
 int gemm_tma_bn(const ConvArgs& a, int max_rows, int num_sms) {
@@ -409,7 +414,8 @@ cudaError_t launch_gemm_tma(const ConvArgs& a, int max_rows, int num_sms, cudaSt
     // fused LayerNorm: 64-wide N tiles, every tile its own CTA (the tiles of an M tile meet)
     if (!gemm_tma_ln_ok(a, max_rows, num_sms) || !a.ln_part || !a.ln_cnt || !a.y || !a.y32 || a.split || a.relu)
       return cudaErrorInvalidValue;
-    return launch_bn<64>(a, max_rows, num_sms, stream);
+    const int n_tiles = a.Cout / 64;
+    return launch_bn<64>(a, max_rows, num_sms / n_tiles * n_tiles, stream);
   }
   // 256-wide N tiles unless they leave more than half of the SMs idle (small-M decode GEMMs)
   switch (gemm_tma_bn(a, max_rows, num_sms)) {

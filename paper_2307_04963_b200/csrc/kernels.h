@@ -79,7 +79,7 @@ struct ConvArgs {
   int g_t = 0, g_S = 0, g_eos = -1;
   // gemm_tma only: residual + LayerNorm fused into the epilogue (the decoder's post-LN sub-layer
   // ends).  v = acc + bias + res32 (res_mode 1) is normalised over its whole row:
-  // the N tiles of one M tile (one tile per CTA, BN = 64) publish per-row partial sums to
+  // the N tiles of one M tile (BN = 64, same round of the persistent loop) publish per-row partial sums to
   // ln_part [rows][2][Cout / 64] and meet on ln_cnt[m_tile] (zero on entry, zero on exit) --
   // mean first, then the centred sum of squares, biased variance, eps; y32 <- LN(v) fp32 and
   // y <- bf16(LN(v)).  y32 may alias res32 (every element is read before it is written, by
@@ -176,7 +176,7 @@ bool gemm_tma_eligible(const ConvArgs& a);
 cudaError_t launch_gemm_tma(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream);
 // N tile width launch_gemm_tma picks for these arguments (64, 128 or 256).
 int gemm_tma_bn(const ConvArgs& a, int max_rows, int num_sms);
-// The fused residual + LayerNorm epilogue (ConvArgs.ln_*) applies: BN = 64, one tile per CTA.
+// The fused residual + LayerNorm epilogue (ConvArgs.ln_*) applies: BN = 64, d / 64 <= 16 N tiles.
 bool gemm_tma_ln_ok(const ConvArgs& a, int max_rows, int num_sms);
 
 // NHWC implicit-GEMM conv with TMA im2col operand loads (conv_gemm.cu): C % 64 == 0, Cout % 64 == 0.

@@ -59,11 +59,11 @@ struct dycl_s2s_s {
   bool fuse_argmax = true;           // LM-head argmax in the GEMM epilogue (DYCL_S2S_FUSE_ARGMAX=0 disables)
   float* am_val = nullptr;           // fused argmax partials [max_batch][vocab / 64]
   int* am_idx = nullptr;
-  // residual + LayerNorm in the epilogue of the out-proj / FFN-down GEMMs of the decode step
-  // (ConvArgs.ln_*; DYCL_S2S_FUSE_LN=0 disables): row partials and per-M-tile meeting counters
+  // residual + LayerNorm in the epilogue of the out-proj / FFN-down GEMMs (decode steps and the
+  // encoder; ConvArgs.ln_*; DYCL_S2S_FUSE_LN=0 disables): row partials and per-M-tile counters
   bool fuse_ln = true;
-  float* ln_part = nullptr;          // [max_batch][2][d / 64]
-  int* ln_cnt = nullptr;             // [max_batch / 128 + 1], zero between launches
+  float* ln_part = nullptr;          // [max_batch * src_len][d / 64] (sum, M2) pairs
+  int* ln_cnt = nullptr;             // one per 128-row M tile, zero between launches
   // DYCL_PREC_BF16X3_PARITY: every bf16 tensor is a split pair [hi | lo] and every GEMM runs
   // on K-concatenated operands [A_hi | A_lo] x [W | W] (weights are exact bf16, so the
   // W_lo terms of the 3-pass product vanish): fp32-accurate products on the tensor cores
@@ -196,7 +196,7 @@ struct S2SExec {
     return e;
   }
   // x32 <- LN(x32 + x W^T + b), xb <- bf16 of it: one GEMM with the LayerNorm in its epilogue
-  // when it applies (decode steps), else the GEMM into `pre` followed by k_layernorm
+  // when it applies, else the GEMM into `pre` followed by k_layernorm
   cudaError_t gemm_res_ln(const uint16_t* x, int K, const uint16_t* w, const float* b, const float* g,
                           const float* be, const int* cnt, int n_static, int max_rows) {
     const int d = s->c.d_model;
@@ -262,6 +262,8 @@ struct S2SExec {
       E(dycl::launch_attn_encoder(aa, B, st));
       pe();
       ++n;
+      // (the encoder keeps 256-wide N tiles + k_layernorm: its LN fused into 64-wide N tiles
+      // measured 0.3 ms slower per batch -- at M = B*S the GEMM's tile width matters more)
       E(gemm(s->att, d, L.wo, L.bo, d, s->x32, nullptr, s->pre, 0, nullptr, R, R));
       E(ln(s->pre, L.lsg, L.lsb, nullptr, R, R));
       E(gemm(s->xb, d, L.w1, L.b1, c.d_ff, nullptr, s->h, nullptr, 1, nullptr, R, R));
@@ -482,10 +484,10 @@ dycl_status dycl_s2s_finalize(dycl_s2s s, int64_t max_batch) {
       (r = alloc(s, &s->am_idx, B * (size_t)(s->c.vocab / 64))) ||
       (r = alloc(s, &s->cur_tok, B)) || (r = alloc(s, &s->active[0], B)) || (r = alloc(s, &s->active[1], B)) ||
       (r = alloc(s, &s->list1, B)) || (r = alloc(s, &s->list0, B)) || (r = alloc(s, &s->counts, 2 * L + 2)) ||
-      (r = alloc(s, &s->flag, B)) || (r = alloc(s, &s->ln_part, B * 2 * (size_t)(d / 64 + 1))) ||
-      (r = alloc(s, &s->ln_cnt, B / 128 + 2)))
+      (r = alloc(s, &s->flag, B)) || (r = alloc(s, &s->ln_part, R * 2 * (size_t)(d / 64 + 1))) ||
+      (r = alloc(s, &s->ln_cnt, R / 128 + 2)))
     return r;
-  SCK(cudaMemset(s->ln_cnt, 0, (B / 128 + 2) * sizeof(int)));
+  SCK(cudaMemset(s->ln_cnt, 0, (R / 128 + 2) * sizeof(int)));
   s->cross.resize(s->dec.size());
   s->cache.resize(s->dec.size());
   for (size_t l = 0; l < s->dec.size(); ++l)
