@@ -147,6 +147,7 @@ struct dycl_graph_s {
     cudaGraphExec_t exec = nullptr;
     const void* key[4] = {};
     int64_t batch = -1;
+    long long goff = -1;             // device-rebalanced runs: the global offset baked into the graph
     int launches = 0;
     uint64_t used = 0;
   };
@@ -1905,24 +1906,36 @@ static dycl_status run_impl(dycl_graph g, const float* input, int64_t batch, flo
   g->prof_stream = st;
   g->rb_sent = g->rb_recv = 0;
   const bool rebal = g->tr && g->rb_policy != 0 && g->n_exits > 0;
-  if (rebal) {
-    // lock step with the other ranks (even with no rows of its own: it may receive some);
-    // results land in the library's result space first, then own rows go to the caller
-    Exec ex{g, st, (int)std::max<int64_t>(batch, 1), g->d_res_logits, g->d_res_path};
+  // a rebalanced run: lock step with the other ranks (even with no rows of its own: it may
+  // receive some); results land in the library's result space first, then own rows go to the
+  // caller. Device-initiated exchanges have no host step, so that run is graph-captured too.
+  auto rebal_body = [&](cudaStream_t s, int* nlaunch) -> dycl_status {
+    Exec ex{g, s, (int)std::max<int64_t>(batch, 1), g->d_res_logits, g->d_res_path};
     ex.out_margin = g->d_res_margin;
     ex.global_offset = global_offset;
     ex.own = (int)batch;
-    if (dycl_status s = ex.run(input)) return s;
-    g->launches_per_run = ex.nlaunch;
+    if (dycl_status r = ex.run(input)) return r;
+    *nlaunch = ex.nlaunch;
     if (batch > 0) {
-      CK(cudaMemcpyAsync(logits, g->d_res_logits, (size_t)batch * g->K * 4, cudaMemcpyDeviceToDevice, st));
-      CK(cudaMemcpyAsync(path, g->d_res_path, (size_t)batch * 4, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(logits, g->d_res_logits, (size_t)batch * g->K * 4, cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemcpyAsync(path, g->d_res_path, (size_t)batch * 4, cudaMemcpyDeviceToDevice, s));
       if (min_margin)
-        CK(cudaMemcpyAsync(min_margin, g->d_res_margin, (size_t)batch * 4, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(min_margin, g->d_res_margin, (size_t)batch * 4, cudaMemcpyDeviceToDevice, s));
     }
-  } else if (batch == 0) {
+    return DYCL_OK;
+  };
+  const bool graphable = g->use_graph && !g->profiling && !g->dbg_ts && !features;
+  if (rebal && g->rb_device && !g->drb_win) {
+    // the symmetric window is set up collectively (every rank's first rebalanced run) -- before
+    // any capture: its allocation / registration cannot be recorded into a graph
+    std::string err;
+    if (!g->tr->window(g->drb_bytes, &g->drb_win, &g->drb_peers, &err)) return fail(g, DYCL_E_NCCL, err);
+  }
+  if (rebal && !(g->rb_device && graphable)) {
+    if (dycl_status r = rebal_body(st, &g->launches_per_run)) return r;
+  } else if (batch == 0 && !rebal) {
     CK(cudaMemsetAsync(g->d_counts, 0, g->n_slots * sizeof(int), st));
-  } else if (!g->use_graph || g->profiling || g->dbg_ts || features) {
+  } else if (!rebal && !graphable) {
     Exec ex{g, st, (int)batch, logits, path};
     ex.out_margin = min_margin;
     ex.out_features = features;
@@ -1931,10 +1944,11 @@ static dycl_status run_impl(dycl_graph g, const float* input, int64_t batch, flo
     g->launches_per_run = ex.nlaunch;
   } else {
     const void* key[4] = {input, logits, path, min_margin};
+    const long long goff = rebal ? global_offset : -1;
     dycl_graph_s::GraphEntry* ge = nullptr;
     for (auto& e : g->graphs)
-      if (e.exec && e.batch == batch && e.key[0] == key[0] && e.key[1] == key[1] && e.key[2] == key[2] &&
-          e.key[3] == key[3])
+      if (e.exec && e.batch == batch && e.goff == goff && e.key[0] == key[0] && e.key[1] == key[1] &&
+          e.key[2] == key[2] && e.key[3] == key[3])
         ge = &e;
     if (!ge) {
       ge = &g->graphs[0];                            // empty slot, else the least recently used
@@ -1946,10 +1960,17 @@ static dycl_status run_impl(dycl_graph g, const float* input, int64_t batch, flo
       }
       if (!g->cap_stream) CK(cudaStreamCreateWithFlags(&g->cap_stream, cudaStreamNonBlocking));
       CK(cudaStreamBeginCapture(g->cap_stream, cudaStreamCaptureModeThreadLocal));
-      Exec ex{g, g->cap_stream, (int)batch, logits, path};
-      ex.out_margin = min_margin;
-      ex.own = (int)batch;
-      const dycl_status r = ex.run(input);
+      int nl = 0;
+      dycl_status r;
+      if (rebal) {
+        r = rebal_body(g->cap_stream, &nl);
+      } else {
+        Exec ex{g, g->cap_stream, (int)batch, logits, path};
+        ex.out_margin = min_margin;
+        ex.own = (int)batch;
+        r = ex.run(input);
+        nl = ex.nlaunch;
+      }
       cudaGraph_t graph = nullptr;
       const cudaError_t ec = cudaStreamEndCapture(g->cap_stream, &graph);
       if (r != DYCL_OK) {
@@ -1965,7 +1986,8 @@ static dycl_status run_impl(dycl_graph g, const float* input, int64_t batch, flo
       }
       for (int i = 0; i < 4; ++i) ge->key[i] = key[i];
       ge->batch = batch;
-      ge->launches = ex.nlaunch;
+      ge->goff = goff;
+      ge->launches = nl;
     }
     ge->used = ++g->graph_clock;
     CK(cudaGraphLaunch(ge->exec, st));
