@@ -94,6 +94,12 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 8 && lane == 0) {
     ptx::tma_prefetch_desc(&tmA);
     ptx::tma_prefetch_desc(&tmB);
+    // the weights do not depend on the predecessor kernel: start pulling this CTA's first N
+    // tile of W into L2 now, while (under PDL) the predecessor is still running -- the decode
+    // GEMMs' weights come from HBM every step (the K/V stream evicts them), and that first
+    // HBM round trip sat on the dependent chain
+    const int first_n = (int)(blockIdx.x % (unsigned)n_tiles);
+    for (int kb = 0; kb < kblocks; ++kb) ptx::tma_prefetch_l2_2d(&tmB, kb * BKE, first_n * BN);
   }
   ptx::tc_fence_before();
   __syncthreads();

@@ -168,6 +168,11 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, uint
       "l"(tmap), "r"(bar), "r"(c0), "r"(c1)
       : "memory");
 }
+// L2 prefetch of one tensor-map box (no SMEM, no barrier): warms L2 for a later tma_load_2d
+__device__ __forceinline__ void tma_prefetch_l2_2d(const void* tmap, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(tmap), "r"(c0), "r"(c1)
+               : "memory");
+}
 // Generic K-major smem descriptor: layout code (0 none, 2 SW128, 4 SW64, 6 SW32),
 // leading byte offset (only used by the non-swizzled layout), stride byte offset.
 __device__ __forceinline__ uint64_t make_smem_desc(uint32_t saddr, uint32_t layout, uint32_t lbo, uint32_t sbo) {

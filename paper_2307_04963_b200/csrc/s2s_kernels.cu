@@ -560,9 +560,22 @@ __global__ void __launch_bounds__(xattn::THREADS, 1)
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 8 && lane == 0) ptx::tma_prefetch_desc(&tmKV);
+  if (warp == 8 && lane == 0) {
+    ptx::tma_prefetch_desc(&tmKV);
+    // this CTA's first row's K / V into L2 before the PDL wait: the live count and the slot list
+    // come from the previous step's compaction (complete: the predecessor only starts its main
+    // part after its own predecessor finished), the K / V rows below position t from earlier
+    // steps or the encoder phase -- only the queries depend on the immediate predecessor
+    const int n0 = a.n_live ? *a.n_live : a.n_static;
+    if ((int)blockIdx.x < n0) {
+      const int rps0 = a.kv ? a.S : a.max_len;
+      const int slot0 = a.slot[blockIdx.x];
+      for (int kvh = 0; kvh < 2; ++kvh)
+        for (int h = 0; h < a.heads; ++h) ptx::tma_prefetch_l2_2d(&tmKV, kvh * a.d + h * 64, slot0 * rps0);
+    }
+  }
   __syncthreads();
-  ptx::pdl_wait();      // PDL (kernels.h): the live count, slots and queries come from predecessors
+  ptx::pdl_wait();      // PDL (kernels.h): the queries (and this step's k, v) come from the predecessor
   ptx::pdl_trigger();
   const int n = a.n_live ? *a.n_live : a.n_static;
   const int d = a.d;

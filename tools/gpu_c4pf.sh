@@ -1,0 +1,10 @@
+#!/bin/bash
+# cfg4: GEMM weights prefetched into L2 before the PDL wait; bench x2 + cfg4 tests
+mkdir -p gpurun_out
+rm -f gpurun_out/c4pf_*.json
+python -c "from paper_2307_04963_b200 import build as B; B.build()" > gpurun_out/build.txt 2>&1
+for i in 1 2; do
+timeout 600 python bench.py --config 4 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/c4pf_$i.json 2> gpurun_out/c4pf.err
+done
+for f in gpurun_out/c4pf_*.json; do python -c "import json,sys; l=json.loads(open('$f').read().strip().splitlines()[-1]); print('$f', round(l['ms_per_step'],2))"; done
+timeout 900 python -m pytest tests -m gpu -q -k "cfg4 or s2s or seq2seq or cfg1 or mlp" 2>&1 | tail -2
