@@ -98,40 +98,56 @@ __global__ void __launch_bounds__(THREADS, 1)
     // tile of W into L2 now, while (under PDL) the predecessor is still running -- the decode
     // GEMMs' weights come from HBM every step (the K/V stream evicts them), and that first
     // HBM round trip sat on the dependent chain
+    // (the first ring round of them is loaded straight into SMEM below; these are the rest)
     const int first_n = (int)(blockIdx.x % (unsigned)n_tiles);
-    for (int kb = 0; kb < kblocks; ++kb) ptx::tma_prefetch_l2_2d(&tmB, kb * BKE, first_n * BN);
+    for (int kb = C::STAGES; kb < kblocks; ++kb) ptx::tma_prefetch_l2_2d(&tmB, kb * BKE, first_n * BN);
   }
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  // PDL: the prologue above (barriers, TMEM, descriptors) overlaps the predecessor's tail;
-  // the live count and every operand are read after it completes
+  // before the PDL wait: the first tile's weight boxes of the first ring round go straight into
+  // SMEM (the weights do not depend on the predecessor; the stage's barrier is armed for A + B
+  // now, the A box follows after the wait)
+  const int pre = kblocks < C::STAGES ? kblocks : C::STAGES;
+  const bool producer = warp == 8 || warp >= 10;
+  const int prod = warp == 8 ? 0 : warp - 9;
+  if (producer && lane == 0) {
+    const int first_n = (int)(blockIdx.x % (unsigned)n_tiles);
+    for (int kb = prod; kb < pre; kb += NPROD) {
+      const uint32_t bar = full0 + 8 * kb;
+      ptx::mbar_arrive_expect_tx(bar, (uint32_t)C::STAGE);
+      ptx::tma_load_2d(ptx::smem_u32(sB + kb * C::B_BYTES), &tmB, bar, kb * BKE, first_n * BN);
+    }
+  }
+  // PDL: the prologue above (barriers, TMEM, descriptors, first weights) overlaps the
+  // predecessor's tail; the live count and the activations are read after it completes
   ptx::pdl_wait();
   ptx::pdl_trigger();
   const int M = a.n_live ? *a.n_live : a.n_static;
   const int m_tiles = (M + BM - 1) / BM;
   const int num_tiles = m_tiles * n_tiles;
 
-  if (warp == 8 || warp >= 10) {
+  if (producer) {
     // k-blocks round-robin over NPROD producer warps: one issuing warp runs ~9 cycles per
     // instruction, slower than the tensor core consumes a 128 x BN x 64 block (conv_gemm.cu)
-    const int prod = warp == 8 ? 0 : warp - 9;
     int stage = prod;
     uint32_t phase = 0;
     int rr = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       const int m_tile = tile / n_tiles, n_tile = tile - m_tile * n_tiles;
+      const bool first = tile == (int)blockIdx.x;
       for (int kb = 0; kb < kblocks; ++kb) {
         const bool mine = rr == prod;
         rr = rr + 1 == NPROD ? 0 : rr + 1;
         if (!mine) continue;
-        ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1);
+        const bool preissued = first && kb < pre;      // barrier armed, B in flight already
+        if (!preissued) ptx::mbar_wait(empty0 + 8 * stage, phase ^ 1);
         if (lane == 0) {
           const uint32_t bar = full0 + 8 * stage;
-          ptx::mbar_arrive_expect_tx(bar, (uint32_t)C::STAGE);
+          if (!preissued) ptx::mbar_arrive_expect_tx(bar, (uint32_t)C::STAGE);
           ptx::tma_load_2d(ptx::smem_u32(sA + stage * C::A_BYTES), &tmA, bar, kb * BKE, m_tile * BM);
-          ptx::tma_load_2d(ptx::smem_u32(sB + stage * C::B_BYTES), &tmB, bar, kb * BKE, n_tile * BN);
+          if (!preissued) ptx::tma_load_2d(ptx::smem_u32(sB + stage * C::B_BYTES), &tmB, bar, kb * BKE, n_tile * BN);
         }
         __syncwarp();
         stage += NPROD;
@@ -139,6 +155,15 @@ __global__ void __launch_bounds__(THREADS, 1)
           stage -= C::STAGES;
           phase ^= 1;
         }
+      }
+    }
+    if ((int)blockIdx.x >= num_tiles && lane == 0) {
+      // no tile for this CTA after all (the live count is below the grid's sizing): complete the
+      // armed stages with an A box of rows 0.. and let them land before the CTA exits
+      for (int kb = prod; kb < pre; kb += NPROD) {
+        const uint32_t bar = full0 + 8 * kb;
+        ptx::tma_load_2d(ptx::smem_u32(sA + kb * C::A_BYTES), &tmA, bar, kb * BKE, 0);
+        ptx::mbar_wait(bar, 0);
       }
     }
   } else if (warp == 9) {
