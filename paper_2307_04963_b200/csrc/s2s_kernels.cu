@@ -560,50 +560,55 @@ __global__ void __launch_bounds__(xattn::THREADS, 1)
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 8 && lane == 0) {
-    ptx::tma_prefetch_desc(&tmKV);
-    // this CTA's first row's K / V into L2 before the PDL wait: the live count and the slot list
-    // come from the previous step's compaction (complete: the predecessor only starts its main
-    // part after its own predecessor finished), the K / V rows below position t from earlier
-    // steps or the encoder phase -- only the queries depend on the immediate predecessor
-    const int n0 = a.n_live ? *a.n_live : a.n_static;
-    if ((int)blockIdx.x < n0) {
-      const int rps0 = a.kv ? a.S : a.max_len;
-      const int slot0 = a.slot[blockIdx.x];
-      for (int kvh = 0; kvh < 2; ++kvh)
-        for (int h = 0; h < a.heads; ++h) ptx::tma_prefetch_l2_2d(&tmKV, kvh * a.d + h * 64, slot0 * rps0);
-    }
-  }
-  __syncthreads();
-  ptx::pdl_wait();      // PDL (kernels.h): the queries (and this step's k, v) come from the predecessor
-  ptx::pdl_trigger();
-  const int n = a.n_live ? *a.n_live : a.n_static;
   const int d = a.d;
   const bool self = a.kv == nullptr;
   const int nk = self ? a.t + 1 : a.S;                 // keys attended
   const int rps = self ? a.max_len : a.S;              // K/V rows per slot
   const uint32_t hbytes = (uint32_t)R * 128;           // one head's {64, R} box
+  __syncthreads();
   if (warp == 8) {
+    // The producer does not depend on the immediate predecessor: the live count and the slot
+    // list come from the previous step's compaction (complete -- a kernel starts its main part
+    // only after its own predecessor finished), the K / V rows below position t from earlier
+    // steps or the encoder phase; only the queries (and this step's k, v) come from the
+    // predecessor. So its first ring round is issued before the PDL wait.
     if (lane == 0) {
-      int st = 0;
+      ptx::tma_prefetch_desc(&tmKV);
+      const int n = a.n_live ? *a.n_live : a.n_static;
+      int st = 0, issued = 0;
       uint32_t ph = 0;
       for (int row = blockIdx.x; row < n; row += gridDim.x) {
         const int slot = a.slot[row];
         for (int kvh = 0; kvh < 2; ++kvh) {          // K block, then V block
-          ptx::mbar_wait(empty0 + 8 * st, ph ^ 1);
+          if (issued == NST) {                         // first ring round out: now wait
+            ptx::pdl_wait();
+            ptx::pdl_trigger();
+          }
+          if (issued >= NST) ptx::mbar_wait(empty0 + 8 * st, ph ^ 1);
           const uint32_t bar = full0 + 8 * st;
           ptx::mbar_arrive_expect_tx(bar, hbytes * (uint32_t)a.heads);
           for (int h = 0; h < a.heads; ++h)
             ptx::tma_load_2d(ptx::smem_u32(smem + st * STAGE + h * hbytes), &tmKV, bar, kvh * d + h * 64, slot * rps);
+          ++issued;
           if (++st == NST) {
             st = 0;
             ph ^= 1;
           }
         }
       }
+      if (issued < NST) {
+        ptx::pdl_wait();
+        ptx::pdl_trigger();
+      }
+    } else {
+      ptx::pdl_wait();
+      ptx::pdl_trigger();
     }
     return;
   }
+  ptx::pdl_wait();      // PDL (kernels.h): the queries (and this step's k, v) come from the predecessor
+  ptx::pdl_trigger();
+  const int n = a.n_live ? *a.n_live : a.n_static;
   if (warp >= a.heads) return;
   const int h = warp;
   int st = 0;

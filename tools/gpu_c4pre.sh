@@ -1,11 +1,11 @@
 #!/bin/bash
 # k_gemm_tma: first-round weight boxes issued before the PDL wait; cfg4 bench x2 + GEMM-using tests
 mkdir -p gpurun_out
-rm -f gpurun_out/c4pre_*.json
+rm -f gpurun_out/c4pre2_*.json
 python -c "from paper_2307_04963_b200 import build as B; B.build()" > gpurun_out/build.txt 2>&1
 for i in 1 2; do
-timeout 600 python bench.py --config 4 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/c4pre_$i.json 2> gpurun_out/c4pre.err
+timeout 600 python bench.py --config 4 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/c4pre2_$i.json 2> gpurun_out/c4pre.err
 done
-for f in gpurun_out/c4pre_*.json; do python -c "import json,sys; l=json.loads(open('$f').read().strip().splitlines()[-1]); print('$f', round(l['ms_per_step'],2))"; done
-timeout 1200 python -m pytest tests -m gpu -q -k "conv_kernel or cfg1 or mlp or cfg4 or s2s or seq2seq or caption or cfg5_resnet50_parity or cfg5_bench" 2>&1 | tail -2
+for f in gpurun_out/c4pre2_*.json; do python -c "import json,sys; l=json.loads(open('$f').read().strip().splitlines()[-1]); print('$f', round(l['ms_per_step'],2))"; done
+timeout 1200 python -m pytest tests -m gpu -q -k "cfg4 or s2s or seq2seq" 2>&1 | tail -2
 tail -3 gpurun_out/c4pre.err
