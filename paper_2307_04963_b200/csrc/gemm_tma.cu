@@ -13,6 +13,8 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "epilogue.cuh"
 #include "kernels.h"
 #include "ptx.cuh"
@@ -33,7 +35,8 @@ struct GCfg {
   // ~190 KB of ring whatever BN: the small-M decode GEMMs are bound by the bytes one CTA
   // keeps in flight (Little's law on the L2 -> SMEM path), not by the tensor core
   static constexpr int STAGES = BN == 64 ? 8 : BN == 128 ? 6 : 4;
-  static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
+  static constexpr int LNX = BN == 64 ? 16 * BM * 8 : 0;   // DSMEM LN partials [<=16 src][BM] float2
+  static constexpr int SMEM = 1024 + STAGES * STAGE + 256 + LNX;
 };
 
 __device__ __forceinline__ void named_bar(int id) { asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory"); }
@@ -71,6 +74,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tfull0 = empty0 + 8 * C::STAGES;
   const uint32_t tempty0 = tfull0 + 16;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
+  const uint32_t lnbar = ptx::smem_u32(bars + 2 * C::STAGES + 6);       // DSMEM LN exchange barrier
+  float2* lnx = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(bars) + 256);   // [src][BM]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = a.Cout / BN;
@@ -85,6 +90,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       ptx::mbar_init(tfull0 + 8 * i, 1);
       ptx::mbar_init(tempty0 + 8 * i, 128);
     }
+    ptx::mbar_init(lnbar, 1);
     ptx::fence_mbar_init();
   }
   // two BN-column fp32 accumulators: allocate only those (a PDL-launched successor on this SM
@@ -104,6 +110,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   ptx::tc_fence_before();
   __syncthreads();
+  if (BN == 64 && a.ln_cluster) ptx::cluster_sync_all();   // peers' LN barriers initialised
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // before the PDL wait: the first tile's weight boxes of the first ring round go straight into
@@ -303,17 +310,34 @@ __global__ void __launch_bounds__(THREADS, 1)
           const float dd = v[q] - mi;
           m2 += dd * dd;
         }
-        float2* part = reinterpret_cast<float2*>(a.ln_part) + (size_t)(m < M ? m : 0) * n_tiles;
-        if (m < M) __stcg(part + n_tile, make_float2(s1, m2));
-        ln_meet(a.ln_cnt + m_tile, n_tiles, wg, r == 0);
         float2 pt[16];                                  // d <= 1024
         float sum = 0.f;
+        if (a.ln_cluster) {
+          // the M tile's N tiles are this cluster (rank = N tile): every thread stores its row's
+          // partial into slot [n_tile][r] of every CTA of the cluster (st.async, completing 8
+          // bytes on that CTA's LN barrier), then waits for the 8 * n_tiles * BM bytes of its own
+          if (r == 0) ptx::mbar_arrive_expect_tx(lnbar, (uint32_t)(n_tiles * BM * 8));
+          const uint32_t slot = ptx::smem_u32(lnx + n_tile * BM + r);
+          for (int t = 0; t < n_tiles; ++t)
+            ptx::st_async_v2(ptx::mapa(slot, (uint32_t)t), s1, m2, ptx::mapa(lnbar, (uint32_t)t));
+          ptx::mbar_wait(lnbar, 0);
 #pragma unroll
-        for (int t = 0; t < 16; ++t)
-          if (t < n_tiles) {
-            pt[t] = __ldcg(part + t);
-            sum += pt[t].x;
-          }
+          for (int t = 0; t < 16; ++t)
+            if (t < n_tiles) {
+              pt[t] = lnx[t * BM + r];
+              sum += pt[t].x;
+            }
+        } else {
+          float2* part = reinterpret_cast<float2*>(a.ln_part) + (size_t)(m < M ? m : 0) * n_tiles;
+          if (m < M) __stcg(part + n_tile, make_float2(s1, m2));
+          ln_meet(a.ln_cnt + m_tile, n_tiles, wg, r == 0);
+#pragma unroll
+          for (int t = 0; t < 16; ++t)
+            if (t < n_tiles) {
+              pt[t] = __ldcg(part + t);
+              sum += pt[t].x;
+            }
+        }
         const float mu = sum / (float)a.Cout;
         float q2 = 0.f;
 #pragma unroll
@@ -325,8 +349,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         const float rstd = rsqrtf(q2 / (float)a.Cout + a.ln_eps);
         // every CTA of the M tile is past its reads once all have counted in twice: the last
         // one re-arms the counter
-        named_bar(1 + wg);
-        if (r == 0 && atomicAdd(a.ln_cnt + m_tile, 1) == 2 * n_tiles - 1) atomicExch(a.ln_cnt + m_tile, 0);
+        if (!a.ln_cluster) {
+          named_bar(1 + wg);
+          if (r == 0 && atomicAdd(a.ln_cnt + m_tile, 1) == 2 * n_tiles - 1) atomicExch(a.ln_cnt + m_tile, 0);
+        }
         if (m < M) {
           float4* yq = reinterpret_cast<float4*>(a.y32 + (size_t)m * a.Cout + col0);
           uint4* yb = reinterpret_cast<uint4*>(a.y + (size_t)m * a.Cout + col0);
@@ -386,7 +412,7 @@ EncodeTiledFn encode_fn() {
 }
 
 template <int BN>
-cudaError_t launch_bn(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream) {
+cudaError_t launch_bn(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t stream, int cluster = 1) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return cudaErrorNotSupported;
   CUtensorMap tmA, tmB;
@@ -414,7 +440,23 @@ cudaError_t launch_bn(const ConvArgs& a, int max_rows, int num_sms, cudaStream_t
   const long long tiles = (long long)((max_rows + BM - 1) / BM) * (a.Cout / BN);
   int grid = (int)(tiles < num_sms ? tiles : num_sms);
   if (grid < 1) grid = 1;
-  return launch_k(k_gemm_tma<BN>, dim3(grid), dim3(THREADS), GCfg<BN>::SMEM, stream, tmA, tmB, a);
+  if (cluster <= 1) return launch_k(k_gemm_tma<BN>, dim3(grid), dim3(THREADS), GCfg<BN>::SMEM, stream, tmA, tmB, a);
+  if (grid % cluster) return cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = GCfg<BN>::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_flag() ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, k_gemm_tma<BN>, tmA, tmB, a);
 }
 
 }  // namespace
@@ -446,6 +488,15 @@ cudaError_t launch_gemm_tma(const ConvArgs& a, int max_rows, int num_sms, cudaSt
     if (!gemm_tma_ln_ok(a, max_rows, num_sms) || !a.ln_part || !a.ln_cnt || !a.y || !a.y32 || a.split || a.relu)
       return cudaErrorInvalidValue;
     const int n_tiles = a.Cout / 64;
+    const long long tiles = (long long)((max_rows + BM - 1) / BM) * n_tiles;
+    // one round (every tile its own CTA) and an M tile's N tiles fit one portable cluster: swap
+    // the row partials through DSMEM (DYCL_LN_CLUSTER=0: through L2 + a counter)
+    const char* lc = getenv("DYCL_LN_CLUSTER");
+    if (tiles <= num_sms && n_tiles <= 8 && !(lc && atoi(lc) == 0)) {
+      ConvArgs b = a;
+      b.ln_cluster = 1;
+      return launch_bn<64>(b, max_rows, num_sms, stream, n_tiles);
+    }
     return launch_bn<64>(a, max_rows, num_sms / n_tiles * n_tiles, stream);
   }
   // 256-wide N tiles unless they leave more than half of the SMs idle (small-M decode GEMMs)

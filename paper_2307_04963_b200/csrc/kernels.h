@@ -89,6 +89,9 @@ struct ConvArgs {
   float* ln_part = nullptr;
   int* ln_cnt = nullptr;
   float ln_eps = 0.f;
+  // set by launch_gemm_tma: the N tiles of an M tile form one thread-block cluster and swap the
+  // row partials through DSMEM (st.async into every peer's SMEM + an mbarrier) instead of L2
+  int ln_cluster = 0;
   long long* ts = nullptr;   // development: conv_gemm phase timestamps (DYCL_TS_CONV)
   int dbg = 0;           // bit5 (32): row-tap mode opt-in; experiments only (results invalid): bit0 skip
                          // epilogue math/stores, bit1 skip MMAs, bit2 skip A loads, bit3 no residual prefetch.
