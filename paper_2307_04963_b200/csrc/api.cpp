@@ -2242,6 +2242,14 @@ dycl_status dycl_set_comm(dycl_graph g, void* nccl_comm, int rank, int world, in
   return set_transport(g, t, rebalance_policy);
 }
 
+// dycl::preload_kernels, tolerating a driver without the module-enumeration entry points (the
+// preload only removes a lazy-loading stall between in-process ranks; it is not needed for
+// correctness of a single-rank or multi-process run)
+static cudaError_t preload_or_skip() {
+  const cudaError_t e = dycl::preload_kernels();
+  return e == cudaErrorNotSupported ? cudaSuccess : e;
+}
+
 dycl_status dycl_set_rebalance_mode(dycl_graph g, int mode) {
   if (!g) return DYCL_E_INVALID_ARG;
   if (mode != DYCL_REBALANCE_MODE_HOST && mode != DYCL_REBALANCE_MODE_DEVICE)
@@ -2253,7 +2261,7 @@ dycl_status dycl_set_rebalance_mode(dycl_graph g, int mode) {
   g->rb_device = mode == DYCL_REBALANCE_MODE_DEVICE;
   // every kernel loaded before the first exchange: a lazy load during a run could wait for a
   // context that one of this process's spinning exchange kernels keeps busy (kernels.h)
-  if (g->rb_device) CK(dycl::preload_kernels());
+  if (g->rb_device) CK(preload_or_skip());
   if (g->rb_device && !g->d_drb_plan) {
     dycl_status s;
     if ((s = dmalloc(g, &g->d_drb_plan, dycl::DRB_MAX_LEVELS * sizeof(dycl::DrbPlan))) ||
@@ -2308,7 +2316,7 @@ dycl_status dycl_set_comm_local(dycl_graph g, dycl_local_group grp, int rank, in
   // grid of one CTA per SM could otherwise never start its last CTA behind a spinner)
   if (world > 1 && g->num_sms > world) g->num_sms -= world;
   CK(cudaSetDevice(g->device));
-  CK(dycl::preload_kernels());                 // ranks of one process share one context (kernels.h)
+  CK(preload_or_skip());                       // ranks of one process share one context (kernels.h)
   return set_transport(g, dycl::make_local_transport(grp->g, rank), rebalance_policy);
 }
 
